@@ -1,0 +1,112 @@
+"""Actor-critic assemblies and their flat-parameter layouts (steps a5, a7).
+
+Test infrastructure only.  The layouts are re-implemented here from the
+documented order in include/ddppo.h / DESIGN.md ("Flat parameter layout"),
+not from the CUDA code.  Rule: tensors are laid out in the listed order,
+row-major, each starting at an offset rounded up to a multiple of 4 floats
+(no padding happens for the shipped configs).
+
+Architectures (BASELINE.json configs; readings Z17-Z22):
+  toy  (configs[0]): goal [d, cos, sin] -> Linear(3,64) -> tanh
+                     -> Linear(64, A+1)   (A = 4 actions; +1 value)
+  gps  (configs[1]): goal -> Linear(3,32) (linear);
+                     prev action -> Embedding(A+1, 32), start token = A;
+                     x = [goal_emb, act_emb] (Z22 order) -> GRU(64, 512)
+                     -> Linear(512, A+1) ("fully connected layer,
+                     resulting in a soft-max distribution ... and an estimate
+                     of the value function").
+"""
+import numpy as np
+
+from . import nets
+
+NUM_ACTIONS = 4
+
+
+def layout(arch, hidden=512, num_actions=NUM_ACTIONS):
+    """Ordered [(name, shape, fan_in)]."""
+    A1 = num_actions + 1
+    if arch == "toy":
+        h = 64
+        return [("fc1.weight", (h, 3), 3), ("fc1.bias", (h,), 3),
+                ("head.weight", (A1, h), h), ("head.bias", (A1,), h)]
+    if arch == "gps":
+        H, G = hidden, 3 * hidden
+        return [("goal_fc.weight", (32, 3), 3), ("goal_fc.bias", (32,), 3),
+                ("act_embed.weight", (A1, 32), 1),
+                ("rnn.weight_ih", (G, 64), H), ("rnn.weight_hh", (G, H), H),
+                ("rnn.bias_ih", (G,), H), ("rnn.bias_hh", (G,), H),
+                ("head.weight", (A1, H), H), ("head.bias", (A1,), H)]
+    raise ValueError(arch)
+
+
+def offsets(arch, **kw):
+    out, off = {}, 0
+    for name, shape, _ in layout(arch, **kw):
+        off = (off + 3) // 4 * 4
+        n = int(np.prod(shape))
+        out[name] = (off, shape)
+        off += n
+    return out, off
+
+
+def unpack(arch, flat, **kw):
+    offs, _ = offsets(arch, **kw)
+    flat = np.asarray(flat, dtype=np.float64)
+    return {k: flat[o:o + int(np.prod(s))].reshape(s) for k, (o, s) in offs.items()}
+
+
+def pack(arch, tensors, **kw):
+    offs, P = offsets(arch, **kw)
+    flat = np.zeros(P)
+    for k, (o, s) in offs.items():
+        flat[o:o + int(np.prod(s))] = np.asarray(tensors[k], dtype=np.float64).reshape(-1)
+    return flat
+
+
+# ---------------------------------------------------------------- forward / backward
+def forward(arch, flat, batch, **kw):
+    """batch: goal [B][T][3], prev_action [B][T], mask [B][T], h0 [B][H].
+
+    Returns logits [B][T][A], values [B][T], cache.
+    """
+    p = unpack(arch, flat, **kw)
+    goal = np.asarray(batch["goal"], dtype=np.float64)
+    if arch == "toy":
+        pre = nets.linear_fwd(goal, p["fc1.weight"], p["fc1.bias"])
+        h = np.tanh(pre)
+        out = nets.linear_fwd(h, p["head.weight"], p["head.bias"])
+        cache = {"goal": goal, "h": h}
+    elif arch == "gps":
+        ge = nets.linear_fwd(goal, p["goal_fc.weight"], p["goal_fc.bias"])
+        ae = nets.embedding_fwd(batch["prev_action"], p["act_embed.weight"])
+        x = np.concatenate([ge, ae], axis=-1)
+        h, rc = nets.gru_seq_fwd(x, np.asarray(batch["mask"], dtype=np.float64),
+                                 np.asarray(batch["h0"], dtype=np.float64),
+                                 p["rnn.weight_ih"], p["rnn.weight_hh"], p["rnn.bias_ih"], p["rnn.bias_hh"])
+        out = nets.linear_fwd(h, p["head.weight"], p["head.bias"])
+        cache = {"goal": goal, "prev_action": np.asarray(batch["prev_action"]), "h": h, "rnn": rc}
+    else:
+        raise ValueError(arch)
+    return out[..., :-1], out[..., -1], cache
+
+
+def backward(arch, flat, cache, dlogits, dvalues, **kw):
+    """dlogits [B][T][A], dvalues [B][T] -> flat gradient [P]."""
+    p = unpack(arch, flat, **kw)
+    dout = np.concatenate([dlogits, dvalues[..., None]], axis=-1)
+    g = {}
+    if arch == "toy":
+        dh, g["head.weight"], g["head.bias"] = nets.linear_bwd(cache["h"], p["head.weight"], dout)
+        dpre = dh * (1.0 - cache["h"] ** 2)
+        _, g["fc1.weight"], g["fc1.bias"] = nets.linear_bwd(cache["goal"], p["fc1.weight"], dpre)
+    elif arch == "gps":
+        dh, g["head.weight"], g["head.bias"] = nets.linear_bwd(cache["h"], p["head.weight"], dout)
+        dx, g["rnn.weight_ih"], g["rnn.weight_hh"], g["rnn.bias_ih"], g["rnn.bias_hh"] = \
+            nets.gru_seq_bwd(dh, cache["rnn"], p["rnn.weight_ih"], p["rnn.weight_hh"])
+        dge, dae = dx[..., :32], dx[..., 32:]
+        _, g["goal_fc.weight"], g["goal_fc.bias"] = nets.linear_bwd(cache["goal"], p["goal_fc.weight"], dge)
+        g["act_embed.weight"] = nets.embedding_bwd(cache["prev_action"], dae, p["act_embed.weight"].shape[0])
+    else:
+        raise ValueError(arch)
+    return pack(arch, g, **kw)

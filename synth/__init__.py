@@ -1,0 +1,169 @@
+"""Seeded synthetic inputs shared by the oracle-side tests and the CUDA path.
+
+This module holds NONE of the method's arithmetic (no GAE, loss, network or
+optimizer math): it only draws rollouts shaped like PointGoal episodes,
+initial parameters, epoch permutations and straggler step costs from
+seeded NumPy Philox generators.  Both the oracle tests and the GPU path
+consume exactly these arrays; nothing here is ever computed by either side.
+
+Recipe:
+  * episodes: start geodesic distance d0 ~ U(1, 20) m, goal bearing
+    theta ~ U(-pi, pi); 4 actions stop / forward 0.25 m / left 10 deg /
+    right 10 deg; a stochastic scripted behaviour policy (forward
+    0.6, turn-towards-goal 0.28, turn-away 0.1, stop 0.02; stop 0.97 once
+    d <= 0.2 m); forward fails (collision, no motion) with prob 0.1;
+    episodes end on stop or after 500 steps.
+  * rewards: -(d_new - d_old) - 0.01 per step plus terminal
+    2.5 * SPL on success, SPL = d0 / max(d0, path length).
+  * goal input [d, cos theta, sin theta]; prev_action = start
+    token A (= 4) after an episode start; mask_t = 1 - done_{t-1}.
+  * V_hat = 2.5 exp(-d/10) - 0.05 d + N(0, 0.1^2) (a stand-in critic, fp32);
+    logp_old = log-probability of the taken action under the behaviour
+    policy; h0 ~ N(0, 0.1^2).
+  * per-step arrays are env-major [E][ld] with ld = round_up(T+1, 4); value
+    row slot L holds the bootstrap V_hat(s_L); everything past L is zero.
+"""
+import numpy as np
+
+NUM_ACTIONS = 4
+START_TOKEN = NUM_ACTIONS
+
+# BASELINE.json configs
+CONFIGS = {
+    "toy": dict(arch="toy", E=2, T=4, epochs=1, minibatches=1, hidden=64),
+    "gps": dict(arch="gps", E=4, T=128, epochs=2, minibatches=2, hidden=512),
+    "stress_gps": dict(arch="gps", E=16, T=128, epochs=2, minibatches=2, hidden=512),
+}
+
+
+def ld_for(T):
+    return (T + 1 + 3) // 4 * 4
+
+
+def _rng(seed, *keys):
+    ss = np.random.SeedSequence([int(seed)] + [int(k) for k in keys])
+    return np.random.Generator(np.random.Philox(ss))
+
+
+def rollout(E, T, seed, rank=0, iteration=0, length=None, hidden=512, ld=None):
+    """One rank's rollout.  `length` (int or [E]) truncates (preemption); default T."""
+    ld = ld or ld_for(T)
+    rng = _rng(seed, 1, rank, iteration)
+    f32 = np.float32
+    rew = np.zeros((E, ld), f32)
+    val = np.zeros((E, ld), f32)
+    done = np.zeros((E, ld), np.uint8)
+    action = np.zeros((E, ld), np.int32)
+    prev_action = np.zeros((E, ld), np.int32)
+    mask = np.zeros((E, ld), f32)
+    logp_old = np.zeros((E, ld), f32)
+    goal = np.zeros((E, T, 3), f32)
+
+    # episode state (vectorised over envs); start mid-episode
+    d0 = rng.uniform(1.0, 20.0, E)
+    d = d0 * rng.uniform(0.3, 1.0, E)
+    theta = rng.uniform(-np.pi, np.pi, E)
+    path = d0 - d
+    age = rng.integers(0, 100, E)
+    prev = rng.integers(0, NUM_ACTIONS, E)
+    m_prev = np.ones(E)
+    for t in range(T + 1):
+        val[:, t] = (2.5 * np.exp(-d / 10.0) - 0.05 * d + rng.normal(0.0, 0.1, E)).astype(f32)
+        if t == T:
+            break
+        goal[:, t, 0] = d
+        goal[:, t, 1] = np.cos(theta)
+        goal[:, t, 2] = np.sin(theta)
+        prev_action[:, t] = prev
+        mask[:, t] = m_prev
+        # behaviour policy: [stop, forward, left, right]
+        towards_left = theta > 0
+        p = np.zeros((E, 4))
+        near = d <= 0.2
+        p[:, 0] = np.where(near, 0.97, 0.02)
+        rest = 1.0 - p[:, 0]
+        p[:, 1] = rest * 0.6 / 0.98
+        p[:, 2] = rest * np.where(towards_left, 0.28, 0.10) / 0.98
+        p[:, 3] = rest * np.where(towards_left, 0.10, 0.28) / 0.98
+        u = rng.random(E)
+        a = (u[:, None] > np.cumsum(p, axis=1)).sum(axis=1).clip(0, 3)
+        action[:, t] = a
+        logp_old[:, t] = np.log(p[np.arange(E), a]).astype(f32)
+        d_old = d.copy()
+        collide = rng.random(E) < 0.1
+        fwd = (a == 1) & ~collide
+        gx = d * np.cos(theta) - 0.25 * fwd
+        gy = d * np.sin(theta)
+        d = np.where(fwd, np.hypot(gx, gy), d)
+        theta = np.where(fwd, np.arctan2(gy, gx), theta)
+        theta = theta + np.where(a == 2, -np.pi / 18, 0.0) + np.where(a == 3, np.pi / 18, 0.0)
+        theta = (theta + np.pi) % (2 * np.pi) - np.pi
+        path = path + 0.25 * fwd
+        r = -(d - d_old) - 0.01
+        age = age + 1
+        ended = (a == 0) | (age >= 500)
+        success = (a == 0) & (d_old <= 0.2)
+        spl = np.where(success, d0 / np.maximum(d0, np.maximum(path, 1e-6)), 0.0)
+        r = r + 2.5 * spl
+        rew[:, t] = r.astype(f32)
+        done[:, t] = ended.astype(np.uint8)
+        # resets
+        nd0 = rng.uniform(1.0, 20.0, E)
+        nth = rng.uniform(-np.pi, np.pi, E)
+        d0 = np.where(ended, nd0, d0)
+        d = np.where(ended, nd0, d)
+        theta = np.where(ended, nth, theta)
+        path = np.where(ended, 0.0, path)
+        age = np.where(ended, 0, age)
+        prev = np.where(ended, START_TOKEN, a)
+        m_prev = np.where(ended, 0.0, 1.0)
+
+    if length is None:
+        length = T
+    length = np.broadcast_to(np.asarray(length, dtype=np.int32), (E,)).copy()
+    for n in range(E):
+        L = int(length[n])
+        for arr in (rew, done, action, prev_action, mask, logp_old):
+            arr[n, L:] = 0
+        val[n, L + 1:] = 0
+        goal[n, L:] = 0
+    h0 = rng.normal(0.0, 0.1, (E, hidden)).astype(f32)
+    return dict(rew=rew, val=val, done=done, length=length, goal=goal, prev_action=prev_action,
+                mask=mask, action=action, logp_old=logp_old, h0=h0, E=E, T=T, ld=ld)
+
+
+def init_params(entries, P, seed):
+    """entries: [(offset, numel, fan_in)] -> fp32 [P]; U(-1/sqrt(fan_in), 1/sqrt(fan_in)) (torch default)."""
+    rng = _rng(seed, 2)
+    out = np.zeros(P, np.float32)
+    for off, n, fan_in in entries:
+        k = 1.0 / np.sqrt(fan_in)
+        out[off:off + n] = rng.uniform(-k, k, n).astype(np.float32)
+    return out
+
+
+def perms(seed, iteration, epochs, E, rank=0):
+    """Epoch permutations of env ids, int32 [epochs][E] (input of step a4)."""
+    rng = _rng(seed, 3, rank, iteration)
+    return np.stack([rng.permutation(E).astype(np.int32) for _ in range(epochs)])
+
+
+def straggler_costs(seed, N, T, homogeneous=False, lo=1.0, hi=20.0):
+    """Per-rank per-step costs in ticks (>= 1): s_w log-uniform[lo, hi] with +-10% jitter."""
+    rng = _rng(seed, 4)
+    s = np.full(N, 10.0) if homogeneous else np.exp(rng.uniform(np.log(lo), np.log(hi), N))
+    jit = rng.uniform(-0.1, 0.1, (N, T))
+    return np.maximum(1, np.rint(s[:, None] * (1.0 + jit))).astype(np.int64)
+
+
+def random_loss_inputs(M, seed, A=NUM_ACTIONS, scale=1.0):
+    """Generic per-sample loss inputs (test fixtures for step a6)."""
+    rng = _rng(seed, 5)
+    f32 = np.float32
+    return dict(logits=(rng.normal(0, scale, (M, A))).astype(f32),
+                values=rng.normal(0, 1, M).astype(f32),
+                actions=rng.integers(0, A, M).astype(np.int32),
+                logp_old=np.log(rng.uniform(0.05, 0.95, M)).astype(f32),
+                values_old=rng.normal(0, 1, M).astype(f32),
+                returns=rng.normal(0, 1, M).astype(f32),
+                adv=rng.normal(0, 1, M).astype(f32))
