@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""DD-PPO learner-step benchmark (BASELINE.json metric: learner experience-steps/sec).
+
+One step = one whole learner step on one rollout per rank (SURVEY.md 8(a) rows a2..a8 + a10):
+GAE -> advantage normalisation (allreduce of sum/sum^2) -> 2 epochs x 2 minibatches of
+{actor-critic fwd, fused PPO loss+grad, bwd, gradient allreduce + clip + Adam} -> step
+accounting allreduce.  Workload: configs[1] "PointGoal GPS+Compass-only" (4 envs/GPU x 128
+steps, goal FC + embedding -> GRU-512 -> heads, 2 epochs x 2 minibatches), synthetic
+PointGoal-shaped rollouts (synth/), random-init weights.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config gps]
+
+Multi-GPU: torchrun (one process per GPU, NCCL); weak scaling (E envs per GPU).  The
+reference arm (--impl reference) is the CPU oracle (oracle/) run as it stands on the host.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps"])
+    ap.add_argument("--seed", type=int, default=1337)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm (the CPU oracle)
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:
+        return None
+
+
+def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None):
+    """Time the oracle's learner step (oracle/learner.py, as it stands) on the same workload."""
+    from oracle import learner as olearner
+    from oracle import models
+    c = synth.CONFIGS[cfgname]
+    offs, P = models.offsets(c["arch"], hidden=c["hidden"])
+    fans = {n: f for n, _, f in models.layout(c["arch"], hidden=c["hidden"])}
+    p = synth.init_params([(o, int(np.prod(s)), fans[k]) for k, (o, s) in offs.items()], P, seed)
+    m = np.zeros(P)
+    v = np.zeros(P)
+    step, n_steps, exp_steps = 0, 0, 0
+    t0 = time.perf_counter()
+    it = 0
+    while True:
+        ro = synth.rollout(c["E"], c["T"], seed, rank=0, iteration=it, hidden=c["hidden"])
+        pm = synth.perms(seed, it, c["epochs"], c["E"])
+        ts = time.perf_counter()
+        p, m, v, step, info = olearner.learner_step(c["arch"], p, m, v, step, [ro], [pm],
+                                                    dict(epochs=c["epochs"], minibatches=c["minibatches"]),
+                                                    hidden=c["hidden"])
+        exp_steps += info["steps"]
+        n_steps += 1
+        it += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_steps and n_steps >= max_steps):
+            break
+        del ts
+    return exp_steps / el, n_steps, el
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    c = synth.CONFIGS[args.config]
+    # each "step" is one oracle learner step on a bounded sample of the workload (whole rollouts)
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        oracle_steps_per_sec(args.config, args.seed, budget_s=0.0, max_steps=1)
+    sps, n, el = oracle_steps_per_sec(args.config, args.seed, budget_s=0.0, max_steps=args.steps)
+    out = {
+        "impl": "reference", "metric": "learner experience-steps/sec", "value": sps,
+        "unit": "experience-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / max(n, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"configs[1] {args.config}: {c['E']} envs x {c['T']} steps, "
+                               f"{c['epochs']} epochs x {c['minibatches']} minibatches, GRU-512",
+                   "rank0_only": True},
+        "cpu_baseline": {"value": sps, "unit": "experience-steps/s", "cores": blas_threads() or cpu_cores(),
+                         "kind": "oracle", "sample": f"{n} whole learner steps (rank-0 rollout, N=1 emulation)"},
+        "e2e": {"value": sps, "unit": "experience-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1911_00357_b200 as dd
+    from paper_1911_00357_b200.learner import Learner
+
+    uid = None
+    if world > 1:
+        obj = [dd.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = dd.Context(rank, world, uid, device=local)
+    c = synth.CONFIGS[args.config]
+    desc = dd.model_desc(c["arch"])
+    lay = dd.param_layout(desc)
+    P = dd.param_count(desc)
+    p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, args.seed)
+    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+    stream = torch.cuda.current_stream()
+    n_roll = 4  # distinct rollouts cycled through (different data every step)
+    rollouts = [synth.rollout(c["E"], c["T"], args.seed, rank=rank, iteration=i, hidden=desc.hidden)
+                for i in range(n_roll)]
+    perms = [synth.perms(args.seed, i, c["epochs"], c["E"], rank=rank) for i in range(n_roll)]
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(i):
+        lrn.load_rollout(rollouts[i % n_roll], perms[i % n_roll])
+        st = lrn.step(stream)
+        counts = dd.ddppo_allreduce_counts(ctx, [lrn.steps_per_rollout()])  # a10 step accounting
+        return st, int(counts[0])
+
+    # warm-up
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    ctx.check()
+
+    # ---- device-timed region: inputs already resident in HBM; L2 flushed between steps
+    sampler = ClockSampler(local)
+    sampler.start()
+    dd.profile_read(ctx, reset=True)
+    dd.profile_enable(ctx, True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    total_exp = 0
+    barrier()
+    t_wall0 = time.perf_counter()
+    for i in range(args.steps):
+        lrn.load_rollout(rollouts[i % n_roll], perms[i % n_roll])  # H2D of inputs, outside the events
+        flush.zero_()
+        ev[i][0].record(stream)
+        lrn.step(stream)
+        counts = dd.ddppo_allreduce_counts(ctx, [lrn.steps_per_rollout()])  # a10 step accounting
+        ev[i][1].record(stream)
+        total_exp += int(counts[0])
+    barrier()
+    t_wall = time.perf_counter() - t_wall0
+    dd.profile_enable(ctx, False)
+    prof = dd.profile_read(ctx, reset=True)
+    clocks = sampler.stop()
+    ctx.check()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms = float(t.item())
+    value = total_exp / (dev_ms / 1e3)
+
+    # ---- end-to-end: host (pinned) rollout -> device each step, stats read back each step
+    e2e = None
+    if not args.no_e2e:
+        pinned = []
+        for i in range(n_roll):
+            hb = lrn.pinned_host_buffers()
+            for k in hb:
+                hb[k].copy_(torch.from_numpy(np.ascontiguousarray(rollouts[i][k])).reshape(hb[k].shape))
+            pinned.append(hb)
+        h2d = sum(v.numel() * v.element_size() for v in pinned[0].values()) + perms[0].nbytes
+        d2h = lrn.stats.numel() * 4
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_exp = 0
+        e0.record(stream)
+        for i in range(args.steps):
+            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True)
+            lrn.step(stream)
+            _ = lrn.stats.cpu()  # D2H of the step's loss statistics
+            counts = dd.ddppo_allreduce_counts(ctx, [lrn.steps_per_rollout()])
+            e_exp += int(counts[0])
+        e1.record(stream)
+        barrier()
+        e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": e_exp / (float(e_ms.item()) / 1e3), "unit": "experience-steps/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---- roofline of the dominant kernel family (device time measured live above)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    fam_ms = {k: v[0] for k, v in prof.items()}
+    dom = max(fam_ms, key=fam_ms.get)
+    launches = {k: v[1] for k, v in prof.items()}
+    roofline = roofline_for(dom, prof, c, lrn, peaks, args.steps)
+    gpu_launches = int(sum(v for k, v in launches.items() if k != "allreduce"))
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sps, n, el = oracle_steps_per_sec(args.config, args.seed, budget_s=12.0)
+        cpu_base = {"value": sps, "unit": "experience-steps/s", "cores": blas_threads() or cpu_cores(),
+                    "kind": "oracle", "sample": f"{n} whole learner steps of the same workload ({el:.1f} s)"}
+
+    if rank == 0:
+        out = {
+            "metric": "learner experience-steps/sec", "value": value, "unit": "experience-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32+f16/bf16-mma", "data": "synthetic",
+            "config": {"workload": f"configs[1] {args.config}: PointGoal GPS+Compass, {c['E']} envs/GPU x "
+                                   f"{c['T']} steps, goal FC + action embedding -> GRU-{desc.hidden} -> heads, "
+                                   f"{c['epochs']} epochs x {c['minibatches']} minibatches, Adam",
+                       "E_per_gpu": c["E"], "T": c["T"], "params": P, "parallelism": f"dp{world}",
+                       "l2": "flushed between timed steps (256 MiB write), per-step CUDA events",
+                       "wall_s_timed_loop": t_wall},
+            "clocks": clocks, "e2e": e2e, "gpu_launches": gpu_launches,
+            "kernel_ms": {k: round(v, 4) for k, v in fam_ms.items() if v > 0},
+            "roofline": roofline, "cpu_baseline": cpu_base,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+def roofline_for(fam, prof, c, lrn, peaks, steps):
+    """Algorithmic work of one launch of the dominant family / its mean device time."""
+    ms, n = prof[fam]
+    per_launch_s = (ms / 1e3) / max(n, 1)
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    bf16 = peaks.get("bf16_tflops_sustained", 1400.0)
+    E, T, H = c["E"], c["T"], lrn.hidden
+    B = E // c["minibatches"]
+    if fam in ("net_fwd", "net_bwd") and c["arch"] == "gps":
+        # per launch: the recurrent matvecs on the dependency chain (fwd: W_hh h and W_ih x; bwd: W_hh^T dg)
+        flops = 2.0 * B * T * (3 * H) * (H + (64 if fam == "net_fwd" else 0))
+        achieved = flops / per_launch_s / 1e12
+        peak = bf16 * 0.5  # fp16 / bf16 mma.sync dense peak taken as the bf16 tensor figure (no tcgen05 here)
+        return {"bound": "tensor", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None, "launch_us": per_launch_s * 1e6,
+                "note": "latency-bound: 128 dependent steps x cluster barrier; see DESIGN.md"}
+    byte_per = {"gae": 17.0 * E * T, "loss": 60.0 * B * T, "adam": 32.0 * lrn.P}
+    b = byte_per.get(fam, 0.0)
+    achieved = b / per_launch_s / 1e9 if b else 0.0
+    return {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "launch_us": per_launch_s * 1e6}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,270 @@
+/*
+ * ddppo.h -- C ABI of the B200-native DD-PPO learner step (libddppo.so).
+ *
+ * Method: Decentralized Distributed PPO, arXiv 1911.00357 (/root/reference/PAPER.md,
+ * cited as P:Lnn = line nn).  One process per GPU runs a worker; every worker owns its
+ * rollout, computes grad J^PPO locally, the gradients are AllReduce-averaged and the same
+ * Adam update is applied everywhere (Eq. 3/4); stragglers' collection is
+ * preempted once p% of the workers are done.
+ *
+ * Conventions (every entry point):
+ *  - Pointers are DEVICE pointers unless the parameter name starts with `host_`.
+ *    The caller owns every buffer; the library never allocates or frees in the hot path.
+ *    The library owns only the opaque ddppo_ctx (NCCL communicator, small scratch, a
+ *    device error word).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
+ *    stream-ordered and asynchronous except the ones marked "blocking".
+ *  - Calls marked "collective" must be issued by every rank in the same order (a mismatch
+ *    deadlocks).  With world == 1 they perform no communication.
+ *  - One ctx must not be used from two streams concurrently (scratch is per ctx).
+ *  - Per-step rollout arrays are env-major [E][ld] (ld = row stride in elements, ld >= T+1,
+ *    ld % 4 == 0 enables 16-byte vector loads).  The value row holds T+1 slots: slot L_n is
+ *    the bootstrap value V(s_{L_n}) of an env truncated at length L_n (P:L171 preemption).
+ *  - Errors: every function returns ddppo_status; ddppo_last_error(ctx) gives the message.
+ *    Non-finite losses/gradients set a device flag that ddppo_check() reports as
+ *    DDPPO_ERR_NUMERICAL.
+ */
+#ifndef DDPPO_H_
+#define DDPPO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDPPO_ABI_VERSION 1
+
+typedef enum {
+  DDPPO_OK = 0,
+  DDPPO_ERR_CONFIG = 1,      /* shape / dim / alignment / enum problem                */
+  DDPPO_ERR_NUMERICAL = 2,   /* non-finite loss or gradient detected on the device     */
+  DDPPO_ERR_PROTOCOL = 3,    /* ranks disagree (layout hash, lengths)                  */
+  DDPPO_ERR_COMM = 4,        /* NCCL error -- fatal to the job (no elasticity) */
+  DDPPO_ERR_CUDA = 5,        /* CUDA runtime error                                     */
+  DDPPO_ERR_UNSUPPORTED = 6  /* device is not sm_100 / feature not built               */
+} ddppo_status;
+
+typedef struct ddppo_ctx ddppo_ctx;
+
+int ddppo_abi_version(void);
+const char* ddppo_status_string(ddppo_status s);
+
+/* ------------------------------------------------------------------ context
+ * Rank 0 calls ddppo_get_unique_id, broadcasts the 128 bytes (e.g. over a torch process
+ * group), then every rank calls ddppo_ctx_create (collective when world > 1). */
+ddppo_status ddppo_get_unique_id(uint8_t host_id[128]);
+ddppo_status ddppo_ctx_create(int rank, int world, const uint8_t* host_id /* NULL if world==1 */,
+                              int device, ddppo_ctx** host_out);
+ddppo_status ddppo_ctx_destroy(ddppo_ctx* ctx);
+const char* ddppo_last_error(const ddppo_ctx* ctx);
+/* blocking: synchronises `stream`, then reads and clears the device error word. */
+ddppo_status ddppo_check(ddppo_ctx* ctx, void* stream);
+
+/* ------------------------------------------------------------------ a2: GAE
+ * P:L218 (sec.4): GAE with discount gamma (0.99) and GAE parameter tau (0.95); per env n,
+ * for t = L_n-1 .. 0:  delta_t = r_t + gamma*V_{t+1}*(1-done_t) - V_t,
+ *                      A_t = delta_t + gamma*tau*(1-done_t)*A_{t+1}, A_{L_n} = 0,
+ *                      R_t = A_t + V_t;  A_t = R_t = 0 for L_n <= t < T.
+ * rew, done, adv, ret: [E][ld]; val: [E][ld] with T+1 meaningful slots; len: [E] (1..T).
+ * stats3 (nullable, device double[3]) receives the local {sum A, sum A^2, n} over valid t
+ * (deterministic fixed-order reduction), the input of ddppo_adv_norm. */
+ddppo_status ddppo_gae(ddppo_ctx* ctx, const float* rew, const float* val, const uint8_t* done,
+                       const int32_t* len, int E, int T, int ld, float gamma, float tau,
+                       float* adv, float* ret, double* stats3, void* stream);
+
+/* ------------------------------------------------------------------ a3: advantage normalisation
+ * Not in the paper (P:L219 says advantages are NOT normalised); required by the north_star.
+ * collective: stats3 (device double[3]) is allreduced (sum) in place across ranks, then
+ * mean_invstd (device float[2]) = { mu = S/n, 1/(sigma + eps) }, sigma^2 = (Q - n mu^2)/(n-1).
+ * The normalisation itself is applied on the fly by ddppo_ppo_loss_grad. */
+ddppo_status ddppo_adv_norm(ddppo_ctx* ctx, double* stats3, float eps, float* mean_invstd,
+                            void* stream);
+
+/* ------------------------------------------------------------------ model description
+ * P:L582-593 (App. C) agent: goal [d, cos th, sin th] -> FC 32; previous-action embedding 32
+ * (start token = num_actions); recurrent policy; FC -> softmax over actions + value.
+ *   DDPPO_ARCH_TOY_MLP : goal -> Linear(3,64) -> tanh -> Linear(64, A+1)        (configs[0])
+ *   DDPPO_ARCH_GPS_GRU : goal -> Linear(3,32); Embedding(A+1,32); x = [goal, act] ->
+ *                        GRU(64, hidden=512) -> Linear(hidden, A+1)              (configs[1])
+ * Flat parameter layout: the tensors below in this order, row-major, each starting at an
+ * offset rounded up to a multiple of 4 floats (PyTorch shapes/conventions):
+ *   TOY: fc1.weight[64][3] fc1.bias[64] head.weight[A+1][64] head.bias[A+1]
+ *   GPS: goal_fc.weight[32][3] goal_fc.bias[32] act_embed.weight[A+1][32]
+ *        rnn.weight_ih[3H][64] rnn.weight_hh[3H][H] rnn.bias_ih[3H] rnn.bias_hh[3H]
+ *        head.weight[A+1][H] head.bias[A+1]           (GRU gate rows r, z, n)
+ * head rows 0..A-1 are the action logits, row A the value.  num_actions must be 4;
+ * GPS requires hidden == 512. */
+typedef enum { DDPPO_ARCH_TOY_MLP = 0, DDPPO_ARCH_GPS_GRU = 1 } ddppo_arch;
+
+typedef struct {
+  int32_t arch;        /* ddppo_arch */
+  int32_t hidden;      /* 64 (toy) / 512 (gps) */
+  int32_t num_actions; /* 4 */
+  int32_t reserved[5];
+} ddppo_model_desc;
+
+typedef struct {
+  char name[48];
+  int64_t offset;   /* in floats */
+  int64_t numel;
+  int32_t ndim;
+  int32_t fan_in;   /* used by the default initialiser U(-1/sqrt(fan_in), 1/sqrt(fan_in)) */
+  int64_t shape[4];
+} ddppo_tensor_info;
+
+ddppo_status ddppo_model_param_count(const ddppo_model_desc* host_desc, int64_t* host_P);
+ddppo_status ddppo_model_param_layout(const ddppo_model_desc* host_desc, ddppo_tensor_info* host_out,
+                                      int cap, int* host_n);
+/* bytes of device workspace ddppo_policy_fwd/bwd need for minibatches of <= max_B envs and
+ * <= T steps (16-byte aligned base required). */
+ddppo_status ddppo_workspace_size(const ddppo_model_desc* host_desc, int max_B, int T,
+                                  size_t* host_bytes);
+
+/* One PPO minibatch = B whole env trajectories (reading Z13: minibatches partition envs,
+ * P:L219).  Samples are ordered m = b*T_run + t (b-th env of env_idx, time t). */
+typedef struct {
+  const float* goal;          /* [E][T][3]   (d, cos th, sin th)            */
+  const int32_t* prev_action; /* [E][ld]     start token = num_actions         */
+  const float* mask;          /* [E][ld]     1 - done_{t-1}; state is multiplied by it */
+  const float* h0;            /* [E][hidden] recurrent state before step 0 (no grad)    */
+  const int32_t* len;         /* [E]         valid steps per env                        */
+  const int32_t* env_idx;     /* [B]         env ids of this minibatch                  */
+  int32_t E, T, ld, B;
+  int32_t T_run;              /* steps to run: max len over the minibatch (host value)  */
+  int32_t n_valid;            /* sum over the B envs of min(len, T_run) (host value)    */
+} ddppo_batch;
+
+/* a5: logits [B][T_run][A], values [B][T_run]; saves activations in ws for the backward. */
+ddppo_status ddppo_policy_fwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const float* params,
+                              const ddppo_batch* host_batch, float* logits, float* values,
+                              void* ws, size_t ws_bytes, void* stream);
+/* a7: grad [P] is OVERWRITTEN with dL/dparams given dL/dlogits, dL/dvalues (same layout as
+ * the forward outputs); requires the ws of the matching ddppo_policy_fwd call. */
+ddppo_status ddppo_policy_bwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const float* params,
+                              const ddppo_batch* host_batch, const float* dlogits,
+                              const float* dvalues, float* grad, void* ws, size_t ws_bytes,
+                              void* stream);
+
+/* ------------------------------------------------------------------ a6: fused PPO loss + gradient
+ * P:L129-138 (Eq. 2) clipped surrogate on r_t = exp(lp - lp_old); value loss
+ * 0.5*max((v-R)^2, (v_clip-R)^2) with v_clip = v_old + clip(v - v_old, +-vclip_eps) (or
+ * 0.5*(v-R)^2 when use_value_clip == 0); entropy bonus.  Per-worker mean over the n_valid
+ * valid samples (P:L171 equal weighting).  L = L_pi + c_v L_v - c_e H.
+ * Tie conventions are torch's (min/max split 1/2-1/2, clamp passes on the closed interval).
+ * stats (device float[8]) = {policy_loss, value_loss, entropy, clip_frac, approx_kl, total,
+ * n_valid, 0}.  dlogits/dvalues have the logits/values layout; invalid samples get 0. */
+typedef struct {
+  const int32_t* action;    /* [E][ld] */
+  const float* logp_old;    /* [E][ld] log pi_old(a_t|o_t) */
+  const float* value_old;   /* [E][ld] V_hat_t of the rollout (the value row)   */
+  const float* ret;         /* [E][ld] R_t (ddppo_gae) */
+  const float* adv;         /* [E][ld] A_t (ddppo_gae, un-normalised) */
+} ddppo_loss_inputs;
+
+typedef struct {
+  float clip_eps;        /* 0.2   */
+  float vclip_eps;       /* 0.2   */
+  float c_v;             /* 0.5   */
+  float c_e;             /* 0.01  */
+  int32_t use_value_clip;
+  int32_t normalize_adv; /* if set, mean_invstd must be non-NULL */
+} ddppo_loss_cfg;
+
+ddppo_status ddppo_ppo_loss_grad(ddppo_ctx* ctx, const float* logits, const float* values,
+                                 const ddppo_batch* host_batch, const ddppo_loss_inputs* host_in,
+                                 const float* mean_invstd, const ddppo_loss_cfg* host_cfg,
+                                 float* dlogits, float* dvalues, float* stats, void* stream);
+
+/* ------------------------------------------------------------------ a8: AllReduce-mean + clip + Adam
+ * P:L150-158 (Eq. 3), P:L219 (Adam, lr 2.5e-4).  collective.  grad [P] is summed over ranks in
+ * place (NCCL, fp32), then one fused pass: g = sum/N; c = min(1, max_grad_norm/(||g||_2+1e-6))
+ * (skipped if max_grad_norm <= 0); Adam (PyTorch form, bias-corrected, `step` = 1-based index
+ * of this update) on every entry whose freeze_mask byte is 0 (freeze_mask nullable).
+ * grad_norm (nullable, device float[1]) receives ||g|| before clipping. */
+typedef struct {
+  float lr, beta1, beta2, eps, max_grad_norm;
+  int32_t step;
+} ddppo_adam_cfg;
+
+ddppo_status ddppo_grad_allreduce_step(ddppo_ctx* ctx, float* grad, float* params, float* m, float* v,
+                                       const uint8_t* freeze_mask, int64_t P,
+                                       const ddppo_adam_cfg* host_cfg, float* grad_norm, void* stream);
+
+/* ------------------------------------------------------------------ a9: preemption protocol
+ * stragglers stop collecting once p% of the workers have finished, but never before
+ * one-fourth of the maximum steps.  Readings: K = ceil(p*N/100) (other_workers: ceil(p*(N-1)/100),
+ * clamped >= 1); min_steps = ceil(T/4) unless overridden (> 0).  Decision after completing a
+ * step: stop iff my_steps >= T, or (my_steps >= min_steps and finished_count >= K). */
+typedef struct {
+  int32_t p_percent;     /* 1..100 (60 works well) */
+  int32_t T;             /* rollout capacity */
+  int32_t min_steps;     /* 0 => ceil(T/4) */
+  int32_t other_workers; /* alternate reading of "p% of the other workers" */
+} ddppo_preempt_cfg;
+
+/* pure host arithmetic (no ctx, no GPU) */
+ddppo_status ddppo_preempt_threshold(const ddppo_preempt_cfg* host_cfg, int world, int* host_K,
+                                     int* host_min_steps);
+ddppo_status ddppo_preempt_decide(const ddppo_preempt_cfg* host_cfg, int world, int my_steps,
+                                  int finished_count, int* host_should_stop);
+/* collective, blocking: allreduce(sum) of {finished (0/1: this rank completed T steps),
+ * active (0/1: still collecting)} across ranks (the paper's TCPStore counter, P:L176/P:L637,
+ * realised as an int32 allreduce per poll tick), then the decision above for this rank. */
+ddppo_status ddppo_preempt_poll(ddppo_ctx* ctx, int my_steps, int finished, int active,
+                                const ddppo_preempt_cfg* host_cfg, int* host_should_stop,
+                                int* host_finished_count, int* host_active_count);
+
+/* a10: collective, blocking int64 sum of n host values (step accounting). */
+ddppo_status ddppo_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n);
+
+/* ------------------------------------------------------------------ the whole learner step
+ * a2..a8 for one rollout on this rank: GAE -> (adv norm) -> epochs x minibatches of
+ * {policy_fwd, ppo_loss_grad, policy_bwd, grad_allreduce_step}.  collective. */
+typedef struct {
+  const float* rew; const float* val; const uint8_t* done; const int32_t* len;
+  const float* goal; const int32_t* prev_action; const float* mask; const float* h0;
+  const int32_t* action; const float* logp_old;
+  const int32_t* perms;       /* [epochs][E] device: env permutation per epoch (a4 input) */
+  const int32_t* host_len;    /* [E] host copy of len */
+  const int32_t* host_perms;  /* [epochs][E] host copy of perms */
+  int32_t E, T, ld;
+} ddppo_rollout;
+
+typedef struct {
+  float gamma, tau, adv_eps;
+  int32_t normalize_adv;
+  int32_t epochs, minibatches;
+  ddppo_loss_cfg loss;
+  ddppo_adam_cfg adam;        /* adam.step = number of updates already taken */
+} ddppo_learner_cfg;
+
+ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int E, int T, int ld,
+                                          int minibatches, int epochs, size_t* host_bytes);
+/* params/m/v [P] updated in place; adv/ret [E][ld] outputs; stats_out (device float
+ * [epochs*minibatches][8]) receives each minibatch's loss stats; host_cfg->adam.step is read,
+ * *host_step_out receives the new update count. */
+ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
+                                const ddppo_rollout* host_ro, const ddppo_learner_cfg* host_cfg,
+                                float* params, float* m, float* v, float* adv, float* ret,
+                                float* stats_out, void* ws, size_t ws_bytes,
+                                int32_t* host_step_out, void* stream);
+
+/* ------------------------------------------------------------------ measurement
+ * Per-kernel-family device time (CUDA events recorded on the launching stream around every
+ * launch of the family while profiling is enabled) and launch counts (always counted).
+ * ddppo_profile_read is blocking (synchronises the recorded events); reset != 0 clears. */
+typedef enum {
+  DDPPO_K_GAE = 0, DDPPO_K_ADV_NORM, DDPPO_K_NET_FWD, DDPPO_K_HEAD, DDPPO_K_LOSS, DDPPO_K_NET_BWD,
+  DDPPO_K_WGRAD, DDPPO_K_ALLREDUCE, DDPPO_K_ADAM, DDPPO_K_OTHER, DDPPO_K_COUNT
+} ddppo_kernel_family;
+
+ddppo_status ddppo_profile_enable(ddppo_ctx* ctx, int enable);
+ddppo_status ddppo_profile_read(ddppo_ctx* ctx, double* host_ms /* [DDPPO_K_COUNT] */,
+                                int64_t* host_launches /* [DDPPO_K_COUNT] */, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDPPO_H_ */

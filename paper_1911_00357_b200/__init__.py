@@ -1,0 +1,219 @@
+"""B200-native DD-PPO learner step (arXiv 1911.00357) behind the C ABI of include/ddppo.h.
+
+The functions below carry the C names and only marshal arguments; torch is used for
+device memory, streams and process groups.  See DESIGN.md.
+"""
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import (ARCH_GPS, ARCH_TOY, AdamCfg, Batch, DdppoError, LearnerCfg, LossCfg, LossInputs, ModelDesc,
+                   PreemptCfg, Rollout, TensorInfo, check, dptr, f32, f64, i32, lib, u8)
+
+__all__ = ["Context", "model_desc", "param_layout", "ddppo_gae", "ddppo_adv_norm", "ddppo_policy_fwd",
+           "ddppo_policy_bwd", "ddppo_ppo_loss_grad", "ddppo_grad_allreduce_step", "ddppo_preempt_poll",
+           "ddppo_preempt_decide", "ddppo_preempt_threshold", "ddppo_allreduce_counts", "ddppo_learner_step",
+           "DdppoError", "lib"]
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def model_desc(arch, hidden=None, num_actions=4):
+    arch_id = {"toy": ARCH_TOY, "gps": ARCH_GPS}.get(arch, arch)
+    if hidden is None:
+        hidden = 64 if arch_id == ARCH_TOY else 512
+    d = ModelDesc()
+    d.arch, d.hidden, d.num_actions = arch_id, hidden, num_actions
+    return d
+
+
+def param_count(desc):
+    P = ctypes.c_int64()
+    check("ddppo_model_param_count", lib.ddppo_model_param_count(ctypes.byref(desc), ctypes.byref(P)))
+    return P.value
+
+
+def param_layout(desc):
+    """[(name, offset, shape, fan_in)] in the documented order."""
+    n = ctypes.c_int()
+    check("ddppo_model_param_layout", lib.ddppo_model_param_layout(ctypes.byref(desc), None, 0, ctypes.byref(n)))
+    arr = (TensorInfo * n.value)()
+    check("ddppo_model_param_layout", lib.ddppo_model_param_layout(ctypes.byref(desc), arr, n.value, ctypes.byref(n)))
+    return [(t.name.decode(), t.offset, tuple(t.shape[:t.ndim]), t.fan_in) for t in arr]
+
+
+def workspace_size(desc, max_B, T):
+    b = ctypes.c_size_t()
+    check("ddppo_workspace_size", lib.ddppo_workspace_size(ctypes.byref(desc), max_B, T, ctypes.byref(b)))
+    return b.value
+
+
+def learner_workspace_size(desc, E, T, ld, minibatches, epochs):
+    b = ctypes.c_size_t()
+    check("ddppo_learner_workspace_size",
+          lib.ddppo_learner_workspace_size(ctypes.byref(desc), E, T, ld, minibatches, epochs, ctypes.byref(b)))
+    return b.value
+
+
+def get_unique_id():
+    buf = (ctypes.c_uint8 * 128)()
+    check("ddppo_get_unique_id", lib.ddppo_get_unique_id(buf))
+    return bytes(buf)
+
+
+class Context:
+    """Owns a ddppo_ctx (NCCL communicator + scratch) for one rank."""
+
+    def __init__(self, rank=0, world=1, unique_id=None, device=0):
+        self.rank, self.world, self.device = rank, world, device
+        h = ctypes.c_void_p()
+        idbuf = None
+        if world > 1:
+            idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        code = lib.ddppo_ctx_create(rank, world, idbuf, device, ctypes.byref(h))
+        check("ddppo_ctx_create", code)
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib.ddppo_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, stream=None):
+        check("ddppo_check", lib.ddppo_check(self.h, _stream(stream)), self.h)
+
+
+def _call(ctx, fn, *args):
+    check(fn, getattr(lib, fn)(ctx.h, *args), ctx.h)
+
+
+def ddppo_gae(ctx, rew, val, done, length, E, T, ld, gamma, tau, adv, ret, stats3=None, stream=None):
+    _call(ctx, "ddppo_gae", f32(rew), f32(val), u8(done), i32(length), E, T, ld, gamma, tau, f32(adv),
+          f32(ret), f64(stats3), _stream(stream))
+
+
+def ddppo_adv_norm(ctx, stats3, eps, mean_invstd, stream=None):
+    _call(ctx, "ddppo_adv_norm", f64(stats3), eps, f32(mean_invstd), _stream(stream))
+
+
+def make_batch(goal, prev_action, mask, h0, length, env_idx, E, T, ld, B, T_run, n_valid):
+    b = Batch()
+    b.goal, b.prev_action, b.mask, b.h0 = f32(goal), i32(prev_action), f32(mask), f32(h0)
+    b.len, b.env_idx = i32(length), i32(env_idx)
+    b.E, b.T, b.ld, b.B, b.T_run, b.n_valid = E, T, ld, B, T_run, n_valid
+    b._keep = (goal, prev_action, mask, h0, length, env_idx)  # the struct holds raw device pointers
+    return b
+
+
+def ddppo_policy_fwd(ctx, desc, params, batch, logits, values, ws, stream=None):
+    _call(ctx, "ddppo_policy_fwd", ctypes.byref(desc), f32(params), ctypes.byref(batch), f32(logits),
+          f32(values), dptr(ws), ws.numel() * ws.element_size(), _stream(stream))
+
+
+def ddppo_policy_bwd(ctx, desc, params, batch, dlogits, dvalues, grad, ws, stream=None):
+    _call(ctx, "ddppo_policy_bwd", ctypes.byref(desc), f32(params), ctypes.byref(batch), f32(dlogits),
+          f32(dvalues), f32(grad), dptr(ws), ws.numel() * ws.element_size(), _stream(stream))
+
+
+def loss_cfg(clip_eps=0.2, vclip_eps=0.2, c_v=0.5, c_e=0.01, use_value_clip=True, normalize_adv=True):
+    c = LossCfg()
+    c.clip_eps, c.vclip_eps, c.c_v, c.c_e = clip_eps, vclip_eps, c_v, c_e
+    c.use_value_clip, c.normalize_adv = int(use_value_clip), int(normalize_adv)
+    return c
+
+
+def ddppo_ppo_loss_grad(ctx, logits, values, batch, action, logp_old, value_old, ret, adv, mean_invstd, cfg,
+                        dlogits, dvalues, stats, stream=None):
+    li = LossInputs()
+    li.action, li.logp_old, li.value_old, li.ret, li.adv = (i32(action), f32(logp_old), f32(value_old),
+                                                            f32(ret), f32(adv))
+    _call(ctx, "ddppo_ppo_loss_grad", f32(logits), f32(values), ctypes.byref(batch), ctypes.byref(li),
+          f32(mean_invstd), ctypes.byref(cfg), f32(dlogits), f32(dvalues), f32(stats), _stream(stream))
+
+
+def adam_cfg(step, lr=2.5e-4, beta1=0.9, beta2=0.999, eps=1e-8, max_grad_norm=0.5):
+    c = AdamCfg()
+    c.lr, c.beta1, c.beta2, c.eps, c.max_grad_norm, c.step = lr, beta1, beta2, eps, max_grad_norm, step
+    return c
+
+
+def ddppo_grad_allreduce_step(ctx, grad, params, m, v, cfg, freeze_mask=None, grad_norm=None, stream=None):
+    _call(ctx, "ddppo_grad_allreduce_step", f32(grad), f32(params), f32(m), f32(v), u8(freeze_mask),
+          params.numel(), ctypes.byref(cfg), f32(grad_norm), _stream(stream))
+
+
+def preempt_cfg(p_percent, T, min_steps=0, other_workers=False):
+    c = PreemptCfg()
+    c.p_percent, c.T, c.min_steps, c.other_workers = p_percent, T, min_steps, int(other_workers)
+    return c
+
+
+def ddppo_preempt_threshold(cfg, world):
+    K, ms = ctypes.c_int(), ctypes.c_int()
+    check("ddppo_preempt_threshold", lib.ddppo_preempt_threshold(ctypes.byref(cfg), world, ctypes.byref(K),
+                                                                 ctypes.byref(ms)))
+    return K.value, ms.value
+
+
+def ddppo_preempt_decide(cfg, world, my_steps, finished_count):
+    out = ctypes.c_int()
+    check("ddppo_preempt_decide", lib.ddppo_preempt_decide(ctypes.byref(cfg), world, my_steps, finished_count,
+                                                           ctypes.byref(out)))
+    return bool(out.value)
+
+
+def ddppo_preempt_poll(ctx, my_steps, finished, active, cfg):
+    stop, fin, act = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _call(ctx, "ddppo_preempt_poll", my_steps, int(finished), int(active), ctypes.byref(cfg), ctypes.byref(stop),
+          ctypes.byref(fin), ctypes.byref(act))
+    return bool(stop.value), fin.value, act.value
+
+
+def ddppo_allreduce_counts(ctx, values):
+    arr = np.ascontiguousarray(np.asarray(values, dtype=np.int64))
+    _call(ctx, "ddppo_allreduce_counts", arr.ctypes.data, arr.size)
+    return arr
+
+
+def learner_cfg(epochs=2, minibatches=2, gamma=0.99, tau=0.95, normalize_adv=True, adv_eps=1e-5, loss=None,
+                adam=None):
+    c = LearnerCfg()
+    c.gamma, c.tau, c.adv_eps, c.normalize_adv = gamma, tau, adv_eps, int(normalize_adv)
+    c.epochs, c.minibatches = epochs, minibatches
+    c.loss = loss or loss_cfg(normalize_adv=normalize_adv)
+    c.adam = adam or adam_cfg(0)
+    return c
+
+
+def profile_enable(ctx, on=True):
+    _call(ctx, "ddppo_profile_enable", int(on))
+
+
+def profile_read(ctx, reset=False):
+    """{family: (ms, launches)} accumulated since the last reset (blocking)."""
+    n = len(_lib.KERNEL_FAMILIES)
+    ms = (ctypes.c_double * n)()
+    la = (ctypes.c_int64 * n)()
+    _call(ctx, "ddppo_profile_read", ms, la, int(reset))
+    return {k: (ms[i], la[i]) for i, k in enumerate(_lib.KERNEL_FAMILIES)}
+
+
+def ddppo_learner_step(ctx, desc, ro, cfg, params, m, v, adv, ret, stats_out, ws, stream=None):
+    """ro: Rollout struct (device pointers + host lengths/perms). Returns the new Adam step count."""
+    step = ctypes.c_int32()
+    _call(ctx, "ddppo_learner_step", ctypes.byref(desc), ctypes.byref(ro), ctypes.byref(cfg), f32(params), f32(m),
+          f32(v), f32(adv), f32(ret), f32(stats_out), dptr(ws), ws.numel() * ws.element_size(),
+          ctypes.byref(step), _stream(stream))
+    return step.value

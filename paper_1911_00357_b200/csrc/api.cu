@@ -1,0 +1,448 @@
+// C-ABI entry points of libddppo.so (include/ddppo.h): context / NCCL plumbing, argument
+// checking, the preemption protocol and the learner-step runtime that sequences the kernels.
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+extern "C" {
+
+int ddppo_abi_version(void) { return DDPPO_ABI_VERSION; }
+
+const char* ddppo_status_string(ddppo_status s) {
+  switch (s) {
+    case DDPPO_OK: return "ok";
+    case DDPPO_ERR_CONFIG: return "config";
+    case DDPPO_ERR_NUMERICAL: return "numerical";
+    case DDPPO_ERR_PROTOCOL: return "protocol";
+    case DDPPO_ERR_COMM: return "comm";
+    case DDPPO_ERR_CUDA: return "cuda";
+    case DDPPO_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown";
+}
+
+ddppo_status ddppo_get_unique_id(uint8_t host_id[128]) {
+  if (!host_id) return DDPPO_ERR_CONFIG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return DDPPO_ERR_COMM;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(host_id, &id, 128);
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_ctx_create(int rank, int world, const uint8_t* host_id, int device, ddppo_ctx** host_out) {
+  if (!host_out || world < 1 || rank < 0 || rank >= world) return DDPPO_ERR_CONFIG;
+  *host_out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return DDPPO_ERR_UNSUPPORTED;
+  if (device < 0 || device >= ndev) return DDPPO_ERR_CONFIG;
+  if (cudaSetDevice(device) != cudaSuccess) return DDPPO_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return DDPPO_ERR_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return DDPPO_ERR_UNSUPPORTED;  // built for sm_100a only
+  ddppo_ctx* ctx = new ddppo_ctx();
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  bool ok = cudaMalloc(&ctx->d_err, sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_counters, CNT_NUM * sizeof(unsigned int)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_partials, kMaxPartials * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_scalars, 64 * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_i32, 64 * sizeof(int32_t)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_i64, kMaxCountVals * sizeof(int64_t)) == cudaSuccess;
+  ok = ok && cudaMemset(ctx->d_err, 0, sizeof(int)) == cudaSuccess &&
+       cudaMemset(ctx->d_counters, 0, CNT_NUM * sizeof(unsigned int)) == cudaSuccess &&
+       cudaDeviceSynchronize() == cudaSuccess;
+  if (!ok) {
+    ddppo_ctx_destroy(ctx);
+    return DDPPO_ERR_CUDA;
+  }
+  if (world > 1) {
+    if (!host_id) {
+      ddppo_ctx_destroy(ctx);
+      return DDPPO_ERR_CONFIG;
+    }
+    ncclUniqueId id;
+    memcpy(&id, host_id, 128);
+    if (ncclCommInitRank(&ctx->comm, world, id, rank) != ncclSuccess) {
+      ctx->comm = nullptr;
+      ddppo_ctx_destroy(ctx);
+      return DDPPO_ERR_COMM;
+    }
+  }
+  *host_out = ctx;
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_ctx_destroy(ddppo_ctx* ctx) {
+  if (!ctx) return DDPPO_OK;
+  for (auto& r : ctx->pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : ctx->pool) cudaEventDestroy(e);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  cudaFree(ctx->d_err);
+  cudaFree(ctx->d_counters);
+  cudaFree(ctx->d_partials);
+  cudaFree(ctx->d_scalars);
+  cudaFree(ctx->d_i32);
+  cudaFree(ctx->d_i64);
+  delete ctx;
+  return DDPPO_OK;
+}
+
+const char* ddppo_last_error(const ddppo_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null ctx"; }
+
+ddppo_status ddppo_check(ddppo_ctx* ctx, void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_CUDA_TRY(ctx, cudaStreamSynchronize(as_stream(stream)));
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  int err = 0;
+  DDPPO_CUDA_TRY(ctx, cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) {
+    DDPPO_CUDA_TRY(ctx, cudaMemset(ctx->d_err, 0, sizeof(int)));
+    ctx->last_error = std::string("non-finite value in ") + ((err & ERR_BIT_LOSS) ? "loss " : "") +
+                      ((err & ERR_BIT_GRAD) ? "gradient" : "");
+    return DDPPO_ERR_NUMERICAL;
+  }
+  return DDPPO_OK;
+}
+
+// ------------------------------------------------------------------ a2 / a3
+ddppo_status ddppo_gae(ddppo_ctx* ctx, const float* rew, const float* val, const uint8_t* done, const int32_t* len,
+                       int E, int T, int ld, float gamma, float tau, float* adv, float* ret, double* stats3,
+                       void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, E == 0 || (rew && val && done && len && adv && ret), "gae: null pointer");
+  return launch_gae(ctx, rew, val, done, len, E, T, ld, gamma, tau, adv, ret, stats3, as_stream(stream));
+}
+
+ddppo_status ddppo_adv_norm(ddppo_ctx* ctx, double* stats3, float eps, float* mean_invstd, void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, stats3 && mean_invstd, "adv_norm: null pointer");
+  cudaStream_t st = as_stream(stream);
+  if (ctx->world > 1) {
+    ProfScope ps(ctx, DDPPO_K_ALLREDUCE, st, 0);
+    DDPPO_NCCL_TRY(ctx, ncclAllReduce(stats3, stats3, 3, ncclFloat64, ncclSum, ctx->comm, st));
+  }
+  return launch_adv_finalize(ctx, stats3, eps, mean_invstd, st);
+}
+
+// ------------------------------------------------------------------ model
+ddppo_status ddppo_model_param_count(const ddppo_model_desc* host_desc, int64_t* host_P) {
+  ModelLayout L;
+  if (!host_P || build_layout(host_desc, &L) != DDPPO_OK) return DDPPO_ERR_CONFIG;
+  *host_P = L.P;
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_model_param_layout(const ddppo_model_desc* host_desc, ddppo_tensor_info* host_out, int cap,
+                                      int* host_n) {
+  ModelLayout L;
+  if (!host_n || build_layout(host_desc, &L) != DDPPO_OK) return DDPPO_ERR_CONFIG;
+  *host_n = L.n;
+  if (host_out)
+    for (int i = 0; i < L.n && i < cap; ++i) host_out[i] = L.t[i];
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_workspace_size(const ddppo_model_desc* host_desc, int max_B, int T, size_t* host_bytes) {
+  ModelLayout L;
+  if (!host_bytes || build_layout(host_desc, &L) != DDPPO_OK || max_B < 1 || T < 1) return DDPPO_ERR_CONFIG;
+  *host_bytes = host_desc->arch == DDPPO_ARCH_TOY_MLP ? toy_workspace(max_B, T) : gps_workspace(max_B, T);
+  return DDPPO_OK;
+}
+
+static ddppo_status check_batch(ddppo_ctx* ctx, const ddppo_batch* b) {
+  DDPPO_REQUIRE(ctx, b != nullptr, "null batch");
+  DDPPO_REQUIRE(ctx, b->B >= 1 && b->T >= 1 && b->T_run >= 1 && b->T_run <= b->T && b->ld >= b->T + 1 &&
+                         b->E >= b->B,
+                "batch: need 1 <= B <= E, 1 <= T_run <= T, ld >= T+1");
+  DDPPO_REQUIRE(ctx, b->goal && b->len && b->env_idx, "batch: null pointer");
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_policy_fwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const float* params,
+                              const ddppo_batch* host_batch, float* logits, float* values, void* ws, size_t ws_bytes,
+                              void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  ModelLayout L;
+  DDPPO_REQUIRE(ctx, build_layout(host_desc, &L) == DDPPO_OK, "bad model descriptor");
+  ddppo_status s = check_batch(ctx, host_batch);
+  if (s != DDPPO_OK) return s;
+  size_t need = 0;
+  ddppo_workspace_size(host_desc, host_batch->B, host_batch->T_run, &need);
+  DDPPO_REQUIRE(ctx, ws && ws_bytes >= need, "workspace too small");
+  if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
+    return toy_fwd(ctx, L, params, *host_batch, logits, values, ws, as_stream(stream));
+  DDPPO_REQUIRE(ctx, host_batch->prev_action && host_batch->mask && host_batch->h0, "gps batch: null pointer");
+  return gps_fwd(ctx, L, params, *host_batch, logits, values, ws, as_stream(stream));
+}
+
+ddppo_status ddppo_policy_bwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const float* params,
+                              const ddppo_batch* host_batch, const float* dlogits, const float* dvalues, float* grad,
+                              void* ws, size_t ws_bytes, void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  ModelLayout L;
+  DDPPO_REQUIRE(ctx, build_layout(host_desc, &L) == DDPPO_OK, "bad model descriptor");
+  ddppo_status s = check_batch(ctx, host_batch);
+  if (s != DDPPO_OK) return s;
+  size_t need = 0;
+  ddppo_workspace_size(host_desc, host_batch->B, host_batch->T_run, &need);
+  DDPPO_REQUIRE(ctx, ws && ws_bytes >= need, "workspace too small");
+  if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
+    return toy_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
+  return gps_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
+}
+
+// ------------------------------------------------------------------ a6
+ddppo_status ddppo_ppo_loss_grad(ddppo_ctx* ctx, const float* logits, const float* values,
+                                 const ddppo_batch* host_batch, const ddppo_loss_inputs* host_in,
+                                 const float* mean_invstd, const ddppo_loss_cfg* host_cfg, float* dlogits,
+                                 float* dvalues, float* stats, void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, host_batch && host_in && host_cfg && logits && values && dlogits && dvalues && stats,
+                "loss: null pointer");
+  DDPPO_REQUIRE(ctx, host_batch->env_idx && host_batch->len && host_batch->ld >= host_batch->T_run,
+                "loss: bad batch");
+  return launch_loss(ctx, logits, values, *host_batch, *host_in, mean_invstd, *host_cfg, dlogits, dvalues, stats,
+                     as_stream(stream));
+}
+
+// ------------------------------------------------------------------ a8
+ddppo_status ddppo_grad_allreduce_step(ddppo_ctx* ctx, float* grad, float* params, float* m, float* v,
+                                       const uint8_t* freeze_mask, int64_t P, const ddppo_adam_cfg* host_cfg,
+                                       float* grad_norm, void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, grad && params && m && v && host_cfg && P >= 1, "grad_allreduce_step: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  if (ctx->world > 1) {
+    ProfScope ps(ctx, DDPPO_K_ALLREDUCE, st, 0);
+    DDPPO_NCCL_TRY(ctx, ncclAllReduce(grad, grad, (size_t)P, ncclFloat32, ncclSum, ctx->comm, st));
+  }
+  return launch_clip_adam(ctx, grad, params, m, v, freeze_mask, P, *host_cfg, 1.f / (float)ctx->world, grad_norm,
+                          st);
+}
+
+// ------------------------------------------------------------------ a9 / a10
+ddppo_status ddppo_preempt_threshold(const ddppo_preempt_cfg* c, int world, int* host_K, int* host_min_steps) {
+  if (!c || world < 1 || c->T < 1 || c->p_percent < 1 || c->p_percent > 100) return DDPPO_ERR_CONFIG;
+  const int base = c->other_workers ? world - 1 : world;
+  int K = (c->p_percent * base + 99) / 100;
+  if (K < 1) K = 1;
+  if (host_K) *host_K = K;
+  if (host_min_steps) *host_min_steps = c->min_steps > 0 ? c->min_steps : (c->T + 3) / 4;
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_preempt_decide(const ddppo_preempt_cfg* c, int world, int my_steps, int finished_count,
+                                  int* host_should_stop) {
+  int K = 0, ms = 0;
+  ddppo_status s = ddppo_preempt_threshold(c, world, &K, &ms);
+  if (s != DDPPO_OK || !host_should_stop) return DDPPO_ERR_CONFIG;
+  *host_should_stop = (my_steps >= c->T) || (my_steps >= ms && finished_count >= K);
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_preempt_poll(ddppo_ctx* ctx, int my_steps, int finished, int active,
+                                const ddppo_preempt_cfg* host_cfg, int* host_should_stop, int* host_finished_count,
+                                int* host_active_count) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  int32_t h[2] = {finished ? 1 : 0, active ? 1 : 0};
+  if (ctx->world > 1) {
+    DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_i32, h, sizeof(h), cudaMemcpyHostToDevice, 0));
+    DDPPO_NCCL_TRY(ctx, ncclAllReduce(ctx->d_i32, ctx->d_i32, 2, ncclInt32, ncclSum, ctx->comm, 0));
+    DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(h, ctx->d_i32, sizeof(h), cudaMemcpyDeviceToHost, 0));
+    DDPPO_CUDA_TRY(ctx, cudaStreamSynchronize(0));
+  }
+  if (host_finished_count) *host_finished_count = h[0];
+  if (host_active_count) *host_active_count = h[1];
+  int stop = 0;
+  ddppo_status s = ddppo_preempt_decide(host_cfg, ctx->world, my_steps, h[0], &stop);
+  if (s != DDPPO_OK) {
+    ctx->last_error = "preempt: bad cfg";
+    return s;
+  }
+  if (host_should_stop) *host_should_stop = stop;
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, host_vals && n >= 0 && n <= kMaxCountVals, "allreduce_counts: 0 <= n <= 64");
+  if (ctx->world == 1 || n == 0) return DDPPO_OK;
+  DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_i64, host_vals, n * sizeof(int64_t), cudaMemcpyHostToDevice, 0));
+  DDPPO_NCCL_TRY(ctx, ncclAllReduce(ctx->d_i64, ctx->d_i64, n, ncclInt64, ncclSum, ctx->comm, 0));
+  DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(host_vals, ctx->d_i64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, 0));
+  DDPPO_CUDA_TRY(ctx, cudaStreamSynchronize(0));
+  return DDPPO_OK;
+}
+
+// ------------------------------------------------------------------ learner step runtime
+namespace {
+struct LearnerWs {
+  double* stats3;
+  float* mean_invstd;
+  float* logits;
+  float* values;
+  float* dlogits;
+  float* dvalues;
+  float* grad;
+  float* grad_norm;
+  void* model_ws;
+  size_t model_bytes;
+};
+size_t carve_learner(const ddppo_model_desc* d, int E, int T, int mb, void* base, LearnerWs* w) {
+  int64_t P = 0;
+  ddppo_model_param_count(d, &P);
+  const int B = E / mb;
+  size_t model_bytes = 0;
+  ddppo_workspace_size(d, B, T, &model_bytes);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? reinterpret_cast<char*>(base) + off : nullptr;
+    off = align_up(off + bytes, 256);
+    return p;
+  };
+  LearnerWs t;
+  t.stats3 = (double*)take(4 * sizeof(double));
+  t.mean_invstd = (float*)take(4 * sizeof(float));
+  t.logits = (float*)take((size_t)B * T * 4 * sizeof(float));
+  t.values = (float*)take((size_t)B * T * sizeof(float));
+  t.dlogits = (float*)take((size_t)B * T * 4 * sizeof(float));
+  t.dvalues = (float*)take((size_t)B * T * sizeof(float));
+  t.grad = (float*)take((size_t)P * sizeof(float));
+  t.grad_norm = (float*)take(8 * sizeof(float));
+  t.model_ws = take(model_bytes);
+  t.model_bytes = model_bytes;
+  if (w) *w = t;
+  return off;
+}
+}  // namespace
+
+ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int E, int T, int ld, int minibatches,
+                                          int epochs, size_t* host_bytes) {
+  ModelLayout L;
+  if (!host_bytes || build_layout(host_desc, &L) != DDPPO_OK || minibatches < 1 || E % minibatches || T < 1 ||
+      ld < T + 1 || epochs < 1)
+    return DDPPO_ERR_CONFIG;
+  *host_bytes = carve_learner(host_desc, E, T, minibatches, nullptr, nullptr);
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const ddppo_rollout* ro,
+                                const ddppo_learner_cfg* cfg, float* params, float* m, float* v, float* adv,
+                                float* ret, float* stats_out, void* ws, size_t ws_bytes, int32_t* host_step_out,
+                                void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  ModelLayout L;
+  DDPPO_REQUIRE(ctx, build_layout(host_desc, &L) == DDPPO_OK, "bad model descriptor");
+  DDPPO_REQUIRE(ctx, ro && cfg && params && m && v && adv && ret && ws, "learner_step: null pointer");
+  DDPPO_REQUIRE(ctx, ro->host_len && ro->host_perms && ro->perms, "learner_step: lengths/perms required");
+  DDPPO_REQUIRE(ctx, cfg->minibatches >= 1 && ro->E % cfg->minibatches == 0 && cfg->epochs >= 1,
+                "learner_step: minibatches must divide E (S:L155)");
+  size_t need = 0;
+  ddppo_status s =
+      ddppo_learner_workspace_size(host_desc, ro->E, ro->T, ro->ld, cfg->minibatches, cfg->epochs, &need);
+  if (s != DDPPO_OK) return s;
+  DDPPO_REQUIRE(ctx, ws_bytes >= need, "learner_step: workspace too small");
+  LearnerWs w;
+  carve_learner(host_desc, ro->E, ro->T, cfg->minibatches, ws, &w);
+  cudaStream_t st = as_stream(stream);
+
+  // a2 GAE (+ local adv stats), a3 global normalisation statistics
+  s = launch_gae(ctx, ro->rew, ro->val, ro->done, ro->len, ro->E, ro->T, ro->ld, cfg->gamma, cfg->tau, adv, ret,
+                 w.stats3, st);
+  if (s != DDPPO_OK) return s;
+  if (cfg->normalize_adv) {
+    s = ddppo_adv_norm(ctx, w.stats3, cfg->adv_eps, w.mean_invstd, stream);
+    if (s != DDPPO_OK) return s;
+  }
+  const int B = ro->E / cfg->minibatches;
+  int L_max = 0;
+  for (int n = 0; n < ro->E; ++n) L_max = std::max(L_max, std::min(ro->host_len[n], ro->T));
+  DDPPO_REQUIRE(ctx, L_max >= 1, "learner_step: empty rollout");
+  ddppo_loss_inputs li = {ro->action, ro->logp_old, ro->val, ret, adv};
+  ddppo_adam_cfg acfg = cfg->adam;
+  int32_t step = acfg.step;
+  for (int e = 0; e < cfg->epochs; ++e) {
+    for (int j = 0; j < cfg->minibatches; ++j) {
+      ddppo_batch b;
+      b.goal = ro->goal;
+      b.prev_action = ro->prev_action;
+      b.mask = ro->mask;
+      b.h0 = ro->h0;
+      b.len = ro->len;
+      b.env_idx = ro->perms + (size_t)e * ro->E + (size_t)j * B;
+      b.E = ro->E;
+      b.T = ro->T;
+      b.ld = ro->ld;
+      b.B = B;
+      // a4: every rank's envs step in lock-step, so the minibatch runs to its longest env
+      int T_run = 0, n_valid = 0;
+      for (int q = 0; q < B; ++q) {
+        const int n = ro->host_perms[(size_t)e * ro->E + (size_t)j * B + q];
+        const int Ln = std::min(ro->host_len[n], ro->T);
+        T_run = std::max(T_run, Ln);
+        n_valid += Ln;
+      }
+      b.T_run = T_run;
+      b.n_valid = n_valid;
+      if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
+        s = toy_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
+      else
+        s = gps_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
+      if (s != DDPPO_OK) return s;
+      float* st_out = stats_out ? stats_out + (size_t)(e * cfg->minibatches + j) * 8 : w.grad_norm;
+      s = launch_loss(ctx, w.logits, w.values, b, li, cfg->normalize_adv ? w.mean_invstd : nullptr, cfg->loss,
+                      w.dlogits, w.dvalues, st_out, st);
+      if (s != DDPPO_OK) return s;
+      if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
+        s = toy_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
+      else
+        s = gps_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
+      if (s != DDPPO_OK) return s;
+      acfg.step = ++step;
+      s = ddppo_grad_allreduce_step(ctx, w.grad, params, m, v, nullptr, L.P, &acfg, nullptr, stream);
+      if (s != DDPPO_OK) return s;
+    }
+  }
+  if (host_step_out) *host_step_out = step;
+  return DDPPO_OK;
+}
+
+// ------------------------------------------------------------------ measurement
+ddppo_status ddppo_profile_enable(ddppo_ctx* ctx, int enable) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  ctx->prof = enable != 0;
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_profile_read(ddppo_ctx* ctx, double* host_ms, int64_t* host_launches, int reset) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  for (auto& r : ctx->pending) {
+    DDPPO_CUDA_TRY(ctx, cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    DDPPO_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, r.a, r.b));
+    ctx->ms[r.fam] += ms;
+    ctx->pool.push_back(r.a);
+    ctx->pool.push_back(r.b);
+  }
+  ctx->pending.clear();
+  for (int i = 0; i < DDPPO_K_COUNT; ++i) {
+    if (host_ms) host_ms[i] = ctx->ms[i];
+    if (host_launches) host_launches[i] = ctx->launches[i];
+    if (reset) {
+      ctx->ms[i] = 0.0;
+      ctx->launches[i] = 0;
+    }
+  }
+  return DDPPO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,211 @@
+// Shared internals of libddppo.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ddppo.h"
+
+struct ddppo_ctx {
+  int rank = 0, world = 1, device = 0, sm_count = 148;
+  ncclComm_t comm = nullptr;
+  // device scratch
+  int* d_err = nullptr;                // non-finite flag (bitmask of tensor ids)
+  unsigned int* d_counters = nullptr;  // last-block-done counters (one slot per kernel family)
+  double* d_partials = nullptr;        // per-block partial sums (fixed-order reductions)
+  float* d_scalars = nullptr;          // clip coef etc.
+  int32_t* d_i32 = nullptr;            // preemption poll buffer
+  int64_t* d_i64 = nullptr;            // counts buffer
+  std::string last_error;
+  // measurement (ddppo_profile_*)
+  bool prof = false;
+  int64_t launches[DDPPO_K_COUNT] = {};
+  double ms[DDPPO_K_COUNT] = {};
+  struct Rec { int fam; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get_event() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+};
+
+// Counts `n` launches of family `fam`; when profiling is on, brackets the scope with events
+// recorded on the launching stream.
+struct ProfScope {
+  ddppo_ctx* ctx;
+  int fam;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(ddppo_ctx* c, int f, cudaStream_t s, int n) : ctx(c), fam(f), st(s) {
+    ctx->launches[fam] += n;
+    if (ctx->prof) {
+      a = ctx->get_event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (ctx->prof && a) {
+      cudaEvent_t b = ctx->get_event();
+      cudaEventRecord(b, st);
+      ctx->pending.push_back({fam, a, b});
+    }
+  }
+};
+
+enum { CNT_GAE = 0, CNT_LOSS = 1, CNT_NORM = 2, CNT_MISC = 3, CNT_NUM = 8 };
+constexpr int kMaxPartials = 1 << 16;   // doubles
+constexpr int kMaxCountVals = 64;
+
+enum { ERR_BIT_LOSS = 1, ERR_BIT_GRAD = 2 };
+
+#define DDPPO_CUDA_TRY(ctx, expr)                                                 \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      if (ctx) (ctx)->last_error = std::string(#expr ": ") + cudaGetErrorString(_e); \
+      return DDPPO_ERR_CUDA;                                                      \
+    }                                                                             \
+  } while (0)
+
+#define DDPPO_NCCL_TRY(ctx, expr)                                                 \
+  do {                                                                            \
+    ncclResult_t _r = (expr);                                                     \
+    if (_r != ncclSuccess) {                                                      \
+      if (ctx) (ctx)->last_error = std::string(#expr ": ") + ncclGetErrorString(_r); \
+      return DDPPO_ERR_COMM;                                                      \
+    }                                                                             \
+  } while (0)
+
+#define DDPPO_REQUIRE(ctx, cond, msg)                                             \
+  do {                                                                            \
+    if (!(cond)) {                                                                \
+      if (ctx) (ctx)->last_error = std::string("config: ") + (msg);               \
+      return DDPPO_ERR_CONFIG;                                                    \
+    }                                                                             \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction of NV doubles per thread; result valid in thread 0.
+// smem must hold NV * (blockDim/32) doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) smem[warp * NV + i] = v[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += smem[w * NV + i];
+      v[i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// "Last block done" pattern: the block reduces its threads' NV values (fixed order), thread 0
+// writes them to partials[blockIdx*NV+i]; the last block to arrive sums the partials in block
+// order (deterministic) into out[0..NV).  Every thread of every block must call it.  Returns
+// true in the (whole) last block.  counter is reset for reuse.
+template <int NV>
+__device__ __forceinline__ bool last_block_reduce(double (&v)[NV], double* partials, unsigned int* counter,
+                                                  double* out, double* smem) {
+  __shared__ bool am_last;
+  block_sum<NV>(v, smem);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) partials[blockIdx.x * NV + i] = v[i];
+    __threadfence();
+    unsigned int prev = atomicAdd(counter, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return false;
+  __threadfence();
+  // fixed partition: thread t sums blocks t, t+bd, ... in order; then the ordered block_sum
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] += ((volatile double*)partials)[b * NV + i];
+  }
+  block_sum<NV>(acc, smem);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) out[i] = acc[i];
+    *counter = 0u;
+  }
+  return true;
+}
+
+inline int grid_for(int n_items, int per_block, int max_blocks) {
+  long long g = (n_items + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (int)g;
+}
+
+// ---------------------------------------------------------------- internal launchers
+ddppo_status launch_gae(ddppo_ctx* ctx, const float* rew, const float* val, const uint8_t* done,
+                        const int32_t* len, int E, int T, int ld, float gamma, float tau, float* adv,
+                        float* ret, double* stats3, cudaStream_t st);
+ddppo_status launch_adv_finalize(ddppo_ctx* ctx, const double* stats3, float eps, float* mean_invstd,
+                                 cudaStream_t st);
+ddppo_status launch_loss(ddppo_ctx* ctx, const float* logits, const float* values, const ddppo_batch& b,
+                         const ddppo_loss_inputs& in, const float* mean_invstd, const ddppo_loss_cfg& cfg,
+                         float* dlogits, float* dvalues, float* stats, cudaStream_t st);
+ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float* m, float* v,
+                              const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
+                              float* grad_norm, cudaStream_t st);
+
+// models
+struct ModelLayout {
+  int64_t P = 0;
+  int n = 0;
+  ddppo_tensor_info t[16];
+};
+ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out);
+int64_t layout_offset(const ModelLayout& L, const char* name);
+
+size_t toy_workspace(int max_B, int T);
+ddppo_status toy_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
+                     float* logits, float* values, void* ws, cudaStream_t st);
+ddppo_status toy_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
+                     const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st);
+
+size_t gps_workspace(int max_B, int T);
+ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
+                     float* logits, float* values, void* ws, cudaStream_t st);
+ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
+                     const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st);
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

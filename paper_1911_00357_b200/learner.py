@@ -1,0 +1,137 @@
+"""Device-resident buffers around ddppo_learner_step (one DD-PPO worker = one GPU).
+
+Holds the rollout arrays in HBM (env-major [E][ld] rows, include/ddppo.h), the fp32 master
+parameters and Adam moments, and the workspace; `step()` is one call into the C ABI.  The
+preemption driver realises P:L171 with ddppo_preempt_poll (one int32 allreduce per tick).
+"""
+import ctypes
+
+import numpy as np
+import torch
+
+from . import (Rollout, adam_cfg, ddppo_learner_step, ddppo_preempt_poll, learner_workspace_size, learner_cfg,
+               loss_cfg, model_desc, param_count, param_layout, preempt_cfg)
+
+ROLLOUT_FIELDS = {  # name -> torch dtype
+    "rew": torch.float32, "val": torch.float32, "done": torch.uint8, "length": torch.int32,
+    "goal": torch.float32, "prev_action": torch.int32, "mask": torch.float32, "h0": torch.float32,
+    "action": torch.int32, "logp_old": torch.float32,
+}
+
+
+class Learner:
+    def __init__(self, ctx, arch, E, T, epochs=2, minibatches=2, hidden=None, params=None, device="cuda",
+                 normalize_adv=True, use_value_clip=True, lr=2.5e-4, max_grad_norm=0.5, ld=None):
+        self.ctx, self.E, self.T = ctx, E, T
+        self.ld = ld or ((T + 1 + 3) // 4 * 4)
+        self.epochs, self.minibatches = epochs, minibatches
+        self.desc = model_desc(arch, hidden)
+        self.hidden = self.desc.hidden
+        self.P = param_count(self.desc)
+        self.layout = param_layout(self.desc)
+        dev = torch.device(device)
+        self.device = dev
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.params = torch.zeros(self.P, **f32) if params is None else torch.as_tensor(params, **f32).clone()
+        self.m = torch.zeros(self.P, **f32)
+        self.v = torch.zeros(self.P, **f32)
+        self.adam_step = 0
+        self.cfg = learner_cfg(epochs, minibatches, normalize_adv=normalize_adv,
+                               loss=loss_cfg(use_value_clip=use_value_clip, normalize_adv=normalize_adv),
+                               adam=adam_cfg(0, lr=lr, max_grad_norm=max_grad_norm))
+        wsb = learner_workspace_size(self.desc, E, T, self.ld, minibatches, epochs)
+        self.ws = torch.empty(wsb // 4 + 64, **f32)
+        ld = self.ld
+        shapes = {"rew": (E, ld), "val": (E, ld), "done": (E, ld), "length": (E,), "goal": (E, T, 3),
+                  "prev_action": (E, ld), "mask": (E, ld), "h0": (E, self.hidden), "action": (E, ld),
+                  "logp_old": (E, ld)}
+        self.dev = {k: torch.zeros(s, dtype=ROLLOUT_FIELDS[k], device=dev) for k, s in shapes.items()}
+        self.perms = torch.zeros((epochs, E), dtype=torch.int32, device=dev)
+        self.adv = torch.zeros((E, ld), **f32)
+        self.ret = torch.zeros((E, ld), **f32)
+        self.stats = torch.zeros((epochs * minibatches, 8), **f32)
+        self.host_len = np.full(E, T, np.int32)
+        self.host_perms = np.zeros((epochs, E), np.int32)
+        self.shapes = shapes
+
+    # --------------------------------------------------------------- inputs
+    def pinned_host_buffers(self):
+        """Page-locked host mirrors of the rollout arrays (for end-to-end timing)."""
+        return {k: torch.zeros(s, dtype=ROLLOUT_FIELDS[k]).pin_memory() for k, s in self.shapes.items()}
+
+    def load_rollout(self, ro, perms, non_blocking=False):
+        """Copy a rollout (synth dict of numpy arrays or pinned torch tensors) + perms to HBM."""
+        for k in self.dev:
+            src = ro[k]
+            if isinstance(src, np.ndarray):
+                src = torch.from_numpy(np.ascontiguousarray(src))
+            self.dev[k].copy_(src.reshape(self.dev[k].shape), non_blocking=non_blocking)
+        p = perms if isinstance(perms, np.ndarray) else perms.numpy()
+        self.host_perms[:] = p
+        self.perms.copy_(torch.from_numpy(np.ascontiguousarray(self.host_perms)), non_blocking=non_blocking)
+        lens = ro["length"]
+        self.host_len[:] = lens.numpy() if isinstance(lens, torch.Tensor) else lens
+
+    # --------------------------------------------------------------- the learner step
+    def _rollout_struct(self):
+        r = Rollout()
+        d = self.dev
+        r.rew, r.val, r.done, r.len = d["rew"].data_ptr(), d["val"].data_ptr(), d["done"].data_ptr(), \
+            d["length"].data_ptr()
+        r.goal, r.prev_action, r.mask, r.h0 = d["goal"].data_ptr(), d["prev_action"].data_ptr(), \
+            d["mask"].data_ptr(), d["h0"].data_ptr()
+        r.action, r.logp_old, r.perms = d["action"].data_ptr(), d["logp_old"].data_ptr(), self.perms.data_ptr()
+        r.host_len = self.host_len.ctypes.data
+        r.host_perms = self.host_perms.ctypes.data
+        r.E, r.T, r.ld = self.E, self.T, self.ld
+        return r
+
+    def step(self, stream=None):
+        self.cfg.adam.step = self.adam_step
+        self._ro = self._rollout_struct()
+        self.adam_step = ddppo_learner_step(self.ctx, self.desc, self._ro, self.cfg, self.params, self.m, self.v,
+                                            self.adv, self.ret, self.stats, self.ws, stream)
+        return self.stats
+
+    def steps_per_rollout(self):
+        return int(np.minimum(self.host_len, self.T).sum())
+
+
+def preempt_collect(ctx, step_costs, T, p_percent, exchange=None, world=None, on_step=None,
+                    other_workers=False):
+    """Collection phase of one rank under the preemption protocol, in virtual ticks.
+
+    step_costs: this rank's per-step costs in ticks (>= 1).  Every tick an active rank advances
+    its current step; then all ranks exchange {finished, active} -- ddppo_preempt_poll, one int32
+    allreduce standing in for the paper's TCPStore counter -- and a rank that
+    just completed a step applies the threshold decision (computed by the C library).  Ranks
+    that stopped keep polling; everybody leaves on the first tick whose exchange shows no
+    active rank.  `exchange(finished, active) -> (finished_count, active_count)` replaces the
+    NCCL poll in the gloo CPU tests (then `world` must be given).  Returns (L, ticks).
+    """
+    from . import ddppo_preempt_decide
+    cfg = preempt_cfg(p_percent, T, other_workers=other_workers)
+    if world is None:
+        world = ctx.world
+    steps, elapsed, tick, active, finished = 0, 0, 0, True, False
+    while True:
+        tick += 1
+        just = False
+        if active:
+            elapsed += 1
+            if elapsed == int(step_costs[steps]):
+                steps += 1
+                elapsed = 0
+                just = True
+                finished = steps == T
+                if on_step is not None:
+                    on_step(steps)
+        if exchange is None:
+            stop, fin, act = ddppo_preempt_poll(ctx, steps, finished, active, cfg)
+        else:
+            fin, act = exchange(int(finished), int(active))
+            stop = ddppo_preempt_decide(cfg, world, steps, fin)
+        if act == 0:
+            return steps, tick
+        if just and active and stop:
+            active = False

@@ -1,0 +1,346 @@
+"""GPU parity of every step of the hot path against the oracle, through the C ABI (-m gpu).
+
+Tolerances (BASELINE.json north_star):
+  GAE / normalisation  |g-o| <= 1e-5|o| + 1e-5 max|o| (per env row)          (fp32 path)
+  loss / dlogits / Adam |g-o| <= 1e-4|o| + 1e-4 max|o| (per tensor)           (fp32 path)
+  toy network           same 1e-4 form
+  GPS network (fp16/bf16 tensor-core recurrence) per-tensor relative L2 <= 2e-2
+  integers (lengths, counts, preemption) bit-exact
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import advnorm, gae, learner, minibatch, models, optim, ppo
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dd():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_1911_00357_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(dd):
+    c = dd.Context(0, 1, device=0)
+    yield c
+    c.close()
+
+
+def cu(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def close_rel(g, o, rel, name=""):
+    g = np.asarray(g, dtype=np.float64)
+    o = np.asarray(o, dtype=np.float64)
+    scale = np.max(np.abs(o)) if o.size else 0.0
+    bad = np.abs(g - o) > rel * np.abs(o) + rel * scale + 1e-30
+    assert not bad.any(), f"{name}: {bad.sum()} / {bad.size} mismatches, max err {np.max(np.abs(g - o))}, scale {scale}"
+
+
+def rel_l2(g, o):
+    g = np.asarray(g, dtype=np.float64)
+    o = np.asarray(o, dtype=np.float64)
+    return np.linalg.norm(g - o) / max(np.linalg.norm(o), 1e-30)
+
+
+# ------------------------------------------------------------------ a2 GAE + a3 stats
+def _gae_case(dd, ctx, E, T, seed, lengths=None, gamma=0.99, tau=0.95, p_done=0.05, ld=None, done_mode=None):
+    rng = np.random.default_rng(seed)
+    ld = ld or synth.ld_for(T)
+    rew = rng.normal(size=(E, ld)).astype(np.float32)
+    val = rng.normal(size=(E, ld)).astype(np.float32)
+    done = (rng.random((E, ld)) < p_done).astype(np.uint8)
+    if done_mode == "all":
+        done[:] = 1
+    elif done_mode == "none":
+        done[:] = 0
+    length = np.full(E, T, np.int32) if lengths is None else np.asarray(lengths, np.int32)
+    if done_mode == "last":
+        done[:] = 0
+        done[np.arange(E), length - 1] = 1
+    adv = torch.full((E, ld), 7.0, device="cuda")
+    ret = torch.full((E, ld), 7.0, device="cuda")
+    st = torch.zeros(3, dtype=torch.float64, device="cuda")
+    dd.ddppo_gae(ctx, cu(rew), cu(val), cu(done), cu(length), E, T, ld, gamma, tau, adv, ret, st)
+    torch.cuda.synchronize()
+    a_o, r_o = gae.gae(rew, val, done, length, gamma, tau)
+    A = adv.cpu().numpy()[:, :T]
+    R = ret.cpu().numpy()[:, :T]
+    Tm = a_o.shape[1]
+    for n in range(E):
+        close_rel(A[n, :Tm], a_o[n], 1e-5, f"adv row {n}")
+        close_rel(R[n, :Tm], r_o[n], 1e-5, f"ret row {n}")
+        assert np.all(A[n, length[n]:] == 0) and np.all(R[n, length[n]:] == 0)
+    so = gae.adv_stats(a_o, length)
+    s = st.cpu().numpy()
+    assert s[2] == so[2]
+    close_rel(s[:2], so[:2], 1e-5, "stats")
+    return s
+
+
+@pytest.mark.parametrize("E,T", [(2, 4), (4, 128), (16, 128), (37, 200), (5, 7), (3, 1), (300, 64)])
+def test_gae_shapes(dd, ctx, E, T):
+    rng = np.random.default_rng(E * 1000 + T)
+    _gae_case(dd, ctx, E, T, 1)
+    _gae_case(dd, ctx, E, T, 2, lengths=rng.integers(1, T + 1, E))
+
+
+@pytest.mark.parametrize("gamma,tau", [(0.0, 0.95), (1.0, 1.0), (0.99, 0.0), (0.5, 0.5)])
+def test_gae_gamma_tau_edges(dd, ctx, gamma, tau):
+    _gae_case(dd, ctx, 8, 128, 3, gamma=gamma, tau=tau, lengths=[128, 1, 32, 127, 64, 100, 128, 2])
+
+
+@pytest.mark.parametrize("mode", ["all", "none", "last"])
+def test_gae_done_edges(dd, ctx, mode):
+    _gae_case(dd, ctx, 6, 128, 4, lengths=[128, 32, 33, 1, 127, 96], done_mode=mode)
+
+
+def test_gae_odd_ld_scalar_path(dd, ctx):
+    _gae_case(dd, ctx, 9, 128, 5, ld=131, lengths=[128, 5, 64, 1, 100, 128, 77, 31, 32])
+
+
+def test_gae_empty(dd, ctx):
+    st = torch.ones(3, dtype=torch.float64, device="cuda")
+    dummy = torch.zeros(8, device="cuda")
+    dd.ddppo_gae(ctx, dummy, dummy, torch.zeros(8, dtype=torch.uint8, device="cuda"),
+                 torch.zeros(1, dtype=torch.int32, device="cuda"), 0, 4, 8, 0.99, 0.95, dummy, dummy, st)
+    torch.cuda.synchronize()
+    assert st.cpu().tolist() == [0, 0, 0]
+
+
+def test_gae_large_sampled(dd, ctx):
+    """Microbench-sized buffer (2^16 x 128): sampled env rows against the oracle."""
+    E, T = 1 << 16, 128
+    ld = synth.ld_for(T)
+    rng = np.random.default_rng(6)
+    rew = rng.normal(size=(E, ld)).astype(np.float32)
+    val = rng.normal(size=(E, ld)).astype(np.float32)
+    done = (rng.random((E, ld)) < 0.02).astype(np.uint8)
+    length = rng.integers(32, T + 1, E).astype(np.int32)
+    adv = torch.empty((E, ld), device="cuda")
+    ret = torch.empty((E, ld), device="cuda")
+    st = torch.zeros(3, dtype=torch.float64, device="cuda")
+    dd.ddppo_gae(ctx, cu(rew), cu(val), cu(done), cu(length), E, T, ld, 0.99, 0.95, adv, ret, st)
+    torch.cuda.synchronize()
+    idx = rng.choice(E, 64, replace=False)
+    a_o, r_o = gae.gae(rew[idx], val[idx], done[idx], length[idx], 0.99, 0.95)
+    A = adv.cpu().numpy()[idx]
+    for i in range(len(idx)):
+        close_rel(A[i, :a_o.shape[1]][:length[idx[i]]], a_o[i][:length[idx[i]]], 1e-5, "adv")
+    # the global stats: exact count, sums within fp32-rounding of the full oracle
+    a_full, _ = gae.gae(rew, val, done, length, 0.99, 0.95)
+    so = gae.adv_stats(a_full, length)
+    s = st.cpu().numpy()
+    assert s[2] == so[2] == length.sum()
+    close_rel(s[:2], so[:2], 1e-5, "stats")
+
+
+def test_adv_norm(dd, ctx):
+    s = _gae_case(dd, ctx, 16, 128, 7, lengths=np.r_[np.full(8, 128), np.full(8, 40)])
+    st = torch.tensor(s, dtype=torch.float64, device="cuda")
+    mi = torch.zeros(2, device="cuda")
+    dd.ddppo_adv_norm(ctx, st, 1e-5, mi)
+    torch.cuda.synchronize()
+    mu, inv = advnorm.mean_invstd(s, 1e-5)
+    close_rel(mi.cpu().numpy(), [mu, inv], 1e-5, "mean_invstd")
+
+
+# ------------------------------------------------------------------ a6 loss
+def _loss_setup(E, T, B, seed, lengths=None):
+    rng = np.random.default_rng(seed)
+    ro = synth.rollout(E, T, seed, length=lengths, hidden=8)
+    a_o, r_o = gae.gae(ro["rew"], ro["val"], ro["done"], ro["length"], 0.99, 0.95)
+    ld = ro["ld"]
+    adv = np.zeros((E, ld), np.float32)
+    ret = np.zeros((E, ld), np.float32)
+    adv[:, :a_o.shape[1]] = a_o
+    ret[:, :r_o.shape[1]] = r_o
+    env_idx = rng.permutation(E)[:B].astype(np.int32)
+    L = ro["length"][env_idx]
+    T_run = int(L.max())
+    logits = rng.normal(0, 1.0, (B, T_run, 4)).astype(np.float32)
+    values = (ro["val"][env_idx, :T_run] + rng.normal(0, 0.3, (B, T_run))).astype(np.float32)
+    return ro, adv, ret, env_idx, T_run, int(L.sum()), logits, values
+
+
+@pytest.mark.parametrize("E,T,B,vclip,norm", [(4, 128, 2, True, True), (16, 128, 8, False, True),
+                                              (2, 4, 2, True, False), (64, 100, 64, True, True)])
+def test_loss_parity(dd, ctx, E, T, B, vclip, norm):
+    lengths = np.random.default_rng(E).integers(max(1, T // 4), T + 1, E)
+    ro, adv, ret, env_idx, T_run, n_valid, logits, values = _loss_setup(E, T, B, E + T, lengths)
+    mis = (0.3, 1.7) if norm else None
+    batch = dd.make_batch(cu(ro["goal"]), cu(ro["prev_action"]), cu(ro["mask"]), cu(ro["h0"]), cu(ro["length"]),
+                          cu(env_idx), E, T, ro["ld"], B, T_run, n_valid)
+    dl = torch.zeros((B, T_run, 4), device="cuda")
+    dv = torch.zeros((B, T_run), device="cuda")
+    stats = torch.zeros(8, device="cuda")
+    keep = [batch]
+    dd.ddppo_ppo_loss_grad(ctx, cu(logits), cu(values), batch, cu(ro["action"]), cu(ro["logp_old"]), cu(ro["val"]),
+                           cu(ret), cu(adv), cu(np.array(mis, np.float32)) if norm else None,
+                           dd.loss_cfg(use_value_clip=vclip, normalize_adv=norm), dl, dv, stats)
+    torch.cuda.synchronize()
+    ctx.check()
+    valid = (np.arange(T_run)[None] < ro["length"][env_idx][:, None]).reshape(-1)
+    f = lambda a: a[env_idx, :T_run].reshape(-1)  # noqa: E731
+    st, dlo, dvo = ppo.loss_and_grad(logits.reshape(-1, 4), values.reshape(-1), f(ro["action"]), f(ro["logp_old"]),
+                                     f(ro["val"]), f(ret), f(adv), valid, use_value_clip=vclip, mean_invstd=mis)
+    close_rel(dl.cpu().numpy().reshape(-1, 4), dlo, 1e-4, "dlogits")
+    close_rel(dv.cpu().numpy().reshape(-1), dvo, 1e-4, "dvalues")
+    s = stats.cpu().numpy()
+    for i, k in enumerate(ppo.STAT_NAMES):
+        assert abs(s[i] - st[k]) <= 1e-4 * abs(st[k]) + 1e-5, (k, s[i], st[k])
+    assert s[6] == n_valid
+    del keep
+
+
+def test_loss_large_sampled(dd, ctx):
+    """M = 2^20 samples (B = 8192 envs x 128): sampled rows against the oracle."""
+    E, T = 8192, 128
+    ld = synth.ld_for(T)
+    rng = np.random.default_rng(9)
+    M = E * T
+    x = synth.random_loss_inputs(M, 10)
+    env_idx = np.arange(E, dtype=np.int32)
+    length = np.full(E, T, np.int32)
+    rowify = lambda a, dt=np.float32: np.pad(a.reshape(E, T), ((0, 0), (0, ld - T))).astype(dt)  # noqa: E731
+    batch = dd.make_batch(cu(np.zeros((E, T, 3), np.float32)), None, None, None, cu(length), cu(env_idx), E, T, ld, E,
+                          T, M)
+    dl = torch.zeros((M, 4), device="cuda")
+    dv = torch.zeros(M, device="cuda")
+    stats = torch.zeros(8, device="cuda")
+    dd.ddppo_ppo_loss_grad(ctx, cu(x["logits"]), cu(x["values"]), batch, cu(rowify(x["actions"], np.int32)),
+                           cu(rowify(x["logp_old"])), cu(rowify(x["values_old"])), cu(rowify(x["returns"])),
+                           cu(rowify(x["adv"])), None, dd.loss_cfg(normalize_adv=False), dl, dv, stats)
+    torch.cuda.synchronize()
+    st, dlo, dvo = ppo.loss_and_grad(x["logits"], x["values"], x["actions"], x["logp_old"], x["values_old"],
+                                     x["returns"], x["adv"], np.ones(M, bool), use_value_clip=True)
+    idx = rng.choice(M, 4096, replace=False)
+    close_rel(dl.cpu().numpy()[idx], dlo[idx], 1e-4, "dlogits")
+    close_rel(dv.cpu().numpy()[idx], dvo[idx], 1e-4, "dvalues")
+    s = stats.cpu().numpy()
+    for i, k in enumerate(ppo.STAT_NAMES):
+        assert abs(s[i] - st[k]) <= 1e-4 * abs(st[k]) + 1e-5, (k, s[i], st[k])
+
+
+# ------------------------------------------------------------------ a8 clip + Adam (N = 1)
+@pytest.mark.parametrize("P,clip,freeze", [(1001, 0.5, False), (890661, 0.5, True), (7, 0.0, False)])
+def test_clip_adam(dd, ctx, P, clip, freeze):
+    rng = np.random.default_rng(P)
+    p = rng.normal(size=P).astype(np.float32)
+    m = rng.normal(0, 0.01, P).astype(np.float32)
+    v = rng.uniform(0, 1e-3, P).astype(np.float32)
+    fr = (rng.random(P) < 0.3).astype(np.uint8) if freeze else None
+    pg, mg, vg = cu(p), cu(m), cu(v)
+    po, mo, vo = p.astype(np.float64), m.astype(np.float64), v.astype(np.float64)
+    gn = torch.zeros(1, device="cuda")
+    for step in (1, 2, 3):
+        g = (rng.normal(size=P) * (0.3 if step != 2 else 1e-4)).astype(np.float32)
+        dd.ddppo_grad_allreduce_step(ctx, cu(g), pg, mg, vg, dd.adam_cfg(step, max_grad_norm=clip),
+                                     freeze_mask=cu(fr) if freeze else None, grad_norm=gn)
+        po, mo, vo, n_o = optim.adam_step(po, g, mo, vo, step, max_grad_norm=clip if clip > 0 else None,
+                                          freeze=fr.astype(bool) if freeze else None)
+        torch.cuda.synchronize()
+        assert abs(gn.item() - n_o) <= 1e-5 * n_o
+    close_rel(pg.cpu().numpy() - p, po - p, 1e-4, "delta params")
+    close_rel(mg.cpu().numpy(), mo, 1e-5, "m")
+    close_rel(vg.cpu().numpy(), vo, 1e-5, "v")
+    if freeze:
+        f = fr.astype(bool)
+        assert np.array_equal(pg.cpu().numpy()[f], p[f])  # bit-identical
+
+
+# ------------------------------------------------------------------ a5 / a7 networks
+def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
+    desc = dd.model_desc(arch)
+    H = desc.hidden
+    lay = dd.param_layout(desc)
+    P = dd.param_count(desc)
+    params = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, seed)
+    ro = synth.rollout(E, T, seed, length=lengths, hidden=H)
+    rng = np.random.default_rng(seed)
+    env_idx = rng.permutation(E)[:B].astype(np.int32)
+    L = ro["length"][env_idx]
+    T_run = int(L.max())
+    batch = dd.make_batch(cu(ro["goal"]), cu(ro["prev_action"]), cu(ro["mask"]), cu(ro["h0"]), cu(ro["length"]),
+                          cu(env_idx), E, T, ro["ld"], B, T_run, int(L.sum()))
+    ws = torch.zeros(dd.workspace_size(desc, B, T_run) // 4 + 64, device="cuda")
+    lg = torch.zeros((B, T_run, 4), device="cuda")
+    vl = torch.zeros((B, T_run), device="cuda")
+    pg = cu(params)
+    dd.ddppo_policy_fwd(ctx, desc, pg, batch, lg, vl, ws)
+    dl = rng.normal(0, 1e-2, (B, T_run, 4)).astype(np.float32)
+    dv = rng.normal(0, 1e-2, (B, T_run)).astype(np.float32)
+    grad = torch.full((P,), 3.0, device="cuda")
+    dd.ddppo_policy_bwd(ctx, desc, pg, batch, cu(dl), cu(dv), grad, ws)
+    torch.cuda.synchronize()
+    ob = {"goal": ro["goal"][env_idx, :T_run], "prev_action": ro["prev_action"][env_idx, :T_run],
+          "mask": ro["mask"][env_idx, :T_run], "h0": ro["h0"][env_idx]}
+    lo, vo, cache = models.forward(arch, params, ob, hidden=H)
+    go = models.backward(arch, params, cache, dl.astype(np.float64), dv.astype(np.float64), hidden=H)
+    return lay, lg.cpu().numpy(), vl.cpu().numpy(), grad.cpu().numpy(), lo, vo, go
+
+
+def test_toy_network_parity(dd, ctx):
+    lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, "toy", 2, 4, 2, 11)
+    close_rel(lg, lo, 1e-4, "logits")
+    close_rel(vl, vo, 1e-4, "values")
+    for name, off, shape, _ in lay:
+        n = int(np.prod(shape))
+        close_rel(g[off:off + n], go[off:off + n], 1e-4, name)
+
+
+@pytest.mark.parametrize("E,T,B,lengths", [(4, 128, 2, None), (16, 128, 8, None), (4, 128, 2, [128, 40, 77, 32]),
+                                           (3, 37, 3, [37, 1, 20]), (8, 300, 1, None)])
+def test_gps_network_parity(dd, ctx, E, T, B, lengths):
+    lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, "gps", E, T, B, 12 + E + T, lengths)
+    assert rel_l2(lg, lo) < 2e-2 and rel_l2(vl, vo) < 2e-2, (rel_l2(lg, lo), rel_l2(vl, vo))
+    for name, off, shape, _ in lay:
+        n = int(np.prod(shape))
+        e = rel_l2(g[off:off + n], go[off:off + n])
+        assert e < 2e-2, (name, e)
+
+
+# ------------------------------------------------------------------ the whole learner step (a2..a8), N = 1
+@pytest.mark.parametrize("cfgname,lengths", [("toy", None), ("gps", None), ("gps", [128, 96, 128, 32])])
+def test_learner_step_parity(dd, ctx, cfgname, lengths):
+    from paper_1911_00357_b200.learner import Learner
+    c = synth.CONFIGS[cfgname]
+    desc = dd.model_desc(c["arch"])
+    lay = dd.param_layout(desc)
+    P = dd.param_count(desc)
+    p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 21)
+    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+    ro = synth.rollout(c["E"], c["T"], 22, length=lengths, hidden=desc.hidden)
+    pm = synth.perms(22, 0, c["epochs"], c["E"])
+    lrn.load_rollout(ro, pm)
+    stats = lrn.step().cpu().numpy()
+    torch.cuda.synchronize()
+    ctx.check()
+    po, mo, vo, step, info = learner.learner_step(c["arch"], p0, np.zeros(P), np.zeros(P), 0, [ro], [pm],
+                                                  dict(epochs=c["epochs"], minibatches=c["minibatches"]),
+                                                  hidden=desc.hidden)
+    assert lrn.adam_step == step == c["epochs"] * c["minibatches"]
+    A = lrn.adv.cpu().numpy()
+    for n in range(c["E"]):
+        close_rel(A[n, :info["adv"][0].shape[1]], info["adv"][0][n], 1e-5, "adv")
+    tol = 1e-4 if cfgname == "toy" else 2e-2
+    for k, ms in enumerate(info["mb_stats"]):
+        for i, name in enumerate(ppo.STAT_NAMES):
+            ref = ms[name]
+            assert abs(stats[k, i] - ref) <= tol * abs(ref) + tol * 1e-2, (k, name, stats[k, i], ref)
+    dp = lrn.params.cpu().numpy().astype(np.float64) - p0
+    dpo = po - p0
+    for name, off, shape, _ in lay:
+        n = int(np.prod(shape))
+        e = rel_l2(dp[off:off + n], dpo[off:off + n])
+        assert e < (1e-3 if cfgname == "toy" else 5e-2), (name, e)

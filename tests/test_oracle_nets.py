@@ -5,7 +5,6 @@ import torch
 import synth
 from oracle import learner, models, nets, ppo
 
-torch.set_default_dtype(torch.float64)
 
 
 def _t(a):
@@ -15,7 +14,7 @@ def _t(a):
 def test_gru_matches_torch_grucell_with_masks():
     rng = np.random.default_rng(0)
     B, T, I, H = 3, 9, 5, 7
-    cell = torch.nn.GRUCell(I, H)
+    cell = torch.nn.GRUCell(I, H).double()
     W_ih, W_hh = cell.weight_ih.detach().numpy(), cell.weight_hh.detach().numpy()
     b_ih, b_hh = cell.bias_ih.detach().numpy(), cell.bias_hh.detach().numpy()
     x = rng.normal(size=(B, T, I))
@@ -41,7 +40,7 @@ def test_gru_matches_torch_grucell_with_masks():
 def test_lstm_matches_torch_lstmcell_with_masks():
     rng = np.random.default_rng(1)
     B, T, I, H = 2, 8, 4, 6
-    cell = torch.nn.LSTMCell(I, H)
+    cell = torch.nn.LSTMCell(I, H).double()
     W_ih, W_hh = cell.weight_ih.detach().numpy(), cell.weight_hh.detach().numpy()
     b_ih, b_hh = cell.bias_ih.detach().numpy(), cell.bias_hh.detach().numpy()
     x = rng.normal(size=(B, T, I))
