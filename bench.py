@@ -158,8 +158,8 @@ def run_reference(args, rank, world):
     c = synth.CONFIGS[args.config]
     # each "step" is one oracle learner step on a bounded sample of the workload (whole rollouts)
     for _ in range(args.warmup if args.warmup < 2 else 1):
-        oracle_steps_per_sec(args.config, args.seed, budget_s=0.0, max_steps=1)
-    sps, n, el = oracle_steps_per_sec(args.config, args.seed, budget_s=0.0, max_steps=args.steps)
+        oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=1)
+    sps, n, el = oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=args.steps)
     out = {
         "impl": "reference", "metric": "learner experience-steps/sec", "value": sps,
         "unit": "experience-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -13,13 +13,16 @@
 //     sequence in REGISTERS as fp16 (fwd) / bf16 (bwd, transposed) mma.sync A-fragments;
 //   * per step each CTA multiplies its rows by h_{t-1} (m16n8k16, batch in the n dimension),
 //     applies the gate nonlinearity for its own 32 units, and pushes the new h slice into every
-//     CTA's shared memory through DSMEM (st.shared::cluster); one cluster barrier per step;
+//     CTA's shared memory through DSMEM (st.shared::cluster); one split cluster barrier per step
+//     (arrive.release right after the DSMEM stores; the global stores of the saved activations
+//     and the prefetch of the next step's inputs run while the barrier completes);
 //   * the backward pass (BPTT) multiplies by W_hh^T: each CTA forms partial products over its
 //     96 rows for all 512 hidden units and sends each 32-unit slice to its owner CTA, which sums
 //     the 16 partials in fixed order (deterministic).
 // Everything that is NOT on the dependency chain is hoisted out of the recurrence: the input
 // projection W_ih x + b_ih for all steps (prologue of the forward kernel) and the weight
-// gradients dW_hh = dG_h^T H_in, dW_ih = dG_x^T X (plain GEMMs after the backward recurrence).
+// gradients dW_hh = dG_h^T H_in, dW_ih = dG_x^T X, dX = dG_x W_ih (GEMMs after the recurrence),
+// all reductions in fixed order.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -28,7 +31,7 @@
 namespace {
 
 constexpr int kH = 512, kG = 3 * kH, kIn = 64, kNC = 16, kUPC = kH / kNC /*32*/, kRows = 3 * kUPC /*96*/;
-constexpr int kBMax = 8, kA1 = 5;
+constexpr int kBMax = 8, kA1 = 5, kTMax = 1024;
 constexpr int kHStride = kH + 8;     // fp16 row stride of the broadcast h buffer (bank-conflict pad)
 constexpr int kDgStride = kRows + 8; // bf16 row stride of the dG_h buffer
 constexpr int kFwdThreads = 384, kBwdThreads = 512;
@@ -39,9 +42,15 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void cluster_sync_all() {
+__device__ __forceinline__ void cluster_arrive_release() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  cluster_arrive_release();
+  cluster_wait_acquire();
 }
 __device__ __forceinline__ uint32_t map_to_cta(const void* smem_ptr, uint32_t cta) {
   uint32_t a = (uint32_t)__cvta_generic_to_shared(smem_ptr), r;
@@ -50,9 +59,6 @@ __device__ __forceinline__ uint32_t map_to_cta(const void* smem_ptr, uint32_t ct
 }
 __device__ __forceinline__ void st_cluster_u16(uint32_t addr, uint16_t v) {
   asm volatile("st.shared::cluster.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
-}
-__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 __device__ __forceinline__ void st_cluster_v2f32(uint32_t addr, float a, float b) {
   asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
@@ -95,43 +101,90 @@ struct GpsPtrs {
   const int32_t* env_idx;
   int B, T, ld, T_run;
   // workspace (sample s = b*T_run + t)
-  float* X;     // [S][64]
-  float* GI;    // [16][T_run][B][96]   CTA-local input projections (incl. b_ih)
-  float* Hs;    // [S][512]  h_t
-  float* Hin;   // [S][512]  mask_t * h_{t-1}
-  float* Rg;    // [S][512]
-  float* Zg;    // [S][512]
-  float* Ng;    // [S][512]
-  float* GHN;   // [S][512]  W_hn h_in + b_hn
-  float* dH;    // [S][512]  dL/dh_t from the head
-  float* dGI;   // [S][1536]
-  float* dGH;   // [S][1536]
-  float* dX;    // [S][64]
+  float* X;      // [S][64]
+  float* GI;     // [16][T_run][B][96]   CTA-local input projections (incl. b_ih)
+  float* Hs;     // [S][512]  h_t
+  float* Hin;    // [S][512]  mask_t * h_{t-1}
+  float4* RZNG;  // [S][512]  (r, z, n, W_hn h_in + b_hn)
+  float* dH;     // [S][512]  dL/dh_t from the head
+  float* dGI;    // [S][1536]
+  float* dGH;    // [S][1536]
+  float* dX;     // [S][64]
 };
 
+// ------------------------------------------------------------------ mbarrier / st.async helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init_cluster() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// acquire at cluster scope: the data came from peer CTAs (st.async ... complete_tx)
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2f(uint32_t raddr, float a, float b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "f"(a), "f"(b), "r"(rbar)
+               : "memory");
+}
+
 // ------------------------------------------------------------------ forward recurrence
+// Per step t: all warps wait on the local mbarrier of buffer t%2 (filled by the 16 CTAs'
+// st.async packets of h_{t-1}), 12 warps run the W_hh h MMAs, the gate warps (one per batch
+// element) finish the GRU cell for the CTA's 32 units and push the new fp16 slice (4 x 16-byte
+// packets per batch element) to every CTA's next buffer with st.async + complete_tx.  No
+// cluster-wide barrier and no release fence sit on the chain.
 struct FwdSmem {
   __half hbuf[2][kBMax][kHStride];  // broadcast h_in (fp16), double-buffered by step parity
   float ghp[2][kRows][kBMax];       // partial W_hh h products of the two k-halves
   float hown[kBMax][kUPC];          // fp32 state h_in for own units
+  __half stage[kBMax][kUPC];        // own new h slice before it is packed into st.async packets
   float bhh[kRows];
-  float wih[kRows][kIn + 1];        // own W_ih rows (prologue)
-  float xs[32][kIn];                // X chunk (prologue)
+  float bih[kRows];
+  uint64_t bar[2];                  // "buffer t%2 holds h_{t-1}" (tx-count barrier)
 };
 
 __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(smem_raw);
+  float* smask = reinterpret_cast<float*>(smem_raw + sizeof(FwdSmem));  // [B][T_run]
   const int c = (int)cluster_ctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int B = p.B, T_run = p.T_run, S = B * T_run;
+  const int g = lane >> 2, tq = lane & 3;
 
-  // ---- prologue 1: zero the h buffers, stage own rows, compute X slice (samples s % 16 == c)
+  // ---- prologue 1: zero the h buffers, stage own biases and masks, X slice (samples s % 16 == c)
   for (int i = tid; i < 2 * kBMax * kHStride; i += blockDim.x) (&sm.hbuf[0][0][0])[i] = __float2half(0.f);
-  for (int i = tid; i < kRows; i += blockDim.x) sm.bhh[i] = p.bhh[grow_of(c, i)];
-  for (int i = tid; i < kRows * kIn; i += blockDim.x) {
-    const int lr = i / kIn, k = i % kIn;
-    sm.wih[lr][k] = p.Wih[(size_t)grow_of(c, lr) * kIn + k];
+  for (int i = tid; i < kRows; i += blockDim.x) {
+    sm.bhh[i] = p.bhh[grow_of(c, i)];
+    sm.bih[i] = p.bih[grow_of(c, i)];
+  }
+  for (int i = tid; i < S; i += blockDim.x) {
+    const int b = i / T_run, t = i - b * T_run;
+    smask[i] = p.mask[(size_t)p.env_idx[b] * p.ld + t];
+  }
+  if (tid == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    fence_mbar_init_cluster();
   }
   for (int i = tid; i < ((S + kNC - 1 - c) / kNC) * kIn; i += blockDim.x) {
     const int s = c + (i / kIn) * kNC, k = i % kIn;
@@ -139,77 +192,109 @@ __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) 
     const int n = p.env_idx[b];
     float x;
     if (k < 32) {
-      const float* g = p.goal + ((size_t)n * p.T + t) * 3;
-      x = p.Wg[k * 3 + 0] * g[0] + p.Wg[k * 3 + 1] * g[1] + p.Wg[k * 3 + 2] * g[2] + p.bg[k];
+      const float* gg = p.goal + ((size_t)n * p.T + t) * 3;
+      x = p.Wg[k * 3 + 0] * gg[0] + p.Wg[k * 3 + 1] * gg[1] + p.Wg[k * 3 + 2] * gg[2] + p.bg[k];
     } else {
       x = p.Emb[p.prev_action[(size_t)n * p.ld + t] * 32 + (k - 32)];
     }
     p.X[(size_t)s * kIn + k] = x;
   }
+  __syncthreads();
   // initial state h_in_0 = mask_0 * h0 (full vector for the MMA operand, own slice in fp32)
   for (int i = tid; i < B * kH; i += blockDim.x) {
     const int b = i / kH, k = i % kH;
-    const int n = p.env_idx[b];
-    const float h = p.mask[(size_t)n * p.ld] * p.h0[(size_t)n * kH + k];
+    const float h = smask[b * T_run] * p.h0[(size_t)p.env_idx[b] * kH + k];
     sm.hbuf[0][b][k] = __float2half(h);
     if (k >= c * kUPC && k < (c + 1) * kUPC) sm.hown[b][k - c * kUPC] = h;
   }
   // W_hh A-fragments: warp w -> m-tile mt = w/2 (16 local rows), k-half kh = w%2 (16 k-tiles)
   const int mt = warp >> 1, kh = warp & 1;
-  const int g = lane >> 2, tq = lane & 3;
   uint32_t afr[16][4];
-  if (warp < 12) {
+  {
     const int r0 = grow_of(c, mt * 16 + g), r1 = grow_of(c, mt * 16 + g + 8);
-    const float* w0 = p.Whh + (size_t)r0 * kH;
-    const float* w1 = p.Whh + (size_t)r1 * kH;
+    const float2* w0 = reinterpret_cast<const float2*>(p.Whh + (size_t)r0 * kH);
+    const float2* w1 = reinterpret_cast<const float2*>(p.Whh + (size_t)r1 * kH);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int k0 = (kh * 16 + j) * 16 + 2 * tq;
-      afr[j][0] = pack_f16(w0[k0], w0[k0 + 1]);
-      afr[j][1] = pack_f16(w1[k0], w1[k0 + 1]);
-      afr[j][2] = pack_f16(w0[k0 + 8], w0[k0 + 9]);
-      afr[j][3] = pack_f16(w1[k0 + 8], w1[k0 + 9]);
+      const int k2 = ((kh * 16 + j) * 16 + 2 * tq) / 2;
+      const float2 a = w0[k2], b = w1[k2], cc = w0[k2 + 4], d = w1[k2 + 4];
+      afr[j][0] = pack_f16(a.x, a.y);
+      afr[j][1] = pack_f16(b.x, b.y);
+      afr[j][2] = pack_f16(cc.x, cc.y);
+      afr[j][3] = pack_f16(d.x, d.y);
     }
   }
   __threadfence();
-  cluster_sync_all();  // X visible cluster-wide; every CTA's smem initialised before remote writes
+  cluster_sync_all();  // X visible cluster-wide; barriers/buffers initialised before remote writes
 
-  // ---- prologue 2: GI[c][t][b][lr] = W_ih[row] . X[s] + b_ih[row]  (off the dependency chain)
-  for (int s0 = 0; s0 < S; s0 += 32) {
-    const int ns = min(32, S - s0);
-    for (int i = tid; i < ns * kIn; i += blockDim.x) sm.xs[i / kIn][i % kIn] = p.X[(size_t)(s0 + i / kIn) * kIn + i % kIn];
-    __syncthreads();
-    for (int i = tid; i < kRows * ns; i += blockDim.x) {
-      const int lr = i % kRows, si = i / kRows;
-      float acc = p.bih[grow_of(c, lr)];
-#pragma unroll 16
-      for (int k = 0; k < kIn; ++k) acc += sm.wih[lr][k] * sm.xs[si][k];
-      const int s = s0 + si, b = s / T_run, t = s - b * T_run;
-      p.GI[(((size_t)c * T_run + t) * B + b) * kRows + lr] = acc;
+  // ---- prologue 2: GI[c][t][b][lr] = W_ih[row] . X[s] + b_ih[row] with m16n8k16 tiles
+  // (6 m-tiles of own rows x S/8 sample tiles x 4 k-tiles; off the dependency chain)
+  {
+    const int mt2 = warp % 6, half = warp / 6;
+    uint32_t wa[4][4];
+    const float2* w0 = reinterpret_cast<const float2*>(p.Wih + (size_t)grow_of(c, mt2 * 16 + g) * kIn);
+    const float2* w1 = reinterpret_cast<const float2*>(p.Wih + (size_t)grow_of(c, mt2 * 16 + g + 8) * kIn);
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt) {
+      const int k2 = (kt * 16 + 2 * tq) / 2;
+      const float2 a = w0[k2], b = w1[k2], cc = w0[k2 + 4], d = w1[k2 + 4];
+      wa[kt][0] = pack_f16(a.x, a.y);
+      wa[kt][1] = pack_f16(b.x, b.y);
+      wa[kt][2] = pack_f16(cc.x, cc.y);
+      wa[kt][3] = pack_f16(d.x, d.y);
     }
-    __syncthreads();
+    const int n_tiles = (S + 7) / 8;
+    for (int nt = half; nt < n_tiles; nt += 2) {
+      const int sb = nt * 8 + g;  // sample of this lane's B-fragment column
+      const float2* xr = reinterpret_cast<const float2*>(p.X + (size_t)min(sb, S - 1) * kIn);
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kt = 0; kt < 4; ++kt) {
+        float2 x0 = xr[(kt * 16 + 2 * tq) / 2], x1 = xr[(kt * 16 + 8 + 2 * tq) / 2];
+        if (sb >= S) x0 = x1 = make_float2(0.f, 0.f);
+        mma_f16(acc, wa[kt], pack_f16(x0.x, x0.y), pack_f16(x1.x, x1.y));
+      }
+      const int lr0 = mt2 * 16 + g;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int lr = lr0 + (e >> 1) * 8, s = nt * 8 + 2 * tq + (e & 1);
+        if (s < S) {
+          const int b = s / T_run, t = s - b * T_run;
+          p.GI[(((size_t)c * T_run + t) * B + b) * kRows + lr] = acc[e] + sm.bih[lr];
+        }
+      }
+    }
   }
+  __syncthreads();
 
   // ---- recurrence
-  const int gu = tid % kUPC, gb = tid / kUPC;  // gate thread: unit, batch (tid < 32*B)
-  const bool gate_thread = tid < kUPC * B;
-  uint32_t remote_h[kNC];
-  if (gate_thread) {
+  const int gu = lane, gb = warp;  // gate thread: warp b handles batch element b, lane = unit
+  const bool gate_warp = warp < B;
+  // st.async packet of this lane: units [8*(lane%4), +8) of batch gb to CTAs lane/4 and lane/4+8
+  uint32_t pk_addr[2] = {0u, 0u}, pk_bar[2][2] = {{0u, 0u}, {0u, 0u}};
+  float gi_r = 0.f, gi_z = 0.f, gi_n = 0.f;
+  const uint32_t tx_bytes = (uint32_t)(kNC * B * kUPC * sizeof(__half));
+  if (gate_warp) {
 #pragma unroll
-    for (int q = 0; q < kNC; ++q) remote_h[q] = map_to_cta(&sm.hbuf[0][gb][c * kUPC + gu], q);
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t q = (uint32_t)(lane / 4 + 8 * j);
+      pk_addr[j] = map_to_cta(&sm.hbuf[0][gb][c * kUPC + 8 * (lane % 4)], q);
+      pk_bar[j][0] = map_to_cta(&sm.bar[0], q);
+      pk_bar[j][1] = map_to_cta(&sm.bar[1], q);
+    }
+    const float* gi = p.GI + ((size_t)c * T_run * B + gb) * kRows;
+    gi_r = gi[gu];
+    gi_z = gi[kUPC + gu];
+    gi_n = gi[2 * kUPC + gu];
   }
   const uint32_t hbuf_parity_bytes = (uint32_t)sizeof(sm.hbuf[0]);
   for (int t = 0; t < T_run; ++t) {
     const int cur = t & 1;
-    float gi_r = 0.f, gi_z = 0.f, gi_n = 0.f, m_next = 0.f;
-    if (gate_thread) {  // prefetch (independent of the chain)
-      const float* gi = p.GI + (((size_t)c * T_run + t) * B + gb) * kRows;
-      gi_r = gi[gu];
-      gi_z = gi[kUPC + gu];
-      gi_n = gi[2 * kUPC + gu];
-      if (t + 1 < T_run) m_next = p.mask[(size_t)p.env_idx[gb] * p.ld + t + 1];
+    if (t > 0) {
+      if (tid == 0) mbar_arrive_expect_tx(&sm.bar[cur], tx_bytes);
+      mbar_wait_parity(&sm.bar[cur], (uint32_t)(((t - 1) >> 1) & 1));
     }
-    if (warp < 12) {
+    {
       float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
       const uint32_t* hb = reinterpret_cast<const uint32_t*>(&sm.hbuf[cur][g][0]);
 #pragma unroll
@@ -220,13 +305,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) 
       }
       // C layout: c[0],c[1] -> (row g, cols 2tq, 2tq+1); c[2],c[3] -> (row g+8, same cols)
       const int row = mt * 16 + g;
-      sm.ghp[kh][row][2 * tq] = c0[0] + c1[0];
-      sm.ghp[kh][row][2 * tq + 1] = c0[1] + c1[1];
-      sm.ghp[kh][row + 8][2 * tq] = c0[2] + c1[2];
-      sm.ghp[kh][row + 8][2 * tq + 1] = c0[3] + c1[3];
+      *reinterpret_cast<float2*>(&sm.ghp[kh][row][2 * tq]) = make_float2(c0[0] + c1[0], c0[1] + c1[1]);
+      *reinterpret_cast<float2*>(&sm.ghp[kh][row + 8][2 * tq]) = make_float2(c0[2] + c1[2], c0[3] + c1[3]);
     }
     __syncthreads();
-    if (gate_thread) {
+    if (gate_warp) {
       const int lr_r = gu, lr_z = kUPC + gu, lr_n = 2 * kUPC + gu;
       const float gh_r = sm.ghp[0][lr_r][gb] + sm.ghp[1][lr_r][gb] + sm.bhh[lr_r];
       const float gh_z = sm.ghp[0][lr_z][gb] + sm.ghp[1][lr_z][gb] + sm.bhh[lr_z];
@@ -236,41 +319,61 @@ __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) 
       const float z = sigmoidf_(gi_z + gh_z);
       const float nn = tanhf(gi_n + r * gh_n);
       const float h = (1.f - z) * nn + z * h_in;
+      if (t + 1 < T_run) {
+        const float hn = smask[gb * T_run + t + 1] * h;
+        sm.hown[gb][gu] = hn;
+        sm.stage[gb][gu] = __float2half(hn);
+        __syncwarp();
+        const uint4 pkt = *reinterpret_cast<const uint4*>(&sm.stage[gb][8 * (lane % 4)]);
+        const uint32_t off = (cur ^ 1) * hbuf_parity_bytes;
+        st_async_v4(pk_addr[0] + off, pkt, pk_bar[0][cur ^ 1]);
+        st_async_v4(pk_addr[1] + off, pkt, pk_bar[1][cur ^ 1]);
+      }
+      // off the chain: save activations, prefetch the next step's input projections
       const size_t o = ((size_t)gb * T_run + t) * kH + c * kUPC + gu;
       p.Hs[o] = h;
       p.Hin[o] = h_in;
-      p.Rg[o] = r;
-      p.Zg[o] = z;
-      p.Ng[o] = nn;
-      p.GHN[o] = gh_n;
-      const float hn = m_next * h;
-      sm.hown[gb][gu] = hn;
+      p.RZNG[o] = make_float4(r, z, nn, gh_n);
       if (t + 1 < T_run) {
-        const uint16_t bits = __half_as_ushort(__float2half(hn));
-        const uint32_t off = (cur ^ 1) * hbuf_parity_bytes;
-#pragma unroll
-        for (int q = 0; q < kNC; ++q) st_cluster_u16(remote_h[q] + off, bits);
+        const float* gi = p.GI + (((size_t)c * T_run + t + 1) * B + gb) * kRows;
+        gi_r = gi[gu];
+        gi_z = gi[kUPC + gu];
+        gi_n = gi[2 * kUPC + gu];
       }
     }
-    cluster_sync_all();
   }
+  cluster_sync_all();  // no CTA exits while a peer could still address its shared memory
 }
 
 // ------------------------------------------------------------------ backward recurrence (BPTT)
+// Iteration i (t = T_run-1-i): gate warps form dG for the CTA's units (local), 16 warps multiply
+// by W_hh^T (bf16 m16n8k16) and st.async their 32-unit x B partials to the owning CTA's
+// recv[i%2] (complete_tx on its mbarrier); the owner sums the 16 partials in CTA order.
 struct BwdSmem {
   __nv_bfloat16 dg[kBMax][kDgStride];    // dG_h of own 96 rows (bf16 MMA operand)
-  float recv[2][kNC][kUPC][kBMax];        // partial W_hh^T dG_h from every CTA, by step parity
+  float recv[2][kNC][kUPC][kBMax];        // partial W_hh^T dG_h from every CTA, by iteration parity
+  uint64_t bar[2];
 };
 
 __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
+  float* smask = reinterpret_cast<float*>(smem_raw + sizeof(BwdSmem));  // [B][T_run]
   const int c = (int)cluster_ctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int B = p.B, T_run = p.T_run;
+  const int B = p.B, T_run = p.T_run, S = B * T_run;
   const int g = lane >> 2, tq = lane & 3;
 
   for (int i = tid; i < kBMax * kDgStride; i += blockDim.x) (&sm.dg[0][0])[i] = __float2bfloat16(0.f);
+  for (int i = tid; i < S; i += blockDim.x) {
+    const int b = i / T_run, t = i - b * T_run;
+    smask[i] = p.mask[(size_t)p.env_idx[b] * p.ld + t];
+  }
+  if (tid == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    fence_mbar_init_cluster();
+  }
   // A-fragments of W_hh^T: warp w -> hidden units j in [32w, 32w+32) (2 m-tiles), k = own 96 rows
   uint32_t afr[2][6][4];
 #pragma unroll
@@ -291,38 +394,54 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
   }
   // destination of this warp's partials: CTA `warp` (owner of units [32*warp, 32*warp+32))
   const uint32_t recv_remote = map_to_cta(&sm.recv[0][c][0][0], (uint32_t)warp);
+  const uint32_t rbar[2] = {map_to_cta(&sm.bar[0], (uint32_t)warp), map_to_cta(&sm.bar[1], (uint32_t)warp)};
   const uint32_t recv_parity_bytes = (uint32_t)sizeof(sm.recv[0]);
+  const int cols = 2 * ((B + 1) / 2);  // columns each source sends (lanes with 2*tq < B, pairs)
+  const uint32_t tx_bytes = (uint32_t)(kNC * kUPC * cols * sizeof(float));
   __syncthreads();
   cluster_sync_all();
 
-  const int gu = tid % kUPC, gb = tid / kUPC;
-  const bool gate_thread = tid < kUPC * B;
-  float carry = 0.f;  // dL/dh_{t} flowing back from step t+1 (already multiplied by mask_{t+1})
-  for (int t = T_run - 1; t >= 0; --t) {
-    const int par = t & 1;
+  const int gu = lane, gb = warp;
+  const bool gate_warp = warp < B;
+  float carry = 0.f;  // dL/dh_t flowing back from step t+1 (already multiplied by mask_{t+1})
+  float dH_t = 0.f, h_in = 0.f;
+  float4 rzng = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (gate_warp) {
+    const size_t o = ((size_t)gb * T_run + T_run - 1) * kH + c * kUPC + gu;
+    dH_t = p.dH[o];
+    rzng = p.RZNG[o];
+    h_in = p.Hin[o];
+  }
+  for (int it = 0; it < T_run; ++it) {
+    const int t = T_run - 1 - it, par = it & 1;
     float dzh = 0.f;
-    if (gate_thread) {
-      const size_t o = ((size_t)gb * T_run + t) * kH + c * kUPC + gu;
-      const float dh = p.dH[o] + carry;
-      const float r = p.Rg[o], z = p.Zg[o], nn = p.Ng[o], ghn = p.GHN[o], h_in = p.Hin[o];
+    if (gate_warp) {
+      const float dh = dH_t + carry;
+      const float r = rzng.x, z = rzng.y, nn = rzng.z, ghn = rzng.w;
       const float dn = dh * (1.f - z);
       const float dz = dh * (h_in - nn);
       const float dn_pre = dn * (1.f - nn * nn);
       const float dr = dn_pre * ghn;
       const float dr_pre = dr * r * (1.f - r);
       const float dz_pre = dz * z * (1.f - z);
+      sm.dg[gb][gu] = __float2bfloat16(dr_pre);
+      sm.dg[gb][kUPC + gu] = __float2bfloat16(dz_pre);
+      sm.dg[gb][2 * kUPC + gu] = __float2bfloat16(dn_pre * r);
+      dzh = dh * z;
+      // off the chain (issued early, consumed never on this path): save dG, prefetch step t-1
       const size_t og = ((size_t)gb * T_run + t) * kG + c * kUPC + gu;
       p.dGI[og] = dr_pre;
       p.dGI[og + kH] = dz_pre;
       p.dGI[og + 2 * kH] = dn_pre;
-      const float dgn = dn_pre * r;
       p.dGH[og] = dr_pre;
       p.dGH[og + kH] = dz_pre;
-      p.dGH[og + 2 * kH] = dgn;
-      sm.dg[gb][gu] = __float2bfloat16(dr_pre);
-      sm.dg[gb][kUPC + gu] = __float2bfloat16(dz_pre);
-      sm.dg[gb][2 * kUPC + gu] = __float2bfloat16(dgn);
-      dzh = dh * z;
+      p.dGH[og + 2 * kH] = dn_pre * r;
+      if (t > 0) {
+        const size_t o = ((size_t)gb * T_run + t - 1) * kH + c * kUPC + gu;
+        dH_t = p.dH[o];
+        rzng = p.RZNG[o];
+        h_in = p.Hin[o];
+      }
     }
     __syncthreads();
     {
@@ -337,22 +456,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
       // rows (unit within the owner's slice): g, g+8 (m-tile 0), 16+g, 24+g (m-tile 1); cols 2tq, 2tq+1
       if (2 * tq < B) {
         const uint32_t base = recv_remote + par * recv_parity_bytes;
-        st_cluster_v2f32(base + (uint32_t)(((g) * kBMax + 2 * tq) * 4), c0[0], c0[1]);
-        st_cluster_v2f32(base + (uint32_t)(((g + 8) * kBMax + 2 * tq) * 4), c0[2], c0[3]);
-        st_cluster_v2f32(base + (uint32_t)(((16 + g) * kBMax + 2 * tq) * 4), c1[0], c1[1]);
-        st_cluster_v2f32(base + (uint32_t)(((24 + g) * kBMax + 2 * tq) * 4), c1[2], c1[3]);
+        st_async_v2f(base + (uint32_t)(((g) * kBMax + 2 * tq) * 4), c0[0], c0[1], rbar[par]);
+        st_async_v2f(base + (uint32_t)(((g + 8) * kBMax + 2 * tq) * 4), c0[2], c0[3], rbar[par]);
+        st_async_v2f(base + (uint32_t)(((16 + g) * kBMax + 2 * tq) * 4), c1[0], c1[1], rbar[par]);
+        st_async_v2f(base + (uint32_t)(((24 + g) * kBMax + 2 * tq) * 4), c1[2], c1[3], rbar[par]);
       }
     }
-    cluster_sync_all();
-    if (gate_thread) {
+    if (gate_warp) {
+      if (tid == 0) mbar_arrive_expect_tx(&sm.bar[par], tx_bytes);
+      mbar_wait_parity(&sm.bar[par], (uint32_t)((it >> 1) & 1));
       float s = 0.f;
 #pragma unroll
       for (int q = 0; q < kNC; ++q) s += sm.recv[par][q][gu][gb];
-      const float m_t = p.mask[(size_t)p.env_idx[gb] * p.ld + t];
-      carry = m_t * (dzh + s);
+      carry = smask[gb * T_run + t] * (dzh + s);
     }
+    __syncthreads();  // every warp's MMA has read dg before the gate warps overwrite it
   }
-  cluster_sync_all();  // nobody exits while a peer may still write into its shared memory
+  cluster_sync_all();  // no CTA exits while a peer could still address its shared memory
 }
 
 // ------------------------------------------------------------------ head (Linear(512, 5)) fwd/bwd
@@ -370,10 +490,8 @@ __global__ void head_fwd_kernel(const float* __restrict__ Wo, const float* __res
 #pragma unroll
     for (int o = 0; o < kA1; ++o) acc[o] = warp_sum(acc[o]);
     if (lane == 0) {
-      logits[(size_t)s * 4 + 0] = acc[0] + bo[0];
-      logits[(size_t)s * 4 + 1] = acc[1] + bo[1];
-      logits[(size_t)s * 4 + 2] = acc[2] + bo[2];
-      logits[(size_t)s * 4 + 3] = acc[3] + bo[3];
+      *reinterpret_cast<float4*>(logits + (size_t)s * 4) =
+          make_float4(acc[0] + bo[0], acc[1] + bo[1], acc[2] + bo[2], acc[3] + bo[3]);
       values[s] = acc[4] + bo[4];
     }
   }
@@ -385,40 +503,86 @@ __global__ void head_dgrad_kernel(const float* __restrict__ Wo, const float* __r
   const size_t n = (size_t)S * kH;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int s = (int)(i / kH), k = (int)(i % kH);
-    const float* dl = dlogits + (size_t)s * 4;
-    dH[i] = Wo[k] * dl[0] + Wo[kH + k] * dl[1] + Wo[2 * kH + k] * dl[2] + Wo[3 * kH + k] * dl[3] +
+    const float4 dl = *reinterpret_cast<const float4*>(dlogits + (size_t)s * 4);
+    dH[i] = Wo[k] * dl.x + Wo[kH + k] * dl.y + Wo[2 * kH + k] * dl.z + Wo[3 * kH + k] * dl.w +
             Wo[4 * kH + k] * dvalues[s];
   }
 }
 
-// dWo[o][k] = sum_s dout[s][o] Hs[s][k];  dbo[o] = sum_s dout[s][o]   (fixed order over s)
-__global__ void head_wgrad_kernel(const float* __restrict__ Hs, const float* __restrict__ dlogits,
-                                  const float* __restrict__ dvalues, int S, float* __restrict__ dWo,
-                                  float* __restrict__ dbo) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < kH) {
-    float a[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int s = 0; s < S; ++s) {
-      const float h = Hs[(size_t)s * kH + k];
-      const float* dl = dlogits + (size_t)s * 4;
-      a[0] += dl[0] * h;
-      a[1] += dl[1] * h;
-      a[2] += dl[2] * h;
-      a[3] += dl[3] * h;
-      a[4] += dvalues[s] * h;
-    }
+// Fixed-order column reductions: 32 columns per CTA x 8 sample chunks (one warp each), chunk
+// partials summed in chunk order.   out[m] = sum_s A[s][m]  (and, for the head, weighted sums).
+constexpr int kRedChunks = 8;
+__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ A, int lda, int S, int M,
+                                                     float* __restrict__ out) {
+  __shared__ float part[kRedChunks][32];
+  const int m = blockIdx.x * 32 + (threadIdx.x & 31), q = threadIdx.x >> 5;
+  const int per = (S + kRedChunks - 1) / kRedChunks;
+  float a = 0.f;
+  if (m < M)
+    for (int s = q * per; s < min(S, (q + 1) * per); ++s) a += A[(size_t)s * lda + m];
+  part[q][threadIdx.x & 31] = a;
+  __syncthreads();
+  if (threadIdx.x < 32 && m < M) {
+    float t = 0.f;
 #pragma unroll
-    for (int o = 0; o < kA1; ++o) dWo[o * kH + k] = a[o];
-  } else if (k < kH + kA1) {
-    const int o = k - kH;
-    float a = 0.f;
-    for (int s = 0; s < S; ++s) a += o < 4 ? dlogits[(size_t)s * 4 + o] : dvalues[s];
-    dbo[o] = a;
+    for (int i = 0; i < kRedChunks; ++i) t += part[i][threadIdx.x];
+    out[m] = t;
+  }
+}
+
+// dWo[o][k] = sum_s dout[s][o] Hs[s][k] (32 k per CTA x 8 sample chunks); CTA 0 also does dbo.
+__global__ void __launch_bounds__(256) head_wgrad_kernel(const float* __restrict__ Hs,
+                                                         const float* __restrict__ dlogits,
+                                                         const float* __restrict__ dvalues, int S,
+                                                         float* __restrict__ dWo, float* __restrict__ dbo) {
+  __shared__ float part[kRedChunks][kA1][33];
+  const int kk = threadIdx.x & 31, q = threadIdx.x >> 5, k = blockIdx.x * 32 + kk;
+  const int per = (S + kRedChunks - 1) / kRedChunks;
+  float a[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f}, bsum[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int s = q * per; s < min(S, (q + 1) * per); ++s) {
+    const float h = Hs[(size_t)s * kH + k];
+    const float4 dl = *reinterpret_cast<const float4*>(dlogits + (size_t)s * 4);
+    const float dv = dvalues[s];
+    a[0] += dl.x * h;
+    a[1] += dl.y * h;
+    a[2] += dl.z * h;
+    a[3] += dl.w * h;
+    a[4] += dv * h;
+    bsum[0] += dl.x;
+    bsum[1] += dl.y;
+    bsum[2] += dl.z;
+    bsum[3] += dl.w;
+    bsum[4] += dv;
+  }
+#pragma unroll
+  for (int o = 0; o < kA1; ++o) part[q][o][kk] = a[o];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int o = 0; o < kA1; ++o) {
+      float t = 0.f;
+#pragma unroll
+      for (int i = 0; i < kRedChunks; ++i) t += part[i][o][kk];
+      dWo[o * kH + k] = t;
+    }
+  }
+  if (blockIdx.x == 0) {  // biases: chunk partials (identical for every kk) in chunk order
+    __syncthreads();
+    if (kk == 0) {
+#pragma unroll
+      for (int o = 0; o < kA1; ++o) part[q][o][32] = bsum[o];
+    }
+    __syncthreads();
+    if (threadIdx.x < kA1) {
+      float t = 0.f;
+      for (int i = 0; i < kRedChunks; ++i) t += part[i][threadIdx.x][32];
+      dbo[threadIdx.x] = t;
+    }
   }
 }
 
 // ------------------------------------------------------------------ weight-gradient GEMMs
-// C[M][N] = sum_s A[s][a_off + m] * Bm[s][n]  (A row stride lda, Bm row stride ldb), fixed s order.
+// C[M][N] = sum_s A[s][m] * Bm[s][n]  (A row stride lda, Bm row stride ldb), fixed s order.
 // 64x64 tile per CTA, 256 threads, 4x4 outputs per thread, s in chunks of 16 through smem.
 __global__ void __launch_bounds__(256) gemm_atb_kernel(const float* __restrict__ A, int lda,
                                                        const float* __restrict__ Bm, int ldb, int S, int M, int N,
@@ -459,69 +623,80 @@ __global__ void __launch_bounds__(256) gemm_atb_kernel(const float* __restrict__
     }
 }
 
-// column sums: out[m] = sum_s A[s][m]
-__global__ void colsum_kernel(const float* __restrict__ A, int lda, int S, int M, float* __restrict__ out) {
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= M) return;
-  float a = 0.f;
-  for (int s = 0; s < S; ++s) a += A[(size_t)s * lda + m];
-  out[m] = a;
-}
-
-// dX[s][k] = sum_row dGI[s][row] * Wih[row][k]   (one warp per sample; lanes over k pairs)
-__global__ void dx_kernel(const float* __restrict__ dGI, const float* __restrict__ Wih, int S, float* __restrict__ dX) {
-  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
-  for (int s = blockIdx.x * warps + (threadIdx.x >> 5); s < S; s += gridDim.x * warps) {
-    const float* d = dGI + (size_t)s * kG;
-    float a0 = 0.f, a1 = 0.f;
-    for (int row = 0; row < kG; ++row) {
-      const float dv = d[row];
-      a0 += dv * Wih[(size_t)row * kIn + lane];
-      a1 += dv * Wih[(size_t)row * kIn + 32 + lane];
+// dX[s][j] = sum_row dGI[s][row] * Wih[row][j]: CTA per 8 samples, thread (j, sample pair),
+// rows streamed in chunks of 128 through shared memory.
+__global__ void __launch_bounds__(256) dx_kernel(const float* __restrict__ dGI, const float* __restrict__ Wih, int S,
+                                                 float* __restrict__ dX) {
+  __shared__ float dg[8][128];
+  const int j = threadIdx.x & 63, q = threadIdx.x >> 6, s0 = blockIdx.x * 8;
+  float a0 = 0.f, a1 = 0.f;
+  for (int r0 = 0; r0 < kG; r0 += 128) {
+    for (int i = threadIdx.x; i < 8 * 128; i += 256) {
+      const int ss = i >> 7, rr = i & 127;
+      dg[ss][rr] = (s0 + ss < S) ? dGI[(size_t)(s0 + ss) * kG + r0 + rr] : 0.f;
     }
-    dX[(size_t)s * kIn + lane] = a0;
-    dX[(size_t)s * kIn + 32 + lane] = a1;
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 128; ++rr) {
+      const float w = Wih[(size_t)(r0 + rr) * kIn + j];
+      a0 += dg[q][rr] * w;
+      a1 += dg[q + 4][rr] * w;
+    }
+    __syncthreads();
   }
+  if (s0 + q < S) dX[(size_t)(s0 + q) * kIn + j] = a0;
+  if (s0 + q + 4 < S) dX[(size_t)(s0 + q + 4) * kIn + j] = a1;
 }
 
-// goal FC and embedding gradients from dX (fixed order over samples)
-__global__ void input_grads_kernel(const float* __restrict__ dX, const float* __restrict__ goal,
-                                   const int32_t* __restrict__ prev_action, const int32_t* __restrict__ env_idx,
-                                   int T, int ld, int T_run, int S, float* __restrict__ dWg, float* __restrict__ dbg,
-                                   float* __restrict__ dEmb) {
-  const int j = threadIdx.x;  // 0..31 goal units, 32..63 embedding dims
-  if (j < 32) {
-    float w0 = 0.f, w1 = 0.f, w2 = 0.f, bb = 0.f;
-    for (int s = 0; s < S; ++s) {
-      const int b = s / T_run, t = s - b * T_run;
-      const float* g = goal + ((size_t)env_idx[b] * T + t) * 3;
-      const float d = dX[(size_t)s * kIn + j];
-      w0 += d * g[0];
-      w1 += d * g[1];
-      w2 += d * g[2];
-      bb += d;
-    }
-    dWg[j * 3 + 0] = w0;
-    dWg[j * 3 + 1] = w1;
-    dWg[j * 3 + 2] = w2;
-    dbg[j] = bb;
-  } else if (j < 64) {
-    float e[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int s = 0; s < S; ++s) {
-      const int b = s / T_run, t = s - b * T_run;
-      const int a = prev_action[(size_t)env_idx[b] * ld + t];
-      const float d = dX[(size_t)s * kIn + j];
+// goal-FC and embedding gradients from dX: thread (j, chunk q of 4), chunk partials summed in order
+__global__ void __launch_bounds__(256) input_grads_kernel(const float* __restrict__ dX, const float* __restrict__ goal,
+                                                          const int32_t* __restrict__ prev_action,
+                                                          const int32_t* __restrict__ env_idx, int T, int ld,
+                                                          int T_run, int S, float* __restrict__ dWg,
+                                                          float* __restrict__ dbg, float* __restrict__ dEmb) {
+  __shared__ float part[4][64][5];
+  const int j = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const int per = (S + 3) / 4;
+  float a[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int s = q * per; s < min(S, (q + 1) * per); ++s) {
+    const int b = s / T_run, t = s - b * T_run;
+    const int n = env_idx[b];
+    const float d = dX[(size_t)s * kIn + j];
+    if (j < 32) {
+      const float* gg = goal + ((size_t)n * T + t) * 3;
+      a[0] += d * gg[0];
+      a[1] += d * gg[1];
+      a[2] += d * gg[2];
+      a[3] += d;
+    } else {
+      const int act = prev_action[(size_t)n * ld + t];
 #pragma unroll
-      for (int q = 0; q < kA1; ++q) e[q] += (a == q) ? d : 0.f;
+      for (int o = 0; o < kA1; ++o) a[o] += (act == o) ? d : 0.f;
     }
+  }
 #pragma unroll
-    for (int q = 0; q < kA1; ++q) dEmb[q * 32 + (j - 32)] = e[q];
+  for (int o = 0; o < 5; ++o) part[q][j][o] = a[o];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    float t[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int o = 0; o < 5; ++o) t[o] += part[i][j][o];
+    if (j < 32) {
+      dWg[j * 3 + 0] = t[0];
+      dWg[j * 3 + 1] = t[1];
+      dWg[j * 3 + 2] = t[2];
+      dbg[j] = t[3];
+    } else {
+#pragma unroll
+      for (int o = 0; o < kA1; ++o) dEmb[o * 32 + (j - 32)] = t[o];
+    }
   }
 }
 
 // ------------------------------------------------------------------ workspace carving
 struct GpsWs {
-  float *X, *GI, *Hs, *Hin, *Rg, *Zg, *Ng, *GHN, *dH, *dGI, *dGH, *dX;
+  float *X, *GI, *Hs, *Hin, *RZNG, *dH, *dGI, *dGH, *dX;
 };
 size_t carve(void* base, int B, int T, GpsWs* w) {
   size_t off = 0;
@@ -536,10 +711,7 @@ size_t carve(void* base, int B, int T, GpsWs* w) {
   tmp.GI = take(S * kG);
   tmp.Hs = take(S * kH);
   tmp.Hin = take(S * kH);
-  tmp.Rg = take(S * kH);
-  tmp.Zg = take(S * kH);
-  tmp.Ng = take(S * kH);
-  tmp.GHN = take(S * kH);
+  tmp.RZNG = take(S * kH * 4);
   tmp.dH = take(S * kH);
   tmp.dGI = take(S * kG);
   tmp.dGH = take(S * kG);
@@ -574,10 +746,7 @@ GpsPtrs make_ptrs(const ModelLayout& L, const float* params, const ddppo_batch& 
   p.GI = w.GI;
   p.Hs = w.Hs;
   p.Hin = w.Hin;
-  p.Rg = w.Rg;
-  p.Zg = w.Zg;
-  p.Ng = w.Ng;
-  p.GHN = w.GHN;
+  p.RZNG = reinterpret_cast<float4*>(w.RZNG);
   p.dH = w.dH;
   p.dGI = w.dGI;
   p.dGH = w.dGH;
@@ -611,14 +780,15 @@ size_t gps_workspace(int max_B, int T) { return carve(nullptr, max_B, T, nullptr
 
 ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                      float* logits, float* values, void* ws, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax, "gps: minibatch must hold 1..8 envs");
+  DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");
   GpsPtrs p = make_ptrs(L, params, b, ws);
+  const int S = b.B * b.T_run;
   {
     ProfScope ps(ctx, DDPPO_K_NET_FWD, st, 1);
-    ddppo_status s = launch_cluster(ctx, gps_gru_fwd_kernel, kFwdThreads, sizeof(FwdSmem), p, st);
+    ddppo_status s =
+        launch_cluster(ctx, gps_gru_fwd_kernel, kFwdThreads, sizeof(FwdSmem) + (size_t)S * sizeof(float), p, st);
     if (s != DDPPO_OK) return s;
   }
-  const int S = b.B * b.T_run;
   ProfScope ps(ctx, DDPPO_K_HEAD, st, 1);
   head_fwd_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, p.bo, p.Hs, S, logits, values);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -627,20 +797,20 @@ ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
 
 ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                      const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax, "gps: minibatch must hold 1..8 envs");
+  DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");
   GpsPtrs p = make_ptrs(L, params, b, ws);
   const int S = b.B * b.T_run;
   {
-  ProfScope ps(ctx, DDPPO_K_HEAD, st, 2);
-  head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, dlogits, dvalues, S, p.dH);
-  head_wgrad_kernel<<<(kH + kA1 + 127) / 128, 128, 0, st>>>(p.Hs, dlogits, dvalues, S,
-                                                            grad + layout_offset(L, "head.weight"),
-                                                            grad + layout_offset(L, "head.bias"));
-  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+    ProfScope ps(ctx, DDPPO_K_HEAD, st, 2);
+    head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, dlogits, dvalues, S, p.dH);
+    head_wgrad_kernel<<<kH / 32, 256, 0, st>>>(p.Hs, dlogits, dvalues, S, grad + layout_offset(L, "head.weight"),
+                                              grad + layout_offset(L, "head.bias"));
+    DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   }
   {
     ProfScope ps(ctx, DDPPO_K_NET_BWD, st, 1);
-    ddppo_status s = launch_cluster(ctx, gps_gru_bwd_kernel, kBwdThreads, sizeof(BwdSmem), p, st);
+    ddppo_status s =
+        launch_cluster(ctx, gps_gru_bwd_kernel, kBwdThreads, sizeof(BwdSmem) + (size_t)S * sizeof(float), p, st);
     if (s != DDPPO_OK) return s;
   }
   // weight gradients (off the dependency chain)
@@ -649,13 +819,13 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
                                                          grad + layout_offset(L, "rnn.weight_hh"), kH);
   gemm_atb_kernel<<<dim3(1, kG / 64), 256, 0, st>>>(p.dGI, kG, p.X, kIn, S, kG, kIn,
                                                    grad + layout_offset(L, "rnn.weight_ih"), kIn);
-  colsum_kernel<<<kG / 128, 128, 0, st>>>(p.dGH, kG, S, kG, grad + layout_offset(L, "rnn.bias_hh"));
-  colsum_kernel<<<kG / 128, 128, 0, st>>>(p.dGI, kG, S, kG, grad + layout_offset(L, "rnn.bias_ih"));
-  dx_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(p.dGI, p.Wih, S, p.dX);
-  input_grads_kernel<<<1, 64, 0, st>>>(p.dX, b.goal, b.prev_action, b.env_idx, b.T, b.ld, b.T_run, S,
-                                       grad + layout_offset(L, "goal_fc.weight"),
-                                       grad + layout_offset(L, "goal_fc.bias"),
-                                       grad + layout_offset(L, "act_embed.weight"));
+  colsum_kernel<<<kG / 32, 256, 0, st>>>(p.dGH, kG, S, kG, grad + layout_offset(L, "rnn.bias_hh"));
+  colsum_kernel<<<kG / 32, 256, 0, st>>>(p.dGI, kG, S, kG, grad + layout_offset(L, "rnn.bias_ih"));
+  dx_kernel<<<(S + 7) / 8, 256, 0, st>>>(p.dGI, p.Wih, S, p.dX);
+  input_grads_kernel<<<1, 256, 0, st>>>(p.dX, b.goal, b.prev_action, b.env_idx, b.T, b.ld, b.T_run, S,
+                                        grad + layout_offset(L, "goal_fc.weight"),
+                                        grad + layout_offset(L, "goal_fc.bias"),
+                                        grad + layout_offset(L, "act_embed.weight"));
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
