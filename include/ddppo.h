@@ -264,6 +264,13 @@ ddppo_status ddppo_profile_enable(ddppo_ctx* ctx, int enable);
 ddppo_status ddppo_profile_read(ddppo_ctx* ctx, double* host_ms /* [DDPPO_K_COUNT] */,
                                 int64_t* host_launches /* [DDPPO_K_COUNT] */, int reset);
 
+/* Diagnostic entry to the tcgen05 GEMM used inside the backward (stream-ordered):
+ * C[m][n] = sum_k A[m*sam + k*sak] * B[n*sbn + k*sbk]; operands rounded to bf16, fp32 accumulate
+ * in TMEM.  C is row-major with leading dimension ldc.  Used by the tests to pin the kernel. */
+ddppo_status ddppo_debug_gemm_bf16(ddppo_ctx* ctx, const float* A, int64_t sam, int64_t sak,
+                                   const float* B, int64_t sbn, int64_t sbk, float* C, int64_t ldc,
+                                   int M, int N, int K, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

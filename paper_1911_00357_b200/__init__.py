@@ -197,6 +197,11 @@ def learner_cfg(epochs=2, minibatches=2, gamma=0.99, tau=0.95, normalize_adv=Tru
     return c
 
 
+def ddppo_debug_gemm_bf16(ctx, A, sam, sak, B, sbn, sbk, C, ldc, M, N, K, stream=None):
+    """C[m][n] = sum_k A(m,k) B(n,k) on the tcgen05 path (A, B, C fp32 CUDA tensors; strides in elements)."""
+    _call(ctx, "ddppo_debug_gemm_bf16", f32(A), sam, sak, f32(B), sbn, sbk, f32(C), ldc, M, N, K, _stream(stream))
+
+
 def profile_enable(ctx, on=True):
     _call(ctx, "ddppo_profile_enable", int(on))
 

@@ -103,6 +103,8 @@ _SIGS = {
                                    c_vp, c_vp, c_size, P_(c_i32), c_vp]),
     "ddppo_profile_enable": (c_int, [c_vp, c_int]),
     "ddppo_profile_read": (c_int, [c_vp, c_vp, c_vp, c_int]),
+    "ddppo_debug_gemm_bf16": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_int, c_int,
+                                      c_vp]),
 }
 KERNEL_FAMILIES = ("gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other")
 for _name, (_res, _args) in _SIGS.items():

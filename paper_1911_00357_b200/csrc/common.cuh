@@ -187,6 +187,18 @@ ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float*
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
                               float* grad_norm, cudaStream_t st);
 
+// tcgen05 GEMM: C[m][n] = sum_k A(m,k) B(n,k) with generic strides (gemm_tc.cu)
+struct GemmTC {
+  const float* A;
+  int64_t sam, sak;
+  const float* B;
+  int64_t sbn, sbk;
+  float* C;
+  int64_t ldc;
+  int M, N, K;
+};
+ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st);
+
 // models
 struct ModelLayout {
   int64_t P = 0;

@@ -31,7 +31,7 @@
 namespace {
 
 constexpr int kH = 512, kG = 3 * kH, kIn = 64, kNC = 16, kUPC = kH / kNC /*32*/, kRows = 3 * kUPC /*96*/;
-constexpr int kBMax = 8, kA1 = 5, kTMax = 1024;
+constexpr int kBMax = 8, kA1 = 5, kTMax = 1024, kU = 12;  // U: 9 used columns, padded to 12
 constexpr int kHStride = kH + 8;     // fp16 row stride of the broadcast h buffer (bank-conflict pad)
 constexpr int kDgStride = kRows + 8; // bf16 row stride of the dG_h buffer
 constexpr int kFwdThreads = 384, kBwdThreads = 512;
@@ -109,7 +109,8 @@ struct GpsPtrs {
   float* dH;     // [S][512]  dL/dh_t from the head
   float* dGI;    // [S][1536]
   float* dGH;    // [S][1536]
-  float* dX;     // [S][64]
+  float* U;      // [S][9]     [goal, 1, onehot(prev_action)]
+  float* Q;      // [1536][9]  dG_x^T U
 };
 
 // ------------------------------------------------------------------ mbarrier / st.async helpers
@@ -198,6 +199,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) 
       x = p.Emb[p.prev_action[(size_t)n * p.ld + t] * 32 + (k - 32)];
     }
     p.X[(size_t)s * kIn + k] = x;
+  }
+  // U[s] = [goal (3), 1, onehot(prev_action) (5)]: the per-sample inputs of the goal FC and the
+  // embedding, so that their gradients (and db_ih) come out of one GEMM Q = dG_x^T U in the bwd
+  for (int i = tid; i < ((S + kNC - 1 - c) / kNC) * kU; i += blockDim.x) {
+    const int s = c + (i / kU) * kNC, k = i % kU;
+    const int b = s / T_run, t = s - b * T_run;
+    const int n = p.env_idx[b];
+    float u;
+    if (k < 3) u = p.goal[((size_t)n * p.T + t) * 3 + k];
+    else if (k == 3) u = 1.f;
+    else if (k < 9) u = (p.prev_action[(size_t)n * p.ld + t] == k - 4) ? 1.f : 0.f;
+    else u = 0.f;
+    p.U[(size_t)s * kU + k] = u;
   }
   __syncthreads();
   // initial state h_in_0 = mask_0 * h0 (full vector for the MMA operand, own slice in fp32)
@@ -519,6 +533,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ A
   const int per = (S + kRedChunks - 1) / kRedChunks;
   float a = 0.f;
   if (m < M)
+#pragma unroll 8
     for (int s = q * per; s < min(S, (q + 1) * per); ++s) a += A[(size_t)s * lda + m];
   part[q][threadIdx.x & 31] = a;
   __syncthreads();
@@ -539,6 +554,7 @@ __global__ void __launch_bounds__(256) head_wgrad_kernel(const float* __restrict
   const int kk = threadIdx.x & 31, q = threadIdx.x >> 5, k = blockIdx.x * 32 + kk;
   const int per = (S + kRedChunks - 1) / kRedChunks;
   float a[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f}, bsum[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
   for (int s = q * per; s < min(S, (q + 1) * per); ++s) {
     const float h = Hs[(size_t)s * kH + k];
     const float4 dl = *reinterpret_cast<const float4*>(dlogits + (size_t)s * 4);
@@ -581,122 +597,50 @@ __global__ void __launch_bounds__(256) head_wgrad_kernel(const float* __restrict
   }
 }
 
-// ------------------------------------------------------------------ weight-gradient GEMMs
-// C[M][N] = sum_s A[s][m] * Bm[s][n]  (A row stride lda, Bm row stride ldb), fixed s order.
-// 64x64 tile per CTA, 256 threads, 4x4 outputs per thread, s in chunks of 16 through smem.
-__global__ void __launch_bounds__(256) gemm_atb_kernel(const float* __restrict__ A, int lda,
-                                                       const float* __restrict__ Bm, int ldb, int S, int M, int N,
-                                                       float* __restrict__ C, int ldc) {
-  __shared__ float As[16][64 + 4];
-  __shared__ float Bs[16][64 + 4];
-  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[4][4] = {};
-  for (int s0 = 0; s0 < S; s0 += 16) {
-    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
-      const int ss = i / 64, j = i % 64;
-      const int s = s0 + ss;
-      As[ss][j] = (s < S && m0 + j < M) ? A[(size_t)s * lda + m0 + j] : 0.f;
-      Bs[ss][j] = (s < S && n0 + j < N) ? Bm[(size_t)s * ldb + n0 + j] : 0.f;
-    }
-    __syncthreads();
+// Input-layer gradients from Q = dG_x^T U (U = [goal, 1, onehot(prev_action)] per sample):
+//   dW_goal[j][c] = sum_row W_ih[row][j] Q[row][c]   (c < 3),  db_goal[j] = ... Q[row][3]
+//   dEmb[a][j]    = sum_row W_ih[row][32+j] Q[row][4+a],      db_ih[row] = Q[row][3]
+// (chain rule through x = [goal_fc(goal), emb(prev_action)]).  Block j reduces its
+// 1536-row dot products in a fixed order (thread partials, then a fixed-order tree).
+__global__ void __launch_bounds__(256) input_layer_grads_kernel(const float* __restrict__ Wih,
+                                                                const float* __restrict__ Q, float* __restrict__ dWg,
+                                                                float* __restrict__ dbg, float* __restrict__ dEmb,
+                                                                float* __restrict__ dbih) {
+  __shared__ float part[8][kU][33];
+  const int j = blockIdx.x;  // 0..63
+  float a[kU];
 #pragma unroll
-    for (int ss = 0; ss < 16; ++ss) {
-      float a[4], b[4];
+  for (int n = 0; n < kU; ++n) a[n] = 0.f;
+#pragma unroll 2
+  for (int row = threadIdx.x; row < kG; row += 256) {
+    const float w = Wih[(size_t)row * kIn + j];
+    const float* q = Q + (size_t)row * kU;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[ss][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[ss][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
-    }
-    __syncthreads();
+    for (int n = 0; n < kU; ++n) a[n] += w * q[n];
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
-      if (m < M && n < N) C[(size_t)m * ldc + n] = acc[i][j];
-    }
-}
-
-// dX[s][j] = sum_row dGI[s][row] * Wih[row][j]: CTA per 8 samples, thread (j, sample pair),
-// rows streamed in chunks of 128 through shared memory.
-__global__ void __launch_bounds__(256) dx_kernel(const float* __restrict__ dGI, const float* __restrict__ Wih, int S,
-                                                 float* __restrict__ dX) {
-  __shared__ float dg[8][128];
-  const int j = threadIdx.x & 63, q = threadIdx.x >> 6, s0 = blockIdx.x * 8;
-  float a0 = 0.f, a1 = 0.f;
-  for (int r0 = 0; r0 < kG; r0 += 128) {
-    for (int i = threadIdx.x; i < 8 * 128; i += 256) {
-      const int ss = i >> 7, rr = i & 127;
-      dg[ss][rr] = (s0 + ss < S) ? dGI[(size_t)(s0 + ss) * kG + r0 + rr] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int rr = 0; rr < 128; ++rr) {
-      const float w = Wih[(size_t)(r0 + rr) * kIn + j];
-      a0 += dg[q][rr] * w;
-      a1 += dg[q + 4][rr] * w;
-    }
-    __syncthreads();
-  }
-  if (s0 + q < S) dX[(size_t)(s0 + q) * kIn + j] = a0;
-  if (s0 + q + 4 < S) dX[(size_t)(s0 + q + 4) * kIn + j] = a1;
-}
-
-// goal-FC and embedding gradients from dX: thread (j, chunk q of 4), chunk partials summed in order
-__global__ void __launch_bounds__(256) input_grads_kernel(const float* __restrict__ dX, const float* __restrict__ goal,
-                                                          const int32_t* __restrict__ prev_action,
-                                                          const int32_t* __restrict__ env_idx, int T, int ld,
-                                                          int T_run, int S, float* __restrict__ dWg,
-                                                          float* __restrict__ dbg, float* __restrict__ dEmb) {
-  __shared__ float part[4][64][5];
-  const int j = threadIdx.x & 63, q = threadIdx.x >> 6;
-  const int per = (S + 3) / 4;
-  float a[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int s = q * per; s < min(S, (q + 1) * per); ++s) {
-    const int b = s / T_run, t = s - b * T_run;
-    const int n = env_idx[b];
-    const float d = dX[(size_t)s * kIn + j];
-    if (j < 32) {
-      const float* gg = goal + ((size_t)n * T + t) * 3;
-      a[0] += d * gg[0];
-      a[1] += d * gg[1];
-      a[2] += d * gg[2];
-      a[3] += d;
-    } else {
-      const int act = prev_action[(size_t)n * ld + t];
-#pragma unroll
-      for (int o = 0; o < kA1; ++o) a[o] += (act == o) ? d : 0.f;
-    }
-  }
-#pragma unroll
-  for (int o = 0; o < 5; ++o) part[q][j][o] = a[o];
+  for (int n = 0; n < kU; ++n) part[warp][n][lane] = a[n];
   __syncthreads();
-  if (threadIdx.x < 64) {
-    float t[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int o = 0; o < 5; ++o) t[o] += part[i][j][o];
+  if (threadIdx.x < kU) {
+    const int n = threadIdx.x;
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w)
+      for (int l = 0; l < 32; ++l) t += part[w][n][l];
     if (j < 32) {
-      dWg[j * 3 + 0] = t[0];
-      dWg[j * 3 + 1] = t[1];
-      dWg[j * 3 + 2] = t[2];
-      dbg[j] = t[3];
-    } else {
-#pragma unroll
-      for (int o = 0; o < kA1; ++o) dEmb[o * 32 + (j - 32)] = t[o];
+      if (n < 3) dWg[j * 3 + n] = t;
+      else if (n == 3) dbg[j] = t;
+    } else if (n >= 4 && n < 9) {
+      dEmb[(n - 4) * 32 + (j - 32)] = t;
     }
   }
+  if (j == 0)
+    for (int row = threadIdx.x; row < kG; row += 256) dbih[row] = Q[(size_t)row * kU + 3];
 }
 
 // ------------------------------------------------------------------ workspace carving
 struct GpsWs {
-  float *X, *GI, *Hs, *Hin, *RZNG, *dH, *dGI, *dGH, *dX;
+  float *X, *GI, *Hs, *Hin, *RZNG, *dH, *dGI, *dGH, *U, *Q;
 };
 size_t carve(void* base, int B, int T, GpsWs* w) {
   size_t off = 0;
@@ -715,7 +659,8 @@ size_t carve(void* base, int B, int T, GpsWs* w) {
   tmp.dH = take(S * kH);
   tmp.dGI = take(S * kG);
   tmp.dGH = take(S * kG);
-  tmp.dX = take(S * kIn);
+  tmp.U = take(S * kU);
+  tmp.Q = take((size_t)kG * kU);
   if (w) *w = tmp;
   return off;
 }
@@ -750,7 +695,8 @@ GpsPtrs make_ptrs(const ModelLayout& L, const float* params, const ddppo_batch& 
   p.dH = w.dH;
   p.dGI = w.dGI;
   p.dGH = w.dGH;
-  p.dX = w.dX;
+  p.U = w.U;
+  p.Q = w.Q;
   return p;
 }
 
@@ -814,18 +760,23 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
     if (s != DDPPO_OK) return s;
   }
   // weight gradients (off the dependency chain)
-  ProfScope ps(ctx, DDPPO_K_WGRAD, st, 6);
-  gemm_atb_kernel<<<dim3(kH / 64, kG / 64), 256, 0, st>>>(p.dGH, kG, p.Hin, kH, S, kG, kH,
-                                                         grad + layout_offset(L, "rnn.weight_hh"), kH);
-  gemm_atb_kernel<<<dim3(1, kG / 64), 256, 0, st>>>(p.dGI, kG, p.X, kIn, S, kG, kIn,
-                                                   grad + layout_offset(L, "rnn.weight_ih"), kIn);
+  ProfScope ps(ctx, DDPPO_K_WGRAD, st, 5);
+  // tcgen05 GEMMs (bf16 operands, fp32 TMEM accumulation) over the S samples:
+  //   dW_hh[row][j] = sum_s dG_h[s][row] H_in[s][j];  dW_ih[row][j] = sum_s dG_x[s][row] X[s][j]
+  //   Q[row][n]     = sum_s dG_x[s][row] U[s][n]   (-> goal FC, embedding and b_ih gradients)
+  ddppo_status gs = launch_gemm_tc(
+      ctx, GemmTC{p.dGH, 1, kG, p.Hin, 1, kH, grad + layout_offset(L, "rnn.weight_hh"), kH, kG, kH, S}, st);
+  if (gs != DDPPO_OK) return gs;
+  gs = launch_gemm_tc(ctx, GemmTC{p.dGI, 1, kG, p.X, 1, kIn, grad + layout_offset(L, "rnn.weight_ih"), kIn, kG, kIn, S},
+                      st);
+  if (gs != DDPPO_OK) return gs;
+  gs = launch_gemm_tc(ctx, GemmTC{p.dGI, 1, kG, p.U, 1, kU, p.Q, kU, kG, kU, S}, st);
+  if (gs != DDPPO_OK) return gs;
   colsum_kernel<<<kG / 32, 256, 0, st>>>(p.dGH, kG, S, kG, grad + layout_offset(L, "rnn.bias_hh"));
-  colsum_kernel<<<kG / 32, 256, 0, st>>>(p.dGI, kG, S, kG, grad + layout_offset(L, "rnn.bias_ih"));
-  dx_kernel<<<(S + 7) / 8, 256, 0, st>>>(p.dGI, p.Wih, S, p.dX);
-  input_grads_kernel<<<1, 256, 0, st>>>(p.dX, b.goal, b.prev_action, b.env_idx, b.T, b.ld, b.T_run, S,
-                                        grad + layout_offset(L, "goal_fc.weight"),
-                                        grad + layout_offset(L, "goal_fc.bias"),
-                                        grad + layout_offset(L, "act_embed.weight"));
+  input_layer_grads_kernel<<<kIn, 256, 0, st>>>(p.Wih, p.Q, grad + layout_offset(L, "goal_fc.weight"),
+                                                grad + layout_offset(L, "goal_fc.bias"),
+                                                grad + layout_offset(L, "act_embed.weight"),
+                                                grad + layout_offset(L, "rnn.bias_ih"));
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
