@@ -32,9 +32,6 @@ namespace {
 
 constexpr int kH = 512, kG = 3 * kH, kIn = 64, kNC = 16, kUPC = kH / kNC /*32*/, kRows = 3 * kUPC /*96*/;
 constexpr int kBMax = 8, kA1 = 5, kTMax = 1024, kU = 12;  // U: 9 used columns, padded to 12
-constexpr int kHStride = kH + 8;     // fp16 row stride of the broadcast h buffer (bank-conflict pad)
-constexpr int kDgStride = kRows + 8; // bf16 row stride of the dG_h buffer
-constexpr int kFwdThreads = 384, kBwdThreads = 512;
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -86,6 +83,28 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+// Single-MUFU forms used on the recurrence's critical path (tanh.approx: ~2^-11 relative error,
+// below the fp16 rounding of the broadcast state).
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigmoid_fast(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
+
+// Debug-build phase trace of the forward recurrence (CTA 0, thread 0): clock64 at
+// 0 = h_{t-1} received, 1 = W_hh h done, 2 = h_t sent.  Compiled out of the product library.
+#ifdef DDPPO_TRACE
+__device__ long long g_trace[8 * kTMax];
+__device__ long long g_trace_b[8 * kTMax];
+#define DDPPO_TRACE_POINT(c, tid, t, k) \
+  if ((c) == 0 && (tid) == 0 && (t) < kTMax) g_trace[8 * (t) + (k)] = clock64();
+#define DDPPO_TRACE_B(c, tid, t, k) \
+  if ((c) == 0 && (tid) == 0 && (t) < kTMax) g_trace_b[8 * (t) + (k)] = clock64();
+#else
+#define DDPPO_TRACE_POINT(c, tid, t, k)
+#define DDPPO_TRACE_B(c, tid, t, k)
+#endif
 
 // local gate row lr in [0,96) of CTA c -> global row of W (gate-major: r | z | n blocks of 512)
 __device__ __forceinline__ int grow_of(int c, int lr) { return (lr / kUPC) * kH + c * kUPC + (lr % kUPC); }
@@ -124,13 +143,15 @@ __device__ __forceinline__ void fence_mbar_init_cluster() {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// acquire at cluster scope: the data came from peer CTAs (st.async ... complete_tx)
+// The data arrives in this CTA's own shared memory through st.async ... complete_tx, whose
+// completion on the local mbarrier makes it visible: the default (CTA-scope) acquire suffices.
+// (A .cluster-scope acquire would make ptxas emit an L1 invalidate, CCTL.IVALL, on every poll.)
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
@@ -148,36 +169,101 @@ __device__ __forceinline__ void st_async_v2f(uint32_t raddr, float a, float b, u
 }
 
 // ------------------------------------------------------------------ forward recurrence
-// Per step t: all warps wait on the local mbarrier of buffer t%2 (filled by the 16 CTAs'
-// st.async packets of h_{t-1}), 12 warps run the W_hh h MMAs, the gate warps (one per batch
-// element) finish the GRU cell for the CTA's 32 units and push the new fp16 slice (4 x 16-byte
-// packets per batch element) to every CTA's next buffer with st.async + complete_tx.  No
-// cluster-wide barrier and no release fence sit on the chain.
+// tcgen05 formulation (one CTA per 32 hidden units, 16-CTA cluster, 256 threads):
+//  * A operand (TMEM, fp16, M = 128 lanes, K = 576 = 512 hidden + 64 input columns):
+//      lanes  0..31  r rows: [W_hr | W_ir]     lanes 32..63  z rows: [W_hz | W_iz]
+//      lanes 64..95  n rows: [W_hn | 0   ]     lanes 96..127 n rows: [0    | W_in]
+//    so ONE accumulation gives r/z pre-activations (input + hidden parts) and the separate
+//    W_hn h and W_in x the n gate needs -- the input projection rides on the same MMAs and no
+//    per-step input projection is read from HBM;
+//  * B operand (smem, fp16 canonical K-major, [16 env rows][576]): the hidden part is filled by
+//    every CTA's st.async packets (8 units of one env = one 16-byte core-matrix row, complete_tx
+//    on this CTA's mbarrier); the input part x_t = [goal_fc(goal_t), emb(prev_action_t)] is
+//    computed locally one step ahead by the otherwise idle warps 4..7;
+//  * per step warps 0..3 each issue 9 of the 36 tcgen05.mma (M=128, N=16, K=16) into their own
+//    TMEM accumulator (issue cost spread over 4 sub-partitions), commit to one mbarrier, read the
+//    four accumulators back (tcgen05.ld.32x32b) and the gate warps finish the GRU cell for the
+//    CTA's 32 units, then push the new h slice.  No cluster barrier, no HBM read on the chain.
+constexpr int kFwdThreads = 256;
+constexpr int kKX = kH + kIn;                  // 576: K of the fused [h; x] operand
+constexpr uint32_t kTileSBO = (kKX / 8) * 128; // 9216 B between 8-row groups of a [rows x 576] tile
+constexpr int kAcc = 4;                        // MMA warps = independent accumulators
+constexpr uint32_t kAccCol0 = kKX / 2;         // TMEM columns [0, 288): A operand (fp16 pairs)
+constexpr int kTmemCols = 512;
+
+__device__ __forceinline__ uint32_t ktile_off(int r, int k) {  // canonical K-major, K = 576
+  return (uint32_t)((r >> 3) * kTileSBO + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// kind::f16, D f32, A f16, B f16, K-major, M = 128, N = 16
+constexpr uint32_t kIdescF16_M128_N16 = (1u << 4) | (0u << 7) | (0u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
 struct FwdSmem {
-  __half hbuf[2][kBMax][kHStride];  // broadcast h_in (fp16), double-buffered by step parity
-  float ghp[2][kRows][kBMax];       // partial W_hh h products of the two k-halves
-  float hown[kBMax][kUPC];          // fp32 state h_in for own units
-  __half stage[kBMax][kUPC];        // own new h slice before it is packed into st.async packets
-  float bhh[kRows];
-  float bih[kRows];
-  uint64_t bar[2];                  // "buffer t%2 holds h_{t-1}" (tx-count barrier)
+  unsigned char h_tile[2][2 * kTileSBO];  // [h_{t-1}; x_t] (fp16) [16 env rows][576], by step parity
+  float acc[128][kBMax];                  // the accumulator rows read back from TMEM
+  float hown[kBMax][kUPC];                // fp32 state h_in for own units
+  unsigned char stage[2][512];            // own new h slice [env][32 units] fp16, by step parity
+  float bias[128];                        // r: b_ir+b_hr, z: b_iz+b_hz, n_h: b_hn, n_x: b_in
+  float wg[32 * 3 + 32];                  // goal FC
+  float emb[kA1 * 32];                    // action embedding
+  uint64_t bar[2];                        // "h_tile[t%2] holds h_{t-1}" (tx-count barrier)
+  uint64_t mma_bar;                       // "the accumulators hold W [h; x]"
+  uint32_t tmem_slot;
 };
 
+// x_t for env b into the B tile (k = 512..575) and, from CTA 0, the X / U rows of sample s
+__device__ __forceinline__ void fwd_input(const GpsPtrs& p, FwdSmem& sm, unsigned char* tile, int b, int j, int t,
+                                          bool write_global) {
+  const int n = p.env_idx[b];
+  const int T_run = p.T_run;
+  const float* gg = p.goal + ((size_t)n * p.T + t) * 3;
+  const int act = p.prev_action[(size_t)n * p.ld + t];
+  float x;
+  if (j < 32) x = sm.wg[j * 3 + 0] * gg[0] + sm.wg[j * 3 + 1] * gg[1] + sm.wg[j * 3 + 2] * gg[2] + sm.wg[96 + j];
+  else x = sm.emb[act * 32 + (j - 32)];
+  *reinterpret_cast<__half*>(tile + ktile_off(b, kH + j)) = __float2half(x);
+  if (write_global) {
+    const size_t s = (size_t)b * T_run + t;
+    p.X[s * kIn + j] = x;
+    if (j < kU) {
+      float u;
+      if (j < 3) u = gg[j];
+      else if (j == 3) u = 1.f;
+      else if (j < 9) u = (act == j - 4) ? 1.f : 0.f;
+      else u = 0.f;
+      p.U[s * kU + j] = u;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(smem_raw);
   float* smask = reinterpret_cast<float*>(smem_raw + sizeof(FwdSmem));  // [B][T_run]
   const int c = (int)cluster_ctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int B = p.B, T_run = p.T_run, S = B * T_run;
-  const int g = lane >> 2, tq = lane & 3;
+  DDPPO_TRACE_POINT(c, tid, kTMax - 1, 5);
 
-  // ---- prologue 1: zero the h buffers, stage own biases and masks, X slice (samples s % 16 == c)
-  for (int i = tid; i < 2 * kBMax * kHStride; i += blockDim.x) (&sm.hbuf[0][0][0])[i] = __float2half(0.f);
-  for (int i = tid; i < kRows; i += blockDim.x) {
-    sm.bhh[i] = p.bhh[grow_of(c, i)];
-    sm.bih[i] = p.bih[grow_of(c, i)];
+  // ---- prologue: operand tiles, biases, masks, barriers, TMEM
+  {
+    uint4* zz = reinterpret_cast<uint4*>(sm.h_tile);
+    for (int i = tid; i < (int)(sizeof(sm.h_tile) / 16); i += blockDim.x) zz[i] = make_uint4(0u, 0u, 0u, 0u);
+    uint4* zs = reinterpret_cast<uint4*>(sm.stage);
+    for (int i = tid; i < (int)(sizeof(sm.stage) / 16); i += blockDim.x) zs[i] = make_uint4(0u, 0u, 0u, 0u);
   }
+  for (int i = tid; i < 128; i += blockDim.x) {
+    float bsum;
+    if (i < 64) bsum = p.bih[grow_of(c, i)] + p.bhh[grow_of(c, i)];
+    else if (i < 96) bsum = p.bhh[grow_of(c, i)];
+    else bsum = p.bih[grow_of(c, i - 32)];
+    sm.bias[i] = bsum;
+  }
+  for (int i = tid; i < 128; i += blockDim.x) sm.wg[i] = i < 96 ? p.Wg[i] : p.bg[i - 96];
+  for (int i = tid; i < kA1 * 32; i += blockDim.x) sm.emb[i] = p.Emb[i];
   for (int i = tid; i < S; i += blockDim.x) {
     const int b = i / T_run, t = i - b * T_run;
     smask[i] = p.mask[(size_t)p.env_idx[b] * p.ld + t];
@@ -185,200 +271,229 @@ __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) 
   if (tid == 0) {
     mbar_init(&sm.bar[0], 1);
     mbar_init(&sm.bar[1], 1);
+    mbar_init(&sm.mma_bar, kAcc);  // one tcgen05.commit per MMA warp
     fence_mbar_init_cluster();
   }
-  for (int i = tid; i < ((S + kNC - 1 - c) / kNC) * kIn; i += blockDim.x) {
-    const int s = c + (i / kIn) * kNC, k = i % kIn;
-    const int b = s / T_run, t = s - b * T_run;
-    const int n = p.env_idx[b];
-    float x;
-    if (k < 32) {
-      const float* gg = p.goal + ((size_t)n * p.T + t) * 3;
-      x = p.Wg[k * 3 + 0] * gg[0] + p.Wg[k * 3 + 1] * gg[1] + p.Wg[k * 3 + 2] * gg[2] + p.bg[k];
-    } else {
-      x = p.Emb[p.prev_action[(size_t)n * p.ld + t] * 32 + (k - 32)];
-    }
-    p.X[(size_t)s * kIn + k] = x;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  // U[s] = [goal (3), 1, onehot(prev_action) (5)]: the per-sample inputs of the goal FC and the
-  // embedding, so that their gradients (and db_ih) come out of one GEMM Q = dG_x^T U in the bwd
-  for (int i = tid; i < ((S + kNC - 1 - c) / kNC) * kU; i += blockDim.x) {
-    const int s = c + (i / kU) * kNC, k = i % kU;
-    const int b = s / T_run, t = s - b * T_run;
-    const int n = p.env_idx[b];
-    float u;
-    if (k < 3) u = p.goal[((size_t)n * p.T + t) * 3 + k];
-    else if (k == 3) u = 1.f;
-    else if (k < 9) u = (p.prev_action[(size_t)n * p.ld + t] == k - 4) ? 1.f : 0.f;
-    else u = 0.f;
-    p.U[(size_t)s * kU + k] = u;
-  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  // initial state h_in_0 = mask_0 * h0 (full vector for the MMA operand, own slice in fp32)
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_slot;
+  // A operand -> TMEM.  Warp w and w+4 share lane quarter w%4 (row r = 32(w%4) + lane) and split
+  // the 288 packed columns: 8 columns (16 weights) per tcgen05.st.32x32b.x8.
+  {
+    const int r = (warp & 3) * 32 + lane;
+    const int gate_row = r < 96 ? r : r - 32;  // n_x rows reuse the n rows' input weights
+    const float* wh = p.Whh + (size_t)grow_of(c, gate_row) * kH;
+    const float* wi = p.Wih + (size_t)grow_of(c, gate_row) * kIn;
+    const bool has_h = r < 96, has_x = r < 64 || r >= 96;
+    const int col_lo = (warp < 4) ? 0 : kAccCol0 / 2;
+#pragma unroll 1
+    for (int col0 = col_lo; col0 < col_lo + (int)kAccCol0 / 2; col0 += 48) {
+      float4 a[24];  // 96 weights = 48 columns: all loads in flight before any conversion
+#pragma unroll
+      for (int q = 0; q < 24; ++q) {
+        const int k = 2 * col0 + 4 * q;
+        a[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < kH) {
+          if (has_h) a[q] = *reinterpret_cast<const float4*>(wh + k);
+        } else if (has_x) {
+          a[q] = *reinterpret_cast<const float4*>(wi + (k - kH));
+        }
+      }
+#pragma unroll
+      for (int sblk = 0; sblk < 6; ++sblk) {  // 8 columns per tcgen05.st
+        uint32_t v[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[2 * q] = pack_f16(a[4 * sblk + q].x, a[4 * sblk + q].y);
+          v[2 * q + 1] = pack_f16(a[4 * sblk + q].z, a[4 * sblk + q].w);
+        }
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(
+                         tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(col0 + 8 * sblk)),
+                     "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                     : "memory");
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  // initial B tile: h_in_0 = mask_0 * h0 and x_0
   for (int i = tid; i < B * kH; i += blockDim.x) {
     const int b = i / kH, k = i % kH;
     const float h = smask[b * T_run] * p.h0[(size_t)p.env_idx[b] * kH + k];
-    sm.hbuf[0][b][k] = __float2half(h);
+    *reinterpret_cast<__half*>(sm.h_tile[0] + ktile_off(b, k)) = __float2half(h);
     if (k >= c * kUPC && k < (c + 1) * kUPC) sm.hown[b][k - c * kUPC] = h;
   }
-  // W_hh A-fragments: warp w -> m-tile mt = w/2 (16 local rows), k-half kh = w%2 (16 k-tiles)
-  const int mt = warp >> 1, kh = warp & 1;
-  uint32_t afr[16][4];
-  {
-    const int r0 = grow_of(c, mt * 16 + g), r1 = grow_of(c, mt * 16 + g + 8);
-    const float2* w0 = reinterpret_cast<const float2*>(p.Whh + (size_t)r0 * kH);
-    const float2* w1 = reinterpret_cast<const float2*>(p.Whh + (size_t)r1 * kH);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int k2 = ((kh * 16 + j) * 16 + 2 * tq) / 2;
-      const float2 a = w0[k2], b = w1[k2], cc = w0[k2 + 4], d = w1[k2 + 4];
-      afr[j][0] = pack_f16(a.x, a.y);
-      afr[j][1] = pack_f16(b.x, b.y);
-      afr[j][2] = pack_f16(cc.x, cc.y);
-      afr[j][3] = pack_f16(d.x, d.y);
-    }
-  }
-  __threadfence();
-  cluster_sync_all();  // X visible cluster-wide; barriers/buffers initialised before remote writes
-
-  // ---- prologue 2: GI[c][t][b][lr] = W_ih[row] . X[s] + b_ih[row] with m16n8k16 tiles
-  // (6 m-tiles of own rows x S/8 sample tiles x 4 k-tiles; off the dependency chain)
-  {
-    const int mt2 = warp % 6, half = warp / 6;
-    uint32_t wa[4][4];
-    const float2* w0 = reinterpret_cast<const float2*>(p.Wih + (size_t)grow_of(c, mt2 * 16 + g) * kIn);
-    const float2* w1 = reinterpret_cast<const float2*>(p.Wih + (size_t)grow_of(c, mt2 * 16 + g + 8) * kIn);
-#pragma unroll
-    for (int kt = 0; kt < 4; ++kt) {
-      const int k2 = (kt * 16 + 2 * tq) / 2;
-      const float2 a = w0[k2], b = w1[k2], cc = w0[k2 + 4], d = w1[k2 + 4];
-      wa[kt][0] = pack_f16(a.x, a.y);
-      wa[kt][1] = pack_f16(b.x, b.y);
-      wa[kt][2] = pack_f16(cc.x, cc.y);
-      wa[kt][3] = pack_f16(d.x, d.y);
-    }
-    const int n_tiles = (S + 7) / 8;
-    for (int nt = half; nt < n_tiles; nt += 2) {
-      const int sb = nt * 8 + g;  // sample of this lane's B-fragment column
-      const float2* xr = reinterpret_cast<const float2*>(p.X + (size_t)min(sb, S - 1) * kIn);
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kt = 0; kt < 4; ++kt) {
-        float2 x0 = xr[(kt * 16 + 2 * tq) / 2], x1 = xr[(kt * 16 + 8 + 2 * tq) / 2];
-        if (sb >= S) x0 = x1 = make_float2(0.f, 0.f);
-        mma_f16(acc, wa[kt], pack_f16(x0.x, x0.y), pack_f16(x1.x, x1.y));
-      }
-      const int lr0 = mt2 * 16 + g;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int lr = lr0 + (e >> 1) * 8, s = nt * 8 + 2 * tq + (e & 1);
-        if (s < S) {
-          const int b = s / T_run, t = s - b * T_run;
-          p.GI[(((size_t)c * T_run + t) * B + b) * kRows + lr] = acc[e] + sm.bih[lr];
-        }
-      }
-    }
-  }
-  __syncthreads();
+  for (int i = tid; i < B * kIn; i += blockDim.x) fwd_input(p, sm, sm.h_tile[0], i / kIn, i % kIn, 0, c == 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // barriers and tiles initialised everywhere before any remote write
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  DDPPO_TRACE_POINT(c, tid, kTMax - 1, 6);
+  DDPPO_TRACE_POINT(c, tid, kTMax - 1, 7);
 
   // ---- recurrence
-  const int gu = lane, gb = warp;  // gate thread: warp b handles batch element b, lane = unit
+  const int gu = lane, gb = warp;  // gate thread: warp b handles env b of the minibatch, lane = unit
   const bool gate_warp = warp < B;
-  // st.async packet of this lane: units [8*(lane%4), +8) of batch gb to CTAs lane/4 and lane/4+8
+  // st.async packet of this lane: units [8*(lane%4), +8) of env gb (one 16-byte core-matrix row of
+  // the peers' B tiles) to CTAs lane/4 and lane/4+8.  (Measured: 128 such packets per step beat
+  // 16 cp.async.bulk copies of the whole 512-byte slice -- the bulk path's fixed latency is higher.)
   uint32_t pk_addr[2] = {0u, 0u}, pk_bar[2][2] = {{0u, 0u}, {0u, 0u}};
-  float gi_r = 0.f, gi_z = 0.f, gi_n = 0.f;
   const uint32_t tx_bytes = (uint32_t)(kNC * B * kUPC * sizeof(__half));
   if (gate_warp) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const uint32_t q = (uint32_t)(lane / 4 + 8 * j);
-      pk_addr[j] = map_to_cta(&sm.hbuf[0][gb][c * kUPC + 8 * (lane % 4)], q);
+      pk_addr[j] = map_to_cta(sm.h_tile[0] + ktile_off(gb, c * kUPC + 8 * (lane % 4)), q);
       pk_bar[j][0] = map_to_cta(&sm.bar[0], q);
       pk_bar[j][1] = map_to_cta(&sm.bar[1], q);
     }
-    const float* gi = p.GI + ((size_t)c * T_run * B + gb) * kRows;
-    gi_r = gi[gu];
-    gi_z = gi[kUPC + gu];
-    gi_n = gi[2 * kUPC + gu];
   }
-  const uint32_t hbuf_parity_bytes = (uint32_t)sizeof(sm.hbuf[0]);
+  const uint32_t h_parity_bytes = (uint32_t)sizeof(sm.h_tile[0]);
+  const uint32_t h_base0 = smem_u32(sm.h_tile[0]);
   for (int t = 0; t < T_run; ++t) {
     const int cur = t & 1;
-    if (t > 0) {
-      if (tid == 0) mbar_arrive_expect_tx(&sm.bar[cur], tx_bytes);
-      mbar_wait_parity(&sm.bar[cur], (uint32_t)(((t - 1) >> 1) & 1));
-    }
-    {
-      float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
-      const uint32_t* hb = reinterpret_cast<const uint32_t*>(&sm.hbuf[cur][g][0]);
-#pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        const int kt0 = kh * 16 + j, kt1 = kt0 + 1;
-        mma_f16(c0, afr[j], hb[kt0 * 8 + tq], hb[kt0 * 8 + 4 + tq]);
-        mma_f16(c1, afr[j + 1], hb[kt1 * 8 + tq], hb[kt1 * 8 + 4 + tq]);
+    if (warp < kAcc) {  // MMA warps: warp a owns accumulator a and K steps kk = a, a+kAcc, ...;
+      // converged warps with warp-uniform operands, one elected lane issues
+      if (t > 0) {
+        if (tid == 0) mbar_arrive_expect_tx(&sm.bar[cur], tx_bytes);
+        mbar_wait_parity(&sm.bar[cur], (uint32_t)(((t - 1) >> 1) & 1));
       }
-      // C layout: c[0],c[1] -> (row g, cols 2tq, 2tq+1); c[2],c[3] -> (row g+8, same cols)
-      const int row = mt * 16 + g;
-      *reinterpret_cast<float2*>(&sm.ghp[kh][row][2 * tq]) = make_float2(c0[0] + c1[0], c0[1] + c1[1]);
-      *reinterpret_cast<float2*>(&sm.ghp[kh][row + 8][2 * tq]) = make_float2(c0[2] + c1[2], c0[3] + c1[3]);
+      DDPPO_TRACE_POINT(c, tid, t, 0);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t bd0 = umma_desc(h_base0 + (uint32_t)cur * h_parity_bytes, 128, kTileSBO);
+      const uint32_t d_acc = tmem + kAccCol0 + 16u * (uint32_t)warp;
+      // descriptor of K step kk = bd0 + 16*kk (start address advances 256 B); A columns 8*kk
+#pragma unroll
+      for (int j = 0; j < kKX / 16 / kAcc; ++j) {
+        const int kk = warp + kAcc * j;
+        asm volatile(
+            "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_acc),
+            "r"(tmem + 8u * (uint32_t)kk), "l"(bd0 + (uint64_t)(16 * kk)), "r"(kIdescF16_M128_N16),
+            "r"((uint32_t)j)
+            : "memory");
+      }
+      asm volatile(
+          "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+              smem_u32(&sm.mma_bar))
+          : "memory");
+      DDPPO_TRACE_POINT(c, tid, t, 3);
+      mbar_wait_parity(&sm.mma_bar, (uint32_t)(t & 1));
+      DDPPO_TRACE_POINT(c, tid, t, 4);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t v[kAcc][8];
+#pragma unroll
+      for (int a = 0; a < kAcc; ++a)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(v[a][0]), "=r"(v[a][1]), "=r"(v[a][2]), "=r"(v[a][3]), "=r"(v[a][4]), "=r"(v[a][5]),
+                       "=r"(v[a][6]), "=r"(v[a][7])
+                     : "r"(tmem + ((uint32_t)(warp * 32) << 16) + kAccCol0 + 16u * (uint32_t)a));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      DDPPO_TRACE_POINT(c, tid, t, 5);
+      float s8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float acc = 0.f;
+#pragma unroll
+        for (int a = 0; a < kAcc; ++a) acc += __uint_as_float(v[a][e]);
+        s8[e] = acc;
+      }
+      const int row = warp * 32 + lane;
+      *reinterpret_cast<float4*>(&sm.acc[row][0]) = make_float4(s8[0], s8[1], s8[2], s8[3]);
+      *reinterpret_cast<float4*>(&sm.acc[row][4]) = make_float4(s8[4], s8[5], s8[6], s8[7]);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    } else if (t + 1 < T_run) {
+      // warps 4..7: x_{t+1} into the other B tile (its last reader, the MMAs of step t-1, are done)
+      for (int i = tid - kAcc * 32; i < B * kIn; i += blockDim.x - kAcc * 32)
+        fwd_input(p, sm, sm.h_tile[cur ^ 1], i / kIn, i % kIn, t + 1, c == 0);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
+    DDPPO_TRACE_POINT(c, tid, t, 1);
     if (gate_warp) {
-      const int lr_r = gu, lr_z = kUPC + gu, lr_n = 2 * kUPC + gu;
-      const float gh_r = sm.ghp[0][lr_r][gb] + sm.ghp[1][lr_r][gb] + sm.bhh[lr_r];
-      const float gh_z = sm.ghp[0][lr_z][gb] + sm.ghp[1][lr_z][gb] + sm.bhh[lr_z];
-      const float gh_n = sm.ghp[0][lr_n][gb] + sm.ghp[1][lr_n][gb] + sm.bhh[lr_n];
+      const int lr_r = gu, lr_z = kUPC + gu, lr_nh = 2 * kUPC + gu, lr_nx = 3 * kUPC + gu;
+      const float pre_r = sm.acc[lr_r][gb] + sm.bias[lr_r];
+      const float pre_z = sm.acc[lr_z][gb] + sm.bias[lr_z];
+      const float gh_n = sm.acc[lr_nh][gb] + sm.bias[lr_nh];
+      const float gi_n = sm.acc[lr_nx][gb] + sm.bias[lr_nx];
       const float h_in = sm.hown[gb][gu];
-      const float r = sigmoidf_(gi_r + gh_r);
-      const float z = sigmoidf_(gi_z + gh_z);
-      const float nn = tanhf(gi_n + r * gh_n);
+      const float r = sigmoid_fast(pre_r);
+      const float z = sigmoid_fast(pre_z);
+      const float nn = tanh_fast(gi_n + r * gh_n);
       const float h = (1.f - z) * nn + z * h_in;
       if (t + 1 < T_run) {
         const float hn = smask[gb * T_run + t + 1] * h;
         sm.hown[gb][gu] = hn;
-        sm.stage[gb][gu] = __float2half(hn);
+        __half* st = reinterpret_cast<__half*>(sm.stage[cur]) + gb * kUPC;
+        st[gu] = __float2half(hn);
         __syncwarp();
-        const uint4 pkt = *reinterpret_cast<const uint4*>(&sm.stage[gb][8 * (lane % 4)]);
-        const uint32_t off = (cur ^ 1) * hbuf_parity_bytes;
+        const uint4 pkt = *reinterpret_cast<const uint4*>(st + 8 * (lane % 4));
+        const uint32_t off = (cur ^ 1) * h_parity_bytes;
         st_async_v4(pk_addr[0] + off, pkt, pk_bar[0][cur ^ 1]);
         st_async_v4(pk_addr[1] + off, pkt, pk_bar[1][cur ^ 1]);
       }
-      // off the chain: save activations, prefetch the next step's input projections
+      DDPPO_TRACE_POINT(c, tid, t, 2);
+      // off the chain: save activations for the head and the backward pass
       const size_t o = ((size_t)gb * T_run + t) * kH + c * kUPC + gu;
       p.Hs[o] = h;
       p.Hin[o] = h_in;
       p.RZNG[o] = make_float4(r, z, nn, gh_n);
-      if (t + 1 < T_run) {
-        const float* gi = p.GI + (((size_t)c * T_run + t + 1) * B + gb) * kRows;
-        gi_r = gi[gu];
-        gi_z = gi[kUPC + gu];
-        gi_n = gi[2 * kUPC + gu];
-      }
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // no CTA exits while a peer could still address its shared memory
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
 // ------------------------------------------------------------------ backward recurrence (BPTT)
-// Iteration i (t = T_run-1-i): gate warps form dG for the CTA's units (local), 16 warps multiply
-// by W_hh^T (bf16 m16n8k16) and st.async their 32-unit x B partials to the owning CTA's
-// recv[i%2] (complete_tx on its mbarrier); the owner sums the 16 partials in CTA order.
+// tcgen05 formulation.  Iteration i (t = T_run-1-i):
+//  * gate warps (warp b = env b, lane = unit) form dG for the CTA's 32 units (local) and write
+//    dG_h into the B operand tile (bf16 canonical K-major [16 env rows][96 own gate rows]);
+//  * warps 0..3 each issue the 6 tcgen05.mma (M=128 hidden units, N=16, K=16) of one 128-unit
+//    tile of W_hh^T (A operand resident in TMEM for the whole sequence, bf16), commit, read the
+//    four tiles' lanes they own back with tcgen05.ld and st.async each unit's partial to the
+//    unit's owner CTA (complete_tx on its mbarrier);
+//  * the owner sums the 16 partials in CTA order (deterministic) -> dL/dh_{t-1}.
+constexpr int kBwdThreads = 256;
+constexpr uint32_t kDgSBO = (kRows / 8) * 128;  // 1536 B between 8-row groups of the [16 x 96] tile
+constexpr uint32_t kBwdD0 = 4 * (kRows / 2);    // TMEM columns [0, 192): 4 tiles x 48 packed columns
+constexpr int kBwdTmemCols = 256;
+// kind::f16, D f32, A bf16, B bf16, K-major, M = 128, N = 16
+constexpr uint32_t kIdescBF16_M128_N16 = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
 struct BwdSmem {
-  __nv_bfloat16 dg[kBMax][kDgStride];    // dG_h of own 96 rows (bf16 MMA operand)
+  unsigned char dg_tile[2 * kDgSBO];      // dG_h (bf16) [16 env rows][96 own rows], canonical layout
   float recv[2][kNC][kUPC][kBMax];        // partial W_hh^T dG_h from every CTA, by iteration parity
-  uint64_t bar[2];
+  uint64_t bar[2];                        // recv[i%2] complete (tx-count)
+  uint64_t mma_bar;
+  uint32_t tmem_slot;
 };
 
+__device__ __forceinline__ uint32_t dg_off(int n, int k) {
+  return (uint32_t)((n >> 3) * kDgSBO + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2);
+}
+
 __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
   float* smask = reinterpret_cast<float*>(smem_raw + sizeof(BwdSmem));  // [B][T_run]
   const int c = (int)cluster_ctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int B = p.B, T_run = p.T_run, S = B * T_run;
-  const int g = lane >> 2, tq = lane & 3;
+  DDPPO_TRACE_B(c, tid, kTMax - 1, 6);
 
-  for (int i = tid; i < kBMax * kDgStride; i += blockDim.x) (&sm.dg[0][0])[i] = __float2bfloat16(0.f);
+  {
+    uint4* zz = reinterpret_cast<uint4*>(sm.dg_tile);
+    for (int i = tid; i < (int)(sizeof(sm.dg_tile) / 16); i += blockDim.x) zz[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
   for (int i = tid; i < S; i += blockDim.x) {
     const int b = i / T_run, t = i - b * T_run;
     smask[i] = p.mask[(size_t)p.env_idx[b] * p.ld + t];
@@ -386,34 +501,65 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
   if (tid == 0) {
     mbar_init(&sm.bar[0], 1);
     mbar_init(&sm.bar[1], 1);
+    mbar_init(&sm.mma_bar, 4);
     fence_mbar_init_cluster();
   }
-  // A-fragments of W_hh^T: warp w -> hidden units j in [32w, 32w+32) (2 m-tiles), k = own 96 rows
-  uint32_t afr[2][6][4];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_slot)),
+                 "n"(kBwdTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_slot;
+  // A operand -> TMEM: tile q (hidden units 128q..128q+127), lane = unit, 48 packed columns of the
+  // 96 own gate rows: A_q[j][lr] = W_hh[grow(c, lr)][128q + j].  Warps w, w+4 share lane quarter
+  // w%4 and split the 4 tiles; loads are coalesced across the warp (consecutive units).
+  {
+    const int jl = (warp & 3) * 32 + lane;
+#pragma unroll 1
+    for (int q = (warp < 4 ? 0 : 2); q < (warp < 4 ? 2 : 4); ++q) {
+      const float* wcol = p.Whh + 128 * q + jl;
+#pragma unroll 1
+      for (int lr0 = 0; lr0 < kRows; lr0 += 48) {
+        float w[48];
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi) {
-    const int j0 = warp * 32 + mi * 16 + g, j1 = j0 + 8;
+        for (int e = 0; e < 48; ++e) w[e] = wcol[(size_t)grow_of(c, lr0 + e) * kH];
 #pragma unroll
-    for (int kt = 0; kt < 6; ++kt) {
-      const int k0 = kt * 16 + 2 * tq;  // local row index
-      const float* wa = p.Whh + (size_t)grow_of(c, k0) * kH;
-      const float* wb = p.Whh + (size_t)grow_of(c, k0 + 1) * kH;
-      const float* wc = p.Whh + (size_t)grow_of(c, k0 + 8) * kH;
-      const float* wd = p.Whh + (size_t)grow_of(c, k0 + 9) * kH;
-      afr[mi][kt][0] = pack_bf16(wa[j0], wb[j0]);
-      afr[mi][kt][1] = pack_bf16(wa[j1], wb[j1]);
-      afr[mi][kt][2] = pack_bf16(wc[j0], wd[j0]);
-      afr[mi][kt][3] = pack_bf16(wc[j1], wd[j1]);
+        for (int sblk = 0; sblk < 3; ++sblk) {
+          uint32_t v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = pack_bf16(w[16 * sblk + 2 * e], w[16 * sblk + 2 * e + 1]);
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(
+                           tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(48 * q + lr0 / 2 + 8 * sblk)),
+                       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                       : "memory");
+        }
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  // destinations of this thread's partials: unit j = 128q + 32w + lane is owned by CTA 4q + w
+  uint32_t dst[4] = {0u, 0u, 0u, 0u}, dbar[4][2] = {{0u, 0u}, {0u, 0u}, {0u, 0u}, {0u, 0u}};
+  if (warp < 4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t owner = (uint32_t)(4 * q + warp);
+      dst[q] = map_to_cta(&sm.recv[0][c][lane][0], owner);
+      dbar[q][0] = map_to_cta(&sm.bar[0], owner);
+      dbar[q][1] = map_to_cta(&sm.bar[1], owner);
     }
   }
-  // destination of this warp's partials: CTA `warp` (owner of units [32*warp, 32*warp+32))
-  const uint32_t recv_remote = map_to_cta(&sm.recv[0][c][0][0], (uint32_t)warp);
-  const uint32_t rbar[2] = {map_to_cta(&sm.bar[0], (uint32_t)warp), map_to_cta(&sm.bar[1], (uint32_t)warp)};
   const uint32_t recv_parity_bytes = (uint32_t)sizeof(sm.recv[0]);
-  const int cols = 2 * ((B + 1) / 2);  // columns each source sends (lanes with 2*tq < B, pairs)
-  const uint32_t tx_bytes = (uint32_t)(kNC * kUPC * cols * sizeof(float));
-  __syncthreads();
+  const uint32_t unit_bytes = B <= 2 ? 8u : (B <= 4 ? 16u : 32u);
+  const uint32_t tx_bytes = (uint32_t)kNC * kUPC * unit_bytes;
+  const uint32_t dg_base = smem_u32(sm.dg_tile);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   const int gu = lane, gb = warp;
   const bool gate_warp = warp < B;
@@ -426,8 +572,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
     rzng = p.RZNG[o];
     h_in = p.Hin[o];
   }
+  DDPPO_TRACE_B(c, tid, kTMax - 1, 7);
   for (int it = 0; it < T_run; ++it) {
     const int t = T_run - 1 - it, par = it & 1;
+    DDPPO_TRACE_B(c, tid, it, 0);
     float dzh = 0.f;
     if (gate_warp) {
       const float dh = dH_t + carry;
@@ -438,11 +586,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
       const float dr = dn_pre * ghn;
       const float dr_pre = dr * r * (1.f - r);
       const float dz_pre = dz * z * (1.f - z);
-      sm.dg[gb][gu] = __float2bfloat16(dr_pre);
-      sm.dg[gb][kUPC + gu] = __float2bfloat16(dz_pre);
-      sm.dg[gb][2 * kUPC + gu] = __float2bfloat16(dn_pre * r);
+      *reinterpret_cast<__nv_bfloat16*>(sm.dg_tile + dg_off(gb, gu)) = __float2bfloat16(dr_pre);
+      *reinterpret_cast<__nv_bfloat16*>(sm.dg_tile + dg_off(gb, kUPC + gu)) = __float2bfloat16(dz_pre);
+      *reinterpret_cast<__nv_bfloat16*>(sm.dg_tile + dg_off(gb, 2 * kUPC + gu)) = __float2bfloat16(dn_pre * r);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       dzh = dh * z;
-      // off the chain (issued early, consumed never on this path): save dG, prefetch step t-1
+      // off the chain: save dG, prefetch step t-1
       const size_t og = ((size_t)gb * T_run + t) * kG + c * kUPC + gu;
       p.dGI[og] = dr_pre;
       p.dGI[og + kH] = dz_pre;
@@ -458,35 +607,66 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
       }
     }
     __syncthreads();
-    {
-      float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
-      const uint32_t* db = reinterpret_cast<const uint32_t*>(&sm.dg[g][0]);
+    DDPPO_TRACE_B(c, tid, it, 1);
+    if (warp < 4) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t bd0 = umma_desc(dg_base, 128, kDgSBO);
+      const uint32_t d_q = tmem + kBwdD0 + 16u * (uint32_t)warp;
 #pragma unroll
-      for (int kt = 0; kt < 6; ++kt) {
-        const uint32_t b0 = db[kt * 8 + tq], b1 = db[kt * 8 + 4 + tq];
-        mma_bf16(c0, afr[0][kt], b0, b1);
-        mma_bf16(c1, afr[1][kt], b0, b1);
+      for (int kk = 0; kk < kRows / 16; ++kk) {
+        asm volatile(
+            "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_q),
+            "r"(tmem + 48u * (uint32_t)warp + 8u * (uint32_t)kk), "l"(bd0 + (uint64_t)(16 * kk)),
+            "r"(kIdescBF16_M128_N16), "r"((uint32_t)kk)
+            : "memory");
       }
-      // rows (unit within the owner's slice): g, g+8 (m-tile 0), 16+g, 24+g (m-tile 1); cols 2tq, 2tq+1
-      if (2 * tq < B) {
-        const uint32_t base = recv_remote + par * recv_parity_bytes;
-        st_async_v2f(base + (uint32_t)(((g) * kBMax + 2 * tq) * 4), c0[0], c0[1], rbar[par]);
-        st_async_v2f(base + (uint32_t)(((g + 8) * kBMax + 2 * tq) * 4), c0[2], c0[3], rbar[par]);
-        st_async_v2f(base + (uint32_t)(((16 + g) * kBMax + 2 * tq) * 4), c1[0], c1[1], rbar[par]);
-        st_async_v2f(base + (uint32_t)(((24 + g) * kBMax + 2 * tq) * 4), c1[2], c1[3], rbar[par]);
+      asm volatile(
+          "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+              smem_u32(&sm.mma_bar))
+          : "memory");
+      DDPPO_TRACE_B(c, tid, it, 2);
+      mbar_wait_parity(&sm.mma_bar, (uint32_t)(it & 1));
+      DDPPO_TRACE_B(c, tid, it, 3);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t v[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(v[q][0]), "=r"(v[q][1]), "=r"(v[q][2]), "=r"(v[q][3]), "=r"(v[q][4]), "=r"(v[q][5]),
+                       "=r"(v[q][6]), "=r"(v[q][7])
+                     : "r"(tmem + ((uint32_t)(warp * 32) << 16) + kBwdD0 + 16u * (uint32_t)q));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      const uint32_t off = (uint32_t)par * recv_parity_bytes;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (unit_bytes == 8u) {
+          st_async_v2f(dst[q] + off, __uint_as_float(v[q][0]), __uint_as_float(v[q][1]), dbar[q][par]);
+        } else {
+          st_async_v4(dst[q] + off, make_uint4(v[q][0], v[q][1], v[q][2], v[q][3]), dbar[q][par]);
+          if (unit_bytes == 32u)
+            st_async_v4(dst[q] + off + 16u, make_uint4(v[q][4], v[q][5], v[q][6], v[q][7]), dbar[q][par]);
+        }
       }
     }
+    DDPPO_TRACE_B(c, tid, it, 4);
     if (gate_warp) {
       if (tid == 0) mbar_arrive_expect_tx(&sm.bar[par], tx_bytes);
       mbar_wait_parity(&sm.bar[par], (uint32_t)((it >> 1) & 1));
+      DDPPO_TRACE_B(c, tid, it, 5);
       float s = 0.f;
 #pragma unroll
       for (int q = 0; q < kNC; ++q) s += sm.recv[par][q][gu][gb];
       carry = smask[gb * T_run + t] * (dzh + s);
     }
-    __syncthreads();  // every warp's MMA has read dg before the gate warps overwrite it
+    __syncthreads();  // the MMAs of this iteration (done: mma_bar) are the last readers of dg_tile
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // no CTA exits while a peer could still address its shared memory
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kBwdTmemCols) : "memory");
 }
 
 // ------------------------------------------------------------------ head (Linear(512, 5)) fwd/bwd
@@ -780,3 +960,12 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
+
+#ifdef DDPPO_TRACE
+extern "C" int ddppo_debug_trace(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * (size_t)n);
+}
+extern "C" int ddppo_debug_trace_bwd(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace_b, sizeof(long long) * (size_t)n);
+}
+#endif

@@ -1,0 +1,107 @@
+"""N = 2 (or more) GPUs: the NCCL paths of steps a3 (adv-norm allreduce), a8 (gradient
+allreduce + Adam), a9 (preemption poll) and a10 (counts) through the C ABI, one process per GPU.
+
+Checks: parameters bit-identical on every rank after a learner step; the update
+equals the oracle's N-rank learner step (per-tensor relative L2 of the parameter update, the
+network tolerance); preemption lengths equal the oracle closed form bit-exactly; step
+accounting is exact.  Skipped when fewer than 2 GPUs are visible."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    import paper_1911_00357_b200 as dd
+    import synth
+    from oracle import preempt
+    from paper_1911_00357_b200.learner import Learner, preempt_collect
+    obj = [dd.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx = dd.Context(rank, world, obj[0], device=rank)
+    out = {}
+    # ---- learner step (gps, one rollout per rank, rank 1 preempted to 40 steps)
+    c = synth.CONFIGS["gps"]
+    desc = dd.model_desc("gps")
+    lay = dd.param_layout(desc)
+    P = dd.param_count(desc)
+    p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 5)
+    lrn = Learner(ctx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+    L = 128 if rank == 0 else 40
+    ro = synth.rollout(c["E"], c["T"], 5, rank=rank, length=L)
+    pm = synth.perms(5, 0, c["epochs"], c["E"], rank=rank)
+    lrn.load_rollout(ro, pm)
+    lrn.step()
+    torch.cuda.synchronize()
+    ctx.check()
+    out["params"] = lrn.params.cpu().numpy()
+    out["stats"] = lrn.stats.cpu().numpy()
+    # ---- a10 counts
+    out["counts"] = dd.ddppo_allreduce_counts(ctx, [c["E"] * L, rank + 1]).tolist()
+    # ---- a9 preemption over NCCL (virtual ticks)
+    T = 32
+    costs = synth.straggler_costs(7, world, T, lo=1.0, hi=8.0)
+    costs[world - 1] *= 5
+    out["L"], out["ticks"] = preempt_collect(ctx, costs[rank], T, 60)
+    out["L_ref"] = preempt.closed_form_lengths(costs, T, 60)[rank]
+    q.put((rank, out))
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_two_rank_learner_step_and_protocols():
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+
+    import synth
+    from oracle import learner
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    assert np.array_equal(res[0]["params"], res[1]["params"])  # rank-identical
+    # oracle: the same two rollouts in one process
+    import paper_1911_00357_b200 as dd
+    c = synth.CONFIGS["gps"]
+    desc = dd.model_desc("gps")
+    lay = dd.param_layout(desc)
+    P = dd.param_count(desc)
+    p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 5)
+    ros = [synth.rollout(c["E"], c["T"], 5, rank=r, length=128 if r == 0 else 40) for r in range(world)]
+    pms = [synth.perms(5, 0, c["epochs"], c["E"], rank=r) for r in range(world)]
+    po, _, _, _, info = learner.learner_step("gps", p0, np.zeros(P), np.zeros(P), 0, ros, pms,
+                                             dict(epochs=c["epochs"], minibatches=c["minibatches"]))
+    dp = res[0]["params"].astype(np.float64) - p0
+    dpo = po - p0
+    for name, off, shape, _ in lay:
+        n = int(np.prod(shape))
+        e = np.linalg.norm(dp[off:off + n] - dpo[off:off + n]) / np.linalg.norm(dpo[off:off + n])
+        assert e < 5e-2, (name, e)
+    assert res[0]["counts"] == res[1]["counts"] == [c["E"] * (128 + 40), 3]
+    for r in range(world):
+        assert res[r]["L"] == res[r]["L_ref"]
+    assert res[0]["ticks"] == res[1]["ticks"]
