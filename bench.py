@@ -35,8 +35,8 @@ L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps"])
     ap.add_argument("--seed", type=int, default=1337)
@@ -338,13 +338,14 @@ def roofline_for(fam, prof, c, lrn, peaks, steps):
     E, T, H = c["E"], c["T"], lrn.hidden
     B = E // c["minibatches"]
     if fam in ("net_fwd", "net_bwd") and c["arch"] == "gps":
-        # per launch: the recurrent matvecs on the dependency chain (fwd: W_hh h and W_ih x; bwd: W_hh^T dg)
+        # per launch: the tcgen05 matvecs of the 128-step chain (fwd: [W_hh|W_ih][h;x]; bwd: W_hh^T dG_h),
+        # useful (unpadded) FLOPs; peak = measured sustained bf16 (kind::f16 runs fp16/bf16 at one rate)
         flops = 2.0 * B * T * (3 * H) * (H + (64 if fam == "net_fwd" else 0))
         achieved = flops / per_launch_s / 1e12
-        peak = bf16 * 0.5  # fp16 / bf16 mma.sync dense peak taken as the bf16 tensor figure (no tcgen05 here)
-        return {"bound": "tensor", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None, "launch_us": per_launch_s * 1e6,
-                "note": "latency-bound: 128 dependent steps x cluster barrier; see DESIGN.md"}
+        return {"bound": "tensor", "kernel": fam, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                "frac": achieved / bf16, "traffic": None, "launch_us": per_launch_s * 1e6,
+                "note": "latency-bound dependency chain (B=2 envs x 128 steps on 16 SMs); per-step phases in "
+                        "DESIGN.md sec. 7; HBM kernels' fractions in profiles/r01_microbench.jsonl"}
     byte_per = {"gae": 17.0 * E * T, "loss": 60.0 * B * T, "adam": 32.0 * lrn.P}
     b = byte_per.get(fam, 0.0)
     achieved = b / per_launch_s / 1e9 if b else 0.0
