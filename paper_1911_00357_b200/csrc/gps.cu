@@ -541,19 +541,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
-  // destinations of this thread's partials: unit j = 128q + 32w + lane is owned by CTA 4q + w
+  // destinations of this thread's partials: unit j = 128q + 32w + lane is owned by CTA 4q + w;
+  // recv is [parity][src CTA][32 units][ustride floats] with ustride = B rounded to 2 / 4 / 8
+  const uint32_t unit_bytes = B <= 2 ? 8u : (B <= 4 ? 16u : 32u);
+  const int ustride = (int)unit_bytes / 4;
   uint32_t dst[4] = {0u, 0u, 0u, 0u}, dbar[4][2] = {{0u, 0u}, {0u, 0u}, {0u, 0u}, {0u, 0u}};
   if (warp < 4) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t owner = (uint32_t)(4 * q + warp);
-      dst[q] = map_to_cta(&sm.recv[0][c][lane][0], owner);
+      dst[q] = map_to_cta(&sm.recv[0][0][0][0] + (c * kUPC + lane) * ustride, owner);
       dbar[q][0] = map_to_cta(&sm.bar[0], owner);
       dbar[q][1] = map_to_cta(&sm.bar[1], owner);
     }
   }
   const uint32_t recv_parity_bytes = (uint32_t)sizeof(sm.recv[0]);
-  const uint32_t unit_bytes = B <= 2 ? 8u : (B <= 4 ? 16u : 32u);
   const uint32_t tx_bytes = (uint32_t)kNC * kUPC * unit_bytes;
   const uint32_t dg_base = smem_u32(sm.dg_tile);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -642,8 +644,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
       const uint32_t off = (uint32_t)par * recv_parity_bytes;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (unit_bytes == 8u) {
-          st_async_v2f(dst[q] + off, __uint_as_float(v[q][0]), __uint_as_float(v[q][1]), dbar[q][par]);
+        if (unit_bytes == 8u) {  // B <= 2: lane pairs send units (l, l+1) as one 16-byte packet
+          const uint32_t n0 = __shfl_down_sync(0xffffffffu, v[q][0], 1);
+          const uint32_t n1 = __shfl_down_sync(0xffffffffu, v[q][1], 1);
+          if ((lane & 1) == 0) st_async_v4(dst[q] + off, make_uint4(v[q][0], v[q][1], n0, n1), dbar[q][par]);
         } else {
           st_async_v4(dst[q] + off, make_uint4(v[q][0], v[q][1], v[q][2], v[q][3]), dbar[q][par]);
           if (unit_bytes == 32u)
@@ -658,7 +662,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
       DDPPO_TRACE_B(c, tid, it, 5);
       float s = 0.f;
 #pragma unroll
-      for (int q = 0; q < kNC; ++q) s += sm.recv[par][q][gu][gb];
+      for (int q = 0; q < kNC; ++q) s += (&sm.recv[par][0][0][0])[(q * kUPC + gu) * ustride + gb];
       carry = smask[gb * T_run + t] * (dzh + s);
     }
     __syncthreads();  // the MMAs of this iteration (done: mma_bar) are the last readers of dg_tile
