@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) 
 constexpr int kBwdThreads = 256;
 constexpr uint32_t kDgSBO = (kRows / 8) * 128;  // 1536 B between 8-row groups of the [16 x 96] tile
 constexpr uint32_t kBwdD0 = 4 * (kRows / 2);    // TMEM columns [0, 192): 4 tiles x 48 packed columns
-constexpr int kBwdTmemCols = 256;
+constexpr int kBwdTmemCols = 512;  // A (192) + 8 accumulators x 16
 // kind::f16, D f32, A bf16, B bf16, K-major, M = 128, N = 16
 constexpr uint32_t kIdescBF16_M128_N16 = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
 
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
   if (tid == 0) {
     mbar_init(&sm.bar[0], 1);
     mbar_init(&sm.bar[1], 1);
-    mbar_init(&sm.mma_bar, 4);
+    mbar_init(&sm.mma_bar, 8);  // one commit per warp
     fence_mbar_init_cluster();
   }
   if (warp == 0) {
@@ -545,15 +545,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
   // recv is [parity][src CTA][32 units][ustride floats] with ustride = B rounded to 2 / 4 / 8
   const uint32_t unit_bytes = B <= 2 ? 8u : (B <= 4 ? 16u : 32u);
   const int ustride = (int)unit_bytes / 4;
-  uint32_t dst[4] = {0u, 0u, 0u, 0u}, dbar[4][2] = {{0u, 0u}, {0u, 0u}, {0u, 0u}, {0u, 0u}};
-  if (warp < 4) {
+  // Warp w reads lane quarter w%4 of tiles q = 2*(w/4), 2*(w/4)+1 (units 128q + 32(w%4) + lane).
+  uint32_t dst[2] = {0u, 0u}, dbar[2][2] = {{0u, 0u}, {0u, 0u}};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t owner = (uint32_t)(4 * q + warp);
-      dst[q] = map_to_cta(&sm.recv[0][0][0][0] + (c * kUPC + lane) * ustride, owner);
-      dbar[q][0] = map_to_cta(&sm.bar[0], owner);
-      dbar[q][1] = map_to_cta(&sm.bar[1], owner);
-    }
+  for (int qi = 0; qi < 2; ++qi) {
+    const int q = 2 * (warp >> 2) + qi;
+    const uint32_t owner = (uint32_t)(4 * q + (warp & 3));
+    dst[qi] = map_to_cta(&sm.recv[0][0][0][0] + (c * kUPC + lane) * ustride, owner);
+    dbar[qi][0] = map_to_cta(&sm.bar[0], owner);
+    dbar[qi][1] = map_to_cta(&sm.bar[1], owner);
   }
   const uint32_t recv_parity_bytes = (uint32_t)sizeof(sm.recv[0]);
   const uint32_t tx_bytes = (uint32_t)kNC * kUPC * unit_bytes;
@@ -610,17 +610,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
     }
     __syncthreads();
     DDPPO_TRACE_B(c, tid, it, 1);
-    if (warp < 4) {
+    {
+      // all 8 warps: warp w issues the 3 K steps 3h..3h+2 (h = w/4) of tile q = w%4 into its own
+      // accumulator D[q][h]; then reads D[q'][0] + D[q'][1] of its lane quarter for 2 tiles q'
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int q_mma = warp & 3, h = warp >> 2;
       const uint64_t bd0 = umma_desc(dg_base, 128, kDgSBO);
-      const uint32_t d_q = tmem + kBwdD0 + 16u * (uint32_t)warp;
+      const uint32_t d_q = tmem + kBwdD0 + 16u * (uint32_t)(2 * q_mma + h);
 #pragma unroll
-      for (int kk = 0; kk < kRows / 16; ++kk) {
+      for (int j = 0; j < 3; ++j) {
+        const int kk = 3 * h + j;
         asm volatile(
             "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_q),
-            "r"(tmem + 48u * (uint32_t)warp + 8u * (uint32_t)kk), "l"(bd0 + (uint64_t)(16 * kk)),
-            "r"(kIdescBF16_M128_N16), "r"((uint32_t)kk)
+            "r"(tmem + 48u * (uint32_t)q_mma + 8u * (uint32_t)kk), "l"(bd0 + (uint64_t)(16 * kk)),
+            "r"(kIdescBF16_M128_N16), "r"((uint32_t)j)
             : "memory");
       }
       asm volatile(
@@ -632,28 +636,45 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
       mbar_wait_parity(&sm.mma_bar, (uint32_t)(it & 1));
       DDPPO_TRACE_B(c, tid, it, 3);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t v[4][8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                     : "=r"(v[q][0]), "=r"(v[q][1]), "=r"(v[q][2]), "=r"(v[q][3]), "=r"(v[q][4]), "=r"(v[q][5]),
-                       "=r"(v[q][6]), "=r"(v[q][7])
-                     : "r"(tmem + ((uint32_t)(warp * 32) << 16) + kBwdD0 + 16u * (uint32_t)q));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + kBwdD0;
       const uint32_t off = (uint32_t)par * recv_parity_bytes;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int qi = 0; qi < 2; ++qi) {
+        const int q = 2 * (warp >> 2) + qi;
+        uint32_t a[8], b[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+                       "=r"(a[7])
+                     : "r"(lane_base + 32u * (uint32_t)q));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]), "=r"(b[4]), "=r"(b[5]), "=r"(b[6]),
+                       "=r"(b[7])
+                     : "r"(lane_base + 32u * (uint32_t)q + 16u));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float s[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] = __uint_as_float(a[e]) + __uint_as_float(b[e]);
         if (unit_bytes == 8u) {  // B <= 2: lane pairs send units (l, l+1) as one 16-byte packet
-          const uint32_t n0 = __shfl_down_sync(0xffffffffu, v[q][0], 1);
-          const uint32_t n1 = __shfl_down_sync(0xffffffffu, v[q][1], 1);
-          if ((lane & 1) == 0) st_async_v4(dst[q] + off, make_uint4(v[q][0], v[q][1], n0, n1), dbar[q][par]);
+          const float n0 = __shfl_down_sync(0xffffffffu, s[0], 1);
+          const float n1 = __shfl_down_sync(0xffffffffu, s[1], 1);
+          if ((lane & 1) == 0)
+            st_async_v4(dst[qi] + off,
+                        make_uint4(__float_as_uint(s[0]), __float_as_uint(s[1]), __float_as_uint(n0),
+                                   __float_as_uint(n1)),
+                        dbar[qi][par]);
         } else {
-          st_async_v4(dst[q] + off, make_uint4(v[q][0], v[q][1], v[q][2], v[q][3]), dbar[q][par]);
+          st_async_v4(dst[qi] + off,
+                      make_uint4(__float_as_uint(s[0]), __float_as_uint(s[1]), __float_as_uint(s[2]),
+                                 __float_as_uint(s[3])),
+                      dbar[qi][par]);
           if (unit_bytes == 32u)
-            st_async_v4(dst[q] + off + 16u, make_uint4(v[q][4], v[q][5], v[q][6], v[q][7]), dbar[q][par]);
+            st_async_v4(dst[qi] + off + 16u,
+                        make_uint4(__float_as_uint(s[4]), __float_as_uint(s[5]), __float_as_uint(s[6]),
+                                   __float_as_uint(s[7])),
+                        dbar[qi][par]);
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     }
     DDPPO_TRACE_B(c, tid, it, 4);
     if (gate_warp) {
