@@ -1,0 +1,186 @@
+"""Visual-encoder layers with manual backward passes (Depth / RGB-D agents, steps a5/a7).
+
+Test infrastructure only.  NumPy float64, NCHW, textbook definitions:
+  * Conv2d without bias (ResNet convention; every conv is followed by GroupNorm),
+    computed as im2col + matmul: y[n,o,i,j] = sum_{c,u,v} W[o,c,u,v] x[n,c,i*s-p+u,j*s-p+v];
+  * GroupNorm ("replace every BatchNorm layer with GroupNorm"; reading Z19:
+    G = 16 groups, eps = 1e-5, per-channel affine): biased variance over (C/G, H, W) per sample;
+  * ReLU; MaxPool 3x3 / stride 2 / pad 1 (Z23) with the first maximum in (u, v) scan order
+    taking the gradient;
+  * half-width ResNet18 ("number of output channels at every layer reduced by half",
+    reading Z23: stem 7x7/2 + maxpool, BasicBlocks 32/64/128/256, stride on the first block of
+    layers 2-4 with a 1x1/stride conv + GN shortcut), then the 3x3 compression conv to 128
+    channels + GN + ReLU (Z20).
+"""
+import numpy as np
+
+
+def _pad(x, p):
+    return np.pad(x, ((0, 0), (0, 0), (p, p), (p, p))) if p else x
+
+
+def im2col(x, kh, kw, s, p):
+    """x [N][C][H][W] -> cols [N*Ho*Wo][C*kh*kw] (column index c*kh*kw + u*kw + v), Ho, Wo."""
+    N, C, H, W = x.shape
+    xp = _pad(x, p)
+    Ho = (H + 2 * p - kh) // s + 1
+    Wo = (W + 2 * p - kw) // s + 1
+    cols = np.empty((N, Ho, Wo, C, kh, kw))
+    for u in range(kh):
+        for v in range(kw):
+            cols[:, :, :, :, u, v] = xp[:, :, u:u + s * Ho:s, v:v + s * Wo:s].transpose(0, 2, 3, 1)
+    return cols.reshape(N * Ho * Wo, C * kh * kw), Ho, Wo
+
+
+def col2im(cols, shape, kh, kw, s, p, Ho, Wo):
+    N, C, H, W = shape
+    xp = np.zeros((N, C, H + 2 * p, W + 2 * p))
+    c6 = cols.reshape(N, Ho, Wo, C, kh, kw)
+    for u in range(kh):
+        for v in range(kw):
+            xp[:, :, u:u + s * Ho:s, v:v + s * Wo:s] += c6[:, :, :, :, u, v].transpose(0, 3, 1, 2)
+    return xp[:, :, p:p + H, p:p + W] if p else xp
+
+
+def conv_fwd(x, W, s, p):
+    N = x.shape[0]
+    O, C, kh, kw = W.shape
+    cols, Ho, Wo = im2col(x, kh, kw, s, p)
+    y = cols @ W.reshape(O, -1).T
+    return y.reshape(N, Ho, Wo, O).transpose(0, 3, 1, 2), (x.shape, cols, Ho, Wo)
+
+
+def conv_bwd(dy, W, s, p, cache):
+    shape, cols, Ho, Wo = cache
+    O, C, kh, kw = W.shape
+    d2 = dy.transpose(0, 2, 3, 1).reshape(-1, O)
+    dW = (d2.T @ cols).reshape(W.shape)
+    dx = col2im(d2 @ W.reshape(O, -1), shape, kh, kw, s, p, Ho, Wo)
+    return dx, dW
+
+
+def gn_fwd(x, gamma, beta, G=16, eps=1e-5):
+    N, C, H, W = x.shape
+    xg = x.reshape(N, G, -1)
+    mu = xg.mean(axis=2, keepdims=True)
+    var = ((xg - mu) ** 2).mean(axis=2, keepdims=True)
+    rstd = 1.0 / np.sqrt(var + eps)
+    xhat = ((xg - mu) * rstd).reshape(N, C, H, W)
+    return xhat * gamma[None, :, None, None] + beta[None, :, None, None], (xhat, rstd, G)
+
+
+def gn_bwd(dy, gamma, cache):
+    xhat, rstd, G = cache
+    N, C, H, W = dy.shape
+    dgamma = (dy * xhat).sum(axis=(0, 2, 3))
+    dbeta = dy.sum(axis=(0, 2, 3))
+    dxhat = (dy * gamma[None, :, None, None]).reshape(N, G, -1)
+    xh = xhat.reshape(N, G, -1)
+    m = dxhat.shape[2]
+    dx = rstd * (dxhat - dxhat.mean(axis=2, keepdims=True) - xh * (dxhat * xh).mean(axis=2, keepdims=True))
+    return dx.reshape(N, C, H, W), dgamma, dbeta
+
+
+def maxpool_fwd(x, k=3, s=2, p=1):
+    N, C, H, W = x.shape
+    xp = np.pad(x, ((0, 0), (0, 0), (p, p), (p, p)), constant_values=-np.inf)
+    Ho = (H + 2 * p - k) // s + 1
+    Wo = (W + 2 * p - k) // s + 1
+    win = np.stack([xp[:, :, u:u + s * Ho:s, v:v + s * Wo:s] for u in range(k) for v in range(k)], axis=-1)
+    arg = win.argmax(axis=-1)  # first maximum in (u, v) scan order
+    return win.max(axis=-1), (x.shape, arg, k, s, p, Ho, Wo)
+
+
+def maxpool_bwd(dy, cache):
+    shape, arg, k, s, p, Ho, Wo = cache
+    N, C, H, W = shape
+    dxp = np.zeros((N, C, H + 2 * p, W + 2 * p))
+    for u in range(k):
+        for v in range(k):
+            sel = (arg == u * k + v)
+            dxp[:, :, u:u + s * Ho:s, v:v + s * Wo:s] += np.where(sel, dy, 0.0)
+    return dxp[:, :, p:p + H, p:p + W]
+
+
+# ---------------------------------------------------------------- half-width ResNet18
+WIDTHS = (32, 64, 128, 256)
+
+
+def resnet18h_spec(in_ch):
+    """Ordered (name, kind, shape, stride, pad) of the encoder's parameter tensors."""
+    spec = [("enc.stem.conv", "conv", (32, in_ch, 7, 7), 2, 3), ("enc.stem.gn", "gn", (32,), 0, 0)]
+    cin = 32
+    for li, c in enumerate(WIDTHS):
+        for bi in range(2):
+            s = 2 if (bi == 0 and li > 0) else 1
+            pre = f"enc.layer{li + 1}.{bi}"
+            spec += [(pre + ".conv1", "conv", (c, cin, 3, 3), s, 1), (pre + ".gn1", "gn", (c,), 0, 0),
+                     (pre + ".conv2", "conv", (c, c, 3, 3), 1, 1), (pre + ".gn2", "gn", (c,), 0, 0)]
+            if s != 1 or cin != c:
+                spec += [(pre + ".down.conv", "conv", (c, cin, 1, 1), s, 0), (pre + ".down.gn", "gn", (c,), 0, 0)]
+            cin = c
+    spec += [("enc.compress.conv", "conv", (128, 256, 3, 3), 1, 1), ("enc.compress.gn", "gn", (128,), 0, 0)]
+    return spec
+
+
+def _conv_gn(x, p, cname, gname, s, pad, relu, caches):
+    y, cc = conv_fwd(x, p[cname + ".weight"], s, pad)
+    z, gc = gn_fwd(y, p[gname + ".weight"], p[gname + ".bias"])
+    caches[cname] = (cc, gc, s, pad)
+    if relu:
+        caches[cname + ".relu"] = z > 0
+        z = np.maximum(z, 0.0)
+    return z
+
+
+def _conv_gn_bwd(dz, p, cname, gname, relu, caches, g):
+    cc, gc, s, pad = caches[cname]
+    if relu:
+        dz = dz * caches[cname + ".relu"]
+    dy, g[gname + ".weight"], g[gname + ".bias"] = gn_bwd(dz, p[gname + ".weight"], gc)
+    dx, g[cname + ".weight"] = conv_bwd(dy, p[cname + ".weight"], s, pad, cc)
+    return dx
+
+
+def resnet18h_fwd(x, p):
+    """x [N][C][64][64] (or larger) -> feature [N][128][h][w] (after compression conv + GN + ReLU)."""
+    caches = {}
+    z = _conv_gn(x, p, "enc.stem.conv", "enc.stem.gn", 2, 3, True, caches)
+    z, caches["pool"] = maxpool_fwd(z)
+    cin = 32
+    for li, c in enumerate(WIDTHS):
+        for bi in range(2):
+            s = 2 if (bi == 0 and li > 0) else 1
+            pre = f"enc.layer{li + 1}.{bi}"
+            a = _conv_gn(z, p, pre + ".conv1", pre + ".gn1", s, 1, True, caches)
+            b = _conv_gn(a, p, pre + ".conv2", pre + ".gn2", 1, 1, False, caches)
+            sc = z
+            if s != 1 or cin != c:
+                sc = _conv_gn(z, p, pre + ".down.conv", pre + ".down.gn", s, 0, False, caches)
+            out = b + sc
+            caches[pre + ".out"] = out > 0
+            z = np.maximum(out, 0.0)
+            cin = c
+    z = _conv_gn(z, p, "enc.compress.conv", "enc.compress.gn", 1, 1, True, caches)
+    return z, caches
+
+
+def resnet18h_bwd(dz, p, caches, g):
+    dz = _conv_gn_bwd(dz, p, "enc.compress.conv", "enc.compress.gn", True, caches, g)
+    blocks = [(li, bi) for li in range(4) for bi in range(2)]
+    for li, bi in reversed(blocks):
+        c = WIDTHS[li]
+        cin = (32 if li == 0 else WIDTHS[li - 1]) if bi == 0 else c
+        s = 2 if (bi == 0 and li > 0) else 1
+        pre = f"enc.layer{li + 1}.{bi}"
+        dout = dz * caches[pre + ".out"]
+        da = _conv_gn_bwd(dout, p, pre + ".conv2", pre + ".gn2", False, caches, g)
+        dx = _conv_gn_bwd(da, p, pre + ".conv1", pre + ".gn1", True, caches, g)
+        if s != 1 or cin != c:
+            dx = dx + _conv_gn_bwd(dout, p, pre + ".down.conv", pre + ".down.gn", False, caches, g)
+        else:
+            dx = dx + dout
+        dz = dx
+    dz = maxpool_bwd(dz, caches["pool"])
+    dx = _conv_gn_bwd(dz, p, "enc.stem.conv", "enc.stem.gn", True, caches, g)
+    return dx

@@ -22,6 +22,9 @@ def minibatch_grad(arch, params, ro, adv, ret, envs, mean_invstd, cfg, hidden=51
     T_run = int(L.max())
     batch = {"goal": ro["goal"][envs, :T_run], "prev_action": ro["prev_action"][envs, :T_run],
              "mask": ro["mask"][envs, :T_run], "h0": ro["h0"][envs]}
+    if "obs" in ro:
+        batch["obs"] = ro["obs"][envs, :T_run]
+        batch["c0"] = ro["c0"][envs]
     logits, values, cache = models.forward(arch, params, batch, hidden=hidden)
     B = len(envs)
     valid = (np.arange(T_run)[None, :] < L[:, None])

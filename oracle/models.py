@@ -15,10 +15,16 @@ Architectures (BASELINE.json configs; readings Z17-Z22):
                      -> Linear(512, A+1) ("fully connected layer,
                      resulting in a soft-max distribution ... and an estimate
                      of the value function").
+  depth (configs[2]): depth [1][64][64] -> half-width ResNet18 (convnets.py)
+                     -> 128x2x2 -> flatten (c, h, w order) -> Linear(512, 512) + ReLU
+                     (Z17, Z20); x = [visual 512, goal_fc 32, act_emb 32]
+                     -> LSTM(576, 512) (PyTorch i, f, g, o) -> Linear(512, A+1).
+fan_in > 0: U(+-1/sqrt(fan_in)) default init; fan_in == 0: ones (GN gamma);
+fan_in < 0: zeros (GN beta).
 """
 import numpy as np
 
-from . import nets
+from . import convnets, nets
 
 NUM_ACTIONS = 4
 
@@ -37,6 +43,20 @@ def layout(arch, hidden=512, num_actions=NUM_ACTIONS):
                 ("rnn.weight_ih", (G, 64), H), ("rnn.weight_hh", (G, H), H),
                 ("rnn.bias_ih", (G,), H), ("rnn.bias_hh", (G,), H),
                 ("head.weight", (A1, H), H), ("head.bias", (A1,), H)]
+    if arch == "depth":
+        H, G = hidden, 4 * hidden
+        out = []
+        for name, kind, shape, _, _ in convnets.resnet18h_spec(1):
+            if kind == "conv":
+                out.append((name + ".weight", shape, shape[1] * shape[2] * shape[3]))
+            else:
+                out += [(name + ".weight", shape, 0), (name + ".bias", shape, -1)]
+        return out + [("visual_fc.weight", (512, 512), 512), ("visual_fc.bias", (512,), 512),
+                      ("goal_fc.weight", (32, 3), 3), ("goal_fc.bias", (32,), 3),
+                      ("act_embed.weight", (A1, 32), 1),
+                      ("rnn.weight_ih", (G, 576), H), ("rnn.weight_hh", (G, H), H),
+                      ("rnn.bias_ih", (G,), H), ("rnn.bias_hh", (G,), H),
+                      ("head.weight", (A1, H), H), ("head.bias", (A1,), H)]
     raise ValueError(arch)
 
 
@@ -86,6 +106,24 @@ def forward(arch, flat, batch, **kw):
                                  p["rnn.weight_ih"], p["rnn.weight_hh"], p["rnn.bias_ih"], p["rnn.bias_hh"])
         out = nets.linear_fwd(h, p["head.weight"], p["head.bias"])
         cache = {"goal": goal, "prev_action": np.asarray(batch["prev_action"]), "h": h, "rnn": rc}
+    elif arch == "depth":
+        obs = np.asarray(batch["obs"], dtype=np.float64)  # [B][T][1][H][W]
+        B, T = obs.shape[:2]
+        feat, ec = convnets.resnet18h_fwd(obs.reshape((B * T,) + obs.shape[2:]), p)
+        flat_f = feat.reshape(B, T, -1)  # (c, h, w) order
+        vpre = nets.linear_fwd(flat_f, p["visual_fc.weight"], p["visual_fc.bias"])
+        vis = np.maximum(vpre, 0.0)
+        ge = nets.linear_fwd(goal, p["goal_fc.weight"], p["goal_fc.bias"])
+        ae = nets.embedding_fwd(batch["prev_action"], p["act_embed.weight"])
+        x = np.concatenate([vis, ge, ae], axis=-1)
+        H = p["rnn.weight_hh"].shape[1]
+        c0 = np.asarray(batch.get("c0", np.zeros((B, H))), dtype=np.float64)
+        h, rc = nets.lstm_seq_fwd(x, np.asarray(batch["mask"], dtype=np.float64),
+                                  np.asarray(batch["h0"], dtype=np.float64), c0,
+                                  p["rnn.weight_ih"], p["rnn.weight_hh"], p["rnn.bias_ih"], p["rnn.bias_hh"])
+        out = nets.linear_fwd(h, p["head.weight"], p["head.bias"])
+        cache = {"goal": goal, "prev_action": np.asarray(batch["prev_action"]), "h": h, "rnn": rc, "enc": ec,
+                 "feat_shape": feat.shape, "flat": flat_f, "vis": vis}
     else:
         raise ValueError(arch)
     return out[..., :-1], out[..., -1], cache
@@ -107,6 +145,17 @@ def backward(arch, flat, cache, dlogits, dvalues, **kw):
         dge, dae = dx[..., :32], dx[..., 32:]
         _, g["goal_fc.weight"], g["goal_fc.bias"] = nets.linear_bwd(cache["goal"], p["goal_fc.weight"], dge)
         g["act_embed.weight"] = nets.embedding_bwd(cache["prev_action"], dae, p["act_embed.weight"].shape[0])
+    elif arch == "depth":
+        dh, g["head.weight"], g["head.bias"] = nets.linear_bwd(cache["h"], p["head.weight"], dout)
+        dx, g["rnn.weight_ih"], g["rnn.weight_hh"], g["rnn.bias_ih"], g["rnn.bias_hh"] = \
+            nets.lstm_seq_bwd(dh, cache["rnn"], p["rnn.weight_ih"], p["rnn.weight_hh"])
+        dvis, dge, dae = dx[..., :512], dx[..., 512:544], dx[..., 544:]
+        _, g["goal_fc.weight"], g["goal_fc.bias"] = nets.linear_bwd(cache["goal"], p["goal_fc.weight"], dge)
+        g["act_embed.weight"] = nets.embedding_bwd(cache["prev_action"], dae, p["act_embed.weight"].shape[0])
+        dvpre = dvis * (cache["vis"] > 0)
+        dflat, g["visual_fc.weight"], g["visual_fc.bias"] = nets.linear_bwd(cache["flat"], p["visual_fc.weight"],
+                                                                            dvpre)
+        convnets.resnet18h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
     else:
         raise ValueError(arch)
     return pack(arch, g, **kw)

@@ -33,7 +33,24 @@ CONFIGS = {
     "toy": dict(arch="toy", E=2, T=4, epochs=1, minibatches=1, hidden=64),
     "gps": dict(arch="gps", E=4, T=128, epochs=2, minibatches=2, hidden=512),
     "stress_gps": dict(arch="gps", E=16, T=128, epochs=2, minibatches=2, hidden=512),
+    "depth": dict(arch="depth", E=4, T=128, epochs=2, minibatches=2, hidden=512, obs=(1, 64, 64)),
 }
+
+
+def depth_frames(rng, E, T, C=1, H=64, W=64):
+    """Smooth depth-like frames in [0, 1]: 3 seeded low-frequency cosine fields drifting over time
+    plus 5 % noise (DESIGN.md input recipe)."""
+    yy, xx = np.meshgrid(np.linspace(0, 1, H), np.linspace(0, 1, W), indexing="ij")
+    out = np.empty((E, T, C, H, W), np.float32)
+    for n in range(E):
+        k = rng.uniform(0.5, 3.0, (3, 2))
+        ph = rng.uniform(0, 2 * np.pi, 3)
+        drift = rng.uniform(-0.05, 0.05, 3)
+        for t in range(T):
+            f = sum(np.cos(2 * np.pi * (k[i, 0] * xx + k[i, 1] * yy) + ph[i] + drift[i] * t) for i in range(3))
+            f = 0.5 + f / 6.0 + 0.05 * rng.standard_normal((H, W))
+            out[n, t] = np.clip(f, 0.0, 1.0)[None].astype(np.float32).repeat(C, axis=0)
+    return out
 
 
 def ld_for(T):
@@ -45,8 +62,9 @@ def _rng(seed, *keys):
     return np.random.Generator(np.random.Philox(ss))
 
 
-def rollout(E, T, seed, rank=0, iteration=0, length=None, hidden=512, ld=None):
-    """One rank's rollout.  `length` (int or [E]) truncates (preemption); default T."""
+def rollout(E, T, seed, rank=0, iteration=0, length=None, hidden=512, ld=None, obs_shape=None):
+    """One rank's rollout.  `length` (int or [E]) truncates (preemption); default T.
+    obs_shape (C, H, W) adds depth-like frames `obs` [E][T][C][H][W] and an LSTM cell state `c0`."""
     ld = ld or ld_for(T)
     rng = _rng(seed, 1, rank, iteration)
     f32 = np.float32
@@ -128,17 +146,28 @@ def rollout(E, T, seed, rank=0, iteration=0, length=None, hidden=512, ld=None):
         val[n, L + 1:] = 0
         goal[n, L:] = 0
     h0 = rng.normal(0.0, 0.1, (E, hidden)).astype(f32)
-    return dict(rew=rew, val=val, done=done, length=length, goal=goal, prev_action=prev_action,
-                mask=mask, action=action, logp_old=logp_old, h0=h0, E=E, T=T, ld=ld)
+    out = dict(rew=rew, val=val, done=done, length=length, goal=goal, prev_action=prev_action,
+               mask=mask, action=action, logp_old=logp_old, h0=h0, E=E, T=T, ld=ld)
+    if obs_shape is not None:
+        obs = depth_frames(_rng(seed, 6, rank, iteration), E, T, *obs_shape)
+        for n in range(E):
+            obs[n, int(length[n]):] = 0
+        out["obs"] = obs
+        out["c0"] = rng.normal(0.0, 0.1, (E, hidden)).astype(f32)
+    return out
 
 
 def init_params(entries, P, seed):
-    """entries: [(offset, numel, fan_in)] -> fp32 [P]; U(-1/sqrt(fan_in), 1/sqrt(fan_in)) (torch default)."""
+    """entries: [(offset, numel, fan_in)] -> fp32 [P]; fan_in > 0: U(-1/sqrt(fan_in), 1/sqrt(fan_in))
+    (torch default), fan_in == 0: ones (GroupNorm gamma), fan_in < 0: zeros (GroupNorm beta)."""
     rng = _rng(seed, 2)
     out = np.zeros(P, np.float32)
     for off, n, fan_in in entries:
-        k = 1.0 / np.sqrt(fan_in)
-        out[off:off + n] = rng.uniform(-k, k, n).astype(np.float32)
+        if fan_in > 0:
+            k = 1.0 / np.sqrt(fan_in)
+            out[off:off + n] = rng.uniform(-k, k, n).astype(np.float32)
+        elif fan_in == 0:
+            out[off:off + n] = 1.0
     return out
 
 

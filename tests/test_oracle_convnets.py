@@ -1,0 +1,172 @@
+"""Pins for oracle.convnets and the Depth model (steps a5/a7 for configs[2]):
+torch.nn.functional fp64 forward + autograd for every layer, special-case identities, and finite
+differences through the whole Depth actor-critic."""
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import synth
+from oracle import convnets, models, ppo
+
+
+def _t(a, grad=False):
+    t = torch.tensor(np.asarray(a, dtype=np.float64))
+    return t.requires_grad_(grad)
+
+
+@pytest.mark.parametrize("k,s,p", [(3, 1, 1), (3, 2, 1), (1, 2, 0), (7, 2, 3), (1, 1, 0)])
+def test_conv_matches_torch(k, s, p):
+    rng = np.random.default_rng(k * 10 + s)
+    x = rng.normal(size=(2, 3, 9, 10))
+    W = rng.normal(size=(4, 3, k, k))
+    y, cache = convnets.conv_fwd(x, W, s, p)
+    xt, Wt = _t(x, True), _t(W, True)
+    yt = F.conv2d(xt, Wt, stride=s, padding=p)
+    assert np.max(np.abs(y - yt.detach().numpy())) < 1e-12
+    dy = rng.normal(size=y.shape)
+    (yt * _t(dy)).sum().backward()
+    dx, dW = convnets.conv_bwd(dy, W, s, p, cache)
+    assert np.max(np.abs(dx - xt.grad.numpy())) < 1e-12
+    assert np.max(np.abs(dW - Wt.grad.numpy())) < 1e-12
+
+
+def test_1x1_conv_is_gemm():
+    rng = np.random.default_rng(0)
+    x = rng.normal(size=(2, 5, 4, 4))
+    W = rng.normal(size=(3, 5, 1, 1))
+    y, _ = convnets.conv_fwd(x, W, 1, 0)
+    ref = np.einsum("oc,nchw->nohw", W[:, :, 0, 0], x)
+    assert np.max(np.abs(y - ref)) < 1e-12
+
+
+@pytest.mark.parametrize("G", [1, 4, 16])
+def test_groupnorm_matches_torch(G):
+    rng = np.random.default_rng(G)
+    x = rng.normal(size=(3, 16, 5, 6)) * 3 + 1
+    gamma, beta = rng.normal(size=16), rng.normal(size=16)
+    y, cache = convnets.gn_fwd(x, gamma, beta, G)
+    xt, gt, bt = _t(x, True), _t(gamma, True), _t(beta, True)
+    yt = F.group_norm(xt, G, gt, bt, eps=1e-5)
+    assert np.max(np.abs(y - yt.detach().numpy())) < 1e-12
+    dy = rng.normal(size=y.shape)
+    (yt * _t(dy)).sum().backward()
+    dx, dg, db = convnets.gn_bwd(dy, gamma, cache)
+    for mine, ref in ((dx, xt.grad), (dg, gt.grad), (db, bt.grad)):
+        assert np.max(np.abs(mine - ref.numpy())) < 1e-11
+
+
+def test_groupnorm_special_cases():
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(2, 8, 3, 3))
+    one, zero = np.ones(8), np.zeros(8)
+    y_in, _ = convnets.gn_fwd(x, one, zero, G=8)  # G = C: instance norm
+    m = x.mean(axis=(2, 3), keepdims=True)
+    v = x.var(axis=(2, 3), keepdims=True)
+    assert np.max(np.abs(y_in - (x - m) / np.sqrt(v + 1e-5))) < 1e-12
+    y_ln, _ = convnets.gn_fwd(x, one, zero, G=1)  # G = 1: layer norm over (C, H, W)
+    m = x.mean(axis=(1, 2, 3), keepdims=True)
+    v = x.var(axis=(1, 2, 3), keepdims=True)
+    assert np.max(np.abs(y_ln - (x - m) / np.sqrt(v + 1e-5))) < 1e-12
+
+
+def test_maxpool_matches_torch_including_ties():
+    rng = np.random.default_rng(2)
+    x = np.maximum(rng.normal(size=(2, 3, 9, 8)), 0.0)  # ReLU zeros create ties
+    y, cache = convnets.maxpool_fwd(x)
+    xt = _t(x, True)
+    yt = F.max_pool2d(xt, 3, 2, 1)
+    assert np.max(np.abs(y - yt.detach().numpy())) < 1e-15
+    dy = rng.normal(size=y.shape)
+    (yt * _t(dy)).sum().backward()
+    assert np.max(np.abs(convnets.maxpool_bwd(dy, cache) - xt.grad.numpy())) < 1e-12
+
+
+class _TorchR18H(torch.nn.Module):
+    """Independent torch.nn construction of the half-width ResNet18 (test-only reference)."""
+
+    def __init__(self, p):
+        super().__init__()
+        self.p = p
+
+    def forward(self, x):
+        p = self.p
+
+        def cg(z, c, g, s, pad, relu):
+            z = F.conv2d(z, p[c + ".weight"], stride=s, padding=pad)
+            z = F.group_norm(z, 16, p[g + ".weight"], p[g + ".bias"], eps=1e-5)
+            return F.relu(z) if relu else z
+        z = cg(x, "enc.stem.conv", "enc.stem.gn", 2, 3, True)
+        z = F.max_pool2d(z, 3, 2, 1)
+        cin = 32
+        for li, c in enumerate(convnets.WIDTHS):
+            for bi in range(2):
+                s = 2 if (bi == 0 and li > 0) else 1
+                pre = f"enc.layer{li + 1}.{bi}"
+                a = cg(z, pre + ".conv1", pre + ".gn1", s, 1, True)
+                b = cg(a, pre + ".conv2", pre + ".gn2", 1, 1, False)
+                sc = cg(z, pre + ".down.conv", pre + ".down.gn", s, 0, False) if (s != 1 or cin != c) else z
+                z = F.relu(b + sc)
+                cin = c
+        return cg(z, "enc.compress.conv", "enc.compress.gn", 1, 1, True)
+
+
+def test_resnet18h_matches_torch():
+    lay = models.layout("depth")
+    offs, P = models.offsets("depth")
+    ent = [(offs[n][0], int(np.prod(s)), f) for n, s, f in lay]
+    flat = synth.init_params(ent, P, 3).astype(np.float64)
+    rng = np.random.default_rng(4)
+    flat += rng.normal(0, 0.05, P) * (np.array([1.0]))  # perturb GN affine away from (1, 0)
+    p = models.unpack("depth", flat)
+    x = synth.depth_frames(rng, 1, 2)[0].astype(np.float64)  # [2][1][64][64]
+    feat, caches = convnets.resnet18h_fwd(x, p)
+    assert feat.shape == (2, 128, 2, 2)
+    pt = {k: _t(v, True) for k, v in p.items() if k.startswith("enc.")}
+    xt = _t(x, True)
+    ft = _TorchR18H(pt)(xt)
+    assert np.max(np.abs(feat - ft.detach().numpy())) < 1e-10
+    dz = rng.normal(size=feat.shape)
+    (ft * _t(dz)).sum().backward()
+    g = {}
+    dx = convnets.resnet18h_bwd(dz, p, caches, g)
+    assert np.max(np.abs(dx - xt.grad.numpy())) < 1e-9
+    for k, v in pt.items():
+        assert np.max(np.abs(g[k] - v.grad.numpy())) < 1e-9 * max(1.0, np.abs(v.grad.numpy()).max()), k
+
+
+def test_depth_layout_size():
+    assert models.offsets("depth")[1] == 5588741
+
+
+def test_depth_model_finite_differences():
+    lay = models.layout("depth")
+    offs, P = models.offsets("depth")
+    ent = [(offs[n][0], int(np.prod(s)), f) for n, s, f in lay]
+    flat = synth.init_params(ent, P, 5).astype(np.float64)
+    ro = synth.rollout(1, 3, 5, obs_shape=(1, 64, 64))
+    batch = {k: ro[k][:, :3] for k in ("goal", "prev_action", "mask")}
+    batch.update(obs=ro["obs"], h0=ro["h0"], c0=ro["c0"])
+    lin = {k: v.astype(np.float64) if v.dtype != np.int32 else v for k, v in synth.random_loss_inputs(3, 6).items()}
+
+    def loss(fl):
+        lg, v, cache = models.forward("depth", fl, batch)
+        st, dl, dv = ppo.loss_and_grad(lg.reshape(3, -1), v.reshape(-1), lin["actions"], lin["logp_old"],
+                                       lin["values_old"], lin["returns"], lin["adv"], np.ones(3, bool))
+        return st["total"], cache, dl.reshape(1, 3, -1), dv.reshape(1, 3)
+
+    L, cache, dl, dv = loss(flat)
+    g = models.backward("depth", flat, cache, dl, dv)
+    rng = np.random.default_rng(7)
+    names = ["enc.stem.conv.weight", "enc.layer2.0.down.conv.weight", "enc.layer4.1.gn2.weight",
+             "enc.compress.conv.weight", "visual_fc.weight", "rnn.weight_ih", "rnn.weight_hh", "goal_fc.weight"]
+    for name in names:
+        o, s = offs[name]
+        for i in rng.choice(int(np.prod(s)), 3, replace=False):
+            fp, fm = flat.copy(), flat.copy()
+            fp[o + i] += 1e-7
+            fm[o + i] -= 1e-7
+            fd = (loss(fp)[0] - loss(fm)[0]) / 2e-7
+            # ReLU / max-pool kinks can sit inside the stencil: 1e-4 relative (the exact layer-by-layer
+            # pins are the torch.autograd cross-checks above)
+            assert abs(fd - g[o + i]) < 1e-4 * max(abs(fd), 1e-3), (name, i, fd, g[o + i])
