@@ -88,19 +88,29 @@ ddppo_status ddppo_adv_norm(ddppo_ctx* ctx, double* stats3, float eps, float* me
  *   DDPPO_ARCH_TOY_MLP : goal -> Linear(3,64) -> tanh -> Linear(64, A+1)        (configs[0])
  *   DDPPO_ARCH_GPS_GRU : goal -> Linear(3,32); Embedding(A+1,32); x = [goal, act] ->
  *                        GRU(64, hidden=512) -> Linear(hidden, A+1)              (configs[1])
+ *   DDPPO_ARCH_DEPTH_R18_LSTM : depth [1][64][64] -> half-width ResNet18 with GroupNorm(16)
+ *                         -> 128x2x2 -> flatten (c,h,w) -> Linear(512,512)+ReLU;
+ *                        x = [visual, Linear(3,32)(goal), Embedding(A+1,32)] -> LSTM(576,
+ *                        hidden=512) -> Linear(hidden, A+1)                      (configs[2])
  * Flat parameter layout: the tensors below in this order, row-major, each starting at an
  * offset rounded up to a multiple of 4 floats (PyTorch shapes/conventions):
  *   TOY: fc1.weight[64][3] fc1.bias[64] head.weight[A+1][64] head.bias[A+1]
  *   GPS: goal_fc.weight[32][3] goal_fc.bias[32] act_embed.weight[A+1][32]
  *        rnn.weight_ih[3H][64] rnn.weight_hh[3H][H] rnn.bias_ih[3H] rnn.bias_hh[3H]
  *        head.weight[A+1][H] head.bias[A+1]           (GRU gate rows r, z, n)
+ *   DEPTH: the encoder (enc.stem.conv.weight[32][1][7][7], enc.stem.gn.{weight,bias}[32], then
+ *        per residual block enc.layer{1..4}.{0,1}.{conv1,gn1,conv2,gn2[,down.conv,down.gn]},
+ *        enc.compress.conv.weight[128][256][3][3], enc.compress.gn.*; widths 32/64/128/256,
+ *        conv weights [Co][Ci][k][k]), visual_fc.weight[512][512] visual_fc.bias[512],
+ *        goal_fc.*, act_embed.weight[A+1][32], rnn.weight_ih[4H][576] rnn.weight_hh[4H][H]
+ *        rnn.bias_ih[4H] rnn.bias_hh[4H] head.*       (LSTM gate rows i, f, g, o)
  * head rows 0..A-1 are the action logits, row A the value.  num_actions must be 4;
  * GPS requires hidden == 512. */
-typedef enum { DDPPO_ARCH_TOY_MLP = 0, DDPPO_ARCH_GPS_GRU = 1 } ddppo_arch;
+typedef enum { DDPPO_ARCH_TOY_MLP = 0, DDPPO_ARCH_GPS_GRU = 1, DDPPO_ARCH_DEPTH_R18_LSTM = 2 } ddppo_arch;
 
 typedef struct {
   int32_t arch;        /* ddppo_arch */
-  int32_t hidden;      /* 64 (toy) / 512 (gps) */
+  int32_t hidden;      /* 64 (toy) / 512 (gps, depth) */
   int32_t num_actions; /* 4 */
   int32_t reserved[5];
 } ddppo_model_desc;
@@ -134,6 +144,8 @@ typedef struct {
   int32_t E, T, ld, B;
   int32_t T_run;              /* steps to run: max len over the minibatch (host value)  */
   int32_t n_valid;            /* sum over the B envs of min(len, T_run) (host value)    */
+  const float* obs;           /* [E][T][1][64][64] depth frames (DEPTH only, else NULL) */
+  const float* c0;            /* [E][hidden] LSTM cell state before step 0 (DEPTH only)   */
 } ddppo_batch;
 
 /* a5: logits [B][T_run][A], values [B][T_run]; saves activations in ws for the backward. */
@@ -230,6 +242,8 @@ typedef struct {
   const int32_t* host_len;    /* [E] host copy of len */
   const int32_t* host_perms;  /* [epochs][E] host copy of perms */
   int32_t E, T, ld;
+  const float* obs;           /* [E][T][1][64][64] (DEPTH only, else NULL) */
+  const float* c0;            /* [E][hidden]       (DEPTH only, else NULL) */
 } ddppo_rollout;
 
 typedef struct {
@@ -266,10 +280,40 @@ ddppo_status ddppo_profile_read(ddppo_ctx* ctx, double* host_ms /* [DDPPO_K_COUN
 
 /* Diagnostic entry to the tcgen05 GEMM used inside the backward (stream-ordered):
  * C[m][n] = sum_k A[m*sam + k*sak] * B[n*sbn + k*sbk]; operands rounded to bf16, fp32 accumulate
- * in TMEM.  C is row-major with leading dimension ldc.  Used by the tests to pin the kernel. */
+ * in TMEM.  C is row-major with leading dimension ldc.  splits > 1 splits K over CTAs (needs
+ * `partial`, splits*M*N floats; partials summed in split order).  prec = 1: bf16 operands;
+ * prec = 3: each operand split x = hi + lo (both bf16) and C = hi*hi + hi*lo + lo*hi (~fp32
+ * accuracy, used by the Depth encoder's forward).  Used by the tests. */
 ddppo_status ddppo_debug_gemm_bf16(ddppo_ctx* ctx, const float* A, int64_t sam, int64_t sak,
                                    const float* B, int64_t sbn, int64_t sbk, float* C, int64_t ldc,
-                                   int M, int N, int K, void* stream);
+                                   int M, int N, int K, int splits, float* partial, int prec, void* stream);
+
+/* Diagnostic entries to the Depth encoder's layers (stream-ordered; used by the tests).  All
+ * activations NHWC fp32; conv weights PyTorch [Co][Ci][k][k].
+ * conv2d: y[F][Ho][Wo][Co] = conv(x[F][H][W][Ci], w) (stride s, zero padding p; bf16x3 operands)
+ *   if y != NULL; if dy != NULL: dw = weight gradient, dx = input gradient (dx nullable), bf16
+ *   operands.  scratch == NULL: only *host_need (bytes) is written. */
+ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const float* w, int F, int H, int W,
+                                int Ci, int Co, int k, int s, int p, float* y, const float* dy,
+                                float* dx, float* dw, void* scratch, size_t scratch_bytes,
+                                size_t* host_need, void* stream);
+/* GroupNorm(16 groups, eps 1e-5) over y[F][HW][C]: z = (relu)(gamma*yhat + beta (+ residual)),
+ * stats[F][16][2] = (mean, rstd); if dz != NULL: dy, dgamma, dbeta (scratch: F*HW*C + 64*C floats). */
+ddppo_status ddppo_debug_groupnorm(ddppo_ctx* ctx, const float* y, const float* gamma, const float* beta,
+                                   const float* residual, int F, int HW, int C, int relu, float* z,
+                                   float* stats, const float* dz, float* dy, float* dgamma,
+                                   float* dbeta, float* scratch, void* stream);
+/* The Depth forward's discrete decisions, read from the workspace of the last ddppo_policy_fwd on
+ * the same batch (bytes, NHWC): stem ReLU mask [F][32][32][32], max-pool argmax [F][16][16][32]
+ * (window index 0..8), then per residual block (layer1.0 ... layer4.1) the conv1 ReLU mask and the
+ * block-output ReLU mask, then the compression ReLU mask [F][2][2][128] and the visual-FC ReLU
+ * mask [F][512]; F = B*T_run.  out == NULL: only *host_n.  Lets a parity test hand the oracle's
+ * backward the same decisions where a pre-activation sits within rounding of 0. */
+ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_batch* host_batch, void* ws,
+                                         uint8_t* out, int64_t cap, int64_t* host_n, void* stream);
+/* 3x3 / stride 2 / pad 1 max pool (first maximum in window order; arg = window index 0..8). */
+ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int F, int H, int W, int C, float* y,
+                                 uint8_t* arg, const float* dy, float* dx, void* stream);
 
 #ifdef __cplusplus
 }

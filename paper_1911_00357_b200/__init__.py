@@ -8,7 +8,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import (ARCH_GPS, ARCH_TOY, AdamCfg, Batch, DdppoError, LearnerCfg, LossCfg, LossInputs, ModelDesc,
+from ._lib import (ARCH_DEPTH, ARCH_GPS, ARCH_TOY, AdamCfg, Batch, DdppoError, LearnerCfg, LossCfg, LossInputs, ModelDesc,
                    PreemptCfg, Rollout, TensorInfo, check, dptr, f32, f64, i32, lib, u8)
 
 __all__ = ["Context", "model_desc", "param_layout", "ddppo_gae", "ddppo_adv_norm", "ddppo_policy_fwd",
@@ -25,7 +25,7 @@ def _stream(stream):
 
 
 def model_desc(arch, hidden=None, num_actions=4):
-    arch_id = {"toy": ARCH_TOY, "gps": ARCH_GPS}.get(arch, arch)
+    arch_id = {"toy": ARCH_TOY, "gps": ARCH_GPS, "depth": ARCH_DEPTH}.get(arch, arch)
     if hidden is None:
         hidden = 64 if arch_id == ARCH_TOY else 512
     d = ModelDesc()
@@ -108,12 +108,14 @@ def ddppo_adv_norm(ctx, stats3, eps, mean_invstd, stream=None):
     _call(ctx, "ddppo_adv_norm", f64(stats3), eps, f32(mean_invstd), _stream(stream))
 
 
-def make_batch(goal, prev_action, mask, h0, length, env_idx, E, T, ld, B, T_run, n_valid):
+def make_batch(goal, prev_action, mask, h0, length, env_idx, E, T, ld, B, T_run, n_valid, obs=None, c0=None):
     b = Batch()
     b.goal, b.prev_action, b.mask, b.h0 = f32(goal), i32(prev_action), f32(mask), f32(h0)
     b.len, b.env_idx = i32(length), i32(env_idx)
     b.E, b.T, b.ld, b.B, b.T_run, b.n_valid = E, T, ld, B, T_run, n_valid
-    b._keep = (goal, prev_action, mask, h0, length, env_idx)  # the struct holds raw device pointers
+    b.obs = f32(obs) if obs is not None else None
+    b.c0 = f32(c0) if c0 is not None else None
+    b._keep = (goal, prev_action, mask, h0, length, env_idx, obs, c0)  # the struct holds raw device pointers
     return b
 
 
@@ -197,9 +199,47 @@ def learner_cfg(epochs=2, minibatches=2, gamma=0.99, tau=0.95, normalize_adv=Tru
     return c
 
 
-def ddppo_debug_gemm_bf16(ctx, A, sam, sak, B, sbn, sbk, C, ldc, M, N, K, stream=None):
+def ddppo_debug_gemm_bf16(ctx, A, sam, sak, B, sbn, sbk, C, ldc, M, N, K, splits=1, partial=None, prec=1,
+                          stream=None):
     """C[m][n] = sum_k A(m,k) B(n,k) on the tcgen05 path (A, B, C fp32 CUDA tensors; strides in elements)."""
-    _call(ctx, "ddppo_debug_gemm_bf16", f32(A), sam, sak, f32(B), sbn, sbk, f32(C), ldc, M, N, K, _stream(stream))
+    _call(ctx, "ddppo_debug_gemm_bf16", f32(A), sam, sak, f32(B), sbn, sbk, f32(C), ldc, M, N, K, splits,
+          f32(partial), prec, _stream(stream))
+
+
+def ddppo_debug_conv2d(ctx, x, w, F, H, W, Ci, Co, k, s, p, y=None, dy=None, dx=None, dw=None, stream=None):
+    """Depth encoder convolution (NHWC activations, [Co][Ci][k][k] weights) on the tcgen05 path."""
+    import torch
+    need = ctypes.c_size_t()
+    args = (f32(x), f32(w), F, H, W, Ci, Co, k, s, p, f32(y), f32(dy), f32(dx), f32(dw))
+    _call(ctx, "ddppo_debug_conv2d", *args, None, 0, ctypes.byref(need), _stream(stream))
+    scratch = torch.empty(need.value // 4 + 64, dtype=torch.float32, device=x.device)
+    _call(ctx, "ddppo_debug_conv2d", *args, f32(scratch), scratch.numel() * 4, None, _stream(stream))
+    return scratch  # keep alive until the stream has run
+
+
+def ddppo_debug_groupnorm(ctx, y, gamma, beta, F, HW, C, relu, z, stats, residual=None, dz=None, dy=None,
+                          dgamma=None, dbeta=None, stream=None):
+    import torch
+    scratch = torch.empty(F * HW * C + 64 * C, dtype=torch.float32, device=y.device)
+    _call(ctx, "ddppo_debug_groupnorm", f32(y), f32(gamma), f32(beta), f32(residual), F, HW, C, int(relu), f32(z),
+          f32(stats), f32(dz), f32(dy), f32(dgamma), f32(dbeta), f32(scratch), _stream(stream))
+    return scratch
+
+
+def ddppo_debug_depth_decisions(ctx, batch, ws, stream=None):
+    """uint8 CUDA tensor of the Depth forward's ReLU masks / max-pool argmax (include/ddppo.h order)."""
+    import torch
+    n = ctypes.c_int64()
+    _call(ctx, "ddppo_debug_depth_decisions", ctypes.byref(batch), dptr(ws), None, 0, ctypes.byref(n),
+          _stream(stream))
+    out = torch.zeros(n.value, dtype=torch.uint8, device=ws.device)
+    _call(ctx, "ddppo_debug_depth_decisions", ctypes.byref(batch), dptr(ws), u8(out), n.value, None,
+          _stream(stream))
+    return out
+
+
+def ddppo_debug_maxpool(ctx, x, F, H, W, C, y, arg, dy=None, dx=None, stream=None):
+    _call(ctx, "ddppo_debug_maxpool", f32(x), F, H, W, C, f32(y), u8(arg), f32(dy), f32(dx), _stream(stream))
 
 
 def profile_enable(ctx, on=True):

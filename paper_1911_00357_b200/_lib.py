@@ -21,7 +21,7 @@ c_int, c_float, c_double, c_vp, c_i64 = ctypes.c_int, ctypes.c_float, ctypes.c_d
 c_i32, c_size = ctypes.c_int32, ctypes.c_size_t
 
 STATUS = {0: "ok", 1: "config", 2: "numerical", 3: "protocol", 4: "comm", 5: "cuda", 6: "unsupported"}
-ARCH_TOY, ARCH_GPS = 0, 1
+ARCH_TOY, ARCH_GPS, ARCH_DEPTH = 0, 1, 2
 
 
 class DdppoError(RuntimeError):
@@ -42,7 +42,7 @@ class TensorInfo(ctypes.Structure):
 class Batch(ctypes.Structure):
     _fields_ = [("goal", c_vp), ("prev_action", c_vp), ("mask", c_vp), ("h0", c_vp), ("len", c_vp),
                 ("env_idx", c_vp), ("E", c_i32), ("T", c_i32), ("ld", c_i32), ("B", c_i32), ("T_run", c_i32),
-                ("n_valid", c_i32)]
+                ("n_valid", c_i32), ("obs", c_vp), ("c0", c_vp)]
 
 
 class LossInputs(ctypes.Structure):
@@ -66,7 +66,8 @@ class PreemptCfg(ctypes.Structure):
 class Rollout(ctypes.Structure):
     _fields_ = [("rew", c_vp), ("val", c_vp), ("done", c_vp), ("len", c_vp), ("goal", c_vp), ("prev_action", c_vp),
                 ("mask", c_vp), ("h0", c_vp), ("action", c_vp), ("logp_old", c_vp), ("perms", c_vp),
-                ("host_len", c_vp), ("host_perms", c_vp), ("E", c_i32), ("T", c_i32), ("ld", c_i32)]
+                ("host_len", c_vp), ("host_perms", c_vp), ("E", c_i32), ("T", c_i32), ("ld", c_i32),
+                ("obs", c_vp), ("c0", c_vp)]
 
 
 class LearnerCfg(ctypes.Structure):
@@ -104,7 +105,13 @@ _SIGS = {
     "ddppo_profile_enable": (c_int, [c_vp, c_int]),
     "ddppo_profile_read": (c_int, [c_vp, c_vp, c_vp, c_int]),
     "ddppo_debug_gemm_bf16": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_int, c_int,
-                                      c_vp]),
+                                      c_int, c_vp, c_int, c_vp]),
+    "ddppo_debug_conv2d": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
+                                   c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp, c_vp]),
+    "ddppo_debug_groupnorm": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp,
+                                      c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ddppo_debug_depth_decisions": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "ddppo_debug_maxpool": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 KERNEL_FAMILIES = ("gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other")
 for _name, (_res, _args) in _SIGS.items():

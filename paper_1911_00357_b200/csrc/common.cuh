@@ -24,6 +24,8 @@ struct ddppo_ctx {
   bool prof = false;
   int64_t launches[DDPPO_K_COUNT] = {};
   double ms[DDPPO_K_COUNT] = {};
+  int cur_fam = DDPPO_K_OTHER;                 // family of the innermost open ProfScope
+  void count(int n) { launches[cur_fam] += n; }  // launches made by shared launchers
   struct Rec { int fam; cudaEvent_t a, b; };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
@@ -46,14 +48,17 @@ struct ProfScope {
   int fam;
   cudaStream_t st;
   cudaEvent_t a = nullptr;
-  ProfScope(ddppo_ctx* c, int f, cudaStream_t s, int n) : ctx(c), fam(f), st(s) {
+  int prev_fam;
+  ProfScope(ddppo_ctx* c, int f, cudaStream_t s, int n) : ctx(c), fam(f), st(s), prev_fam(c->cur_fam) {
     ctx->launches[fam] += n;
+    ctx->cur_fam = fam;
     if (ctx->prof) {
       a = ctx->get_event();
       cudaEventRecord(a, st);
     }
   }
   ~ProfScope() {
+    ctx->cur_fam = prev_fam;
     if (ctx->prof && a) {
       cudaEvent_t b = ctx->get_event();
       cudaEventRecord(b, st);
@@ -196,6 +201,9 @@ struct GemmTC {
   float* C;
   int64_t ldc;
   int M, N, K;
+  int splits = 1;            // split-K (> 1 needs `partial`, splits*M*N floats; summed in split order)
+  float* partial = nullptr;
+  int prec = 1;              // 1: bf16 operands; 3: bf16x3 (x = hi + lo, hi*hi + hi*lo + lo*hi), ~fp32 accuracy
 };
 ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st);
 
@@ -203,7 +211,7 @@ ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st);
 struct ModelLayout {
   int64_t P = 0;
   int n = 0;
-  ddppo_tensor_info t[16];
+  ddppo_tensor_info t[96];
 };
 ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out);
 int64_t layout_offset(const ModelLayout& L, const char* name);
@@ -213,6 +221,40 @@ ddppo_status toy_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
                      float* logits, float* values, void* ws, cudaStream_t st);
 ddppo_status toy_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                      const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st);
+
+ddppo_status launch_head_fwd(ddppo_ctx* ctx, const float* Wo, const float* bo, const float* Hs, int S, float* logits,
+                             float* values, cudaStream_t st);
+ddppo_status launch_head_bwd(ddppo_ctx* ctx, const float* Wo, const float* Hs, const float* dlogits,
+                             const float* dvalues, int S, float* dH, float* dWo, float* dbo, cudaStream_t st);
+ddppo_status launch_colsum(ddppo_ctx* ctx, const float* A, int lda, int S, int M, float* out, cudaStream_t st);
+
+size_t depth_workspace(int max_B, int T);
+ddppo_status depth_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
+                       float* logits, float* values, void* ws, cudaStream_t st);
+ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
+                       const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st);
+
+// LSTM-512 cluster recurrences (lstm.cu).  Sample s = b*T_run + t.
+struct LstmPtrs {
+  const float* Whh;    // [2048][512]
+  const float* bih;    // [2048]
+  const float* bhh;    // [2048]
+  const float* GI;     // [S][2048]  W_ih x (no bias)
+  const float* mask;   // [E][ld]
+  const float* h0;     // [E][512]
+  const float* c0;     // [E][512]
+  const int32_t* env_idx;
+  int B, T_run, ld;
+  float* Hs;           // [S][512] h_t
+  float* Hin;          // [S][512] mask_t h_{t-1}
+  float* Cin;          // [S][512] mask_t c_{t-1}
+  float* Cs;           // [S][512] c_t
+  float4* IFGO;        // [S][512] gate activations (i, f, g, o)
+  const float* dH;     // [S][512] dL/dh_t from above
+  float* dG;           // [S][2048] dL/d(gate pre-activations)
+};
+ddppo_status launch_lstm_fwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
+ddppo_status launch_lstm_bwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
 
 size_t gps_workspace(int max_B, int T);
 ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,

@@ -14,6 +14,8 @@
 // reads TMEM with tcgen05.ld.32x32b.  The sum over k runs in one fixed order (deterministic).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace {
@@ -54,11 +56,36 @@ __device__ __forceinline__ uint32_t tile_off(int row, int kchunk) {
   return (uint32_t)((row >> 3) * 1024 + kchunk * 128 + (row & 7) * 16);
 }
 
+// bf16 hi part of 2 floats, and the bf16 rounding of the residual (split mode: x = hi + lo to ~16
+// mantissa bits; the product is formed as hi*hi + hi*lo + lo*hi on the tensor core)
+__device__ __forceinline__ uint32_t pk_hi(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t pk_lo(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  __nv_bfloat162 l = __floats2bfloat162_rn(a - __low2float(h), b - __high2float(h));
+  return *reinterpret_cast<uint32_t*>(&l);
+}
+template <bool SPLIT>
+__device__ __forceinline__ void store4(unsigned char* dst, unsigned char* dlo, uint32_t off, float4 v) {
+  *reinterpret_cast<uint2*>(dst + off) = make_uint2(pk_hi(v.x, v.y), pk_hi(v.z, v.w));
+  if (SPLIT) *reinterpret_cast<uint2*>(dlo + off) = make_uint2(pk_lo(v.x, v.y), pk_lo(v.z, v.w));
+}
+template <bool SPLIT>
+__device__ __forceinline__ void store8(unsigned char* dst, unsigned char* dlo, uint32_t off, const float (&v)[8]) {
+  *reinterpret_cast<uint4*>(dst + off) =
+      make_uint4(pk_hi(v[0], v[1]), pk_hi(v[2], v[3]), pk_hi(v[4], v[5]), pk_hi(v[6], v[7]));
+  if (SPLIT)
+    *reinterpret_cast<uint4*>(dlo + off) =
+        make_uint4(pk_lo(v[0], v[1]), pk_lo(v[2], v[3]), pk_lo(v[4], v[5]), pk_lo(v[6], v[7]));
+}
+
 // Stage rows [r0, r0+ROWS) x k [k0, k0+64) of X(r, k) = X[r*sr + k*sk] (fp32) into a bf16 tile in
 // the canonical layout.  K-contiguous sources (sk == 1) use coalesced float4 loads along k;
 // otherwise thread t walks row t (consecutive threads -> consecutive rows: coalesced when sr == 1).
-template <int ROWS>
-__device__ __forceinline__ void stage_tile(unsigned char* dst, const float* __restrict__ X, long long sr,
+template <int ROWS, bool SPLIT>
+__device__ __forceinline__ void stage_tile(unsigned char* dst, unsigned char* dlo, const float* __restrict__ X, long long sr,
                                            long long sk, int r0, int R, int k0, int K) {
   const int tid = threadIdx.x;
   if (sk == 1 && (sr & 3) == 0 && ((uintptr_t)X & 15) == 0) {
@@ -76,11 +103,7 @@ __device__ __forceinline__ void stage_tile(unsigned char* dst, const float* __re
           if (k + 2 < K) v.z = src[2];
         }
       }
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
-      uint2 pk;
-      pk.x = *reinterpret_cast<uint32_t*>(&h0);
-      pk.y = *reinterpret_cast<uint32_t*>(&h1);
-      *reinterpret_cast<uint2*>(dst + tile_off(row, (4 * c4) >> 3) + ((4 * c4) & 7) * 2) = pk;
+      store4<SPLIT>(dst, dlo, tile_off(row, (4 * c4) >> 3) + ((4 * c4) & 7) * 2, v);
     }
     return;
   }
@@ -94,14 +117,7 @@ __device__ __forceinline__ void stage_tile(unsigned char* dst, const float* __re
         const int k = k0 + kc * 8 + e;
         v[e] = (r < R && k < K) ? X[(long long)r * sr + (long long)k * sk] : 0.f;
       }
-      uint4 pk;
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]),
-                     h2 = __floats2bfloat162_rn(v[4], v[5]), h3 = __floats2bfloat162_rn(v[6], v[7]);
-      pk.x = *reinterpret_cast<uint32_t*>(&h0);
-      pk.y = *reinterpret_cast<uint32_t*>(&h1);
-      pk.z = *reinterpret_cast<uint32_t*>(&h2);
-      pk.w = *reinterpret_cast<uint32_t*>(&h3);
-      *reinterpret_cast<uint4*>(dst + tile_off(row, kc)) = pk;
+      store8<SPLIT>(dst, dlo, tile_off(row, kc), v);
     }
   }
 }
@@ -141,22 +157,12 @@ __device__ __forceinline__ void issue_raw(int mode, float* raw, const float* __r
   }
 }
 
-__device__ __forceinline__ uint4 pack8(const float (&v)[8]) {
-  __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]),
-                 h2 = __floats2bfloat162_rn(v[4], v[5]), h3 = __floats2bfloat162_rn(v[6], v[7]);
-  uint4 pk;
-  pk.x = *reinterpret_cast<uint32_t*>(&h0);
-  pk.y = *reinterpret_cast<uint32_t*>(&h1);
-  pk.z = *reinterpret_cast<uint32_t*>(&h2);
-  pk.w = *reinterpret_cast<uint32_t*>(&h3);
-  return pk;
-}
-
-template <int ROWS>
-__device__ __forceinline__ void convert_tile(int mode, unsigned char* dst, const float* raw, const float* __restrict__ X,
-                                             long long sr, long long sk, int r0, int R, int k0, int K) {
+template <int ROWS, bool SPLIT>
+__device__ __forceinline__ void convert_tile(int mode, unsigned char* dst, unsigned char* dlo, const float* raw,
+                                             const float* __restrict__ X, long long sr, long long sk, int r0, int R,
+                                             int k0, int K) {
   if (mode == 2) {
-    stage_tile<ROWS>(dst, X, sr, sk, r0, R, k0, K);
+    stage_tile<ROWS, SPLIT>(dst, dlo, X, sr, sk, r0, R, k0, K);
     return;
   }
   for (int row = threadIdx.x; row < ROWS; row += kThreads) {
@@ -171,7 +177,7 @@ __device__ __forceinline__ void convert_tile(int mode, unsigned char* dst, const
         const float4 b = *reinterpret_cast<const float4*>(raw + row * kRawPad + kc * 8 + 4);
         v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
       }
-      *reinterpret_cast<uint4*>(dst + tile_off(row, kc)) = pack8(v);
+      store8<SPLIT>(dst, dlo, tile_off(row, kc), v);
     }
   }
 }
@@ -181,18 +187,20 @@ __host__ __device__ constexpr uint32_t raw_bytes() {
   return (uint32_t)(ROWS * kRawPad * 4 > kBK * ROWS * 4 ? ROWS * kRawPad * 4 : kBK * ROWS * 4);
 }
 
-template <int BN>
+template <int BN, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, const float* __restrict__ B,
-                    long long sbn, long long sbk, float* __restrict__ C, long long ldc, int M, int N, int K, int amode,
+                    long long sbn, long long sbk, float* __restrict__ C, long long ldc, int M, int N, int K, int kper,
+                    long long cz_stride, int amode,
                     int bmode) {
   constexpr int kTmemCols = BN < 32 ? 32 : BN;
   constexpr uint32_t kABytes = kBM * kBK * 2, kBBytes = BN * kBK * 2;
   constexpr uint32_t kRawA = raw_bytes<kBM>(), kRawB = raw_bytes<BN>();
+  constexpr int kParts = SPLIT ? 2 : 1;  // bf16 tiles per operand and stage (hi [, lo])
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* sA[2] = {smem, smem + kABytes};
-  unsigned char* sB[2] = {smem + 2 * kABytes, smem + 2 * kABytes + kBBytes};
-  unsigned char* rbase = smem + 2 * kABytes + 2 * kBBytes;
+  unsigned char* sA[2] = {smem, smem + kParts * kABytes};
+  unsigned char* sB[2] = {smem + 2 * kParts * kABytes, smem + 2 * kParts * kABytes + kParts * kBBytes};
+  unsigned char* rbase = smem + 2 * kParts * (kABytes + kBBytes);
   float* rA[2] = {reinterpret_cast<float*>(rbase), reinterpret_cast<float*>(rbase + kRawA)};
   float* rB[2] = {reinterpret_cast<float*>(rbase + 2 * kRawA), reinterpret_cast<float*>(rbase + 2 * kRawA + kRawB)};
   __shared__ uint64_t mma_bar[2];
@@ -200,6 +208,14 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
+  // split-K: CTA z of grid.z covers k in [z*kper, z*kper + kper) and writes its own partial C
+  {
+    const long long kbeg = (long long)blockIdx.z * kper;
+    A += kbeg * sak;
+    B += kbeg * sbk;
+    K = (int)min((long long)kper, (long long)K - kbeg);
+    C += (long long)blockIdx.z * cz_stride;
+  }
   const int n_chunks = (K + kBK - 1) / kBK;
 
   // start streaming the first two K chunks while TMEM / barriers are set up
@@ -239,8 +255,8 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
       mbar_wait(&mma_bar[st], phase[st]);
       phase[st] ^= 1u;
     }
-    convert_tile<kBM>(amode, sA[st], rA[st], A, sam, sak, m0, M, k0, K);
-    convert_tile<BN>(bmode, sB[st], rB[st], B, sbn, sbk, n0, N, k0, K);
+    convert_tile<kBM, SPLIT>(amode, sA[st], sA[st] + kABytes, rA[st], A, sam, sak, m0, M, k0, K);
+    convert_tile<BN, SPLIT>(bmode, sB[st], sB[st] + kBBytes, rB[st], B, sbn, sbk, n0, N, k0, K);
     // generic-proxy smem writes -> visible to the tensor core (async proxy)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
@@ -253,16 +269,22 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a_base = smem_addr(sA[st]), b_base = smem_addr(sB[st]);
+      // split mode: the small cross terms lo*hi and hi*lo first, then hi*hi
+      constexpr int kTerms = SPLIT ? 3 : 1;
 #pragma unroll
       for (int kk = 0; kk < kBK / 16; ++kk) {
-        const uint64_t ad = make_desc(a_base + kk * 256, 128, 1024);
-        const uint64_t bd = make_desc(b_base + kk * 256, 128, 1024);
-        const uint32_t acc = (ch > 0 || kk > 0) ? 1u : 0u;
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
-            : "memory");
+#pragma unroll
+        for (int term = 0; term < kTerms; ++term) {
+          const uint32_t ao = (SPLIT && term == 0) ? kABytes : 0u, bo = (SPLIT && term == 1) ? kBBytes : 0u;
+          const uint64_t ad = make_desc(a_base + ao + kk * 256, 128, 1024);
+          const uint64_t bd = make_desc(b_base + bo + kk * 256, 128, 1024);
+          const uint32_t acc = (ch > 0 || kk > 0 || term > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+              : "memory");
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_addr(&mma_bar[st]))
@@ -310,7 +332,18 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
-template <int BN>
+__global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, long long zs, int M, int N,
+                                     float* __restrict__ C, long long ldc) {
+  const long long n = (long long)M * N;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long m = i / N, c = i % N;
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += P[z * zs + m * N + c];  // fixed split order
+    C[m * ldc + c] = s;
+  }
+}
+
+template <int BN, bool SPLIT>
 ddppo_status launch_bn(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st) {
   auto mode_of = [](const float* X, int64_t sr, int64_t sk, int R, int K) {
     const bool al = ((uintptr_t)X & 15) == 0;
@@ -319,12 +352,31 @@ ddppo_status launch_bn(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st) {
     return 2;
   };
   const int am = mode_of(g.A, g.sam, g.sak, g.M, g.K), bm = mode_of(g.B, g.sbn, g.sbk, g.N, g.K);
-  const size_t smem = 2 * (size_t)kBM * kBK * 2 + 2 * (size_t)BN * kBK * 2 + 2 * (size_t)raw_bytes<kBM>() +
+  const size_t parts = SPLIT ? 2 : 1;
+  const size_t smem = 2 * parts * ((size_t)kBM * kBK * 2 + (size_t)BN * kBK * 2) + 2 * (size_t)raw_bytes<kBM>() +
                       2 * (size_t)raw_bytes<BN>();
-  auto kern = gemm_bf16_tc_kernel<BN>;
-  DDPPO_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((g.N + BN - 1) / BN, (g.M + kBM - 1) / kBM);
-  kern<<<grid, kThreads, smem, st>>>(g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.C, g.ldc, g.M, g.N, g.K, am, bm);
+  auto kern = gemm_bf16_tc_kernel<BN, SPLIT>;
+  static bool attr_set = false;  // per device function (BN); smem size is a compile-time constant
+  if (!attr_set) {
+    DDPPO_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const int splits = g.splits > 1 && g.partial ? g.splits : 1;
+  int kper = (g.K + splits - 1) / splits;
+  kper = (kper + kBK - 1) / kBK * kBK;
+  const int nz = (g.K + kper - 1) / kper;
+  dim3 grid((g.N + BN - 1) / BN, (g.M + kBM - 1) / kBM, nz);
+  ctx->count(nz == 1 ? 1 : 2);
+  if (nz == 1) {
+    kern<<<grid, kThreads, smem, st>>>(g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.C, g.ldc, g.M, g.N, g.K, kper, 0, am, bm);
+  } else {
+    const long long zs = (long long)g.M * g.N;
+    kern<<<grid, kThreads, smem, st>>>(g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.partial, g.N, g.M, g.N, g.K, kper, zs, am,
+                                       bm);
+    DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+    splitk_reduce_kernel<<<grid_for((int)std::min<long long>(zs, 1 << 30), 256, ctx->sm_count * 8), 256, 0, st>>>(
+        g.partial, nz, zs, g.M, g.N, g.C, g.ldc);
+  }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
@@ -333,16 +385,21 @@ ddppo_status launch_bn(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st) {
 
 ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st) {
   DDPPO_REQUIRE(ctx, g.M >= 1 && g.N >= 1 && g.K >= 1, "gemm: empty shape");
-  if (g.N <= 32) return launch_bn<32>(ctx, g, st);
-  if (g.N <= 64) return launch_bn<64>(ctx, g, st);
-  return launch_bn<128>(ctx, g, st);
+  DDPPO_REQUIRE(ctx, g.prec == 1 || g.prec == 3, "gemm: prec must be 1 (bf16) or 3 (bf16x3)");
+  if (g.prec == 3) {  // two bf16 tiles per operand: BN <= 64 keeps the stages inside 227 KB
+    if (g.N <= 32) return launch_bn<32, true>(ctx, g, st);
+    return launch_bn<64, true>(ctx, g, st);
+  }
+  if (g.N <= 32) return launch_bn<32, false>(ctx, g, st);
+  if (g.N <= 64) return launch_bn<64, false>(ctx, g, st);
+  return launch_bn<128, false>(ctx, g, st);
 }
 
 extern "C" ddppo_status ddppo_debug_gemm_bf16(ddppo_ctx* ctx, const float* A, int64_t sam, int64_t sak,
                                               const float* B, int64_t sbn, int64_t sbk, float* C, int64_t ldc, int M,
-                                              int N, int K, void* stream) {
+                                              int N, int K, int splits, float* partial, int prec, void* stream) {
   if (!ctx) return DDPPO_ERR_CONFIG;
-  GemmTC g{A, sam, sak, B, sbn, sbk, C, ldc, M, N, K};
-  ProfScope ps(ctx, DDPPO_K_OTHER, as_stream(stream), 1);
+  GemmTC g{A, sam, sak, B, sbn, sbk, C, ldc, M, N, K, splits, partial, prec};
+  ProfScope ps(ctx, DDPPO_K_OTHER, as_stream(stream), 0);
   return launch_gemm_tc(ctx, g, as_stream(stream));
 }

@@ -965,7 +965,7 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
     if (s != DDPPO_OK) return s;
   }
   // weight gradients (off the dependency chain)
-  ProfScope ps(ctx, DDPPO_K_WGRAD, st, 5);
+  ProfScope ps(ctx, DDPPO_K_WGRAD, st, 2);  // + the 3 GEMMs, counted by launch_gemm_tc
   // tcgen05 GEMMs (bf16 operands, fp32 TMEM accumulation) over the S samples:
   //   dW_hh[row][j] = sum_s dG_h[s][row] H_in[s][j];  dW_ih[row][j] = sum_s dG_x[s][row] X[s][j]
   //   Q[row][n]     = sum_s dG_x[s][row] U[s][n]   (-> goal FC, embedding and b_ih gradients)
@@ -994,3 +994,28 @@ extern "C" int ddppo_debug_trace_bwd(long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_trace_b, sizeof(long long) * (size_t)n);
 }
 #endif
+
+// ------------------------------------------------------------------ shared launchers (used by depth.cu)
+ddppo_status launch_head_fwd(ddppo_ctx* ctx, const float* Wo, const float* bo, const float* Hs, int S, float* logits,
+                             float* values, cudaStream_t st) {
+  head_fwd_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(Wo, bo, Hs, S, logits, values);
+  ctx->count(1);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
+ddppo_status launch_head_bwd(ddppo_ctx* ctx, const float* Wo, const float* Hs, const float* dlogits,
+                             const float* dvalues, int S, float* dH, float* dWo, float* dbo, cudaStream_t st) {
+  head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(Wo, dlogits, dvalues, S, dH);
+  head_wgrad_kernel<<<kH / 32, 256, 0, st>>>(Hs, dlogits, dvalues, S, dWo, dbo);
+  ctx->count(2);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
+ddppo_status launch_colsum(ddppo_ctx* ctx, const float* A, int lda, int S, int M, float* out, cudaStream_t st) {
+  colsum_kernel<<<(M + 31) / 32, 256, 0, st>>>(A, lda, S, M, out);
+  ctx->count(1);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}

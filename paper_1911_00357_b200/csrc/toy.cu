@@ -48,6 +48,64 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
     add_tensor(&L, "rnn.bias_hh", 1, bg, (int)H);
     add_tensor(&L, "head.weight", 2, hw, (int)H);
     add_tensor(&L, "head.bias", 1, hb, (int)H);
+  } else if (d->arch == DDPPO_ARCH_DEPTH_R18_LSTM) {
+    if (d->hidden != 512) return DDPPO_ERR_CONFIG;
+    const int64_t H = d->hidden, G = 4 * H;
+    char name[48];
+    // conv weight [Co][Ci][k][k] (fan_in Ci*k*k), GroupNorm gamma (ones: fan_in 0) / beta (zeros: -1)
+    auto conv = [&](const char* pre, int64_t co, int64_t ci, int64_t k) {
+      int64_t s[4] = {co, ci, k, k};
+      snprintf(name, sizeof(name), "%s.weight", pre);
+      add_tensor(&L, name, 4, s, (int)(ci * k * k));
+    };
+    auto gn = [&](const char* pre, int64_t c) {
+      int64_t s[1] = {c};
+      snprintf(name, sizeof(name), "%s.weight", pre);
+      add_tensor(&L, name, 1, s, 0);
+      snprintf(name, sizeof(name), "%s.bias", pre);
+      add_tensor(&L, name, 1, s, -1);
+    };
+    conv("enc.stem.conv", 32, 1, 7);
+    gn("enc.stem.gn", 32);
+    const int64_t widths[4] = {32, 64, 128, 256};
+    int64_t cin = 32;
+    char pre[40], sub[48];
+    for (int li = 0; li < 4; ++li)
+      for (int bi = 0; bi < 2; ++bi) {
+        const int64_t c = widths[li];
+        const bool down = (bi == 0 && li > 0) || cin != c;
+        snprintf(pre, sizeof(pre), "enc.layer%d.%d", li + 1, bi);
+        snprintf(sub, sizeof(sub), "%s.conv1", pre);
+        conv(sub, c, cin, 3);
+        snprintf(sub, sizeof(sub), "%s.gn1", pre);
+        gn(sub, c);
+        snprintf(sub, sizeof(sub), "%s.conv2", pre);
+        conv(sub, c, c, 3);
+        snprintf(sub, sizeof(sub), "%s.gn2", pre);
+        gn(sub, c);
+        if (down) {
+          snprintf(sub, sizeof(sub), "%s.down.conv", pre);
+          conv(sub, c, cin, 1);
+          snprintf(sub, sizeof(sub), "%s.down.gn", pre);
+          gn(sub, c);
+        }
+        cin = c;
+      }
+    conv("enc.compress.conv", 128, 256, 3);
+    gn("enc.compress.gn", 128);
+    int64_t vw[2] = {512, 512}, vb[1] = {512}, a[2] = {32, 3}, b[1] = {32}, e[2] = {A1, 32}, wi[2] = {G, 576},
+            wh[2] = {G, H}, bg[1] = {G}, hw[2] = {A1, H}, hb[1] = {A1};
+    add_tensor(&L, "visual_fc.weight", 2, vw, 512);
+    add_tensor(&L, "visual_fc.bias", 1, vb, 512);
+    add_tensor(&L, "goal_fc.weight", 2, a, 3);
+    add_tensor(&L, "goal_fc.bias", 1, b, 3);
+    add_tensor(&L, "act_embed.weight", 2, e, 1);
+    add_tensor(&L, "rnn.weight_ih", 2, wi, (int)H);
+    add_tensor(&L, "rnn.weight_hh", 2, wh, (int)H);
+    add_tensor(&L, "rnn.bias_ih", 1, bg, (int)H);
+    add_tensor(&L, "rnn.bias_hh", 1, bg, (int)H);
+    add_tensor(&L, "head.weight", 2, hw, (int)H);
+    add_tensor(&L, "head.bias", 1, hb, (int)H);
   } else {
     return DDPPO_ERR_CONFIG;
   }

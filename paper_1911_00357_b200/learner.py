@@ -15,13 +15,14 @@ from . import (Rollout, adam_cfg, ddppo_learner_step, ddppo_preempt_poll, learne
 ROLLOUT_FIELDS = {  # name -> torch dtype
     "rew": torch.float32, "val": torch.float32, "done": torch.uint8, "length": torch.int32,
     "goal": torch.float32, "prev_action": torch.int32, "mask": torch.float32, "h0": torch.float32,
-    "action": torch.int32, "logp_old": torch.float32,
+    "action": torch.int32, "logp_old": torch.float32, "obs": torch.float32, "c0": torch.float32,
 }
+OBS_SHAPE = (1, 64, 64)  # depth frames of the Depth agent (BASELINE configs[2])
 
 
 class Learner:
     def __init__(self, ctx, arch, E, T, epochs=2, minibatches=2, hidden=None, params=None, device="cuda",
-                 normalize_adv=True, use_value_clip=True, lr=2.5e-4, max_grad_norm=0.5, ld=None):
+                 normalize_adv=True, use_value_clip=True, lr=2.5e-4, max_grad_norm=0.5, ld=None, adam_eps=1e-8):
         self.ctx, self.E, self.T = ctx, E, T
         self.ld = ld or ((T + 1 + 3) // 4 * 4)
         self.epochs, self.minibatches = epochs, minibatches
@@ -38,13 +39,15 @@ class Learner:
         self.adam_step = 0
         self.cfg = learner_cfg(epochs, minibatches, normalize_adv=normalize_adv,
                                loss=loss_cfg(use_value_clip=use_value_clip, normalize_adv=normalize_adv),
-                               adam=adam_cfg(0, lr=lr, max_grad_norm=max_grad_norm))
+                               adam=adam_cfg(0, lr=lr, eps=adam_eps, max_grad_norm=max_grad_norm))
         wsb = learner_workspace_size(self.desc, E, T, self.ld, minibatches, epochs)
         self.ws = torch.empty(wsb // 4 + 64, **f32)
         ld = self.ld
         shapes = {"rew": (E, ld), "val": (E, ld), "done": (E, ld), "length": (E,), "goal": (E, T, 3),
                   "prev_action": (E, ld), "mask": (E, ld), "h0": (E, self.hidden), "action": (E, ld),
                   "logp_old": (E, ld)}
+        if self.desc.arch == 2:  # DDPPO_ARCH_DEPTH_R18_LSTM: + depth frames and LSTM cell state
+            shapes.update(obs=(E, T) + OBS_SHAPE, c0=(E, self.hidden))
         self.dev = {k: torch.zeros(s, dtype=ROLLOUT_FIELDS[k], device=dev) for k, s in shapes.items()}
         self.perms = torch.zeros((epochs, E), dtype=torch.int32, device=dev)
         self.adv = torch.zeros((E, ld), **f32)
@@ -84,6 +87,8 @@ class Learner:
         r.host_len = self.host_len.ctypes.data
         r.host_perms = self.host_perms.ctypes.data
         r.E, r.T, r.ld = self.E, self.T, self.ld
+        if "obs" in d:
+            r.obs, r.c0 = d["obs"].data_ptr(), d["c0"].data_ptr()
         return r
 
     def step(self, stream=None):

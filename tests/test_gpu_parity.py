@@ -12,7 +12,7 @@ import pytest
 import torch
 
 import synth
-from oracle import advnorm, gae, learner, minibatch, models, optim, ppo
+from oracle import advnorm, convnets, gae, learner, minibatch, models, optim, ppo
 
 pytestmark = pytest.mark.gpu
 
@@ -266,18 +266,21 @@ def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     params = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, seed)
-    ro = synth.rollout(E, T, seed, length=lengths, hidden=H)
+    depth = arch == "depth"
+    ro = synth.rollout(E, T, seed, length=lengths, hidden=H, obs_shape=(1, 64, 64) if depth else None)
     rng = np.random.default_rng(seed)
     env_idx = rng.permutation(E)[:B].astype(np.int32)
     L = ro["length"][env_idx]
     T_run = int(L.max())
     batch = dd.make_batch(cu(ro["goal"]), cu(ro["prev_action"]), cu(ro["mask"]), cu(ro["h0"]), cu(ro["length"]),
-                          cu(env_idx), E, T, ro["ld"], B, T_run, int(L.sum()))
+                          cu(env_idx), E, T, ro["ld"], B, T_run, int(L.sum()),
+                          obs=cu(ro["obs"]) if depth else None, c0=cu(ro["c0"]) if depth else None)
     ws = torch.zeros(dd.workspace_size(desc, B, T_run) // 4 + 64, device="cuda")
     lg = torch.zeros((B, T_run, 4), device="cuda")
     vl = torch.zeros((B, T_run), device="cuda")
     pg = cu(params)
     dd.ddppo_policy_fwd(ctx, desc, pg, batch, lg, vl, ws)
+    dec = dd.ddppo_debug_depth_decisions(ctx, batch, ws).cpu().numpy() if depth else None
     dl = rng.normal(0, 1e-2, (B, T_run, 4)).astype(np.float32)
     dv = rng.normal(0, 1e-2, (B, T_run)).astype(np.float32)
     grad = torch.full((P,), 3.0, device="cuda")
@@ -285,9 +288,90 @@ def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
     torch.cuda.synchronize()
     ob = {"goal": ro["goal"][env_idx, :T_run], "prev_action": ro["prev_action"][env_idx, :T_run],
           "mask": ro["mask"][env_idx, :T_run], "h0": ro["h0"][env_idx]}
+    if depth:
+        ob.update(obs=ro["obs"][env_idx, :T_run], c0=ro["c0"][env_idx])
     lo, vo, cache = models.forward(arch, params, ob, hidden=H)
+    if depth:
+        _adopt_decisions(params, ob, cache, dec, B * T_run)
     go = models.backward(arch, params, cache, dl.astype(np.float64), dv.astype(np.float64), hidden=H)
     return lay, lg.cpu().numpy(), vl.cpu().numpy(), grad.cpu().numpy(), lo, vo, go
+
+
+def _adopt_decisions(params, ob, cache, dec, F, tie=1e-4):
+    """Hand the oracle's backward the kernel forward's ReLU masks / max-pool argmax (reading Z24):
+    every decision the two sides take differently must be a near-tie in the oracle's fp64
+    forward (|pre-activation| <= tie * rms of its layer; pool: within tie of the window max),
+    i.e. a case where both choices are correct; everything else must agree exactly."""
+    p = models.unpack("depth", params)
+    x = np.asarray(ob["obs"], np.float64).reshape((F,) + ob["obs"].shape[2:])
+    enc = cache["enc"]
+    off = [0]
+
+    def take(shape_nchw):
+        n = int(np.prod(shape_nchw))
+        N, C, Hh, Ww = shape_nchw
+        a = dec[off[0]:off[0] + n].reshape(N, Hh, Ww, C).transpose(0, 3, 1, 2)
+        off[0] += n
+        return a
+
+    flips = [0]
+
+    def adopt(key, pre):
+        gpu = take(pre.shape).astype(bool)
+        ref = pre > 0
+        diff = gpu != ref
+        if diff.any():
+            rms = np.sqrt(np.mean(pre ** 2))
+            assert np.all(np.abs(pre[diff]) <= tie * rms), (key, np.abs(pre[diff]).max() / rms)
+            flips[0] += int(diff.sum())
+        enc[key] = gpu
+
+    def cg(z, c, g, s, pad):
+        y, _ = convnets.conv_fwd(z, p[c + ".weight"], s, pad)
+        return convnets.gn_fwd(y, p[g + ".weight"], p[g + ".bias"])[0]
+
+    pre = cg(x, "enc.stem.conv", "enc.stem.gn", 2, 3)
+    adopt("enc.stem.conv.relu", pre)
+    z = pre * enc["enc.stem.conv.relu"]
+    _, pc = convnets.maxpool_fwd(z)
+    N, C, Hh, Ww = z.shape
+    Ho = pc[5]
+    gpu_arg = take((N, C, Ho, Ho)).astype(np.int64)
+    if not np.array_equal(gpu_arg, pc[1]):
+        zp = np.pad(z, ((0, 0), (0, 0), (1, 1), (1, 1)), constant_values=-np.inf)
+        win = np.stack([zp[:, :, u:u + 2 * Ho:2, v:v + 2 * Ho:2] for u in range(3) for v in range(3)], axis=-1)
+        mx = win.max(axis=-1)
+        picked = np.take_along_axis(win, gpu_arg[..., None], -1)[..., 0]
+        d = gpu_arg != pc[1]
+        assert np.all(mx[d] - picked[d] <= tie * np.sqrt(np.mean(z ** 2))), "pool argmax"
+        flips[0] += int(d.sum())
+    enc["pool"] = pc[:1] + (gpu_arg,) + pc[2:]
+    z, _ = convnets.maxpool_fwd(z)  # the pooled values are the same whichever tied element is picked
+    cin = 32
+    for li, c in enumerate(convnets.WIDTHS):
+        for bi in range(2):
+            s = 2 if (bi == 0 and li > 0) else 1
+            pre_name = f"enc.layer{li + 1}.{bi}"
+            a = cg(z, pre_name + ".conv1", pre_name + ".gn1", s, 1)
+            adopt(pre_name + ".conv1.relu", a)
+            a = a * enc[pre_name + ".conv1.relu"]
+            b = cg(a, pre_name + ".conv2", pre_name + ".gn2", 1, 1)
+            sc = cg(z, pre_name + ".down.conv", pre_name + ".down.gn", s, 0) if (s != 1 or cin != c) else z
+            out = b + sc
+            adopt(pre_name + ".out", out)
+            z = out * enc[pre_name + ".out"]
+            cin = c
+    pre = cg(z, "enc.compress.conv", "enc.compress.gn", 1, 1)
+    adopt("enc.compress.conv.relu", pre)
+    vis = dec[off[0]:off[0] + F * 512].reshape(cache["vis"].shape).astype(bool)
+    vpre = cache["flat"] @ p["visual_fc.weight"].T + p["visual_fc.bias"]
+    d = vis != (vpre > 0)
+    assert np.all(np.abs(vpre[d]) <= tie * np.sqrt(np.mean(vpre ** 2))), "visual fc relu"
+    flips[0] += int(d.sum())
+    cache["vis"] = vis.astype(np.float64)  # backward only reads its > 0 mask
+    off[0] += F * 512
+    assert off[0] == dec.size
+    return flips[0]
 
 
 def test_toy_network_parity(dd, ctx):
@@ -310,37 +394,70 @@ def test_gps_network_parity(dd, ctx, E, T, B, lengths):
         assert e < 2e-2, (name, e)
 
 
+# Depth agent (configs[2]): bf16x3 forward GEMMs, bf16 gradient GEMMs, fp16 LSTM recurrence;
+# north_star's 2e-2 per-tensor relative L2 for bf16-GEMM network gradients, with the oracle's
+# backward taking the kernel's ReLU / max-pool decisions where they are near-ties (reading Z24).
+@pytest.mark.parametrize("E,T,B,lengths", [(2, 6, 2, [6, 3]), (3, 20, 2, [20, 7, 13])])
+def test_depth_network_parity(dd, ctx, E, T, B, lengths):
+    lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, "depth", E, T, B, 40 + E + T, lengths)
+    assert rel_l2(lg, lo) < 1e-3 and rel_l2(vl, vo) < 1e-3, (rel_l2(lg, lo), rel_l2(vl, vo))
+    bad = []
+    for name, off, shape, _ in lay:
+        n = int(np.prod(shape))
+        e = rel_l2(g[off:off + n], go[off:off + n])
+        if not e < 2e-2:
+            bad.append((name, e))
+    assert not bad, bad
+
+
 # ------------------------------------------------------------------ the whole learner step (a2..a8), N = 1
-@pytest.mark.parametrize("cfgname,lengths", [("toy", None), ("gps", None), ("gps", [128, 96, 128, 32])])
+@pytest.mark.parametrize("cfgname,lengths", [("toy", None), ("gps", None), ("gps", [128, 96, 128, 32]),
+                                             ("depth", [12, 5, 12, 9])])
 def test_learner_step_parity(dd, ctx, cfgname, lengths):
     from paper_1911_00357_b200.learner import Learner
-    c = synth.CONFIGS[cfgname]
+    c = dict(synth.CONFIGS[cfgname])
+    adam_eps = 1e-8
+    if cfgname == "depth":
+        c["T"] = 12  # the oracle's fp64 ResNet keeps this case to seconds
+        # Adam's first steps are lr*sign(g) wherever |g| >> eps, so an element whose oracle gradient
+        # sits within the bf16 error of 0 may legitimately step the other way; eps = 1e-3 (of the
+        # order of a typical encoder |g|) makes the update a smooth function of g, so the gradient
+        # tolerance carries over to the parameters (both sides use the same eps).
+        adam_eps = 1e-3
     desc = dd.model_desc(c["arch"])
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 21)
-    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
-    ro = synth.rollout(c["E"], c["T"], 22, length=lengths, hidden=desc.hidden)
+    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, adam_eps=adam_eps)
+    ro = synth.rollout(c["E"], c["T"], 22, length=lengths, hidden=desc.hidden, obs_shape=c.get("obs"))
     pm = synth.perms(22, 0, c["epochs"], c["E"])
     lrn.load_rollout(ro, pm)
     stats = lrn.step().cpu().numpy()
     torch.cuda.synchronize()
     ctx.check()
     po, mo, vo, step, info = learner.learner_step(c["arch"], p0, np.zeros(P), np.zeros(P), 0, [ro], [pm],
-                                                  dict(epochs=c["epochs"], minibatches=c["minibatches"]),
+                                                  dict(epochs=c["epochs"], minibatches=c["minibatches"],
+                                                       adam_eps=adam_eps),
                                                   hidden=desc.hidden)
     assert lrn.adam_step == step == c["epochs"] * c["minibatches"]
     A = lrn.adv.cpu().numpy()
     for n in range(c["E"]):
         close_rel(A[n, :info["adv"][0].shape[1]], info["adv"][0][n], 1e-5, "adv")
-    tol = 1e-4 if cfgname == "toy" else 2e-2
+    tol = {"toy": 1e-4, "gps": 2e-2, "depth": 3e-2}[cfgname]
     for k, ms in enumerate(info["mb_stats"]):
         for i, name in enumerate(ppo.STAT_NAMES):
             ref = ms[name]
             assert abs(stats[k, i] - ref) <= tol * abs(ref) + tol * 1e-2, (k, name, stats[k, i], ref)
     dp = lrn.params.cpu().numpy().astype(np.float64) - p0
     dpo = po - p0
+    bad = []
     for name, off, shape, _ in lay:
         n = int(np.prod(shape))
         e = rel_l2(dp[off:off + n], dpo[off:off + n])
-        assert e < (1e-3 if cfgname == "toy" else 5e-2), (name, e)
+        # depth: the learner's 4 internal minibatches take their own ReLU / max-pool decisions, which
+        # cannot be handed to the oracle here (test_depth_network_parity does that); a decision
+        # flipped at a near-tie perturbs the earliest encoder layers most, hence 1e-1 for enc.*
+        lim = 1e-3 if cfgname == "toy" else (1e-1 if name.startswith("enc.") else 5e-2)
+        if not e < lim:
+            bad.append((name, round(e, 4)))
+    assert not bad, bad
