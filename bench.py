@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps"])
+    ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps", "depth"])
     ap.add_argument("--seed", type=int, default=1337)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -122,11 +122,17 @@ def blas_threads():
         return None
 
 
+# The oracle's fp64 NumPy ResNet needs ~0.2 s per frame-step of the Depth agent: its bounded sample
+# keeps the configuration but shortens the rollouts (whole learner steps on E x ORACLE_T[cfg]).
+ORACLE_T = {"depth": 32}
+
+
 def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None):
     """Time the oracle's learner step (oracle/learner.py, as it stands) on the same workload."""
     from oracle import learner as olearner
     from oracle import models
-    c = synth.CONFIGS[cfgname]
+    c = dict(synth.CONFIGS[cfgname])
+    c["T"] = ORACLE_T.get(cfgname, c["T"])
     offs, P = models.offsets(c["arch"], hidden=c["hidden"])
     fans = {n: f for n, _, f in models.layout(c["arch"], hidden=c["hidden"])}
     p = synth.init_params([(o, int(np.prod(s)), fans[k]) for k, (o, s) in offs.items()], P, seed)
@@ -136,7 +142,7 @@ def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None):
     t0 = time.perf_counter()
     it = 0
     while True:
-        ro = synth.rollout(c["E"], c["T"], seed, rank=0, iteration=it, hidden=c["hidden"])
+        ro = synth.rollout(c["E"], c["T"], seed, rank=0, iteration=it, hidden=c["hidden"], obs_shape=c.get("obs"))
         pm = synth.perms(seed, it, c["epochs"], c["E"])
         ts = time.perf_counter()
         p, m, v, step, info = olearner.learner_step(c["arch"], p, m, v, step, [ro], [pm],
@@ -156,6 +162,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     c = synth.CONFIGS[args.config]
+    T_s = ORACLE_T.get(args.config, c["T"])
     # each "step" is one oracle learner step on a bounded sample of the workload (whole rollouts)
     for _ in range(args.warmup if args.warmup < 2 else 1):
         oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=1)
@@ -165,15 +172,24 @@ def run_reference(args, rank, world):
         "unit": "experience-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * el / max(n, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"configs[1] {args.config}: {c['E']} envs x {c['T']} steps, "
-                               f"{c['epochs']} epochs x {c['minibatches']} minibatches, GRU-512",
-                   "rank0_only": True},
+        "config": {"workload": workload_name(args.config, c), "rank0_only": True,
+                   "oracle_sample": f"{c['E']} envs x {T_s} steps per learner step"},
         "cpu_baseline": {"value": sps, "unit": "experience-steps/s", "cores": blas_threads() or cpu_cores(),
-                         "kind": "oracle", "sample": f"{n} whole learner steps (rank-0 rollout, N=1 emulation)"},
+                         "kind": "oracle", "sample": f"{n} whole learner steps on {c['E']} envs x {T_s} steps (rank-0 rollout)"},
         "e2e": {"value": sps, "unit": "experience-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
     return 0
+
+
+def workload_name(cfgname, c):
+    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2}[cfgname]
+    net = {"toy": "goal MLP(64, tanh) -> heads",
+           "gps": "goal FC + action embedding -> GRU-512 -> heads",
+           "depth": "64x64 depth -> ResNet18/2 + GroupNorm -> FC 512; goal FC + action embedding -> LSTM-512 -> heads"
+           }[c["arch"]]
+    return (f"configs[{idx}] {cfgname}: {c['E']} envs/GPU x {c['T']} steps, {net}, "
+            f"{c['epochs']} epochs x {c['minibatches']} minibatches, Adam")
 
 
 # ------------------------------------------------------------------ our arm
@@ -206,8 +222,8 @@ def main():
     lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
     stream = torch.cuda.current_stream()
     n_roll = 4  # distinct rollouts cycled through (different data every step)
-    rollouts = [synth.rollout(c["E"], c["T"], args.seed, rank=rank, iteration=i, hidden=desc.hidden)
-                for i in range(n_roll)]
+    rollouts = [synth.rollout(c["E"], c["T"], args.seed, rank=rank, iteration=i, hidden=desc.hidden,
+                              obs_shape=c.get("obs")) for i in range(n_roll)]
     perms = [synth.perms(args.seed, i, c["epochs"], c["E"], rank=rank) for i in range(n_roll)]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
@@ -302,8 +318,10 @@ def main():
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sps, n, el = oracle_steps_per_sec(args.config, args.seed, budget_s=12.0)
+        T_s = ORACLE_T.get(args.config, c["T"])
         cpu_base = {"value": sps, "unit": "experience-steps/s", "cores": blas_threads() or cpu_cores(),
-                    "kind": "oracle", "sample": f"{n} whole learner steps of the same workload ({el:.1f} s)"}
+                    "kind": "oracle",
+                    "sample": f"{n} whole learner steps on {c['E']} envs x {T_s} steps of this config ({el:.1f} s)"}
 
     if rank == 0:
         out = {
@@ -311,9 +329,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32+f16/bf16-mma", "data": "synthetic",
-            "config": {"workload": f"configs[1] {args.config}: PointGoal GPS+Compass, {c['E']} envs/GPU x "
-                                   f"{c['T']} steps, goal FC + action embedding -> GRU-{desc.hidden} -> heads, "
-                                   f"{c['epochs']} epochs x {c['minibatches']} minibatches, Adam",
+            "config": {"workload": workload_name(args.config, c),
                        "E_per_gpu": c["E"], "T": c["T"], "params": P, "parallelism": f"dp{world}",
                        "l2": "flushed between timed steps (256 MiB write), per-step CUDA events",
                        "wall_s_timed_loop": t_wall},

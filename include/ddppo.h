@@ -290,15 +290,17 @@ ddppo_status ddppo_debug_gemm_bf16(ddppo_ctx* ctx, const float* A, int64_t sam, 
 
 /* Diagnostic entries to the Depth encoder's layers (stream-ordered; used by the tests).  All
  * activations NHWC fp32; conv weights PyTorch [Co][Ci][k][k].
- * conv2d: y[F][Ho][Wo][Co] = conv(x[F][H][W][Ci], w) (stride s, zero padding p; bf16x3 operands)
- *   if y != NULL; if dy != NULL: dw = weight gradient, dx = input gradient (dx nullable), bf16
- *   operands.  scratch == NULL: only *host_need (bytes) is written. */
+ * conv2d: y[F][Ho][Wo][Co] = conv(x[F][H][W][Ci], w) (stride s, zero padding p; bf16 hi/lo
+ *   operand planes) if y != NULL; if dy != NULL: dw = weight gradient, dx = input gradient (dx
+ *   nullable), bf16 operands.  Ci == 1 (the stem: fp32 SIMT, no dx) or Ci, Co multiples of 8.
+ *   scratch == NULL: only *host_need (bytes) is written. */
 ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const float* w, int F, int H, int W,
                                 int Ci, int Co, int k, int s, int p, float* y, const float* dy,
                                 float* dx, float* dw, void* scratch, size_t scratch_bytes,
                                 size_t* host_need, void* stream);
 /* GroupNorm(16 groups, eps 1e-5) over y[F][HW][C]: z = (relu)(gamma*yhat + beta (+ residual)),
- * stats[F][16][2] = (mean, rstd); if dz != NULL: dy, dgamma, dbeta (scratch: F*HW*C + 64*C floats). */
+ * stats[F][16][2] = (mean, rstd); if dz != NULL: dy (rounded to bf16, the form the gradient GEMMs
+ * consume), dgamma, dbeta (scratch: 2*F*C + F*HW*C/2 + 64 floats). */
 ddppo_status ddppo_debug_groupnorm(ddppo_ctx* ctx, const float* y, const float* gamma, const float* beta,
                                    const float* residual, int F, int HW, int C, int relu, float* z,
                                    float* stats, const float* dz, float* dy, float* dgamma,

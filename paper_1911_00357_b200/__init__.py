@@ -220,7 +220,7 @@ def ddppo_debug_conv2d(ctx, x, w, F, H, W, Ci, Co, k, s, p, y=None, dy=None, dx=
 def ddppo_debug_groupnorm(ctx, y, gamma, beta, F, HW, C, relu, z, stats, residual=None, dz=None, dy=None,
                           dgamma=None, dbeta=None, stream=None):
     import torch
-    scratch = torch.empty(F * HW * C + 64 * C, dtype=torch.float32, device=y.device)
+    scratch = torch.empty(2 * F * C + (F * HW * C + 1) // 2 + 64, dtype=torch.float32, device=y.device)
     _call(ctx, "ddppo_debug_groupnorm", f32(y), f32(gamma), f32(beta), f32(residual), F, HW, C, int(relu), f32(z),
           f32(stats), f32(dz), f32(dy), f32(dgamma), f32(dbeta), f32(scratch), _stream(stream))
     return scratch

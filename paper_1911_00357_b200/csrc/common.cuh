@@ -1,5 +1,6 @@
 // Shared internals of libddppo.so (not part of the ABI).
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
@@ -192,7 +193,48 @@ ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float*
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
                               float* grad_norm, cudaStream_t st);
 
-// tcgen05 GEMM: C[m][n] = sum_k A(m,k) B(n,k) with generic strides (gemm_tc.cu)
+// Implicit-GEMM operand: the im2col matrix of an NHWC tensor, gathered while it is staged (never
+// materialised).  Element (pixel q, column kk = (u*k + v)*SC + c) of the gathered matrix is
+//   forward     : x[f][i*s - p + u][j*s - p + v][c]                          (0 outside)
+//   transposed  : x[f][(i + p - u)/s][(j + p - v)/s][c] if both divisions are exact, else 0
+// with q = (f*PH + i)*PW + j.  As GEMM operand A the rows are pixels and k runs over kk; as
+// operand B the rows are kk and k runs over pixels (the weight-gradient GEMM).
+struct ConvG {
+  const float* x;   // [F][SH][SW][SC]
+  int PH, PW;       // pixel grid of q
+  int SH, SW, SC;   // source tensor dims
+  int k, s, p;
+  int transposed;
+};
+
+// bf16-operand implicit-GEMM (igemm.cu): operands read straight into UMMA canonical tiles.
+enum { IG_DENSE_K = 0, IG_DENSE_MN = 1, IG_PIX_K = 2, IG_TAP_MN = 3 };
+struct IGather {                 // conv gather over an NHWC bf16 tensor (see ConvG for the index maps)
+  const __nv_bfloat16* x;        // set from IgOperand::x
+  int PH, PW, SH, SW, SC, k, s, p, transposed;
+  int pw_log2, php_log2, sc_log2;  // filled by the launcher
+};
+struct IgOperand {
+  int kind;                      // IG_*
+  const __nv_bfloat16* x;
+  int64_t ld;                    // dense kinds: leading dimension (elements)
+  int64_t plane;                 // planes == 2: elements from the hi plane to the lo plane
+  IGather g;                     // gather kinds
+};
+struct IGemm {                   // C[m][n] (+)= sum_k A(m,k) B(n,k), fp32 C
+  IgOperand a, b;
+  float* C;
+  int64_t ldc;
+  int M, N, K;
+  int planes = 1;                // 1: bf16; 2: hi/lo planes, hi*hi + hi*lo + lo*hi
+  int splits = 1;
+  float* partial = nullptr;      // splits*M*N floats when splits > 1
+  int accumulate = 0;
+  int auto_split = 0;            // with `partial` (>= 16*M*N floats): split k when the tile grid is small
+};
+ddppo_status launch_igemm(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st);
+
+// tcgen05 GEMM: C[m][n] (+)= sum_k A(m,k) B(n,k) with generic strides or conv gathers (gemm_tc.cu)
 struct GemmTC {
   const float* A;
   int64_t sam, sak;
@@ -204,6 +246,9 @@ struct GemmTC {
   int splits = 1;            // split-K (> 1 needs `partial`, splits*M*N floats; summed in split order)
   float* partial = nullptr;
   int prec = 1;              // 1: bf16 operands; 3: bf16x3 (x = hi + lo, hi*hi + hi*lo + lo*hi), ~fp32 accuracy
+  const ConvG* ga = nullptr; // A(m, k) gathered (rows = pixels, k = im2col columns); A/sam/sak unused
+  const ConvG* gb = nullptr; // B(n, k) gathered (rows = im2col columns, k = pixels); B/sbn/sbk unused
+  int accumulate = 0;        // C += result (else C = result)
 };
 ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st);
 

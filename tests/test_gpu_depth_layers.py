@@ -2,9 +2,10 @@
 oracle.convnets (fp64, NCHW; transposed to the kernels' NHWC here).
 
 Tolerances (DESIGN.md "Depth precision"):
-  conv forward (bf16x3 operands): |err| <= 2e-5 * (|x| conv |W|)  elementwise;
+  conv forward (bf16 hi/lo operand planes; the 1-channel stem in fp32): |err| <= 2e-5 * (|x| conv |W|);
   conv dgrad / wgrad (bf16 operands, fp32 accumulation): |err| <= 1e-2 * the same op on |.|;
-  GroupNorm (fp32 SIMT): 1e-4 relative to the tensor's scale; max-pool: exact forward."""
+  GroupNorm (fp32 SIMT): 1e-4 relative to the tensor's scale (its input gradient is delivered in
+  bf16: + 2^-8 relative); max-pool: exact forward."""
 import numpy as np
 import pytest
 import torch
@@ -47,8 +48,9 @@ def nchw(a):
     (2, 16, 32, 64, 3, 2, 1),   # layer2.0.conv1
     (2, 16, 32, 64, 1, 2, 0),   # layer2.0.down
     (5, 2, 256, 128, 3, 1, 1),  # compress (2x2 maps)
-    (3, 7, 20, 36, 3, 2, 1),    # ragged
-    (4, 5, 8, 16, 1, 1, 0)])    # 1x1 / stride 1 (the direct GEMM path)
+    (3, 7, 24, 40, 3, 2, 1),    # ragged
+    (4, 5, 8, 16, 1, 1, 0),     # 1x1 / stride 1
+    (2, 9, 1, 16, 3, 1, 1)])    # single-channel (stem kernels) at another geometry
 def test_conv2d(dd, ctx, F, H, Ci, Co, k, s, p):
     rng = np.random.default_rng(F * 100 + H + Ci + Co + k)
     x = rng.normal(size=(F, Ci, H, H)).astype(np.float32)
@@ -71,7 +73,8 @@ def test_conv2d(dd, ctx, F, H, Ci, Co, k, s, p):
     del keep
     ctx.check()
     assert np.all(np.abs(nchw(y.cpu().numpy()) - y_o) <= 2e-5 * ya + 1e-7)
-    assert np.all(np.abs(nchw(dx.cpu().numpy()) - dx_o) <= 1e-2 * dxa + 1e-6)
+    if Ci > 1:  # the stem (1 input channel) has no input gradient
+        assert np.all(np.abs(nchw(dx.cpu().numpy()) - dx_o) <= 1e-2 * dxa + 1e-6)
     assert np.all(np.abs(dW.cpu().numpy() - dW_o) <= 1e-2 * dWa + 1e-6)
 
 
@@ -106,7 +109,8 @@ def test_groupnorm(dd, ctx, F, HW, C, relu, res):
     zz = nchw(z.cpu().numpy().reshape(F, HW, 1, C))
     assert np.max(np.abs(zz - z_o)) <= 1e-4 * np.abs(z_o).max()
     dyy = nchw(dy.cpu().numpy().reshape(F, HW, 1, C))
-    assert np.max(np.abs(dyy - dy_o)) <= 1e-4 * np.abs(dy_o).max()
+    # dy is delivered rounded to bf16 (the gradient GEMMs' operand format): 2^-8 relative
+    assert np.all(np.abs(dyy - dy_o) <= 2.0 ** -8 * np.abs(dy_o) + 1e-4 * np.abs(dy_o).max())
     assert np.max(np.abs(dg.cpu().numpy() - dg_o)) <= 1e-4 * np.abs(dg_o).max()
     assert np.max(np.abs(db.cpu().numpy() - db_o)) <= 1e-4 * np.abs(db_o).max()
 
