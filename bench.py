@@ -345,6 +345,31 @@ def main():
     return 0
 
 
+def depth_encoder_macs():
+    """Multiply-accumulates per frame of the Depth agent's encoder (64x64 -> ResNet18/2 -> 128x2x2)."""
+    macs, stem = 0, 0
+
+    def conv(h, ci, co, k, s, p):
+        nonlocal macs
+        ho = (h + 2 * p - k) // s + 1
+        macs += ho * ho * co * ci * k * k
+        return ho
+    h = conv(64, 1, 32, 7, 2, 3)
+    stem = macs
+    h = (h + 2 - 3) // 2 + 1  # max-pool
+    cin = 32
+    for li, c in enumerate((32, 64, 128, 256)):
+        for bi in range(2):
+            s = 2 if (bi == 0 and li > 0) else 1
+            h1 = conv(h, cin, c, 3, s, 1)
+            conv(h1, c, c, 3, 1, 1)
+            if s != 1 or cin != c:
+                conv(h, cin, c, 1, s, 0)
+            h, cin = h1, c
+    conv(h, 256, 128, 3, 1, 1)
+    return {"all": macs, "stem": stem}
+
+
 def roofline_for(fam, prof, c, lrn, peaks, steps):
     """Algorithmic work of one launch of the dominant family / its mean device time."""
     ms, n = prof[fam]
@@ -362,6 +387,20 @@ def roofline_for(fam, prof, c, lrn, peaks, steps):
                 "frac": achieved / bf16, "traffic": None, "launch_us": per_launch_s * 1e6,
                 "note": "latency-bound dependency chain (B=2 envs x 128 steps on 16 SMs); per-step phases in "
                         "DESIGN.md sec. 7; HBM kernels' fractions in profiles/r01_microbench.jsonl"}
+    if fam in ("net_fwd", "net_bwd") and c["arch"] == "depth":
+        # the family = one minibatch pass: encoder implicit GEMMs (+ GroupNorm / pool SIMT), FC,
+        # LSTM input GEMM and recurrence; algorithmic FLOPs = the dense contractions, counted once
+        # (the forward's bf16x3 operand planes cost 3 MMAs per product but count once here)
+        frames = B * T
+        enc = depth_encoder_macs()
+        dense_fwd = 2.0 * (enc["all"] + 512 * 512 + 576 * 2048 + 2048 * H)
+        dense_bwd = 2.0 * (2 * enc["all"] - enc["stem"] + 2 * (512 * 512 + 576 * 2048) + 2 * 2048 * H)
+        flops = frames * (dense_fwd if fam == "net_fwd" else dense_bwd)
+        achieved = flops / per_launch_s / 1e12
+        return {"bound": "tensor", "kernel": fam, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                "frac": achieved / bf16, "traffic": None, "launch_us": per_launch_s * 1e6,
+                "note": "kernel family of one minibatch pass (ResNet18/2 implicit GEMMs + GroupNorm + LSTM-512 "
+                        "recurrence); per-kernel split in profiles/"}
     byte_per = {"gae": 17.0 * E * T, "loss": 60.0 * B * T, "adam": 32.0 * lrn.P}
     b = byte_per.get(fam, 0.0)
     achieved = b / per_launch_s / 1e9 if b else 0.0

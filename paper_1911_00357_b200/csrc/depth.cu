@@ -169,11 +169,18 @@ __global__ void __launch_bounds__(kThreads) stem_wgrad_kernel(const float* __res
   for (int q0 = 0; q0 < Ho * Wo; q0 += kStemPix) {
     const int nq = min(kStemPix, Ho * Wo - q0);
     __syncthreads();  // xs staged / previous chunk consumed
-    for (int e = threadIdx.x; e < nq * kk; e += blockDim.x) {
-      const int q = e / kk, tap = e - q * kk;
+    // im2col rows of the chunk: thread pair per pixel (no division in the tap loops)
+    for (int e = threadIdx.x; e < 2 * nq; e += blockDim.x) {
+      const int q = e >> 1, half = e & 1;
       const int i = (q0 + q) / Wo, j = (q0 + q) - i * Wo;
-      const int yy = i * s - p + tap / k, xx = j * s - p + tap % k;
-      cs[q * kStemTapPad + tap] = (yy >= 0 && yy < H && xx >= 0 && xx < Wd) ? xs[yy * Wd + xx] : 0.f;
+      for (int u = half; u < k; u += 2) {
+        const int yy = i * s - p + u;
+        const bool yok = yy >= 0 && yy < H;
+        for (int v = 0; v < k; ++v) {
+          const int xx = j * s - p + v;
+          cs[q * kStemTapPad + u * k + v] = (yok && xx >= 0 && xx < Wd) ? xs[yy * Wd + xx] : 0.f;
+        }
+      }
     }
     for (int e = threadIdx.x; e < nq * Co; e += blockDim.x)
       ds[e] = __bfloat162float(dy[((size_t)f * Ho * Wo + q0) * Co + e]);

@@ -22,7 +22,7 @@
 
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kThreads = 256;
+constexpr int kBM = 128, kBK = 64, kThreads = 512;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
@@ -345,11 +345,12 @@ igemm_kernel(const OpDev opA, const OpDev opB, float* __restrict__ C, long long 
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // epilogue (TMEM lanes = rows): 32 x 8 blocks transposed through shared memory for row-contiguous stores
   float* tr = reinterpret_cast<float*>(smem) + warp * (32 * 9);
-  // warp w reads TMEM lane quarter w % 4 (rows), column half w / 4
+  // warp w reads TMEM lane quarter w % 4 (rows) and column slice w / 4 of BN / (warps / 4) columns
   const int row0 = m0 + (warp & 3) * 32;
-  constexpr int kHalf = BN / 2;
+  constexpr int kSlice = BN / (kThreads / 128);
+  static_assert(kSlice >= 8 && kSlice % 8 == 0, "epilogue column slice");
 #pragma unroll 1
-  for (int c0 = (warp >> 2) * kHalf; c0 < (warp >> 2) * kHalf + kHalf; c0 += 8) {
+  for (int c0 = (warp >> 2) * kSlice; c0 < (warp >> 2) * kSlice + kSlice; c0 += 8) {
     uint32_t r[8];
     const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
     asm volatile(
