@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps", "depth"])
+    ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps", "depth", "stress"])
     ap.add_argument("--seed", type=int, default=1337)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -124,7 +124,7 @@ def blas_threads():
 
 # The oracle's fp64 NumPy ResNet needs ~0.2 s per frame-step of the Depth agent: its bounded sample
 # keeps the configuration but shortens the rollouts (whole learner steps on E x ORACLE_T[cfg]).
-ORACLE_T = {"depth": 32}
+ORACLE_T = {"depth": 32, "stress": 8}
 
 
 def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None):
@@ -183,7 +183,7 @@ def run_reference(args, rank, world):
 
 
 def workload_name(cfgname, c):
-    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2}[cfgname]
+    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2, "stress": 4}[cfgname]
     net = {"toy": "goal MLP(64, tanh) -> heads",
            "gps": "goal FC + action embedding -> GRU-512 -> heads",
            "depth": "64x64 depth -> ResNet18/2 + GroupNorm -> FC 512; goal FC + action embedding -> LSTM-512 -> heads"
@@ -195,6 +195,9 @@ def workload_name(cfgname, c):
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
+    # one JSON line on stdout: keep NCCL's version banner (NCCL_DEBUG=VERSION) off it
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -222,8 +225,24 @@ def main():
     lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
     stream = torch.cuda.current_stream()
     n_roll = 4  # distinct rollouts cycled through (different data every step)
+    preempt = None
+    lengths = [None] * n_roll
+    if c.get("preempt_p"):
+        # configs[4]: each rollout's collection phase under the preemption protocol (untimed, virtual
+        # ticks, one NCCL int32 poll per tick); every env of a rank stops at the rank's L_w
+        from paper_1911_00357_b200.learner import preempt_collect
+        preempt = {"p_percent": c["preempt_p"], "T": c["T"], "rollouts": []}
+        K, ms = dd.ddppo_preempt_threshold(dd.preempt_cfg(c["preempt_p"], c["T"]), world)
+        preempt.update(K=K, min_steps=ms)
+        for i in range(n_roll):
+            costs = synth.straggler_costs(args.seed + i, world, c["T"])[rank]
+            L_w, ticks = preempt_collect(ctx, costs, c["T"], c["preempt_p"])
+            lengths[i] = [L_w] * c["E"]
+            cnt = dd.ddppo_allreduce_counts(ctx, [c["E"] * L_w, c["E"] * (c["T"] - L_w), 1 if L_w < c["T"] else 0])
+            preempt["rollouts"].append({"ticks": ticks, "collected": int(cnt[0]), "preempted_steps": int(cnt[1]),
+                                        "preempted_ranks": int(cnt[2]), "rank0_L": L_w})
     rollouts = [synth.rollout(c["E"], c["T"], args.seed, rank=rank, iteration=i, hidden=desc.hidden,
-                              obs_shape=c.get("obs")) for i in range(n_roll)]
+                              obs_shape=c.get("obs"), length=lengths[i]) for i in range(n_roll)]
     perms = [synth.perms(args.seed, i, c["epochs"], c["E"], rank=rank) for i in range(n_roll)]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
@@ -333,7 +352,7 @@ def main():
                        "E_per_gpu": c["E"], "T": c["T"], "params": P, "parallelism": f"dp{world}",
                        "l2": "flushed between timed steps (256 MiB write), per-step CUDA events",
                        "wall_s_timed_loop": t_wall},
-            "clocks": clocks, "e2e": e2e, "gpu_launches": gpu_launches,
+            "clocks": clocks, "e2e": e2e, "gpu_launches": gpu_launches, "preemption": preempt,
             "kernel_ms": {k: round(v, 4) for k, v in fam_ms.items() if v > 0},
             "roofline": roofline, "cpu_baseline": cpu_base,
         }
@@ -373,6 +392,8 @@ def depth_encoder_macs():
 def roofline_for(fam, prof, c, lrn, peaks, steps):
     """Algorithmic work of one launch of the dominant family / its mean device time."""
     ms, n = prof[fam]
+    if c["arch"] == "depth" and fam in ("net_fwd", "net_bwd"):
+        n = steps * c["epochs"] * c["minibatches"]  # one "launch" = one minibatch pass of the family
     per_launch_s = (ms / 1e3) / max(n, 1)
     hbm = peaks.get("hbm_gbs", 6650.0)
     bf16 = peaks.get("bf16_tflops_sustained", 1400.0)

@@ -10,7 +10,9 @@ Test infrastructure only.  NumPy float64, NCHW, textbook definitions:
   * half-width ResNet18 ("number of output channels at every layer reduced by half",
     reading Z23: stem 7x7/2 + maxpool, BasicBlocks 32/64/128/256, stride on the first block of
     layers 2-4 with a 1x1/stride conv + GN shortcut), then the 3x3 compression conv to 128
-    channels + GN + ReLU (P:L582, Z20).
+    channels + GN + ReLU (P:L582, Z20);
+  * half-width ResNet50 for the RGB-D agent (bottlenecks [3, 4, 6, 3], 2x2 average pooling of the
+    256^2 input first, channel-wise RGB normalisation P:L367) -> 1024x4x4 -> compression to 128x4x4.
 """
 import numpy as np
 
@@ -183,4 +185,106 @@ def resnet18h_bwd(dz, p, caches, g):
         dz = dx
     dz = maxpool_bwd(dz, caches["pool"])
     dx = _conv_gn_bwd(dz, p, "enc.stem.conv", "enc.stem.gn", True, caches, g)
+    return dx
+
+
+# ---------------------------------------------------------------- RGB-D agent (configs[3])
+# P:L212 / P:L582 (half-width ResNet50 "1024x4x4"), reading Z23: 2x2 average pooling of the 256^2
+# input, stem 7x7/2 conv + GN + ReLU + 3x3/2 max-pool, bottleneck blocks [3, 4, 6, 3] with widths
+# 32/64/128/256 (outputs x4), stride on the 3x3 (v1.5) of the first block of layers 2-4, 1x1/stride
+# conv + GN shortcut when the shape changes; compression 3x3 conv 1024 -> 128 + GN + ReLU (Z20).
+# RGB channels are normalised channel-wise before the encoder (reading R7).
+R50_BLOCKS = (3, 4, 6, 3)
+RGB_MEAN = (0.485 * 255.0, 0.456 * 255.0, 0.406 * 255.0)
+RGB_STD = (0.229 * 255.0, 0.224 * 255.0, 0.225 * 255.0)
+
+
+def avgpool2_fwd(x):
+    """2x2 / stride 2 average pooling (H, W even)."""
+    N, C, H, W = x.shape
+    return x.reshape(N, C, H // 2, 2, W // 2, 2).mean(axis=(3, 5))
+
+
+def avgpool2_bwd(dy):
+    return np.repeat(np.repeat(dy, 2, axis=2), 2, axis=3) / 4.0
+
+
+def rgbd_normalize(x):
+    """x [N][4][H][W]: RGB in [0, 255] -> (x - mean_c) / std_c; depth (channel 3) unchanged."""
+    out = np.array(x, dtype=np.float64, copy=True)
+    for c in range(3):
+        out[:, c] = (out[:, c] - RGB_MEAN[c]) / RGB_STD[c]
+    return out
+
+
+def resnet50h_spec(in_ch):
+    """Ordered (name, kind, shape, stride, pad) of the RGB-D encoder's parameter tensors."""
+    spec = [("enc.stem.conv", "conv", (32, in_ch, 7, 7), 2, 3), ("enc.stem.gn", "gn", (32,), 0, 0)]
+    cin = 32
+    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+        for bi in range(nb):
+            s = 2 if (bi == 0 and li > 0) else 1
+            pre = f"enc.layer{li + 1}.{bi}"
+            spec += [(pre + ".conv1", "conv", (w, cin, 1, 1), 1, 0), (pre + ".gn1", "gn", (w,), 0, 0),
+                     (pre + ".conv2", "conv", (w, w, 3, 3), s, 1), (pre + ".gn2", "gn", (w,), 0, 0),
+                     (pre + ".conv3", "conv", (4 * w, w, 1, 1), 1, 0), (pre + ".gn3", "gn", (4 * w,), 0, 0)]
+            if s != 1 or cin != 4 * w:
+                spec += [(pre + ".down.conv", "conv", (4 * w, cin, 1, 1), s, 0),
+                         (pre + ".down.gn", "gn", (4 * w,), 0, 0)]
+            cin = 4 * w
+    spec += [("enc.compress.conv", "conv", (128, 1024, 3, 3), 1, 1), ("enc.compress.gn", "gn", (128,), 0, 0)]
+    return spec
+
+
+def resnet50h_fwd(x, p):
+    """x [N][4][256][256] (raw RGB-D) -> feature [N][128][4][4]."""
+    caches = {}
+    z = avgpool2_fwd(rgbd_normalize(x))
+    z = _conv_gn(z, p, "enc.stem.conv", "enc.stem.gn", 2, 3, True, caches)
+    z, caches["pool"] = maxpool_fwd(z)
+    cin = 32
+    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+        for bi in range(nb):
+            s = 2 if (bi == 0 and li > 0) else 1
+            pre = f"enc.layer{li + 1}.{bi}"
+            a = _conv_gn(z, p, pre + ".conv1", pre + ".gn1", 1, 0, True, caches)
+            b = _conv_gn(a, p, pre + ".conv2", pre + ".gn2", s, 1, True, caches)
+            c3 = _conv_gn(b, p, pre + ".conv3", pre + ".gn3", 1, 0, False, caches)
+            sc = z
+            if s != 1 or cin != 4 * w:
+                sc = _conv_gn(z, p, pre + ".down.conv", pre + ".down.gn", s, 0, False, caches)
+            out = c3 + sc
+            caches[pre + ".out"] = out > 0
+            z = np.maximum(out, 0.0)
+            cin = 4 * w
+    z = _conv_gn(z, p, "enc.compress.conv", "enc.compress.gn", 1, 1, True, caches)
+    return z, caches
+
+
+def resnet50h_bwd(dz, p, caches, g):
+    """Parameter gradients into g; returns the gradient wrt the raw input."""
+    dz = _conv_gn_bwd(dz, p, "enc.compress.conv", "enc.compress.gn", True, caches, g)
+    blocks = []
+    cin = 32
+    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+        for bi in range(nb):
+            blocks.append((li, bi, w, cin))
+            cin = 4 * w
+    for li, bi, w, cin in reversed(blocks):
+        s = 2 if (bi == 0 and li > 0) else 1
+        pre = f"enc.layer{li + 1}.{bi}"
+        dout = dz * caches[pre + ".out"]
+        db = _conv_gn_bwd(dout, p, pre + ".conv3", pre + ".gn3", False, caches, g)
+        da = _conv_gn_bwd(db, p, pre + ".conv2", pre + ".gn2", True, caches, g)
+        dx = _conv_gn_bwd(da, p, pre + ".conv1", pre + ".gn1", True, caches, g)
+        if s != 1 or cin != 4 * w:
+            dx = dx + _conv_gn_bwd(dout, p, pre + ".down.conv", pre + ".down.gn", False, caches, g)
+        else:
+            dx = dx + dout
+        dz = dx
+    dz = maxpool_bwd(dz, caches["pool"])
+    dz = _conv_gn_bwd(dz, p, "enc.stem.conv", "enc.stem.gn", True, caches, g)
+    dx = avgpool2_bwd(dz)
+    for c in range(3):
+        dx[:, c] /= RGB_STD[c]
     return dx

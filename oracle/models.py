@@ -19,6 +19,11 @@ Architectures (BASELINE.json configs; readings Z17-Z22):
                      -> 128x2x2 -> flatten (c, h, w order) -> Linear(512, 512) + ReLU
                      (Z17, Z20); x = [visual 512, goal_fc 32, act_emb 32]
                      -> LSTM(576, 512) (PyTorch i, f, g, o) -> Linear(512, A+1).
+  rgbd (configs[3]): RGB-D [4][256][256] (RGB in [0, 255] normalised channel-wise) ->
+                     2x2 avg-pool -> half-width ResNet50 (convnets.py) -> 128x4x4 -> flatten ->
+                     Linear(2048, 512) + ReLU; x = [visual, goal_fc, act_emb] -> 2-layer LSTM-512
+                     (layer 2 reads layer 1's h) -> Linear(512, A+1).  h0 / c0 are
+                     [B][2*512] (layer-major).
 fan_in > 0: U(+-1/sqrt(fan_in)) default init; fan_in == 0: ones (GN gamma);
 fan_in < 0: zeros (GN beta).
 """
@@ -57,6 +62,21 @@ def layout(arch, hidden=512, num_actions=NUM_ACTIONS):
                       ("rnn.weight_ih", (G, 576), H), ("rnn.weight_hh", (G, H), H),
                       ("rnn.bias_ih", (G,), H), ("rnn.bias_hh", (G,), H),
                       ("head.weight", (A1, H), H), ("head.bias", (A1,), H)]
+    if arch == "rgbd":
+        H, G = hidden, 4 * hidden
+        out = []
+        for name, kind, shape, _, _ in convnets.resnet50h_spec(4):
+            if kind == "conv":
+                out.append((name + ".weight", shape, shape[1] * shape[2] * shape[3]))
+            else:
+                out += [(name + ".weight", shape, 0), (name + ".bias", shape, -1)]
+        out += [("visual_fc.weight", (512, 2048), 2048), ("visual_fc.bias", (512,), 2048),
+                ("goal_fc.weight", (32, 3), 3), ("goal_fc.bias", (32,), 3),
+                ("act_embed.weight", (A1, 32), 1)]
+        for layer, nin in ((0, 576), (1, H)):
+            out += [(f"rnn.weight_ih_l{layer}", (G, nin), H), (f"rnn.weight_hh_l{layer}", (G, H), H),
+                    (f"rnn.bias_ih_l{layer}", (G,), H), (f"rnn.bias_hh_l{layer}", (G,), H)]
+        return out + [("head.weight", (A1, H), H), ("head.bias", (A1,), H)]
     raise ValueError(arch)
 
 
@@ -124,6 +144,29 @@ def forward(arch, flat, batch, **kw):
         out = nets.linear_fwd(h, p["head.weight"], p["head.bias"])
         cache = {"goal": goal, "prev_action": np.asarray(batch["prev_action"]), "h": h, "rnn": rc, "enc": ec,
                  "feat_shape": feat.shape, "flat": flat_f, "vis": vis}
+    elif arch == "rgbd":
+        obs = np.asarray(batch["obs"], dtype=np.float64)  # [B][T][4][256][256]
+        B, T = obs.shape[:2]
+        feat, ec = convnets.resnet50h_fwd(obs.reshape((B * T,) + obs.shape[2:]), p)
+        flat_f = feat.reshape(B, T, -1)  # (c, h, w) order, 2048
+        vis = np.maximum(nets.linear_fwd(flat_f, p["visual_fc.weight"], p["visual_fc.bias"]), 0.0)
+        ge = nets.linear_fwd(goal, p["goal_fc.weight"], p["goal_fc.bias"])
+        ae = nets.embedding_fwd(batch["prev_action"], p["act_embed.weight"])
+        H = p["rnn.weight_hh_l0"].shape[1]
+        mask = np.asarray(batch["mask"], dtype=np.float64)
+        h0 = np.asarray(batch["h0"], dtype=np.float64).reshape(B, 2, H)
+        c0 = np.asarray(batch["c0"], dtype=np.float64).reshape(B, 2, H)
+        x = np.concatenate([vis, ge, ae], axis=-1)
+        rcs = []
+        for layer in range(2):
+            x, rc = nets.lstm_seq_fwd(x, mask, h0[:, layer], c0[:, layer], p[f"rnn.weight_ih_l{layer}"],
+                                      p[f"rnn.weight_hh_l{layer}"], p[f"rnn.bias_ih_l{layer}"],
+                                      p[f"rnn.bias_hh_l{layer}"])
+            rcs.append(rc)
+        h = x
+        out = nets.linear_fwd(h, p["head.weight"], p["head.bias"])
+        cache = {"goal": goal, "prev_action": np.asarray(batch["prev_action"]), "h": h, "rnn": rcs, "enc": ec,
+                 "feat_shape": feat.shape, "flat": flat_f, "vis": vis}
     else:
         raise ValueError(arch)
     return out[..., :-1], out[..., -1], cache
@@ -156,6 +199,20 @@ def backward(arch, flat, cache, dlogits, dvalues, **kw):
         dflat, g["visual_fc.weight"], g["visual_fc.bias"] = nets.linear_bwd(cache["flat"], p["visual_fc.weight"],
                                                                             dvpre)
         convnets.resnet18h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
+    elif arch == "rgbd":
+        dh, g["head.weight"], g["head.bias"] = nets.linear_bwd(cache["h"], p["head.weight"], dout)
+        for layer in (1, 0):
+            dh, g[f"rnn.weight_ih_l{layer}"], g[f"rnn.weight_hh_l{layer}"], g[f"rnn.bias_ih_l{layer}"], \
+                g[f"rnn.bias_hh_l{layer}"] = nets.lstm_seq_bwd(dh, cache["rnn"][layer], p[f"rnn.weight_ih_l{layer}"],
+                                                               p[f"rnn.weight_hh_l{layer}"])
+        dx = dh
+        dvis, dge, dae = dx[..., :512], dx[..., 512:544], dx[..., 544:]
+        _, g["goal_fc.weight"], g["goal_fc.bias"] = nets.linear_bwd(cache["goal"], p["goal_fc.weight"], dge)
+        g["act_embed.weight"] = nets.embedding_bwd(cache["prev_action"], dae, p["act_embed.weight"].shape[0])
+        dvpre = dvis * (cache["vis"] > 0)
+        dflat, g["visual_fc.weight"], g["visual_fc.bias"] = nets.linear_bwd(cache["flat"], p["visual_fc.weight"],
+                                                                            dvpre)
+        convnets.resnet50h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
     else:
         raise ValueError(arch)
     return pack(arch, g, **kw)

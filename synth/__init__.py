@@ -34,6 +34,12 @@ CONFIGS = {
     "gps": dict(arch="gps", E=4, T=128, epochs=2, minibatches=2, hidden=512),
     "stress_gps": dict(arch="gps", E=16, T=128, epochs=2, minibatches=2, hidden=512),
     "depth": dict(arch="depth", E=4, T=128, epochs=2, minibatches=2, hidden=512, obs=(1, 64, 64)),
+    # configs[4]: the Depth agent with 16 envs/GPU, collection under the preemption protocol with
+    # synthetic stragglers (p = 60 %, minimum T/4); SURVEY 8 pins the depth model for it
+    # configs[3]: the paper-shaped RGB-D agent (half-width ResNet50 + 2-layer LSTM-512)
+    "rgbd": dict(arch="rgbd", E=4, T=128, epochs=2, minibatches=2, hidden=512, obs=(4, 256, 256), rnn_layers=2),
+    "stress": dict(arch="depth", E=16, T=128, epochs=2, minibatches=2, hidden=512, obs=(1, 64, 64),
+                   preempt_p=60),
 }
 
 
@@ -53,6 +59,25 @@ def depth_frames(rng, E, T, C=1, H=64, W=64):
     return out
 
 
+def rgbd_frames(rng, E, T, H=256, W=256):
+    """RGB-D frames [E][T][4][H][W]: RGB in [0, 255] (integer-valued, like camera bytes) and depth in
+    [0, 1], each channel a drifting sum of 3 seeded low-frequency cosine fields + 5 % noise."""
+    yy, xx = np.meshgrid(np.linspace(0, 1, H), np.linspace(0, 1, W), indexing="ij")
+    out = np.empty((E, T, 4, H, W), np.float32)
+    for n in range(E):
+        for ch in range(4):
+            k = rng.uniform(0.5, 3.0, (3, 2))
+            ph = rng.uniform(0, 2 * np.pi, 3)
+            drift = rng.uniform(-0.05, 0.05, 3)
+            base = [2 * np.pi * (k[i, 0] * xx + k[i, 1] * yy) + ph[i] for i in range(3)]
+            cb, sb = [np.cos(b) for b in base], [np.sin(b) for b in base]
+            for t in range(T):
+                f = sum(cb[i] * np.cos(drift[i] * t) - sb[i] * np.sin(drift[i] * t) for i in range(3))
+                f = np.clip(0.5 + f / 6.0 + 0.05 * rng.standard_normal((H, W)), 0.0, 1.0)
+                out[n, t, ch] = np.rint(255.0 * f) if ch < 3 else f
+    return out
+
+
 def ld_for(T):
     return (T + 1 + 3) // 4 * 4
 
@@ -62,9 +87,10 @@ def _rng(seed, *keys):
     return np.random.Generator(np.random.Philox(ss))
 
 
-def rollout(E, T, seed, rank=0, iteration=0, length=None, hidden=512, ld=None, obs_shape=None):
+def rollout(E, T, seed, rank=0, iteration=0, length=None, hidden=512, ld=None, obs_shape=None, rnn_layers=1):
     """One rank's rollout.  `length` (int or [E]) truncates (preemption); default T.
-    obs_shape (C, H, W) adds depth-like frames `obs` [E][T][C][H][W] and an LSTM cell state `c0`."""
+    obs_shape (C, H, W) adds frames `obs` [E][T][C][H][W] (C = 4: RGB-D) and an LSTM cell state `c0`;
+    recurrent states are [E][rnn_layers * hidden] (layer-major)."""
     ld = ld or ld_for(T)
     rng = _rng(seed, 1, rank, iteration)
     f32 = np.float32
@@ -145,15 +171,18 @@ def rollout(E, T, seed, rank=0, iteration=0, length=None, hidden=512, ld=None, o
             arr[n, L:] = 0
         val[n, L + 1:] = 0
         goal[n, L:] = 0
-    h0 = rng.normal(0.0, 0.1, (E, hidden)).astype(f32)
+    h0 = rng.normal(0.0, 0.1, (E, rnn_layers * hidden)).astype(f32)
     out = dict(rew=rew, val=val, done=done, length=length, goal=goal, prev_action=prev_action,
                mask=mask, action=action, logp_old=logp_old, h0=h0, E=E, T=T, ld=ld)
     if obs_shape is not None:
-        obs = depth_frames(_rng(seed, 6, rank, iteration), E, T, *obs_shape)
+        if obs_shape[0] == 4:
+            obs = rgbd_frames(_rng(seed, 6, rank, iteration), E, T, *obs_shape[1:])
+        else:
+            obs = depth_frames(_rng(seed, 6, rank, iteration), E, T, *obs_shape)
         for n in range(E):
             obs[n, int(length[n]):] = 0
         out["obs"] = obs
-        out["c0"] = rng.normal(0.0, 0.1, (E, hidden)).astype(f32)
+        out["c0"] = rng.normal(0.0, 0.1, (E, rnn_layers * hidden)).astype(f32)
     return out
 
 

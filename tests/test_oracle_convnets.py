@@ -170,3 +170,105 @@ def test_depth_model_finite_differences():
             # ReLU / max-pool kinks can sit inside the stencil: 1e-4 relative (the exact layer-by-layer
             # pins are the torch.autograd cross-checks above)
             assert abs(fd - g[o + i]) < 1e-4 * max(abs(fd), 1e-3), (name, i, fd, g[o + i])
+
+
+# ---------------------------------------------------------------- RGB-D agent (configs[3])
+def test_avgpool_matches_torch():
+    rng = np.random.default_rng(9)
+    x = rng.normal(size=(2, 3, 8, 6))
+    xt = _t(x, True)
+    yt = F.avg_pool2d(xt, 2, 2)
+    assert np.max(np.abs(convnets.avgpool2_fwd(x) - yt.detach().numpy())) < 1e-14
+    dy = rng.normal(size=yt.shape)
+    (yt * _t(dy)).sum().backward()
+    assert np.max(np.abs(convnets.avgpool2_bwd(dy) - xt.grad.numpy())) < 1e-14
+
+
+class _TorchR50H(torch.nn.Module):
+    """Independent torch construction of the RGB-D encoder (normalise, avg-pool, ResNet50/2, compress)."""
+
+    def __init__(self, p):
+        super().__init__()
+        self.p = p
+
+    def forward(self, x):
+        p = self.p
+        mean = torch.tensor([0.485, 0.456, 0.406, 0.0], dtype=torch.float64).view(1, 4, 1, 1) * 255.0
+        std = torch.tensor([0.229, 0.224, 0.225, 1.0 / 255.0], dtype=torch.float64).view(1, 4, 1, 1) * 255.0
+        z = F.avg_pool2d((x - mean) / std, 2)
+
+        def cg(z, c, g, s, pad, relu):
+            z = F.conv2d(z, p[c + ".weight"], stride=s, padding=pad)
+            z = F.group_norm(z, 16, p[g + ".weight"], p[g + ".bias"], eps=1e-5)
+            return F.relu(z) if relu else z
+        z = F.max_pool2d(cg(z, "enc.stem.conv", "enc.stem.gn", 2, 3, True), 3, 2, 1)
+        cin = 32
+        for li, (w, nb) in enumerate(zip(convnets.WIDTHS, convnets.R50_BLOCKS)):
+            for bi in range(nb):
+                s = 2 if (bi == 0 and li > 0) else 1
+                pre = f"enc.layer{li + 1}.{bi}"
+                a = cg(z, pre + ".conv1", pre + ".gn1", 1, 0, True)
+                b = cg(a, pre + ".conv2", pre + ".gn2", s, 1, True)
+                c3 = cg(b, pre + ".conv3", pre + ".gn3", 1, 0, False)
+                sc = cg(z, pre + ".down.conv", pre + ".down.gn", s, 0, False) if (s != 1 or cin != 4 * w) else z
+                z = F.relu(c3 + sc)
+                cin = 4 * w
+        return cg(z, "enc.compress.conv", "enc.compress.gn", 1, 1, True)
+
+
+def test_resnet50h_matches_torch():
+    lay = models.layout("rgbd")
+    offs, P = models.offsets("rgbd")
+    ent = [(offs[n][0], int(np.prod(s)), f) for n, s, f in lay]
+    flat = synth.init_params(ent, P, 13).astype(np.float64)
+    rng = np.random.default_rng(14)
+    flat += rng.normal(0, 0.05, P)  # GN affine away from (1, 0)
+    p = models.unpack("rgbd", flat)
+    x = synth.rgbd_frames(rng, 1, 2, H=64, W=64)[0].astype(np.float64)  # [2][4][64][64] (smaller maps)
+    feat, caches = convnets.resnet50h_fwd(x, p)
+    pt = {k: _t(v, True) for k, v in p.items() if k.startswith("enc.")}
+    xt = _t(x, True)
+    ft = _TorchR50H(pt)(xt)
+    assert feat.shape == tuple(ft.shape)
+    assert np.max(np.abs(feat - ft.detach().numpy())) < 1e-10
+    dz = rng.normal(size=feat.shape)
+    (ft * _t(dz)).sum().backward()
+    g = {}
+    dx = convnets.resnet50h_bwd(dz, p, caches, g)
+    assert np.max(np.abs(dx - xt.grad.numpy())) < 1e-9 * max(1.0, np.abs(xt.grad.numpy()).max())
+    for k, v in pt.items():
+        assert np.max(np.abs(g[k] - v.grad.numpy())) < 1e-9 * max(1.0, np.abs(v.grad.numpy()).max()), k
+
+
+def test_rgbd_layout_size():
+    # half-width ResNet50 (bottlenecks 3/4/6/3) + compression + FC 2048->512 + 2-layer LSTM-512 + head
+    assert models.offsets("rgbd")[1] == 12459621
+
+
+def test_rgbd_model_finite_differences():
+    lay = models.layout("rgbd")
+    offs, P = models.offsets("rgbd")
+    ent = [(offs[n][0], int(np.prod(s)), f) for n, s, f in lay]
+    flat = synth.init_params(ent, P, 15).astype(np.float64)
+    ro = synth.rollout(1, 2, 16, obs_shape=(4, 256, 256), rnn_layers=2)
+    batch = {k: ro[k][:, :2] for k in ("goal", "prev_action", "mask")}
+    batch.update(obs=ro["obs"], h0=ro["h0"], c0=ro["c0"])
+    lin = {k: v.astype(np.float64) if v.dtype != np.int32 else v for k, v in synth.random_loss_inputs(2, 17).items()}
+
+    def loss(fl):
+        lg, v, cache = models.forward("rgbd", fl, batch)
+        st, dl, dv = ppo.loss_and_grad(lg.reshape(2, -1), v.reshape(-1), lin["actions"], lin["logp_old"],
+                                       lin["values_old"], lin["returns"], lin["adv"], np.ones(2, bool))
+        return st["total"], cache, dl.reshape(1, 2, -1), dv.reshape(1, 2)
+
+    L, cache, dl, dv = loss(flat)
+    g = models.backward("rgbd", flat, cache, dl, dv)
+    rng = np.random.default_rng(18)
+    for name in ["enc.stem.conv.weight", "enc.layer3.0.conv3.weight", "rnn.weight_hh_l0", "rnn.weight_ih_l1"]:
+        o, s = offs[name]
+        for i in rng.choice(int(np.prod(s)), 2, replace=False):
+            fp, fm = flat.copy(), flat.copy()
+            fp[o + i] += 1e-7
+            fm[o + i] -= 1e-7
+            fd = (loss(fp)[0] - loss(fm)[0]) / 2e-7
+            assert abs(fd - g[o + i]) < 1e-4 * max(abs(fd), 1e-3), (name, i, fd, g[o + i])
