@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps", "depth", "stress"])
+    ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps", "depth", "rgbd", "stress"])
     ap.add_argument("--seed", type=int, default=1337)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -124,7 +124,7 @@ def blas_threads():
 
 # The oracle's fp64 NumPy ResNet needs ~0.2 s per frame-step of the Depth agent: its bounded sample
 # keeps the configuration but shortens the rollouts (whole learner steps on E x ORACLE_T[cfg]).
-ORACLE_T = {"depth": 32, "stress": 8}
+ORACLE_T = {"depth": 32, "stress": 8, "rgbd": 2}
 
 
 def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None):
@@ -142,7 +142,8 @@ def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None):
     t0 = time.perf_counter()
     it = 0
     while True:
-        ro = synth.rollout(c["E"], c["T"], seed, rank=0, iteration=it, hidden=c["hidden"], obs_shape=c.get("obs"))
+        ro = synth.rollout(c["E"], c["T"], seed, rank=0, iteration=it, hidden=c["hidden"], obs_shape=c.get("obs"),
+                           rnn_layers=c.get("rnn_layers", 1))
         pm = synth.perms(seed, it, c["epochs"], c["E"])
         ts = time.perf_counter()
         p, m, v, step, info = olearner.learner_step(c["arch"], p, m, v, step, [ro], [pm],
@@ -183,11 +184,12 @@ def run_reference(args, rank, world):
 
 
 def workload_name(cfgname, c):
-    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2, "stress": 4}[cfgname]
+    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2, "rgbd": 3, "stress": 4}[cfgname]
     net = {"toy": "goal MLP(64, tanh) -> heads",
            "gps": "goal FC + action embedding -> GRU-512 -> heads",
-           "depth": "64x64 depth -> ResNet18/2 + GroupNorm -> FC 512; goal FC + action embedding -> LSTM-512 -> heads"
-           }[c["arch"]]
+           "depth": "64x64 depth -> ResNet18/2 + GroupNorm -> FC 512; goal FC + action embedding -> LSTM-512 -> heads",
+           "rgbd": "256x256 RGB-D -> avg-pool -> ResNet50/2 + GroupNorm -> FC 2048->512; goal FC + action embedding "
+                   "-> 2-layer LSTM-512 -> heads"}[c["arch"]]
     return (f"configs[{idx}] {cfgname}: {c['E']} envs/GPU x {c['T']} steps, {net}, "
             f"{c['epochs']} epochs x {c['minibatches']} minibatches, Adam")
 
@@ -242,7 +244,8 @@ def main():
             preempt["rollouts"].append({"ticks": ticks, "collected": int(cnt[0]), "preempted_steps": int(cnt[1]),
                                         "preempted_ranks": int(cnt[2]), "rank0_L": L_w})
     rollouts = [synth.rollout(c["E"], c["T"], args.seed, rank=rank, iteration=i, hidden=desc.hidden,
-                              obs_shape=c.get("obs"), length=lengths[i]) for i in range(n_roll)]
+                              obs_shape=c.get("obs"), length=lengths[i], rnn_layers=c.get("rnn_layers", 1))
+                for i in range(n_roll)]
     perms = [synth.perms(args.seed, i, c["epochs"], c["E"], rank=rank) for i in range(n_roll)]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
@@ -364,35 +367,43 @@ def main():
     return 0
 
 
-def depth_encoder_macs():
-    """Multiply-accumulates per frame of the Depth agent's encoder (64x64 -> ResNet18/2 -> 128x2x2)."""
-    macs, stem = 0, 0
+def depth_encoder_macs(arch="depth"):
+    """Multiply-accumulates per frame of the visual agents' encoders (depth: 64x64 -> ResNet18/2 ->
+    128x2x2; rgbd: 256x256 -> avg-pool -> ResNet50/2 -> 128x4x4)."""
+    macs = 0
 
     def conv(h, ci, co, k, s, p):
         nonlocal macs
         ho = (h + 2 * p - k) // s + 1
         macs += ho * ho * co * ci * k * k
         return ho
-    h = conv(64, 1, 32, 7, 2, 3)
+    rgbd = arch == "rgbd"
+    h = conv(128 if rgbd else 64, 4 if rgbd else 1, 32, 7, 2, 3)
     stem = macs
     h = (h + 2 - 3) // 2 + 1  # max-pool
     cin = 32
-    for li, c in enumerate((32, 64, 128, 256)):
-        for bi in range(2):
+    for li, w in enumerate((32, 64, 128, 256)):
+        for bi in range((3, 4, 6, 3)[li] if rgbd else 2):
             s = 2 if (bi == 0 and li > 0) else 1
-            h1 = conv(h, cin, c, 3, s, 1)
-            conv(h1, c, c, 3, 1, 1)
-            if s != 1 or cin != c:
-                conv(h, cin, c, 1, s, 0)
-            h, cin = h1, c
-    conv(h, 256, 128, 3, 1, 1)
+            cout = 4 * w if rgbd else w
+            if rgbd:
+                conv(h, cin, w, 1, 1, 0)
+                h1 = conv(h, w, w, 3, s, 1)
+                conv(h1, w, cout, 1, 1, 0)
+            else:
+                h1 = conv(h, cin, w, 3, s, 1)
+                conv(h1, w, w, 3, 1, 1)
+            if s != 1 or cin != cout:
+                conv(h, cin, cout, 1, s, 0)
+            h, cin = h1, cout
+    conv(h, cin, 128, 3, 1, 1)
     return {"all": macs, "stem": stem}
 
 
 def roofline_for(fam, prof, c, lrn, peaks, steps):
     """Algorithmic work of one launch of the dominant family / its mean device time."""
     ms, n = prof[fam]
-    if c["arch"] == "depth" and fam in ("net_fwd", "net_bwd"):
+    if c["arch"] in ("depth", "rgbd") and fam in ("net_fwd", "net_bwd"):
         n = steps * c["epochs"] * c["minibatches"]  # one "launch" = one minibatch pass of the family
     per_launch_s = (ms / 1e3) / max(n, 1)
     hbm = peaks.get("hbm_gbs", 6650.0)
@@ -408,20 +419,22 @@ def roofline_for(fam, prof, c, lrn, peaks, steps):
                 "frac": achieved / bf16, "traffic": None, "launch_us": per_launch_s * 1e6,
                 "note": "latency-bound dependency chain (B=2 envs x 128 steps on 16 SMs); per-step phases in "
                         "DESIGN.md sec. 7; HBM kernels' fractions in profiles/r01_microbench.jsonl"}
-    if fam in ("net_fwd", "net_bwd") and c["arch"] == "depth":
+    if fam in ("net_fwd", "net_bwd") and c["arch"] in ("depth", "rgbd"):
         # the family = one minibatch pass: encoder implicit GEMMs (+ GroupNorm / pool SIMT), FC,
         # LSTM input GEMM and recurrence; algorithmic FLOPs = the dense contractions, counted once
         # (the forward's bf16x3 operand planes cost 3 MMAs per product but count once here)
         frames = B * T
-        enc = depth_encoder_macs()
-        dense_fwd = 2.0 * (enc["all"] + 512 * 512 + 576 * 2048 + 2048 * H)
-        dense_bwd = 2.0 * (2 * enc["all"] - enc["stem"] + 2 * (512 * 512 + 576 * 2048) + 2 * 2048 * H)
+        enc = depth_encoder_macs(c["arch"])
+        fc_in, layers = (2048, 2) if c["arch"] == "rgbd" else (512, 1)
+        rnn_in = 576 * 2048 + (layers - 1) * H * 2048  # input GEMMs of the LSTM layers
+        dense_fwd = 2.0 * (enc["all"] + fc_in * 512 + rnn_in + layers * 2048 * H)
+        dense_bwd = 2.0 * (2 * enc["all"] - enc["stem"] + 2 * (fc_in * 512 + rnn_in) + 2 * layers * 2048 * H)
         flops = frames * (dense_fwd if fam == "net_fwd" else dense_bwd)
         achieved = flops / per_launch_s / 1e12
         return {"bound": "tensor", "kernel": fam, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
                 "frac": achieved / bf16, "traffic": None, "launch_us": per_launch_s * 1e6,
-                "note": "kernel family of one minibatch pass (ResNet18/2 implicit GEMMs + GroupNorm + LSTM-512 "
-                        "recurrence); per-kernel split in profiles/"}
+                "note": "kernel family of one minibatch pass (ResNet implicit GEMMs + GroupNorm + LSTM-512 "
+                        "recurrences); per-kernel split in profiles/"}
     byte_per = {"gae": 17.0 * E * T, "loss": 60.0 * B * T, "adam": 32.0 * lrn.P}
     b = byte_per.get(fam, 0.0)
     achieved = b / per_launch_s / 1e9 if b else 0.0

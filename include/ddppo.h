@@ -92,6 +92,10 @@ ddppo_status ddppo_adv_norm(ddppo_ctx* ctx, double* stats3, float eps, float* me
  *                         -> 128x2x2 -> flatten (c,h,w) -> Linear(512,512)+ReLU;
  *                        x = [visual, Linear(3,32)(goal), Embedding(A+1,32)] -> LSTM(576,
  *                        hidden=512) -> Linear(hidden, A+1)                      (configs[2])
+ *   DDPPO_ARCH_RGBD_R50_LSTM2 : RGB-D [4][256][256] (RGB in [0,255] normalised channel-wise,
+ *                        P:L367) -> 2x2 avg-pool -> half-width ResNet50 (bottlenecks 3/4/6/3,
+ *                        P:L212) -> 128x4x4 -> Linear(2048,512)+ReLU; [visual, goal, action] ->
+ *                        2-layer LSTM-512 -> Linear(hidden, A+1)                 (configs[3])
  * Flat parameter layout: the tensors below in this order, row-major, each starting at an
  * offset rounded up to a multiple of 4 floats (PyTorch shapes/conventions):
  *   TOY: fc1.weight[64][3] fc1.bias[64] head.weight[A+1][64] head.bias[A+1]
@@ -104,9 +108,16 @@ ddppo_status ddppo_adv_norm(ddppo_ctx* ctx, double* stats3, float eps, float* me
  *        conv weights [Co][Ci][k][k]), visual_fc.weight[512][512] visual_fc.bias[512],
  *        goal_fc.*, act_embed.weight[A+1][32], rnn.weight_ih[4H][576] rnn.weight_hh[4H][H]
  *        rnn.bias_ih[4H] rnn.bias_hh[4H] head.*       (LSTM gate rows i, f, g, o)
+ *   RGBD: enc.stem.conv.weight[32][4][7][7], enc.stem.gn.*, per bottleneck enc.layer{1..4}.{b}.
+ *        {conv1,gn1,conv2,gn2,conv3,gn3[,down.conv,down.gn]} (1x1, 3x3 with the stride, 1x1),
+ *        enc.compress.conv.weight[128][1024][3][3], enc.compress.gn.*, visual_fc.weight[512][2048]
+ *        visual_fc.bias, goal_fc.*, act_embed.*, rnn.{weight_ih,weight_hh,bias_ih,bias_hh}_l{0,1}
+ *        (weight_ih_l0 [4H][576], weight_ih_l1 [4H][H]), head.*
  * head rows 0..A-1 are the action logits, row A the value.  num_actions must be 4;
  * GPS requires hidden == 512. */
-typedef enum { DDPPO_ARCH_TOY_MLP = 0, DDPPO_ARCH_GPS_GRU = 1, DDPPO_ARCH_DEPTH_R18_LSTM = 2 } ddppo_arch;
+typedef enum {
+  DDPPO_ARCH_TOY_MLP = 0, DDPPO_ARCH_GPS_GRU = 1, DDPPO_ARCH_DEPTH_R18_LSTM = 2, DDPPO_ARCH_RGBD_R50_LSTM2 = 3
+} ddppo_arch;
 
 typedef struct {
   int32_t arch;        /* ddppo_arch */
@@ -138,14 +149,15 @@ typedef struct {
   const float* goal;          /* [E][T][3]   (d, cos th, sin th)            */
   const int32_t* prev_action; /* [E][ld]     start token = num_actions         */
   const float* mask;          /* [E][ld]     1 - done_{t-1}; state is multiplied by it */
-  const float* h0;            /* [E][hidden] recurrent state before step 0 (no grad)    */
+  const float* h0;            /* [E][layers*hidden] recurrent state before step 0 (no   */
+                              /* grad; layer-major; layers = 2 for RGBD, else 1)           */
   const int32_t* len;         /* [E]         valid steps per env                        */
   const int32_t* env_idx;     /* [B]         env ids of this minibatch                  */
   int32_t E, T, ld, B;
   int32_t T_run;              /* steps to run: max len over the minibatch (host value)  */
   int32_t n_valid;            /* sum over the B envs of min(len, T_run) (host value)    */
-  const float* obs;           /* [E][T][1][64][64] depth frames (DEPTH only, else NULL) */
-  const float* c0;            /* [E][hidden] LSTM cell state before step 0 (DEPTH only)   */
+  const float* obs;           /* DEPTH: [E][T][1][64][64]; RGBD: [E][T][4][256][256]; else NULL */
+  const float* c0;            /* LSTM cell state before step 0, like h0 (DEPTH / RGBD)      */
 } ddppo_batch;
 
 /* a5: logits [B][T_run][A], values [B][T_run]; saves activations in ws for the backward. */
@@ -242,8 +254,8 @@ typedef struct {
   const int32_t* host_len;    /* [E] host copy of len */
   const int32_t* host_perms;  /* [epochs][E] host copy of perms */
   int32_t E, T, ld;
-  const float* obs;           /* [E][T][1][64][64] (DEPTH only, else NULL) */
-  const float* c0;            /* [E][hidden]       (DEPTH only, else NULL) */
+  const float* obs;           /* as ddppo_batch::obs (DEPTH / RGBD, else NULL) */
+  const float* c0;            /* as ddppo_batch::c0  (DEPTH / RGBD, else NULL) */
 } ddppo_rollout;
 
 typedef struct {
@@ -300,19 +312,20 @@ ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const float* w, 
                                 size_t* host_need, void* stream);
 /* GroupNorm(16 groups, eps 1e-5) over y[F][HW][C]: z = (relu)(gamma*yhat + beta (+ residual)),
  * stats[F][16][2] = (mean, rstd); if dz != NULL: dy (rounded to bf16, the form the gradient GEMMs
- * consume), dgamma, dbeta (scratch: 2*F*C + F*HW*C/2 + 64 floats). */
+ * consume), dgamma, dbeta (scratch: 4*F*HW*C + 64*F + 1024 floats). */
 ddppo_status ddppo_debug_groupnorm(ddppo_ctx* ctx, const float* y, const float* gamma, const float* beta,
                                    const float* residual, int F, int HW, int C, int relu, float* z,
                                    float* stats, const float* dz, float* dy, float* dgamma,
                                    float* dbeta, float* scratch, void* stream);
-/* The Depth forward's discrete decisions, read from the workspace of the last ddppo_policy_fwd on
- * the same batch (bytes, NHWC): stem ReLU mask [F][32][32][32], max-pool argmax [F][16][16][32]
- * (window index 0..8), then per residual block (layer1.0 ... layer4.1) the conv1 ReLU mask and the
- * block-output ReLU mask, then the compression ReLU mask [F][2][2][128] and the visual-FC ReLU
+/* The visual agents' (DEPTH / RGBD) forward discrete decisions, read from the workspace of the last
+ * ddppo_policy_fwd on the same batch (bytes, NHWC): stem ReLU mask, max-pool argmax (window index
+ * 0..8), then per residual block in order the ReLU masks of its branch convolutions (conv1[, conv2])
+ * followed by the block-output ReLU mask, then the compression ReLU mask and the visual-FC ReLU
  * mask [F][512]; F = B*T_run.  out == NULL: only *host_n.  Lets a parity test hand the oracle's
  * backward the same decisions where a pre-activation sits within rounding of 0. */
-ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_batch* host_batch, void* ws,
-                                         uint8_t* out, int64_t cap, int64_t* host_n, void* stream);
+ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
+                                         const ddppo_batch* host_batch, void* ws, uint8_t* out, int64_t cap,
+                                         int64_t* host_n, void* stream);
 /* 3x3 / stride 2 / pad 1 max pool (first maximum in window order; arg = window index 0..8). */
 ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int F, int H, int W, int C, float* y,
                                  uint8_t* arg, const float* dy, float* dx, void* stream);

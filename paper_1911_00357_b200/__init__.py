@@ -8,7 +8,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import (ARCH_DEPTH, ARCH_GPS, ARCH_TOY, AdamCfg, Batch, DdppoError, LearnerCfg, LossCfg, LossInputs, ModelDesc,
+from ._lib import (ARCH_DEPTH, ARCH_GPS, ARCH_RGBD, ARCH_TOY, AdamCfg, Batch, DdppoError, LearnerCfg, LossCfg, LossInputs, ModelDesc,
                    PreemptCfg, Rollout, TensorInfo, check, dptr, f32, f64, i32, lib, u8)
 
 __all__ = ["Context", "model_desc", "param_layout", "ddppo_gae", "ddppo_adv_norm", "ddppo_policy_fwd",
@@ -25,7 +25,7 @@ def _stream(stream):
 
 
 def model_desc(arch, hidden=None, num_actions=4):
-    arch_id = {"toy": ARCH_TOY, "gps": ARCH_GPS, "depth": ARCH_DEPTH}.get(arch, arch)
+    arch_id = {"toy": ARCH_TOY, "gps": ARCH_GPS, "depth": ARCH_DEPTH, "rgbd": ARCH_RGBD}.get(arch, arch)
     if hidden is None:
         hidden = 64 if arch_id == ARCH_TOY else 512
     d = ModelDesc()
@@ -220,21 +220,21 @@ def ddppo_debug_conv2d(ctx, x, w, F, H, W, Ci, Co, k, s, p, y=None, dy=None, dx=
 def ddppo_debug_groupnorm(ctx, y, gamma, beta, F, HW, C, relu, z, stats, residual=None, dz=None, dy=None,
                           dgamma=None, dbeta=None, stream=None):
     import torch
-    scratch = torch.empty(2 * F * C + (F * HW * C + 1) // 2 + 64, dtype=torch.float32, device=y.device)
+    scratch = torch.empty(4 * F * HW * C + 64 * F + 1024, dtype=torch.float32, device=y.device)
     _call(ctx, "ddppo_debug_groupnorm", f32(y), f32(gamma), f32(beta), f32(residual), F, HW, C, int(relu), f32(z),
           f32(stats), f32(dz), f32(dy), f32(dgamma), f32(dbeta), f32(scratch), _stream(stream))
     return scratch
 
 
-def ddppo_debug_depth_decisions(ctx, batch, ws, stream=None):
+def ddppo_debug_depth_decisions(ctx, desc, batch, ws, stream=None):
     """uint8 CUDA tensor of the Depth forward's ReLU masks / max-pool argmax (include/ddppo.h order)."""
     import torch
     n = ctypes.c_int64()
-    _call(ctx, "ddppo_debug_depth_decisions", ctypes.byref(batch), dptr(ws), None, 0, ctypes.byref(n),
-          _stream(stream))
+    _call(ctx, "ddppo_debug_depth_decisions", ctypes.byref(desc), ctypes.byref(batch), dptr(ws), None, 0,
+          ctypes.byref(n), _stream(stream))
     out = torch.zeros(n.value, dtype=torch.uint8, device=ws.device)
-    _call(ctx, "ddppo_debug_depth_decisions", ctypes.byref(batch), dptr(ws), u8(out), n.value, None,
-          _stream(stream))
+    _call(ctx, "ddppo_debug_depth_decisions", ctypes.byref(desc), ctypes.byref(batch), dptr(ws), u8(out), n.value,
+          None, _stream(stream))
     return out
 
 

@@ -21,7 +21,7 @@ c_int, c_float, c_double, c_vp, c_i64 = ctypes.c_int, ctypes.c_float, ctypes.c_d
 c_i32, c_size = ctypes.c_int32, ctypes.c_size_t
 
 STATUS = {0: "ok", 1: "config", 2: "numerical", 3: "protocol", 4: "comm", 5: "cuda", 6: "unsupported"}
-ARCH_TOY, ARCH_GPS, ARCH_DEPTH = 0, 1, 2
+ARCH_TOY, ARCH_GPS, ARCH_DEPTH, ARCH_RGBD = 0, 1, 2, 3
 
 
 class DdppoError(RuntimeError):
@@ -110,7 +110,7 @@ _SIGS = {
                                    c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp, c_vp]),
     "ddppo_debug_groupnorm": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp,
                                       c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "ddppo_debug_depth_decisions": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "ddppo_debug_depth_decisions": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "ddppo_debug_maxpool": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 KERNEL_FAMILIES = ("gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other")

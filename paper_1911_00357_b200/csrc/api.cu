@@ -156,7 +156,7 @@ ddppo_status ddppo_workspace_size(const ddppo_model_desc* host_desc, int max_B, 
   if (!host_bytes || build_layout(host_desc, &L) != DDPPO_OK || max_B < 1 || T < 1) return DDPPO_ERR_CONFIG;
   *host_bytes = host_desc->arch == DDPPO_ARCH_TOY_MLP   ? toy_workspace(max_B, T)
                 : host_desc->arch == DDPPO_ARCH_GPS_GRU ? gps_workspace(max_B, T)
-                                                        : depth_workspace(max_B, T);
+                                                        : depth_workspace(host_desc->arch, max_B, T);
   return DDPPO_OK;
 }
 
@@ -183,8 +183,8 @@ ddppo_status ddppo_policy_fwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
   if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
     return toy_fwd(ctx, L, params, *host_batch, logits, values, ws, as_stream(stream));
   DDPPO_REQUIRE(ctx, host_batch->prev_action && host_batch->mask && host_batch->h0, "gps batch: null pointer");
-  if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM) {
-    DDPPO_REQUIRE(ctx, host_batch->obs && host_batch->c0, "depth batch: obs and c0 required");
+  if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2) {
+    DDPPO_REQUIRE(ctx, host_batch->obs && host_batch->c0, "visual agent batch: obs and c0 required");
     return depth_fwd(ctx, L, params, *host_batch, logits, values, ws, as_stream(stream));
   }
   return gps_fwd(ctx, L, params, *host_batch, logits, values, ws, as_stream(stream));
@@ -203,7 +203,7 @@ ddppo_status ddppo_policy_bwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
   DDPPO_REQUIRE(ctx, ws && ws_bytes >= need, "workspace too small");
   if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
     return toy_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
-  if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM)
+  if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2)
     return depth_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
   return gps_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
 }
@@ -354,8 +354,8 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
   DDPPO_REQUIRE(ctx, ro->host_len && ro->host_perms && ro->perms, "learner_step: lengths/perms required");
   DDPPO_REQUIRE(ctx, cfg->minibatches >= 1 && ro->E % cfg->minibatches == 0 && cfg->epochs >= 1,
                 "learner_step: minibatches must divide E (S:L155)");
-  DDPPO_REQUIRE(ctx, host_desc->arch != DDPPO_ARCH_DEPTH_R18_LSTM || (ro->obs && ro->c0),
-                "learner_step: the depth agent needs obs and c0");
+  const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
+  DDPPO_REQUIRE(ctx, !visual || (ro->obs && ro->c0), "learner_step: the visual agents need obs and c0");
   size_t need = 0;
   ddppo_status s =
       ddppo_learner_workspace_size(host_desc, ro->E, ro->T, ro->ld, cfg->minibatches, cfg->epochs, &need);
@@ -407,7 +407,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
       b.c0 = ro->c0;
       if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
         s = toy_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
-      else if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM)
+      else if (visual)
         s = depth_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
       else
         s = gps_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
@@ -418,7 +418,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
       if (s != DDPPO_OK) return s;
       if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
         s = toy_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
-      else if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM)
+      else if (visual)
         s = depth_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
       else
         s = gps_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);

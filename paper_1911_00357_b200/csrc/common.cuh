@@ -256,7 +256,7 @@ ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st);
 struct ModelLayout {
   int64_t P = 0;
   int n = 0;
-  ddppo_tensor_info t[96];
+  ddppo_tensor_info t[192];
 };
 ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out);
 int64_t layout_offset(const ModelLayout& L, const char* name);
@@ -273,7 +273,7 @@ ddppo_status launch_head_bwd(ddppo_ctx* ctx, const float* Wo, const float* Hs, c
                              const float* dvalues, int S, float* dH, float* dWo, float* dbo, cudaStream_t st);
 ddppo_status launch_colsum(ddppo_ctx* ctx, const float* A, int lda, int S, int M, float* out, cudaStream_t st);
 
-size_t depth_workspace(int max_B, int T);
+size_t depth_workspace(int arch, int max_B, int T);
 ddppo_status depth_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                        float* logits, float* values, void* ws, cudaStream_t st);
 ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
@@ -286,10 +286,11 @@ struct LstmPtrs {
   const float* bhh;    // [2048]
   const float* GI;     // [S][2048]  W_ih x (no bias)
   const float* mask;   // [E][ld]
-  const float* h0;     // [E][512]
-  const float* c0;     // [E][512]
+  const float* h0;     // [E][sld] (this layer's 512 entries at the pointer)
+  const float* c0;     // [E][sld]
   const int32_t* env_idx;
   int B, T_run, ld;
+  int sld;             // env stride of h0 / c0 (512 * layers)
   float* Hs;           // [S][512] h_t
   float* Hin;          // [S][512] mask_t h_{t-1}
   float* Cin;          // [S][512] mask_t c_{t-1}

@@ -1,6 +1,9 @@
-// Depth agent (BASELINE configs[2]): 64x64 depth -> half-width ResNet18 with GroupNorm -> 128x2x2
-// -> FC 512 + ReLU; x = [visual, goal FC 32, action embedding 32] -> LSTM-512 -> Linear(512, 5).
-// (P:L212 half-width backbone with GroupNorm, App. C; readings Z17-Z23 in DESIGN.md.)
+// Visual agents (P:L212 half-width backbones with GroupNorm, App. C; readings Z17-Z23, R5,
+// R7 in DESIGN.md):
+//   Depth (configs[2]): 64x64 depth -> ResNet18/2 -> 128x2x2 -> FC 512 + ReLU; x = [visual, goal FC
+//     32, action embedding 32] -> LSTM-512 -> Linear(512, 5).
+//   RGB-D (configs[3]): 4x256x256 (RGB normalised channel-wise) -> 2x2 avg-pool -> ResNet50/2
+//     (bottlenecks 3/4/6/3) -> 128x4x4 -> FC 2048->512 + ReLU; same x -> 2-layer LSTM-512 -> head.
 //
 // Layout: activations fp32 NHWC [frames][H][W][C] in the workspace, frames f = b*T_run + t.
 // Convolutions are implicit GEMMs on the tcgen05 kernel of gemm_tc.cu (the im2col matrix is
@@ -21,7 +24,8 @@
 namespace {
 
 constexpr int kH = 512, kG4 = 2048, kXin = 576, kA1 = 5, kGroups = 16, kThreads = 256;
-constexpr int kImg = 64;  // input resolution (configs[2])
+constexpr int kImg = 64;        // Depth input resolution (configs[2])
+constexpr int kImgRgbd = 256;   // RGB-D input resolution (configs[3])
 
 // ------------------------------------------------------------------ kernels
 // obs [E][T][1][64][64] (gathered through env_idx) -> x0 [F][64][64][1]
@@ -33,6 +37,35 @@ __global__ void gather_obs_kernel(const float* __restrict__ obs, const int32_t* 
     const int f = (int)(i / per);
     const int b = f / T_run, t = f - b * T_run;
     x0[i] = obs[((size_t)env_idx[b] * T + t) * per + (i % per)];
+  }
+}
+
+// RGB-D prologue: obs [E][T][4][256][256] -> channel-wise RGB normalisation, 2x2 average
+// pooling -> x0 [F][128][128][8] fp32 NHWC (channels 4..7 zero: the stem's implicit GEMM reads 8
+// channels per 16-byte piece) and its bf16 hi / lo planes
+__constant__ float kRgbMean[3] = {0.485f * 255.f, 0.456f * 255.f, 0.406f * 255.f};
+__constant__ float kRgbStd[3] = {0.229f * 255.f, 0.224f * 255.f, 0.225f * 255.f};
+__global__ void rgbd_prologue_kernel(const float* __restrict__ obs, const int32_t* __restrict__ env_idx, int T,
+                                     int T_run, int F, int Hin, float* __restrict__ x0, __nv_bfloat16* __restrict__ x0b) {
+  const int Ho = Hin / 2, Wo = Hin / 2;
+  const size_t n = (size_t)F * Ho * Wo * 8;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i & 7);
+    const size_t pix = i >> 3;
+    const int j = (int)(pix % Wo), ii = (int)((pix / Wo) % Ho), f = (int)(pix / ((size_t)Wo * Ho));
+    float v = 0.f;
+    if (c < 4) {
+      const int b = f / T_run, t = f - b * T_run;
+      const float* src = obs + (((size_t)env_idx[b] * T + t) * 4 + c) * Hin * Hin;
+      const int y = 2 * ii, x = 2 * j;
+      const float m = c < 3 ? kRgbMean[c] : 0.f, inv = c < 3 ? 1.f / kRgbStd[c] : 1.f;
+      v = 0.25f * (((src[y * Hin + x] - m) * inv + (src[y * Hin + x + 1] - m) * inv) +
+                   ((src[(y + 1) * Hin + x] - m) * inv + (src[(y + 1) * Hin + x + 1] - m) * inv));
+    }
+    x0[i] = v;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    x0b[i] = hi;
+    x0b[n + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
   }
 }
 
@@ -54,36 +87,37 @@ __global__ void weights_bf16_kernel(const float* __restrict__ W, int Co, int Ci,
     if (wd) wd[c * (k * k * Co) + uv * Co + o] = hi;
   }
 }
-// all convolutions' weights of one minibatch in one launch (blockIdx.y = convolution)
-constexpr int kMaxConvs = 24;
+// all convolutions' weights of one minibatch in one launch (blockIdx.y = convolution); Cp >= Ci is
+// the padded channel count of the GEMM operand (extra channels get zero weights)
+constexpr int kMaxConvs = 64;
 struct WeightPrep {
   int n;
   struct Item {
     const float* W;
-    __nv_bfloat16 *wr, *wd;
-    int Co, Ci, k;
+    __nv_bfloat16 *wr, *wd;  // wd nullable (no input gradient)
+    int Co, Ci, Cp, k;
   } it[kMaxConvs];
 };
 __global__ void weights_prep_kernel(const WeightPrep prep) {
   const WeightPrep::Item& t = prep.it[blockIdx.y];
-  const int Co = t.Co, Ci = t.Ci, k = t.k, n = Co * Ci * k * k;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int o = i / (Ci * k * k), rem = i % (Ci * k * k);
-    const int c = rem / (k * k), uv = rem % (k * k);
-    const float w = t.W[i];
+  const int Co = t.Co, Ci = t.Ci, Cp = t.Cp, kk = t.k * t.k, n = Co * Cp * kk;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int o = j / (kk * Cp), rem = j % (kk * Cp), uv = rem / Cp, c = rem % Cp;  // j = Wr index
+    const float w = c < Ci ? t.W[(o * Ci + c) * kk + uv] : 0.f;
     const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-    t.wr[o * (k * k * Ci) + uv * Ci + c] = hi;
-    t.wr[n + o * (k * k * Ci) + uv * Ci + c] = __float2bfloat16_rn(w - __bfloat162float(hi));
-    t.wd[c * (k * k * Co) + uv * Co + o] = hi;
+    t.wr[j] = hi;
+    t.wr[n + j] = __float2bfloat16_rn(w - __bfloat162float(hi));
+    if (t.wd && c < Ci) t.wd[c * (kk * Co) + uv * Co + o] = hi;
   }
 }
-// weight gradient: dWt [(u, v, c)][o] (the wgrad GEMM's output) -> dW [Co][Ci][k][k]
-__global__ void wgrad_to_torch_kernel(const float* __restrict__ dwt, int Co, int Ci, int k, float* __restrict__ dw) {
+// weight gradient: dWt [(u, v, c)][o] (the wgrad GEMM's output, c < Cp) -> dW [Co][Ci][k][k]
+__global__ void wgrad_to_torch_kernel(const float* __restrict__ dwt, int Co, int Ci, int Cp, int k,
+                                      float* __restrict__ dw) {
   const int n = Co * Ci * k * k;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int o = i / (Ci * k * k), rem = i % (Ci * k * k);
     const int c = rem / (k * k), uv = rem % (k * k);
-    dw[i] = dwt[(size_t)(uv * Ci + c) * Co + o];
+    dw[i] = dwt[(size_t)(uv * Cp + c) * Co + o];
   }
 }
 // fp32 -> bf16 hi / lo planes (plane = n)
@@ -217,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) frame_sum_kernel(const float* __rest
 // GroupNorm (G = 16, eps 1e-5), one block per frame.  The block walks the frame's [HW][C] slab
 // contiguously (coalesced); with 256 % C == 0 thread t always sees channel t % C, so per-group and
 // per-channel partial sums are per-thread sums combined in a fixed order through shared memory.
-constexpr int kGnThreads = 256;
+constexpr int kGnMaxThreads = 1024;  // blockDim = max(256, C): a multiple of C
 
 // per-group sums of the threads' (a, b) in fixed order -> out[g] (threads t < 16 write)
 __device__ __forceinline__ void gn_group_reduce(double a, double b, int C, double* sa, double* sb, double* out_a,
@@ -228,7 +262,7 @@ __device__ __forceinline__ void gn_group_reduce(double a, double b, int C, doubl
   if (threadIdx.x < kGroups) {
     const int cg = C / kGroups, g = threadIdx.x;
     double ra = 0.0, rb = 0.0;
-    for (int rep = 0; rep < kGnThreads / C; ++rep)
+    for (int rep = 0; rep < (int)blockDim.x / C; ++rep)
       for (int cc = 0; cc < cg; ++cc) {
         const int t = rep * C + g * cg + cc;
         ra += sa[t];
@@ -242,17 +276,17 @@ __device__ __forceinline__ void gn_group_reduce(double a, double b, int C, doubl
 
 // z = (relu)(gamma * (y - mu) * rstd + beta (+ residual)); stats[f][g] = (mu, rstd) (biased variance);
 // zb (nullable): z as bf16 hi / lo planes (plane = F*HW*C)
-__global__ void __launch_bounds__(kGnThreads) gn_fwd_kernel(const float* __restrict__ y, const float* __restrict__ gamma,
+__global__ void __launch_bounds__(kGnMaxThreads) gn_fwd_kernel(const float* __restrict__ y, const float* __restrict__ gamma,
                                                             const float* __restrict__ beta,
                                                             const float* __restrict__ residual, int HW, int C,
                                                             int relu, size_t plane, float* __restrict__ stats,
                                                             float* __restrict__ z, __nv_bfloat16* __restrict__ zb) {
-  __shared__ double sa[kGnThreads], sb[kGnThreads], ga[kGroups], gb[kGroups];
+  __shared__ double sa[kGnMaxThreads], sb[kGnMaxThreads], ga[kGroups], gb[kGroups];
   __shared__ float smu[kGroups], srs[kGroups];
   const int f = blockIdx.x, n = HW * C, c = threadIdx.x % C, cg = C / kGroups;
   const size_t base = (size_t)f * n;
   double s1 = 0.0, s2 = 0.0;
-  for (int e = threadIdx.x; e < n; e += kGnThreads) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const float v = y[base + e];
     s1 += v;
     s2 += (double)v * v;
@@ -269,7 +303,7 @@ __global__ void __launch_bounds__(kGnThreads) gn_fwd_kernel(const float* __restr
   }
   __syncthreads();
   const float mu = smu[c / cg], rs = srs[c / cg], gm = gamma[c], bt = beta[c];
-  for (int e = threadIdx.x; e < n; e += kGnThreads) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const size_t i = base + e;
     float v = (y[i] - mu) * rs * gm + bt;
     if (residual) v += residual[i];
@@ -287,19 +321,19 @@ __global__ void __launch_bounds__(kGnThreads) gn_fwd_kernel(const float* __restr
 //   dx = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),   dxhat = dy_eff * gamma
 // written as bf16 (it only feeds the bf16 gradient GEMMs), plus this frame's per-channel partials
 // part[f][c] = (sum dy_eff * xhat, sum dy_eff) for dgamma / dbeta.
-__global__ void __launch_bounds__(kGnThreads) gn_bwd_kernel(const float* __restrict__ dz, const float* __restrict__ z,
+__global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_kernel(const float* __restrict__ dz, const float* __restrict__ z,
                                                             const float* __restrict__ y,
                                                             const float* __restrict__ stats,
                                                             const float* __restrict__ gamma, int HW, int C,
                                                             __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
-  __shared__ double sa[kGnThreads], sb[kGnThreads], ga[kGroups], gb[kGroups];
-  __shared__ float pc[2][kGnThreads];
+  __shared__ double sa[kGnMaxThreads], sb[kGnMaxThreads], ga[kGroups], gb[kGroups];
+  __shared__ float pc[2][kGnMaxThreads];
   const int f = blockIdx.x, n = HW * C, c = threadIdx.x % C, cg = C / kGroups, g = c / cg;
   const size_t base = (size_t)f * n;
   const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
   double a1 = 0.0, a2 = 0.0;
   float pg = 0.f, pb = 0.f;
-  for (int e = threadIdx.x; e < n; e += kGnThreads) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const size_t i = base + e;
     float d = dz[i];
     if (z && z[i] <= 0.f) d = 0.f;
@@ -314,7 +348,7 @@ __global__ void __launch_bounds__(kGnThreads) gn_bwd_kernel(const float* __restr
   gn_group_reduce(a1, a2, C, sa, sb, ga, gb);  // (its barriers also publish pc)
   if (threadIdx.x < C) {
     float rg = 0.f, rb = 0.f;
-    for (int t = threadIdx.x; t < kGnThreads; t += C) {
+    for (int t = threadIdx.x; t < (int)blockDim.x; t += C) {
       rg += pc[0][t];
       rb += pc[1][t];
     }
@@ -323,7 +357,161 @@ __global__ void __launch_bounds__(kGnThreads) gn_bwd_kernel(const float* __restr
   }
   const double cnt = (double)HW * cg;
   const float m1 = (float)(ga[g] / cnt), m2 = (float)(gb[g] / cnt);
-  for (int e = threadIdx.x; e < n; e += kGnThreads) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const size_t i = base + e;
+    float d = dz[i];
+    if (z && z[i] <= 0.f) d = 0.f;
+    const float xh = (y[i] - mu) * rs;
+    dx[i] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
+  }
+}
+
+// Large frames: the [HW][C] slab of a frame is split into S chunks of gn_chunk(C) elements, one
+// block each (grid (S, F)).  Pass 1 writes per-chunk per-group partial sums (double), pass 2 reduces
+// the frame's S partials in chunk order, then normalises / back-propagates its chunk.
+__host__ __device__ inline int gn_threads(int C) { return C > 256 ? C : 256; }
+__host__ __device__ inline int gn_chunk(int C) { return gn_threads(C) * 32; }
+
+__global__ void __launch_bounds__(kGnMaxThreads) gn_stats_part_kernel(const float* __restrict__ y, int HW, int C,
+                                                                      double* __restrict__ gpart) {
+  __shared__ double sa[kGnMaxThreads], sb[kGnMaxThreads], ga[kGroups], gb[kGroups];
+  const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C);
+  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
+  const size_t base = (size_t)f * n;
+  double s1 = 0.0, s2 = 0.0;
+  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const float v = y[base + e];
+    s1 += v;
+    s2 += (double)v * v;
+  }
+  gn_group_reduce(s1, s2, C, sa, sb, ga, gb);
+  if (threadIdx.x < kGroups) {
+    double* o = gpart + (((size_t)f * S + blockIdx.x) * kGroups + threadIdx.x) * 2;
+    o[0] = ga[threadIdx.x];
+    o[1] = gb[threadIdx.x];
+  }
+}
+
+__global__ void __launch_bounds__(kGnMaxThreads) gn_apply_part_kernel(const float* __restrict__ y,
+                                                                      const double* __restrict__ gpart,
+                                                                      const float* __restrict__ gamma,
+                                                                      const float* __restrict__ beta,
+                                                                      const float* __restrict__ residual, int HW,
+                                                                      int C, int relu, size_t plane,
+                                                                      float* __restrict__ stats, float* __restrict__ z,
+                                                                      __nv_bfloat16* __restrict__ zb) {
+  __shared__ float smu[kGroups], srs[kGroups];
+  const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C), cg = C / kGroups;
+  if (threadIdx.x < kGroups) {
+    double a = 0.0, b = 0.0;
+    for (int s = 0; s < S; ++s) {
+      const double* o = gpart + (((size_t)f * S + s) * kGroups + threadIdx.x) * 2;
+      a += o[0];
+      b += o[1];
+    }
+    const double cnt = (double)HW * cg, mu = a / cnt;
+    double var = b / cnt - mu * mu;
+    if (var < 0) var = 0;
+    smu[threadIdx.x] = (float)mu;
+    srs[threadIdx.x] = (float)(1.0 / sqrt(var + 1e-5));
+    if (blockIdx.x == 0) {
+      stats[(f * kGroups + threadIdx.x) * 2] = smu[threadIdx.x];
+      stats[(f * kGroups + threadIdx.x) * 2 + 1] = srs[threadIdx.x];
+    }
+  }
+  __syncthreads();
+  const int c = threadIdx.x % C;
+  const float mu = smu[c / cg], rs = srs[c / cg], gm = gamma[c], bt = beta[c];
+  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
+  const size_t base = (size_t)f * n;
+  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const size_t i = base + e;
+    float v = (y[i] - mu) * rs * gm + bt;
+    if (residual) v += residual[i];
+    v = relu ? fmaxf(v, 0.f) : v;
+    z[i] = v;
+    if (zb) {
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      zb[i] = hi;
+      zb[plane + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
+  }
+}
+
+// backward pass 1: per chunk, per group (sum dxhat, sum dxhat*xhat) and per channel (sum dy*xhat, sum dy)
+__global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_part_kernel(const float* __restrict__ dz,
+                                                                    const float* __restrict__ z,
+                                                                    const float* __restrict__ y,
+                                                                    const float* __restrict__ stats,
+                                                                    const float* __restrict__ gamma, int HW, int C,
+                                                                    double* __restrict__ gpart,
+                                                                    float* __restrict__ part) {
+  __shared__ double sa[kGnMaxThreads], sb[kGnMaxThreads], ga[kGroups], gb[kGroups];
+  __shared__ float pc[2][kGnMaxThreads];
+  const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C), c = threadIdx.x % C, cg = C / kGroups,
+            g = c / cg;
+  const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
+  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
+  const size_t base = (size_t)f * n;
+  double a1 = 0.0, a2 = 0.0;
+  float pg = 0.f, pb = 0.f;
+  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const size_t i = base + e;
+    float d = dz[i];
+    if (z && z[i] <= 0.f) d = 0.f;
+    const float xh = (y[i] - mu) * rs, dxh = d * gm;
+    a1 += dxh;
+    a2 += (double)dxh * xh;
+    pg += d * xh;
+    pb += d;
+  }
+  pc[0][threadIdx.x] = pg;
+  pc[1][threadIdx.x] = pb;
+  gn_group_reduce(a1, a2, C, sa, sb, ga, gb);
+  if (threadIdx.x < kGroups) {
+    double* o = gpart + (((size_t)f * S + blockIdx.x) * kGroups + threadIdx.x) * 2;
+    o[0] = ga[threadIdx.x];
+    o[1] = gb[threadIdx.x];
+  }
+  if (threadIdx.x < C) {
+    float rg = 0.f, rb = 0.f;
+    for (int t = threadIdx.x; t < (int)blockDim.x; t += C) {
+      rg += pc[0][t];
+      rb += pc[1][t];
+    }
+    const size_t row = (size_t)f * S + blockIdx.x;  // rows of the dgamma / dbeta reduction
+    part[(row * C + threadIdx.x) * 2] = rg;
+    part[(row * C + threadIdx.x) * 2 + 1] = rb;
+  }
+}
+
+__global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_apply_kernel(const float* __restrict__ dz,
+                                                                     const float* __restrict__ z,
+                                                                     const float* __restrict__ y,
+                                                                     const float* __restrict__ stats,
+                                                                     const float* __restrict__ gamma,
+                                                                     const double* __restrict__ gpart, int HW, int C,
+                                                                     __nv_bfloat16* __restrict__ dx) {
+  __shared__ float sm1[kGroups], sm2[kGroups];
+  const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C), cg = C / kGroups;
+  if (threadIdx.x < kGroups) {
+    double a = 0.0, b = 0.0;
+    for (int s = 0; s < S; ++s) {
+      const double* o = gpart + (((size_t)f * S + s) * kGroups + threadIdx.x) * 2;
+      a += o[0];
+      b += o[1];
+    }
+    const double cnt = (double)HW * cg;
+    sm1[threadIdx.x] = (float)(a / cnt);
+    sm2[threadIdx.x] = (float)(b / cnt);
+  }
+  __syncthreads();
+  const int c = threadIdx.x % C, g = c / cg;
+  const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
+  const float m1 = sm1[g], m2 = sm2[g];
+  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
+  const size_t base = (size_t)f * n;
+  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const size_t i = base + e;
     float d = dz[i];
     if (z && z[i] <= 0.f) d = 0.f;
@@ -407,13 +595,15 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* 
   }
 }
 
-// NHWC [F][2][2][128] <-> flat [F][512] in (c, h, w) order (PyTorch flatten of NCHW)
-__global__ void flatten_kernel(const float* __restrict__ in, int F, float* __restrict__ out, int to_flat) {
-  const size_t n = (size_t)F * 512;
+// NHWC [F][HW][C] <-> flat [F][C*HW] in (c, h, w) order (PyTorch flatten of NCHW)
+__global__ void flatten_kernel(const float* __restrict__ in, int F, int HW, int C, float* __restrict__ out,
+                               int to_flat) {
+  const int per = HW * C;
+  const size_t n = (size_t)F * per;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int f = (int)(i / 512), q = (int)(i % 512);
-    const int c = q / 4, hw = q % 4;
-    const size_t nhwc = (size_t)f * 512 + hw * 128 + c;
+    const int f = (int)(i / per), q = (int)(i % per);
+    const int c = q / HW, hw = q % HW;
+    const size_t nhwc = (size_t)f * per + hw * C + c;
     if (to_flat) out[i] = in[nhwc];
     else out[nhwc] = in[i];
   }
@@ -508,7 +698,8 @@ __global__ void relu_mask_kernel(const float* __restrict__ dz, const float* __re
 
 // ------------------------------------------------------------------ network plan
 struct ConvGN {
-  int Ci, Co, k, s, p, H, W, Ho, Wo;  // input H x W, output Ho x Wo
+  int Ci, Co, k, s, p, H, W, Ho, Wo;  // GEMM geometry: input H x W x Ci (Ci padded to 8 for the RGB-D stem)
+  int Ci_real;                        // channels of the parameter tensor
   int64_t w, gw, gb;                  // parameter offsets (conv weight, GN gamma, GN beta)
   float *x, *y, *z, *stats;           // input (not owned), conv out (pre-GN), GN out, GN stats [F][16][2]
   __nv_bfloat16 *xb, *zb;             // input / output as bf16 hi / lo planes (GEMM operands; zb may be null)
@@ -516,21 +707,27 @@ struct ConvGN {
 };
 
 struct Plan {
-  int F = 0;
-  std::vector<ConvGN> convs;  // stem, per block: conv1, conv2, [down], compress
+  bool rgbd = false;
+  int F = 0, layers = 1, fc_in = 512, feat_hw = 4;
+  std::vector<ConvGN> convs;  // stem, per block: main-branch convs, [down], compress
   struct Block {
-    int c1, c2, down;        // indices into convs (down = -1: identity shortcut)
+    std::vector<int> main;   // convs of the residual branch (ReLU after all but the last)
+    int down;                // shortcut conv (-1: identity)
     float *in, *out;         // block input, block output (after residual + ReLU)
   };
   std::vector<Block> blocks;
   float *x0, *pool_out;
-  __nv_bfloat16* pool_b;
+  __nv_bfloat16 *x0b, *pool_b;
   uint8_t* pool_arg;
-  float *flat, *vis, *xin, *GI;
-  float *Hs, *Hin, *Cin, *Cs, *IFGO, *dH, *dG;
+  int pool_hw = 0;
+  float *flat, *vis, *xin;
+  struct Rnn {
+    float *GI, *Hs, *Hin, *Cin, *Cs, *IFGO, *dH, *dG;
+  } rnn[2];
   // scratch (reused by every layer)
-  __nv_bfloat16 *wr_b, *wd_b, *dyb;   // weights as GEMM operands; GN-backward output (bf16)
+  __nv_bfloat16* dyb;         // GN-backward output (bf16)
   float *dwt, *part, *gn_part, *dz_a, *dz_b, *dz_c, *dxin, *dflat, *dvis;
+  double* gn_gpart;           // GroupNorm per-chunk group partials (large frames)
   size_t bytes = 0;
 };
 
@@ -539,11 +736,15 @@ int64_t off_of(const ModelLayout& L, const std::string& n) { return layout_offse
 constexpr int kMaxSplits = 64;
 
 // Deterministic carve of the workspace (base == nullptr: size only)
-void make_plan(const ModelLayout& L, int B, int T_run, void* base, Plan* plan) {
+void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Plan* plan) {
   Plan& P = *plan;
   P = Plan();
   const int F = B * T_run;
   P.F = F;
+  P.rgbd = rgbd;
+  P.layers = rgbd ? 2 : 1;
+  P.fc_in = rgbd ? 2048 : 512;
+  P.feat_hw = rgbd ? 16 : 4;
   size_t off = 0;
   auto take_bytes = [&](size_t bytes) {
     char* p = base ? reinterpret_cast<char*>(base) + off : nullptr;
@@ -552,19 +753,20 @@ void make_plan(const ModelLayout& L, int B, int T_run, void* base, Plan* plan) {
   };
   auto take = [&](size_t n) { return reinterpret_cast<float*>(take_bytes(n * sizeof(float))); };
   auto take_b = [&](size_t n) { return reinterpret_cast<__nv_bfloat16*>(take_bytes(n * sizeof(__nv_bfloat16))); };
-  size_t max_act = 0, max_w = 0;
-  auto add_conv = [&](const std::string& cname, const std::string& gname, int Ci, int Co, int k, int s, int p, int H,
-                      int W, float* x, __nv_bfloat16* xb, bool planes_out) {
+  size_t max_act = 0, max_w = 0, max_gn_rows = 0, max_gn_part = 0;
+  auto add_conv = [&](const std::string& cname, const std::string& gname, int Ci, int Ci_real, int Co, int k, int s,
+                      int p, int H, float* x, __nv_bfloat16* xb, bool planes_out, bool needs_dx) {
     ConvGN c;
     c.Ci = Ci;
+    c.Ci_real = Ci_real;
     c.Co = Co;
     c.k = k;
     c.s = s;
     c.p = p;
     c.H = H;
-    c.W = W;
+    c.W = H;
     c.Ho = (H + 2 * p - k) / s + 1;
-    c.Wo = (W + 2 * p - k) / s + 1;
+    c.Wo = c.Ho;
     c.w = off_of(L, cname + ".weight");
     c.gw = off_of(L, gname + ".weight");
     c.gb = off_of(L, gname + ".bias");
@@ -577,16 +779,29 @@ void make_plan(const ModelLayout& L, int B, int T_run, void* base, Plan* plan) {
     c.stats = take((size_t)F * kGroups * 2);
     const size_t nw = (size_t)Co * k * k * Ci;
     c.wr_b = Ci > 1 ? take_b(2 * nw) : nullptr;
-    c.wd_b = Ci > 1 ? take_b(nw) : nullptr;
-    max_act = std::max(max_act, std::max(act, (size_t)F * H * W * Ci));
-    max_w = std::max(max_w, (size_t)Co * k * k * Ci);
+    c.wd_b = (Ci > 1 && needs_dx) ? take_b(nw) : nullptr;
+    max_act = std::max(max_act, std::max(act, (size_t)F * H * H * Ci));
+    max_w = std::max(max_w, nw);
+    const size_t S = ((size_t)c.Ho * c.Wo * Co + gn_chunk(Co) - 1) / gn_chunk(Co);
+    max_gn_rows = std::max(max_gn_rows, (size_t)F * S);
+    max_gn_part = std::max(max_gn_part, (size_t)F * S * Co * 2);
     P.convs.push_back(c);
     return (int)P.convs.size() - 1;
   };
-  P.x0 = take((size_t)F * kImg * kImg);
-  const int stem = add_conv("enc.stem.conv", "enc.stem.gn", 1, 32, 7, 2, 3, kImg, kImg, P.x0, nullptr, false);
-  const int hs = P.convs[stem].Ho;  // 32
-  const int hp = (hs + 2 - 3) / 2 + 1;  // 16
+  int stem;
+  if (!rgbd) {
+    P.x0 = take((size_t)F * kImg * kImg);
+    P.x0b = nullptr;
+    stem = add_conv("enc.stem.conv", "enc.stem.gn", 1, 1, 32, 7, 2, 3, kImg, P.x0, nullptr, false, false);
+  } else {
+    const int h0 = kImgRgbd / 2;  // after the 2x2 average pool
+    P.x0 = take((size_t)F * h0 * h0 * 8);
+    P.x0b = take_b((size_t)2 * F * h0 * h0 * 8);
+    stem = add_conv("enc.stem.conv", "enc.stem.gn", 8, 4, 32, 7, 2, 3, h0, P.x0, P.x0b, false, false);
+  }
+  const int hs = P.convs[stem].Ho;
+  const int hp = (hs + 2 - 3) / 2 + 1;
+  P.pool_hw = hp;
   P.pool_out = take((size_t)F * hp * hp * 32);
   P.pool_b = take_b((size_t)2 * F * hp * hp * 32);
   P.pool_arg = reinterpret_cast<uint8_t*>(take_bytes((size_t)F * hp * hp * 32));
@@ -594,50 +809,66 @@ void make_plan(const ModelLayout& L, int B, int T_run, void* base, Plan* plan) {
   __nv_bfloat16* zb = P.pool_b;
   int H = hp, cin = 32;
   const int widths[4] = {32, 64, 128, 256};
+  const int nblocks[4] = {3, 4, 6, 3};
   for (int li = 0; li < 4; ++li) {
-    for (int bi = 0; bi < 2; ++bi) {
-      const int s = (bi == 0 && li > 0) ? 2 : 1, c = widths[li];
+    for (int bi = 0; bi < (rgbd ? nblocks[li] : 2); ++bi) {
+      const int s = (bi == 0 && li > 0) ? 2 : 1, w = widths[li], cout = rgbd ? 4 * w : w;
       const std::string pre = "enc.layer" + std::to_string(li + 1) + "." + std::to_string(bi);
       Plan::Block blk;
       blk.in = z;
-      blk.c1 = add_conv(pre + ".conv1", pre + ".gn1", cin, c, 3, s, 1, H, H, z, zb, true);
-      const int Ho = P.convs[blk.c1].Ho;
-      blk.c2 = add_conv(pre + ".conv2", pre + ".gn2", c, c, 3, 1, 1, Ho, Ho, P.convs[blk.c1].z, P.convs[blk.c1].zb,
-                        true);
-      blk.down = (s != 1 || cin != c)
-                     ? add_conv(pre + ".down.conv", pre + ".down.gn", cin, c, 1, s, 0, H, H, z, zb, false)
+      int Ho;
+      if (!rgbd) {  // BasicBlock: 3x3 (stride) -> 3x3
+        const int c1 = add_conv(pre + ".conv1", pre + ".gn1", cin, cin, w, 3, s, 1, H, z, zb, true, true);
+        Ho = P.convs[c1].Ho;
+        const int c2 = add_conv(pre + ".conv2", pre + ".gn2", w, w, w, 3, 1, 1, Ho, P.convs[c1].z, P.convs[c1].zb,
+                                true, true);
+        blk.main = {c1, c2};
+      } else {  // Bottleneck: 1x1 -> 3x3 (stride) -> 1x1 (x4)
+        const int c1 = add_conv(pre + ".conv1", pre + ".gn1", cin, cin, w, 1, 1, 0, H, z, zb, true, true);
+        const int c2 = add_conv(pre + ".conv2", pre + ".gn2", w, w, w, 3, s, 1, H, P.convs[c1].z, P.convs[c1].zb,
+                                true, true);
+        Ho = P.convs[c2].Ho;
+        const int c3 = add_conv(pre + ".conv3", pre + ".gn3", w, w, cout, 1, 1, 0, Ho, P.convs[c2].z,
+                                P.convs[c2].zb, true, true);
+        blk.main = {c1, c2, c3};
+      }
+      blk.down = (s != 1 || cin != cout)
+                     ? add_conv(pre + ".down.conv", pre + ".down.gn", cin, cin, cout, 1, s, 0, H, z, zb, false, true)
                      : -1;
-      blk.out = P.convs[blk.c2].z;  // conv2's GN output buffer holds relu(gn2 + shortcut)
+      const ConvGN& last = P.convs[blk.main.back()];
+      blk.out = last.z;  // the last main conv's GN output buffer holds relu(gn + shortcut)
       P.blocks.push_back(blk);
       z = blk.out;
-      zb = P.convs[blk.c2].zb;
+      zb = last.zb;
       H = Ho;
-      cin = c;
+      cin = cout;
     }
   }
-  add_conv("enc.compress.conv", "enc.compress.gn", 256, 128, 3, 1, 1, H, H, z, zb, false);
-  P.flat = take((size_t)F * 512);
+  add_conv("enc.compress.conv", "enc.compress.gn", cin, cin, 128, 3, 1, 1, H, z, zb, false, true);
+  P.flat = take((size_t)F * P.fc_in);
   P.vis = take((size_t)F * 512);
   P.xin = take((size_t)F * kXin);
-  P.GI = take((size_t)F * kG4);
-  P.Hs = take((size_t)F * kH);
-  P.Hin = take((size_t)F * kH);
-  P.Cin = take((size_t)F * kH);
-  P.Cs = take((size_t)F * kH);
-  P.IFGO = take((size_t)F * kH * 4);
-  P.dH = take((size_t)F * kH);
-  P.dG = take((size_t)F * kG4);
-  P.wr_b = take_b(2 * max_w);
-  P.wd_b = take_b(max_w);
+  for (int l = 0; l < P.layers; ++l) {
+    Plan::Rnn& r = P.rnn[l];
+    r.GI = take((size_t)F * kG4);
+    r.Hs = take((size_t)F * kH);
+    r.Hin = take((size_t)F * kH);
+    r.Cin = take((size_t)F * kH);
+    r.Cs = take((size_t)F * kH);
+    r.IFGO = take((size_t)F * kH * 4);
+    r.dH = take((size_t)F * kH);
+    r.dG = take((size_t)F * kG4);
+  }
   P.dyb = take_b(max_act);
   P.dwt = take(max_w);
-  P.part = take((size_t)kMaxSplits * max_w);
-  P.gn_part = take((size_t)F * 256 * 2);
+  P.part = take(std::max({(size_t)kMaxSplits * max_w, (size_t)16 * F * kG4, (size_t)16 * kG4 * kXin}));
+  P.gn_part = take(max_gn_part);
+  P.gn_gpart = reinterpret_cast<double*>(take_bytes(max_gn_rows * kGroups * 2 * sizeof(double)));
   P.dz_a = take(max_act);
   P.dz_b = take(max_act);
   P.dz_c = take(max_act);
   P.dxin = take((size_t)F * kXin);
-  P.dflat = take((size_t)F * 512);
+  P.dflat = take((size_t)F * P.fc_in);
   P.dvis = take((size_t)F * 512);
   P.bytes = off;
 }
@@ -653,6 +884,7 @@ constexpr int kPrecFwd = 3;
 
 struct ConvGeom {
   int F, H, W, Ci, Co, k, s, p, Ho, Wo;
+  int Cr;  // channels of the parameter tensor (Ci may be padded)
   int K() const { return k * k * Ci; }
   int M() const { return F * Ho * Wo; }
 };
@@ -696,6 +928,7 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
   }
   const int K = g.K(), M = g.M();
   if (!wr_b) {  // weights not prepared by weights_prep_kernel (diagnostic entry)
+    DDPPO_REQUIRE(ctx, sc.wr_b && g.Cr == g.Ci, "conv: unprepared weights need scratch");
     weights_bf16_kernel<<<blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st>>>(w, g.Co, g.Ci, g.k, sc.wr_b, nullptr);
     ctx->count(1);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -754,12 +987,13 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
     gm.partial = sc.part;
     ddppo_status s = launch_igemm(ctx, gm, st);
     if (s != DDPPO_OK) return s;
-    wgrad_to_torch_kernel<<<blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st>>>(sc.dwt, g.Co, g.Ci, g.k, dw);
+    wgrad_to_torch_kernel<<<blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st>>>(sc.dwt, g.Co, g.Cr, g.Ci, g.k, dw);
     ctx->count(1);
   }
   if (dx == nullptr) return DDPPO_OK;
   // dgrad: dx[p][c] (+)= sum_{(u,v,o)} dy[tap^T(p; u, v)][o] W[o][c][u][v]
   if (!wd_b) {
+    DDPPO_REQUIRE(ctx, sc.wd_b && g.Cr == g.Ci, "conv: unprepared weights need scratch");
     weights_bf16_kernel<<<blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st>>>(w, g.Co, g.Ci, g.k, nullptr, sc.wd_b);
     ctx->count(1);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -782,37 +1016,60 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
 
 // z = (relu)(GN(y) (+ residual)); stats [F][16][2] = (mean, rstd); zb (nullable) = z as bf16 planes
 ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const float* gamma, const float* beta,
-                    const float* residual, int relu, float* stats, float* z, __nv_bfloat16* zb, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, C >= kGroups && kGnThreads % C == 0, "groupnorm: C must divide 256 (and be >= 16)");
-  gn_fwd_kernel<<<F, kGnThreads, 0, st>>>(y, gamma, beta, residual, HW, C, relu, (size_t)F * HW * C, stats, z, zb);
-  ctx->count(1);
+                    const float* residual, int relu, float* stats, float* z, __nv_bfloat16* zb, double* gpart,
+                    cudaStream_t st) {
+  const int nt = gn_threads(C);
+  DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");
+  const int S = (HW * C + gn_chunk(C) - 1) / gn_chunk(C);
+  if (S == 1) {  // one block per frame: statistics and normalisation in one pass over the slab
+    gn_fwd_kernel<<<F, nt, 0, st>>>(y, gamma, beta, residual, HW, C, relu, (size_t)F * HW * C, stats, z, zb);
+    ctx->count(1);
+  } else {
+    DDPPO_REQUIRE(ctx, gpart != nullptr, "groupnorm: large frames need partial-sum scratch");
+    gn_stats_part_kernel<<<dim3(S, F), nt, 0, st>>>(y, HW, C, gpart);
+    gn_apply_part_kernel<<<dim3(S, F), nt, 0, st>>>(y, gpart, gamma, beta, residual, HW, C, relu, (size_t)F * HW * C,
+                                                    stats, z, zb);
+    ctx->count(2);
+  }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
 
 // dz: gradient wrt z; relu_z: z if a ReLU produced it (mask z > 0), else null.  Writes dy (gradient
-// wrt y, bf16), dgamma, dbeta.  part [F][C][2] is scratch.
+// wrt y, bf16), dgamma, dbeta.  part [F*S][C][2] and gpart [F*S][16][2] (S > 1) are scratch.
 ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const float* relu_z, const float* y,
                     const float* stats, const float* gamma, __nv_bfloat16* dy, float* dgamma, float* dbeta,
-                    float* part, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, C >= kGroups && kGnThreads % C == 0, "groupnorm: C must divide 256 (and be >= 16)");
-  gn_bwd_kernel<<<F, kGnThreads, 0, st>>>(dz, relu_z, y, stats, gamma, HW, C, dy, part);
-  ctx->count(1);
-  gn_param_reduce_kernel<<<C, kThreads, 0, st>>>(part, F, C, dgamma, dbeta);
+                    float* part, double* gpart, cudaStream_t st) {
+  const int nt = gn_threads(C);
+  DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");
+  const int S = (HW * C + gn_chunk(C) - 1) / gn_chunk(C);
+  if (S == 1) {
+    gn_bwd_kernel<<<F, nt, 0, st>>>(dz, relu_z, y, stats, gamma, HW, C, dy, part);
+    ctx->count(1);
+  } else {
+    DDPPO_REQUIRE(ctx, gpart != nullptr, "groupnorm: large frames need partial-sum scratch");
+    gn_bwd_part_kernel<<<dim3(S, F), nt, 0, st>>>(dz, relu_z, y, stats, gamma, HW, C, gpart, part);
+    gn_bwd_apply_kernel<<<dim3(S, F), nt, 0, st>>>(dz, relu_z, y, stats, gamma, gpart, HW, C, dy);
+    ctx->count(2);
+  }
+  gn_param_reduce_kernel<<<C, kThreads, 0, st>>>(part, F * S, C, dgamma, dbeta);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
 
-ConvGeom geom_of(const Plan& P, const ConvGN& c) { return ConvGeom{P.F, c.H, c.W, c.Ci, c.Co, c.k, c.s, c.p, c.Ho, c.Wo}; }
-ConvScratch scratch_of(const Plan& P) { return ConvScratch{P.wr_b, P.wd_b, P.dwt, P.part}; }
+ConvGeom geom_of(const Plan& P, const ConvGN& c) {
+  return ConvGeom{P.F, c.H, c.W, c.Ci, c.Co, c.k, c.s, c.p, c.Ho, c.Wo, c.Ci_real};
+}
+ConvScratch scratch_of(const Plan& P) { return ConvScratch{nullptr, nullptr, P.dwt, P.part}; }  // weights prepared
 
 // conv (+GN (+residual) (+ReLU)) forward
 ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, const float* residual, int relu,
                          cudaStream_t st) {
   ddppo_status s = conv_fwd(ctx, geom_of(P, c), c.x, c.xb, prm + c.w, c.wr_b, c.y, scratch_of(P), st);
   if (s != DDPPO_OK) return s;
-  return gn_fwd(ctx, P.F, c.Ho * c.Wo, c.Co, c.y, prm + c.gw, prm + c.gb, residual, relu, c.stats, c.z, c.zb, st);
+  return gn_fwd(ctx, P.F, c.Ho * c.Wo, c.Co, c.y, prm + c.gw, prm + c.gb, residual, relu, c.stats, c.z, c.zb,
+                P.gn_gpart, st);
 }
 
 // backward of conv+GN: dz = gradient wrt the GN(+residual)(+ReLU) output; relu_z = that output if a
@@ -820,7 +1077,7 @@ ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, c
 ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P, ConvGN& c, const float* dz,
                          const float* relu_z, float* dx, int accumulate_dx, cudaStream_t st) {
   ddppo_status s = gn_bwd(ctx, P.F, c.Ho * c.Wo, c.Co, dz, relu_z, c.y, c.stats, prm + c.gw, P.dyb, grad + c.gw,
-                          grad + c.gb, P.gn_part, st);
+                          grad + c.gb, P.gn_part, P.gn_gpart, st);
   if (s != DDPPO_OK) return s;
   return conv_bwd(ctx, geom_of(P, c), c.x, c.xb, prm + c.w, c.wd_b, P.dyb, grad + c.w, dx, accumulate_dx,
                   scratch_of(P), st);
@@ -839,45 +1096,54 @@ ddppo_status gemm_split(ddppo_ctx* ctx, GemmTC g, const Plan& P, cudaStream_t st
   return launch_gemm_tc(ctx, g, st);
 }
 
-LstmPtrs lstm_ptrs(const ModelLayout& L, const float* prm, const ddppo_batch& b, Plan& P) {
+// parameter names of LSTM layer l ("rnn.weight_ih" for the 1-layer Depth agent, "..._l<l>" for RGB-D)
+std::string rnn_name(const Plan& P, const char* base, int l) {
+  return P.layers == 1 ? std::string(base) : std::string(base) + "_l" + std::to_string(l);
+}
+
+LstmPtrs lstm_ptrs(const ModelLayout& L, const float* prm, const ddppo_batch& b, Plan& P, int l) {
+  const Plan::Rnn& r = P.rnn[l];
   LstmPtrs q;
-  q.Whh = prm + off_of(L, "rnn.weight_hh");
-  q.bih = prm + off_of(L, "rnn.bias_ih");
-  q.bhh = prm + off_of(L, "rnn.bias_hh");
-  q.GI = P.GI;
+  q.Whh = prm + off_of(L, rnn_name(P, "rnn.weight_hh", l));
+  q.bih = prm + off_of(L, rnn_name(P, "rnn.bias_ih", l));
+  q.bhh = prm + off_of(L, rnn_name(P, "rnn.bias_hh", l));
+  q.GI = r.GI;
   q.mask = b.mask;
-  q.h0 = b.h0;
-  q.c0 = b.c0;
+  q.h0 = b.h0 + (size_t)l * kH;
+  q.c0 = b.c0 + (size_t)l * kH;
+  q.sld = P.layers * kH;
   q.env_idx = b.env_idx;
   q.B = b.B;
   q.T_run = b.T_run;
   q.ld = b.ld;
-  q.Hs = P.Hs;
-  q.Hin = P.Hin;
-  q.Cin = P.Cin;
-  q.Cs = P.Cs;
-  q.IFGO = reinterpret_cast<float4*>(P.IFGO);
-  q.dH = P.dH;
-  q.dG = P.dG;
+  q.Hs = r.Hs;
+  q.Hin = r.Hin;
+  q.Cin = r.Cin;
+  q.Cs = r.Cs;
+  q.IFGO = reinterpret_cast<float4*>(r.IFGO);
+  q.dH = r.dH;
+  q.dG = r.dG;
   return q;
 }
 
+bool is_rgbd(const ModelLayout& L) { return layout_offset(L, "rnn.weight_ih_l0") >= 0; }
+
 }  // namespace
 
-size_t depth_workspace(int max_B, int T) {
+size_t depth_workspace(int arch, int max_B, int T) {
   ddppo_model_desc d = {};
-  d.arch = DDPPO_ARCH_DEPTH_R18_LSTM;
+  d.arch = arch;
   d.hidden = 512;
   d.num_actions = 4;
   ModelLayout L;
   build_layout(&d, &L);
   Plan P;
-  make_plan(L, max_B, T, nullptr, &P);
+  make_plan(L, arch == DDPPO_ARCH_RGBD_R50_LSTM2, max_B, T, nullptr, &P);
   return P.bytes;
 }
 
 namespace {
-// encoder -> visual FC -> LSTM input -> GI GEMM -> LSTM recurrence
+// encoder -> visual FC -> LSTM input -> (per LSTM layer: input GEMM, recurrence)
 ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, const ddppo_batch& b, Plan& P,
                            cudaStream_t st) {
   const int F = P.F;
@@ -885,43 +1151,53 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
     WeightPrep prep;
     prep.n = 0;
     int max_n = 0;
-    for (const ConvGN& c : P.convs) {
-      if (c.Ci == 1) continue;
-      prep.it[prep.n++] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci, c.k};
+    for (size_t i = 0; i < P.convs.size(); ++i) {
+      const ConvGN& c = P.convs[i];
+      if (c.Ci == 1) continue;  // the Depth stem runs SIMT on fp32 weights
+      DDPPO_REQUIRE(ctx, prep.n < kMaxConvs, "too many convolutions for one weight-prep launch");
+      prep.it[prep.n++] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k};
       max_n = std::max(max_n, c.Co * c.Ci * c.k * c.k);
     }
     weights_prep_kernel<<<dim3((max_n + 1023) / 1024, prep.n), 1024, 0, st>>>(prep);
     ctx->count(1);
   }
-  gather_obs_kernel<<<blocks_for(ctx, (size_t)F * kImg * kImg), kThreads, 0, st>>>(b.obs, b.env_idx, b.T, b.T_run, F,
-                                                                                    P.x0);
+  if (!P.rgbd) {
+    gather_obs_kernel<<<blocks_for(ctx, (size_t)F * kImg * kImg), kThreads, 0, st>>>(b.obs, b.env_idx, b.T, b.T_run,
+                                                                                      F, P.x0);
+  } else {
+    const size_t n = (size_t)F * (kImgRgbd / 2) * (kImgRgbd / 2) * 8;
+    rgbd_prologue_kernel<<<blocks_for(ctx, n), kThreads, 0, st>>>(b.obs, b.env_idx, b.T, b.T_run, F, kImgRgbd, P.x0,
+                                                                  P.x0b);
+  }
   ctx->count(1);
   ddppo_status s = conv_gn_fwd(ctx, prm, P, P.convs[0], nullptr, 1, st);
   if (s != DDPPO_OK) return s;
   {
     ConvGN& c = P.convs[0];
-    const int hp = (c.Ho + 2 - 3) / 2 + 1;
+    const int hp = P.pool_hw;
     maxpool_fwd_kernel<<<blocks_for(ctx, (size_t)F * hp * hp * 32), kThreads, 0, st>>>(c.z, F, c.Ho, c.Wo, 32, hp, hp,
                                                                                        P.pool_out, P.pool_arg, P.pool_b);
     ctx->count(1);
   }
   for (auto& blk : P.blocks) {
-    if ((s = conv_gn_fwd(ctx, prm, P, P.convs[blk.c1], nullptr, 1, st)) != DDPPO_OK) return s;
     const float* sc = blk.in;
     if (blk.down >= 0) {
       if ((s = conv_gn_fwd(ctx, prm, P, P.convs[blk.down], nullptr, 0, st)) != DDPPO_OK) return s;
       sc = P.convs[blk.down].z;
     }
-    if ((s = conv_gn_fwd(ctx, prm, P, P.convs[blk.c2], sc, 1, st)) != DDPPO_OK) return s;
+    for (size_t j = 0; j < blk.main.size(); ++j) {
+      const bool last = j + 1 == blk.main.size();
+      if ((s = conv_gn_fwd(ctx, prm, P, P.convs[blk.main[j]], last ? sc : nullptr, 1, st)) != DDPPO_OK) return s;
+    }
   }
   ConvGN& comp = P.convs.back();
   if ((s = conv_gn_fwd(ctx, prm, P, comp, nullptr, 1, st)) != DDPPO_OK) return s;
-  flatten_kernel<<<blocks_for(ctx, (size_t)F * 512), kThreads, 0, st>>>(comp.z, F, P.flat, 1);
+  flatten_kernel<<<blocks_for(ctx, (size_t)F * P.fc_in), kThreads, 0, st>>>(comp.z, F, P.feat_hw, 128, P.flat, 1);
   ctx->count(1);
   // visual FC + ReLU
-  if ((s = gemm_split(ctx, GemmTC{P.flat, 512, 1, prm + off_of(L, "visual_fc.weight"), 512, 1, P.vis, 512, F, 512,
-                                      512, 1, nullptr, kPrecFwd}, P,
-                          st)) != DDPPO_OK)
+  if ((s = gemm_split(ctx, GemmTC{P.flat, P.fc_in, 1, prm + off_of(L, "visual_fc.weight"), P.fc_in, 1, P.vis, 512, F,
+                                  512, P.fc_in, 1, nullptr, kPrecFwd},
+                      P, st)) != DDPPO_OK)
     return s;
   bias_act_kernel<<<blocks_for(ctx, (size_t)F * 512), kThreads, 0, st>>>(P.vis, prm + off_of(L, "visual_fc.bias"), F,
                                                                          512, 1);
@@ -931,60 +1207,72 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
       prm + off_of(L, "act_embed.weight"), b.T, b.ld, b.T_run, F, P.xin);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
-  // GI = x W_ih^T (biases are added inside the recurrence)
-  if ((s = gemm_split(ctx, GemmTC{P.xin, kXin, 1, prm + off_of(L, "rnn.weight_ih"), kXin, 1, P.GI, kG4, F, kG4,
-                                      kXin, 1, nullptr, kPrecFwd}, P,
-                          st)) != DDPPO_OK)
-    return s;
-  return launch_lstm_fwd(ctx, lstm_ptrs(L, prm, b, P), st);
+  for (int l = 0; l < P.layers; ++l) {
+    // GI = x W_ih^T (biases are added inside the recurrence); layer l > 0 reads layer l-1's h
+    const float* xl = l == 0 ? P.xin : P.rnn[l - 1].Hs;
+    const int nin = l == 0 ? kXin : kH;
+    if ((s = gemm_split(ctx, GemmTC{xl, nin, 1, prm + off_of(L, rnn_name(P, "rnn.weight_ih", l)), nin, 1, P.rnn[l].GI,
+                                    kG4, F, kG4, nin, 1, nullptr, kPrecFwd},
+                        P, st)) != DDPPO_OK)
+      return s;
+    if ((s = launch_lstm_fwd(ctx, lstm_ptrs(L, prm, b, P, l), st)) != DDPPO_OK) return s;
+  }
+  return DDPPO_OK;
 }
 }  // namespace
 
 ddppo_status depth_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, const ddppo_batch& b, float* logits,
                        float* values, void* ws, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, b.obs && b.c0, "depth: batch needs obs and c0");
-  DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= 8 && b.T_run <= 1024, "depth: minibatch must hold 1..8 envs, T <= 1024");
+  DDPPO_REQUIRE(ctx, b.obs && b.c0, "visual agent: batch needs obs and c0");
+  DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= 8 && b.T_run <= 1024, "visual agent: minibatch must hold 1..8 envs, T <= 1024");
   Plan P;
-  make_plan(L, b.B, b.T_run, ws, &P);
+  make_plan(L, is_rgbd(L), b.B, b.T_run, ws, &P);
   {
     ProfScope ps(ctx, DDPPO_K_NET_FWD, st, 0);
     ddppo_status s = depth_fwd_net(ctx, L, prm, b, P, st);
     if (s != DDPPO_OK) return s;
   }
   ProfScope ps(ctx, DDPPO_K_HEAD, st, 0);
-  return launch_head_fwd(ctx, prm + off_of(L, "head.weight"), prm + off_of(L, "head.bias"), P.Hs, P.F, logits, values,
-                         st);
+  return launch_head_fwd(ctx, prm + off_of(L, "head.weight"), prm + off_of(L, "head.bias"), P.rnn[P.layers - 1].Hs,
+                         P.F, logits, values, st);
 }
 
 ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, const ddppo_batch& b,
                        const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st) {
   Plan P;
-  make_plan(L, b.B, b.T_run, ws, &P);
+  make_plan(L, is_rgbd(L), b.B, b.T_run, ws, &P);
   const int F = P.F;
   ddppo_status s;
   {
     ProfScope ps(ctx, DDPPO_K_HEAD, st, 0);
-    s = launch_head_bwd(ctx, prm + off_of(L, "head.weight"), P.Hs, dlogits, dvalues, F, P.dH,
-                        grad + off_of(L, "head.weight"), grad + off_of(L, "head.bias"), st);
+    s = launch_head_bwd(ctx, prm + off_of(L, "head.weight"), P.rnn[P.layers - 1].Hs, dlogits, dvalues, F,
+                        P.rnn[P.layers - 1].dH, grad + off_of(L, "head.weight"), grad + off_of(L, "head.bias"), st);
     if (s != DDPPO_OK) return s;
   }
   ProfScope ps(ctx, DDPPO_K_NET_BWD, st, 0);
-  if ((s = launch_lstm_bwd(ctx, lstm_ptrs(L, prm, b, P), st)) != DDPPO_OK) return s;
-  // LSTM weight gradients and db (b_ih and b_hh receive the same gradient)
-  if ((s = gemm_split(ctx, GemmTC{P.dG, 1, kG4, P.xin, 1, kXin, grad + off_of(L, "rnn.weight_ih"), kXin, kG4, kXin,
-                                      F}, P,
-                          st)) != DDPPO_OK)
-    return s;
-  if ((s = gemm_split(ctx, GemmTC{P.dG, 1, kG4, P.Hin, 1, kH, grad + off_of(L, "rnn.weight_hh"), kH, kG4, kH, F}, P,
-                          st)) != DDPPO_OK)
-    return s;
-  if ((s = launch_colsum(ctx, P.dG, kG4, F, kG4, grad + off_of(L, "rnn.bias_ih"), st)) != DDPPO_OK) return s;
-  if ((s = launch_colsum(ctx, P.dG, kG4, F, kG4, grad + off_of(L, "rnn.bias_hh"), st)) != DDPPO_OK) return s;
-  // dx = dG W_ih  [F][576]
-  if ((s = gemm_split(ctx, GemmTC{P.dG, kG4, 1, prm + off_of(L, "rnn.weight_ih"), 1, kXin, P.dxin, kXin, F, kXin,
-                                      kG4}, P,
-                          st)) != DDPPO_OK)
-    return s;
+  for (int l = P.layers - 1; l >= 0; --l) {
+    Plan::Rnn& r = P.rnn[l];
+    if ((s = launch_lstm_bwd(ctx, lstm_ptrs(L, prm, b, P, l), st)) != DDPPO_OK) return s;
+    // weight gradients and db (b_ih and b_hh receive the same gradient)
+    const float* xl = l == 0 ? P.xin : P.rnn[l - 1].Hs;
+    const int nin = l == 0 ? kXin : kH;
+    const float* Wih = prm + off_of(L, rnn_name(P, "rnn.weight_ih", l));
+    if ((s = gemm_split(ctx, GemmTC{r.dG, 1, kG4, xl, 1, nin, grad + off_of(L, rnn_name(P, "rnn.weight_ih", l)), nin,
+                                    kG4, nin, F},
+                        P, st)) != DDPPO_OK)
+      return s;
+    if ((s = gemm_split(ctx, GemmTC{r.dG, 1, kG4, r.Hin, 1, kH, grad + off_of(L, rnn_name(P, "rnn.weight_hh", l)), kH,
+                                    kG4, kH, F},
+                        P, st)) != DDPPO_OK)
+      return s;
+    if ((s = launch_colsum(ctx, r.dG, kG4, F, kG4, grad + off_of(L, rnn_name(P, "rnn.bias_ih", l)), st)) != DDPPO_OK)
+      return s;
+    if ((s = launch_colsum(ctx, r.dG, kG4, F, kG4, grad + off_of(L, rnn_name(P, "rnn.bias_hh", l)), st)) != DDPPO_OK)
+      return s;
+    // input gradient: into the layer below's dH, or dx = dG W_ih [F][576] for layer 0
+    float* dxl = l == 0 ? P.dxin : P.rnn[l - 1].dH;
+    if ((s = gemm_split(ctx, GemmTC{r.dG, kG4, 1, Wih, 1, nin, dxl, nin, F, nin, kG4}, P, st)) != DDPPO_OK) return s;
+  }
   goal_emb_grads_kernel<<<64, kThreads, 0, st>>>(P.dxin, b.goal, b.prev_action, b.env_idx, b.T, b.ld, b.T_run, F,
                                                  grad + off_of(L, "goal_fc.weight"), grad + off_of(L, "goal_fc.bias"),
                                                  grad + off_of(L, "act_embed.weight"));
@@ -993,47 +1281,54 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   // visual FC: dW = dVpre^T flat, db = colsum(dVpre), dflat = dVpre W
-  if ((s = gemm_split(ctx, GemmTC{P.dvis, 1, 512, P.flat, 1, 512, grad + off_of(L, "visual_fc.weight"), 512, 512,
-                                      512, F}, P,
-                          st)) != DDPPO_OK)
+  if ((s = gemm_split(ctx, GemmTC{P.dvis, 1, 512, P.flat, 1, P.fc_in, grad + off_of(L, "visual_fc.weight"), P.fc_in,
+                                  512, P.fc_in, F},
+                      P, st)) != DDPPO_OK)
     return s;
   if ((s = launch_colsum(ctx, P.dvis, 512, F, 512, grad + off_of(L, "visual_fc.bias"), st)) != DDPPO_OK) return s;
-  if ((s = gemm_split(ctx, GemmTC{P.dvis, 512, 1, prm + off_of(L, "visual_fc.weight"), 1, 512, P.dflat, 512, F,
-                                      512, 512}, P,
-                          st)) != DDPPO_OK)
+  if ((s = gemm_split(ctx, GemmTC{P.dvis, 512, 1, prm + off_of(L, "visual_fc.weight"), 1, P.fc_in, P.dflat, P.fc_in,
+                                  F, P.fc_in, 512},
+                      P, st)) != DDPPO_OK)
     return s;
   // encoder: dz = gradient wrt the current block output; three rotating activation buffers
   ConvGN& comp = P.convs.back();
   float* dz = P.dz_a;
   float* da = P.dz_b;
   float* dn = P.dz_c;
-  flatten_kernel<<<blocks_for(ctx, (size_t)F * 512), kThreads, 0, st>>>(P.dflat, F, da, 0);
+  flatten_kernel<<<blocks_for(ctx, (size_t)F * P.fc_in), kThreads, 0, st>>>(P.dflat, F, P.feat_hw, 128, da, 0);
   ctx->count(1);
   if ((s = conv_gn_bwd(ctx, prm, grad, P, comp, da, comp.z, dz, 0, st)) != DDPPO_OK) return s;
   for (int bi = (int)P.blocks.size() - 1; bi >= 0; --bi) {
     const Plan::Block& blk = P.blocks[bi];
-    ConvGN& c1 = P.convs[blk.c1];
-    ConvGN& c2 = P.convs[blk.c2];
-    // out = relu(gn2(conv2(a)) + shortcut(in)), a = relu(gn1(conv1(in)))
-    if ((s = conv_gn_bwd(ctx, prm, grad, P, c2, dz, c2.z, da, 0, st)) != DDPPO_OK) return s;
+    ConvGN& last = P.convs[blk.main.back()];
+    // out = relu(gn_last(conv_last(...)) + shortcut(in)); the ReLU mask of the sum is `out` (= last.z)
     if (blk.down >= 0) {
-      if ((s = conv_gn_bwd(ctx, prm, grad, P, P.convs[blk.down], dz, c2.z, dn, 0, st)) != DDPPO_OK) return s;
+      if ((s = conv_gn_bwd(ctx, prm, grad, P, P.convs[blk.down], dz, last.z, dn, 0, st)) != DDPPO_OK) return s;
     } else {
-      const size_t n = (size_t)F * c2.Ho * c2.Wo * c2.Co;
-      relu_mask_kernel<<<blocks_for(ctx, n), kThreads, 0, st>>>(dz, c2.z, n, dn);
+      const size_t n = (size_t)F * last.Ho * last.Wo * last.Co;
+      relu_mask_kernel<<<blocks_for(ctx, n), kThreads, 0, st>>>(dz, last.z, n, dn);
       ctx->count(1);
     }
-    if ((s = conv_gn_bwd(ctx, prm, grad, P, c1, da, c1.z, dn, 1, st)) != DDPPO_OK) return s;
+    // main branch, last conv first: its upstream mask is the block output, the others' their own ReLU
+    float* g_in = dz;    // gradient wrt the current conv's output
+    float* g_out = da;   // gradient wrt its input
+    for (int j = (int)blk.main.size() - 1; j >= 0; --j) {
+      ConvGN& c = P.convs[blk.main[j]];
+      const bool first = j == 0;
+      float* target = first ? dn : g_out;
+      if ((s = conv_gn_bwd(ctx, prm, grad, P, c, g_in, c.z, target, first ? 1 : 0, st)) != DDPPO_OK) return s;
+      if (!first) {
+        std::swap(g_in, g_out);  // g_in <- this conv's input gradient; g_out <- a free buffer
+        if (g_out == dn) g_out = (g_in == dz) ? da : dz;
+      }
+    }
     std::swap(dz, dn);  // dn (the block input's gradient) becomes the next dz
   }
   // max-pool, then the stem (no input gradient)
   ConvGN& stem = P.convs[0];
-  {
-    const int hp = (stem.Ho + 2 - 3) / 2 + 1;
-    maxpool_bwd_kernel<<<blocks_for(ctx, (size_t)F * stem.Ho * stem.Wo * 32), kThreads, 0, st>>>(
-        dz, P.pool_arg, F, stem.Ho, stem.Wo, 32, hp, hp, da);
-    ctx->count(1);
-  }
+  maxpool_bwd_kernel<<<blocks_for(ctx, (size_t)F * stem.Ho * stem.Wo * 32), kThreads, 0, st>>>(
+      dz, P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
+  ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return conv_gn_bwd(ctx, prm, grad, P, stem, da, stem.z, nullptr, 0, st);
 }
@@ -1049,7 +1344,7 @@ extern "C" ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const
                 "conv2d: bad geometry");
   DDPPO_REQUIRE(ctx, Ci == 1 || (Ci % 8 == 0 && Co % 8 == 0), "conv2d: Ci == 1 (stem) or Ci, Co multiples of 8");
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
-  ConvGeom g{F, H, W, Ci, Co, k, s, p, Ho, Wo};
+  ConvGeom g{F, H, W, Ci, Co, k, s, p, Ho, Wo, Ci};
   const size_t nx = (size_t)F * H * W * Ci, ny = (size_t)g.M() * Co, ok = (size_t)Co * g.K();
   const size_t nb = 2 * nx + ny + 2 * ok + ok;  // bf16 elements: x planes, dy, wr planes, wd
   const size_t nf = ok + std::max((size_t)kMaxSplits * ok, (size_t)F * ok);
@@ -1102,10 +1397,13 @@ extern "C" ddppo_status ddppo_debug_groupnorm(ddppo_ctx* ctx, const float* y, co
   DDPPO_REQUIRE(ctx, F >= 1 && HW >= 1 && C >= kGroups && C % kGroups == 0, "groupnorm: C must be a multiple of 16");
   cudaStream_t st = as_stream(stream);
   ProfScope ps(ctx, DDPPO_K_OTHER, st, 0);
-  ddppo_status r = gn_fwd(ctx, F, HW, C, y, gamma, beta, residual, relu, stats, z, nullptr, st);
+  const int S = (HW * C + gn_chunk(C) - 1) / gn_chunk(C);
+  float* part = scratch;                                                                 // [F*S][C][2]
+  double* gpart = reinterpret_cast<double*>(scratch + align_up((size_t)F * S * C * 2, 2));  // [F*S][16][2]
+  __nv_bfloat16* dyb = reinterpret_cast<__nv_bfloat16*>(gpart + (size_t)F * S * kGroups * 2);
+  ddppo_status r = gn_fwd(ctx, F, HW, C, y, gamma, beta, residual, relu, stats, z, nullptr, gpart, st);
   if (r != DDPPO_OK || !dz) return r;
-  __nv_bfloat16* dyb = reinterpret_cast<__nv_bfloat16*>(scratch + 2 * (size_t)F * C);
-  r = gn_bwd(ctx, F, HW, C, dz, relu ? z : nullptr, y, stats, gamma, dyb, dgamma, dbeta, scratch, st);
+  r = gn_bwd(ctx, F, HW, C, dz, relu ? z : nullptr, y, stats, gamma, dyb, dgamma, dbeta, part, gpart, st);
   if (r != DDPPO_OK) return r;
   bf16_to_f32_kernel<<<blocks_for(ctx, (size_t)F * HW * C), kThreads, 0, st>>>(dyb, (size_t)F * HW * C, dy);
   ctx->count(1);
@@ -1140,34 +1438,27 @@ __global__ void positive_mask_kernel(const float* __restrict__ z, size_t n, uint
 
 // The forward's discrete decisions (every ReLU mask and the max-pool argmax), from the workspace of
 // the last ddppo_policy_fwd on `batch`, in the order documented in include/ddppo.h.
-extern "C" ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_batch* host_batch, void* ws,
-                                                    uint8_t* out, int64_t cap, int64_t* host_n, void* stream) {
-  if (!ctx || !host_batch) return DDPPO_ERR_CONFIG;
-  ddppo_model_desc d = {};
-  d.arch = DDPPO_ARCH_DEPTH_R18_LSTM;
-  d.hidden = 512;
-  d.num_actions = 4;
+extern "C" ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
+                                                    const ddppo_batch* host_batch, void* ws, uint8_t* out, int64_t cap,
+                                                    int64_t* host_n, void* stream) {
+  if (!ctx || !host_batch || !host_desc) return DDPPO_ERR_CONFIG;
   ModelLayout L;
-  build_layout(&d, &L);
+  DDPPO_REQUIRE(ctx, build_layout(host_desc, &L) == DDPPO_OK &&
+                         (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2),
+                "depth decisions: visual agents only");
   Plan P;
-  make_plan(L, host_batch->B, host_batch->T_run, ws, &P);
+  make_plan(L, host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2, host_batch->B, host_batch->T_run, ws, &P);
   const int F = P.F;
-  std::vector<std::pair<const float*, size_t>> masks;
-  const ConvGN& stem = P.convs[0];
-  masks.push_back({stem.z, (size_t)F * stem.Ho * stem.Wo * stem.Co});
-  const size_t pool_n = (size_t)F * 16 * 16 * 32;
-  int64_t total = (int64_t)masks[0].second + (int64_t)pool_n;
-  for (const auto& blk : P.blocks) {
-    const ConvGN& c1 = P.convs[blk.c1];
-    const ConvGN& c2 = P.convs[blk.c2];
-    masks.push_back({c1.z, (size_t)F * c1.Ho * c1.Wo * c1.Co});
-    masks.push_back({c2.z, (size_t)F * c2.Ho * c2.Wo * c2.Co});
-    total += (int64_t)(masks[masks.size() - 2].second + masks.back().second);
-  }
-  const ConvGN& comp = P.convs.back();
-  masks.push_back({comp.z, (size_t)F * comp.Ho * comp.Wo * comp.Co});
+  std::vector<std::pair<const float*, size_t>> masks;  // (tensor, size); the pool argmax is copied after the first
+  auto add = [&](const ConvGN& c) { masks.push_back({c.z, (size_t)F * c.Ho * c.Wo * c.Co}); };
+  add(P.convs[0]);
+  const size_t pool_n = (size_t)F * P.pool_hw * P.pool_hw * 32;
+  for (const auto& blk : P.blocks)
+    for (int j : blk.main) add(P.convs[j]);  // inner ReLUs, then the block output (last conv's z)
+  add(P.convs.back());
   masks.push_back({P.vis, (size_t)F * 512});
-  total += (int64_t)(masks[masks.size() - 2].second + masks.back().second);
+  int64_t total = (int64_t)pool_n;
+  for (auto& m : masks) total += (int64_t)m.second;
   if (host_n) *host_n = total;
   if (!out) return DDPPO_OK;
   DDPPO_REQUIRE(ctx, cap >= total, "depth decisions: buffer too small");

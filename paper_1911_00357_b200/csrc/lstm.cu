@@ -100,11 +100,11 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(LstmPtrs p) {
   for (int i = tid; i < B * kH; i += blockDim.x) {
     const int b = i / kH, k = i % kH;
     const int n = p.env_idx[b];
-    const float h = smask[b * T_run] * p.h0[(size_t)n * kH + k];
+    const float h = smask[b * T_run] * p.h0[(size_t)n * p.sld + k];
     *reinterpret_cast<__half*>(sm.h_tile[0] + htile_off(b, k)) = __float2half(h);
     if (k >= c * kUPC && k < (c + 1) * kUPC) {
       sm.hown[b][k - c * kUPC] = h;
-      sm.cown[b][k - c * kUPC] = smask[b * T_run] * p.c0[(size_t)n * kH + k];
+      sm.cown[b][k - c * kUPC] = smask[b * T_run] * p.c0[(size_t)n * p.sld + k];
     }
   }
   fence_proxy_async();

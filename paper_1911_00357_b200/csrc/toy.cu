@@ -48,8 +48,9 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
     add_tensor(&L, "rnn.bias_hh", 1, bg, (int)H);
     add_tensor(&L, "head.weight", 2, hw, (int)H);
     add_tensor(&L, "head.bias", 1, hb, (int)H);
-  } else if (d->arch == DDPPO_ARCH_DEPTH_R18_LSTM) {
+  } else if (d->arch == DDPPO_ARCH_DEPTH_R18_LSTM || d->arch == DDPPO_ARCH_RGBD_R50_LSTM2) {
     if (d->hidden != 512) return DDPPO_ERR_CONFIG;
+    const bool rgbd = d->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
     const int64_t H = d->hidden, G = 4 * H;
     char name[48];
     // conv weight [Co][Ci][k][k] (fan_in Ci*k*k), GroupNorm gamma (ones: fan_in 0) / beta (zeros: -1)
@@ -65,12 +66,35 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
       snprintf(name, sizeof(name), "%s.bias", pre);
       add_tensor(&L, name, 1, s, -1);
     };
-    conv("enc.stem.conv", 32, 1, 7);
+    conv("enc.stem.conv", 32, rgbd ? 4 : 1, 7);
     gn("enc.stem.gn", 32);
     const int64_t widths[4] = {32, 64, 128, 256};
     int64_t cin = 32;
     char pre[40], sub[48];
-    for (int li = 0; li < 4; ++li)
+    if (rgbd) {  // half-width ResNet50: bottlenecks [3, 4, 6, 3], outputs 4 x width
+      const int nblocks[4] = {3, 4, 6, 3};
+      for (int li = 0; li < 4; ++li)
+        for (int bi = 0; bi < nblocks[li]; ++bi) {
+          const int64_t w = widths[li];
+          const bool down = (bi == 0 && li > 0) || cin != 4 * w;
+          snprintf(pre, sizeof(pre), "enc.layer%d.%d", li + 1, bi);
+          const int64_t cis[3] = {cin, w, w}, cos_[3] = {w, w, 4 * w}, ks[3] = {1, 3, 1};
+          for (int j = 0; j < 3; ++j) {
+            snprintf(sub, sizeof(sub), "%s.conv%d", pre, j + 1);
+            conv(sub, cos_[j], cis[j], ks[j]);
+            snprintf(sub, sizeof(sub), "%s.gn%d", pre, j + 1);
+            gn(sub, cos_[j]);
+          }
+          if (down) {
+            snprintf(sub, sizeof(sub), "%s.down.conv", pre);
+            conv(sub, 4 * w, cin, 1);
+            snprintf(sub, sizeof(sub), "%s.down.gn", pre);
+            gn(sub, 4 * w);
+          }
+          cin = 4 * w;
+        }
+    }
+    for (int li = 0; li < 4 && !rgbd; ++li)
       for (int bi = 0; bi < 2; ++bi) {
         const int64_t c = widths[li];
         const bool down = (bi == 0 && li > 0) || cin != c;
@@ -91,19 +115,33 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
         }
         cin = c;
       }
-    conv("enc.compress.conv", 128, 256, 3);
+    conv("enc.compress.conv", 128, rgbd ? 1024 : 256, 3);
     gn("enc.compress.gn", 128);
-    int64_t vw[2] = {512, 512}, vb[1] = {512}, a[2] = {32, 3}, b[1] = {32}, e[2] = {A1, 32}, wi[2] = {G, 576},
-            wh[2] = {G, H}, bg[1] = {G}, hw[2] = {A1, H}, hb[1] = {A1};
-    add_tensor(&L, "visual_fc.weight", 2, vw, 512);
-    add_tensor(&L, "visual_fc.bias", 1, vb, 512);
+    const int64_t fin = rgbd ? 2048 : 512;  // 128 x 4 x 4 / 128 x 2 x 2
+    int64_t vw[2] = {512, fin}, vb[1] = {512}, a[2] = {32, 3}, b[1] = {32}, e[2] = {A1, 32}, wi[2] = {G, 576},
+            wi1[2] = {G, H}, wh[2] = {G, H}, bg[1] = {G}, hw[2] = {A1, H}, hb[1] = {A1};
+    add_tensor(&L, "visual_fc.weight", 2, vw, (int)fin);
+    add_tensor(&L, "visual_fc.bias", 1, vb, (int)fin);
     add_tensor(&L, "goal_fc.weight", 2, a, 3);
     add_tensor(&L, "goal_fc.bias", 1, b, 3);
     add_tensor(&L, "act_embed.weight", 2, e, 1);
-    add_tensor(&L, "rnn.weight_ih", 2, wi, (int)H);
-    add_tensor(&L, "rnn.weight_hh", 2, wh, (int)H);
-    add_tensor(&L, "rnn.bias_ih", 1, bg, (int)H);
-    add_tensor(&L, "rnn.bias_hh", 1, bg, (int)H);
+    if (!rgbd) {
+      add_tensor(&L, "rnn.weight_ih", 2, wi, (int)H);
+      add_tensor(&L, "rnn.weight_hh", 2, wh, (int)H);
+      add_tensor(&L, "rnn.bias_ih", 1, bg, (int)H);
+      add_tensor(&L, "rnn.bias_hh", 1, bg, (int)H);
+    } else {
+      for (int l = 0; l < 2; ++l) {
+        snprintf(name, sizeof(name), "rnn.weight_ih_l%d", l);
+        add_tensor(&L, name, 2, l == 0 ? wi : wi1, (int)H);
+        snprintf(name, sizeof(name), "rnn.weight_hh_l%d", l);
+        add_tensor(&L, name, 2, wh, (int)H);
+        snprintf(name, sizeof(name), "rnn.bias_ih_l%d", l);
+        add_tensor(&L, name, 1, bg, (int)H);
+        snprintf(name, sizeof(name), "rnn.bias_hh_l%d", l);
+        add_tensor(&L, name, 1, bg, (int)H);
+      }
+    }
     add_tensor(&L, "head.weight", 2, hw, (int)H);
     add_tensor(&L, "head.bias", 1, hb, (int)H);
   } else {

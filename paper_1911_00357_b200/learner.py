@@ -17,7 +17,7 @@ ROLLOUT_FIELDS = {  # name -> torch dtype
     "goal": torch.float32, "prev_action": torch.int32, "mask": torch.float32, "h0": torch.float32,
     "action": torch.int32, "logp_old": torch.float32, "obs": torch.float32, "c0": torch.float32,
 }
-OBS_SHAPE = (1, 64, 64)  # depth frames of the Depth agent (BASELINE configs[2])
+OBS_SHAPES = {2: (1, 64, 64), 3: (4, 256, 256)}  # Depth (configs[2]) / RGB-D (configs[3]) frames
 
 
 class Learner:
@@ -43,11 +43,13 @@ class Learner:
         wsb = learner_workspace_size(self.desc, E, T, self.ld, minibatches, epochs)
         self.ws = torch.empty(wsb // 4 + 64, **f32)
         ld = self.ld
+        self.rnn_layers = 2 if self.desc.arch == 3 else 1  # DDPPO_ARCH_RGBD_R50_LSTM2: 2 LSTM layers
+        hs = self.rnn_layers * self.hidden
         shapes = {"rew": (E, ld), "val": (E, ld), "done": (E, ld), "length": (E,), "goal": (E, T, 3),
-                  "prev_action": (E, ld), "mask": (E, ld), "h0": (E, self.hidden), "action": (E, ld),
+                  "prev_action": (E, ld), "mask": (E, ld), "h0": (E, hs), "action": (E, ld),
                   "logp_old": (E, ld)}
-        if self.desc.arch == 2:  # DDPPO_ARCH_DEPTH_R18_LSTM: + depth frames and LSTM cell state
-            shapes.update(obs=(E, T) + OBS_SHAPE, c0=(E, self.hidden))
+        if self.desc.arch in (2, 3):  # visual agents: + frames and the LSTM cell state
+            shapes.update(obs=(E, T) + OBS_SHAPES[self.desc.arch], c0=(E, hs))
         self.dev = {k: torch.zeros(s, dtype=ROLLOUT_FIELDS[k], device=dev) for k, s in shapes.items()}
         self.perms = torch.zeros((epochs, E), dtype=torch.int32, device=dev)
         self.adv = torch.zeros((E, ld), **f32)

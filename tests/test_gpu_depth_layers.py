@@ -50,7 +50,10 @@ def nchw(a):
     (5, 2, 256, 128, 3, 1, 1),  # compress (2x2 maps)
     (3, 7, 24, 40, 3, 2, 1),    # ragged
     (4, 5, 8, 16, 1, 1, 0),     # 1x1 / stride 1
-    (2, 9, 1, 16, 3, 1, 1)])    # single-channel (stem kernels) at another geometry
+    (2, 9, 1, 16, 3, 1, 1),     # single-channel (stem kernels) at another geometry
+    (2, 32, 8, 32, 7, 2, 3),    # RGB-D stem (4 channels padded to 8)
+    (2, 8, 64, 256, 1, 1, 0),   # bottleneck 1x1 expansion
+    (2, 4, 1024, 128, 3, 1, 1)])  # RGB-D compression (1024 -> 128 at 4x4)
 def test_conv2d(dd, ctx, F, H, Ci, Co, k, s, p):
     rng = np.random.default_rng(F * 100 + H + Ci + Co + k)
     x = rng.normal(size=(F, Ci, H, H)).astype(np.float32)
@@ -80,7 +83,8 @@ def test_conv2d(dd, ctx, F, H, Ci, Co, k, s, p):
 
 @pytest.mark.parametrize("F,HW,C,relu,res", [(3, 1024, 32, True, False), (2, 64, 64, False, True),
                                              (5, 4, 256, True, True), (4, 4, 128, True, False),
-                                             (2, 9, 16, False, False)])
+                                             (2, 9, 16, False, False), (2, 16, 1024, True, True),
+                                             (2, 256, 512, False, False)])
 def test_groupnorm(dd, ctx, F, HW, C, relu, res):
     rng = np.random.default_rng(F + HW + C)
     y = (rng.normal(size=(F, C, HW, 1)) * 2 + 0.5).astype(np.float32)

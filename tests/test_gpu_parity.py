@@ -260,27 +260,31 @@ def test_clip_adam(dd, ctx, P, clip, freeze):
 
 
 # ------------------------------------------------------------------ a5 / a7 networks
+VISUAL = {"depth": dict(obs=(1, 64, 64), layers=1), "rgbd": dict(obs=(4, 256, 256), layers=2)}
+
+
 def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
     desc = dd.model_desc(arch)
     H = desc.hidden
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     params = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, seed)
-    depth = arch == "depth"
-    ro = synth.rollout(E, T, seed, length=lengths, hidden=H, obs_shape=(1, 64, 64) if depth else None)
+    vis = VISUAL.get(arch)
+    ro = synth.rollout(E, T, seed, length=lengths, hidden=H, obs_shape=vis["obs"] if vis else None,
+                       rnn_layers=vis["layers"] if vis else 1)
     rng = np.random.default_rng(seed)
     env_idx = rng.permutation(E)[:B].astype(np.int32)
     L = ro["length"][env_idx]
     T_run = int(L.max())
     batch = dd.make_batch(cu(ro["goal"]), cu(ro["prev_action"]), cu(ro["mask"]), cu(ro["h0"]), cu(ro["length"]),
                           cu(env_idx), E, T, ro["ld"], B, T_run, int(L.sum()),
-                          obs=cu(ro["obs"]) if depth else None, c0=cu(ro["c0"]) if depth else None)
+                          obs=cu(ro["obs"]) if vis else None, c0=cu(ro["c0"]) if vis else None)
     ws = torch.zeros(dd.workspace_size(desc, B, T_run) // 4 + 64, device="cuda")
     lg = torch.zeros((B, T_run, 4), device="cuda")
     vl = torch.zeros((B, T_run), device="cuda")
     pg = cu(params)
     dd.ddppo_policy_fwd(ctx, desc, pg, batch, lg, vl, ws)
-    dec = dd.ddppo_debug_depth_decisions(ctx, batch, ws).cpu().numpy() if depth else None
+    dec = dd.ddppo_debug_depth_decisions(ctx, desc, batch, ws).cpu().numpy() if vis else None
     dl = rng.normal(0, 1e-2, (B, T_run, 4)).astype(np.float32)
     dv = rng.normal(0, 1e-2, (B, T_run)).astype(np.float32)
     grad = torch.full((P,), 3.0, device="cuda")
@@ -288,21 +292,21 @@ def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
     torch.cuda.synchronize()
     ob = {"goal": ro["goal"][env_idx, :T_run], "prev_action": ro["prev_action"][env_idx, :T_run],
           "mask": ro["mask"][env_idx, :T_run], "h0": ro["h0"][env_idx]}
-    if depth:
+    if vis:
         ob.update(obs=ro["obs"][env_idx, :T_run], c0=ro["c0"][env_idx])
     lo, vo, cache = models.forward(arch, params, ob, hidden=H)
-    if depth:
-        _adopt_decisions(params, ob, cache, dec, B * T_run)
+    if vis:
+        _adopt_decisions(arch, params, ob, cache, dec, B * T_run)
     go = models.backward(arch, params, cache, dl.astype(np.float64), dv.astype(np.float64), hidden=H)
     return lay, lg.cpu().numpy(), vl.cpu().numpy(), grad.cpu().numpy(), lo, vo, go
 
 
-def _adopt_decisions(params, ob, cache, dec, F, tie=1e-4):
-    """Hand the oracle's backward the kernel forward's ReLU masks / max-pool argmax (reading Z24):
+def _adopt_decisions(arch, params, ob, cache, dec, F, tie=1e-4):
+    """Hand the oracle's backward the kernel forward's ReLU masks / max-pool argmax (reading R6):
     every decision the two sides take differently must be a near-tie in the oracle's fp64
     forward (|pre-activation| <= tie * rms of its layer; pool: within tie of the window max),
     i.e. a case where both choices are correct; everything else must agree exactly."""
-    p = models.unpack("depth", params)
+    p = models.unpack(arch, params)
     x = np.asarray(ob["obs"], np.float64).reshape((F,) + ob["obs"].shape[2:])
     enc = cache["enc"]
     off = [0]
@@ -314,25 +318,22 @@ def _adopt_decisions(params, ob, cache, dec, F, tie=1e-4):
         off[0] += n
         return a
 
-    flips = [0]
-
     def adopt(key, pre):
         gpu = take(pre.shape).astype(bool)
-        ref = pre > 0
-        diff = gpu != ref
+        diff = gpu != (pre > 0)
         if diff.any():
             rms = np.sqrt(np.mean(pre ** 2))
             assert np.all(np.abs(pre[diff]) <= tie * rms), (key, np.abs(pre[diff]).max() / rms)
-            flips[0] += int(diff.sum())
         enc[key] = gpu
+        return pre * gpu
 
     def cg(z, c, g, s, pad):
         y, _ = convnets.conv_fwd(z, p[c + ".weight"], s, pad)
         return convnets.gn_fwd(y, p[g + ".weight"], p[g + ".bias"])[0]
 
-    pre = cg(x, "enc.stem.conv", "enc.stem.gn", 2, 3)
-    adopt("enc.stem.conv.relu", pre)
-    z = pre * enc["enc.stem.conv.relu"]
+    if arch == "rgbd":
+        x = convnets.avgpool2_fwd(convnets.rgbd_normalize(x))
+    z = adopt("enc.stem.conv.relu", cg(x, "enc.stem.conv", "enc.stem.gn", 2, 3))
     _, pc = convnets.maxpool_fwd(z)
     N, C, Hh, Ww = z.shape
     Ho = pc[5]
@@ -340,38 +341,37 @@ def _adopt_decisions(params, ob, cache, dec, F, tie=1e-4):
     if not np.array_equal(gpu_arg, pc[1]):
         zp = np.pad(z, ((0, 0), (0, 0), (1, 1), (1, 1)), constant_values=-np.inf)
         win = np.stack([zp[:, :, u:u + 2 * Ho:2, v:v + 2 * Ho:2] for u in range(3) for v in range(3)], axis=-1)
-        mx = win.max(axis=-1)
         picked = np.take_along_axis(win, gpu_arg[..., None], -1)[..., 0]
         d = gpu_arg != pc[1]
-        assert np.all(mx[d] - picked[d] <= tie * np.sqrt(np.mean(z ** 2))), "pool argmax"
-        flips[0] += int(d.sum())
+        assert np.all(win.max(axis=-1)[d] - picked[d] <= tie * np.sqrt(np.mean(z ** 2))), "pool argmax"
     enc["pool"] = pc[:1] + (gpu_arg,) + pc[2:]
     z, _ = convnets.maxpool_fwd(z)  # the pooled values are the same whichever tied element is picked
     cin = 32
-    for li, c in enumerate(convnets.WIDTHS):
-        for bi in range(2):
+    nblocks = convnets.R50_BLOCKS if arch == "rgbd" else (2, 2, 2, 2)
+    for li, (w, nb) in enumerate(zip(convnets.WIDTHS, nblocks)):
+        for bi in range(nb):
             s = 2 if (bi == 0 and li > 0) else 1
-            pre_name = f"enc.layer{li + 1}.{bi}"
-            a = cg(z, pre_name + ".conv1", pre_name + ".gn1", s, 1)
-            adopt(pre_name + ".conv1.relu", a)
-            a = a * enc[pre_name + ".conv1.relu"]
-            b = cg(a, pre_name + ".conv2", pre_name + ".gn2", 1, 1)
-            sc = cg(z, pre_name + ".down.conv", pre_name + ".down.gn", s, 0) if (s != 1 or cin != c) else z
-            out = b + sc
-            adopt(pre_name + ".out", out)
-            z = out * enc[pre_name + ".out"]
-            cin = c
-    pre = cg(z, "enc.compress.conv", "enc.compress.gn", 1, 1)
-    adopt("enc.compress.conv.relu", pre)
+            pre = f"enc.layer{li + 1}.{bi}"
+            if arch == "rgbd":  # bottleneck 1x1 -> 3x3 (stride) -> 1x1
+                cout = 4 * w
+                a = adopt(pre + ".conv1.relu", cg(z, pre + ".conv1", pre + ".gn1", 1, 0))
+                a = adopt(pre + ".conv2.relu", cg(a, pre + ".conv2", pre + ".gn2", s, 1))
+                b = cg(a, pre + ".conv3", pre + ".gn3", 1, 0)
+            else:
+                cout = w
+                a = adopt(pre + ".conv1.relu", cg(z, pre + ".conv1", pre + ".gn1", s, 1))
+                b = cg(a, pre + ".conv2", pre + ".gn2", 1, 1)
+            sc = cg(z, pre + ".down.conv", pre + ".down.gn", s, 0) if (s != 1 or cin != cout) else z
+            z = adopt(pre + ".out", b + sc)
+            cin = cout
+    adopt("enc.compress.conv.relu", cg(z, "enc.compress.conv", "enc.compress.gn", 1, 1))
     vis = dec[off[0]:off[0] + F * 512].reshape(cache["vis"].shape).astype(bool)
     vpre = cache["flat"] @ p["visual_fc.weight"].T + p["visual_fc.bias"]
     d = vis != (vpre > 0)
     assert np.all(np.abs(vpre[d]) <= tie * np.sqrt(np.mean(vpre ** 2))), "visual fc relu"
-    flips[0] += int(d.sum())
     cache["vis"] = vis.astype(np.float64)  # backward only reads its > 0 mask
     off[0] += F * 512
     assert off[0] == dec.size
-    return flips[0]
 
 
 def test_toy_network_parity(dd, ctx):
@@ -410,15 +410,29 @@ def test_depth_network_parity(dd, ctx, E, T, B, lengths):
     assert not bad, bad
 
 
+# RGB-D agent (configs[3]): the same tolerances; 256x256 frames keep the fp64 oracle to a few frames
+@pytest.mark.parametrize("E,T,B,lengths", [(2, 2, 2, [2, 1])])
+def test_rgbd_network_parity(dd, ctx, E, T, B, lengths):
+    lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, "rgbd", E, T, B, 60 + E + T, lengths)
+    assert rel_l2(lg, lo) < 1e-3 and rel_l2(vl, vo) < 1e-3, (rel_l2(lg, lo), rel_l2(vl, vo))
+    bad = []
+    for name, off, shape, _ in lay:
+        n = int(np.prod(shape))
+        e = rel_l2(g[off:off + n], go[off:off + n])
+        if not e < 2e-2:
+            bad.append((name, e))
+    assert not bad, bad
+
+
 # ------------------------------------------------------------------ the whole learner step (a2..a8), N = 1
 @pytest.mark.parametrize("cfgname,lengths", [("toy", None), ("gps", None), ("gps", [128, 96, 128, 32]),
-                                             ("depth", [12, 5, 12, 9])])
+                                             ("depth", [12, 5, 12, 9]), ("rgbd", [2, 1, 2, 2])])
 def test_learner_step_parity(dd, ctx, cfgname, lengths):
     from paper_1911_00357_b200.learner import Learner
     c = dict(synth.CONFIGS[cfgname])
     adam_eps = 1e-8
-    if cfgname == "depth":
-        c["T"] = 12  # the oracle's fp64 ResNet keeps this case to seconds
+    if cfgname in ("depth", "rgbd"):
+        c["T"] = 12 if cfgname == "depth" else 2  # the oracle's fp64 ResNets keep this case to seconds
         # Adam's first steps are lr*sign(g) wherever |g| >> eps, so an element whose oracle gradient
         # sits within the bf16 error of 0 may legitimately step the other way; eps = 1e-3 (of the
         # order of a typical encoder |g|) makes the update a smooth function of g, so the gradient
@@ -429,7 +443,8 @@ def test_learner_step_parity(dd, ctx, cfgname, lengths):
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 21)
     lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, adam_eps=adam_eps)
-    ro = synth.rollout(c["E"], c["T"], 22, length=lengths, hidden=desc.hidden, obs_shape=c.get("obs"))
+    ro = synth.rollout(c["E"], c["T"], 22, length=lengths, hidden=desc.hidden, obs_shape=c.get("obs"),
+                       rnn_layers=c.get("rnn_layers", 1))
     pm = synth.perms(22, 0, c["epochs"], c["E"])
     lrn.load_rollout(ro, pm)
     stats = lrn.step().cpu().numpy()
@@ -443,7 +458,7 @@ def test_learner_step_parity(dd, ctx, cfgname, lengths):
     A = lrn.adv.cpu().numpy()
     for n in range(c["E"]):
         close_rel(A[n, :info["adv"][0].shape[1]], info["adv"][0][n], 1e-5, "adv")
-    tol = {"toy": 1e-4, "gps": 2e-2, "depth": 3e-2}[cfgname]
+    tol = {"toy": 1e-4, "gps": 2e-2, "depth": 3e-2, "rgbd": 3e-2}[cfgname]
     for k, ms in enumerate(info["mb_stats"]):
         for i, name in enumerate(ppo.STAT_NAMES):
             ref = ms[name]
@@ -454,10 +469,13 @@ def test_learner_step_parity(dd, ctx, cfgname, lengths):
     for name, off, shape, _ in lay:
         n = int(np.prod(shape))
         e = rel_l2(dp[off:off + n], dpo[off:off + n])
-        # depth: the learner's 4 internal minibatches take their own ReLU / max-pool decisions, which
-        # cannot be handed to the oracle here (test_depth_network_parity does that); a decision
-        # flipped at a near-tie perturbs the earliest encoder layers most, hence 1e-1 for enc.*
-        lim = 1e-3 if cfgname == "toy" else (1e-1 if name.startswith("enc.") else 5e-2)
+        # visual agents: the learner's 4 internal minibatches take their own ReLU / max-pool decisions,
+        # which cannot be handed to the oracle here (test_{depth,rgbd}_network_parity do that and pin
+        # every gradient at 2e-2); decisions flipped at near-ties perturb the earliest encoder layers
+        # most -- ResNet18/2 (~0.3 M ReLU sites per frame) stays within 1e-1, ResNet50/2 (~1.8 M)
+        # within 5e-1 -- so enc.* is checked loosely here and everything downstream at 5e-2
+        enc_lim = {"depth": 1e-1, "rgbd": 5e-1}.get(cfgname, 5e-2)
+        lim = 1e-3 if cfgname == "toy" else (enc_lim if name.startswith("enc.") else 5e-2)
         if not e < lim:
             bad.append((name, round(e, 4)))
     assert not bad, bad
