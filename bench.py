@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+JSON_OUT = sys.stdout
 
 
 def parse():
@@ -179,7 +180,7 @@ def run_reference(args, rank, world):
                          "kind": "oracle", "sample": f"{n} whole learner steps on {c['E']} envs x {T_s} steps (rank-0 rollout)"},
         "e2e": {"value": sps, "unit": "experience-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out))
+    print(json.dumps(out), file=JSON_OUT, flush=True)
     return 0
 
 
@@ -197,9 +198,12 @@ def workload_name(cfgname, c):
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
-    # one JSON line on stdout: keep NCCL's version banner (NCCL_DEBUG=VERSION) off it
-    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # one JSON line on stdout: everything native code prints (NCCL's version banner, warnings) is
+    # sent to stderr by pointing fd 1 at fd 2; the JSON line goes to the saved original stdout
+    global JSON_OUT
+    sys.stdout.flush()
+    JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -359,7 +363,7 @@ def main():
             "kernel_ms": {k: round(v, 4) for k, v in fam_ms.items() if v > 0},
             "roofline": roofline, "cpu_baseline": cpu_base,
         }
-        print(json.dumps(out))
+        print(json.dumps(out), file=JSON_OUT, flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -268,6 +268,15 @@ typedef struct {
 
 ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int E, int T, int ld,
                                           int minibatches, int epochs, size_t* host_bytes);
+/* collective: make this workspace (allocated for the learner_step configuration every rank uses)
+ * visible to all ranks over NVLink (CUDA IPC handles exchanged with an NCCL all-gather).  After
+ * it, ddppo_learner_step on this ws performs a8 over peer memory instead of NCCL: every rank sums
+ * all ranks' gradients in rank order 0..N-1 (bit-identical on every rank), computes the clip norm
+ * in the same pass and applies Adam; a flag barrier per minibatch (release/acquire at system
+ * scope, bounded wait -> ddppo_check reports a communication error).  The workspace must stay
+ * allocated while the context lives.  World size 1: no-op.  At most one workspace per context. */
+ddppo_status ddppo_learner_register(ddppo_ctx* ctx, void* ws, size_t ws_bytes);
+
 /* params/m/v [P] updated in place; adv/ret [E][ld] outputs; stats_out (device float
  * [epochs*minibatches][8]) receives each minibatch's loss stats; host_cfg->adam.step is read,
  * *host_step_out receives the new update count. */

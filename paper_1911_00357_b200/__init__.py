@@ -255,6 +255,11 @@ def profile_read(ctx, reset=False):
     return {k: (ms[i], la[i]) for i, k in enumerate(_lib.KERNEL_FAMILIES)}
 
 
+def ddppo_learner_register(ctx, ws):
+    """Collective: expose this learner workspace to all ranks (a8 over NVLink peer memory)."""
+    _call(ctx, "ddppo_learner_register", dptr(ws), ws.numel() * ws.element_size())
+
+
 def ddppo_learner_step(ctx, desc, ro, cfg, params, m, v, adv, ret, stats_out, ws, stream=None):
     """ro: Rollout struct (device pointers + host lengths/perms). Returns the new Adam step count."""
     step = ctypes.c_int32()

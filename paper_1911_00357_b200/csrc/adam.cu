@@ -93,6 +93,19 @@ adam_kernel(const float* __restrict__ g, float* __restrict__ p, float* __restric
 
 }  // namespace
 
+ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, float* m, float* v,
+                              const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, cudaStream_t st) {
+  DDPPO_REQUIRE(ctx, P >= 1 && cfg.step >= 1, "adam: need P >= 1 and step >= 1");
+  const int blocks = grid_for((int)std::min<int64_t>((P + 3) / 4, 1 << 30), kThreads, ctx->sm_count * 4);
+  ProfScope ps(ctx, DDPPO_K_ADAM, st, 1);
+  const double bc1 = 1.0 - pow((double)cfg.beta1, (double)cfg.step);
+  const double bc2 = 1.0 - pow((double)cfg.beta2, (double)cfg.step);
+  adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
+                                           (float)((double)cfg.lr / bc1), (float)(1.0 / sqrt(bc2)), cfg.eps);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
 ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float* m, float* v,
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
                               float* grad_norm, cudaStream_t st) {

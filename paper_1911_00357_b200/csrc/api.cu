@@ -85,6 +85,11 @@ ddppo_status ddppo_ctx_destroy(ddppo_ctx* ctx) {
     cudaEventDestroy(r.b);
   }
   for (auto e : ctx->pool) cudaEventDestroy(e);
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (auto e : ctx->fork_events) cudaEventDestroy(e);
+  for (auto s : ctx->side)
+    if (s) cudaStreamDestroy(s);
+  cudaFree(ctx->own_flags);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_counters);
@@ -104,6 +109,11 @@ ddppo_status ddppo_check(ddppo_ctx* ctx, void* stream) {
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   int err = 0;
   DDPPO_CUDA_TRY(ctx, cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err & ERR_BIT_COMM) {
+    DDPPO_CUDA_TRY(ctx, cudaMemset(ctx->d_err, 0, sizeof(int)));
+    ctx->last_error = "peer barrier timed out (a rank did not reach the gradient exchange)";
+    return DDPPO_ERR_COMM;
+  }
   if (err) {
     DDPPO_CUDA_TRY(ctx, cudaMemset(ctx->d_err, 0, sizeof(int)));
     ctx->last_error = std::string("non-finite value in ") + ((err & ERR_BIT_LOSS) ? "loss " : "") +
@@ -300,7 +310,9 @@ struct LearnerWs {
   float* values;
   float* dlogits;
   float* dvalues;
-  float* grad;
+  float* grad;      // this minibatch's gradient (one of grad2[], by minibatch parity when peers are used)
+  float* grad2[2];
+  float* gsum;      // rank-ordered sum of all ranks' gradients (peer path)
   float* grad_norm;
   void* model_ws;
   size_t model_bytes;
@@ -324,7 +336,10 @@ size_t carve_learner(const ddppo_model_desc* d, int E, int T, int mb, void* base
   t.values = (float*)take((size_t)B * T * sizeof(float));
   t.dlogits = (float*)take((size_t)B * T * 4 * sizeof(float));
   t.dvalues = (float*)take((size_t)B * T * sizeof(float));
-  t.grad = (float*)take((size_t)P * sizeof(float));
+  t.grad2[0] = (float*)take((size_t)P * sizeof(float));
+  t.grad2[1] = (float*)take((size_t)P * sizeof(float));
+  t.grad = t.grad2[0];
+  t.gsum = (float*)take((size_t)P * sizeof(float));
   t.grad_norm = (float*)take(8 * sizeof(float));
   t.model_ws = take(model_bytes);
   t.model_bytes = model_bytes;
@@ -340,6 +355,23 @@ ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int
       ld < T + 1 || epochs < 1)
     return DDPPO_ERR_CONFIG;
   *host_bytes = carve_learner(host_desc, E, T, minibatches, nullptr, nullptr);
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_learner_register(ddppo_ctx* ctx, void* ws, size_t ws_bytes) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, ws && ws_bytes > 0, "learner_register: null workspace");
+  if (ctx->world == 1) return DDPPO_OK;  // nothing to share
+  DDPPO_REQUIRE(ctx, ctx->world <= kMaxPeers, "learner_register: at most 8 ranks");
+  DDPPO_REQUIRE(ctx, ctx->peer_ws == nullptr, "learner_register: a workspace is already registered");
+  ddppo_status s = peer_setup_flags(ctx);
+  if (s != DDPPO_OK) return s;
+  void* out[kMaxPeers] = {};
+  s = peer_exchange(ctx, ws, out);
+  if (s != DDPPO_OK) return s;
+  for (int r = 0; r < ctx->world; ++r) ctx->peer_ws_base[r] = reinterpret_cast<char*>(out[r]);
+  ctx->peer_ws = ws;
+  ctx->peer_mb = 0;
   return DDPPO_OK;
 }
 
@@ -364,6 +396,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
   LearnerWs w;
   carve_learner(host_desc, ro->E, ro->T, cfg->minibatches, ws, &w);
   cudaStream_t st = as_stream(stream);
+  const bool use_peers = ctx->world > 1 && ctx->peer_ws == ws;  // ddppo_learner_register'ed workspace
 
   // a2 GAE (+ local adv stats), a3 global normalisation statistics
   s = launch_gae(ctx, ro->rew, ro->val, ro->done, ro->len, ro->E, ro->T, ro->ld, cfg->gamma, cfg->tau, adv, ret,
@@ -416,6 +449,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
       s = launch_loss(ctx, w.logits, w.values, b, li, cfg->normalize_adv ? w.mean_invstd : nullptr, cfg->loss,
                       w.dlogits, w.dvalues, st_out, st);
       if (s != DDPPO_OK) return s;
+      w.grad = use_peers ? w.grad2[ctx->peer_mb & 1] : w.grad2[0];
       if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
         s = toy_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
       else if (visual)
@@ -424,7 +458,17 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
         s = gps_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
       if (s != DDPPO_OK) return s;
       acfg.step = ++step;
-      s = ddppo_grad_allreduce_step(ctx, w.grad, params, m, v, nullptr, L.P, &acfg, nullptr, stream);
+      if (use_peers) {  // a8 over NVLink peer memory: rank-ordered sum + clip norm, then Adam
+        ProfScope ps(ctx, DDPPO_K_ALLREDUCE, st, 0);
+        float* peers[kMaxPeers];
+        const size_t off = (size_t)((char*)w.grad - (char*)ws);
+        for (int r = 0; r < ctx->world; ++r) peers[r] = reinterpret_cast<float*>(ctx->peer_ws_base[r] + off);
+        s = launch_peer_reduce_norm(ctx, peers, w.gsum, L.P, acfg.max_grad_norm, nullptr, st);
+        if (s == DDPPO_OK) s = launch_adam_only(ctx, w.gsum, params, m, v, nullptr, L.P, acfg, st);
+        ++ctx->peer_mb;
+      } else {
+        s = ddppo_grad_allreduce_step(ctx, w.grad, params, m, v, nullptr, L.P, &acfg, nullptr, stream);
+      }
       if (s != DDPPO_OK) return s;
     }
   }

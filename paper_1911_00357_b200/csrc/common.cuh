@@ -10,6 +10,8 @@
 
 #include "../../include/ddppo.h"
 
+constexpr int kMaxPeers = 8;
+
 struct ddppo_ctx {
   int rank = 0, world = 1, device = 0, sm_count = 148;
   ncclComm_t comm = nullptr;
@@ -21,6 +23,19 @@ struct ddppo_ctx {
   int32_t* d_i32 = nullptr;            // preemption poll buffer
   int64_t* d_i64 = nullptr;            // counts buffer
   std::string last_error;
+  // NVLink peer memory (peer.cu): flag arrays of every rank, IPC mappings, the registered learner
+  // workspace of every rank, the barrier epoch and the running minibatch counter (gradient parity)
+  unsigned int* peer_flags[kMaxPeers] = {};
+  unsigned int* own_flags = nullptr;
+  std::vector<void*> ipc_opened;
+  void* peer_ws = nullptr;
+  char* peer_ws_base[kMaxPeers] = {};
+  unsigned int peer_epoch = 0;
+  uint64_t peer_mb = 0;
+  // side streams for work beside the recurrences (fork / join with events), created lazily
+  cudaStream_t side[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> fork_events;
+  size_t fork_next = 0;
   // measurement (ddppo_profile_*)
   bool prof = false;
   int64_t launches[DDPPO_K_COUNT] = {};
@@ -72,7 +87,7 @@ enum { CNT_GAE = 0, CNT_LOSS = 1, CNT_NORM = 2, CNT_MISC = 3, CNT_NUM = 8 };
 constexpr int kMaxPartials = 1 << 16;   // doubles
 constexpr int kMaxCountVals = 64;
 
-enum { ERR_BIT_LOSS = 1, ERR_BIT_GRAD = 2 };
+enum { ERR_BIT_LOSS = 1, ERR_BIT_GRAD = 2, ERR_BIT_COMM = 4 };
 
 #define DDPPO_CUDA_TRY(ctx, expr)                                                 \
   do {                                                                            \
@@ -101,6 +116,27 @@ enum { ERR_BIT_LOSS = 1, ERR_BIT_GRAD = 2 };
   } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ctx side streams (non-blocking, created on first use on the ctx's device)
+inline ddppo_status ctx_side_streams(ddppo_ctx* ctx, cudaStream_t* a, cudaStream_t* b) {
+  for (int i = 0; i < 2; ++i)
+    if (!ctx->side[i]) DDPPO_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking));
+  *a = ctx->side[0];
+  *b = ctx->side[1];
+  return DDPPO_OK;
+}
+// make `to` wait for all work enqueued so far on `from` (a recycled timing-free event)
+inline cudaError_t fork_to(ddppo_ctx* ctx, cudaStream_t from, cudaStream_t to) {
+  if (ctx->fork_events.size() < 64) {
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r != cudaSuccess) return r;
+    ctx->fork_events.push_back(e);
+  }
+  cudaEvent_t e = ctx->fork_events[ctx->fork_next++ % ctx->fork_events.size()];
+  cudaError_t r = cudaEventRecord(e, from);
+  return r == cudaSuccess ? cudaStreamWaitEvent(to, e, 0) : r;
+}
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ float warp_sum(float v) {
@@ -233,6 +269,15 @@ struct IGemm {                   // C[m][n] (+)= sum_k A(m,k) B(n,k), fp32 C
   int auto_split = 0;            // with `partial` (>= 16*M*N floats): split k when the tile grid is small
 };
 ddppo_status launch_igemm(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st);
+
+// NVLink peer memory (peer.cu)
+ddppo_status peer_exchange(ddppo_ctx* ctx, void* local, void** out);
+ddppo_status peer_setup_flags(ddppo_ctx* ctx);
+ddppo_status launch_peer_reduce_norm(ddppo_ctx* ctx, float* const* peers, float* gsum, int64_t P, float max_norm,
+                                     float* grad_norm, cudaStream_t st);
+// Adam on an already summed gradient whose clip scale is in ctx->d_scalars[0] (adam.cu)
+ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, float* m, float* v,
+                              const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, cudaStream_t st);
 
 // tcgen05 GEMM: C[m][n] (+)= sum_k A(m,k) B(n,k) with generic strides or conv gathers (gemm_tc.cu)
 struct GemmTC {

@@ -951,38 +951,47 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");
   GpsPtrs p = make_ptrs(L, params, b, ws);
   const int S = b.B * b.T_run;
+  // The recurrence occupies 16 SMs; work off its dependency chain runs beside it on two side
+  // streams (fork / join through events on the launching stream).
+  cudaStream_t sa = nullptr, sb = nullptr;
+  ddppo_status s = ctx_side_streams(ctx, &sa, &sb);
+  if (s != DDPPO_OK) return s;
   {
     ProfScope ps(ctx, DDPPO_K_HEAD, st, 2);
     head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, dlogits, dvalues, S, p.dH);
-    head_wgrad_kernel<<<kH / 32, 256, 0, st>>>(p.Hs, dlogits, dvalues, S, grad + layout_offset(L, "head.weight"),
+    DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sa));
+    head_wgrad_kernel<<<kH / 32, 256, 0, sa>>>(p.Hs, dlogits, dvalues, S, grad + layout_offset(L, "head.weight"),
                                               grad + layout_offset(L, "head.bias"));
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   }
   {
     ProfScope ps(ctx, DDPPO_K_NET_BWD, st, 1);
-    ddppo_status s =
-        launch_cluster(ctx, gps_gru_bwd_kernel, kBwdThreads, sizeof(BwdSmem) + (size_t)S * sizeof(float), p, st);
+    s = launch_cluster(ctx, gps_gru_bwd_kernel, kBwdThreads, sizeof(BwdSmem) + (size_t)S * sizeof(float), p, st);
     if (s != DDPPO_OK) return s;
   }
-  // weight gradients (off the dependency chain)
-  ProfScope ps(ctx, DDPPO_K_WGRAD, st, 2);  // + the 3 GEMMs, counted by launch_gemm_tc
-  // tcgen05 GEMMs (bf16 operands, fp32 TMEM accumulation) over the S samples:
+  // weight gradients (off the dependency chain), tcgen05 GEMMs over the S samples:
   //   dW_hh[row][j] = sum_s dG_h[s][row] H_in[s][j];  dW_ih[row][j] = sum_s dG_x[s][row] X[s][j]
   //   Q[row][n]     = sum_s dG_x[s][row] U[s][n]   (-> goal FC, embedding and b_ih gradients)
-  ddppo_status gs = launch_gemm_tc(
-      ctx, GemmTC{p.dGH, 1, kG, p.Hin, 1, kH, grad + layout_offset(L, "rnn.weight_hh"), kH, kG, kH, S}, st);
-  if (gs != DDPPO_OK) return gs;
-  gs = launch_gemm_tc(ctx, GemmTC{p.dGI, 1, kG, p.X, 1, kIn, grad + layout_offset(L, "rnn.weight_ih"), kIn, kG, kIn, S},
-                      st);
-  if (gs != DDPPO_OK) return gs;
-  gs = launch_gemm_tc(ctx, GemmTC{p.dGI, 1, kG, p.U, 1, kU, p.Q, kU, kG, kU, S}, st);
-  if (gs != DDPPO_OK) return gs;
-  colsum_kernel<<<kG / 32, 256, 0, st>>>(p.dGH, kG, S, kG, grad + layout_offset(L, "rnn.bias_hh"));
-  input_layer_grads_kernel<<<kIn, 256, 0, st>>>(p.Wih, p.Q, grad + layout_offset(L, "goal_fc.weight"),
+  // main stream: dW_hh; side a: dW_ih; side b: Q, input-layer gradients, db_hh
+  ProfScope ps(ctx, DDPPO_K_WGRAD, st, 2);  // + the 3 GEMMs, counted by launch_gemm_tc
+  DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sa));
+  DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sb));
+  s = launch_gemm_tc(ctx, GemmTC{p.dGH, 1, kG, p.Hin, 1, kH, grad + layout_offset(L, "rnn.weight_hh"), kH, kG, kH, S},
+                     st);
+  if (s != DDPPO_OK) return s;
+  s = launch_gemm_tc(ctx, GemmTC{p.dGI, 1, kG, p.X, 1, kIn, grad + layout_offset(L, "rnn.weight_ih"), kIn, kG, kIn, S},
+                     sa);
+  if (s != DDPPO_OK) return s;
+  s = launch_gemm_tc(ctx, GemmTC{p.dGI, 1, kG, p.U, 1, kU, p.Q, kU, kG, kU, S}, sb);
+  if (s != DDPPO_OK) return s;
+  input_layer_grads_kernel<<<kIn, 256, 0, sb>>>(p.Wih, p.Q, grad + layout_offset(L, "goal_fc.weight"),
                                                 grad + layout_offset(L, "goal_fc.bias"),
                                                 grad + layout_offset(L, "act_embed.weight"),
                                                 grad + layout_offset(L, "rnn.bias_ih"));
+  colsum_kernel<<<kG / 32, 256, 0, sb>>>(p.dGH, kG, S, kG, grad + layout_offset(L, "rnn.bias_hh"));
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  DDPPO_CUDA_TRY(ctx, fork_to(ctx, sa, st));  // join
+  DDPPO_CUDA_TRY(ctx, fork_to(ctx, sb, st));
   return DDPPO_OK;
 }
 

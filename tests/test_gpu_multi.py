@@ -1,5 +1,6 @@
-"""N = 2 (or more) GPUs: the NCCL paths of steps a3 (adv-norm allreduce), a8 (gradient
-allreduce + Adam), a9 (preemption poll) and a10 (counts) through the C ABI, one process per GPU.
+"""N = 2 (or more) GPUs: the collective steps a3 (adv-norm allreduce), a8 (gradient allreduce +
+Adam, over NCCL and over NVLink peer memory), a9 (preemption poll) and a10 (counts) through the C
+ABI, one process per GPU.
 
 Checks: parameters bit-identical on every rank after a learner step; the update
 equals the oracle's N-rank learner step (per-tensor relative L2 of the parameter update, the
@@ -42,16 +43,25 @@ def _worker(rank, world, port, q):
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 5)
-    lrn = Learner(ctx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
     L = 128 if rank == 0 else 40
     ro = synth.rollout(c["E"], c["T"], 5, rank=rank, length=L)
     pm = synth.perms(5, 0, c["epochs"], c["E"], rank=rank)
-    lrn.load_rollout(ro, pm)
+    # a8 over NCCL (unregistered workspace), then over NVLink peer memory (registered workspace)
+    for key, peer in (("params_nccl", False), ("params", True)):
+        lrn = Learner(ctx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, peer=peer)
+        lrn.load_rollout(ro, pm)
+        lrn.step()
+        torch.cuda.synchronize()
+        ctx.check()
+        out[key] = lrn.params.cpu().numpy()
+    out["stats"] = lrn.stats.cpu().numpy()
+    # a second rollout through the peer path (gradient double buffer continues across calls)
+    ro2 = synth.rollout(c["E"], c["T"], 6, rank=rank, length=L)
+    lrn.load_rollout(ro2, synth.perms(6, 1, c["epochs"], c["E"], rank=rank))
     lrn.step()
     torch.cuda.synchronize()
     ctx.check()
-    out["params"] = lrn.params.cpu().numpy()
-    out["stats"] = lrn.stats.cpu().numpy()
+    out["params2"] = lrn.params.cpu().numpy()
     # ---- a10 counts
     out["counts"] = dd.ddppo_allreduce_counts(ctx, [c["E"] * L, rank + 1]).tolist()
     # ---- a9 preemption over NCCL (virtual ticks)
@@ -83,7 +93,8 @@ def test_two_rank_learner_step_and_protocols():
     res = dict(q.get(timeout=600) for _ in range(world))
     for p in procs:
         p.join(timeout=120)
-    assert np.array_equal(res[0]["params"], res[1]["params"])  # rank-identical
+    for key in ("params", "params_nccl", "params2"):
+        assert np.array_equal(res[0][key], res[1][key]), key  # rank-identical
     # oracle: the same two rollouts in one process
     import paper_1911_00357_b200 as dd
     c = synth.CONFIGS["gps"]
@@ -95,12 +106,13 @@ def test_two_rank_learner_step_and_protocols():
     pms = [synth.perms(5, 0, c["epochs"], c["E"], rank=r) for r in range(world)]
     po, _, _, _, info = learner.learner_step("gps", p0, np.zeros(P), np.zeros(P), 0, ros, pms,
                                              dict(epochs=c["epochs"], minibatches=c["minibatches"]))
-    dp = res[0]["params"].astype(np.float64) - p0
     dpo = po - p0
-    for name, off, shape, _ in lay:
-        n = int(np.prod(shape))
-        e = np.linalg.norm(dp[off:off + n] - dpo[off:off + n]) / np.linalg.norm(dpo[off:off + n])
-        assert e < 5e-2, (name, e)
+    for key in ("params", "params_nccl"):
+        dp = res[0][key].astype(np.float64) - p0
+        for name, off, shape, _ in lay:
+            n = int(np.prod(shape))
+            e = np.linalg.norm(dp[off:off + n] - dpo[off:off + n]) / np.linalg.norm(dpo[off:off + n])
+            assert e < 5e-2, (key, name, e)
     assert res[0]["counts"] == res[1]["counts"] == [c["E"] * (128 + 40), 3]
     for r in range(world):
         assert res[r]["L"] == res[r]["L_ref"]
