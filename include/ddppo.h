@@ -277,6 +277,12 @@ ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int
  * allocated while the context lives.  World size 1: no-op.  At most one workspace per context. */
 ddppo_status ddppo_learner_register(ddppo_ctx* ctx, void* ws, size_t ws_bytes);
 
+/* CUDA graphs for ddppo_learner_step (default on): the step is captured once per (configuration,
+ * buffer addresses, minibatch shapes) -- after one eager run of a new configuration -- and
+ * replayed; Adam's update count and the peer-barrier epoch are kept on the device so nothing
+ * host-side is baked into the graph.  While per-family profiling is enabled the step runs eagerly. */
+ddppo_status ddppo_set_graphs(ddppo_ctx* ctx, int enable);
+
 /* params/m/v [P] updated in place; adv/ret [E][ld] outputs; stats_out (device float
  * [epochs*minibatches][8]) receives each minibatch's loss stats; host_cfg->adam.step is read,
  * *host_step_out receives the new update count. */

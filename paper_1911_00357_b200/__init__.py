@@ -255,6 +255,11 @@ def profile_read(ctx, reset=False):
     return {k: (ms[i], la[i]) for i, k in enumerate(_lib.KERNEL_FAMILIES)}
 
 
+def ddppo_set_graphs(ctx, enable=True):
+    """CUDA-graph replay of ddppo_learner_step (default on; eager while profiling)."""
+    _call(ctx, "ddppo_set_graphs", int(enable))
+
+
 def ddppo_learner_register(ctx, ws):
     """Collective: expose this learner workspace to all ranks (a8 over NVLink peer memory)."""
     _call(ctx, "ddppo_learner_register", dptr(ws), ws.numel() * ws.element_size())

@@ -112,6 +112,7 @@ _SIGS = {
                                       c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ddppo_debug_depth_decisions": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "ddppo_learner_register": (c_int, [c_vp, c_vp, ctypes.c_size_t]),
+    "ddppo_set_graphs": (c_int, [c_vp, c_int]),
     "ddppo_debug_maxpool": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 KERNEL_FAMILIES = ("gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other")

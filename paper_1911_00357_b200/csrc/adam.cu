@@ -52,10 +52,21 @@ __device__ __forceinline__ void adam_one(float& p, float& m, float& v, float g, 
   p = p - step_size * (m / denom);
 }
 
+// step = (dstep ? *dstep : 0) + step_add (the learner runtime keeps the update count on the device, so
+// a captured CUDA graph needs no host-side scalar); bias corrections in fp64 once per block
 __global__ void __launch_bounds__(kThreads)
 adam_kernel(const float* __restrict__ g, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
             const uint8_t* __restrict__ freeze, int64_t P, const float* __restrict__ scalars, float b1, float b2,
-            float step_size, float inv_sqrt_bc2, float eps) {
+            float lr, const int* __restrict__ dstep, int step_add, float eps) {
+  __shared__ float sbc[2];
+  if (threadIdx.x == 0) {
+    const int step = (dstep ? *dstep : 0) + step_add;
+    const double bc1 = 1.0 - pow((double)b1, (double)step), bc2 = 1.0 - pow((double)b2, (double)step);
+    sbc[0] = (float)((double)lr / bc1);
+    sbc[1] = (float)(1.0 / sqrt(bc2));
+  }
+  __syncthreads();
+  const float step_size = sbc[0], inv_sqrt_bc2 = sbc[1];
   const float scale = scalars[0];
   const int64_t P4 = P / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -94,22 +105,22 @@ adam_kernel(const float* __restrict__ g, float* __restrict__ p, float* __restric
 }  // namespace
 
 ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, float* m, float* v,
-                              const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, P >= 1 && cfg.step >= 1, "adam: need P >= 1 and step >= 1");
+                              const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep,
+                              int step_add, cudaStream_t st) {
+  DDPPO_REQUIRE(ctx, P >= 1 && (dstep || step_add >= 1), "adam: need P >= 1 and step >= 1");
   const int blocks = grid_for((int)std::min<int64_t>((P + 3) / 4, 1 << 30), kThreads, ctx->sm_count * 4);
   ProfScope ps(ctx, DDPPO_K_ADAM, st, 1);
-  const double bc1 = 1.0 - pow((double)cfg.beta1, (double)cfg.step);
-  const double bc2 = 1.0 - pow((double)cfg.beta2, (double)cfg.step);
   adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
-                                           (float)((double)cfg.lr / bc1), (float)(1.0 / sqrt(bc2)), cfg.eps);
+                                           cfg.lr, dstep, step_add, cfg.eps);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
 
 ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float* m, float* v,
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
-                              float* grad_norm, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, P >= 1 && cfg.step >= 1, "adam: need P >= 1 and step >= 1");
+                              float* grad_norm, cudaStream_t st, const int* dstep, int step_add) {
+  if (!dstep) step_add = cfg.step;
+  DDPPO_REQUIRE(ctx, P >= 1 && (dstep || step_add >= 1), "adam: need P >= 1 and step >= 1");
   DDPPO_REQUIRE(ctx, (uintptr_t)grad % 16 == 0 && (uintptr_t)params % 16 == 0 && (uintptr_t)m % 16 == 0 &&
                          (uintptr_t)v % 16 == 0 && (freeze == nullptr || (uintptr_t)freeze % 4 == 0),
                 "adam: buffers must be 16-byte aligned");
@@ -118,12 +129,8 @@ ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float*
   grad_norm_kernel<<<blocks, kThreads, 0, st>>>(grad, P, inv_world, cfg.max_grad_norm, ctx->d_partials,
                                                 ctx->d_counters + CNT_NORM, ctx->d_scalars, grad_norm, ctx->d_err);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
-  const double bc1 = 1.0 - pow((double)cfg.beta1, (double)cfg.step);
-  const double bc2 = 1.0 - pow((double)cfg.beta2, (double)cfg.step);
-  const float step_size = (float)((double)cfg.lr / bc1);
-  const float inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
   adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
-                                           step_size, inv_sqrt_bc2, cfg.eps);
+                                           cfg.lr, dstep, step_add, cfg.eps);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }

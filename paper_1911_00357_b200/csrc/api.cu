@@ -7,6 +7,8 @@
 
 #include "common.cuh"
 
+void destroy_graph_cache(ddppo_ctx* ctx);
+
 extern "C" {
 
 int ddppo_abi_version(void) { return DDPPO_ABI_VERSION; }
@@ -85,6 +87,9 @@ ddppo_status ddppo_ctx_destroy(ddppo_ctx* ctx) {
     cudaEventDestroy(r.b);
   }
   for (auto e : ctx->pool) cudaEventDestroy(e);
+  destroy_graph_cache(ctx);
+  cudaFree(ctx->d_step);
+  cudaFree(ctx->d_peer_epoch);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto e : ctx->fork_events) cudaEventDestroy(e);
   for (auto s : ctx->side)
@@ -375,46 +380,37 @@ ddppo_status ddppo_learner_register(ddppo_ctx* ctx, void* ws, size_t ws_bytes) {
   return DDPPO_OK;
 }
 
-ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const ddppo_rollout* ro,
-                                const ddppo_learner_cfg* cfg, float* params, float* m, float* v, float* adv,
-                                float* ret, float* stats_out, void* ws, size_t ws_bytes, int32_t* host_step_out,
-                                void* stream) {
-  if (!ctx) return DDPPO_ERR_CONFIG;
-  ModelLayout L;
-  DDPPO_REQUIRE(ctx, build_layout(host_desc, &L) == DDPPO_OK, "bad model descriptor");
-  DDPPO_REQUIRE(ctx, ro && cfg && params && m && v && adv && ret && ws, "learner_step: null pointer");
-  DDPPO_REQUIRE(ctx, ro->host_len && ro->host_perms && ro->perms, "learner_step: lengths/perms required");
-  DDPPO_REQUIRE(ctx, cfg->minibatches >= 1 && ro->E % cfg->minibatches == 0 && cfg->epochs >= 1,
-                "learner_step: minibatches must divide E (S:L155)");
-  const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
-  DDPPO_REQUIRE(ctx, !visual || (ro->obs && ro->c0), "learner_step: the visual agents need obs and c0");
-  size_t need = 0;
-  ddppo_status s =
-      ddppo_learner_workspace_size(host_desc, ro->E, ro->T, ro->ld, cfg->minibatches, cfg->epochs, &need);
-  if (s != DDPPO_OK) return s;
-  DDPPO_REQUIRE(ctx, ws_bytes >= need, "learner_step: workspace too small");
-  LearnerWs w;
-  carve_learner(host_desc, ro->E, ro->T, cfg->minibatches, ws, &w);
-  cudaStream_t st = as_stream(stream);
-  const bool use_peers = ctx->world > 1 && ctx->peer_ws == ws;  // ddppo_learner_register'ed workspace
+}  // extern "C"
 
+namespace {
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+__global__ void add_int_kernel(int* p, int v) { *p += v; }
+
+struct MbShape {
+  int T_run, n_valid;
+};
+
+// a2..a8 for one rollout, every host-side value fixed by (config, pointers, mbs): replayable as a
+// CUDA graph.  Adam's update count is read on the device (*ctx->d_step + k + 1 for minibatch k).
+ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_model_desc* host_desc,
+                          const ddppo_rollout* ro, const ddppo_learner_cfg* cfg, float* params, float* m, float* v,
+                          float* adv, float* ret, float* stats_out, void* ws, LearnerWs& w, cudaStream_t st,
+                          const std::vector<MbShape>& mbs, bool use_peers, uint64_t peer_mb0) {
+  const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
   // a2 GAE (+ local adv stats), a3 global normalisation statistics
-  s = launch_gae(ctx, ro->rew, ro->val, ro->done, ro->len, ro->E, ro->T, ro->ld, cfg->gamma, cfg->tau, adv, ret,
-                 w.stats3, st);
+  ddppo_status s = launch_gae(ctx, ro->rew, ro->val, ro->done, ro->len, ro->E, ro->T, ro->ld, cfg->gamma, cfg->tau,
+                              adv, ret, w.stats3, st);
   if (s != DDPPO_OK) return s;
   if (cfg->normalize_adv) {
-    s = ddppo_adv_norm(ctx, w.stats3, cfg->adv_eps, w.mean_invstd, stream);
+    s = ddppo_adv_norm(ctx, w.stats3, cfg->adv_eps, w.mean_invstd, st);
     if (s != DDPPO_OK) return s;
   }
   const int B = ro->E / cfg->minibatches;
-  int L_max = 0;
-  for (int n = 0; n < ro->E; ++n) L_max = std::max(L_max, std::min(ro->host_len[n], ro->T));
-  DDPPO_REQUIRE(ctx, L_max >= 1, "learner_step: empty rollout");
   ddppo_loss_inputs li = {ro->action, ro->logp_old, ro->val, ret, adv};
-  ddppo_adam_cfg acfg = cfg->adam;
-  int32_t step = acfg.step;
+  const ddppo_adam_cfg acfg = cfg->adam;
+  int k = 0;
   for (int e = 0; e < cfg->epochs; ++e) {
-    for (int j = 0; j < cfg->minibatches; ++j) {
+    for (int j = 0; j < cfg->minibatches; ++j, ++k) {
       ddppo_batch b;
       b.goal = ro->goal;
       b.prev_action = ro->prev_action;
@@ -426,16 +422,8 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
       b.T = ro->T;
       b.ld = ro->ld;
       b.B = B;
-      // a4: every rank's envs step in lock-step, so the minibatch runs to its longest env
-      int T_run = 0, n_valid = 0;
-      for (int q = 0; q < B; ++q) {
-        const int n = ro->host_perms[(size_t)e * ro->E + (size_t)j * B + q];
-        const int Ln = std::min(ro->host_len[n], ro->T);
-        T_run = std::max(T_run, Ln);
-        n_valid += Ln;
-      }
-      b.T_run = T_run;
-      b.n_valid = n_valid;
+      b.T_run = mbs[k].T_run;  // a4: the minibatch runs to its longest env
+      b.n_valid = mbs[k].n_valid;
       b.obs = ro->obs;
       b.c0 = ro->c0;
       if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
@@ -443,36 +431,209 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
       else if (visual)
         s = depth_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
       else
-        s = gps_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
+        s = gps_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st, /*skip_head=*/true);
       if (s != DDPPO_OK) return s;
-      float* st_out = stats_out ? stats_out + (size_t)(e * cfg->minibatches + j) * 8 : w.grad_norm;
-      s = launch_loss(ctx, w.logits, w.values, b, li, cfg->normalize_adv ? w.mean_invstd : nullptr, cfg->loss,
-                      w.dlogits, w.dvalues, st_out, st);
+      float* st_out = stats_out ? stats_out + (size_t)k * 8 : w.grad_norm;
+      const float* mis = cfg->normalize_adv ? w.mean_invstd : nullptr;
+      if (host_desc->arch == DDPPO_ARCH_GPS_GRU) {  // head + loss + head input gradient in one kernel
+        const float *Wo, *bo, *Hs;
+        float* dH;
+        gps_head_io(L, params, b, w.model_ws, &Wo, &bo, &Hs, &dH);
+        s = launch_head_loss(ctx, Wo, bo, Hs, b, li, mis, cfg->loss, w.dlogits, w.dvalues, dH, st_out, st);
+      } else {
+        s = launch_loss(ctx, w.logits, w.values, b, li, mis, cfg->loss, w.dlogits, w.dvalues, st_out, st);
+      }
       if (s != DDPPO_OK) return s;
-      w.grad = use_peers ? w.grad2[ctx->peer_mb & 1] : w.grad2[0];
+      w.grad = use_peers ? w.grad2[(peer_mb0 + k) & 1] : w.grad2[0];
       if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
         s = toy_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
       else if (visual)
         s = depth_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
       else
-        s = gps_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st);
+        s = gps_bwd(ctx, L, params, b, w.dlogits, w.dvalues, w.grad, w.model_ws, st, /*dh_ready=*/true);
       if (s != DDPPO_OK) return s;
-      acfg.step = ++step;
       if (use_peers) {  // a8 over NVLink peer memory: rank-ordered sum + clip norm, then Adam
         ProfScope ps(ctx, DDPPO_K_ALLREDUCE, st, 0);
         float* peers[kMaxPeers];
         const size_t off = (size_t)((char*)w.grad - (char*)ws);
         for (int r = 0; r < ctx->world; ++r) peers[r] = reinterpret_cast<float*>(ctx->peer_ws_base[r] + off);
         s = launch_peer_reduce_norm(ctx, peers, w.gsum, L.P, acfg.max_grad_norm, nullptr, st);
-        if (s == DDPPO_OK) s = launch_adam_only(ctx, w.gsum, params, m, v, nullptr, L.P, acfg, st);
-        ++ctx->peer_mb;
+        if (s == DDPPO_OK) s = launch_adam_only(ctx, w.gsum, params, m, v, nullptr, L.P, acfg, ctx->d_step, k + 1, st);
       } else {
-        s = ddppo_grad_allreduce_step(ctx, w.grad, params, m, v, nullptr, L.P, &acfg, nullptr, stream);
+        if (ctx->world > 1) {
+          ProfScope ps(ctx, DDPPO_K_ALLREDUCE, st, 0);
+          DDPPO_NCCL_TRY(ctx, ncclAllReduce(w.grad, w.grad, (size_t)L.P, ncclFloat32, ncclSum, ctx->comm, st));
+        }
+        s = launch_clip_adam(ctx, w.grad, params, m, v, nullptr, L.P, acfg, 1.f / (float)ctx->world, nullptr, st,
+                             ctx->d_step, k + 1);
       }
       if (s != DDPPO_OK) return s;
     }
   }
-  if (host_step_out) *host_step_out = step;
+  add_int_kernel<<<1, 1, 0, st>>>(ctx->d_step, k);  // the device update count advances with the step
+  ctx->count(1);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
+template <typename T>
+void key_put(std::vector<unsigned char>& key, const T& v) {
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(&v);
+  key.insert(key.end(), p, p + sizeof(T));
+}
+}  // namespace
+
+struct ddppo_ctx::GraphCache {
+  std::vector<unsigned char> key;
+  std::vector<unsigned char> seen;  // last key run eagerly: captured when it repeats (lazy setup done)
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches[DDPPO_K_COUNT] = {};
+  cudaStream_t stream = nullptr;  // capture / replay stream (non-blocking; the caller's may be legacy)
+};
+
+void destroy_graph_cache(ddppo_ctx* ctx) {
+  if (!ctx->graph) return;
+  if (ctx->graph->exec) cudaGraphExecDestroy(ctx->graph->exec);
+  if (ctx->graph->stream) cudaStreamDestroy(ctx->graph->stream);
+  delete ctx->graph;
+  ctx->graph = nullptr;
+}
+
+extern "C" {
+
+ddppo_status ddppo_set_graphs(ddppo_ctx* ctx, int enable) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  ctx->graphs = enable != 0;
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const ddppo_rollout* ro,
+                                const ddppo_learner_cfg* cfg, float* params, float* m, float* v, float* adv,
+                                float* ret, float* stats_out, void* ws, size_t ws_bytes, int32_t* host_step_out,
+                                void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  ModelLayout L;
+  DDPPO_REQUIRE(ctx, build_layout(host_desc, &L) == DDPPO_OK, "bad model descriptor");
+  DDPPO_REQUIRE(ctx, ro && cfg && params && m && v && adv && ret && ws, "learner_step: null pointer");
+  DDPPO_REQUIRE(ctx, ro->host_len && ro->host_perms && ro->perms, "learner_step: lengths/perms required");
+  DDPPO_REQUIRE(ctx, cfg->minibatches >= 1 && ro->E % cfg->minibatches == 0 && cfg->epochs >= 1,
+                "learner_step: minibatches must divide E (S:L155)");
+  DDPPO_REQUIRE(ctx, cfg->adam.step >= 0, "learner_step: adam.step must be >= 0");
+  const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
+  DDPPO_REQUIRE(ctx, !visual || (ro->obs && ro->c0), "learner_step: the visual agents need obs and c0");
+  size_t need = 0;
+  ddppo_status s =
+      ddppo_learner_workspace_size(host_desc, ro->E, ro->T, ro->ld, cfg->minibatches, cfg->epochs, &need);
+  if (s != DDPPO_OK) return s;
+  DDPPO_REQUIRE(ctx, ws_bytes >= need, "learner_step: workspace too small");
+  LearnerWs w;
+  carve_learner(host_desc, ro->E, ro->T, cfg->minibatches, ws, &w);
+  cudaStream_t st = as_stream(stream);
+  const bool use_peers = ctx->world > 1 && ctx->peer_ws == ws;  // ddppo_learner_register'ed workspace
+  // a4 on the host: every minibatch's T_run / n_valid from the host copies of lengths and perms
+  const int B = ro->E / cfg->minibatches;
+  int L_max = 0;
+  for (int n = 0; n < ro->E; ++n) L_max = std::max(L_max, std::min(ro->host_len[n], ro->T));
+  DDPPO_REQUIRE(ctx, L_max >= 1, "learner_step: empty rollout");
+  std::vector<MbShape> mbs;
+  for (int e = 0; e < cfg->epochs; ++e)
+    for (int j = 0; j < cfg->minibatches; ++j) {
+      MbShape sh = {0, 0};
+      for (int q = 0; q < B; ++q) {
+        const int n = ro->host_perms[(size_t)e * ro->E + (size_t)j * B + q];
+        DDPPO_REQUIRE(ctx, n >= 0 && n < ro->E, "learner_step: perms must hold env ids");
+        const int Ln = std::min(ro->host_len[n], ro->T);
+        sh.T_run = std::max(sh.T_run, Ln);
+        sh.n_valid += Ln;
+      }
+      mbs.push_back(sh);
+    }
+  const int n_mb = (int)mbs.size();
+  // Adam's update count lives on the device; (re)seed it when the caller's count differs
+  if (!ctx->d_step) DDPPO_CUDA_TRY(ctx, cudaMalloc(&ctx->d_step, sizeof(int)));
+  if ((int64_t)cfg->adam.step != ctx->step_expected) {
+    set_int_kernel<<<1, 1, 0, st>>>(ctx->d_step, cfg->adam.step);
+    ctx->count(1);
+    DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  }
+  const uint64_t mb0 = ctx->peer_mb;
+  const bool graph = ctx->graphs && !ctx->prof;  // per-family profiling needs per-launch events
+  if (!graph) {
+    s = learner_body(ctx, L, host_desc, ro, cfg, params, m, v, adv, ret, stats_out, ws, w, st, mbs, use_peers, mb0);
+  } else {
+    // the whole step as one CUDA graph, captured once per (configuration, buffers, minibatch shapes)
+    std::vector<unsigned char> key;
+    key_put(key, *host_desc);
+    ddppo_rollout rk = *ro;
+    rk.host_len = nullptr;
+    rk.host_perms = nullptr;
+    key_put(key, rk);
+    ddppo_learner_cfg ck = *cfg;
+    ck.adam.step = 0;
+    key_put(key, ck);
+    for (const void* p : {(const void*)params, (const void*)m, (const void*)v, (const void*)adv, (const void*)ret,
+                          (const void*)stats_out, (const void*)ws})
+      key_put(key, p);
+    key_put(key, use_peers);
+    key_put(key, (int)(mb0 & 1));
+    for (const MbShape& sh : mbs) key_put(key, sh);
+    if (!ctx->graph) {
+      ctx->graph = new ddppo_ctx::GraphCache();
+      DDPPO_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->graph->stream, cudaStreamNonBlocking));
+    }
+    ddppo_ctx::GraphCache& gc = *ctx->graph;
+    cudaStream_t gs = gc.stream;
+    const bool hit = gc.exec != nullptr && gc.key == key;
+    if (!hit && gc.seen != key) {
+      // first time with this configuration: run eagerly (lazy allocations, attribute setup), capture
+      // when it repeats
+      gc.seen = key;
+      DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, gs));
+      s = learner_body(ctx, L, host_desc, ro, cfg, params, m, v, adv, ret, stats_out, ws, w, gs, mbs, use_peers,
+                       mb0);
+      if (s != DDPPO_OK) return s;
+      DDPPO_CUDA_TRY(ctx, fork_to(ctx, gs, st));
+      ctx->step_expected = (int64_t)cfg->adam.step + n_mb;
+      ctx->peer_mb = mb0 + (uint64_t)n_mb;
+      if (host_step_out) *host_step_out = cfg->adam.step + n_mb;
+      return DDPPO_OK;
+    }
+    if (!hit) {
+      if (gc.exec) {
+        cudaGraphExecDestroy(gc.exec);
+        gc.exec = nullptr;
+      }
+      int64_t before[DDPPO_K_COUNT];
+      memcpy(before, ctx->launches, sizeof(before));
+      DDPPO_CUDA_TRY(ctx, cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+      s = learner_body(ctx, L, host_desc, ro, cfg, params, m, v, adv, ret, stats_out, ws, w, gs, mbs, use_peers,
+                       mb0);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(gs, &g);
+      if (s != DDPPO_OK || ce != cudaSuccess || !g) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        memcpy(ctx->launches, before, sizeof(before));
+        if (s != DDPPO_OK) return s;
+        ctx->last_error = std::string("learner_step: graph capture failed: ") + cudaGetErrorString(ce);
+        return DDPPO_ERR_CUDA;
+      }
+      const cudaError_t ie = cudaGraphInstantiate(&gc.exec, g, 0);
+      cudaGraphDestroy(g);
+      DDPPO_CUDA_TRY(ctx, ie);
+      gc.key = key;
+      for (int i = 0; i < DDPPO_K_COUNT; ++i) gc.launches[i] = ctx->launches[i] - before[i];
+      memcpy(ctx->launches, before, sizeof(before));
+    }
+    DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, gs));
+    DDPPO_CUDA_TRY(ctx, cudaGraphLaunch(gc.exec, gs));
+    DDPPO_CUDA_TRY(ctx, fork_to(ctx, gs, st));
+    for (int i = 0; i < DDPPO_K_COUNT; ++i) ctx->launches[i] += gc.launches[i];
+  }
+  if (s != DDPPO_OK) return s;
+  ctx->step_expected = (int64_t)cfg->adam.step + n_mb;
+  ctx->peer_mb = mb0 + (uint64_t)n_mb;
+  if (host_step_out) *host_step_out = cfg->adam.step + n_mb;
   return DDPPO_OK;
 }
 

@@ -30,8 +30,14 @@ struct ddppo_ctx {
   std::vector<void*> ipc_opened;
   void* peer_ws = nullptr;
   char* peer_ws_base[kMaxPeers] = {};
-  unsigned int peer_epoch = 0;
+  unsigned int* d_peer_epoch = nullptr;  // barrier epoch, advanced on the device by the barrier kernel
   uint64_t peer_mb = 0;
+  // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step
+  int* d_step = nullptr;
+  int64_t step_expected = -1;       // value *d_step will hold once the enqueued work has run
+  bool graphs = true;               // ddppo_set_graphs
+  struct GraphCache;
+  GraphCache* graph = nullptr;
   // side streams for work beside the recurrences (fork / join with events), created lazily
   cudaStream_t side[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> fork_events;
@@ -225,9 +231,10 @@ ddppo_status launch_adv_finalize(ddppo_ctx* ctx, const double* stats3, float eps
 ddppo_status launch_loss(ddppo_ctx* ctx, const float* logits, const float* values, const ddppo_batch& b,
                          const ddppo_loss_inputs& in, const float* mean_invstd, const ddppo_loss_cfg& cfg,
                          float* dlogits, float* dvalues, float* stats, cudaStream_t st);
+// Adam's update count: host cfg.step (dstep == null) or device *dstep + step_add (learner runtime)
 ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float* m, float* v,
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
-                              float* grad_norm, cudaStream_t st);
+                              float* grad_norm, cudaStream_t st, const int* dstep = nullptr, int step_add = 0);
 
 // Implicit-GEMM operand: the im2col matrix of an NHWC tensor, gathered while it is staged (never
 // materialised).  Element (pixel q, column kk = (u*k + v)*SC + c) of the gathered matrix is
@@ -277,7 +284,8 @@ ddppo_status launch_peer_reduce_norm(ddppo_ctx* ctx, float* const* peers, float*
                                      float* grad_norm, cudaStream_t st);
 // Adam on an already summed gradient whose clip scale is in ctx->d_scalars[0] (adam.cu)
 ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, float* m, float* v,
-                              const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, cudaStream_t st);
+                              const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep,
+                              int step_add, cudaStream_t st);
 
 // tcgen05 GEMM: C[m][n] (+)= sum_k A(m,k) B(n,k) with generic strides or conv gathers (gemm_tc.cu)
 struct GemmTC {
@@ -349,8 +357,16 @@ ddppo_status launch_lstm_bwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st)
 
 size_t gps_workspace(int max_B, int T);
 ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
-                     float* logits, float* values, void* ws, cudaStream_t st);
+                     float* logits, float* values, void* ws, cudaStream_t st, bool skip_head = false);
 ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
-                     const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st);
+                     const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st,
+                     bool dh_ready = false);
+// the GPS workspace's head operands (W_o, b_o, H) and head input-gradient buffer
+ddppo_status gps_head_io(const ModelLayout& L, const float* params, const ddppo_batch& b, void* ws, const float** Wo,
+                         const float** bo, const float** Hs, float** dH);
+// fused head + PPO loss + head input gradient (loss.cu), the learner runtime's GPS path
+ddppo_status launch_head_loss(ddppo_ctx* ctx, const float* Wo, const float* bo, const float* Hs, const ddppo_batch& b,
+                              const ddppo_loss_inputs& in, const float* mean_invstd, const ddppo_loss_cfg& cfg,
+                              float* dlogits, float* dvalues, float* dH, float* stats, cudaStream_t st);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

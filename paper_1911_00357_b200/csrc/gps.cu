@@ -929,8 +929,18 @@ ddppo_status launch_cluster(ddppo_ctx* ctx, K kernel, int threads, size_t smem, 
 
 size_t gps_workspace(int max_B, int T) { return carve(nullptr, max_B, T, nullptr); }
 
+ddppo_status gps_head_io(const ModelLayout& L, const float* params, const ddppo_batch& b, void* ws, const float** Wo,
+                        const float** bo, const float** Hs, float** dH) {
+  GpsPtrs p = make_ptrs(L, params, b, ws);
+  *Wo = p.Wo;
+  *bo = p.bo;
+  *Hs = p.Hs;
+  *dH = p.dH;
+  return DDPPO_OK;
+}
+
 ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
-                     float* logits, float* values, void* ws, cudaStream_t st) {
+                     float* logits, float* values, void* ws, cudaStream_t st, bool skip_head) {
   DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");
   GpsPtrs p = make_ptrs(L, params, b, ws);
   const int S = b.B * b.T_run;
@@ -940,6 +950,7 @@ ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
         launch_cluster(ctx, gps_gru_fwd_kernel, kFwdThreads, sizeof(FwdSmem) + (size_t)S * sizeof(float), p, st);
     if (s != DDPPO_OK) return s;
   }
+  if (skip_head) return DDPPO_OK;  // the learner runtime fuses head + loss + head input gradient
   ProfScope ps(ctx, DDPPO_K_HEAD, st, 1);
   head_fwd_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, p.bo, p.Hs, S, logits, values);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -947,7 +958,8 @@ ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
 }
 
 ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
-                     const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st) {
+                     const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st,
+                     bool dh_ready) {
   DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");
   GpsPtrs p = make_ptrs(L, params, b, ws);
   const int S = b.B * b.T_run;
@@ -957,8 +969,9 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   ddppo_status s = ctx_side_streams(ctx, &sa, &sb);
   if (s != DDPPO_OK) return s;
   {
-    ProfScope ps(ctx, DDPPO_K_HEAD, st, 2);
-    head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, dlogits, dvalues, S, p.dH);
+    ProfScope ps(ctx, DDPPO_K_HEAD, st, dh_ready ? 1 : 2);
+    if (!dh_ready)
+      head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, dlogits, dvalues, S, p.dH);
     DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sa));
     head_wgrad_kernel<<<kH / 32, 256, 0, sa>>>(p.Hs, dlogits, dvalues, S, grad + layout_offset(L, "head.weight"),
                                               grad + layout_offset(L, "head.bias"));

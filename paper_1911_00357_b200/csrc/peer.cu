@@ -40,8 +40,14 @@ struct PeerArgs {
 };
 
 // one warp: lane j signals rank j ("my gradient is final") and then waits for rank j's signal
-__global__ void peer_barrier_kernel(const PeerArgs args, int world, int rank, unsigned int epoch, int* err) {
+__global__ void peer_barrier_kernel(const PeerArgs args, int world, int rank, unsigned int* d_epoch, int* err) {
   const int j = threadIdx.x;
+  unsigned int epoch = 0;
+  if (j == 0) {
+    epoch = *d_epoch + 1;  // every rank advances its own counter identically (one barrier per minibatch)
+    *d_epoch = epoch;
+  }
+  epoch = __shfl_sync(0xffffffffu, epoch, 0);
   if (j < world) {
     __threadfence_system();  // this rank's gradient (earlier kernels) before the signal
     st_release_sys(args.flags[j] + rank, epoch);
@@ -170,6 +176,9 @@ ddppo_status peer_setup_flags(ddppo_ctx* ctx) {
   DDPPO_CUDA_TRY(ctx, cudaMemset(f, 0, kMaxPeers * sizeof(unsigned int)));
   DDPPO_CUDA_TRY(ctx, cudaDeviceSynchronize());
   ctx->own_flags = f;
+  DDPPO_CUDA_TRY(ctx, cudaMalloc(&ctx->d_peer_epoch, sizeof(unsigned int)));
+  DDPPO_CUDA_TRY(ctx, cudaMemset(ctx->d_peer_epoch, 0, sizeof(unsigned int)));
+  DDPPO_CUDA_TRY(ctx, cudaDeviceSynchronize());
   void* out[kMaxPeers] = {};
   ddppo_status s = peer_exchange(ctx, f, out);
   if (s != DDPPO_OK) return s;
@@ -187,8 +196,7 @@ ddppo_status launch_peer_reduce_norm(ddppo_ctx* ctx, float* const* peers, float*
     a.flags[j] = ctx->peer_flags[j];
     DDPPO_REQUIRE(ctx, (uintptr_t)peers[j] % 16 == 0, "peer: gradient buffers must be 16-byte aligned");
   }
-  const unsigned int epoch = ++ctx->peer_epoch;
-  peer_barrier_kernel<<<1, 32, 0, st>>>(a, ctx->world, ctx->rank, epoch, ctx->d_err);
+  peer_barrier_kernel<<<1, 32, 0, st>>>(a, ctx->world, ctx->rank, ctx->d_peer_epoch, ctx->d_err);
   const int blocks = grid_for((int)std::min<int64_t>((P + 3) / 4, 1 << 30), kThreads, ctx->sm_count * 4);
   peer_reduce_norm_kernel<<<blocks, kThreads, 0, st>>>(a, ctx->world, P, 1.f / (float)ctx->world, max_norm, gsum,
                                                        ctx->d_partials, ctx->d_counters + CNT_NORM, ctx->d_scalars,

@@ -479,3 +479,31 @@ def test_learner_step_parity(dd, ctx, cfgname, lengths):
         if not e < lim:
             bad.append((name, round(e, 4)))
     assert not bad, bad
+
+
+# ------------------------------------------------------------------ CUDA-graph replay of the learner step
+@pytest.mark.parametrize("cfgname", ["gps", "toy"])
+def test_learner_graph_replay_matches_eager(dd, ctx, cfgname):
+    """Three learner steps: eager (graphs off) vs captured-and-replayed (the second step is captured,
+    the third replays) -- the parameters, Adam moments and loss statistics agree bit for bit."""
+    from paper_1911_00357_b200.learner import Learner
+    c = synth.CONFIGS[cfgname]
+    desc = dd.model_desc(c["arch"])
+    lay = dd.param_layout(desc)
+    P = dd.param_count(desc)
+    p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 31)
+    out = {}
+    for graphs in (False, True):
+        dd.ddppo_set_graphs(ctx, graphs)
+        lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+        for it in range(3):
+            ro = synth.rollout(c["E"], c["T"], 32, iteration=it, hidden=desc.hidden)
+            lrn.load_rollout(ro, synth.perms(32, it, c["epochs"], c["E"]))
+            lrn.step()
+        torch.cuda.synchronize()
+        ctx.check()
+        out[graphs] = (lrn.params.cpu().numpy(), lrn.m.cpu().numpy(), lrn.v.cpu().numpy(), lrn.stats.cpu().numpy(),
+                       lrn.adam_step)
+    dd.ddppo_set_graphs(ctx, True)
+    for a, b in zip(out[False], out[True]):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
