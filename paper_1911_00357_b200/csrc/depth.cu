@@ -973,7 +973,11 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
   const int K = g.K(), M = g.M();
   // wgrad: dWt[(u,v,c)][o] = sum_q x[tap(q; u, v)][c] dy[q][o]  (k runs over the M output pixels)
   {
-    const int splits = std::max(1, std::min(kMaxSplits, M / 2048));
+    // split the pixel range so that ~2 CTAs per SM stream (each >= 4 chunks of 64 pixels)
+    const int bn = g.Co <= 32 ? 32 : g.Co <= 64 ? 64 : 128;
+    const long long tiles = (long long)((g.Co + bn - 1) / bn) * ((K + 127) / 128);
+    const int splits = (int)std::max(1LL, std::min<long long>({(2LL * ctx->sm_count + tiles - 1) / tiles,
+                                                               (long long)M / 256, (long long)kMaxSplits}));
     IGemm gm;
     gm.a = op_pix(xb, g.Ho, g.Wo, g.H, g.W, g.Ci, g, 0, 0);
     gm.a.kind = IG_TAP_MN;
