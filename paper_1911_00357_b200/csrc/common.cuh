@@ -236,23 +236,13 @@ ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float*
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
                               float* grad_norm, cudaStream_t st, const int* dstep = nullptr, int step_add = 0);
 
-// Implicit-GEMM operand: the im2col matrix of an NHWC tensor, gathered while it is staged (never
-// materialised).  Element (pixel q, column kk = (u*k + v)*SC + c) of the gathered matrix is
-//   forward     : x[f][i*s - p + u][j*s - p + v][c]                          (0 outside)
-//   transposed  : x[f][(i + p - u)/s][(j + p - v)/s][c] if both divisions are exact, else 0
-// with q = (f*PH + i)*PW + j.  As GEMM operand A the rows are pixels and k runs over kk; as
-// operand B the rows are kk and k runs over pixels (the weight-gradient GEMM).
-struct ConvG {
-  const float* x;   // [F][SH][SW][SC]
-  int PH, PW;       // pixel grid of q
-  int SH, SW, SC;   // source tensor dims
-  int k, s, p;
-  int transposed;
-};
-
 // bf16-operand implicit-GEMM (igemm.cu): operands read straight into UMMA canonical tiles.
 enum { IG_DENSE_K = 0, IG_DENSE_MN = 1, IG_PIX_K = 2, IG_TAP_MN = 3 };
-struct IGather {                 // conv gather over an NHWC bf16 tensor (see ConvG for the index maps)
+// Conv gather over an NHWC bf16 tensor x[F][SH][SW][SC] (the implicit-GEMM view of im2col): element
+// (pixel q, column kk = (u*k + v)*SC + c) is, with q = (f*PH + i)*PW + j,
+//   forward     : x[f][i*s - p + u][j*s - p + v][c]                          (0 outside)
+//   transposed  : x[f][(i + p - u)/s][(j + p - v)/s][c] if both divisions are exact, else 0
+struct IGather {
   const __nv_bfloat16* x;        // set from IgOperand::x
   int PH, PW, SH, SW, SC, k, s, p, transposed;
   int pw_log2, php_log2, sc_log2;  // filled by the launcher
@@ -287,7 +277,7 @@ ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, 
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep,
                               int step_add, cudaStream_t st);
 
-// tcgen05 GEMM: C[m][n] (+)= sum_k A(m,k) B(n,k) with generic strides or conv gathers (gemm_tc.cu)
+// tcgen05 GEMM: C[m][n] (+)= sum_k A(m,k) B(n,k) over fp32 operands with generic strides (gemm_tc.cu)
 struct GemmTC {
   const float* A;
   int64_t sam, sak;
@@ -299,8 +289,6 @@ struct GemmTC {
   int splits = 1;            // split-K (> 1 needs `partial`, splits*M*N floats; summed in split order)
   float* partial = nullptr;
   int prec = 1;              // 1: bf16 operands; 3: bf16x3 (x = hi + lo, hi*hi + hi*lo + lo*hi), ~fp32 accuracy
-  const ConvG* ga = nullptr; // A(m, k) gathered (rows = pixels, k = im2col columns); A/sam/sak unused
-  const ConvG* gb = nullptr; // B(n, k) gathered (rows = im2col columns, k = pixels); B/sbn/sbk unused
   int accumulate = 0;        // C += result (else C = result)
 };
 ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st);

@@ -1,6 +1,6 @@
-// tcgen05 (5th-gen tensor core) GEMM for the dense contractions that are NOT on the recurrence's
-// dependency chain: the GRU weight gradients dW_hh = dG_h^T H_in, dW_ih = dG_x^T X and the input
-// gradient dX = dG_x W_ih (step a7).
+// tcgen05 (5th-gen tensor core) GEMM over fp32 operands for the dense contractions off the
+// recurrences' dependency chains: the GRU / LSTM weight gradients (dW_hh = dG_h^T H_in, ...),
+// input gradients (dX = dG W_ih), the LSTM input projections and the visual FC (steps a5 / a7).
 //
 //   C[m][n] = sum_k A(m, k) * B(n, k)      A(m,k) = A[m*sam + k*sak], B(n,k) = B[n*sbn + k*sbk]
 //
@@ -12,6 +12,9 @@
 // tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16) and tcgen05.commit signals an mbarrier
 // per smem stage (2 stages: the next K chunk is staged while the tensor core runs); the epilogue
 // reads TMEM with tcgen05.ld.32x32b.  The sum over k runs in one fixed order (deterministic).
+// Options: prec = 3 stages each operand as two bf16 tiles (x = hi + lo) and accumulates
+// lo*hi + hi*lo + hi*hi (~fp32 products, the visual agents' forward); splits > 1 splits k over
+// grid.z into partial tiles summed afterwards in split order.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -133,50 +136,13 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // Operand staging modes (host-selected): 0 = rows contiguous in HBM (X[r + k*sk]), raw fp32 tile
 // [64 k][ROWS]; 1 = k contiguous (X[r*sr + k]), raw tile [ROWS][68]; 2 = anything else (direct
-// loads, no raw tile).  Conv gathers (ConvG, implicit GEMM): 3 = rows are pixels, 4 consecutive
-// im2col columns are 4 consecutive channels (SC % 4 == 0) -> raw tile as mode 1; 4 = rows are
-// im2col columns, k runs over pixels (SC % 4 == 0) -> raw tile as mode 0; 5 / 6 = the same two
-// gathers with scalar loads (any SC; the 1-channel stem).  Modes 0/1/3/4 copy HBM -> smem with
-// 16-byte cp.async (zero-fill outside the tensor / the padding), then the CTA converts the raw
-// fp32 tile to the bf16 canonical tile.
+// loads, no raw tile).  Modes 0/1 copy HBM -> smem with 16-byte cp.async (no registers, many
+// copies in flight), then the CTA converts the raw fp32 tile to the bf16 canonical tile.
 constexpr int kRawPad = 68;
 
-// source address of gathered element (pixel (fSH/SH, i, j), tap (u, v), channel c), or null (= 0)
-__device__ __forceinline__ const float* conv_src(const ConvG& g, int fSH, int i, int j, int u, int v, int c) {
-  int y, xx;
-  if (!g.transposed) {
-    y = i * g.s - g.p + u;
-    xx = j * g.s - g.p + v;
-  } else {
-    const int ty = i + g.p - u, tx = j + g.p - v;
-    if (ty < 0 || tx < 0) return nullptr;
-    if (g.s == 1) {
-      y = ty;
-      xx = tx;
-    } else {
-      if (ty % g.s || tx % g.s) return nullptr;
-      y = ty / g.s;
-      xx = tx / g.s;
-    }
-  }
-  if (y < 0 || y >= g.SH || xx < 0 || xx >= g.SW) return nullptr;
-  return g.x + (((long long)(fSH + y) * g.SW + xx) * g.SC + c);
-}
-// pixel q -> (f*SH, i, j)
-__device__ __forceinline__ int3 pixel_of(const ConvG& g, int q) {
-  const int php = g.PH * g.PW, f = q / php, rem = q - f * php, i = rem / g.PW;
-  return make_int3(f * g.SH, i, rem - i * g.PW);
-}
-// im2col column kk -> (u, v, c)
-__device__ __forceinline__ int3 tap_of(const ConvG& g, int kk) {
-  const int uv = kk / g.SC, c = kk - uv * g.SC, u = uv / g.k;
-  return make_int3(u, uv - u * g.k, c);
-}
-
-// rt: per-row table of the CTA's gathered rows (pixels: {f*SH, i, j, valid}; columns: {u, v, c, valid})
 template <int ROWS>
 __device__ __forceinline__ void issue_raw(int mode, float* raw, const float* __restrict__ X, long long sr, long long sk,
-                                          int r0, int R, int k0, int K, const ConvG& g, const int4* rt, int kg0) {
+                                          int r0, int R, int k0, int K) {
   const int tid = threadIdx.x;
   if (mode == 0) {
     for (int i = tid; i < kBK * (ROWS / 4); i += kThreads) {
@@ -192,83 +158,24 @@ __device__ __forceinline__ void issue_raw(int mode, float* raw, const float* __r
       const float* src = ok ? X + (long long)r * sr + k : X;
       cp_async16(smem_addr(raw + row * kRawPad + 4 * j), src, ok ? 16u : 0u);
     }
-  } else if (mode == 3) {  // rows = pixels (table), k = im2col columns kg0 + k
-    for (int i = tid; i < ROWS * (kBK / 4); i += kThreads) {
-      const int row = i / (kBK / 4), j = i % (kBK / 4), k = k0 + 4 * j;
-      const int4 pr = rt[row];
-      const float* src = nullptr;
-      if (pr.w && k < K) {
-        const int3 t = tap_of(g, kg0 + k);
-        src = conv_src(g, pr.x, pr.y, pr.z, t.x, t.y, t.z);
-      }
-      cp_async16(smem_addr(raw + row * kRawPad + 4 * j), src ? src : g.x, src ? 16u : 0u);
-    }
-  } else if (mode == 4) {  // rows = im2col columns (table), k = pixels kg0 + k
-    for (int i = tid; i < kBK * (ROWS / 4); i += kThreads) {
-      const int kk = i / (ROWS / 4), j = i % (ROWS / 4), k = k0 + kk;
-      const int4 tr = rt[4 * j];
-      const float* src = nullptr;
-      if (tr.w && k < K) {
-        const int3 px = pixel_of(g, kg0 + k);
-        src = conv_src(g, px.x, px.y, px.z, tr.x, tr.y, tr.z);
-      }
-      cp_async16(smem_addr(raw + kk * ROWS + 4 * j), src ? src : g.x, src ? 16u : 0u);
-    }
+
   }
 }
 
-template <bool SPLIT>
-__device__ __forceinline__ void store1(unsigned char* dst, unsigned char* dlo, uint32_t off, float v) {
-  const __nv_bfloat16 h = __float2bfloat16_rn(v);
-  *reinterpret_cast<__nv_bfloat16*>(dst + off) = h;
-  if (SPLIT) *reinterpret_cast<__nv_bfloat16*>(dlo + off) = __float2bfloat16_rn(v - __bfloat162float(h));
-}
 
 template <int ROWS, bool SPLIT>
 __device__ __forceinline__ void convert_tile(int mode, unsigned char* dst, unsigned char* dlo, const float* raw,
                                              const float* __restrict__ X, long long sr, long long sk, int r0, int R,
-                                             int k0, int K, const ConvG& g, const int4* rt, int kg0) {
+                                             int k0, int K) {
   if (mode == 2) {
     stage_tile<ROWS, SPLIT>(dst, dlo, X, sr, sk, r0, R, k0, K);
-    return;
-  }
-  if (mode == 5) {  // rows = pixels, scalar gather over the im2col columns
-    for (int row = threadIdx.x; row < ROWS; row += kThreads) {
-      const int4 pr = rt[row];
-#pragma unroll 1
-      for (int kc = 0; kc < kBK / 8; ++kc) {
-        float v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int k = k0 + kc * 8 + e;
-          const float* src = nullptr;
-          if (pr.w && k < K) {
-            const int3 t = tap_of(g, kg0 + k);
-            src = conv_src(g, pr.x, pr.y, pr.z, t.x, t.y, t.z);
-          }
-          v[e] = src ? *src : 0.f;
-        }
-        store8<SPLIT>(dst, dlo, tile_off(row, kc), v);
-      }
-    }
-    return;
-  }
-  if (mode == 6) {  // rows = im2col columns, k = pixels: one pixel per thread, rows strided
-    const int kq = threadIdx.x % kBK, k = k0 + kq;
-    const bool kok = k < K;
-    const int3 px = kok ? pixel_of(g, kg0 + k) : make_int3(0, 0, 0);
-    for (int row = threadIdx.x / kBK; row < ROWS; row += kThreads / kBK) {
-      const int4 tr = rt[row];
-      const float* src = (kok && tr.w) ? conv_src(g, px.x, px.y, px.z, tr.x, tr.y, tr.z) : nullptr;
-      store1<SPLIT>(dst, dlo, tile_off(row, kq >> 3) + (kq & 7) * 2, src ? *src : 0.f);
-    }
     return;
   }
   for (int row = threadIdx.x; row < ROWS; row += kThreads) {
 #pragma unroll
     for (int kc = 0; kc < kBK / 8; ++kc) {
       float v[8];
-      if (mode == 0 || mode == 4) {
+      if (mode == 0) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[e] = raw[(kc * 8 + e) * ROWS + row];
       } else {
@@ -281,20 +188,6 @@ __device__ __forceinline__ void convert_tile(int mode, unsigned char* dst, unsig
   }
 }
 
-// per-row gather tables of the CTA's rows (modes 3/5: pixels; 4/6: im2col columns)
-template <int ROWS>
-__device__ __forceinline__ void fill_rows(int mode, const ConvG& g, int r0, int R, int4* rt) {
-  for (int row = threadIdx.x; row < ROWS; row += kThreads) {
-    const int r = r0 + row;
-    if (mode == 3 || mode == 5) {
-      const int3 px = pixel_of(g, r < R ? r : 0);
-      rt[row] = make_int4(px.x, px.y, px.z, r < R);
-    } else if (mode == 4 || mode == 6) {
-      const int3 t = tap_of(g, r < R ? r : 0);
-      rt[row] = make_int4(t.x, t.y, t.z, r < R);
-    }
-  }
-}
 
 template <int ROWS>
 __host__ __device__ constexpr uint32_t raw_bytes() {
@@ -305,7 +198,7 @@ template <int BN, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, const float* __restrict__ B,
                     long long sbn, long long sbk, float* __restrict__ C, long long ldc, int M, int N, int K, int kper,
-                    long long cz_stride, int amode, int bmode, const ConvG ga, const ConvG gb, int accumulate) {
+                    long long cz_stride, int amode, int bmode, int accumulate) {
   constexpr int kTmemCols = BN < 32 ? 32 : BN;
   constexpr uint32_t kABytes = kBM * kBK * 2, kBBytes = BN * kBK * 2;
   constexpr uint32_t kRawA = raw_bytes<kBM>(), kRawB = raw_bytes<BN>();
@@ -318,12 +211,10 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
   float* rB[2] = {reinterpret_cast<float*>(rbase + 2 * kRawA), reinterpret_cast<float*>(rbase + 2 * kRawA + kRawB)};
   __shared__ uint64_t mma_bar[2];
   __shared__ uint32_t tmem_base_slot;
-  __shared__ int4 rtA[kBM], rtB[BN];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
   // split-K: CTA z of grid.z covers k in [z*kper, z*kper + kper) and writes its own partial C
-  const int kg0 = blockIdx.z * kper;  // global k of this split's first column (gather modes)
   {
     const long long kbeg = (long long)blockIdx.z * kper;
     A += kbeg * sak;
@@ -332,17 +223,14 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
     C += (long long)blockIdx.z * cz_stride;
   }
   const int n_chunks = (K + kBK - 1) / kBK;
-  if (amode >= 3) fill_rows<kBM>(amode, ga, m0, M, rtA);
-  if (bmode >= 3) fill_rows<BN>(bmode, gb, n0, N, rtB);
-  if (amode >= 3 || bmode >= 3) __syncthreads();
 
   // start streaming the first two K chunks while TMEM / barriers are set up
-  issue_raw<kBM>(amode, rA[0], A, sam, sak, m0, M, 0, K, ga, rtA, kg0);
-  issue_raw<BN>(bmode, rB[0], B, sbn, sbk, n0, N, 0, K, gb, rtB, kg0);
+  issue_raw<kBM>(amode, rA[0], A, sam, sak, m0, M, 0, K);
+  issue_raw<BN>(bmode, rB[0], B, sbn, sbk, n0, N, 0, K);
   cp_async_commit();
   if (n_chunks > 1) {
-    issue_raw<kBM>(amode, rA[1], A, sam, sak, m0, M, kBK, K, ga, rtA, kg0);
-    issue_raw<BN>(bmode, rB[1], B, sbn, sbk, n0, N, kBK, K, gb, rtB, kg0);
+    issue_raw<kBM>(amode, rA[1], A, sam, sak, m0, M, kBK, K);
+    issue_raw<BN>(bmode, rB[1], B, sbn, sbk, n0, N, kBK, K);
   }
   cp_async_commit();
 
@@ -373,15 +261,15 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
       mbar_wait(&mma_bar[st], phase[st]);
       phase[st] ^= 1u;
     }
-    convert_tile<kBM, SPLIT>(amode, sA[st], sA[st] + kABytes, rA[st], A, sam, sak, m0, M, k0, K, ga, rtA, kg0);
-    convert_tile<BN, SPLIT>(bmode, sB[st], sB[st] + kBBytes, rB[st], B, sbn, sbk, n0, N, k0, K, gb, rtB, kg0);
+    convert_tile<kBM, SPLIT>(amode, sA[st], sA[st] + kABytes, rA[st], A, sam, sak, m0, M, k0, K);
+    convert_tile<BN, SPLIT>(bmode, sB[st], sB[st] + kBBytes, rB[st], B, sbn, sbk, n0, N, k0, K);
     // generic-proxy smem writes -> visible to the tensor core (async proxy)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     // the raw stage is free again: stream chunk ch+2 into it
     if (ch + 2 < n_chunks) {
-      issue_raw<kBM>(amode, rA[st], A, sam, sak, m0, M, k0 + 2 * kBK, K, ga, rtA, kg0);
-      issue_raw<BN>(bmode, rB[st], B, sbn, sbk, n0, N, k0 + 2 * kBK, K, gb, rtB, kg0);
+      issue_raw<kBM>(amode, rA[st], A, sam, sak, m0, M, k0 + 2 * kBK, K);
+      issue_raw<BN>(bmode, rB[st], B, sbn, sbk, n0, N, k0 + 2 * kBK, K);
     }
     cp_async_commit();
     if (tid == 0) {
@@ -472,12 +360,7 @@ ddppo_status launch_bn(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st) {
     if (al && sk == 1 && sr % 4 == 0 && K % 4 == 0) return 1;
     return 2;
   };
-  const int am = g.ga ? (g.ga->SC % 4 == 0 && ((uintptr_t)g.ga->x & 15) == 0 ? 3 : 5)
-                     : mode_of(g.A, g.sam, g.sak, g.M, g.K);
-  const int bm = g.gb ? (g.gb->SC % 4 == 0 && ((uintptr_t)g.gb->x & 15) == 0 ? 4 : 6)
-                     : mode_of(g.B, g.sbn, g.sbk, g.N, g.K);
-  const ConvG none = {};
-  const ConvG ga = g.ga ? *g.ga : none, gb = g.gb ? *g.gb : none;
+  const int am = mode_of(g.A, g.sam, g.sak, g.M, g.K), bm = mode_of(g.B, g.sbn, g.sbk, g.N, g.K);
   const size_t parts = SPLIT ? 2 : 1;
   const size_t smem = 2 * parts * ((size_t)kBM * kBK * 2 + (size_t)BN * kBK * 2) + 2 * (size_t)raw_bytes<kBM>() +
                       2 * (size_t)raw_bytes<BN>();
@@ -495,11 +378,11 @@ ddppo_status launch_bn(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st) {
   ctx->count(nz == 1 ? 1 : 2);
   if (nz == 1) {
     kern<<<grid, kThreads, smem, st>>>(g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.C, g.ldc, g.M, g.N, g.K, kper, 0, am, bm,
-                                       ga, gb, g.accumulate);
+                                       g.accumulate);
   } else {
     const long long zs = (long long)g.M * g.N;
     kern<<<grid, kThreads, smem, st>>>(g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.partial, g.N, g.M, g.N, g.K, kper, zs, am,
-                                       bm, ga, gb, 0);
+                                       bm, 0);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     splitk_reduce_kernel<<<grid_for((int)std::min<long long>(zs, 1 << 30), 256, ctx->sm_count * 8), 256, 0, st>>>(
         g.partial, nz, zs, g.M, g.N, g.C, g.ldc, g.accumulate);
