@@ -316,22 +316,35 @@ def main():
     if not args.no_e2e:
         pinned = []
         for i in range(n_roll):
-            hb = lrn.pinned_host_buffers()
+            hb = lrn.pinned_host_buffers()  # one packed pinned arena per rollout (single H2D copy)
             for k in hb:
-                hb[k].copy_(torch.from_numpy(np.ascontiguousarray(rollouts[i][k])).reshape(hb[k].shape))
+                if k not in ("__arena__", "perms"):
+                    hb[k].copy_(torch.from_numpy(np.ascontiguousarray(rollouts[i][k])).reshape(hb[k].shape))
             pinned.append(hb)
-        h2d = sum(v.numel() * v.element_size() for v in pinned[0].values()) + perms[0].nbytes
+        h2d = pinned[0]["__arena__"].numel()
         d2h = lrn.stats.numel() * 4
+        # a training loop's shape: step i+1 is enqueued before step i's statistics are read back (two
+        # statistics buffers, D2H on a copy stream after step i's completion event)
+        stats_dev = [torch.zeros_like(lrn.stats) for _ in range(2)]
+        stats_host = [torch.zeros(lrn.stats.shape, dtype=lrn.stats.dtype).pin_memory() for _ in range(2)]
+        copy_stream = torch.cuda.Stream()
+        done = [torch.cuda.Event() for _ in range(2)]
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_exp = 0
         e0.record(stream)
         for i in range(args.steps):
             lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True)
-            lrn.step(stream)
-            _ = lrn.stats.cpu()  # D2H of the step's loss statistics
+            lrn.step(stream, stats=stats_dev[i % 2])
+            copy_stream.wait_stream(stream)
+            with torch.cuda.stream(copy_stream):
+                stats_host[i % 2].copy_(stats_dev[i % 2], non_blocking=True)  # D2H of the step's loss statistics
+                done[i % 2].record(copy_stream)
+            if i > 0:
+                done[(i - 1) % 2].synchronize()  # step i-1's result is on the host
             counts = dd.ddppo_allreduce_counts(ctx, [lrn.steps_per_rollout()])
             e_exp += int(counts[0])
+        done[(args.steps - 1) % 2].synchronize()
         e1.record(stream)
         barrier()
         e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")

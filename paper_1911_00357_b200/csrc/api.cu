@@ -484,16 +484,23 @@ void key_put(std::vector<unsigned char>& key, const T& v) {
 }  // namespace
 
 struct ddppo_ctx::GraphCache {
-  std::vector<unsigned char> key;
+  struct Entry {
+    std::vector<unsigned char> key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches[DDPPO_K_COUNT] = {};
+    uint64_t used = 0;
+  };
+  static constexpr size_t kMaxEntries = 4;  // e.g. double-buffered outputs: a few live keys
+  std::vector<Entry> entries;
   std::vector<unsigned char> seen;  // last key run eagerly: captured when it repeats (lazy setup done)
-  cudaGraphExec_t exec = nullptr;
-  int64_t launches[DDPPO_K_COUNT] = {};
-  cudaStream_t stream = nullptr;  // capture / replay stream (non-blocking; the caller's may be legacy)
+  uint64_t clock = 0;
+  cudaStream_t stream = nullptr;    // capture / replay stream (non-blocking; the caller's may be legacy)
 };
 
 void destroy_graph_cache(ddppo_ctx* ctx) {
   if (!ctx->graph) return;
-  if (ctx->graph->exec) cudaGraphExecDestroy(ctx->graph->exec);
+  for (auto& e : ctx->graph->entries)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
   if (ctx->graph->stream) cudaStreamDestroy(ctx->graph->stream);
   delete ctx->graph;
   ctx->graph = nullptr;
@@ -583,7 +590,9 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
     }
     ddppo_ctx::GraphCache& gc = *ctx->graph;
     cudaStream_t gs = gc.stream;
-    const bool hit = gc.exec != nullptr && gc.key == key;
+    ddppo_ctx::GraphCache::Entry* hit = nullptr;
+    for (auto& e : gc.entries)
+      if (e.key == key) hit = &e;
     if (!hit && gc.seen != key) {
       // first time with this configuration: run eagerly (lazy allocations, attribute setup), capture
       // when it repeats
@@ -599,9 +608,12 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
       return DDPPO_OK;
     }
     if (!hit) {
-      if (gc.exec) {
-        cudaGraphExecDestroy(gc.exec);
-        gc.exec = nullptr;
+      if (gc.entries.size() >= ddppo_ctx::GraphCache::kMaxEntries) {  // evict the least recently used
+        size_t lru = 0;
+        for (size_t i = 1; i < gc.entries.size(); ++i)
+          if (gc.entries[i].used < gc.entries[lru].used) lru = i;
+        cudaGraphExecDestroy(gc.entries[lru].exec);
+        gc.entries.erase(gc.entries.begin() + (long)lru);
       }
       int64_t before[DDPPO_K_COUNT];
       memcpy(before, ctx->launches, sizeof(before));
@@ -618,17 +630,21 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
         ctx->last_error = std::string("learner_step: graph capture failed: ") + cudaGetErrorString(ce);
         return DDPPO_ERR_CUDA;
       }
-      const cudaError_t ie = cudaGraphInstantiate(&gc.exec, g, 0);
+      ddppo_ctx::GraphCache::Entry e;
+      const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
       cudaGraphDestroy(g);
       DDPPO_CUDA_TRY(ctx, ie);
-      gc.key = key;
-      for (int i = 0; i < DDPPO_K_COUNT; ++i) gc.launches[i] = ctx->launches[i] - before[i];
+      e.key = key;
+      for (int i = 0; i < DDPPO_K_COUNT; ++i) e.launches[i] = ctx->launches[i] - before[i];
       memcpy(ctx->launches, before, sizeof(before));
+      gc.entries.push_back(std::move(e));
+      hit = &gc.entries.back();
     }
+    hit->used = ++gc.clock;
     DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, gs));
-    DDPPO_CUDA_TRY(ctx, cudaGraphLaunch(gc.exec, gs));
+    DDPPO_CUDA_TRY(ctx, cudaGraphLaunch(hit->exec, gs));
     DDPPO_CUDA_TRY(ctx, fork_to(ctx, gs, st));
-    for (int i = 0; i < DDPPO_K_COUNT; ++i) ctx->launches[i] += gc.launches[i];
+    for (int i = 0; i < DDPPO_K_COUNT; ++i) ctx->launches[i] += hit->launches[i];
   }
   if (s != DDPPO_OK) return s;
   ctx->step_expected = (int64_t)cfg->adam.step + n_mb;

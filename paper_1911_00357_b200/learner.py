@@ -54,8 +54,19 @@ class Learner:
                   "logp_old": (E, ld)}
         if self.desc.arch in (2, 3):  # visual agents: + frames and the LSTM cell state
             shapes.update(obs=(E, T) + OBS_SHAPES[self.desc.arch], c0=(E, hs))
-        self.dev = {k: torch.zeros(s, dtype=ROLLOUT_FIELDS[k], device=dev) for k, s in shapes.items()}
-        self.perms = torch.zeros((epochs, E), dtype=torch.int32, device=dev)
+        # all rollout arrays + the epoch permutations in one device arena (256-byte aligned fields), so a
+        # packed host arena reaches HBM in a single copy
+        shapes["perms"] = (epochs, E)
+        self._layout, off = {}, 0
+        for k, shp in shapes.items():
+            dt = ROLLOUT_FIELDS.get(k, torch.int32)
+            nbytes = int(np.prod(shp)) * torch.empty((), dtype=dt).element_size()
+            self._layout[k] = (off, shp, dt, nbytes)
+            off = (off + nbytes + 255) // 256 * 256
+        self._arena_bytes = off
+        self.arena = torch.zeros(off, dtype=torch.uint8, device=dev)
+        self.dev = {k: self._view(self.arena, k) for k in shapes if k != "perms"}
+        self.perms = self._view(self.arena, "perms")
         self.adv = torch.zeros((E, ld), **f32)
         self.ret = torch.zeros((E, ld), **f32)
         self.stats = torch.zeros((epochs * minibatches, 8), **f32)
@@ -64,12 +75,26 @@ class Learner:
         self.shapes = shapes
 
     # --------------------------------------------------------------- inputs
+    def _view(self, arena, k):
+        off, shp, dt, nbytes = self._layout[k]
+        return arena[off:off + nbytes].view(dt).view(shp)
+
     def pinned_host_buffers(self):
-        """Page-locked host mirrors of the rollout arrays (for end-to-end timing)."""
-        return {k: torch.zeros(s, dtype=ROLLOUT_FIELDS[k]).pin_memory() for k, s in self.shapes.items()}
+        """Page-locked host mirror of the rollout arena (views per field, incl. "perms"); loading it is
+        one H2D copy."""
+        arena = torch.zeros(self._arena_bytes, dtype=torch.uint8).pin_memory()
+        views = {k: self._view(arena, k) for k in self._layout}
+        views["__arena__"] = arena
+        return views
 
     def load_rollout(self, ro, perms, non_blocking=False):
-        """Copy a rollout (synth dict of numpy arrays or pinned torch tensors) + perms to HBM."""
+        """Copy a rollout (synth dict of numpy arrays, or a pinned_host_buffers() arena) + perms to HBM."""
+        if "__arena__" in ro:  # packed pinned arena: perms are inside it
+            ro["perms"].copy_(torch.as_tensor(np.asarray(perms, dtype=np.int32)))
+            self.arena.copy_(ro["__arena__"], non_blocking=non_blocking)
+            self.host_perms[:] = ro["perms"].numpy()
+            self.host_len[:] = ro["length"].numpy()
+            return
         for k in self.dev:
             src = ro[k]
             if isinstance(src, np.ndarray):
@@ -97,12 +122,15 @@ class Learner:
             r.obs, r.c0 = d["obs"].data_ptr(), d["c0"].data_ptr()
         return r
 
-    def step(self, stream=None):
+    def step(self, stream=None, stats=None):
+        """One learner step (stream-ordered).  `stats` (optional [epochs*minibatches][8] CUDA tensor)
+        receives the loss statistics instead of self.stats (double-buffering for pipelined reads)."""
         self.cfg.adam.step = self.adam_step
         self._ro = self._rollout_struct()
+        out = self.stats if stats is None else stats
         self.adam_step = ddppo_learner_step(self.ctx, self.desc, self._ro, self.cfg, self.params, self.m, self.v,
-                                            self.adv, self.ret, self.stats, self.ws, stream)
-        return self.stats
+                                            self.adv, self.ret, out, self.ws, stream)
+        return out
 
     def steps_per_rollout(self):
         return int(np.minimum(self.host_len, self.T).sum())
