@@ -124,6 +124,109 @@ gae_kernel(const float* __restrict__ rew, const float* __restrict__ val, const u
   last_block_reduce<3>(acc, partials, counter, stats3, red);
 }
 
+// Single-chunk fast path (T <= 128, 16-byte rows): each warp loads TWO env rows (its own and the
+// row one grid-stride further) before scanning either, so twice the bytes are in flight per warp.
+struct GaeRow {
+  float r[4], v[5];
+  uint32_t dd;
+  int L;
+};
+__device__ __forceinline__ void gae_load(const float* __restrict__ rew, const float* __restrict__ val,
+                                         const uint8_t* __restrict__ done, const int32_t* __restrict__ len, int n,
+                                         int E, int T, int ld, int lane, GaeRow& g) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) g.r[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) g.v[k] = 0.f;
+  g.dd = 0;
+  g.L = 0;
+  if (n >= E) return;
+  g.L = min(max(len[n], 0), T);
+  const size_t row = (size_t)n * ld;
+  const int t0 = lane * 4;
+  if (t0 < T && t0 <= g.L) {
+    const float4 r4 = *reinterpret_cast<const float4*>(rew + row + t0);
+    const float4 v4 = *reinterpret_cast<const float4*>(val + row + t0);
+    g.dd = *reinterpret_cast<const uint32_t*>(done + row + t0);
+    g.r[0] = r4.x; g.r[1] = r4.y; g.r[2] = r4.z; g.r[3] = r4.w;
+    g.v[0] = v4.x; g.v[1] = v4.y; g.v[2] = v4.z; g.v[3] = v4.w;
+  }
+  if ((lane == 31 || t0 + 4 >= T) && t0 + 4 <= g.L && t0 < T) g.v[4] = val[row + t0 + 4];  // bootstrap slot
+}
+__device__ __forceinline__ void gae_scan_store(const GaeRow& g, int n, int E, int T, int ld, int lane, float gamma,
+                                               float gt, float* __restrict__ adv, float* __restrict__ ret, double& s,
+                                               double& q, double& cnt) {
+  const int t0 = lane * 4, L = g.L;
+  const size_t row = (size_t)n * ld;
+  float vn = __shfl_down_sync(0xffffffffu, g.v[0], 1);
+  if (lane == 31 || t0 + 4 >= T) vn = g.v[4];
+  float dl[4], c[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool valid = t0 + k < L;
+    const float nd = 1.f - (float)((g.dd >> (8 * k)) & 0xffu);
+    const float vnext = (k < 3) ? g.v[k + 1] : vn;
+    dl[k] = valid ? (g.r[k] + gamma * vnext * nd - g.v[k]) : 0.f;
+    c[k] = valid ? gt * nd : 0.f;
+  }
+  float D = dl[3], C = c[3];
+#pragma unroll
+  for (int k = 2; k >= 0; --k) {
+    D = dl[k] + c[k] * D;
+    C = c[k] * C;
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float D2 = __shfl_down_sync(0xffffffffu, D, off);
+    const float C2 = __shfl_down_sync(0xffffffffu, C, off);
+    if (lane + off < 32) {
+      D = D + C * D2;
+      C = C * C2;
+    }
+  }
+  float a_next = __shfl_down_sync(0xffffffffu, D, 1);  // A_{t0+4} (carry 0 after the last chunk)
+  if (lane == 31) a_next = 0.f;
+  float A[4], R[4];
+  A[3] = dl[3] + c[3] * a_next;
+#pragma unroll
+  for (int k = 2; k >= 0; --k) A[k] = dl[k] + c[k] * A[k + 1];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool valid = t0 + k < L;
+    R[k] = valid ? A[k] + g.v[k] : 0.f;
+    if (valid) {
+      s += (double)A[k];
+      q += (double)A[k] * (double)A[k];
+      cnt += 1.0;
+    }
+  }
+  if (n < E && t0 < T) {
+    *reinterpret_cast<float4*>(adv + row + t0) = make_float4(A[0], A[1], A[2], A[3]);
+    *reinterpret_cast<float4*>(ret + row + t0) = make_float4(R[0], R[1], R[2], R[3]);
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+gae1_kernel(const float* __restrict__ rew, const float* __restrict__ val, const uint8_t* __restrict__ done,
+            const int32_t* __restrict__ len, int E, int T, int ld, float gamma, float tau, float* __restrict__ adv,
+            float* __restrict__ ret, double* partials, unsigned int* counter, double* stats3) {
+  __shared__ double red[3 * kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float gt = gamma * tau;
+  double s = 0.0, q = 0.0, cnt = 0.0;
+  const int stride = gridDim.x * kWarps;
+  for (int n = blockIdx.x * kWarps + warp; n < E; n += 2 * stride) {
+    GaeRow g0, g1;
+    gae_load(rew, val, done, len, n, E, T, ld, lane, g0);
+    gae_load(rew, val, done, len, n + stride, E, T, ld, lane, g1);
+    gae_scan_store(g0, n, E, T, ld, lane, gamma, gt, adv, ret, s, q, cnt);
+    if (n + stride < E) gae_scan_store(g1, n + stride, E, T, ld, lane, gamma, gt, adv, ret, s, q, cnt);
+  }
+  if (stats3 == nullptr) return;
+  double acc[3] = {s, q, cnt};
+  last_block_reduce<3>(acc, partials, counter, stats3, red);
+}
+
 __global__ void adv_finalize_kernel(const double* stats3, float eps, float* mean_invstd) {
   if (threadIdx.x != 0) return;
   const double S = stats3[0], Q = stats3[1], n = stats3[2];
@@ -148,7 +251,10 @@ ddppo_status launch_gae(ddppo_ctx* ctx, const float* rew, const float* val, cons
                    ((uintptr_t)adv % 16 == 0) && ((uintptr_t)ret % 16 == 0) && ((uintptr_t)done % 4 == 0);
   const int blocks = grid_for(E, kWarps, ctx->sm_count * 8);
   ProfScope ps(ctx, DDPPO_K_GAE, st, 1);
-  if (vec)
+  if (vec && T <= 128)
+    gae1_kernel<<<blocks, kWarps * 32, 0, st>>>(rew, val, done, len, E, T, ld, gamma, tau, adv, ret, ctx->d_partials,
+                                                ctx->d_counters + CNT_GAE, stats3);
+  else if (vec)
     gae_kernel<true><<<blocks, kWarps * 32, 0, st>>>(rew, val, done, len, E, T, ld, gamma, tau, adv, ret,
                                                      ctx->d_partials, ctx->d_counters + CNT_GAE, stats3);
   else
