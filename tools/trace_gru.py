@@ -1,6 +1,7 @@
 """Phase timing of the GRU forward recurrence (debug build tools/libddppo_trace.so, CTA 0 thread 0).
 Slots: 0 h received, 3 MMAs issued+committed, 4 accumulator ready, 5 TMEM read, 1 after CTA barrier, 2 h sent."""
-import ctypes, os
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1911_00357_b200._lib as L
 lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libddppo_trace.so"))
