@@ -17,6 +17,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <vector>
 
 #include "common.cuh"
@@ -252,6 +253,10 @@ __global__ void __launch_bounds__(kThreads) frame_sum_kernel(const float* __rest
 // contiguously (coalesced); with 256 % C == 0 thread t always sees channel t % C, so per-group and
 // per-channel partial sums are per-thread sums combined in a fixed order through shared memory.
 constexpr int kGnMaxThreads = 1024;  // blockDim = max(256, C): a multiple of C
+__host__ __device__ inline int gn_threads(int C) { return C > 256 ? C : 256; }
+constexpr int kGnChunk = 8192;  // elements per chunk (a multiple of every C): kGnChunk / blockDim per thread
+__host__ __device__ inline int gn_chunk(int) { return kGnChunk; }
+__host__ __device__ constexpr int gn_bound(int nv) { return kGnChunk / nv < 1024 ? kGnChunk / nv : 1024; }
 
 // per-group sums of the threads' (a, b) in fixed order -> out[g] (threads t < 16 write)
 __device__ __forceinline__ void gn_group_reduce(double a, double b, int C, double* sa, double* sb, double* out_a,
@@ -275,21 +280,32 @@ __device__ __forceinline__ void gn_group_reduce(double a, double b, int C, doubl
 }
 
 // z = (relu)(gamma * (y - mu) * rstd + beta (+ residual)); stats[f][g] = (mu, rstd) (biased variance);
-// zb (nullable): z as bf16 hi / lo planes (plane = F*HW*C)
-__global__ void __launch_bounds__(kGnMaxThreads) gn_fwd_kernel(const float* __restrict__ y, const float* __restrict__ gamma,
+// zb (nullable): z as bf16 hi / lo planes (plane = F*HW*C).  Thread t holds elements t + i*blockDim
+// (i < NV, NV*blockDim >= HW*C) in registers: every load of the slab is in flight at once and the
+// slab is read from memory once.
+template <int NV>
+__global__ void __launch_bounds__(gn_bound(NV)) gn_fwd_kernel(const float* __restrict__ y, const float* __restrict__ gamma,
                                                             const float* __restrict__ beta,
                                                             const float* __restrict__ residual, int HW, int C,
                                                             int relu, size_t plane, float* __restrict__ stats,
                                                             float* __restrict__ z, __nv_bfloat16* __restrict__ zb) {
-  __shared__ double sa[kGnMaxThreads], sb[kGnMaxThreads], ga[kGroups], gb[kGroups];
+  __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
   __shared__ float smu[kGroups], srs[kGroups];
   const int f = blockIdx.x, n = HW * C, c = threadIdx.x % C, cg = C / kGroups;
   const size_t base = (size_t)f * n;
+  float v[NV], rv[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    v[i] = e < n ? y[base + e] : 0.f;
+    rv[i] = (residual && e < n) ? residual[base + e] : 0.f;
+  }
+  asm volatile("" ::: "memory");  // every load above is issued before any result is consumed
   double s1 = 0.0, s2 = 0.0;
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const float v = y[base + e];
-    s1 += v;
-    s2 += (double)v * v;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    s1 += v[i];
+    s2 += (double)v[i] * v[i];
   }
   gn_group_reduce(s1, s2, C, sa, sb, ga, gb);
   if (threadIdx.x < kGroups) {
@@ -303,41 +319,76 @@ __global__ void __launch_bounds__(kGnMaxThreads) gn_fwd_kernel(const float* __re
   }
   __syncthreads();
   const float mu = smu[c / cg], rs = srs[c / cg], gm = gamma[c], bt = beta[c];
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const size_t i = base + e;
-    float v = (y[i] - mu) * rs * gm + bt;
-    if (residual) v += residual[i];
-    v = relu ? fmaxf(v, 0.f) : v;
-    z[i] = v;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    if (e >= n) break;
+    const size_t idx = base + e;
+    float o = (v[i] - mu) * rs * gm + bt;
+    if (residual) o += rv[i];
+    o = relu ? fmaxf(o, 0.f) : o;
+    z[idx] = o;
     if (zb) {  // bf16 hi / lo planes: the next convolution's operand
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      zb[i] = hi;
-      zb[plane + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
+      const __nv_bfloat16 hi = __float2bfloat16_rn(o);
+      zb[idx] = hi;
+      zb[plane + idx] = __float2bfloat16_rn(o - __bfloat162float(hi));
     }
   }
 }
 
+// Backward staging: elements [e0, e1) of the block's slab of dz, z (ReLU mask, nullable) and y go
+// HBM -> shared memory with 16-byte cp.async (zero-filled past e1), every copy in flight at once and
+// no register waiting on a load (register-cached loads let the compiler consume the mask early,
+// which serialised the loads); thread t then reads its elements t + i*blockDim from shared memory.
+__device__ __forceinline__ void gn_cp16(float* dst, const float* src, bool ok) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16u : 0u) : "memory");
+}
+__device__ __forceinline__ void gn_stage_bwd(float* s_dz, float* s_z, float* s_y, const float* __restrict__ dz,
+                                             const float* __restrict__ z, const float* __restrict__ y, size_t base,
+                                             int e0, int e1, int cap) {
+  for (int j = threadIdx.x; j < cap / 4; j += blockDim.x) {
+    const int e = e0 + 4 * j;
+    const bool ok = e < e1;
+    const size_t o = ok ? base + e : 0;
+    gn_cp16(s_dz + 4 * j, dz + o, ok);
+    if (z) gn_cp16(s_z + 4 * j, z + o, ok);
+    gn_cp16(s_y + 4 * j, y + o, ok);
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+}
+__host__ __device__ constexpr size_t gn_bwd_smem(int nv, int nt) { return (size_t)3 * nv * nt * sizeof(float); }
+
 // dy_eff = dz * [z > 0] (relu_z nullable): GN backward per group
 //   dx = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),   dxhat = dy_eff * gamma
 // written as bf16 (it only feeds the bf16 gradient GEMMs), plus this frame's per-channel partials
-// part[f][c] = (sum dy_eff * xhat, sum dy_eff) for dgamma / dbeta.
-__global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_kernel(const float* __restrict__ dz, const float* __restrict__ z,
+// part[f][c] = (sum dy_eff * xhat, sum dy_eff) for dgamma / dbeta.  One block per frame; the slab is
+// read from HBM once (shared-memory staged).
+template <int NV>
+__global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_kernel(const float* __restrict__ dz, const float* __restrict__ z,
                                                             const float* __restrict__ y,
                                                             const float* __restrict__ stats,
                                                             const float* __restrict__ gamma, int HW, int C,
                                                             __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
-  __shared__ double sa[kGnMaxThreads], sb[kGnMaxThreads], ga[kGroups], gb[kGroups];
-  __shared__ float pc[2][kGnMaxThreads];
+  __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
+  __shared__ float pc[2][gn_bound(NV)];
+  extern __shared__ __align__(16) float gsm[];
+  const int cap = NV * blockDim.x;
+  float *s_dz = gsm, *s_z = gsm + cap, *s_y = gsm + 2 * cap;
   const int f = blockIdx.x, n = HW * C, c = threadIdx.x % C, cg = C / kGroups, g = c / cg;
   const size_t base = (size_t)f * n;
+  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, 0, n, cap);
   const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
   double a1 = 0.0, a2 = 0.0;
   float pg = 0.f, pb = 0.f;
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const size_t i = base + e;
-    float d = dz[i];
-    if (z && z[i] <= 0.f) d = 0.f;
-    const float xh = (y[i] - mu) * rs, dxh = d * gm;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    if (e >= n) break;
+    float d = s_dz[e];
+    if (z && s_z[e] <= 0.f) d = 0.f;
+    const float xh = (s_y[e] - mu) * rs, dxh = d * gm;
     a1 += dxh;
     a2 += (double)dxh * xh;
     pg += d * xh;
@@ -357,32 +408,40 @@ __global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_kernel(const float* __re
   }
   const double cnt = (double)HW * cg;
   const float m1 = (float)(ga[g] / cnt), m2 = (float)(gb[g] / cnt);
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const size_t i = base + e;
-    float d = dz[i];
-    if (z && z[i] <= 0.f) d = 0.f;
-    const float xh = (y[i] - mu) * rs;
-    dx[i] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    if (e >= n) break;
+    float d = s_dz[e];
+    if (z && s_z[e] <= 0.f) d = 0.f;
+    const float xh = (s_y[e] - mu) * rs;
+    dx[base + e] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
   }
 }
 
 // Large frames: the [HW][C] slab of a frame is split into S chunks of gn_chunk(C) elements, one
 // block each (grid (S, F)).  Pass 1 writes per-chunk per-group partial sums (double), pass 2 reduces
 // the frame's S partials in chunk order, then normalises / back-propagates its chunk.
-__host__ __device__ inline int gn_threads(int C) { return C > 256 ? C : 256; }
-__host__ __device__ inline int gn_chunk(int C) { return gn_threads(C) * 32; }
 
-__global__ void __launch_bounds__(kGnMaxThreads) gn_stats_part_kernel(const float* __restrict__ y, int HW, int C,
+template <int NV>
+__global__ void __launch_bounds__(gn_bound(NV)) gn_stats_part_kernel(const float* __restrict__ y, int HW, int C,
                                                                       double* __restrict__ gpart) {
-  __shared__ double sa[kGnMaxThreads], sb[kGnMaxThreads], ga[kGroups], gb[kGroups];
+  __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
   const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C);
   const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const size_t base = (size_t)f * n;
+  float v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {  // all loads in flight
+    const int e = e0 + threadIdx.x + i * blockDim.x;
+    v[i] = e < e1 ? y[base + e] : 0.f;
+  }
+  asm volatile("" ::: "memory");  // every load above is issued before any result is consumed
   double s1 = 0.0, s2 = 0.0;
-  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const float v = y[base + e];
-    s1 += v;
-    s2 += (double)v * v;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    s1 += v[i];
+    s2 += (double)v[i] * v[i];
   }
   gn_group_reduce(s1, s2, C, sa, sb, ga, gb);
   if (threadIdx.x < kGroups) {
@@ -392,7 +451,8 @@ __global__ void __launch_bounds__(kGnMaxThreads) gn_stats_part_kernel(const floa
   }
 }
 
-__global__ void __launch_bounds__(kGnMaxThreads) gn_apply_part_kernel(const float* __restrict__ y,
+template <int NV>
+__global__ void __launch_bounds__(gn_bound(NV)) gn_apply_part_kernel(const float* __restrict__ y,
                                                                       const double* __restrict__ gpart,
                                                                       const float* __restrict__ gamma,
                                                                       const float* __restrict__ beta,
@@ -424,42 +484,60 @@ __global__ void __launch_bounds__(kGnMaxThreads) gn_apply_part_kernel(const floa
   const float mu = smu[c / cg], rs = srs[c / cg], gm = gamma[c], bt = beta[c];
   const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const size_t base = (size_t)f * n;
-  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const size_t i = base + e;
-    float v = (y[i] - mu) * rs * gm + bt;
-    if (residual) v += residual[i];
-    v = relu ? fmaxf(v, 0.f) : v;
-    z[i] = v;
+  float v[NV], rv[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = e0 + threadIdx.x + i * blockDim.x;
+    v[i] = e < e1 ? y[base + e] : 0.f;
+    rv[i] = (residual && e < e1) ? residual[base + e] : 0.f;
+  }
+  asm volatile("" ::: "memory");  // every load above is issued before any result is consumed
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = e0 + threadIdx.x + i * blockDim.x;
+    if (e >= e1) break;
+    const size_t idx = base + e;
+    float o = (v[i] - mu) * rs * gm + bt;
+    if (residual) o += rv[i];
+    o = relu ? fmaxf(o, 0.f) : o;
+    z[idx] = o;
     if (zb) {
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      zb[i] = hi;
-      zb[plane + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
+      const __nv_bfloat16 hi = __float2bfloat16_rn(o);
+      zb[idx] = hi;
+      zb[plane + idx] = __float2bfloat16_rn(o - __bfloat162float(hi));
     }
   }
 }
 
 // backward pass 1: per chunk, per group (sum dxhat, sum dxhat*xhat) and per channel (sum dy*xhat, sum dy)
-__global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_part_kernel(const float* __restrict__ dz,
-                                                                    const float* __restrict__ z,
-                                                                    const float* __restrict__ y,
-                                                                    const float* __restrict__ stats,
-                                                                    const float* __restrict__ gamma, int HW, int C,
-                                                                    double* __restrict__ gpart,
-                                                                    float* __restrict__ part) {
-  __shared__ double sa[kGnMaxThreads], sb[kGnMaxThreads], ga[kGroups], gb[kGroups];
-  __shared__ float pc[2][kGnMaxThreads];
+template <int NV>
+__global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_part_kernel(const float* __restrict__ dz,
+                                                                  const float* __restrict__ z,
+                                                                  const float* __restrict__ y,
+                                                                  const float* __restrict__ stats,
+                                                                  const float* __restrict__ gamma, int HW, int C,
+                                                                  double* __restrict__ gpart,
+                                                                  float* __restrict__ part) {
+  __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
+  __shared__ float pc[2][gn_bound(NV)];
+  extern __shared__ __align__(16) float gsm[];
+  const int cap = NV * blockDim.x;
+  float *s_dz = gsm, *s_z = gsm + cap, *s_y = gsm + 2 * cap;
   const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C), c = threadIdx.x % C, cg = C / kGroups,
             g = c / cg;
-  const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
   const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const size_t base = (size_t)f * n;
+  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, e0, e1, cap);
+  const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
   double a1 = 0.0, a2 = 0.0;
   float pg = 0.f, pb = 0.f;
-  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const size_t i = base + e;
-    float d = dz[i];
-    if (z && z[i] <= 0.f) d = 0.f;
-    const float xh = (y[i] - mu) * rs, dxh = d * gm;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    if (e0 + e >= e1) break;
+    float d = s_dz[e];
+    if (z && s_z[e] <= 0.f) d = 0.f;
+    const float xh = (s_y[e] - mu) * rs, dxh = d * gm;
     a1 += dxh;
     a2 += (double)dxh * xh;
     pg += d * xh;
@@ -485,15 +563,31 @@ __global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_part_kernel(const float*
   }
 }
 
-__global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_apply_kernel(const float* __restrict__ dz,
-                                                                     const float* __restrict__ z,
-                                                                     const float* __restrict__ y,
-                                                                     const float* __restrict__ stats,
-                                                                     const float* __restrict__ gamma,
-                                                                     const double* __restrict__ gpart, int HW, int C,
-                                                                     __nv_bfloat16* __restrict__ dx) {
+template <int NV>
+__global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_apply_kernel(const float* __restrict__ dz,
+                                                                   const float* __restrict__ z,
+                                                                   const float* __restrict__ y,
+                                                                   const float* __restrict__ stats,
+                                                                   const float* __restrict__ gamma,
+                                                                   const double* __restrict__ gpart, int HW, int C,
+                                                                   __nv_bfloat16* __restrict__ dx) {
   __shared__ float sm1[kGroups], sm2[kGroups];
+  extern __shared__ __align__(16) float gsm[];
+  const int cap = NV * blockDim.x;
+  float *s_dz = gsm, *s_z = gsm + cap, *s_y = gsm + 2 * cap;
   const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C), cg = C / kGroups;
+  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
+  const size_t base = (size_t)f * n;
+  // the copies fly while the 16 group sums are reduced
+  for (int j = threadIdx.x; j < cap / 4; j += blockDim.x) {
+    const int e = e0 + 4 * j;
+    const bool ok = e < e1;
+    const size_t o = ok ? base + e : 0;
+    gn_cp16(s_dz + 4 * j, dz + o, ok);
+    if (z) gn_cp16(s_z + 4 * j, z + o, ok);
+    gn_cp16(s_y + 4 * j, y + o, ok);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   if (threadIdx.x < kGroups) {
     double a = 0.0, b = 0.0;
     for (int s = 0; s < S; ++s) {
@@ -505,18 +599,19 @@ __global__ void __launch_bounds__(kGnMaxThreads) gn_bwd_apply_kernel(const float
     sm1[threadIdx.x] = (float)(a / cnt);
     sm2[threadIdx.x] = (float)(b / cnt);
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   const int c = threadIdx.x % C, g = c / cg;
   const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
   const float m1 = sm1[g], m2 = sm2[g];
-  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
-  const size_t base = (size_t)f * n;
-  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const size_t i = base + e;
-    float d = dz[i];
-    if (z && z[i] <= 0.f) d = 0.f;
-    const float xh = (y[i] - mu) * rs;
-    dx[i] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    if (e0 + e >= e1) break;
+    float d = s_dz[e];
+    if (z && s_z[e] <= 0.f) d = 0.f;
+    const float xh = (s_y[e] - mu) * rs;
+    dx[base + e0 + e] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
   }
 }
 
@@ -1018,6 +1113,9 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
   return launch_igemm(ctx, gm, st);
 }
 
+// elements per thread of a one-block frame (<= NV)
+static int gn_vpt(int n, int nt) { return (n + nt - 1) / nt; }
+
 // z = (relu)(GN(y) (+ residual)); stats [F][16][2] = (mean, rstd); zb (nullable) = z as bf16 planes
 ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const float* gamma, const float* beta,
                     const float* residual, int relu, float* stats, float* z, __nv_bfloat16* zb, double* gpart,
@@ -1026,13 +1124,26 @@ ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const 
   DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");
   const int S = (HW * C + gn_chunk(C) - 1) / gn_chunk(C);
   if (S == 1) {  // one block per frame: statistics and normalisation in one pass over the slab
-    gn_fwd_kernel<<<F, nt, 0, st>>>(y, gamma, beta, residual, HW, C, relu, (size_t)F * HW * C, stats, z, zb);
+    const int nv = gn_vpt(HW * C, nt);
+#define GN_FWD(NV) gn_fwd_kernel<NV><<<F, nt, 0, st>>>(y, gamma, beta, residual, HW, C, relu, (size_t)F * HW * C, stats, z, zb)
+    if (nv <= 4) GN_FWD(4);
+    else if (nv <= 8) GN_FWD(8);
+    else if (nv <= 16) GN_FWD(16);
+    else GN_FWD(32);
+#undef GN_FWD
     ctx->count(1);
   } else {
     DDPPO_REQUIRE(ctx, gpart != nullptr, "groupnorm: large frames need partial-sum scratch");
-    gn_stats_part_kernel<<<dim3(S, F), nt, 0, st>>>(y, HW, C, gpart);
-    gn_apply_part_kernel<<<dim3(S, F), nt, 0, st>>>(y, gpart, gamma, beta, residual, HW, C, relu, (size_t)F * HW * C,
-                                                    stats, z, zb);
+#define GN_FWD2(NV)                                                                                          \
+  do {                                                                                                       \
+  gn_stats_part_kernel<NV><<<dim3(S, F), nt, 0, st>>>(y, HW, C, gpart);                                      \
+  gn_apply_part_kernel<NV><<<dim3(S, F), nt, 0, st>>>(y, gpart, gamma, beta, residual, HW, C, relu,          \
+                                                      (size_t)F * HW * C, stats, z, zb); \
+  } while (0)
+    if (nt == 1024) GN_FWD2(8);
+    else if (nt == 512) GN_FWD2(16);
+    else GN_FWD2(32);
+#undef GN_FWD2
     ctx->count(2);
   }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -1041,19 +1152,55 @@ ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const 
 
 // dz: gradient wrt z; relu_z: z if a ReLU produced it (mask z > 0), else null.  Writes dy (gradient
 // wrt y, bf16), dgamma, dbeta.  part [F*S][C][2] and gpart [F*S][16][2] (S > 1) are scratch.
+template <typename K>
+static ddppo_status gn_smem_attr(ddppo_ctx* ctx, K kernel, size_t bytes) {
+  static std::map<const void*, size_t> set;  // per kernel: the largest size opted in so far
+  size_t& cur = set[reinterpret_cast<const void*>(kernel)];
+  if (bytes > cur) {  // (static + dynamic shared memory above 48 KB needs the opt-in)
+    DDPPO_CUDA_TRY(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+  }
+  return DDPPO_OK;
+}
+
 ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const float* relu_z, const float* y,
                     const float* stats, const float* gamma, __nv_bfloat16* dy, float* dgamma, float* dbeta,
                     float* part, double* gpart, cudaStream_t st) {
+  ddppo_status s = DDPPO_OK;
   const int nt = gn_threads(C);
   DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");
   const int S = (HW * C + gn_chunk(C) - 1) / gn_chunk(C);
   if (S == 1) {
-    gn_bwd_kernel<<<F, nt, 0, st>>>(dz, relu_z, y, stats, gamma, HW, C, dy, part);
+    const int nv = gn_vpt(HW * C, nt);
+#define GN_BWD(NV)                                                                                           \
+  do {                                                                                                       \
+    s = gn_smem_attr(ctx, gn_bwd_kernel<NV>, gn_bwd_smem(NV, nt));                                           \
+    if (s != DDPPO_OK) return s;                                                                             \
+    gn_bwd_kernel<NV><<<F, nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, HW, C, dy, part);     \
+  } while (0)
+    if (nv <= 4) GN_BWD(4);
+    else if (nv <= 8) GN_BWD(8);
+    else if (nv <= 16) GN_BWD(16);
+    else GN_BWD(32);
+#undef GN_BWD
     ctx->count(1);
   } else {
     DDPPO_REQUIRE(ctx, gpart != nullptr, "groupnorm: large frames need partial-sum scratch");
-    gn_bwd_part_kernel<<<dim3(S, F), nt, 0, st>>>(dz, relu_z, y, stats, gamma, HW, C, gpart, part);
-    gn_bwd_apply_kernel<<<dim3(S, F), nt, 0, st>>>(dz, relu_z, y, stats, gamma, gpart, HW, C, dy);
+#define GN_BWD2(NV)                                                                                          \
+  do {                                                                                                       \
+    s = gn_smem_attr(ctx, gn_bwd_part_kernel<NV>, gn_bwd_smem(NV, nt));                                      \
+    if (s != DDPPO_OK) return s;                                                                             \
+    s = gn_smem_attr(ctx, gn_bwd_apply_kernel<NV>, gn_bwd_smem(NV, nt));                                     \
+    if (s != DDPPO_OK) return s;                                                                             \
+    gn_bwd_part_kernel<NV><<<dim3(S, F), nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, HW, C,  \
+                                                                       gpart, part);                        \
+    gn_bwd_apply_kernel<NV><<<dim3(S, F), nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, gpart, \
+                                                                        HW, C, dy);                         \
+  } while (0)
+    if (nt == 1024) GN_BWD2(8);
+    else if (nt == 512) GN_BWD2(16);
+    else GN_BWD2(32);
+#undef GN_BWD2
     ctx->count(2);
   }
   gn_param_reduce_kernel<<<C, kThreads, 0, st>>>(part, F * S, C, dgamma, dbeta);
