@@ -184,31 +184,37 @@ __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restr
   }
 }
 // per-frame partial weight gradient of the stem: part[f][o*k*k + tap] = sum_q dy[f][q][o] col[q][tap],
-// pixels in chunks of kStemPix: the chunk's im2col rows and dy rows are staged in shared memory;
-// lane = output channel, warps stride over taps (pixel order fixed)
-constexpr int kStemPix = 128, kStemTapPad = 65;
+// pixels in chunks of kStemPix: the chunk's im2col rows and dy rows are staged in shared memory.
+// Register-blocked outer products: thread (half, o-quad, tap-quad) accumulates a 4 x 4 tile over the
+// chunk's pixels of its parity half (2 float4 shared loads feed 16 FMAs); the two halves are added
+// in a fixed order at the end.
+constexpr int kStemPix = 128, kStemTapPad = 68;
 __global__ void __launch_bounds__(kThreads) stem_wgrad_kernel(const float* __restrict__ x,
                                                               const __nv_bfloat16* __restrict__ dy, int H, int Wd,
                                                               int Co, int k, int s, int p, int Ho, int Wo,
                                                               float* __restrict__ part) {
   extern __shared__ __align__(16) float sm[];
   float* xs = sm;                               // [H][Wd]
-  float* cs = xs + H * Wd;                      // [kStemPix][kStemTapPad]
+  float* cs = xs + (H * Wd + 3) / 4 * 4;        // [kStemPix][kStemTapPad] (16-byte aligned rows)
   float* ds = cs + kStemPix * kStemTapPad;      // [kStemPix][Co]
-  const int f = blockIdx.x, kk = k * k, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int f = blockIdx.x, kk = k * k;
+  const int half = threadIdx.x >> 7, r = threadIdx.x & 127;
+  const int oq = Co / 4, o0 = 4 * (r % oq), t0 = 4 * (r / oq);
+  const bool active = r < oq * 16;  // 16 tap quads cover k*k <= 64
   for (int i = threadIdx.x; i < H * Wd; i += blockDim.x) xs[i] = x[(size_t)f * H * Wd + i];
-  constexpr int kMaxT = 8;  // taps per warp (k*k <= 64)
-  float acc[kMaxT];
+  float acc[4][4];
 #pragma unroll
-  for (int t = 0; t < kMaxT; ++t) acc[t] = 0.f;
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b2 = 0; b2 < 4; ++b2) acc[a][b2] = 0.f;
   for (int q0 = 0; q0 < Ho * Wo; q0 += kStemPix) {
     const int nq = min(kStemPix, Ho * Wo - q0);
     __syncthreads();  // xs staged / previous chunk consumed
     // im2col rows of the chunk: thread pair per pixel (no division in the tap loops)
     for (int e = threadIdx.x; e < 2 * nq; e += blockDim.x) {
-      const int q = e >> 1, half = e & 1;
+      const int q = e >> 1, hv = e & 1;
       const int i = (q0 + q) / Wo, j = (q0 + q) - i * Wo;
-      for (int u = half; u < k; u += 2) {
+      for (int u = hv; u < k; u += 2) {
         const int yy = i * s - p + u;
         const bool yok = yy >= 0 && yy < H;
         for (int v = 0; v < k; ++v) {
@@ -216,27 +222,41 @@ __global__ void __launch_bounds__(kThreads) stem_wgrad_kernel(const float* __res
           cs[q * kStemTapPad + u * k + v] = (yok && xx >= 0 && xx < Wd) ? xs[yy * Wd + xx] : 0.f;
         }
       }
+      if (hv == 0)
+        for (int t = kk; t < kStemTapPad; ++t) cs[q * kStemTapPad + t] = 0.f;
     }
     for (int e = threadIdx.x; e < nq * Co; e += blockDim.x)
       ds[e] = __bfloat162float(dy[((size_t)f * Ho * Wo + q0) * Co + e]);
     __syncthreads();
-    if (lane < Co) {
-      for (int q = 0; q < nq; ++q) {
-        const float d = ds[q * Co + lane];
+    if (active) {
+#pragma unroll 4
+      for (int q = half; q < nq; q += 2) {
+        const float4 d = *reinterpret_cast<const float4*>(ds + q * Co + o0);
+        const float4 c = *reinterpret_cast<const float4*>(cs + q * kStemTapPad + t0);
+        const float dv[4] = {d.x, d.y, d.z, d.w}, cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-        for (int t = 0; t < kMaxT; ++t) {
-          const int tap = warp + t * nw;
-          if (tap < kk) acc[t] = fmaf(d, cs[q * kStemTapPad + tap], acc[t]);
-        }
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2) acc[a][b2] = fmaf(dv[a], cv[b2], acc[a][b2]);
       }
     }
   }
-  if (lane < Co) {
+  __syncthreads();
+  float* red = cs;  // [128][16] partials of the odd half
+  if (half == 1 && active)
 #pragma unroll
-    for (int t = 0; t < kMaxT; ++t) {
-      const int tap = warp + t * nw;
-      if (tap < kk) part[(size_t)f * Co * kk + lane * kk + tap] = acc[t];
-    }
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b2 = 0; b2 < 4; ++b2) red[r * 16 + a * 4 + b2] = acc[a][b2];
+  __syncthreads();
+  if (half == 0 && active) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b2 = 0; b2 < 4; ++b2) {
+        const int tap = t0 + b2;
+        if (tap < kk) part[(size_t)f * Co * kk + (o0 + a) * kk + tap] = acc[a][b2] + red[r * 16 + a * 4 + b2];
+      }
   }
 }
 // dW[i] = sum over frames (fixed order) of part[f][i]
@@ -1049,7 +1069,7 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
                       const ConvScratch& sc, cudaStream_t st) {
   if (is_stem(g)) {
     DDPPO_REQUIRE(ctx, dx == nullptr, "stem conv: no input gradient");
-    const size_t smem = ((size_t)g.H * g.W + (size_t)kStemPix * (kStemTapPad + g.Co)) * sizeof(float);
+    const size_t smem = (((size_t)g.H * g.W + 3) / 4 * 4 + (size_t)kStemPix * (kStemTapPad + g.Co)) * sizeof(float);
     DDPPO_REQUIRE(ctx, smem <= 200 * 1024, "stem conv: frame too large for shared memory");
     static bool attr_set = false;
     if (!attr_set) {
