@@ -341,7 +341,8 @@ ddppo_status ddppo_debug_groupnorm(ddppo_ctx* ctx, const float* y, const float* 
 ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
                                          const ddppo_batch* host_batch, void* ws, uint8_t* out, int64_t cap,
                                          int64_t* host_n, void* stream);
-/* 3x3 / stride 2 / pad 1 max pool (first maximum in window order; arg = window index 0..8). */
+/* 3x3 / stride 2 / pad 1 max pool (first maximum in window order; arg = window index 0..8).
+   x [F][H][W][C] channels-last, C % 4 == 0 (else DDPPO_ERR_CONFIG); y / arg [F][Ho][Wo][C]. */
 ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int F, int H, int W, int C, float* y,
                                  uint8_t* arg, const float* dy, float* dx, void* stream);
 

@@ -654,60 +654,91 @@ __global__ void __launch_bounds__(kThreads) gn_param_reduce_kernel(const float* 
   }
 }
 
-// 3x3 / stride 2 / pad 1 max pool with the first maximum in (u, v) order
+// 3x3 / stride 2 / pad 1 max pool with the first maximum in (u, v) order.  Thread = (output pixel,
+// 4 channels): the 9 window loads (float4) are independent and in flight together; 32-bit indices.
 __global__ void maxpool_fwd_kernel(const float* __restrict__ x, int F, int H, int W, int C, int Ho, int Wo,
                                    float* __restrict__ y, uint8_t* __restrict__ arg, __nv_bfloat16* __restrict__ yb) {
-  const size_t n = (size_t)F * Ho * Wo * C;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    const size_t pix = i / C;
-    const int j = (int)(pix % Wo), ii = (int)((pix / Wo) % Ho), f = (int)(pix / ((size_t)Wo * Ho));
-    float best = -INFINITY;
-    int ba = 0;
-    for (int u = 0; u < 3; ++u)
-      for (int v = 0; v < 3; ++v) {
-        const int yy = 2 * ii - 1 + u, xx = 2 * j - 1 + v;
-        if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
-        const float val = x[(((size_t)f * H + yy) * W + xx) * C + c];
-        if (val > best) {
-          best = val;
-          ba = u * 3 + v;
-        }
+  const int C4 = C >> 2, n4 = F * Ho * Wo * C4;
+  const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i4 >= n4) return;
+  const int c4 = i4 % C4, pix = i4 / C4;
+  const int j = pix % Wo, ii = (pix / Wo) % Ho, f = pix / (Wo * Ho);
+  float4 w[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int yy = 2 * ii - 1 + t / 3, xx = 2 * j - 1 + t % 3;
+    w[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W)
+               ? *reinterpret_cast<const float4*>(x + ((f * H + yy) * W + xx) * C + 4 * c4)
+               : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+  }
+  float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  int ba[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const float v[4] = {w[t].x, w[t].y, w[t].z, w[t].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (v[e] > best[e]) {
+        best[e] = v[e];
+        ba[e] = t;
       }
-    y[i] = best;
-    arg[i] = (uint8_t)ba;
-    if (yb) {
-      const __nv_bfloat16 hi = __float2bfloat16_rn(best);
-      yb[i] = hi;
-      yb[n + i] = __float2bfloat16_rn(best - __bfloat162float(hi));
+  }
+  const int o = pix * C + 4 * c4;
+  *reinterpret_cast<float4*>(y + o) = make_float4(best[0], best[1], best[2], best[3]);
+  *reinterpret_cast<uchar4*>(arg + o) = make_uchar4((uint8_t)ba[0], (uint8_t)ba[1], (uint8_t)ba[2], (uint8_t)ba[3]);
+  if (yb) {
+    __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      hi[e] = __float2bfloat16_rn(best[e]);
+      lo[e] = __float2bfloat16_rn(best[e] - __bfloat162float(hi[e]));
     }
+    const size_t n = (size_t)F * Ho * Wo * C;
+    *reinterpret_cast<uint2*>(yb + o) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(yb + n + o) = *reinterpret_cast<const uint2*>(lo);
   }
 }
-// dx[f][y][x][c] = sum over windows whose argmax is (y, x) of dy (gather, fixed order)
+// dx[f][y][x][c] = sum over windows whose argmax is (y, x) of dy (gather, fixed window order).
+// Thread = (input pixel, 4 channels); the <= 4 candidate windows' arg / dy loads are all issued
+// before any comparison.
 __global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* __restrict__ arg, int F, int H, int W,
                                    int C, int Ho, int Wo, float* __restrict__ dx) {
-  const size_t n = (size_t)F * H * W * C;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    const size_t pix = i / C;
-    const int xx = (int)(pix % W), y = (int)((pix / W) % H), f = (int)(pix / ((size_t)W * H));
-    float acc = 0.f;
-    for (int u = 0; u < 3; ++u) {
-      const int yy = y + 1 - u;
-      if (yy < 0 || (yy & 1)) continue;
-      const int ii = yy >> 1;
-      if (ii >= Ho) continue;
-      for (int v = 0; v < 3; ++v) {
-        const int xv = xx + 1 - v;
-        if (xv < 0 || (xv & 1)) continue;
-        const int j = xv >> 1;
-        if (j >= Wo) continue;
-        const size_t o = (((size_t)f * Ho + ii) * Wo + j) * C + c;
-        if (arg[o] == u * 3 + v) acc += dy[o];
-      }
-    }
-    dx[i] = acc;
+  const int C4 = C >> 2, n4 = F * H * W * C4;
+  const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i4 >= n4) return;
+  const int c4 = i4 % C4, pix = i4 / C4;
+  const int xx = pix % W, yq = (pix / W) % H, f = pix / (W * H);
+  // windows (ii, jj) with 2*ii - 1 + u = y, u in [0, 3)
+  uchar4 a[4];
+  float4 d[4];
+  int uv[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    // even y: one window (u = 1); odd y: two (u = 0, 2); the same for x / v
+    const int u = (yq & 1) ? 2 * (q >> 1) : 1, v = (xx & 1) ? 2 * (q & 1) : 1;
+    const int yy = yq + 1 - u, xv = xx + 1 - v;
+    const int ii = yy >> 1, jj = xv >> 1;
+    const bool dup = (!(yq & 1) && (q >> 1)) || (!(xx & 1) && (q & 1));
+    const bool ok = !dup && yy >= 0 && xv >= 0 && ii < Ho && jj < Wo;
+    uv[q] = ok ? u * 3 + v : -1;
+    const int o = ((f * Ho + (ok ? ii : 0)) * Wo + (ok ? jj : 0)) * C + 4 * c4;
+    a[q] = ok ? *reinterpret_cast<const uchar4*>(arg + o) : make_uchar4(255, 255, 255, 255);
+    d[q] = ok ? *reinterpret_cast<const float4*>(dy + o) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int u = 0; u < 3; ++u)  // the reference order: windows by (u, v) ascending
+#pragma unroll
+    for (int v = 0; v < 3; ++v)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (uv[q] == u * 3 + v) {
+          if (a[q].x == u * 3 + v) acc[0] += d[q].x;
+          if (a[q].y == u * 3 + v) acc[1] += d[q].y;
+          if (a[q].z == u * 3 + v) acc[2] += d[q].z;
+          if (a[q].w == u * 3 + v) acc[3] += d[q].w;
+        }
+  *reinterpret_cast<float4*>(dx + pix * C + 4 * c4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
 }
 
 // NHWC [F][HW][C] <-> flat [F][C*HW] in (c, h, w) order (PyTorch flatten of NCHW)
@@ -1346,8 +1377,8 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
   {
     ConvGN& c = P.convs[0];
     const int hp = P.pool_hw;
-    maxpool_fwd_kernel<<<blocks_for(ctx, (size_t)F * hp * hp * 32), kThreads, 0, st>>>(c.z, F, c.Ho, c.Wo, 32, hp, hp,
-                                                                                       P.pool_out, P.pool_arg, P.pool_b);
+    maxpool_fwd_kernel<<<(F * hp * hp * 8 + kThreads - 1) / kThreads, kThreads, 0, st>>>(
+        c.z, F, c.Ho, c.Wo, 32, hp, hp, P.pool_out, P.pool_arg, P.pool_b);
     ctx->count(1);
   }
   for (auto& blk : P.blocks) {
@@ -1497,7 +1528,7 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   }
   // max-pool, then the stem (no input gradient)
   ConvGN& stem = P.convs[0];
-  maxpool_bwd_kernel<<<blocks_for(ctx, (size_t)F * stem.Ho * stem.Wo * 32), kThreads, 0, st>>>(
+  maxpool_bwd_kernel<<<(F * stem.Ho * stem.Wo * 8 + kThreads - 1) / kThreads, kThreads, 0, st>>>(
       dz, P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -1585,15 +1616,17 @@ extern "C" ddppo_status ddppo_debug_groupnorm(ddppo_ctx* ctx, const float* y, co
 extern "C" ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int F, int H, int W, int C, float* y,
                                             uint8_t* arg, const float* dy, float* dx, void* stream) {
   if (!ctx) return DDPPO_ERR_CONFIG;
-  DDPPO_REQUIRE(ctx, F >= 1 && H >= 2 && W >= 2 && C >= 1, "maxpool: bad geometry");
+  DDPPO_REQUIRE(ctx, F >= 1 && H >= 2 && W >= 2 && C >= 4 && C % 4 == 0, "maxpool: bad geometry (C % 4 == 0)");
+  DDPPO_REQUIRE(ctx, (size_t)F * H * W * C < (1u << 31), "maxpool: tensor too large");
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
   cudaStream_t st = as_stream(stream);
   ProfScope ps(ctx, DDPPO_K_OTHER, st, 0);
-  maxpool_fwd_kernel<<<blocks_for(ctx, (size_t)F * Ho * Wo * C), kThreads, 0, st>>>(x, F, H, W, C, Ho, Wo, y, arg,
+  maxpool_fwd_kernel<<<(F * Ho * Wo * (C / 4) + kThreads - 1) / kThreads, kThreads, 0, st>>>(x, F, H, W, C, Ho, Wo, y, arg,
                                                                                      nullptr);
   ctx->count(1);
   if (dy) {
-    maxpool_bwd_kernel<<<blocks_for(ctx, (size_t)F * H * W * C), kThreads, 0, st>>>(dy, arg, F, H, W, C, Ho, Wo, dx);
+    maxpool_bwd_kernel<<<(F * H * W * (C / 4) + kThreads - 1) / kThreads, kThreads, 0, st>>>(dy, arg, F, H, W, C, Ho,
+                                                                                          Wo, dx);
     ctx->count(1);
   }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
