@@ -48,25 +48,42 @@ __constant__ float kRgbMean[3] = {0.485f * 255.f, 0.456f * 255.f, 0.406f * 255.f
 __constant__ float kRgbStd[3] = {0.229f * 255.f, 0.224f * 255.f, 0.225f * 255.f};
 __global__ void rgbd_prologue_kernel(const float* __restrict__ obs, const int32_t* __restrict__ env_idx, int T,
                                      int T_run, int F, int Hin, float* __restrict__ x0, __nv_bfloat16* __restrict__ x0b) {
-  const int Ho = Hin / 2, Wo = Hin / 2;
+  // thread = (frame, output row, pair of output columns): one float4 per input channel and row
+  const int Ho = Hin / 2, Wo = Hin / 2, WP = Wo / 2;
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= F * Ho * WP) return;
+  const int jp = item % WP, ii = (item / WP) % Ho, f = item / (WP * Ho);
+  const int b = f / T_run, t = f - b * T_run;
+  const float* src = obs + ((size_t)env_idx[b] * T + t) * 4 * Hin * Hin + (size_t)(2 * ii) * Hin + 4 * jp;
+  float4 r0[4], r1[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    r0[c] = *reinterpret_cast<const float4*>(src + (size_t)c * Hin * Hin);
+    r1[c] = *reinterpret_cast<const float4*>(src + (size_t)c * Hin * Hin + Hin);
+  }
   const size_t n = (size_t)F * Ho * Wo * 8;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i & 7);
-    const size_t pix = i >> 3;
-    const int j = (int)(pix % Wo), ii = (int)((pix / Wo) % Ho), f = (int)(pix / ((size_t)Wo * Ho));
-    float v = 0.f;
-    if (c < 4) {
-      const int b = f / T_run, t = f - b * T_run;
-      const float* src = obs + (((size_t)env_idx[b] * T + t) * 4 + c) * Hin * Hin;
-      const int y = 2 * ii, x = 2 * j;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // output pixel (ii, 2*jp + h)
+    float v[8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
       const float m = c < 3 ? kRgbMean[c] : 0.f, inv = c < 3 ? 1.f / kRgbStd[c] : 1.f;
-      v = 0.25f * (((src[y * Hin + x] - m) * inv + (src[y * Hin + x + 1] - m) * inv) +
-                   ((src[(y + 1) * Hin + x] - m) * inv + (src[(y + 1) * Hin + x + 1] - m) * inv));
+      const float a0 = h ? r0[c].z : r0[c].x, a1 = h ? r0[c].w : r0[c].y;
+      const float b0 = h ? r1[c].z : r1[c].x, b1 = h ? r1[c].w : r1[c].y;
+      v[c] = 0.25f * (((a0 - m) * inv + (a1 - m) * inv) + ((b0 - m) * inv + (b1 - m) * inv));
+      v[c + 4] = 0.f;
     }
-    x0[i] = v;
-    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-    x0b[i] = hi;
-    x0b[n + i] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    const size_t o = (((size_t)f * Ho + ii) * Wo + 2 * jp + h) * 8;
+    *reinterpret_cast<float4*>(x0 + o) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(x0 + o + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      hi[c] = __float2bfloat16_rn(v[c]);
+      lo[c] = __float2bfloat16_rn(v[c] - __bfloat162float(hi[c]));
+    }
+    *reinterpret_cast<uint4*>(x0b + o) = *reinterpret_cast<const uint4*>(hi);
+    *reinterpret_cast<uint4*>(x0b + n + o) = *reinterpret_cast<const uint4*>(lo);
   }
 }
 
@@ -88,11 +105,13 @@ __global__ void weights_bf16_kernel(const float* __restrict__ W, int Co, int Ci,
     if (wd) wd[c * (k * k * Co) + uv * Co + o] = hi;
   }
 }
-// all convolutions' weights of one minibatch in one launch (blockIdx.y = convolution); Cp >= Ci is
-// the padded channel count of the GEMM operand (extra channels get zero weights)
+// all convolutions' weights of one minibatch in one launch: the convolutions' Wr index ranges are
+// concatenated (off[i] = start of convolution i), one thread per element; Cp >= Ci is the padded
+// channel count of the GEMM operand (extra channels get zero weights)
 constexpr int kMaxConvs = 64;
 struct WeightPrep {
   int n;
+  int off[kMaxConvs + 1];
   struct Item {
     const float* W;
     __nv_bfloat16 *wr, *wd;  // wd nullable (no input gradient)
@@ -100,16 +119,23 @@ struct WeightPrep {
   } it[kMaxConvs];
 };
 __global__ void weights_prep_kernel(const WeightPrep prep) {
-  const WeightPrep::Item& t = prep.it[blockIdx.y];
-  const int Co = t.Co, Ci = t.Ci, Cp = t.Cp, kk = t.k * t.k, n = Co * Cp * kk;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const int o = j / (kk * Cp), rem = j % (kk * Cp), uv = rem / Cp, c = rem % Cp;  // j = Wr index
-    const float w = c < Ci ? t.W[(o * Ci + c) * kk + uv] : 0.f;
-    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-    t.wr[j] = hi;
-    t.wr[n + j] = __float2bfloat16_rn(w - __bfloat162float(hi));
-    if (t.wd && c < Ci) t.wd[c * (kk * Co) + uv * Co + o] = hi;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= prep.off[prep.n]) return;
+  int lo = 0, hi_i = prep.n - 1;  // the convolution holding g: off[lo] <= g < off[lo + 1]
+  while (lo < hi_i) {
+    const int mid = (lo + hi_i + 1) >> 1;
+    if (prep.off[mid] <= g) lo = mid;
+    else hi_i = mid - 1;
   }
+  const WeightPrep::Item& t = prep.it[lo];
+  const int Co = t.Co, Ci = t.Ci, Cp = t.Cp, kk = t.k * t.k, n = Co * Cp * kk;
+  const int j = g - prep.off[lo];  // Wr index
+  const int o = j / (kk * Cp), rem = j - o * (kk * Cp), uv = rem / Cp, c = rem - uv * Cp;
+  const float w = c < Ci ? t.W[(o * Ci + c) * kk + uv] : 0.f;
+  const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+  t.wr[j] = hi;
+  t.wr[n + j] = __float2bfloat16_rn(w - __bfloat162float(hi));
+  if (t.wd && c < Ci) t.wd[c * (kk * Co) + uv * Co + o] = hi;
 }
 // weight gradient: dWt [(u, v, c)][o] (the wgrad GEMM's output, c < Cp) -> dW [Co][Ci][k][k]
 __global__ void wgrad_to_torch_kernel(const float* __restrict__ dwt, int Co, int Ci, int Cp, int k,
@@ -1352,24 +1378,25 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
   {
     WeightPrep prep;
     prep.n = 0;
-    int max_n = 0;
+    prep.off[0] = 0;
     for (size_t i = 0; i < P.convs.size(); ++i) {
       const ConvGN& c = P.convs[i];
       if (c.Ci == 1) continue;  // the Depth stem runs SIMT on fp32 weights
       DDPPO_REQUIRE(ctx, prep.n < kMaxConvs, "too many convolutions for one weight-prep launch");
-      prep.it[prep.n++] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k};
-      max_n = std::max(max_n, c.Co * c.Ci * c.k * c.k);
+      prep.it[prep.n] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k};
+      prep.off[prep.n + 1] = prep.off[prep.n] + c.Co * c.Ci * c.k * c.k;
+      ++prep.n;
     }
-    weights_prep_kernel<<<dim3((max_n + 1023) / 1024, prep.n), 1024, 0, st>>>(prep);
+    weights_prep_kernel<<<(prep.off[prep.n] + 255) / 256, 256, 0, st>>>(prep);
     ctx->count(1);
   }
   if (!P.rgbd) {
     gather_obs_kernel<<<blocks_for(ctx, (size_t)F * kImg * kImg), kThreads, 0, st>>>(b.obs, b.env_idx, b.T, b.T_run,
                                                                                       F, P.x0);
   } else {
-    const size_t n = (size_t)F * (kImgRgbd / 2) * (kImgRgbd / 2) * 8;
-    rgbd_prologue_kernel<<<blocks_for(ctx, n), kThreads, 0, st>>>(b.obs, b.env_idx, b.T, b.T_run, F, kImgRgbd, P.x0,
-                                                                  P.x0b);
+    DDPPO_REQUIRE(ctx, kImgRgbd % 4 == 0, "rgbd: input width must be a multiple of 4");
+    rgbd_prologue_kernel<<<(F * (kImgRgbd / 2) * (kImgRgbd / 4) + kThreads - 1) / kThreads, kThreads, 0, st>>>(
+        b.obs, b.env_idx, b.T, b.T_run, F, kImgRgbd, P.x0, P.x0b);
   }
   ctx->count(1);
   ddppo_status s = conv_gn_fwd(ctx, prm, P, P.convs[0], nullptr, 1, st);
