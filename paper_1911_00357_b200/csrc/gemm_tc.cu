@@ -23,7 +23,7 @@
 
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kThreads = 128;
+constexpr int kBM = 128, kBK = 64, kThreads = 256;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -171,9 +171,10 @@ __device__ __forceinline__ void convert_tile(int mode, unsigned char* dst, unsig
     stage_tile<ROWS, SPLIT>(dst, dlo, X, sr, sk, r0, R, k0, K);
     return;
   }
-  for (int row = threadIdx.x; row < ROWS; row += kThreads) {
-#pragma unroll
-    for (int kc = 0; kc < kBK / 8; ++kc) {
+  // (row, 8-wide k piece) pairs over all threads; consecutive threads take consecutive rows
+  for (int pidx = threadIdx.x; pidx < ROWS * (kBK / 8); pidx += kThreads) {
+    const int row = pidx % ROWS, kc = pidx / ROWS;
+    {
       float v[8];
       if (mode == 0) {
 #pragma unroll
@@ -306,15 +307,16 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
     if (n_chunks >= 2) mbar_wait(&mma_bar[st ^ 1], phase[st ^ 1]);
   }
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // epilogue: warp w owns TMEM lanes (rows) 32w..32w+31; 32x8 blocks are transposed through
-  // shared memory (the A stage buffer, free now) so that every store instruction writes
-  // contiguous columns of one row.
+  // epilogue: warp w owns TMEM lanes (rows) 32(w%4)..+31 and column half w/4; 32x8 blocks are
+  // transposed through shared memory (the A stage buffer, free now) so that every store
+  // instruction writes contiguous columns of one row.
   float* tr = reinterpret_cast<float*>(sA[0]) + warp * (32 * 9);
-  const int row0 = m0 + warp * 32;
+  const int row0 = m0 + (warp & 3) * 32;
+  constexpr int kHalf = BN / 2;
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 8) {
+  for (int c0 = (warp >> 2) * kHalf; c0 < (warp >> 2) * kHalf + kHalf; c0 += 8) {
     uint32_t r[8];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
