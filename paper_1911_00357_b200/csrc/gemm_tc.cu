@@ -23,7 +23,7 @@
 
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kThreads = 256;
+constexpr int kBM = 128, kBK = 64, kThreads = 512;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -312,7 +312,8 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
   // instruction writes contiguous columns of one row.
   float* tr = reinterpret_cast<float*>(sA[0]) + warp * (32 * 9);
   const int row0 = m0 + (warp & 3) * 32;
-  constexpr int kHalf = BN / 2;
+  constexpr int kHalf = BN / (kThreads / 128);  // columns per warp
+  static_assert(kHalf >= 8 && kHalf % 8 == 0, "epilogue column slice");
 #pragma unroll 1
   for (int c0 = (warp >> 2) * kHalf; c0 < (warp >> 2) * kHalf + kHalf; c0 += 8) {
     uint32_t r[8];
