@@ -209,57 +209,56 @@ __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restr
     }
   }
 }
-// per-frame partial weight gradient of the stem: part[f][o*k*k + tap] = sum_q dy[f][q][o] col[q][tap],
-// pixels in chunks of kStemPix: the chunk's im2col rows and dy rows are staged in shared memory.
-// Register-blocked outer products: thread (half, o-quad, tap-quad) accumulates a 4 x 4 tile over the
-// chunk's pixels of its parity half (2 float4 shared loads feed 16 FMAs); the two halves are added
-// in a fixed order at the end.
-constexpr int kStemPix = 128, kStemTapPad = 68;
+// per-frame partial weight gradient of the stem: part[f][o*k*k + tap] = sum_q dy[f][q][o] col[q][tap].
+// The frame (zero-padded) and all of its dy rows (bf16) sit in shared memory, loaded once; the
+// im2col values are read straight from the padded frame.  Register-blocked outer products: thread
+// (half, o-quad, tap-quad) accumulates a 4 x 4 tile over the output rows of its parity; the two
+// halves are added in a fixed order at the end.
 __global__ void __launch_bounds__(kThreads) stem_wgrad_kernel(const float* __restrict__ x,
                                                               const __nv_bfloat16* __restrict__ dy, int H, int Wd,
                                                               int Co, int k, int s, int p, int Ho, int Wo,
                                                               float* __restrict__ part) {
   extern __shared__ __align__(16) float sm[];
-  float* xs = sm;                               // [H][Wd]
-  float* cs = xs + (H * Wd + 3) / 4 * 4;        // [kStemPix][kStemTapPad] (16-byte aligned rows)
-  float* ds = cs + kStemPix * kStemTapPad;      // [kStemPix][Co]
+  const int HP = H + 2 * p, WP = Wd + 2 * p;
+  __nv_bfloat16* dys = reinterpret_cast<__nv_bfloat16*>(sm);           // [Ho*Wo][Co]
+  float* xp = sm + (Ho * Wo * Co / 2 + 3) / 4 * 4;                      // [HP][WP] zero-padded frame
   const int f = blockIdx.x, kk = k * k;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(dy + (size_t)f * Ho * Wo * Co);
+    uint4* dst = reinterpret_cast<uint4*>(dys);
+    for (int i = threadIdx.x; i < Ho * Wo * Co / 8; i += blockDim.x) dst[i] = src[i];
+  }
+  for (int i = threadIdx.x; i < HP * WP; i += blockDim.x) {
+    const int yy = i / WP - p, xx = i % WP - p;
+    xp[i] = (yy >= 0 && yy < H && xx >= 0 && xx < Wd) ? x[((size_t)f * H + yy) * Wd + xx] : 0.f;
+  }
+  __syncthreads();
   const int half = threadIdx.x >> 7, r = threadIdx.x & 127;
   const int oq = Co / 4, o0 = 4 * (r % oq), t0 = 4 * (r / oq);
   const bool active = r < oq * 16;  // 16 tap quads cover k*k <= 64
-  for (int i = threadIdx.x; i < H * Wd; i += blockDim.x) xs[i] = x[(size_t)f * H * Wd + i];
+  int off[4];
+#pragma unroll
+  for (int kq = 0; kq < 4; ++kq) {
+    const int tap = t0 + kq;
+    off[kq] = tap < kk ? (tap / k) * WP + (tap % k) : 0;  // taps past k*k: computed, never stored
+  }
   float acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b2 = 0; b2 < 4; ++b2) acc[a][b2] = 0.f;
-  for (int q0 = 0; q0 < Ho * Wo; q0 += kStemPix) {
-    const int nq = min(kStemPix, Ho * Wo - q0);
-    __syncthreads();  // xs staged / previous chunk consumed
-    // im2col rows of the chunk: thread pair per pixel (no division in the tap loops)
-    for (int e = threadIdx.x; e < 2 * nq; e += blockDim.x) {
-      const int q = e >> 1, hv = e & 1;
-      const int i = (q0 + q) / Wo, j = (q0 + q) - i * Wo;
-      for (int u = hv; u < k; u += 2) {
-        const int yy = i * s - p + u;
-        const bool yok = yy >= 0 && yy < H;
-        for (int v = 0; v < k; ++v) {
-          const int xx = j * s - p + v;
-          cs[q * kStemTapPad + u * k + v] = (yok && xx >= 0 && xx < Wd) ? xs[yy * Wd + xx] : 0.f;
-        }
-      }
-      if (hv == 0)
-        for (int t = kk; t < kStemTapPad; ++t) cs[q * kStemTapPad + t] = 0.f;
-    }
-    for (int e = threadIdx.x; e < nq * Co; e += blockDim.x)
-      ds[e] = __bfloat162float(dy[((size_t)f * Ho * Wo + q0) * Co + e]);
-    __syncthreads();
-    if (active) {
+  if (active) {
+    for (int i = half; i < Ho; i += 2) {
+      const float* xrow = xp + i * s * WP;
+      const __nv_bfloat16* drow = dys + (size_t)i * Wo * Co + o0;
 #pragma unroll 4
-      for (int q = half; q < nq; q += 2) {
-        const float4 d = *reinterpret_cast<const float4*>(ds + q * Co + o0);
-        const float4 c = *reinterpret_cast<const float4*>(cs + q * kStemTapPad + t0);
-        const float dv[4] = {d.x, d.y, d.z, d.w}, cv[4] = {c.x, c.y, c.z, c.w};
+      for (int j = 0; j < Wo; ++j) {
+        const float* xb = xrow + j * s;
+        const float cv[4] = {xb[off[0]], xb[off[1]], xb[off[2]], xb[off[3]]};
+        const uint2 d2 = *reinterpret_cast<const uint2*>(drow + j * Co);
+        const float2 d01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d2.x));
+        const float2 d23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&d2.y));
+        const float dv[4] = {d01.x, d01.y, d23.x, d23.y};
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -268,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) stem_wgrad_kernel(const float* __res
     }
   }
   __syncthreads();
-  float* red = cs;  // [128][16] partials of the odd half
+  float* red = xp;  // [128][16] partials of the odd half (the frame is no longer needed)
   if (half == 1 && active)
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -1126,7 +1125,9 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
                       const ConvScratch& sc, cudaStream_t st) {
   if (is_stem(g)) {
     DDPPO_REQUIRE(ctx, dx == nullptr, "stem conv: no input gradient");
-    const size_t smem = (((size_t)g.H * g.W + 3) / 4 * 4 + (size_t)kStemPix * (kStemTapPad + g.Co)) * sizeof(float);
+    DDPPO_REQUIRE(ctx, (g.Ho * g.Wo * g.Co) % 8 == 0, "stem conv: Ho*Wo*Co must be a multiple of 8");
+    const size_t hp = (size_t)(g.H + 2 * g.p) * (g.W + 2 * g.p);
+    const size_t smem = (((size_t)g.Ho * g.Wo * g.Co / 2 + 3) / 4 * 4 + std::max<size_t>(hp, 128 * 16)) * sizeof(float);
     DDPPO_REQUIRE(ctx, smem <= 200 * 1024, "stem conv: frame too large for shared memory");
     static bool attr_set = false;
     if (!attr_set) {
