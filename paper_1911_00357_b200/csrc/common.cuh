@@ -264,6 +264,10 @@ struct IGemm {                   // C[m][n] (+)= sum_k A(m,k) B(n,k), fp32 C
   float* partial = nullptr;      // splits*M*N floats when splits > 1
   int accumulate = 0;
   int auto_split = 0;            // with `partial` (>= 16*M*N floats): split k when the tile grid is small
+  // weight-gradient epilogue: C is [(u, v, c < wg_cp)][o] (M = k*k*wg_cp, N = Co); instead of C, the
+  // split sum is written straight to wg_out in PyTorch order [o][c < wg_cr][u][v] (needs `partial`)
+  float* wg_out = nullptr;
+  int wg_cp = 0, wg_cr = 0, wg_kk = 0;
 };
 ddppo_status launch_igemm(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st);
 

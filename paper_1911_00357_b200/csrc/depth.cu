@@ -137,16 +137,6 @@ __global__ void weights_prep_kernel(const WeightPrep prep) {
   t.wr[n + j] = __float2bfloat16_rn(w - __bfloat162float(hi));
   if (t.wd && c < Ci) t.wd[c * (kk * Co) + uv * Co + o] = hi;
 }
-// weight gradient: dWt [(u, v, c)][o] (the wgrad GEMM's output, c < Cp) -> dW [Co][Ci][k][k]
-__global__ void wgrad_to_torch_kernel(const float* __restrict__ dwt, int Co, int Ci, int Cp, int k,
-                                      float* __restrict__ dw) {
-  const int n = Co * Ci * k * k;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int o = i / (Ci * k * k), rem = i % (Ci * k * k);
-    const int c = rem / (k * k), uv = rem % (k * k);
-    dw[i] = dwt[(size_t)(uv * Cp + c) * Co + o];
-  }
-}
 // fp32 -> bf16 hi / lo planes (plane = n)
 __global__ void to_planes_kernel(const float* __restrict__ x, size_t n, __nv_bfloat16* __restrict__ xb) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -1162,10 +1152,12 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
     gm.K = M;
     gm.splits = splits;
     gm.partial = sc.part;
+    gm.wg_out = dw;  // the split sum lands in PyTorch order [o][c][u][v] (no dWt round trip)
+    gm.wg_cp = g.Ci;
+    gm.wg_cr = g.Cr;
+    gm.wg_kk = g.k * g.k;
     ddppo_status s = launch_igemm(ctx, gm, st);
     if (s != DDPPO_OK) return s;
-    wgrad_to_torch_kernel<<<blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st>>>(sc.dwt, g.Co, g.Cr, g.Ci, g.k, dw);
-    ctx->count(1);
   }
   if (dx == nullptr) return DDPPO_OK;
   // dgrad: dx[p][c] (+)= sum_{(u,v,o)} dy[tap^T(p; u, v)][o] W[o][c][u][v]

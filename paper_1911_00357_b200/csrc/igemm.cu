@@ -392,6 +392,20 @@ __global__ void ig_splitk_reduce_kernel(const float* __restrict__ P, int splits,
   }
 }
 
+// weight gradient: dW[o][c][uv] = sum over the splits (fixed order) of P[z][(uv*Cp + c)*N + o], c < Cr
+// (walks P in order: coalesced split reads, one scattered store per element)
+__global__ void ig_splitk_reduce_wgrad_kernel(const float* __restrict__ P, int splits, long long zs, int N, int Cp,
+                                              int Cr, int kk, float* __restrict__ dw) {
+  const int n = kk * Cp * N;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int m = i / N, o = i - m * N, uv = m / Cp, c = m - uv * Cp;
+    if (c >= Cr) continue;
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += __ldcg(P + z * zs + i);
+    dw[(o * Cr + c) * kk + uv] = s;
+  }
+}
+
 int log2_exact(int v) {
   if (v <= 0 || (v & (v - 1))) return -1;
   int l = 0;
@@ -435,6 +449,19 @@ ddppo_status launch_ig(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st) {
   const int nz = (g.K + kper - 1) / kper;
   const OpDev a = to_dev(g.a, g.M), b = to_dev(g.b, g.N);
   dim3 grid((g.N + BN - 1) / BN, (g.M + kBM - 1) / kBM, nz);
+  if (g.wg_out) {
+    // weight gradient: partial tiles (plain stores), then the split sum in PyTorch weight order
+    DDPPO_REQUIRE(ctx, g.partial && !g.accumulate && g.M == g.wg_kk * g.wg_cp, "igemm: bad weight-gradient epilogue");
+    const long long zs = (long long)g.M * g.N;
+    ctx->count(2);
+    kern<<<grid, kThreads, smem, st>>>(a, b, g.partial, g.N, g.M, g.N, g.K, kper, zs, 0);
+    DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+    const int n = g.M * g.N;
+    ig_splitk_reduce_wgrad_kernel<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, st>>>(
+        g.partial, nz, zs, g.N, g.wg_cp, g.wg_cr, g.wg_kk, g.wg_out);
+    DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+    return DDPPO_OK;
+  }
   ctx->count(nz == 1 ? 1 : 2);
   if (nz == 1) {
     kern<<<grid, kThreads, smem, st>>>(a, b, g.C, g.ldc, g.M, g.N, g.K, kper, 0, g.accumulate);
