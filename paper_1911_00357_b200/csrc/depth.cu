@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kThreads) frame_sum_kernel(const float* __rest
 // contiguously (coalesced); with 256 % C == 0 thread t always sees channel t % C, so per-group and
 // per-channel partial sums are per-thread sums combined in a fixed order through shared memory.
 constexpr int kGnMaxThreads = 1024;  // blockDim = max(256, C): a multiple of C
+constexpr int kMaxConvsGn = 64;
 __host__ __device__ inline int gn_threads(int C) { return C > 256 ? C : 256; }
 constexpr int kGnChunk = 8192;  // elements per chunk (a multiple of every C): kGnChunk / blockDim per thread
 __host__ __device__ inline int gn_chunk(int) { return kGnChunk; }
@@ -669,6 +670,39 @@ __global__ void __launch_bounds__(kThreads) gn_param_reduce_kernel(const float* 
   }
 }
 
+// every GroupNorm layer's dgamma / dbeta of one backward pass in one launch: block = one channel of
+// one layer (ch_off[i] = first block of layer i); the same fixed-order reduction as gn_param_reduce
+struct GnParamAll {
+  int n;
+  int ch_off[kMaxConvsGn + 1];
+  struct Item {
+    const float* part;
+    float *dgamma, *dbeta;
+    int rows, C;
+  } it[kMaxConvsGn];
+};
+__global__ void __launch_bounds__(kThreads) gn_param_reduce_all_kernel(const GnParamAll a) {
+  __shared__ double red[2 * (kThreads / 32)];
+  int lo = 0, hi = a.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.ch_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const GnParamAll::Item& t = a.it[lo];
+  const int c = blockIdx.x - a.ch_off[lo];
+  double acc[2] = {0.0, 0.0};
+  for (int f = threadIdx.x; f < t.rows; f += blockDim.x) {
+    acc[0] += t.part[((size_t)f * t.C + c) * 2];
+    acc[1] += t.part[((size_t)f * t.C + c) * 2 + 1];
+  }
+  block_sum<2>(acc, red);
+  if (threadIdx.x == 0) {
+    t.dgamma[c] = (float)acc[0];
+    t.dbeta[c] = (float)acc[1];
+  }
+}
+
 // 3x3 / stride 2 / pad 1 max pool with the first maximum in (u, v) order.  Thread = (output pixel,
 // 4 channels): the 9 window loads (float4) are independent and in flight together; 32-bit indices.
 __global__ void maxpool_fwd_kernel(const float* __restrict__ x, int F, int H, int W, int C, int Ho, int Wo,
@@ -863,6 +897,8 @@ struct ConvGN {
   int Ci_real;                        // channels of the parameter tensor
   int64_t w, gw, gb;                  // parameter offsets (conv weight, GN gamma, GN beta)
   float *x, *y, *z, *stats;           // input (not owned), conv out (pre-GN), GN out, GN stats [F][16][2]
+  float* gn_part;                     // this layer's dgamma / dbeta row partials [F*S][Co][2]
+  int gn_rows;                        // F*S
   __nv_bfloat16 *xb, *zb;             // input / output as bf16 hi / lo planes (GEMM operands; zb may be null)
   __nv_bfloat16 *wr_b, *wd_b;         // this minibatch's weights as GEMM operands (Wr planes, Wd)
 };
@@ -946,6 +982,8 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
     const size_t S = ((size_t)c.Ho * c.Wo * Co + gn_chunk(Co) - 1) / gn_chunk(Co);
     max_gn_rows = std::max(max_gn_rows, (size_t)F * S);
     max_gn_part = std::max(max_gn_part, (size_t)F * S * Co * 2);
+    c.gn_part = take((size_t)F * S * Co * 2);  // per layer: reduced once after the whole backward
+    c.gn_rows = (int)(F * S);
     P.convs.push_back(c);
     return (int)P.convs.size() - 1;
   };
@@ -1235,7 +1273,7 @@ static ddppo_status gn_smem_attr(ddppo_ctx* ctx, K kernel, size_t bytes) {
 
 ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const float* relu_z, const float* y,
                     const float* stats, const float* gamma, __nv_bfloat16* dy, float* dgamma, float* dbeta,
-                    float* part, double* gpart, cudaStream_t st) {
+                    float* part, double* gpart, cudaStream_t st, bool reduce_params = true) {
   ddppo_status s = DDPPO_OK;
   const int nt = gn_threads(C);
   DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");
@@ -1273,8 +1311,10 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
 #undef GN_BWD2
     ctx->count(2);
   }
-  gn_param_reduce_kernel<<<C, kThreads, 0, st>>>(part, F * S, C, dgamma, dbeta);
-  ctx->count(1);
+  if (reduce_params) {  // else the caller reduces `part` later (gn_param_reduce_all)
+    gn_param_reduce_kernel<<<C, kThreads, 0, st>>>(part, F * S, C, dgamma, dbeta);
+    ctx->count(1);
+  }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
@@ -1298,7 +1338,7 @@ ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, c
 ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P, ConvGN& c, const float* dz,
                          const float* relu_z, float* dx, int accumulate_dx, cudaStream_t st) {
   ddppo_status s = gn_bwd(ctx, P.F, c.Ho * c.Wo, c.Co, dz, relu_z, c.y, c.stats, prm + c.gw, P.dyb, grad + c.gw,
-                          grad + c.gb, P.gn_part, P.gn_gpart, st);
+                          grad + c.gb, c.gn_part, P.gn_gpart, st, /*reduce_params=*/false);
   if (s != DDPPO_OK) return s;
   return conv_bwd(ctx, geom_of(P, c), c.x, c.xb, prm + c.w, c.wd_b, P.dyb, grad + c.w, dx, accumulate_dx,
                   scratch_of(P), st);
@@ -1552,7 +1592,21 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
       dz, P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
-  return conv_gn_bwd(ctx, prm, grad, P, stem, da, stem.z, nullptr, 0, st);
+  if ((s = conv_gn_bwd(ctx, prm, grad, P, stem, da, stem.z, nullptr, 0, st)) != DDPPO_OK) return s;
+  // all layers' dgamma / dbeta from their row partials, one launch
+  GnParamAll a;
+  a.n = 0;
+  a.ch_off[0] = 0;
+  for (const ConvGN& c : P.convs) {
+    DDPPO_REQUIRE(ctx, a.n < kMaxConvsGn, "too many GroupNorm layers for one reduction launch");
+    a.it[a.n] = GnParamAll::Item{c.gn_part, grad + c.gw, grad + c.gb, c.gn_rows, c.Co};
+    a.ch_off[a.n + 1] = a.ch_off[a.n] + c.Co;
+    ++a.n;
+  }
+  gn_param_reduce_all_kernel<<<a.ch_off[a.n], kThreads, 0, st>>>(a);
+  ctx->count(1);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
 }
 
 // ------------------------------------------------------------------ diagnostic entries (tests)
