@@ -492,7 +492,9 @@ struct ddppo_ctx::GraphCache {
   };
   static constexpr size_t kMaxEntries = 4;  // e.g. double-buffered outputs: a few live keys
   std::vector<Entry> entries;
-  std::vector<unsigned char> seen;  // last key run eagerly: captured when it repeats (lazy setup done)
+  // keys run eagerly so far (most recent last, a few kept): a key is captured when it repeats (its
+  // lazy setup is done) -- also when keys alternate (e.g. double-buffered statistics)
+  std::vector<std::vector<unsigned char>> seen;
   uint64_t clock = 0;
   cudaStream_t stream = nullptr;    // capture / replay stream (non-blocking; the caller's may be legacy)
 };
@@ -593,10 +595,13 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
     ddppo_ctx::GraphCache::Entry* hit = nullptr;
     for (auto& e : gc.entries)
       if (e.key == key) hit = &e;
-    if (!hit && gc.seen != key) {
+    bool seen_before = false;
+    for (const auto& k : gc.seen) seen_before = seen_before || k == key;
+    if (!hit && !seen_before) {
       // first time with this configuration: run eagerly (lazy allocations, attribute setup), capture
       // when it repeats
-      gc.seen = key;
+      gc.seen.push_back(key);
+      if (gc.seen.size() > 2 * ddppo_ctx::GraphCache::kMaxEntries) gc.seen.erase(gc.seen.begin());
       DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, gs));
       s = learner_body(ctx, L, host_desc, ro, cfg, params, m, v, adv, ret, stats_out, ws, w, gs, mbs, use_peers,
                        mb0);
