@@ -507,3 +507,32 @@ def test_learner_graph_replay_matches_eager(dd, ctx, cfgname):
     dd.ddppo_set_graphs(ctx, True)
     for a, b in zip(out[False], out[True]):
         assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.gpu
+def test_learner_graph_alternating_stats_buffers(dd, ctx):
+    """Double-buffered statistics (the pipelined training loop): the two keys alternate, each is
+    captured on its second use and replayed after -- five steps agree bit for bit with eager."""
+    from paper_1911_00357_b200.learner import Learner
+    c = synth.CONFIGS["gps"]
+    desc = dd.model_desc(c["arch"])
+    lay = dd.param_layout(desc)
+    P = dd.param_count(desc)
+    p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 41)
+    out = {}
+    for graphs in (False, True):
+        dd.ddppo_set_graphs(ctx, graphs)
+        lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+        bufs = [torch.zeros_like(lrn.stats) for _ in range(2)]
+        rec = []
+        for it in range(5):
+            ro = synth.rollout(c["E"], c["T"], 42, iteration=it, hidden=desc.hidden)
+            lrn.load_rollout(ro, synth.perms(42, it, c["epochs"], c["E"]))
+            lrn.step(stats=bufs[it % 2])
+            torch.cuda.synchronize()
+            rec.append(bufs[it % 2].cpu().numpy().copy())
+        ctx.check()
+        out[graphs] = (lrn.params.cpu().numpy(), np.stack(rec))
+    dd.ddppo_set_graphs(ctx, True)
+    for a, b in zip(out[False], out[True]):
+        assert np.array_equal(a, b)
