@@ -985,7 +985,7 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   // weight gradients (off the dependency chain), tcgen05 GEMMs over the S samples:
   //   dW_hh[row][j] = sum_s dG_h[s][row] H_in[s][j];  dW_ih[row][j] = sum_s dG_x[s][row] X[s][j]
   //   Q[row][n]     = sum_s dG_x[s][row] U[s][n]   (-> goal FC, embedding and b_ih gradients)
-  // main stream: dW_hh; side a: dW_ih; side b: Q, input-layer gradients, db_hh
+  // main stream: dW_hh, db_hh; side a: (head weight gradient,) dW_ih; side b: Q, input-layer gradients
   ProfScope ps(ctx, DDPPO_K_WGRAD, st, 2);  // + the 3 GEMMs, counted by launch_gemm_tc
   DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sa));
   DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sb));
@@ -1001,7 +1001,8 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
                                                 grad + layout_offset(L, "goal_fc.bias"),
                                                 grad + layout_offset(L, "act_embed.weight"),
                                                 grad + layout_offset(L, "rnn.bias_ih"));
-  colsum_kernel<<<kG / 32, 256, 0, sb>>>(p.dGH, kG, S, kG, grad + layout_offset(L, "rnn.bias_hh"));
+  // (b_hh's gradient on the launching stream after dW_hh: the three chains then end within ~1 us)
+  colsum_kernel<<<kG / 32, 256, 0, st>>>(p.dGH, kG, S, kG, grad + layout_offset(L, "rnn.bias_hh"));
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   DDPPO_CUDA_TRY(ctx, fork_to(ctx, sa, st));  // join
   DDPPO_CUDA_TRY(ctx, fork_to(ctx, sb, st));
