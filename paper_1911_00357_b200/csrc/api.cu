@@ -426,23 +426,17 @@ ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_mode
       b.n_valid = mbs[k].n_valid;
       b.obs = ro->obs;
       b.c0 = ro->c0;
+      float* st_out = stats_out ? stats_out + (size_t)k * 8 : w.grad_norm;
+      const float* mis = cfg->normalize_adv ? w.mean_invstd : nullptr;
       if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
         s = toy_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
       else if (visual)
         s = depth_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
-      else
-        s = gps_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st, /*skip_head=*/true);
+      else  // GPS: the recurrence with head + PPO loss + head input gradient in its epilogue, one launch
+        s = gps_fwd_loss(ctx, L, params, b, li, mis, cfg->loss, w.dlogits, w.dvalues, st_out, w.model_ws, st);
       if (s != DDPPO_OK) return s;
-      float* st_out = stats_out ? stats_out + (size_t)k * 8 : w.grad_norm;
-      const float* mis = cfg->normalize_adv ? w.mean_invstd : nullptr;
-      if (host_desc->arch == DDPPO_ARCH_GPS_GRU) {  // head + loss + head input gradient in one kernel
-        const float *Wo, *bo, *Hs;
-        float* dH;
-        gps_head_io(L, params, b, w.model_ws, &Wo, &bo, &Hs, &dH);
-        s = launch_head_loss(ctx, Wo, bo, Hs, b, li, mis, cfg->loss, w.dlogits, w.dvalues, dH, st_out, st);
-      } else {
+      if (host_desc->arch != DDPPO_ARCH_GPS_GRU)
         s = launch_loss(ctx, w.logits, w.values, b, li, mis, cfg->loss, w.dlogits, w.dvalues, st_out, st);
-      }
       if (s != DDPPO_OK) return s;
       w.grad = use_peers ? w.grad2[(peer_mb0 + k) & 1] : w.grad2[0];
       if (host_desc->arch == DDPPO_ARCH_TOY_MLP)

@@ -353,12 +353,9 @@ ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
 ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                      const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st,
                      bool dh_ready = false);
-// the GPS workspace's head operands (W_o, b_o, H) and head input-gradient buffer
-ddppo_status gps_head_io(const ModelLayout& L, const float* params, const ddppo_batch& b, void* ws, const float** Wo,
-                         const float** bo, const float** Hs, float** dH);
-// fused head + PPO loss + head input gradient (loss.cu), the learner runtime's GPS path
-ddppo_status launch_head_loss(ddppo_ctx* ctx, const float* Wo, const float* bo, const float* Hs, const ddppo_batch& b,
-                              const ddppo_loss_inputs& in, const float* mean_invstd, const ddppo_loss_cfg& cfg,
-                              float* dlogits, float* dvalues, float* dH, float* stats, cudaStream_t st);
+// the recurrence + fused head / PPO loss / head input gradient (one launch; the learner runtime)
+ddppo_status gps_fwd_loss(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
+                          const ddppo_loss_inputs& in, const float* mean_invstd, const ddppo_loss_cfg& cfg,
+                          float* dlogits, float* dvalues, float* stats, void* ws, cudaStream_t st);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

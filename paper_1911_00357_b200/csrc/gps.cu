@@ -26,7 +26,10 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <string.h>
+
 #include "common.cuh"
+#include "ppo_sample.cuh"
 
 namespace {
 
@@ -130,6 +133,15 @@ struct GpsPtrs {
   float* dGH;    // [S][1536]
   float* U;      // [S][9]     [goal, 1, onehot(prev_action)]
   float* Q;      // [1536][9]  dG_x^T U
+  // fused head + PPO loss + head input gradient after the recurrence (learner runtime; on = 0: off)
+  struct Loss {
+    int on, use_vclip;
+    const int32_t *len, *action;
+    const float *logp_old, *value_old, *ret, *adv, *mean_invstd;
+    float inv_n, eps, vclip_eps, c_v, c_e, n_valid;
+    float *dlogits, *dvalues, *stats;
+    int* err;
+  } loss;
 };
 
 // ------------------------------------------------------------------ mbarrier / st.async helpers
@@ -450,6 +462,88 @@ __global__ void __launch_bounds__(kFwdThreads, 1) gps_gru_fwd_kernel(GpsPtrs p) 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // no CTA exits while a peer could still address its shared memory
+  if (p.loss.on) {
+    // ---- fused head + PPO loss + head input gradient (a5 head, a6): the cluster barrier above made
+    // every CTA's h_t rows visible; warp per sample over the cluster's 128 warps: logits / value =
+    // W_o h + b_o, the sample's loss gradient (ppo_sample), dH = W_o^T [dlogits; dvalue]; loss
+    // statistics summed per CTA, then over the 16 CTAs in CTA order (DSMEM) -- deterministic.
+    float* wo = reinterpret_cast<float*>(sm.h_tile);  // [5][512] + b_o (the B tiles are free now)
+    double* red = reinterpret_cast<double*>(sm.h_tile[1]);      // block_sum scratch [6][8]
+    double* cta_part = red + 64;                                   // this CTA's 6 sums
+    for (int i = tid; i < 5 * kH; i += blockDim.x) wo[i] = p.Wo[i];
+    if (tid < 5) wo[5 * kH + tid] = p.bo[tid];
+    __syncthreads();
+    const auto& L = p.loss;
+    float mu = 0.f, invstd = 1.f;
+    if (L.mean_invstd) {
+      mu = L.mean_invstd[0];
+      invstd = L.mean_invstd[1];
+    }
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    const int M = B * T_run;
+    for (int m = c * (kFwdThreads / 32) + warp; m < M; m += kNC * (kFwdThreads / 32)) {
+      const int b = m / T_run, t = m - b * T_run;
+      const int n = p.env_idx[b];
+      const float* h = p.Hs + (size_t)m * kH;
+      float hv[kH / 32];
+      float out[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < kH / 32; ++i) {
+        hv[i] = h[lane + 32 * i];
+#pragma unroll
+        for (int o = 0; o < 5; ++o) out[o] += wo[o * kH + lane + 32 * i] * hv[i];
+      }
+#pragma unroll
+      for (int o = 0; o < 5; ++o) out[o] = warp_sum(out[o]) + wo[5 * kH + o];
+      float4 dz = make_float4(0.f, 0.f, 0.f, 0.f);
+      float dv = 0.f;
+      if (t < L.len[n]) {  // (warp-uniform)
+        const size_t s = (size_t)n * p.ld + t;
+        const float A = L.mean_invstd ? (L.adv[s] - mu) * invstd : L.adv[s];
+        const SampleOut o = ppo_sample(make_float4(out[0], out[1], out[2], out[3]), out[4], L.action[s], L.logp_old[s],
+                                       L.value_old[s], L.ret[s], A, L.inv_n, L.eps, L.vclip_eps, L.c_v, L.c_e,
+                                       L.use_vclip);
+        dz = o.dz;
+        dv = o.dv;
+        if (lane == 0) {
+          acc[0] += (double)o.surr;
+          acc[1] += (double)o.lv;
+          acc[2] += (double)o.H;
+          acc[3] += (double)o.clipped;
+          acc[4] += (double)o.kl;
+        }
+      }
+      if (lane == 0) {
+        *reinterpret_cast<float4*>(L.dlogits + (size_t)m * 4) = dz;
+        L.dvalues[m] = dv;
+      }
+      float* dh = p.dH + (size_t)m * kH;
+#pragma unroll
+      for (int i = 0; i < kH / 32; ++i) {
+        const int k = lane + 32 * i;
+        dh[k] = wo[k] * dz.x + wo[kH + k] * dz.y + wo[2 * kH + k] * dz.z + wo[3 * kH + k] * dz.w + wo[4 * kH + k] * dv;
+      }
+    }
+    block_sum<6>(acc, red);
+    if (tid == 0)
+#pragma unroll
+      for (int i = 0; i < 6; ++i) cta_part[i] = acc[i];
+    cluster_sync_all();  // every CTA's sums are in place
+    if (c == 0 && tid == 0) {
+      double fin[6] = {0, 0, 0, 0, 0, 0};
+      for (int j = 0; j < kNC; ++j) {
+        const uint32_t ra = map_to_cta(cta_part, (uint32_t)j);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          double v;
+          asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra + 8u * (uint32_t)i) : "memory");
+          fin[i] += v;
+        }
+      }
+      write_stats(fin, L.inv_n, L.c_v, L.c_e, L.n_valid, L.stats, L.err);
+    }
+    cluster_sync_all();  // CTA 0 has read every peer's sums
+  }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
@@ -872,6 +966,7 @@ size_t carve(void* base, int B, int T, GpsWs* w) {
 
 GpsPtrs make_ptrs(const ModelLayout& L, const float* params, const ddppo_batch& b, void* ws) {
   GpsPtrs p;
+  memset(&p, 0, sizeof(p));  // (loss.on = 0: no fused head / loss unless gps_fwd_loss asks for it)
   p.Wg = params + layout_offset(L, "goal_fc.weight");
   p.bg = params + layout_offset(L, "goal_fc.bias");
   p.Emb = params + layout_offset(L, "act_embed.weight");
@@ -929,16 +1024,6 @@ ddppo_status launch_cluster(ddppo_ctx* ctx, K kernel, int threads, size_t smem, 
 
 size_t gps_workspace(int max_B, int T) { return carve(nullptr, max_B, T, nullptr); }
 
-ddppo_status gps_head_io(const ModelLayout& L, const float* params, const ddppo_batch& b, void* ws, const float** Wo,
-                        const float** bo, const float** Hs, float** dH) {
-  GpsPtrs p = make_ptrs(L, params, b, ws);
-  *Wo = p.Wo;
-  *bo = p.bo;
-  *Hs = p.Hs;
-  *dH = p.dH;
-  return DDPPO_OK;
-}
-
 ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                      float* logits, float* values, void* ws, cudaStream_t st, bool skip_head) {
   DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");
@@ -955,6 +1040,41 @@ ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   head_fwd_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, p.bo, p.Hs, S, logits, values);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
+}
+
+// learner runtime: the recurrence with the head, the PPO loss and the head's input gradient fused
+// into its epilogue (dlogits / dvalues / dH / stats written by the same launch)
+ddppo_status gps_fwd_loss(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
+                          const ddppo_loss_inputs& in, const float* mean_invstd, const ddppo_loss_cfg& cfg,
+                          float* dlogits, float* dvalues, float* stats, void* ws, cudaStream_t st) {
+  DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");
+  DDPPO_REQUIRE(ctx, b.n_valid >= 1, "loss: need n_valid >= 1");
+  DDPPO_REQUIRE(ctx, !cfg.normalize_adv || mean_invstd, "loss: normalize_adv needs mean_invstd");
+  DDPPO_REQUIRE(ctx, (uintptr_t)dlogits % 16 == 0, "loss: dlogits must be 16-byte aligned");
+  GpsPtrs p = make_ptrs(L, params, b, ws);
+  GpsPtrs::Loss& l = p.loss;
+  l.on = 1;
+  l.use_vclip = cfg.use_value_clip;
+  l.len = b.len;
+  l.action = in.action;
+  l.logp_old = in.logp_old;
+  l.value_old = in.value_old;
+  l.ret = in.ret;
+  l.adv = in.adv;
+  l.mean_invstd = cfg.normalize_adv ? mean_invstd : nullptr;
+  l.inv_n = 1.f / (float)b.n_valid;
+  l.eps = cfg.clip_eps;
+  l.vclip_eps = cfg.vclip_eps;
+  l.c_v = cfg.c_v;
+  l.c_e = cfg.c_e;
+  l.n_valid = (float)b.n_valid;
+  l.dlogits = dlogits;
+  l.dvalues = dvalues;
+  l.stats = stats;
+  l.err = ctx->d_err;
+  const int S = b.B * b.T_run;
+  ProfScope ps(ctx, DDPPO_K_NET_FWD, st, 1);
+  return launch_cluster(ctx, gps_gru_fwd_kernel, kFwdThreads, sizeof(FwdSmem) + (size_t)S * sizeof(float), p, st);
 }
 
 ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
