@@ -95,6 +95,8 @@ ddppo_status ddppo_ctx_destroy(ddppo_ctx* ctx) {
   for (auto s : ctx->side)
     if (s) cudaStreamDestroy(s);
   cudaFree(ctx->own_flags);
+  if (ctx->cnt_stream) cudaStreamDestroy(ctx->cnt_stream);
+  if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_counters);
@@ -299,6 +301,9 @@ ddppo_status ddppo_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n) {
   if (!ctx) return DDPPO_ERR_CONFIG;
   DDPPO_REQUIRE(ctx, host_vals && n >= 0 && n <= kMaxCountVals, "allreduce_counts: 0 <= n <= 64");
   if (ctx->world == 1 || n == 0) return DDPPO_OK;
+  // with the NVLink peer areas set up (a registered learner): an exchange on the context's own
+  // stream, so the host does not wait behind the learner work queued on the caller's stream
+  if (ctx->peer_flags[ctx->rank]) return peer_allreduce_counts(ctx, host_vals, n);
   DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_i64, host_vals, n * sizeof(int64_t), cudaMemcpyHostToDevice, 0));
   DDPPO_NCCL_TRY(ctx, ncclAllReduce(ctx->d_i64, ctx->d_i64, n, ncclInt64, ncclSum, ctx->comm, 0));
   DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(host_vals, ctx->d_i64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, 0));

@@ -31,6 +31,9 @@ struct ddppo_ctx {
   void* peer_ws = nullptr;
   char* peer_ws_base[kMaxPeers] = {};
   unsigned int* d_peer_epoch = nullptr;  // barrier epoch, advanced on the device by the barrier kernel
+  unsigned int* d_cnt_epoch = nullptr;   // counts-exchange epoch (ddppo_allreduce_counts over NVLink)
+  cudaStream_t cnt_stream = nullptr;     // its own non-blocking stream: not queued behind learner work
+  int64_t* h_cnt = nullptr;              // pinned host result
   uint64_t peer_mb = 0;
   // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step
   int* d_step = nullptr;
@@ -274,6 +277,9 @@ ddppo_status launch_igemm(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st);
 // NVLink peer memory (peer.cu)
 ddppo_status peer_exchange(ddppo_ctx* ctx, void* local, void** out);
 ddppo_status peer_setup_flags(ddppo_ctx* ctx);
+// sum of n <= kMaxCountVals int64 over the ranks (rank order) through the peer flag areas, on the
+// context's own stream (host-blocking on that stream only)
+ddppo_status peer_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n);
 ddppo_status launch_peer_reduce_norm(ddppo_ctx* ctx, float* const* peers, float* gsum, int64_t P, float max_norm,
                                      float* grad_norm, cudaStream_t st);
 // Adam on an already summed gradient whose clip scale is in ctx->d_scalars[0] (adam.cu)

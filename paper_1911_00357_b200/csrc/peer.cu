@@ -126,6 +126,52 @@ ddppo_status allocation_base(ddppo_ctx* ctx, const void* p, char** base) {
   return DDPPO_OK;
 }
 
+// One IPC-shared area per rank: the learner barrier's flags (first, peer_flags[j] points here), the
+// counts exchange's flags and its values, double-buffered by epoch parity: rank r writes slot
+// [e & 1][r] of every peer's area, then signals; a rank can only reach epoch e + 2 after every peer
+// signalled e + 1, i.e. after every peer finished reading epoch e's values.
+struct PeerArea {
+  unsigned int flags[kMaxPeers];
+  unsigned int cnt_flags[kMaxPeers];
+  long long vals[2][kMaxPeers][kMaxCountVals];
+};
+
+struct CountArgs {
+  PeerArea* area[kMaxPeers];
+  long long v[kMaxCountVals];
+};
+
+__global__ void peer_counts_kernel(const CountArgs a, int world, int rank, int n, unsigned int* d_epoch,
+                                   long long* out, int* err) {
+  __shared__ unsigned int s_epoch;
+  if (threadIdx.x == 0) {
+    s_epoch = *d_epoch + 1;
+    *d_epoch = s_epoch;
+  }
+  __syncthreads();
+  const unsigned int epoch = s_epoch;
+  const int par = (int)(epoch & 1u);
+  const int j = threadIdx.x;
+  if (j < world) {
+    for (int i = 0; i < n; ++i) a.area[j]->vals[par][rank][i] = a.v[i];
+    __threadfence_system();
+    st_release_sys(&a.area[j]->cnt_flags[rank], epoch);
+    long long spins = 0;
+    while ((int)(ld_acquire_sys(&a.area[rank]->cnt_flags[j]) - epoch) < 0) {
+      if (++spins > kSpinLimit) {
+        atomicOr(err, ERR_BIT_COMM);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (j < n) {
+    long long t = 0;
+    for (int r = 0; r < world; ++r) t += ((volatile long long*)a.area[rank]->vals[par][r])[j];  // rank order
+    out[j] = t;
+  }
+}
+
 struct Shared {
   cudaIpcMemHandle_t handle;
   unsigned long long offset;
@@ -172,12 +218,13 @@ ddppo_status peer_exchange(ddppo_ctx* ctx, void* local, void** out) {
 ddppo_status peer_setup_flags(ddppo_ctx* ctx) {
   if (ctx->peer_flags[ctx->rank]) return DDPPO_OK;
   unsigned int* f = nullptr;
-  DDPPO_CUDA_TRY(ctx, cudaMalloc(&f, kMaxPeers * sizeof(unsigned int)));
-  DDPPO_CUDA_TRY(ctx, cudaMemset(f, 0, kMaxPeers * sizeof(unsigned int)));
+  DDPPO_CUDA_TRY(ctx, cudaMalloc(&f, sizeof(PeerArea)));
+  DDPPO_CUDA_TRY(ctx, cudaMemset(f, 0, sizeof(PeerArea)));
   DDPPO_CUDA_TRY(ctx, cudaDeviceSynchronize());
   ctx->own_flags = f;
-  DDPPO_CUDA_TRY(ctx, cudaMalloc(&ctx->d_peer_epoch, sizeof(unsigned int)));
-  DDPPO_CUDA_TRY(ctx, cudaMemset(ctx->d_peer_epoch, 0, sizeof(unsigned int)));
+  DDPPO_CUDA_TRY(ctx, cudaMalloc(&ctx->d_peer_epoch, 2 * sizeof(unsigned int)));
+  DDPPO_CUDA_TRY(ctx, cudaMemset(ctx->d_peer_epoch, 0, 2 * sizeof(unsigned int)));
+  ctx->d_cnt_epoch = ctx->d_peer_epoch + 1;
   DDPPO_CUDA_TRY(ctx, cudaDeviceSynchronize());
   void* out[kMaxPeers] = {};
   ddppo_status s = peer_exchange(ctx, f, out);
@@ -203,5 +250,26 @@ ddppo_status launch_peer_reduce_norm(ddppo_ctx* ctx, float* const* peers, float*
                                                        grad_norm, ctx->d_err);
   ctx->count(2);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
+ddppo_status peer_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n) {
+  DDPPO_REQUIRE(ctx, ctx->world <= kMaxPeers && ctx->peer_flags[ctx->rank] && n <= kMaxCountVals,
+                "peer counts: flags not set up");
+  if (!ctx->cnt_stream) {
+    DDPPO_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->cnt_stream, cudaStreamNonBlocking));
+    DDPPO_CUDA_TRY(ctx, cudaMallocHost(&ctx->h_cnt, kMaxCountVals * sizeof(int64_t)));
+  }
+  CountArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int j = 0; j < ctx->world; ++j) a.area[j] = reinterpret_cast<PeerArea*>(ctx->peer_flags[j]);
+  for (int i = 0; i < n; ++i) a.v[i] = (long long)host_vals[i];
+  peer_counts_kernel<<<1, 64, 0, ctx->cnt_stream>>>(a, ctx->world, ctx->rank, n, ctx->d_cnt_epoch,
+                                                     reinterpret_cast<long long*>(ctx->d_i64), ctx->d_err);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_cnt, ctx->d_i64, n * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                      ctx->cnt_stream));
+  DDPPO_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->cnt_stream));
+  for (int i = 0; i < n; ++i) host_vals[i] = ctx->h_cnt[i];
   return DDPPO_OK;
 }

@@ -64,6 +64,8 @@ def _worker(rank, world, port, q):
     out["params2"] = lrn.params.cpu().numpy()
     # ---- a10 counts
     out["counts"] = dd.ddppo_allreduce_counts(ctx, [c["E"] * L, rank + 1]).tolist()
+    # (registered learner: the NVLink exchange; repeated calls cycle its double-buffered slots)
+    out["counts_rep"] = [dd.ddppo_allreduce_counts(ctx, [10 * i + rank, -i]).tolist() for i in range(5)]
     # ---- a9 preemption over NCCL (virtual ticks)
     T = 32
     costs = synth.straggler_costs(7, world, T, lo=1.0, hi=8.0)
@@ -114,6 +116,7 @@ def test_two_rank_learner_step_and_protocols():
             e = np.linalg.norm(dp[off:off + n] - dpo[off:off + n]) / np.linalg.norm(dpo[off:off + n])
             assert e < 5e-2, (key, name, e)
     assert res[0]["counts"] == res[1]["counts"] == [c["E"] * (128 + 40), 3]
+    assert res[0]["counts_rep"] == res[1]["counts_rep"] == [[20 * i + 1, -2 * i] for i in range(5)]
     for r in range(world):
         assert res[r]["L"] == res[r]["L_ref"]
     assert res[0]["ticks"] == res[1]["ticks"]
