@@ -435,6 +435,17 @@ def depth_encoder_macs(arch="depth"):
     return {"all": macs, "stem": stem}
 
 
+def _traffic(*kernels):
+    """DRAM bytes per launch of a kernel from the committed ncu --set full capture summary
+    (profiles/r01_traffic.json, tools/make_traffic.py); None if it was not captured."""
+    try:
+        t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    vals = [t[k]["bytes_per_launch"] for k in kernels if k in t]
+    return sum(vals) if len(vals) == len(kernels) else None
+
+
 def roofline_for(fam, prof, c, lrn, peaks, steps):
     """Algorithmic work of one launch of the dominant family / its mean device time."""
     ms, n = prof[fam]
@@ -450,8 +461,10 @@ def roofline_for(fam, prof, c, lrn, peaks, steps):
         # useful (unpadded) FLOPs; peak = measured sustained bf16 (kind::f16 runs fp16/bf16 at one rate)
         flops = 2.0 * B * T * (3 * H) * (H + (64 if fam == "net_fwd" else 0))
         achieved = flops / per_launch_s / 1e12
+        kern = "gps_gru_fwd_kernel" if fam == "net_fwd" else "gps_gru_bwd_kernel"
         return {"bound": "tensor", "kernel": fam, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": None, "launch_us": per_launch_s * 1e6,
+                "frac": achieved / bf16, "traffic": _traffic(kern), "traffic_kernel": kern,
+                "launch_us": per_launch_s * 1e6,
                 "note": "latency-bound dependency chain (B=2 envs x 128 steps on 16 SMs); per-step phases in "
                         "DESIGN.md sec. 7; HBM kernels' fractions in profiles/r01_microbench.jsonl"}
     if fam in ("net_fwd", "net_bwd") and c["arch"] in ("depth", "rgbd"):
@@ -473,8 +486,9 @@ def roofline_for(fam, prof, c, lrn, peaks, steps):
     byte_per = {"gae": 17.0 * E * T, "loss": 60.0 * B * T, "adam": 32.0 * lrn.P}
     b = byte_per.get(fam, 0.0)
     achieved = b / per_launch_s / 1e9 if b else 0.0
+    traffic = {"adam": _traffic("grad_norm_kernel", "adam_kernel")}.get(fam)
     return {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "launch_us": per_launch_s * 1e6}
+            "frac": achieved / hbm, "traffic": traffic, "launch_us": per_launch_s * 1e6}
 
 
 if __name__ == "__main__":

@@ -14,4 +14,5 @@ ncu --set full --import-source on --clock-control none -k regex:"igemm_kernel|gn
 python bench.py --config rgbd --steps 5 --warmup 3 > gpurun_out/prof/rgbd_bench.json 2>/dev/null
 python tools/kprof.py rgbd 2 > gpurun_out/prof/kprof_rgbd.txt 2>&1
 python tools/microbench.py > gpurun_out/prof/microbench.jsonl 2> gpurun_out/prof/microbench.err
+# then, here: cp the captures into profiles/ and run tools/make_traffic.py + tools/make_summary.py
 echo done
