@@ -133,6 +133,7 @@ struct GpsPtrs {
   float* dGH;    // [S][1536]
   float* U;      // [S][9]     [goal, 1, onehot(prev_action)]
   float* Q;      // [1536][9]  dG_x^T U
+  float* dbhh;   // [1536] b_hh gradient = sum_s dG_h[s], summed by the BPTT kernel (nullable)
   // fused head + PPO loss + head input gradient after the recurrence (learner runtime; on = 0: off)
   struct Loss {
     int on, use_vclip;
@@ -660,6 +661,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
   const int gu = lane, gb = warp;
   const bool gate_warp = warp < B;
   float carry = 0.f;  // dL/dh_t flowing back from step t+1 (already multiplied by mask_{t+1})
+  float sum_r = 0.f, sum_z = 0.f, sum_n = 0.f;  // this (env, unit)'s dG_h summed over t (-> b_hh grad)
   float dH_t = 0.f, h_in = 0.f;
   float4 rzng = make_float4(0.f, 0.f, 0.f, 0.f);
   if (gate_warp) {
@@ -695,6 +697,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
       p.dGH[og] = dr_pre;
       p.dGH[og + kH] = dz_pre;
       p.dGH[og + 2 * kH] = dn_pre * r;
+      sum_r += dr_pre;
+      sum_z += dz_pre;
+      sum_n += dn_pre * r;
       if (t > 0) {
         const size_t o = ((size_t)gb * T_run + t - 1) * kH + c * kUPC + gu;
         dH_t = p.dH[o];
@@ -784,6 +789,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // no CTA exits while a peer could still address its shared memory
+  if (p.dbhh) {
+    // b_hh gradient of the CTA's 96 gate rows: per (env, unit) sums over t, then over envs in order
+    // (the receive buffers are free: every peer has left the recurrence)
+    float* red = &sm.recv[0][0][0][0];  // [B][96]
+    if (gate_warp) {
+      red[gb * kRows + gu] = sum_r;
+      red[gb * kRows + kUPC + gu] = sum_z;
+      red[gb * kRows + 2 * kUPC + gu] = sum_n;
+    }
+    __syncthreads();
+    if (tid < kRows) {
+      float a = 0.f;
+      for (int b = 0; b < B; ++b) a += red[b * kRows + tid];
+      p.dbhh[(tid / kUPC) * kH + c * kUPC + tid % kUPC] = a;
+    }
+  }
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kBwdTmemCols) : "memory");
 }
@@ -1082,6 +1103,7 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
                      bool dh_ready) {
   DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");
   GpsPtrs p = make_ptrs(L, params, b, ws);
+  p.dbhh = grad + layout_offset(L, "rnn.bias_hh");  // summed by the BPTT kernel (no colsum pass)
   const int S = b.B * b.T_run;
   // The recurrence occupies 16 SMs; work off its dependency chain runs beside it on two side
   // streams (fork / join through events on the launching stream).
@@ -1105,7 +1127,8 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   // weight gradients (off the dependency chain), tcgen05 GEMMs over the S samples:
   //   dW_hh[row][j] = sum_s dG_h[s][row] H_in[s][j];  dW_ih[row][j] = sum_s dG_x[s][row] X[s][j]
   //   Q[row][n]     = sum_s dG_x[s][row] U[s][n]   (-> goal FC, embedding and b_ih gradients)
-  // main stream: dW_hh, db_hh; side a: (head weight gradient,) dW_ih; side b: Q, input-layer gradients
+  // main stream: dW_hh; side a: (head weight gradient,) dW_ih; side b: Q, input-layer gradients
+  // (db_hh is summed by the BPTT kernel itself)
   ProfScope ps(ctx, DDPPO_K_WGRAD, st, 2);  // + the 3 GEMMs, counted by launch_gemm_tc
   DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sa));
   DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sb));
@@ -1121,8 +1144,6 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
                                                 grad + layout_offset(L, "goal_fc.bias"),
                                                 grad + layout_offset(L, "act_embed.weight"),
                                                 grad + layout_offset(L, "rnn.bias_ih"));
-  // (b_hh's gradient on the launching stream after dW_hh: the three chains then end within ~1 us)
-  colsum_kernel<<<kG / 32, 256, 0, st>>>(p.dGH, kG, S, kG, grad + layout_offset(L, "rnn.bias_hh"));
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   DDPPO_CUDA_TRY(ctx, fork_to(ctx, sa, st));  // join
   DDPPO_CUDA_TRY(ctx, fork_to(ctx, sb, st));
