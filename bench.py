@@ -165,7 +165,13 @@ def run_reference(args, rank, world):
         return 0
     c = synth.CONFIGS[args.config]
     T_s = ORACLE_T.get(args.config, c["T"])
-    # each "step" is one oracle learner step on a bounded sample of the workload (whole rollouts)
+    # each "step" is one oracle learner step on a bounded sample of the workload (whole rollouts); all of
+    # the host's cores (torchrun exports OMP_NUM_THREADS=1 to every rank; rank 0 runs alone here)
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(limits=cpu_cores())
+    except Exception:
+        limiter = None
     for _ in range(args.warmup if args.warmup < 2 else 1):
         oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=1)
     sps, n, el = oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=args.steps)
@@ -180,6 +186,8 @@ def run_reference(args, rank, world):
                          "kind": "oracle", "sample": f"{n} whole learner steps on {c['E']} envs x {T_s} steps (rank-0 rollout)"},
         "e2e": {"value": sps, "unit": "experience-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if limiter is not None:
+        limiter.restore_original_limits()
     print(json.dumps(out), file=JSON_OUT, flush=True)
     return 0
 
