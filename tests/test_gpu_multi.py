@@ -37,6 +37,8 @@ def _worker(rank, world, port, q):
     dist.broadcast_object_list(obj, src=0)
     ctx = dd.Context(rank, world, obj[0], device=rank)
     out = {}
+    # a10 before any learner is registered: the NCCL path
+    out["counts_nccl"] = dd.ddppo_allreduce_counts(ctx, [rank + 5, 7]).tolist()
     # ---- learner step (gps, one rollout per rank, rank 1 preempted to 40 steps)
     c = synth.CONFIGS["gps"]
     desc = dd.model_desc("gps")
@@ -115,6 +117,7 @@ def test_two_rank_learner_step_and_protocols():
             n = int(np.prod(shape))
             e = np.linalg.norm(dp[off:off + n] - dpo[off:off + n]) / np.linalg.norm(dpo[off:off + n])
             assert e < 5e-2, (key, name, e)
+    assert res[0]["counts_nccl"] == res[1]["counts_nccl"] == [11, 14]
     assert res[0]["counts"] == res[1]["counts"] == [c["E"] * (128 + 40), 3]
     assert res[0]["counts_rep"] == res[1]["counts_rep"] == [[20 * i + 1, -2 * i] for i in range(5)]
     for r in range(world):
