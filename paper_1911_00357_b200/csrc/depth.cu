@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <map>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -651,6 +652,91 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_apply_kernel(const float*
   }
 }
 
+// Large frames, one pass: the S chunks of a frame form a thread-block cluster (S <= 16).  Each CTA
+// stages its chunk (cp.async), computes its per-group sums and per-channel dgamma / dbeta rows, the
+// cluster barrier publishes the group sums, every CTA adds the S of them in CTA order through DSMEM
+// (the same order and arithmetic as gn_bwd_apply_kernel's loop over the chunk partials) and writes
+// dx from the staged chunk: dz / z / y are read from HBM once instead of twice.
+template <int NV>
+__global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_cluster_kernel(const float* __restrict__ dz,
+                                                                     const float* __restrict__ z,
+                                                                     const float* __restrict__ y,
+                                                                     const float* __restrict__ stats,
+                                                                     const float* __restrict__ gamma, int HW, int C,
+                                                                     float* __restrict__ part,
+                                                                     __nv_bfloat16* __restrict__ dx) {
+  __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
+  __shared__ float pc[2][gn_bound(NV)];
+  __shared__ float sm1[kGroups], sm2[kGroups];
+  extern __shared__ __align__(16) float gsm[];
+  const int cap = NV * blockDim.x;
+  float *s_dz = gsm, *s_z = gsm + cap, *s_y = gsm + 2 * cap;
+  const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C), c = threadIdx.x % C, cg = C / kGroups,
+            g = c / cg;
+  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
+  const size_t base = (size_t)f * n;
+  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, e0, e1, cap);
+  const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
+  double a1 = 0.0, a2 = 0.0;
+  float pg = 0.f, pb = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    if (e0 + e >= e1) break;
+    float d = s_dz[e];
+    if (z && s_z[e] <= 0.f) d = 0.f;
+    const float xh = (s_y[e] - mu) * rs, dxh = d * gm;
+    a1 += dxh;
+    a2 += (double)dxh * xh;
+    pg += d * xh;
+    pb += d;
+  }
+  pc[0][threadIdx.x] = pg;
+  pc[1][threadIdx.x] = pb;
+  gn_group_reduce(a1, a2, C, sa, sb, ga, gb);  // ga / gb: this chunk's group sums (its barriers publish pc)
+  if (threadIdx.x < C) {
+    float rg = 0.f, rb = 0.f;
+    for (int t = threadIdx.x; t < (int)blockDim.x; t += C) {
+      rg += pc[0][t];
+      rb += pc[1][t];
+    }
+    const size_t row = (size_t)f * S + blockIdx.x;  // rows of the dgamma / dbeta reduction
+    part[(row * C + threadIdx.x) * 2] = rg;
+    part[(row * C + threadIdx.x) * 2 + 1] = rb;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (threadIdx.x < kGroups) {
+    double a = 0.0, b = 0.0;
+    const uint32_t la = (uint32_t)__cvta_generic_to_shared(&ga[threadIdx.x]),
+                   lb = (uint32_t)__cvta_generic_to_shared(&gb[threadIdx.x]);
+    for (int r = 0; r < S; ++r) {
+      uint32_t ra, rb2;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(r));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb2) : "r"(lb), "r"(r));
+      double va, vb;
+      asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(va) : "r"(ra) : "memory");
+      asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(vb) : "r"(rb2) : "memory");
+      a += va;
+      b += vb;
+    }
+    const double cnt = (double)HW * cg;
+    sm1[threadIdx.x] = (float)(a / cnt);
+    sm2[threadIdx.x] = (float)(b / cnt);
+  }
+  // every CTA has read every peer's group sums before any CTA leaves (or rewrites ga / gb)
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  const float m1 = sm1[g], m2 = sm2[g];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    if (e0 + e >= e1) break;
+    float d = s_dz[e];
+    if (z && s_z[e] <= 0.f) d = 0.f;
+    const float xh = (s_y[e] - mu) * rs;
+    dx[base + e0 + e] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
+  }
+}
+
 // dgamma[c], dbeta[c] = sums over frames (in frame order, blocked: thread t takes frames t, t+256,
 // ...; then the fixed-order block reduction) of the per-frame partials
 __global__ void __launch_bounds__(kThreads) gn_param_reduce_kernel(const float* __restrict__ part, int F, int C,
@@ -1271,6 +1357,45 @@ static ddppo_status gn_smem_attr(ddppo_ctx* ctx, K kernel, size_t bytes) {
   return DDPPO_OK;
 }
 
+// cluster launch of gn_bwd_cluster_kernel (S CTAs per frame); *done = false if clusters of S such CTAs
+// cannot be resident (the caller falls back to the two-kernel path)
+template <typename K>
+static ddppo_status gn_bwd_cluster(ddppo_ctx* ctx, K kern, int S, int F, int nt, size_t smem, const float* dz,
+                                   const float* relu_z, const float* y, const float* stats, const float* gamma,
+                                   int HW, int C, float* part, __nv_bfloat16* dy, cudaStream_t st, bool* done) {
+  static std::map<std::pair<const void*, int>, bool> ok_cache;
+  *done = false;
+  ddppo_status s = gn_smem_attr(ctx, kern, smem);
+  if (s != DDPPO_OK) return s;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(S, F, 1);
+  cfg.blockDim = dim3(nt, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), S);
+  auto it = ok_cache.find(key);
+  if (it == ok_cache.end()) {
+    bool ok = true;
+    if (S > 8) ok = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    int nclus = 0;
+    ok = ok && cudaOccupancyMaxActiveClusters(&nclus, kern, &cfg) == cudaSuccess && nclus > 0;
+    cudaGetLastError();
+    it = ok_cache.emplace(key, ok).first;
+  }
+  if (!it->second) return DDPPO_OK;
+  DDPPO_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, dz, relu_z, y, stats, gamma, HW, C, part, dy));
+  ctx->count(1);
+  *done = true;
+  return DDPPO_OK;
+}
+
 ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const float* relu_z, const float* y,
                     const float* stats, const float* gamma, __nv_bfloat16* dy, float* dgamma, float* dbeta,
                     float* part, double* gpart, cudaStream_t st, bool reduce_params = true) {
@@ -1305,11 +1430,23 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
     gn_bwd_apply_kernel<NV><<<dim3(S, F), nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, gpart, \
                                                                         HW, C, dy);                         \
   } while (0)
-    if (nt == 1024) GN_BWD2(8);
-    else if (nt == 512) GN_BWD2(16);
-    else GN_BWD2(32);
+    bool done = false;
+    if (S <= 16) {  // one pass: the frame's chunks as a thread-block cluster
+#define GN_BWDC(NV) s = gn_bwd_cluster(ctx, gn_bwd_cluster_kernel<NV>, S, F, nt, gn_bwd_smem(NV, nt), dz, relu_z, y, \
+                                      stats, gamma, HW, C, part, dy, st, &done)
+      if (nt == 1024) GN_BWDC(8);
+      else if (nt == 512) GN_BWDC(16);
+      else GN_BWDC(32);
+#undef GN_BWDC
+      if (s != DDPPO_OK) return s;
+    }
+    if (!done) {
+      if (nt == 1024) GN_BWD2(8);
+      else if (nt == 512) GN_BWD2(16);
+      else GN_BWD2(32);
+      ctx->count(2);
+    }
 #undef GN_BWD2
-    ctx->count(2);
   }
   if (reduce_params) {  // else the caller reduces `part` later (gn_param_reduce_all)
     gn_param_reduce_kernel<<<C, kThreads, 0, st>>>(part, F * S, C, dgamma, dbeta);
