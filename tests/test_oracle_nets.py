@@ -126,8 +126,9 @@ def test_model_gradients_finite_differences_and_torch():
             assert abs(fd - g[i]) < 1e-7 * max(1.0, abs(fd)), (arch, i, fd, g[i])
 
 
-def test_learner_equal_buffers_two_ranks_equals_one_rank_and_equal_weighting():
-    """N=2 with identical buffers == N=1; unequal lengths -> mean of per-rank grads."""
+def test_learner_equal_buffers_two_ranks_equals_one_rank():
+    """N=2 with identical buffers == N=1.  The weighting itself is pinned by
+    test_learner_composition_matches_torch_ddp_objective."""
     H = 8
     ent, P = _entries("gps", H)
     p0 = synth.init_params(ent, P, 0)
@@ -144,3 +145,76 @@ def test_learner_equal_buffers_two_ranks_equals_one_rank_and_equal_weighting():
     # both ranks' grads are computed at the same params; the update used their plain mean
     assert tr[0]["rank"] == 0 and tr[1]["rank"] == 1
     assert np.array_equal(tr[0]["params"], tr[1]["params"])
+
+
+def _torch_ppo_mean(z, v, act, lpo, vo, R, A, eps=0.2, c_v=0.5, c_e=0.01):
+    """Eq. 2 + Z3/Z4 written in torch: the per-worker mean over its valid samples."""
+    logp = torch.log_softmax(z, dim=1)
+    lp = logp.gather(1, act[:, None])[:, 0]
+    rho = torch.exp(lp - lpo)
+    surr = torch.minimum(rho * A, torch.clamp(rho, 1 - eps, 1 + eps) * A)
+    vc = vo + torch.clamp(v - vo, -eps, eps)
+    lv = 0.5 * torch.maximum((v - R) ** 2, (vc - R) ** 2)
+    ent = -(logp.exp() * logp).sum(1)
+    return -surr.mean() + c_v * lv.mean() - c_e * ent.mean()
+
+
+def test_learner_composition_matches_torch_ddp_objective():
+    """Pins oracle.learner_step's cross-rank composition against an independent torch construction:
+    toy actor-critic (R2) built from torch.nn.Linear, the DD-PPO objective (1/N) sum_r mean_r(loss)
+    (P:L171 equal worker weighting; Eq. 3/4 gradient mean), advantages normalised with statistics
+    of the concatenated valid entries of all ranks (Z2, torch.std unbiased), global-norm clip 0.5 on
+    the averaged gradient (Z15, torch.nn.utils.clip_grad_norm_), torch.optim.Adam (Z14) stepping
+    once per minibatch.  Unequal lengths (12 vs 5) make per-sample and per-rank weighting differ;
+    two minibatches x two epochs exercise the Adam step index."""
+    E, T = 4, 12
+    ent, P = _entries("toy", 512)
+    p0 = synth.init_params(ent, P, 11)
+    ros = [synth.rollout(E, T, 21, rank=0, hidden=8), synth.rollout(E, T, 21, rank=1, hidden=8, length=[5, 12, 3, 7])]
+    pms = [synth.perms(4, 0, 2, E, rank=r) for r in range(2)]
+    po, _, _, step, info = learner.learner_step("toy", p0, np.zeros(P), np.zeros(P), 0, ros, pms, dict(epochs=2),
+                                                hidden=8)
+    assert step == 4
+    # global advantage statistics == one rank holding the concatenation of every valid entry (Z2)
+    from oracle import gae as ogae
+    advs = [ogae.gae(ro["rew"], ro["val"], ro["done"], ro["length"], 0.99, 0.95) for ro in ros]
+    cat = np.concatenate([a[np.arange(a.shape[1])[None, :] < np.asarray(ro["length"])[:, None]]
+                          for (a, _), ro in zip(advs, ros)])
+    assert info["adv_stats"][2] == cat.size == 12 * 4 + 5 + 12 + 3 + 7
+    ct = torch.tensor(cat)
+    mu, sd = float(ct.mean()), float(ct.std(unbiased=True))
+    assert abs(info["mean_invstd"][0] - mu) < 1e-12 and abs(1.0 / info["mean_invstd"][1] - (sd + 1e-5)) < 1e-12
+    # the torch DD-PPO learner
+    fc1, head = torch.nn.Linear(3, 64).double(), torch.nn.Linear(64, 5).double()
+    lay = {n: (off, shape) for (n, shape, _), off in zip(models.layout("toy"), [e[0] for e in ent])}
+    with torch.no_grad():
+        for mod, pre in ((fc1, "fc1"), (head, "head")):
+            for attr in ("weight", "bias"):
+                off, shape = lay[pre + "." + attr]
+                getattr(mod, attr).copy_(_t(p0[off:off + int(np.prod(shape))].reshape(shape)))
+    prm = list(fc1.parameters()) + list(head.parameters())
+    opt = torch.optim.Adam(prm, lr=2.5e-4, betas=(0.9, 0.999), eps=1e-8)
+    for e in range(2):
+        for j in range(2):
+            opt.zero_grad()
+            tot = 0.0
+            for r, ro in enumerate(ros):
+                envs = pms[r][e][j * 2:(j + 1) * 2]
+                sel = [(n, t) for n in envs for t in range(int(ro["length"][n]))]
+                ni, ti = np.array([s[0] for s in sel]), np.array([s[1] for s in sel])
+                out = head(torch.tanh(fc1(_t(ro["goal"][ni, ti]))))
+                A, R = advs[r]
+                An = (_t(A[ni, ti]) - mu) / (sd + 1e-5)
+                tot = tot + _torch_ppo_mean(out[:, :4], out[:, 4], torch.tensor(ro["action"][ni, ti].astype(np.int64)),
+                                            _t(ro["logp_old"][ni, ti]), _t(ro["val"][ni, ti]), _t(R[ni, ti]), An)
+            (tot / 2).backward()
+            torch.nn.utils.clip_grad_norm_(prm, 0.5)
+            opt.step()
+    mine = {n: po[off:off + int(np.prod(s))].reshape(s) for n, (off, s) in lay.items()}
+    for mod, pre in ((fc1, "fc1"), (head, "head")):
+        for attr in ("weight", "bias"):
+            ref = getattr(mod, attr).detach().numpy()
+            d = mine[pre + "." + attr] - ref
+            assert np.max(np.abs(d)) < 1e-10, (pre, attr, np.max(np.abs(d)))
+    # and the update is not trivially zero
+    assert np.max(np.abs(po - p0)) > 1e-4
