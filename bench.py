@@ -236,7 +236,7 @@ def main():
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, args.seed)
-    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, normalize_adv=True)
     stream = torch.cuda.current_stream()
     n_roll = 4  # distinct rollouts cycled through (different data every step)
     preempt = None

@@ -277,6 +277,30 @@ ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int
  * allocated while the context lives.  World size 1: no-op.  At most one workspace per context. */
 ddppo_status ddppo_learner_register(ddppo_ctx* ctx, void* ws, size_t ws_bytes);
 
+/* Layout agreement at rendezvous ("layout is identical across all workers ... checked at
+ * rendezvous by exchanging a layout hash"; S:L329 length mismatch -> fatal protocol error).
+ * ddppo_layout_hash (pure host): 64-bit FNV-1a over the flat parameter layout of desc (every tensor's
+ * name, offset, numel, shape, in order) and the learner geometry (E, T, ld, minibatches, epochs).
+ * ddppo_layout_check (collective): all-gathers every rank's hash over NCCL; DDPPO_ERR_PROTOCOL (on
+ * every rank, ddppo_last_error lists the disagreeing ranks) if any differs.  World size 1: OK. */
+ddppo_status ddppo_layout_hash(const ddppo_model_desc* host_desc, int E, int T, int ld, int minibatches,
+                               int epochs, uint64_t* host_hash);
+ddppo_status ddppo_layout_check(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, int E, int T, int ld,
+                                int minibatches, int epochs);
+
+/* a8 over peer memory (after ddppo_learner_register), Eq. 3:
+ *   DDPPO_A8_SHARDED (default): reduce-scatter -> clip + Adam on this rank's 1/N shard -> all-gather
+ *     (NEXT-2; rank r owns float4 units [Q*r/N, Q*(r+1)/N) of the flat vector, Q = P/4, the last
+ *     rank also the P%4 tail).  NVLink volume 2(N-1)/N*4P per rank.  Parameters stay bit-identical
+ *     on all ranks; Adam's m / v are only maintained on the owned shard (ZeRO-1).
+ *   DDPPO_A8_ALLREAD: every rank reads all N gradients and runs the full Adam ((N-1)*4P bytes).
+ * Both sum the N gradients in rank order 0..N-1 (identical per-element sums).  Any wait on a peer is
+ * bounded (30 s of %globaltimer): on timeout the exchange leaves params / m / v untouched and
+ * ddppo_check returns DDPPO_ERR_COMM (fatal).  Host-side setting, read when a learner step
+ * is built (graphs are keyed by it). */
+typedef enum { DDPPO_A8_SHARDED = 0, DDPPO_A8_ALLREAD = 1 } ddppo_a8_mode;
+ddppo_status ddppo_set_a8_mode(ddppo_ctx* ctx, int mode);
+
 /* CUDA graphs for ddppo_learner_step (default on): the step is captured once per (configuration,
  * buffer addresses, minibatch shapes) -- after one eager run of a new configuration -- and
  * replayed; Adam's update count and the peer-barrier epoch are kept on the device so nothing
@@ -341,6 +365,22 @@ ddppo_status ddppo_debug_groupnorm(ddppo_ctx* ctx, const float* y, const float* 
 ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
                                          const ddppo_batch* host_batch, void* ws, uint8_t* out, int64_t cap,
                                          int64_t* host_n, void* stream);
+/* Single-device emulation of the peer-memory a8 over N in 1..8 ranks (tests): host_grads[r],
+ * host_params[r], host_m[r], host_v[r], host_gsum[r] are device buffers of P floats for emulated rank
+ * r; the exchange runs exactly the kernels of the multi-GPU path (barrier as N warps of one block,
+ * then each phase rank by rank), with the flag areas and staged shards in `scratch`.
+ * host_cfg->step = 1-based Adam step.  Outputs: params/m/v (m/v: owned shard only in SHARDED mode)
+ * and gsum (rank-ordered gradient sum; SHARDED: the owned shard only).  scratch == NULL: *host_need. */
+ddppo_status ddppo_debug_peer_a8(ddppo_ctx* ctx, int N, int mode, float* const* host_grads,
+                                 float* const* host_params, float* const* host_m, float* const* host_v,
+                                 int64_t P, const ddppo_adam_cfg* host_cfg, float* const* host_gsum,
+                                 void* scratch, size_t scratch_bytes, size_t* host_need, void* stream);
+/* Single-device emulation of the a10 peer counts exchange (the kernel of ddppo_allreduce_counts
+ * once a learner is registered) over N ranks as N co-resident blocks (cooperative launch):
+ * host_out[r*n + i] = sum over ranks (rank order) of host_vals[j*n + i].  Blocking. */
+ddppo_status ddppo_debug_peer_counts(ddppo_ctx* ctx, int N, const int64_t* host_vals, int n,
+                                     int64_t* host_out, void* scratch, size_t scratch_bytes,
+                                     size_t* host_need);
 /* 3x3 / stride 2 / pad 1 max pool (first maximum in window order; arg = window index 0..8).
    x [F][H][W][C] channels-last, C % 4 == 0 (else DDPPO_ERR_CONFIG); y / arg [F][Ho][Wo][C]. */
 ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int F, int H, int W, int C, float* y,

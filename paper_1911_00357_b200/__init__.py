@@ -272,3 +272,55 @@ def ddppo_learner_step(ctx, desc, ro, cfg, params, m, v, adv, ret, stats_out, ws
           f32(v), f32(adv), f32(ret), f32(stats_out), dptr(ws), ws.numel() * ws.element_size(),
           ctypes.byref(step), _stream(stream))
     return step.value
+
+
+def ddppo_set_a8_mode(ctx, mode):
+    """"sharded" (reduce-scatter -> shard Adam -> all-gather, default) or "allread" (v1)."""
+    _call(ctx, "ddppo_set_a8_mode", {"sharded": _lib.A8_SHARDED, "allread": _lib.A8_ALLREAD}.get(mode, mode))
+
+
+def _ptr_array(ts):
+    arr = (ctypes.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = f32(t)
+    return arr
+
+
+def ddppo_debug_peer_a8(ctx, mode, grads, params, m, v, cfg, gsum, stream=None):
+    """Single-device emulation of the peer-memory a8 over N = len(grads) ranks (lists of [P] tensors)."""
+    import torch
+    mode = {"sharded": _lib.A8_SHARDED, "allread": _lib.A8_ALLREAD}.get(mode, mode)
+    N, P = len(grads), params[0].numel()
+    arrs = [_ptr_array(x) for x in (grads, params, m, v, gsum)]
+    need = ctypes.c_size_t()
+    _call(ctx, "ddppo_debug_peer_a8", N, mode, *arrs[:4], P, ctypes.byref(cfg), arrs[4], None, 0,
+          ctypes.byref(need), _stream(stream))
+    scratch = torch.empty(need.value, dtype=torch.uint8, device=params[0].device)
+    _call(ctx, "ddppo_debug_peer_a8", N, mode, *arrs[:4], P, ctypes.byref(cfg), arrs[4], dptr(scratch),
+          need.value, None, _stream(stream))
+    return scratch
+
+
+def ddppo_debug_peer_counts(ctx, vals):
+    """vals [N][n] int64 -> [N][n]: each emulated rank's rank-ordered sums (blocking)."""
+    import torch
+    v = np.ascontiguousarray(np.asarray(vals, dtype=np.int64))
+    N, n = v.shape
+    out = np.zeros_like(v)
+    need = ctypes.c_size_t()
+    _call(ctx, "ddppo_debug_peer_counts", N, v.ctypes.data, n, out.ctypes.data, None, 0, ctypes.byref(need))
+    scratch = torch.empty(need.value, dtype=torch.uint8, device=f"cuda:{ctx.device}")
+    _call(ctx, "ddppo_debug_peer_counts", N, v.ctypes.data, n, out.ctypes.data, dptr(scratch), need.value, None)
+    return out
+
+
+def ddppo_layout_hash(desc, E, T, ld, minibatches, epochs):
+    h = ctypes.c_uint64()
+    check("ddppo_layout_hash", lib.ddppo_layout_hash(ctypes.byref(desc), E, T, ld, minibatches, epochs,
+                                                     ctypes.byref(h)))
+    return h.value
+
+
+def ddppo_layout_check(ctx, desc, E, T, ld, minibatches, epochs):
+    """Collective: DdppoError(protocol) unless every rank has the same layout hash."""
+    _call(ctx, "ddppo_layout_check", ctypes.byref(desc), E, T, ld, minibatches, epochs)

@@ -22,6 +22,7 @@ c_i32, c_size = ctypes.c_int32, ctypes.c_size_t
 
 STATUS = {0: "ok", 1: "config", 2: "numerical", 3: "protocol", 4: "comm", 5: "cuda", 6: "unsupported"}
 ARCH_TOY, ARCH_GPS, ARCH_DEPTH, ARCH_RGBD = 0, 1, 2, 3
+A8_SHARDED, A8_ALLREAD = 0, 1
 
 
 class DdppoError(RuntimeError):
@@ -113,6 +114,12 @@ _SIGS = {
     "ddppo_debug_depth_decisions": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "ddppo_learner_register": (c_int, [c_vp, c_vp, ctypes.c_size_t]),
     "ddppo_set_graphs": (c_int, [c_vp, c_int]),
+    "ddppo_set_a8_mode": (c_int, [c_vp, c_int]),
+    "ddppo_layout_hash": (c_int, [P_(ModelDesc), c_int, c_int, c_int, c_int, c_int, P_(ctypes.c_uint64)]),
+    "ddppo_layout_check": (c_int, [c_vp, P_(ModelDesc), c_int, c_int, c_int, c_int, c_int]),
+    "ddppo_debug_peer_a8": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_i64, P_(AdamCfg), c_vp, c_vp,
+                                    c_size, P_(c_size), c_vp]),
+    "ddppo_debug_peer_counts": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_size, P_(c_size)]),
     "ddppo_debug_maxpool": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 KERNEL_FAMILIES = ("gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other")

@@ -44,21 +44,17 @@ grad_norm_kernel(const float* __restrict__ g, int64_t P, float inv_world, float 
   }
 }
 
-__device__ __forceinline__ void adam_one(float& p, float& m, float& v, float g, float b1, float b2, float step_size,
-                                         float inv_sqrt_bc2, float eps) {
-  m = b1 * m + (1.f - b1) * g;
-  v = b2 * v + (1.f - b2) * g * g;
-  const float denom = sqrtf(v) * inv_sqrt_bc2 + eps;
-  p = p - step_size * (m / denom);
-}
 
 // step = (dstep ? *dstep : 0) + step_add (the learner runtime keeps the update count on the device, so
 // a captured CUDA graph needs no host-side scalar); bias corrections in fp64 once per block
 __global__ void __launch_bounds__(kThreads)
 adam_kernel(const float* __restrict__ g, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
             const uint8_t* __restrict__ freeze, int64_t P, const float* __restrict__ scalars, float b1, float b2,
-            float lr, const int* __restrict__ dstep, int step_add, float eps) {
+            float lr, const int* __restrict__ dstep, int step_add, float eps, const int* err) {
   __shared__ float sbc[2];
+  // a failed peer exchange (ERR_BIT_COMM) or a non-finite gradient norm (ERR_BIT_GRAD) leaves
+  // the parameters untouched until ddppo_check reports it
+  if (err && (*(volatile const int*)err & (ERR_BIT_COMM | ERR_BIT_GRAD))) return;
   if (threadIdx.x == 0) {
     const int step = (dstep ? *dstep : 0) + step_add;
     const double bc1 = 1.0 - pow((double)b1, (double)step), bc2 = 1.0 - pow((double)b2, (double)step);
@@ -111,7 +107,7 @@ ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, 
   const int blocks = grid_for((int)std::min<int64_t>((P + 3) / 4, 1 << 30), kThreads, ctx->sm_count * 4);
   ProfScope ps(ctx, DDPPO_K_ADAM, st, 1);
   adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
-                                           cfg.lr, dstep, step_add, cfg.eps);
+                                           cfg.lr, dstep, step_add, cfg.eps, ctx->d_err);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
@@ -130,7 +126,7 @@ ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float*
                                                 ctx->d_counters + CNT_NORM, ctx->d_scalars, grad_norm, ctx->d_err);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
-                                           cfg.lr, dstep, step_add, cfg.eps);
+                                           cfg.lr, dstep, step_add, cfg.eps, ctx->d_err);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }

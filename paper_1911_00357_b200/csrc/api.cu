@@ -117,8 +117,10 @@ ddppo_status ddppo_check(ddppo_ctx* ctx, void* stream) {
   int err = 0;
   DDPPO_CUDA_TRY(ctx, cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err & ERR_BIT_COMM) {
+    // the exchange left parameters untouched; counters of kernels that returned early are reset
     DDPPO_CUDA_TRY(ctx, cudaMemset(ctx->d_err, 0, sizeof(int)));
-    ctx->last_error = "peer barrier timed out (a rank did not reach the gradient exchange)";
+    DDPPO_CUDA_TRY(ctx, cudaMemset(ctx->d_counters, 0, CNT_NUM * sizeof(unsigned int)));
+    ctx->last_error = "peer exchange timed out (a rank did not reach the gradient exchange)";
     return DDPPO_ERR_COMM;
   }
   if (err) {
@@ -323,6 +325,7 @@ struct LearnerWs {
   float* grad;      // this minibatch's gradient (one of grad2[], by minibatch parity when peers are used)
   float* grad2[2];
   float* gsum;      // rank-ordered sum of all ranks' gradients (peer path)
+  float* pgather;   // this rank's updated parameter shard, read by the peers (sharded a8)
   float* grad_norm;
   void* model_ws;
   size_t model_bytes;
@@ -350,6 +353,7 @@ size_t carve_learner(const ddppo_model_desc* d, int E, int T, int mb, void* base
   t.grad2[1] = (float*)take((size_t)P * sizeof(float));
   t.grad = t.grad2[0];
   t.gsum = (float*)take((size_t)P * sizeof(float));
+  t.pgather = (float*)take((size_t)P * sizeof(float));
   t.grad_norm = (float*)take(8 * sizeof(float));
   t.model_ws = take(model_bytes);
   t.model_bytes = model_bytes;
@@ -365,6 +369,57 @@ ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int
       ld < T + 1 || epochs < 1)
     return DDPPO_ERR_CONFIG;
   *host_bytes = carve_learner(host_desc, E, T, minibatches, nullptr, nullptr);
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_layout_hash(const ddppo_model_desc* host_desc, int E, int T, int ld, int minibatches, int epochs,
+                               uint64_t* host_hash) {
+  ModelLayout L;
+  if (!host_hash || build_layout(host_desc, &L) != DDPPO_OK) return DDPPO_ERR_CONFIG;
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* c = reinterpret_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+  };
+  for (int i = 0; i < L.n; ++i) {
+    const ddppo_tensor_info& t = L.t[i];
+    mix(t.name, strnlen(t.name, sizeof(t.name)));
+    mix(&t.offset, sizeof(t.offset));
+    mix(&t.numel, sizeof(t.numel));
+    mix(&t.ndim, sizeof(t.ndim));
+    mix(t.shape, sizeof(int64_t) * (size_t)t.ndim);
+  }
+  const int32_t geo[5] = {E, T, ld, minibatches, epochs};
+  mix(geo, sizeof(geo));
+  *host_hash = h;
+  return DDPPO_OK;
+}
+
+ddppo_status ddppo_layout_check(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, int E, int T, int ld,
+                                int minibatches, int epochs) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  uint64_t h = 0;
+  DDPPO_REQUIRE(ctx, ddppo_layout_hash(host_desc, E, T, ld, minibatches, epochs, &h) == DDPPO_OK,
+                "layout_check: bad model descriptor");
+  if (ctx->world == 1) return DDPPO_OK;
+  uint64_t* d = nullptr;
+  DDPPO_CUDA_TRY(ctx, cudaMalloc(&d, sizeof(uint64_t) * ctx->world));
+  std::vector<uint64_t> all(ctx->world);
+  ncclResult_t nr = ncclSuccess;
+  cudaError_t ce = cudaMemcpy(d + ctx->rank, &h, sizeof(h), cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) nr = ncclAllGather(d + ctx->rank, d, 1, ncclUint64, ctx->comm, 0);
+  if (ce == cudaSuccess && nr == ncclSuccess)
+    ce = cudaMemcpy(all.data(), d, sizeof(uint64_t) * ctx->world, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  DDPPO_CUDA_TRY(ctx, ce);
+  DDPPO_NCCL_TRY(ctx, nr);
+  std::string bad;
+  for (int r = 0; r < ctx->world; ++r)
+    if (all[r] != all[0]) bad += " " + std::to_string(r);
+  if (!bad.empty()) {
+    ctx->last_error = "layout hash differs from rank 0's on rank(s)" + bad;
+    return DDPPO_ERR_PROTOCOL;
+  }
   return DDPPO_OK;
 }
 
@@ -454,10 +509,13 @@ ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_mode
       if (use_peers) {  // a8 over NVLink peer memory: rank-ordered sum + clip norm, then Adam
         ProfScope ps(ctx, DDPPO_K_ALLREDUCE, st, 0);
         float* peers[kMaxPeers];
-        const size_t off = (size_t)((char*)w.grad - (char*)ws);
-        for (int r = 0; r < ctx->world; ++r) peers[r] = reinterpret_cast<float*>(ctx->peer_ws_base[r] + off);
-        s = launch_peer_reduce_norm(ctx, peers, w.gsum, L.P, acfg.max_grad_norm, nullptr, st);
-        if (s == DDPPO_OK) s = launch_adam_only(ctx, w.gsum, params, m, v, nullptr, L.P, acfg, ctx->d_step, k + 1, st);
+        float* pgs[kMaxPeers];
+        const size_t off = (size_t)((char*)w.grad - (char*)ws), off_pg = (size_t)((char*)w.pgather - (char*)ws);
+        for (int r = 0; r < ctx->world; ++r) {
+          peers[r] = reinterpret_cast<float*>(ctx->peer_ws_base[r] + off);
+          pgs[r] = reinterpret_cast<float*>(ctx->peer_ws_base[r] + off_pg);
+        }
+        s = launch_peer_a8(ctx, peers, pgs, w.gsum, params, m, v, L.P, acfg, ctx->d_step, k + 1, st);
       } else {
         if (ctx->world > 1) {
           ProfScope ps(ctx, DDPPO_K_ALLREDUCE, st, 0);
@@ -509,6 +567,13 @@ void destroy_graph_cache(ddppo_ctx* ctx) {
 
 extern "C" {
 
+ddppo_status ddppo_set_a8_mode(ddppo_ctx* ctx, int mode) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, mode == DDPPO_A8_SHARDED || mode == DDPPO_A8_ALLREAD, "set_a8_mode: unknown mode");
+  ctx->a8_mode = mode;
+  return DDPPO_OK;
+}
+
 ddppo_status ddppo_set_graphs(ddppo_ctx* ctx, int enable) {
   if (!ctx) return DDPPO_ERR_CONFIG;
   ctx->graphs = enable != 0;
@@ -527,6 +592,8 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
   DDPPO_REQUIRE(ctx, cfg->minibatches >= 1 && ro->E % cfg->minibatches == 0 && cfg->epochs >= 1,
                 "learner_step: minibatches must divide E (S:L155)");
   DDPPO_REQUIRE(ctx, cfg->adam.step >= 0, "learner_step: adam.step must be >= 0");
+  DDPPO_REQUIRE(ctx, (cfg->normalize_adv != 0) == (cfg->loss.normalize_adv != 0),
+                "learner_step: normalize_adv and loss.normalize_adv must agree");
   const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
   DDPPO_REQUIRE(ctx, !visual || (ro->obs && ro->c0), "learner_step: the visual agents need obs and c0");
   size_t need = 0;
@@ -583,6 +650,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
                           (const void*)stats_out, (const void*)ws})
       key_put(key, p);
     key_put(key, use_peers);
+    key_put(key, ctx->a8_mode);
     key_put(key, (int)(mb0 & 1));
     for (const MbShape& sh : mbs) key_put(key, sh);
     if (!ctx->graph) {

@@ -35,6 +35,7 @@ struct ddppo_ctx {
   cudaStream_t cnt_stream = nullptr;     // its own non-blocking stream: not queued behind learner work
   int64_t* h_cnt = nullptr;              // pinned host result
   uint64_t peer_mb = 0;
+  int a8_mode = DDPPO_A8_SHARDED;       // ddppo_set_a8_mode
   // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step
   int* d_step = nullptr;
   int64_t step_expected = -1;       // value *d_step will hold once the enqueued work has run
@@ -159,6 +160,15 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// One Adam element (PyTorch form; step_size = lr / (1 - b1^t), inv_sqrt_bc2 = 1 / sqrt(1 - b2^t))
+__device__ __forceinline__ void adam_one(float& p, float& m, float& v, float g, float b1, float b2, float step_size,
+                                         float inv_sqrt_bc2, float eps) {
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  const float denom = sqrtf(v) * inv_sqrt_bc2 + eps;
+  p = p - step_size * (m / denom);
+}
+
 // Deterministic block reduction of NV doubles per thread; result valid in thread 0.
 // smem must hold NV * (blockDim/32) doubles.
 template <int NV>
@@ -280,8 +290,11 @@ ddppo_status peer_setup_flags(ddppo_ctx* ctx);
 // sum of n <= kMaxCountVals int64 over the ranks (rank order) through the peer flag areas, on the
 // context's own stream (host-blocking on that stream only)
 ddppo_status peer_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n);
-ddppo_status launch_peer_reduce_norm(ddppo_ctx* ctx, float* const* peers, float* gsum, int64_t P, float max_norm,
-                                     float* grad_norm, cudaStream_t st);
+// a8 of one minibatch over peer memory (ctx->a8_mode): peers[j] = rank j's gradient, pgs[j] = rank j's
+// staged-shard buffer (both as mapped here); gsum scratch [P]; Adam step = *dstep + step_add
+ddppo_status launch_peer_a8(ddppo_ctx* ctx, float* const* peers, float* const* pgs, float* gsum, float* params,
+                            float* m, float* v, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep, int step_add,
+                            cudaStream_t st);
 // Adam on an already summed gradient whose clip scale is in ctx->d_scalars[0] (adam.cu)
 ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, float* m, float* v,
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep,

@@ -9,7 +9,7 @@ import ctypes
 import numpy as np
 import torch
 
-from . import (Rollout, adam_cfg, ddppo_learner_register, ddppo_learner_step, ddppo_preempt_poll,
+from . import (Rollout, adam_cfg, ddppo_layout_check, ddppo_learner_register, ddppo_learner_step, ddppo_preempt_poll,
                learner_workspace_size, learner_cfg,
                loss_cfg, model_desc, param_count, param_layout, preempt_cfg)
 
@@ -22,8 +22,10 @@ OBS_SHAPES = {2: (1, 64, 64), 3: (4, 256, 256)}  # Depth (configs[2]) / RGB-D (c
 
 
 class Learner:
+    """normalize_adv defaults to the paper's setting (off); north_star's hot path (bench.py)
+    turns it on explicitly."""
     def __init__(self, ctx, arch, E, T, epochs=2, minibatches=2, hidden=None, params=None, device="cuda",
-                 normalize_adv=True, use_value_clip=True, lr=2.5e-4, max_grad_norm=0.5, ld=None, adam_eps=1e-8,
+                 normalize_adv=False, use_value_clip=True, lr=2.5e-4, max_grad_norm=0.5, ld=None, adam_eps=1e-8,
                  peer=True):
         self.ctx, self.E, self.T = ctx, E, T
         self.ld = ld or ((T + 1 + 3) // 4 * 4)
@@ -44,8 +46,10 @@ class Learner:
                                adam=adam_cfg(0, lr=lr, eps=adam_eps, max_grad_norm=max_grad_norm))
         wsb = learner_workspace_size(self.desc, E, T, self.ld, minibatches, epochs)
         self.ws = torch.empty(wsb // 4 + 64, **f32)
-        if peer and getattr(ctx, "world", 1) > 1:
-            ddppo_learner_register(ctx, self.ws)  # a8 over NVLink peer memory (collective)
+        if getattr(ctx, "world", 1) > 1:
+            ddppo_layout_check(ctx, self.desc, E, T, self.ld, minibatches, epochs)  # S:L26 (collective)
+            if peer:
+                ddppo_learner_register(ctx, self.ws)  # a8 over NVLink peer memory (collective)
         ld = self.ld
         self.rnn_layers = 2 if self.desc.arch == 3 else 1  # DDPPO_ARCH_RGBD_R50_LSTM2: 2 LSTM layers
         hs = self.rnn_layers * self.hidden

@@ -67,3 +67,13 @@ def test_preempt_threshold_and_decide_match_oracle():
     assert dd.ddppo_preempt_threshold(dd.preempt_cfg(60, 128, min_steps=10), 4) == (3, 10)
     with pytest.raises(dd.DdppoError):
         dd.ddppo_preempt_threshold(dd.preempt_cfg(0, 128), 4)
+
+
+def test_layout_hash_distinguishes_configs():
+    """the rendezvous layout hash must change with the model and with the learner geometry."""
+    base = dict(E=4, T=128, ld=132, minibatches=2, epochs=2)
+    h = {arch: dd.ddppo_layout_hash(dd.model_desc(arch), **base) for arch in ("toy", "gps", "depth", "rgbd")}
+    assert len(set(h.values())) == 4
+    assert dd.ddppo_layout_hash(dd.model_desc("gps"), **base) == h["gps"]  # deterministic
+    for k, v in (("E", 8), ("T", 64), ("ld", 136), ("minibatches", 4), ("epochs", 1)):
+        assert dd.ddppo_layout_hash(dd.model_desc("depth"), **dict(base, **{k: v})) != h["depth"], k

@@ -50,7 +50,7 @@ def _worker(rank, world, port, q):
     pm = synth.perms(5, 0, c["epochs"], c["E"], rank=rank)
     # a8 over NCCL (unregistered workspace), then over NVLink peer memory (registered workspace)
     for key, peer in (("params_nccl", False), ("params", True)):
-        lrn = Learner(ctx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, peer=peer)
+        lrn = Learner(ctx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, peer=peer, normalize_adv=True)
         lrn.load_rollout(ro, pm)
         lrn.step()
         torch.cuda.synchronize()

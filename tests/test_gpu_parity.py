@@ -442,7 +442,7 @@ def test_learner_step_parity(dd, ctx, cfgname, lengths):
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 21)
-    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, adam_eps=adam_eps)
+    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, adam_eps=adam_eps, normalize_adv=True)
     ro = synth.rollout(c["E"], c["T"], 22, length=lengths, hidden=desc.hidden, obs_shape=c.get("obs"),
                        rnn_layers=c.get("rnn_layers", 1))
     pm = synth.perms(22, 0, c["epochs"], c["E"])
@@ -495,7 +495,7 @@ def test_learner_graph_replay_matches_eager(dd, ctx, cfgname):
     out = {}
     for graphs in (False, True):
         dd.ddppo_set_graphs(ctx, graphs)
-        lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+        lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, normalize_adv=True)
         for it in range(3):
             ro = synth.rollout(c["E"], c["T"], 32, iteration=it, hidden=desc.hidden)
             lrn.load_rollout(ro, synth.perms(32, it, c["epochs"], c["E"]))
@@ -522,7 +522,7 @@ def test_learner_graph_alternating_stats_buffers(dd, ctx):
     out = {}
     for graphs in (False, True):
         dd.ddppo_set_graphs(ctx, graphs)
-        lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+        lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, normalize_adv=True)
         bufs = [torch.zeros_like(lrn.stats) for _ in range(2)]
         rec = []
         for it in range(5):

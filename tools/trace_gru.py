@@ -16,7 +16,7 @@ ctx = dd.Context(0, 1)
 c = synth.CONFIGS["gps"]
 desc = dd.model_desc("gps"); lay = dd.param_layout(desc); P = dd.param_count(desc)
 p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 0)
-lrn = Learner(ctx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0)
+lrn = Learner(ctx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, normalize_adv=True)
 lrn.load_rollout(synth.rollout(c["E"], c["T"], 0), synth.perms(0, 0, 2, c["E"]))
 for _ in range(3): lrn.step()
 torch.cuda.synchronize()
