@@ -4,11 +4,12 @@
 One step = one whole learner step on one rollout per rank (SURVEY.md 8(a) rows a2..a8 + a10):
 GAE -> advantage normalisation (allreduce of sum/sum^2) -> 2 epochs x 2 minibatches of
 {actor-critic fwd, fused PPO loss+grad, bwd, gradient allreduce + clip + Adam} -> step
-accounting allreduce.  Workload: configs[1] "PointGoal GPS+Compass-only" (4 envs/GPU x 128
-steps, goal FC + embedding -> GRU-512 -> heads, 2 epochs x 2 minibatches), synthetic
-PointGoal-shaped rollouts (synth/), random-init weights.
+accounting allreduce.  Default workload: configs[2] "Depth agent" -- the configuration
+BASELINE.json's metric ("at 1/2/4/8 B200") is quoted on: 4 envs/GPU x 128 steps of 64x64 depth,
+half-width ResNet18 + GroupNorm + LSTM-512, 2 epochs x 2 minibatches; synthetic PointGoal-shaped
+rollouts (synth/), random-init weights.  --config gps|rgbd|stress|toy selects the other configs.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config gps]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config depth]
 
 Multi-GPU: torchrun (one process per GPU, NCCL); weak scaling (E envs per GPU).  The
 reference arm (--impl reference) is the CPU oracle (oracle/) run as it stands on the host.
@@ -39,7 +40,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gps", choices=["gps", "toy", "stress_gps", "depth", "rgbd", "stress"])
+    ap.add_argument("--config", default="depth", choices=["gps", "toy", "stress_gps", "depth", "rgbd", "stress"])
     ap.add_argument("--seed", type=int, default=1337)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -128,12 +129,12 @@ def blas_threads():
 ORACLE_T = {"depth": 32, "stress": 8, "rgbd": 2}
 
 
-def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None):
+def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None, T=None):
     """Time the oracle's learner step (oracle/learner.py, as it stands) on the same workload."""
     from oracle import learner as olearner
     from oracle import models
     c = dict(synth.CONFIGS[cfgname])
-    c["T"] = ORACLE_T.get(cfgname, c["T"])
+    c["T"] = T or ORACLE_T.get(cfgname, c["T"])
     offs, P = models.offsets(c["arch"], hidden=c["hidden"])
     fans = {n: f for n, _, f in models.layout(c["arch"], hidden=c["hidden"])}
     p = synth.init_params([(o, int(np.prod(s)), fans[k]) for k, (o, s) in offs.items()], P, seed)
@@ -164,17 +165,21 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     c = synth.CONFIGS[args.config]
-    T_s = ORACLE_T.get(args.config, c["T"])
-    # each "step" is one oracle learner step on a bounded sample of the workload (whole rollouts); all of
-    # the host's cores (torchrun exports OMP_NUM_THREADS=1 to every rank; rank 0 runs alone here)
+    # each "step" is one oracle learner step on a bounded sample of the workload (whole rollouts of
+    # T_s steps); all of the host's cores (torchrun exports OMP_NUM_THREADS=1 to every rank; rank 0
+    # runs alone here)
     try:
         from threadpoolctl import threadpool_limits
         limiter = threadpool_limits(limits=cpu_cores())
     except Exception:
         limiter = None
+    T_s = ORACLE_T.get(args.config, c["T"])
+    # size the sample so that the K timed steps take about two minutes (probe: one step at T = 2)
+    _, _, el1 = oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=1, T=2)
+    T_s = int(max(2, min(T_s, 2 * 120.0 / (max(args.steps, 1) * max(el1, 1e-3)))))
     for _ in range(args.warmup if args.warmup < 2 else 1):
-        oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=1)
-    sps, n, el = oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=args.steps)
+        oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=1, T=T_s)
+    sps, n, el = oracle_steps_per_sec(args.config, args.seed, budget_s=1e9, max_steps=args.steps, T=T_s)
     out = {
         "impl": "reference", "metric": "learner experience-steps/sec", "value": sps,
         "unit": "experience-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -341,6 +346,10 @@ def main():
         stats_host = [torch.zeros(lrn.stats.shape, dtype=lrn.stats.dtype).pin_memory() for _ in range(2)]
         copy_stream = torch.cuda.Stream()
         done = [torch.cuda.Event() for _ in range(2)]
+        for i in range(2):  # warm the loop's own buffers (not timed)
+            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True)
+            lrn.step(stream, stats=stats_dev[i % 2])
+            dd.ddppo_allreduce_counts(ctx, [lrn.steps_per_rollout()])
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_exp = 0
@@ -491,7 +500,7 @@ def roofline_for(fam, prof, c, lrn, peaks, steps):
                 "frac": achieved / bf16, "traffic": None, "launch_us": per_launch_s * 1e6,
                 "note": "kernel family of one minibatch pass (ResNet implicit GEMMs + GroupNorm + LSTM-512 "
                         "recurrences); per-kernel split in profiles/"}
-    byte_per = {"gae": 17.0 * E * T, "loss": 60.0 * B * T, "adam": 32.0 * lrn.P}
+    byte_per = {"gae": 17.0 * E * T, "loss": 60.0 * B * T, "adam": 28.0 * lrn.P}  # Adam: read g, p, m, v; write p, m, v
     b = byte_per.get(fam, 0.0)
     achieved = b / per_launch_s / 1e9 if b else 0.0
     traffic = {"adam": _traffic("grad_norm_kernel", "adam_kernel")}.get(fam)

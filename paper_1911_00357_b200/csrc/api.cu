@@ -327,10 +327,11 @@ struct LearnerWs {
   float* gsum;      // rank-ordered sum of all ranks' gradients (peer path)
   float* pgather;   // this rank's updated parameter shard, read by the peers (sharded a8)
   float* grad_norm;
+  float* stats;     // [epochs*minibatches][8] loss statistics (copied to the caller's stats_out after the step)
   void* model_ws;
   size_t model_bytes;
 };
-size_t carve_learner(const ddppo_model_desc* d, int E, int T, int mb, void* base, LearnerWs* w) {
+size_t carve_learner(const ddppo_model_desc* d, int E, int T, int mb, int epochs, void* base, LearnerWs* w) {
   int64_t P = 0;
   ddppo_model_param_count(d, &P);
   const int B = E / mb;
@@ -355,6 +356,7 @@ size_t carve_learner(const ddppo_model_desc* d, int E, int T, int mb, void* base
   t.gsum = (float*)take((size_t)P * sizeof(float));
   t.pgather = (float*)take((size_t)P * sizeof(float));
   t.grad_norm = (float*)take(8 * sizeof(float));
+  t.stats = (float*)take((size_t)epochs * mb * 8 * sizeof(float));
   t.model_ws = take(model_bytes);
   t.model_bytes = model_bytes;
   if (w) *w = t;
@@ -368,7 +370,7 @@ ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int
   if (!host_bytes || build_layout(host_desc, &L) != DDPPO_OK || minibatches < 1 || E % minibatches || T < 1 ||
       ld < T + 1 || epochs < 1)
     return DDPPO_ERR_CONFIG;
-  *host_bytes = carve_learner(host_desc, E, T, minibatches, nullptr, nullptr);
+  *host_bytes = carve_learner(host_desc, E, T, minibatches, epochs, nullptr, nullptr);
   return DDPPO_OK;
 }
 
@@ -486,7 +488,7 @@ ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_mode
       b.n_valid = mbs[k].n_valid;
       b.obs = ro->obs;
       b.c0 = ro->c0;
-      float* st_out = stats_out ? stats_out + (size_t)k * 8 : w.grad_norm;
+      float* st_out = w.stats + (size_t)k * 8;
       const float* mis = cfg->normalize_adv ? w.mean_invstd : nullptr;
       if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
         s = toy_fwd(ctx, L, params, b, w.logits, w.values, w.model_ws, st);
@@ -602,7 +604,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
   if (s != DDPPO_OK) return s;
   DDPPO_REQUIRE(ctx, ws_bytes >= need, "learner_step: workspace too small");
   LearnerWs w;
-  carve_learner(host_desc, ro->E, ro->T, cfg->minibatches, ws, &w);
+  carve_learner(host_desc, ro->E, ro->T, cfg->minibatches, cfg->epochs, ws, &w);
   cudaStream_t st = as_stream(stream);
   const bool use_peers = ctx->world > 1 && ctx->peer_ws == ws;  // ddppo_learner_register'ed workspace
   // a4 on the host: every minibatch's T_run / n_valid from the host copies of lengths and perms
@@ -646,8 +648,9 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
     ddppo_learner_cfg ck = *cfg;
     ck.adam.step = 0;
     key_put(key, ck);
+    // (stats_out is not part of the key: the graph writes the workspace's statistics, copied out below)
     for (const void* p : {(const void*)params, (const void*)m, (const void*)v, (const void*)adv, (const void*)ret,
-                          (const void*)stats_out, (const void*)ws})
+                          (const void*)ws})
       key_put(key, p);
     key_put(key, use_peers);
     key_put(key, ctx->a8_mode);
@@ -674,6 +677,9 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
                        mb0);
       if (s != DDPPO_OK) return s;
       DDPPO_CUDA_TRY(ctx, fork_to(ctx, gs, st));
+      if (stats_out)
+        DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(stats_out, w.stats, (size_t)n_mb * 8 * sizeof(float),
+                                            cudaMemcpyDeviceToDevice, st));
       ctx->step_expected = (int64_t)cfg->adam.step + n_mb;
       ctx->peer_mb = mb0 + (uint64_t)n_mb;
       if (host_step_out) *host_step_out = cfg->adam.step + n_mb;
@@ -719,6 +725,9 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
     for (int i = 0; i < DDPPO_K_COUNT; ++i) ctx->launches[i] += hit->launches[i];
   }
   if (s != DDPPO_OK) return s;
+  if (stats_out)  // outside the graph: the caller may alternate statistics buffers without new captures
+    DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(stats_out, w.stats, (size_t)n_mb * 8 * sizeof(float),
+                                        cudaMemcpyDeviceToDevice, st));
   ctx->step_expected = (int64_t)cfg->adam.step + n_mb;
   ctx->peer_mb = mb0 + (uint64_t)n_mb;
   if (host_step_out) *host_step_out = cfg->adam.step + n_mb;

@@ -2,7 +2,8 @@
 sizes far above L2, through the C ABI.  Algorithmic bytes per unit:
   GAE   17 B / element   (r 4 + V 4 + done 1 + A 4 + R 4)
   loss  60 B / sample    (logits 16 + value 4 + action 4 + lp_old 4 + V_old 4 + R 4 + A 4; dlogits 16 + dv 4)
-  Adam  32 B / parameter (grad read twice 8 + p, m, v read 12 + p, m, v write 12)
+  Adam  28 B / parameter algorithmic (g, p, m, v read 16 + p, m, v write 12; the norm pass's second
+        read of g is not counted)
 Prints one JSON line per kernel.  Usage: python tools/microbench.py [--reps 10]
 """
 import argparse
@@ -95,7 +96,7 @@ def main():
         step[0] += 1
         dd.ddppo_grad_allreduce_step(ctx, grad, prm, m, v, dd.adam_cfg(step[0]))
     s = timed(adam, args.reps, flush)
-    b = 32.0 * P
+    b = 28.0 * P
     out.append(dict(kernel="clip_adam", units=P, unit="parameter", algorithmic_bytes=b, seconds=s,
                     achieved_gbs=b / s / 1e9, peak_gbs=hbm, frac=b / s / 1e9 / hbm))
     ctx.check()
