@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=1337)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--conv-engine", default="tma", choices=["tma", "cpasync"],
+                    help="visual encoders' convolutions: TMA-fed warp-specialised tcgen05 (default) or the round-1 "
+                         "cp.async kernel (A/B)")
+    ap.add_argument("--a8", default="sharded", choices=["sharded", "allread"], help="peer-memory a8 form (N > 1)")
     return ap.parse_args()
 
 
@@ -236,6 +240,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     ctx = dd.Context(rank, world, uid, device=local)
+    dd.ddppo_set_conv_engine(ctx, args.conv_engine)
+    dd.ddppo_set_a8_mode(ctx, args.a8)
     c = synth.CONFIGS[args.config]
     desc = dd.model_desc(c["arch"])
     lay = dd.param_layout(desc)

@@ -301,6 +301,14 @@ ddppo_status ddppo_layout_check(ddppo_ctx* ctx, const ddppo_model_desc* host_des
 typedef enum { DDPPO_A8_SHARDED = 0, DDPPO_A8_ALLREAD = 1 } ddppo_a8_mode;
 ddppo_status ddppo_set_a8_mode(ddppo_ctx* ctx, int mode);
 
+/* Engine of the visual encoders' implicit-GEMM convolutions (same arithmetic, host-side setting):
+ *   DDPPO_CONV_TMA (default): TMA im2col / tiled boxes feeding a warp-specialised persistent tcgen05
+ *     kernel (FPROP, stride-1 DGRAD, WGRAD of every convolution with a multiple of 32 input channels);
+ *   DDPPO_CONV_CPASYNC: the cp.async-staged tcgen05 kernel (round 1; also the fallback for the
+ *     stride-2 input gradients and the 8-channel RGB-D stem). */
+typedef enum { DDPPO_CONV_CPASYNC = 0, DDPPO_CONV_TMA = 1 } ddppo_conv_engine;
+ddppo_status ddppo_set_conv_engine(ddppo_ctx* ctx, int engine);
+
 /* CUDA graphs for ddppo_learner_step (default on): the step is captured once per (configuration,
  * buffer addresses, minibatch shapes) -- after one eager run of a new configuration -- and
  * replayed; Adam's update count and the peer-barrier epoch are kept on the device so nothing

@@ -324,3 +324,8 @@ def ddppo_layout_hash(desc, E, T, ld, minibatches, epochs):
 def ddppo_layout_check(ctx, desc, E, T, ld, minibatches, epochs):
     """Collective: DdppoError(protocol) unless every rank has the same layout hash."""
     _call(ctx, "ddppo_layout_check", ctypes.byref(desc), E, T, ld, minibatches, epochs)
+
+
+def ddppo_set_conv_engine(ctx, engine):
+    """"tma" (TMA-fed warp-specialised tcgen05 convolutions, default) or "cpasync" (round-1 kernel)."""
+    _call(ctx, "ddppo_set_conv_engine", {"cpasync": 0, "tma": 1}.get(engine, engine))

@@ -115,6 +115,7 @@ _SIGS = {
     "ddppo_learner_register": (c_int, [c_vp, c_vp, ctypes.c_size_t]),
     "ddppo_set_graphs": (c_int, [c_vp, c_int]),
     "ddppo_set_a8_mode": (c_int, [c_vp, c_int]),
+    "ddppo_set_conv_engine": (c_int, [c_vp, c_int]),
     "ddppo_layout_hash": (c_int, [P_(ModelDesc), c_int, c_int, c_int, c_int, c_int, P_(ctypes.c_uint64)]),
     "ddppo_layout_check": (c_int, [c_vp, P_(ModelDesc), c_int, c_int, c_int, c_int, c_int]),
     "ddppo_debug_peer_a8": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_i64, P_(AdamCfg), c_vp, c_vp,

@@ -576,6 +576,13 @@ ddppo_status ddppo_set_a8_mode(ddppo_ctx* ctx, int mode) {
   return DDPPO_OK;
 }
 
+ddppo_status ddppo_set_conv_engine(ddppo_ctx* ctx, int engine) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, engine == DDPPO_CONV_TMA || engine == DDPPO_CONV_CPASYNC, "set_conv_engine: unknown engine");
+  ctx->conv_engine = engine;
+  return DDPPO_OK;
+}
+
 ddppo_status ddppo_set_graphs(ddppo_ctx* ctx, int enable) {
   if (!ctx) return DDPPO_ERR_CONFIG;
   ctx->graphs = enable != 0;
@@ -654,6 +661,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
       key_put(key, p);
     key_put(key, use_peers);
     key_put(key, ctx->a8_mode);
+    key_put(key, ctx->conv_engine);
     key_put(key, (int)(mb0 & 1));
     for (const MbShape& sh : mbs) key_put(key, sh);
     if (!ctx->graph) {

@@ -36,6 +36,7 @@ struct ddppo_ctx {
   int64_t* h_cnt = nullptr;              // pinned host result
   uint64_t peer_mb = 0;
   int a8_mode = DDPPO_A8_SHARDED;       // ddppo_set_a8_mode
+  int conv_engine = DDPPO_CONV_TMA;     // ddppo_set_conv_engine
   // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step
   int* d_step = nullptr;
   int64_t step_expected = -1;       // value *d_step will hold once the enqueued work has run
@@ -283,6 +284,22 @@ struct IGemm {                   // C[m][n] (+)= sum_k A(m,k) B(n,k), fp32 C
   int wg_cp = 0, wg_cr = 0, wg_kk = 0;
 };
 ddppo_status launch_igemm(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st);
+// C[m][n] (+)= sum_z part[z*zs + m*N + n] (split order); weight-gradient form: dw[o][c < Cr][tap] =
+// sum_z part[z*zs + (tap*Cp + c)*N + o]
+ddppo_status launch_splitk_reduce(ddppo_ctx* ctx, const float* part, int splits, int64_t zs, int M, int N, float* C,
+                                  int64_t ldc, int accumulate, cudaStream_t st);
+ddppo_status launch_splitk_reduce_wgrad(ddppo_ctx* ctx, const float* part, int splits, int64_t zs, int N, int Cp, int Cr,
+                                        int kk, float* dw, cudaStream_t st);
+
+// TMA-fed tcgen05 implicit-GEMM convolutions (tconv.cu): FPROP / stride-1 DGRAD (flip) and WGRAD over
+// NHWC bf16 tensors; *splits_out > 1: the result is in `partial` ([splits][M][N]) for the reductions above
+ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xplane, int F, int H, int W, int C,
+                              int k, int s, int p, int flip, const __nv_bfloat16* w, int64_t wplane, int N, int planes,
+                              float* out, int64_t ldc, int accumulate, float* partial, int max_splits,
+                              int* splits_out, cudaStream_t st);
+ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, int H, int W, int C, int k, int s,
+                                int p, const __nv_bfloat16* dy, int N, float* partial, int max_splits, int* splits_out,
+                                cudaStream_t st);
 
 // NVLink peer memory (peer.cu)
 ddppo_status peer_exchange(ddppo_ctx* ctx, void* local, void** out);

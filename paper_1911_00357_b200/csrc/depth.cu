@@ -1010,6 +1010,7 @@ struct Plan {
   // scratch (reused by every layer)
   __nv_bfloat16* dyb;         // GN-backward output (bf16)
   float *dwt, *part, *gn_part, *dz_a, *dz_b, *dz_c, *dxin, *dflat, *dvis;
+  size_t part_n = 0;
   double* gn_gpart;           // GroupNorm per-chunk group partials (large frames)
   size_t bytes = 0;
 };
@@ -1146,7 +1147,8 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   }
   P.dyb = take_b(max_act);
   P.dwt = take(max_w);
-  P.part = take(std::max({(size_t)kMaxSplits * max_w, (size_t)16 * F * kG4, (size_t)16 * kG4 * kXin}));
+  P.part_n = std::max({(size_t)kMaxSplits * max_w, (size_t)16 * F * kG4, (size_t)16 * kG4 * kXin});
+  P.part = take(P.part_n);
   P.gn_part = take(max_gn_part);
   P.gn_gpart = reinterpret_cast<double*>(take_bytes(max_gn_rows * kGroups * 2 * sizeof(double)));
   P.dz_a = take(max_act);
@@ -1176,7 +1178,12 @@ struct ConvGeom {
 struct ConvScratch {
   __nv_bfloat16 *wr_b, *wd_b;  // weights as bf16 (hi/lo planes) / bf16
   float *dwt, *part;           // weight-gradient GEMM output [(u,v,c)][o], split-K partials
+  size_t part_n;               // floats available at part
 };
+// split count the partial buffer can hold for an M x N output (<= cap)
+inline int split_cap(const ConvScratch& sc, long long M, long long N, int cap) {
+  return (int)std::max(1LL, std::min<long long>(cap, (long long)(sc.part_n / (size_t)(M * N))));
+}
 
 bool is_stem(const ConvGeom& g) { return g.Ci == 1; }
 
@@ -1219,6 +1226,14 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     wr_b = sc.wr_b;
   }
+  if (ctx->conv_engine == DDPPO_CONV_TMA && g.Ci % 32 == 0) {
+    int splits = 1;
+    ddppo_status r = launch_tconv_fwd(ctx, xb, (int64_t)g.F * g.H * g.W * g.Ci, g.F, g.H, g.W, g.Ci, g.k, g.s, g.p, 0,
+                                      wr_b, (int64_t)g.Co * K, g.Co, 2, y, g.Co, 0, sc.part,
+                                      split_cap(sc, M, g.Co, 16), &splits, st);
+    if (r != DDPPO_OK || splits == 1) return r;
+    return launch_splitk_reduce(ctx, sc.part, splits, (int64_t)M * g.Co, M, g.Co, y, g.Co, 0, st);
+  }
   IGemm gm;
   gm.a = op_pix(xb, g.Ho, g.Wo, g.H, g.W, g.Ci, g, 0, (int64_t)g.F * g.H * g.W * g.Ci);
   gm.b = op_dense(IG_DENSE_K, wr_b, K, (int64_t)g.Co * K);
@@ -1259,7 +1274,14 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
   }
   const int K = g.K(), M = g.M();
   // wgrad: dWt[(u,v,c)][o] = sum_q x[tap(q; u, v)][c] dy[q][o]  (k runs over the M output pixels)
-  {
+  if (ctx->conv_engine == DDPPO_CONV_TMA && g.Ci % 32 == 0) {
+    int splits = 1;
+    ddppo_status r = launch_tconv_wgrad(ctx, xb, g.F, g.H, g.W, g.Ci, g.k, g.s, g.p, dy, g.Co, sc.part,
+                                        split_cap(sc, K, g.Co, kMaxSplits), &splits, st);
+    if (r == DDPPO_OK)
+      r = launch_splitk_reduce_wgrad(ctx, sc.part, splits, (int64_t)K * g.Co, g.Co, g.Ci, g.Cr, g.k * g.k, dw, st);
+    if (r != DDPPO_OK) return r;
+  } else {
     // split the pixel range so that ~2 CTAs per SM stream (each >= 4 chunks of 64 pixels)
     const int bn = g.Co <= 32 ? 32 : g.Co <= 64 ? 64 : 128;
     const long long tiles = (long long)((g.Co + bn - 1) / bn) * ((K + 127) / 128);
@@ -1293,6 +1315,15 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
     wd_b = sc.wd_b;
   }
   const int Kd = g.k * g.k * g.Co;
+  if (ctx->conv_engine == DDPPO_CONV_TMA && g.s == 1 && g.Co % 32 == 0) {
+    // stride 1: the input gradient is the convolution of dy with the mirrored window
+    int splits = 1;
+    const int Md = g.F * g.H * g.W;
+    ddppo_status r = launch_tconv_fwd(ctx, dy, 0, g.F, g.Ho, g.Wo, g.Co, g.k, 1, g.k - 1 - g.p, 1, wd_b, 0, g.Ci, 1, dx,
+                                      g.Ci, accumulate_dx, sc.part, split_cap(sc, Md, g.Ci, 16), &splits, st);
+    if (r != DDPPO_OK || splits == 1) return r;
+    return launch_splitk_reduce(ctx, sc.part, splits, (int64_t)Md * g.Ci, Md, g.Ci, dx, g.Ci, accumulate_dx, st);
+  }
   IGemm gm;
   gm.a = op_pix(dy, g.H, g.W, g.Ho, g.Wo, g.Co, g, 1, 0);
   gm.b = op_dense(IG_DENSE_K, wd_b, Kd, 0);
@@ -1459,7 +1490,7 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
 ConvGeom geom_of(const Plan& P, const ConvGN& c) {
   return ConvGeom{P.F, c.H, c.W, c.Ci, c.Co, c.k, c.s, c.p, c.Ho, c.Wo, c.Ci_real};
 }
-ConvScratch scratch_of(const Plan& P) { return ConvScratch{nullptr, nullptr, P.dwt, P.part}; }  // weights prepared
+ConvScratch scratch_of(const Plan& P) { return ConvScratch{nullptr, nullptr, P.dwt, P.part, P.part_n}; }  // weights prepared
 
 // conv (+GN (+residual) (+ReLU)) forward
 ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, const float* residual, int relu,
@@ -1778,6 +1809,7 @@ extern "C" ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const
   sc.wd_b = reinterpret_cast<__nv_bfloat16*>(take(ok * 2));
   sc.dwt = reinterpret_cast<float*>(take(ok * 4));
   sc.part = reinterpret_cast<float*>(take((nf - ok) * 4));
+  sc.part_n = nf - ok;
   cudaStream_t st = as_stream(stream);
   ProfScope ps(ctx, DDPPO_K_OTHER, st, 0);
   to_planes_kernel<<<blocks_for(ctx, nx), kThreads, 0, st>>>(x, nx, xb);

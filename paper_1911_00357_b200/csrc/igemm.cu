@@ -479,6 +479,25 @@ ddppo_status launch_ig(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st) {
 
 }  // namespace
 
+ddppo_status launch_splitk_reduce(ddppo_ctx* ctx, const float* part, int splits, int64_t zs, int M, int N, float* C,
+                                  int64_t ldc, int accumulate, cudaStream_t st) {
+  ig_splitk_reduce_kernel<<<grid_for((int)std::min<int64_t>(zs, 1 << 30), 256, ctx->sm_count * 8), 256, 0, st>>>(
+      part, splits, zs, M, N, C, ldc, accumulate);
+  ctx->count(1);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
+ddppo_status launch_splitk_reduce_wgrad(ddppo_ctx* ctx, const float* part, int splits, int64_t zs, int N, int Cp, int Cr,
+                                        int kk, float* dw, cudaStream_t st) {
+  const int n = kk * Cp * N;
+  ig_splitk_reduce_wgrad_kernel<<<grid_for(n, 256, ctx->sm_count * 8), 256, 0, st>>>(part, splits, zs, N, Cp, Cr, kk,
+                                                                                     dw);
+  ctx->count(1);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
 ddppo_status launch_igemm(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st) {
   DDPPO_REQUIRE(ctx, g.M >= 1 && g.N >= 1 && g.K >= 1, "igemm: empty shape");
   const bool a_k = g.a.kind == IG_DENSE_K || g.a.kind == IG_PIX_K, b_k = g.b.kind == IG_DENSE_K || g.b.kind == IG_PIX_K;

@@ -1,0 +1,509 @@
+// TMA-fed, warp-specialised, persistent tcgen05 implicit-GEMM convolution (a5 / a7 for the visual
+// agents' encoders, P:L212 / P:L582-584; BASELINE.json north_star: "Encoder ... GEMMs use
+// tcgen05/TMEM tiles fed by TMA").
+//
+//   FPROP  y[q][o]        = sum_{(u,v,c)} x[q @ (u,v)][c] Wr[o][(u,v,c)]        q = output pixel
+//   DGRAD  dx[q][c]       = sum_{(u,v,o)} dy[q @ (k-1-u,k-1-v)][o] Wd[c][(u,v,o)]  (stride-1 convs)
+//   WGRAD  dWt[(u,v,c)][o] = sum_q x[q @ (u,v)][c] dy[q][o]
+//
+// The im2col matrix never exists: the A operand of FPROP / DGRAD (pixels x channels, K-major) and
+// of WGRAD (channels x pixels, MN-major) is loaded by the TMA unit in im2col mode
+// (cp.async.bulk.tensor.4d.im2col) straight from the NHWC bf16 activation: a box of 128
+// consecutive output pixels (walking W, then H, then frames) x CS channels of one filter tap, the
+// tap given as the instruction's im2col offsets, padding and ragged tails zero-filled by the TMA
+// unit.  Weights (FPROP / DGRAD B) and dy (WGRAD B) are plain 2-D tiled TMA boxes.  Swizzle
+// 64 B (CS = 32) or 128 B (CS = 64) on both sides, matching the UMMA descriptors.
+//
+// CTA = 6 warps, persistent over a static list of (tile, split) work items:
+//   warp 0     TMA producer (one elected lane): stage ring of STAGES {A, B} boxes, full/empty mbarriers
+//   warp 1     MMA issuer: tcgen05.mma.kind::f16 (M = 128, N = BN, K = 16) into one of two TMEM
+//              accumulators, tcgen05.commit -> empty[stage] (slot reuse) and -> tmem_full[acc]
+//   warps 2-5  epilogue: tcgen05.ld (each warp its TMEM lane quarter), fp32 rows to global (or a
+//              split-K partial), then tmem_empty[acc] -- so tile i's epilogue overlaps tile i+1's
+//              main loop.
+// Precision: NPL = 1 (bf16 operands) or 2 (x = hi + lo bf16 planes, products lo*hi + hi*lo +
+// hi*hi, ~16-bit mantissas; the Depth forward decides ReLU / max-pool masks with it).
+#include <cuda.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kBM = 128;         // output rows per tile (TMEM lanes)
+constexpr int kPix = 128;        // pixels per im2col box (FPROP rows / WGRAD k-chunk)
+constexpr int kThreadsTC = 192;  // producer warp, MMA warp, 4 epilogue warps
+enum { TC_FWD = 0, TC_WGRAD = 1 };
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(s_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tma_im2col(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c, int w, int h,
+                                           int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(s_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(s_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n"
+      : "=r"(p));
+  return p != 0;
+}
+// UMMA shared-memory descriptor (sm100): start, LBO, SBO (bytes), layout 2 = SW128, 4 = SW64
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
+}
+template <int BYTES_ROW>
+__host__ __device__ constexpr uint32_t swz_layout() { return BYTES_ROW == 128 ? 2u : 4u; }
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit1(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_u32(bar))
+               : "memory");
+}
+
+struct TcArgs {
+  int M, N;               // output rows / columns
+  int n_k, kper;          // k-iterations (FPROP/DGRAD: taps x channel slices; WGRAD: pixel chunks), per split
+  int tiles_m, tiles_n, n_work;
+  int Ho, Wo, s, p, k;    // im2col traversal geometry (output pixel grid of the box walk)
+  int C, nsl;             // channels of the im2col'd tensor, C / CS
+  int flip;               // DGRAD: tap (u, v) reads offset (k-1-u, k-1-v)
+  float* out;
+  long long ldc, zs;      // row stride of the output, split stride (split-K partials)
+  int accumulate;
+};
+
+// first output pixel q -> im2col box coordinates (W, H, N) of its receptive field's corner
+__device__ __forceinline__ void pix_coords(const TcArgs& a, int q, int& w, int& h, int& n) {
+  const int hw = a.Ho * a.Wo;
+  n = q / hw;
+  const int r = q - n * hw;
+  const int oh = r / a.Wo;
+  h = oh * a.s - a.p;
+  w = (r - oh * a.Wo) * a.s - a.p;
+}
+
+template <int CS, int BN, int NPL, int MODE, int STAGES>
+struct TcCfg {
+  static constexpr int kRowB = CS * 2;                                        // A (FPROP) / K-row bytes
+  static constexpr uint32_t kABox = kPix * CS * 2;                            // one im2col box
+  static constexpr uint32_t kA = MODE == TC_FWD ? kABox : kBM * kPix * 2;     // A tile (WGRAD: 128/CS boxes)
+  static constexpr uint32_t kB = MODE == TC_FWD ? BN * CS * 2 : kPix * BN * 2;
+  static constexpr uint32_t kStage = NPL * (kA + kB);
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 256;
+  static constexpr size_t kSmem = (size_t)STAGES * kStage + 1024;
+};
+
+template <int CS, int BN, int NPL, int MODE, int STAGES>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+             const __grid_constant__ CUtensorMap mB0, const __grid_constant__ CUtensorMap mB1, const TcArgs a) {
+  using Cfg = TcCfg<CS, BN, NPL, MODE, STAGES>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024 - (s_u32(smem_raw) & 1023)) & 1023);
+  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mb_init(&tfull[i], 1);
+      mb_init(&tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mA0)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mB0)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(&tmem_slot)),
+                 "n"(Cfg::kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+  const int tiles = a.tiles_m * a.tiles_n;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int wi = blockIdx.x; wi < a.n_work; wi += gridDim.x) {
+        const int z = wi / tiles, t = wi - z * tiles;
+        const int m0 = (t % a.tiles_m) * kBM, n0 = (t / a.tiles_m) * BN;
+        const int k0 = z * a.kper, k1 = min(a.n_k, k0 + a.kper);
+        int w = 0, h = 0, n = 0;
+        if (MODE == TC_FWD) pix_coords(a, m0, w, h, n);
+        for (int it = k0; it < k1; ++it) {
+          mb_wait(&empty[stage], ph ^ 1u);
+          mb_expect_tx(&full[stage], Cfg::kStage);
+          const uint32_t sA = s_u32(smem + stage * Cfg::kStage), sB = sA + NPL * Cfg::kA;
+          if constexpr (MODE == TC_FWD) {
+            const int tap = it / a.nsl, sl = it - tap * a.nsl;
+            const int u = tap / a.k, v = tap - u * a.k;
+            const uint16_t ow = (uint16_t)(a.flip ? a.k - 1 - v : v), oh = (uint16_t)(a.flip ? a.k - 1 - u : u);
+            tma_im2col(sA, &mA0, &full[stage], sl * CS, w, h, n, ow, oh);
+            tma_2d(sB, &mB0, &full[stage], tap * a.C + sl * CS, n0);
+            if constexpr (NPL == 2) {
+              tma_im2col(sA + Cfg::kA, &mA1, &full[stage], sl * CS, w, h, n, ow, oh);
+              tma_2d(sB + Cfg::kB, &mB1, &full[stage], tap * a.C + sl * CS, n0);
+            }
+          } else {
+            // k-chunk = pixels [it*128, +128); A = 128/CS boxes of (tap, channel slice) rows of this M-block
+            pix_coords(a, it * kPix, w, h, n);
+            const int taps = a.k * a.k;
+#pragma unroll
+            for (int b = 0; b < kBM / CS; ++b) {
+              const int row0 = m0 + b * CS;
+              int tap = row0 / a.C;
+              const int c0 = row0 - tap * a.C;
+              tap = min(tap, taps - 1);  // rows past the last tap: any valid box (masked in the epilogue)
+              const int u = tap / a.k, v = tap - u * a.k;
+              tma_im2col(sA + b * Cfg::kABox, &mA0, &full[stage], c0, w, h, n, (uint16_t)v, (uint16_t)u);
+            }
+            tma_2d(sB, &mB0, &full[stage], n0, it * kPix);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MODE == TC_WGRAD) << 15) |
+                               ((uint32_t)(MODE == TC_WGRAD) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(kBM >> 4) << 24);
+    int stage = 0, acc = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int wi = blockIdx.x; wi < a.n_work; wi += gridDim.x) {
+      const int z = wi / tiles;
+      const int k0 = z * a.kper, k1 = min(a.n_k, k0 + a.kper);
+      mb_wait(&tempty[acc], aph ^ 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d = tmem + (uint32_t)(acc * BN);
+      for (int it = k0; it < k1; ++it) {
+        mb_wait(&full[stage], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (elect_one()) {
+          const uint32_t sA = s_u32(smem + stage * Cfg::kStage), sB = sA + NPL * Cfg::kA;
+          if constexpr (MODE == TC_FWD) {
+            constexpr uint32_t L = swz_layout<CS * 2>(), SBO = 8 * CS * 2;
+#pragma unroll
+            for (int kk = 0; kk < CS / 16; ++kk) {
+#pragma unroll
+              for (int t = 0; t < (NPL == 2 ? 3 : 1); ++t) {  // NPL == 2: lo*hi, hi*lo, hi*hi
+                const uint32_t ao = (NPL == 2 && t == 0) ? Cfg::kA : 0u, bo = (NPL == 2 && t == 1) ? Cfg::kB : 0u;
+                const uint64_t ad = sdesc(sA + ao + kk * 32, 16, SBO, L), bd = sdesc(sB + bo + kk * 32, 16, SBO, L);
+                mma_f16(d, ad, bd, idesc, (it > k0 || kk > 0 || t > 0) ? 1u : 0u);
+              }
+            }
+          } else {
+            constexpr uint32_t LA = swz_layout<CS * 2>(), LB = swz_layout<BN * 2>();
+#pragma unroll
+            for (int kk = 0; kk < kPix / 16; ++kk) {
+              const uint64_t ad = sdesc(sA + kk * 16 * CS * 2, Cfg::kABox, 8 * CS * 2, LA);
+              const uint64_t bd = sdesc(sB + kk * 16 * BN * 2, Cfg::kB, 8 * BN * 2, LB);
+              mma_f16(d, ad, bd, idesc, (it > k0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit1(&empty[stage]);  // frees the slot once these MMAs have read it
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          ph ^= 1u;
+        }
+      }
+      if (elect_one()) mma_commit1(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1u;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (TMEM -> global)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int wi = blockIdx.x; wi < a.n_work; wi += gridDim.x) {
+      const int z = wi / tiles, t = wi - z * tiles;
+      const int m0 = (t % a.tiles_m) * kBM, n0 = (t / a.tiles_m) * BN;
+      const bool part = a.zs != 0;
+      float* out = a.out + (part ? (long long)z * a.zs : 0LL);
+      mb_wait(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = m0 + q * 32 + lane;
+      float* orow = out + (long long)row * a.ldc + n0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 8) {
+        uint32_t r[8];
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < a.M && n0 + c0 < a.N) {
+          float4 v0 = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]),
+                                  __uint_as_float(r[3]));
+          float4 v1 = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]),
+                                  __uint_as_float(r[7]));
+          float4* o = reinterpret_cast<float4*>(orow + c0);
+          if (a.accumulate && !part) {
+            const float4 p0 = o[0], p1 = o[1];
+            v0.x += p0.x; v0.y += p0.y; v0.z += p0.z; v0.w += p0.w;
+            v1.x += p1.x; v1.y += p1.y; v1.z += p1.z; v1.w += p1.w;
+          }
+          o[0] = v0;
+          o[1] = v1;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mb_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1u;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::kTmemCols) : "memory");
+}
+
+// ---------------------------------------------------------------- host: tensor maps
+typedef CUresult (*EncIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+typedef CUresult (*EncTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <typename F>
+ddppo_status driver_fn(ddppo_ctx* ctx, const char* name, F* out) {
+  if (*out) return DDPPO_OK;
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  DDPPO_CUDA_TRY(ctx, cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q));
+  DDPPO_REQUIRE(ctx, f != nullptr && q == cudaDriverEntryPointSuccess, "tconv: driver entry point unavailable");
+  *out = reinterpret_cast<F>(f);
+  return DDPPO_OK;
+}
+
+CUtensorMapSwizzle swz_for(int row_bytes) {
+  return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                                         : CU_TENSOR_MAP_SWIZZLE_32B;
+}
+
+// im2col view of x[F][H][W][C] (bf16) for a k x k / stride s / pad p window: boxes of 128 output
+// pixels x cs channels
+ddppo_status map_im2col(ddppo_ctx* ctx, CUtensorMap* m, const __nv_bfloat16* x, int F, int H, int W, int C, int k,
+                        int s, int p, int cs) {
+  static EncIm2colFn enc = nullptr;
+  ddppo_status st = driver_fn(ctx, "cuTensorMapEncodeIm2col", &enc);
+  if (st != DDPPO_OK) return st;
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)F};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  const int lower[2] = {-p, -p}, upper[2] = {p - (k - 1), p - (k - 1)};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<__nv_bfloat16*>(x), dims, strides, lower, upper,
+                   (cuuint32_t)cs, (cuuint32_t)kPix, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_for(cs * 2),
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DDPPO_REQUIRE(ctx, r == CUDA_SUCCESS, "tconv: cuTensorMapEncodeIm2col rejected the geometry");
+  return DDPPO_OK;
+}
+// 2-D tiles of a row-major [rows][cols] bf16 matrix: boxes of box_rows x box_cols
+ddppo_status map_2d(ddppo_ctx* ctx, CUtensorMap* m, const __nv_bfloat16* x, int64_t rows, int64_t cols, int box_cols,
+                    int box_rows) {
+  static EncTiledFn enc = nullptr;
+  ddppo_status st = driver_fn(ctx, "cuTensorMapEncodeTiled", &enc);
+  if (st != DDPPO_OK) return st;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(x), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz_for(box_cols * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DDPPO_REQUIRE(ctx, r == CUDA_SUCCESS, "tconv: cuTensorMapEncodeTiled rejected the matrix");
+  return DDPPO_OK;
+}
+
+template <int CS, int BN, int NPL, int MODE>
+ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, cudaStream_t st) {
+  constexpr uint32_t kStage = TcCfg<CS, BN, NPL, MODE, 1>::kStage;
+  constexpr int STAGES = (int)std::min<uint32_t>(8u, (200u * 1024u) / kStage);
+  static_assert(STAGES >= 2, "stage too large");
+  using Cfg = TcCfg<CS, BN, NPL, MODE, STAGES>;
+  auto kern = tconv_kernel<CS, BN, NPL, MODE, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    DDPPO_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    attr = true;
+  }
+  const int per_sm = std::max(1, (int)((227u * 1024u) / (Cfg::kSmem + 2048)));
+  const int grid = std::max(1, std::min(a.n_work, ctx->sm_count * std::min(per_sm, 2)));
+  kern<<<grid, kThreadsTC, Cfg::kSmem, st>>>(maps[0], maps[1], maps[2], maps[3], a);
+  ctx->count(1);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
+// split-K: enough (tile, split) work items for ~2 per SM, each >= min_iters k-iterations
+void plan_splits(ddppo_ctx* ctx, TcArgs& a, int min_iters, int max_splits) {
+  const int tiles = a.tiles_m * a.tiles_n;
+  int splits = 1;
+  if (max_splits > 1)
+    splits = std::max(1, std::min({(2 * ctx->sm_count + tiles - 1) / tiles, a.n_k / std::max(1, min_iters), max_splits}));
+  a.kper = (a.n_k + splits - 1) / splits;
+  splits = (a.n_k + a.kper - 1) / a.kper;
+  a.n_work = tiles * splits;
+}
+
+}  // namespace
+
+// FPROP (flip = 0) or stride-1 DGRAD (flip = 1) over x[F][H][W][C]:
+//   out[q][o] (+)= sum_{tap, c} x[q @ tap][c] w[o][tap*C + c],  q over the F x Ho x Wo output grid.
+// w: [N][k*k*C] bf16 (plane stride wplane elements when planes == 2; x likewise xplane).
+// With `partial` (>= splits*M*N floats) and a long k loop the work is split over K; the caller's
+// reduction then sums the partials (returns the split count in *splits_out, 1 = written to out).
+ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xplane, int F, int H, int W, int C,
+                              int k, int s, int p, int flip, const __nv_bfloat16* w, int64_t wplane, int N, int planes,
+                              float* out, int64_t ldc, int accumulate, float* partial, int max_splits,
+                              int* splits_out, cudaStream_t st) {
+  DDPPO_REQUIRE(ctx, C % 32 == 0 && N % 8 == 0 && ldc % 4 == 0, "tconv: C % 32 == 0, N % 8 == 0 required");
+  DDPPO_REQUIRE(ctx, !flip || s == 1, "tconv: transposed taps only for stride-1 convolutions");
+  DDPPO_REQUIRE(ctx, ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0 && ((uintptr_t)out & 15) == 0,
+                "tconv: 16-byte aligned operands required");
+  const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
+  const int cs = C % 64 == 0 ? 64 : 32;
+  const int bn = N <= 32 ? 32 : N <= 64 ? 64 : 128;
+  TcArgs a = {};
+  a.M = F * Ho * Wo;
+  a.N = N;
+  a.Ho = Ho;
+  a.Wo = Wo;
+  a.s = s;
+  a.p = p;
+  a.k = k;
+  a.C = C;
+  a.nsl = C / cs;
+  a.flip = flip;
+  a.n_k = k * k * a.nsl;
+  a.tiles_m = (a.M + kBM - 1) / kBM;
+  a.tiles_n = (N + bn - 1) / bn;
+  plan_splits(ctx, a, 4, partial ? max_splits : 1);
+  const int splits = a.n_work / (a.tiles_m * a.tiles_n);
+  a.out = splits > 1 ? partial : out;
+  a.ldc = splits > 1 ? N : ldc;
+  a.zs = splits > 1 ? (long long)a.M * N : 0;
+  a.accumulate = accumulate;
+  if (splits_out) *splits_out = splits;
+  CUtensorMap maps[4];
+  memset(maps, 0, sizeof(maps));
+  const int K = k * k * C;
+  // im2col geometry of the box walk: FPROP walks x with the conv's own window; DGRAD walks dy with
+  // the mirrored window (pad k-1-p), producing the input-resolution grid
+  ddppo_status r = map_im2col(ctx, &maps[0], x, F, H, W, C, k, s, p, cs);
+  if (r == DDPPO_OK && planes == 2) r = map_im2col(ctx, &maps[1], x + xplane, F, H, W, C, k, s, p, cs);
+  if (r == DDPPO_OK) r = map_2d(ctx, &maps[2], w, N, K, cs, bn);
+  if (r == DDPPO_OK && planes == 2) r = map_2d(ctx, &maps[3], w + wplane, N, K, cs, bn);
+  if (r != DDPPO_OK) return r;
+#define TC_CASE(CS_, BN_, NPL_) \
+  if (cs == CS_ && bn == BN_ && planes == NPL_) return run<CS_, BN_, NPL_, TC_FWD>(ctx, maps, a, st);
+  TC_CASE(32, 32, 1) TC_CASE(32, 64, 1) TC_CASE(32, 128, 1) TC_CASE(64, 32, 1) TC_CASE(64, 64, 1)
+  TC_CASE(64, 128, 1) TC_CASE(32, 32, 2) TC_CASE(32, 64, 2) TC_CASE(32, 128, 2) TC_CASE(64, 32, 2)
+  TC_CASE(64, 64, 2) TC_CASE(64, 128, 2)
+#undef TC_CASE
+  DDPPO_REQUIRE(ctx, false, "tconv: no instantiation for this shape");
+  return DDPPO_ERR_CONFIG;
+}
+
+// WGRAD: partial[z][(u*k+v)*C + c][o] = sum over the split's output pixels q of
+//   x[q @ (u, v)][c] * dy[q][o]   (x [F][H][W][C] bf16, dy [F*Ho*Wo][N] bf16); splits returned in
+// *splits_out (partials always: the caller's reduction writes the weight gradient).
+ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, int H, int W, int C, int k, int s,
+                                int p, const __nv_bfloat16* dy, int N, float* partial, int max_splits, int* splits_out,
+                                cudaStream_t st) {
+  DDPPO_REQUIRE(ctx, C % 32 == 0 && N % 8 == 0, "tconv wgrad: C % 32 == 0, N % 8 == 0 required");
+  DDPPO_REQUIRE(ctx, ((uintptr_t)x & 15) == 0 && ((uintptr_t)dy & 15) == 0 && ((uintptr_t)partial & 15) == 0,
+                "tconv wgrad: 16-byte aligned operands required");
+  const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
+  const int cs = C % 64 == 0 ? 64 : 32;
+  const int bn = N <= 32 ? 32 : 64;
+  TcArgs a = {};
+  a.M = k * k * C;
+  a.N = N;
+  a.Ho = Ho;
+  a.Wo = Wo;
+  a.s = s;
+  a.p = p;
+  a.k = k;
+  a.C = C;
+  a.nsl = C / cs;
+  const int pix = F * Ho * Wo;
+  a.n_k = (pix + kPix - 1) / kPix;
+  a.tiles_m = (a.M + kBM - 1) / kBM;
+  a.tiles_n = (N + bn - 1) / bn;
+  plan_splits(ctx, a, 2, max_splits);
+  const int splits = a.n_work / (a.tiles_m * a.tiles_n);
+  a.out = partial;
+  a.ldc = N;
+  a.zs = (long long)a.M * N;
+  a.accumulate = 0;
+  if (splits_out) *splits_out = splits;
+  CUtensorMap maps[4];
+  memset(maps, 0, sizeof(maps));
+  ddppo_status r = map_im2col(ctx, &maps[0], x, F, H, W, C, k, s, p, cs);
+  if (r == DDPPO_OK) r = map_2d(ctx, &maps[2], dy, pix, N, bn, kPix);
+  if (r != DDPPO_OK) return r;
+  if (cs == 32 && bn == 32) return run<32, 32, 1, TC_WGRAD>(ctx, maps, a, st);
+  if (cs == 32 && bn == 64) return run<32, 64, 1, TC_WGRAD>(ctx, maps, a, st);
+  if (cs == 64 && bn == 32) return run<64, 32, 1, TC_WGRAD>(ctx, maps, a, st);
+  return run<64, 64, 1, TC_WGRAD>(ctx, maps, a, st);
+}

@@ -53,8 +53,13 @@ def nchw(a):
     (2, 9, 1, 16, 3, 1, 1),     # single-channel (stem kernels) at another geometry
     (2, 32, 8, 32, 7, 2, 3),    # RGB-D stem (4 channels padded to 8)
     (2, 8, 64, 256, 1, 1, 0),   # bottleneck 1x1 expansion
-    (2, 4, 1024, 128, 3, 1, 1)])  # RGB-D compression (1024 -> 128 at 4x4)
-def test_conv2d(dd, ctx, F, H, Ci, Co, k, s, p):
+    (2, 4, 1024, 128, 3, 1, 1),   # RGB-D compression (1024 -> 128 at 4x4)
+    (256, 16, 32, 32, 3, 1, 1),   # layer1 at the config's minibatch (F = 256 frames: 512 tiles)
+    (256, 2, 256, 256, 3, 1, 1),  # layer4 at the config's minibatch (split-K)
+    (7, 9, 96, 40, 3, 1, 1)])     # odd spatial size, 3 channel slices, ragged M
+@pytest.mark.parametrize("engine", ["tma", "cpasync"])
+def test_conv2d(dd, ctx, F, H, Ci, Co, k, s, p, engine):
+    dd.ddppo_set_conv_engine(ctx, engine)
     rng = np.random.default_rng(F * 100 + H + Ci + Co + k)
     x = rng.normal(size=(F, Ci, H, H)).astype(np.float32)
     x[x < -0.5] = 0.0  # post-ReLU-like inputs with exact zeros
