@@ -55,9 +55,11 @@ ddppo_status ddppo_ctx_create(int rank, int world, const uint8_t* host_id, int d
             cudaMalloc(&ctx->d_partials, kMaxPartials * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&ctx->d_scalars, 64 * sizeof(float)) == cudaSuccess &&
             cudaMalloc(&ctx->d_i32, 64 * sizeof(int32_t)) == cudaSuccess &&
-            cudaMalloc(&ctx->d_i64, kMaxCountVals * sizeof(int64_t)) == cudaSuccess;
+            cudaMalloc(&ctx->d_i64, kMaxCountVals * sizeof(int64_t)) == cudaSuccess &&
+            cudaMalloc(&ctx->d_tile_cnt, kMaxTileCounters * sizeof(int)) == cudaSuccess;
   ok = ok && cudaMemset(ctx->d_err, 0, sizeof(int)) == cudaSuccess &&
        cudaMemset(ctx->d_counters, 0, CNT_NUM * sizeof(unsigned int)) == cudaSuccess &&
+       cudaMemset(ctx->d_tile_cnt, 0, kMaxTileCounters * sizeof(int)) == cudaSuccess &&
        cudaDeviceSynchronize() == cudaSuccess;
   if (!ok) {
     ddppo_ctx_destroy(ctx);
@@ -104,6 +106,7 @@ ddppo_status ddppo_ctx_destroy(ddppo_ctx* ctx) {
   cudaFree(ctx->d_scalars);
   cudaFree(ctx->d_i32);
   cudaFree(ctx->d_i64);
+  cudaFree(ctx->d_tile_cnt);
   delete ctx;
   return DDPPO_OK;
 }
@@ -666,7 +669,11 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
     for (const MbShape& sh : mbs) key_put(key, sh);
     if (!ctx->graph) {
       ctx->graph = new ddppo_ctx::GraphCache();
-      DDPPO_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->graph->stream, cudaStreamNonBlocking));
+      // the critical path (the capture / replay stream) at the highest priority: work forked to the
+      // side streams (weight gradients) only fills SMs the chain of input gradients leaves idle
+      int lo = 0, hi = 0;
+      DDPPO_CUDA_TRY(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      DDPPO_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->graph->stream, cudaStreamNonBlocking, hi));
     }
     ddppo_ctx::GraphCache& gc = *ctx->graph;
     cudaStream_t gs = gc.stream;

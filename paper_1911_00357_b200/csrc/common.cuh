@@ -37,6 +37,7 @@ struct ddppo_ctx {
   uint64_t peer_mb = 0;
   int a8_mode = DDPPO_A8_SHARDED;       // ddppo_set_a8_mode
   int conv_engine = DDPPO_CONV_TMA;     // ddppo_set_conv_engine
+  int* d_tile_cnt = nullptr;            // split-K tile arrival counters (tconv.cu), zero between kernels
   // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step
   int* d_step = nullptr;
   int64_t step_expected = -1;       // value *d_step will hold once the enqueued work has run
@@ -97,6 +98,7 @@ struct ProfScope {
 enum { CNT_GAE = 0, CNT_LOSS = 1, CNT_NORM = 2, CNT_MISC = 3, CNT_NUM = 8 };
 constexpr int kMaxPartials = 1 << 16;   // doubles
 constexpr int kMaxCountVals = 64;
+constexpr int kMaxTileCounters = 1 << 16;
 
 enum { ERR_BIT_LOSS = 1, ERR_BIT_GRAD = 2, ERR_BIT_COMM = 4 };
 
@@ -295,11 +297,11 @@ ddppo_status launch_splitk_reduce_wgrad(ddppo_ctx* ctx, const float* part, int s
 // NHWC bf16 tensors; *splits_out > 1: the result is in `partial` ([splits][M][N]) for the reductions above
 ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xplane, int F, int H, int W, int C,
                               int k, int s, int p, int flip, const __nv_bfloat16* w, int64_t wplane, int N, int planes,
-                              float* out, int64_t ldc, int accumulate, float* partial, int max_splits,
+                              float* out, int64_t ldc, int accumulate, float* partial, int max_splits, int slot,
                               int* splits_out, cudaStream_t st);
 ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, int H, int W, int C, int k, int s,
-                                int p, const __nv_bfloat16* dy, int N, float* partial, int max_splits, int* splits_out,
-                                cudaStream_t st);
+                                int p, const __nv_bfloat16* dy, int N, float* dw, int Cr, float* partial, int max_splits,
+                                int slot, int* splits_out, cudaStream_t st);
 
 // NVLink peer memory (peer.cu)
 ddppo_status peer_exchange(ddppo_ctx* ctx, void* local, void** out);

@@ -987,6 +987,8 @@ struct ConvGN {
   int gn_rows;                        // F*S
   __nv_bfloat16 *xb, *zb;             // input / output as bf16 hi / lo planes (GEMM operands; zb may be null)
   __nv_bfloat16 *wr_b, *wd_b;         // this minibatch's weights as GEMM operands (Wr planes, Wd)
+  __nv_bfloat16* dyb;                 // GN-backward output (gradient wrt y, bf16): read by dgrad and, on the
+                                      // side stream, by wgrad -- one buffer per layer
 };
 
 struct Plan {
@@ -1011,6 +1013,9 @@ struct Plan {
   __nv_bfloat16* dyb;         // GN-backward output (bf16)
   float *dwt, *part, *gn_part, *dz_a, *dz_b, *dz_c, *dxin, *dflat, *dvis;
   size_t part_n = 0;
+  float *part_w = nullptr, *part2 = nullptr;  // side-stream partials (weight gradients)
+  size_t part_w_n = 0;
+  cudaStream_t side = nullptr;                // backward: weight gradients run here (fork / join)
   double* gn_gpart;           // GroupNorm per-chunk group partials (large frames)
   size_t bytes = 0;
 };
@@ -1064,6 +1069,7 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
     const size_t nw = (size_t)Co * k * k * Ci;
     c.wr_b = Ci > 1 ? take_b(2 * nw) : nullptr;
     c.wd_b = (Ci > 1 && needs_dx) ? take_b(nw) : nullptr;
+    c.dyb = take_b(act);
     max_act = std::max(max_act, std::max(act, (size_t)F * H * H * Ci));
     max_w = std::max(max_w, nw);
     const size_t S = ((size_t)c.Ho * c.Wo * Co + gn_chunk(Co) - 1) / gn_chunk(Co);
@@ -1149,6 +1155,11 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   P.dwt = take(max_w);
   P.part_n = std::max({(size_t)kMaxSplits * max_w, (size_t)16 * F * kG4, (size_t)16 * kG4 * kXin});
   P.part = take(P.part_n);
+  // side-stream scratch: weight-gradient partials (tconv split-K: at most ~2 work items of 128 x 64 per
+  // SM; the stem's per-frame partials) and the LSTM / visual-FC weight-gradient GEMMs' partials
+  P.part_w_n = std::max((size_t)2 * 160 * 128 * 128, (size_t)F * 32 * 64);
+  P.part_w = take(P.part_w_n);
+  P.part2 = take((size_t)16 << 20);
   P.gn_part = take(max_gn_part);
   P.gn_gpart = reinterpret_cast<double*>(take_bytes(max_gn_rows * kGroups * 2 * sizeof(double)));
   P.dz_a = take(max_act);
@@ -1179,6 +1190,7 @@ struct ConvScratch {
   __nv_bfloat16 *wr_b, *wd_b;  // weights as bf16 (hi/lo planes) / bf16
   float *dwt, *part;           // weight-gradient GEMM output [(u,v,c)][o], split-K partials
   size_t part_n;               // floats available at part
+  int slot = 0;                // tconv tile-counter slot (one per concurrently running stream)
 };
 // split count the partial buffer can hold for an M x N output (<= cap)
 inline int split_cap(const ConvScratch& sc, long long M, long long N, int cap) {
@@ -1230,7 +1242,7 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
     int splits = 1;
     ddppo_status r = launch_tconv_fwd(ctx, xb, (int64_t)g.F * g.H * g.W * g.Ci, g.F, g.H, g.W, g.Ci, g.k, g.s, g.p, 0,
                                       wr_b, (int64_t)g.Co * K, g.Co, 2, y, g.Co, 0, sc.part,
-                                      split_cap(sc, M, g.Co, 16), &splits, st);
+                                      split_cap(sc, M, g.Co, 16), sc.slot, &splits, st);
     if (r != DDPPO_OK || splits == 1) return r;
     return launch_splitk_reduce(ctx, sc.part, splits, (int64_t)M * g.Co, M, g.Co, y, g.Co, 0, st);
   }
@@ -1248,12 +1260,10 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
   return launch_igemm(ctx, gm, st);
 }
 
-// dy (bf16, gradient wrt the conv output) -> dw (PyTorch order); dx (+)= input gradient (if dx)
-ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const __nv_bfloat16* xb, const float* w,
-                      const __nv_bfloat16* wd_b, const __nv_bfloat16* dy, float* dw, float* dx, int accumulate_dx,
-                      const ConvScratch& sc, cudaStream_t st) {
+// dy (bf16, gradient wrt the conv output) -> dw (PyTorch order)
+ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const __nv_bfloat16* xb,
+                        const __nv_bfloat16* dy, float* dw, const ConvScratch& sc, cudaStream_t st) {
   if (is_stem(g)) {
-    DDPPO_REQUIRE(ctx, dx == nullptr, "stem conv: no input gradient");
     DDPPO_REQUIRE(ctx, (g.Ho * g.Wo * g.Co) % 8 == 0, "stem conv: Ho*Wo*Co must be a multiple of 8");
     const size_t hp = (size_t)(g.H + 2 * g.p) * (g.W + 2 * g.p);
     const size_t smem = (((size_t)g.Ho * g.Wo * g.Co / 2 + 3) / 4 * 4 + std::max<size_t>(hp, 128 * 16)) * sizeof(float);
@@ -1276,11 +1286,8 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
   // wgrad: dWt[(u,v,c)][o] = sum_q x[tap(q; u, v)][c] dy[q][o]  (k runs over the M output pixels)
   if (ctx->conv_engine == DDPPO_CONV_TMA && g.Ci % 32 == 0) {
     int splits = 1;
-    ddppo_status r = launch_tconv_wgrad(ctx, xb, g.F, g.H, g.W, g.Ci, g.k, g.s, g.p, dy, g.Co, sc.part,
-                                        split_cap(sc, K, g.Co, kMaxSplits), &splits, st);
-    if (r == DDPPO_OK)
-      r = launch_splitk_reduce_wgrad(ctx, sc.part, splits, (int64_t)K * g.Co, g.Co, g.Ci, g.Cr, g.k * g.k, dw, st);
-    if (r != DDPPO_OK) return r;
+    return launch_tconv_wgrad(ctx, xb, g.F, g.H, g.W, g.Ci, g.k, g.s, g.p, dy, g.Co, dw, g.Cr, sc.part,
+                              split_cap(sc, K, g.Co, kMaxSplits), sc.slot, &splits, st);
   } else {
     // split the pixel range so that ~2 CTAs per SM stream (each >= 4 chunks of 64 pixels)
     const int bn = g.Co <= 32 ? 32 : g.Co <= 64 ? 64 : 128;
@@ -1302,10 +1309,15 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
     gm.wg_cp = g.Ci;
     gm.wg_cr = g.Cr;
     gm.wg_kk = g.k * g.k;
-    ddppo_status s = launch_igemm(ctx, gm, st);
-    if (s != DDPPO_OK) return s;
+    return launch_igemm(ctx, gm, st);
   }
-  if (dx == nullptr) return DDPPO_OK;
+}
+
+// dx (+)= input gradient of the convolution (not for the stem)
+ddppo_status conv_dgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* w, const __nv_bfloat16* wd_b,
+                        const __nv_bfloat16* dy, float* dx, int accumulate_dx, const ConvScratch& sc, cudaStream_t st) {
+  DDPPO_REQUIRE(ctx, !is_stem(g), "stem conv: no input gradient");
+  const int K = g.K();
   // dgrad: dx[p][c] (+)= sum_{(u,v,o)} dy[tap^T(p; u, v)][o] W[o][c][u][v]
   if (!wd_b) {
     DDPPO_REQUIRE(ctx, sc.wd_b && g.Cr == g.Ci, "conv: unprepared weights need scratch");
@@ -1320,7 +1332,7 @@ ddppo_status conv_bwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
     int splits = 1;
     const int Md = g.F * g.H * g.W;
     ddppo_status r = launch_tconv_fwd(ctx, dy, 0, g.F, g.Ho, g.Wo, g.Co, g.k, 1, g.k - 1 - g.p, 1, wd_b, 0, g.Ci, 1, dx,
-                                      g.Ci, accumulate_dx, sc.part, split_cap(sc, Md, g.Ci, 16), &splits, st);
+                                      g.Ci, accumulate_dx, sc.part, split_cap(sc, Md, g.Ci, 16), sc.slot, &splits, st);
     if (r != DDPPO_OK || splits == 1) return r;
     return launch_splitk_reduce(ctx, sc.part, splits, (int64_t)Md * g.Ci, Md, g.Ci, dx, g.Ci, accumulate_dx, st);
   }
@@ -1503,24 +1515,34 @@ ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, c
 
 // backward of conv+GN: dz = gradient wrt the GN(+residual)(+ReLU) output; relu_z = that output if a
 // ReLU followed (its > 0 mask), else null.  Writes dW, dgamma, dbeta into grad; dx (+)= into dx.
+// The weight gradient only feeds a8, so with a side stream it leaves the critical path: it is
+// forked after the GN backward (its own dy buffer and partials) and joined once after the backward.
 ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P, ConvGN& c, const float* dz,
                          const float* relu_z, float* dx, int accumulate_dx, cudaStream_t st) {
-  ddppo_status s = gn_bwd(ctx, P.F, c.Ho * c.Wo, c.Co, dz, relu_z, c.y, c.stats, prm + c.gw, P.dyb, grad + c.gw,
+  ddppo_status s = gn_bwd(ctx, P.F, c.Ho * c.Wo, c.Co, dz, relu_z, c.y, c.stats, prm + c.gw, c.dyb, grad + c.gw,
                           grad + c.gb, c.gn_part, P.gn_gpart, st, /*reduce_params=*/false);
   if (s != DDPPO_OK) return s;
-  return conv_bwd(ctx, geom_of(P, c), c.x, c.xb, prm + c.w, c.wd_b, P.dyb, grad + c.w, dx, accumulate_dx,
-                  scratch_of(P), st);
+  const ConvGeom g = geom_of(P, c);
+  if (P.side) {
+    DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, P.side));
+    ConvScratch ws = {nullptr, nullptr, P.dwt, P.part_w, P.part_w_n, 1};
+    s = conv_wgrad(ctx, g, c.x, c.xb, c.dyb, grad + c.w, ws, P.side);
+  } else {
+    s = conv_wgrad(ctx, g, c.x, c.xb, c.dyb, grad + c.w, scratch_of(P), st);
+  }
+  if (s != DDPPO_OK || dx == nullptr) return s;
+  return conv_dgrad(ctx, g, prm + c.w, c.wd_b, c.dyb, dx, accumulate_dx, scratch_of(P), st);
 }
 
 // gemm_tc with split-K chosen so that small-M / long-K GEMMs still fill the GPU (partials in P.part)
-ddppo_status gemm_split(ddppo_ctx* ctx, GemmTC g, const Plan& P, cudaStream_t st) {
+ddppo_status gemm_split(ddppo_ctx* ctx, GemmTC g, const Plan& P, cudaStream_t st, float* part = nullptr) {
   const int bn = g.N <= 32 ? 32 : (g.N <= 64 || g.prec == 3) ? 64 : 128;
   const long long tiles = (long long)((g.N + bn - 1) / bn) * ((g.M + 127) / 128);
   const int chunks = (g.K + 63) / 64;
   const int splits = (int)std::max(1LL, std::min<long long>({(2LL * ctx->sm_count + tiles - 1) / tiles, chunks / 2, 16}));
   if (splits > 1) {
     g.splits = splits;
-    g.partial = P.part;
+    g.partial = part ? part : P.part;
   }
   return launch_gemm_tc(ctx, g, st);
 }
@@ -1680,6 +1702,14 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     if (s != DDPPO_OK) return s;
   }
   ProfScope ps(ctx, DDPPO_K_NET_BWD, st, 0);
+  // weight gradients (LSTM, visual FC, convolutions) only feed a8: they run on a side stream beside
+  // the chain of input gradients, joined once at the end
+  cudaStream_t wst = st;
+  if (ctx->conv_engine == DDPPO_CONV_TMA) {
+    cudaStream_t sb = nullptr;
+    if ((s = ctx_side_streams(ctx, &P.side, &sb)) != DDPPO_OK) return s;
+    wst = P.side;
+  }
   for (int l = P.layers - 1; l >= 0; --l) {
     Plan::Rnn& r = P.rnn[l];
     if ((s = launch_lstm_bwd(ctx, lstm_ptrs(L, prm, b, P, l), st)) != DDPPO_OK) return s;
@@ -1687,17 +1717,18 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     const float* xl = l == 0 ? P.xin : P.rnn[l - 1].Hs;
     const int nin = l == 0 ? kXin : kH;
     const float* Wih = prm + off_of(L, rnn_name(P, "rnn.weight_ih", l));
+    if (wst != st) DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, wst));
     if ((s = gemm_split(ctx, GemmTC{r.dG, 1, kG4, xl, 1, nin, grad + off_of(L, rnn_name(P, "rnn.weight_ih", l)), nin,
                                     kG4, nin, F},
-                        P, st)) != DDPPO_OK)
+                        P, wst, P.part2)) != DDPPO_OK)
       return s;
     if ((s = gemm_split(ctx, GemmTC{r.dG, 1, kG4, r.Hin, 1, kH, grad + off_of(L, rnn_name(P, "rnn.weight_hh", l)), kH,
                                     kG4, kH, F},
-                        P, st)) != DDPPO_OK)
+                        P, wst, P.part2)) != DDPPO_OK)
       return s;
-    if ((s = launch_colsum(ctx, r.dG, kG4, F, kG4, grad + off_of(L, rnn_name(P, "rnn.bias_ih", l)), st)) != DDPPO_OK)
+    if ((s = launch_colsum(ctx, r.dG, kG4, F, kG4, grad + off_of(L, rnn_name(P, "rnn.bias_ih", l)), wst)) != DDPPO_OK)
       return s;
-    if ((s = launch_colsum(ctx, r.dG, kG4, F, kG4, grad + off_of(L, rnn_name(P, "rnn.bias_hh", l)), st)) != DDPPO_OK)
+    if ((s = launch_colsum(ctx, r.dG, kG4, F, kG4, grad + off_of(L, rnn_name(P, "rnn.bias_hh", l)), wst)) != DDPPO_OK)
       return s;
     // input gradient: into the layer below's dH, or dx = dG W_ih [F][576] for layer 0
     float* dxl = l == 0 ? P.dxin : P.rnn[l - 1].dH;
@@ -1710,12 +1741,13 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   vis_mask_kernel<<<blocks_for(ctx, (size_t)F * 512), kThreads, 0, st>>>(P.dxin, P.vis, F, P.dvis);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
-  // visual FC: dW = dVpre^T flat, db = colsum(dVpre), dflat = dVpre W
+  // visual FC: dW = dVpre^T flat, db = colsum(dVpre) (side stream), dflat = dVpre W
+  if (wst != st) DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, wst));
   if ((s = gemm_split(ctx, GemmTC{P.dvis, 1, 512, P.flat, 1, P.fc_in, grad + off_of(L, "visual_fc.weight"), P.fc_in,
                                   512, P.fc_in, F},
-                      P, st)) != DDPPO_OK)
+                      P, wst, P.part2)) != DDPPO_OK)
     return s;
-  if ((s = launch_colsum(ctx, P.dvis, 512, F, 512, grad + off_of(L, "visual_fc.bias"), st)) != DDPPO_OK) return s;
+  if ((s = launch_colsum(ctx, P.dvis, 512, F, 512, grad + off_of(L, "visual_fc.bias"), wst)) != DDPPO_OK) return s;
   if ((s = gemm_split(ctx, GemmTC{P.dvis, 512, 1, prm + off_of(L, "visual_fc.weight"), 1, P.fc_in, P.dflat, P.fc_in,
                                   F, P.fc_in, 512},
                       P, st)) != DDPPO_OK)
@@ -1774,6 +1806,7 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   gn_param_reduce_all_kernel<<<a.ch_off[a.n], kThreads, 0, st>>>(a);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  if (wst != st) DDPPO_CUDA_TRY(ctx, fork_to(ctx, wst, st));  // join: every weight gradient is final
   return DDPPO_OK;
 }
 
@@ -1821,7 +1854,9 @@ extern "C" ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const
   if (dy) {
     to_bf16_kernel<<<blocks_for(ctx, ny), kThreads, 0, st>>>(dy, ny, dyb);
     ctx->count(1);
-    return conv_bwd(ctx, g, x, xb, w, nullptr, dyb, dw, Ci == 1 ? nullptr : dx, 0, sc, st);
+    ddppo_status r = conv_wgrad(ctx, g, x, xb, dyb, dw, sc, st);
+    if (r != DDPPO_OK || Ci == 1 || dx == nullptr) return r;
+    return conv_dgrad(ctx, g, w, nullptr, dyb, dx, 0, sc, st);
   }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;

@@ -70,6 +70,11 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uin
       "l"(reinterpret_cast<uint64_t>(map)), "r"(s_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ bool elect_one() {
   uint32_t p = 0;
   asm volatile(
@@ -103,9 +108,13 @@ struct TcArgs {
   int Ho, Wo, s, p, k;    // im2col traversal geometry (output pixel grid of the box walk)
   int C, nsl;             // channels of the im2col'd tensor, C / CS
   int flip;               // DGRAD: tap (u, v) reads offset (k-1-u, k-1-v)
-  float* out;
-  long long ldc, zs;      // row stride of the output, split stride (split-K partials)
-  int accumulate;
+  float* out;             // result: [M][ldc] rows (FPROP / DGRAD), or the weight gradient (wg)
+  long long ldc;
+  int accumulate;         // out (+)= (FPROP / DGRAD)
+  int splits;             // > 1: partial tiles in part[z][M][N]; the last split of a tile sums them
+  float* part;
+  int* cnt;               // per-tile arrival counters (zero; reset by the last arrival)
+  int wg, Cr;             // WGRAD: write out[o][c < Cr][tap] (PyTorch order; rows are (tap, c < C))
 };
 
 // first output pixel q -> im2col box coordinates (W, H, N) of its receptive field's corner
@@ -116,6 +125,27 @@ __device__ __forceinline__ void pix_coords(const TcArgs& a, int q, int& w, int& 
   const int oh = r / a.Wo;
   h = oh * a.s - a.p;
   w = (r - oh * a.Wo) * a.s - a.p;
+}
+
+// 8 consecutive output columns of one row: rows of out (FPROP / DGRAD, optionally accumulated), or
+// the weight gradient in PyTorch order out[o][c][tap] for row = tap * C + c (c < Cr)
+__device__ __forceinline__ void store_final(const TcArgs& a, int row, int col, const float (&v)[8]) {
+  if (!a.wg) {
+    float4* o = reinterpret_cast<float4*>(a.out + (long long)row * a.ldc + col);
+    float4 v0 = make_float4(v[0], v[1], v[2], v[3]), v1 = make_float4(v[4], v[5], v[6], v[7]);
+    if (a.accumulate) {
+      const float4 p0 = o[0], p1 = o[1];
+      v0.x += p0.x; v0.y += p0.y; v0.z += p0.z; v0.w += p0.w;
+      v1.x += p1.x; v1.y += p1.y; v1.z += p1.z; v1.w += p1.w;
+    }
+    o[0] = v0;
+    o[1] = v1;
+  } else {
+    const int kk = a.k * a.k, tap = row / a.C, c = row - tap * a.C;
+    if (c >= a.Cr) return;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a.out[((long long)(col + e) * a.Cr + c) * kk + tap] = v[e];
+  }
 }
 
 template <int CS, int BN, int NPL, int MODE, int STAGES>
@@ -267,17 +297,17 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
   } else {
     // ------------------------------------------------------------ epilogue (TMEM -> global)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int et = threadIdx.x - 64;  // 0..127
     int acc = 0;
     uint32_t aph = 0;
     for (int wi = blockIdx.x; wi < a.n_work; wi += gridDim.x) {
       const int z = wi / tiles, t = wi - z * tiles;
       const int m0 = (t % a.tiles_m) * kBM, n0 = (t / a.tiles_m) * BN;
-      const bool part = a.zs != 0;
-      float* out = a.out + (part ? (long long)z * a.zs : 0LL);
+      const int row = m0 + q * 32 + lane;
+      const bool rok = row < a.M;
       mb_wait(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = m0 + q * 32 + lane;
-      float* orow = out + (long long)row * a.ldc + n0;
+      float* prow = a.splits > 1 ? a.part + ((long long)z * a.M + row) * a.N + n0 : nullptr;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 8) {
         uint32_t r[8];
@@ -286,26 +316,58 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
                      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                      : "r"(ta));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < a.M && n0 + c0 < a.N) {
-          float4 v0 = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]),
-                                  __uint_as_float(r[3]));
-          float4 v1 = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]),
-                                  __uint_as_float(r[7]));
-          float4* o = reinterpret_cast<float4*>(orow + c0);
-          if (a.accumulate && !part) {
-            const float4 p0 = o[0], p1 = o[1];
-            v0.x += p0.x; v0.y += p0.y; v0.z += p0.z; v0.w += p0.w;
-            v1.x += p1.x; v1.y += p1.y; v1.z += p1.z; v1.w += p1.w;
+        if (rok && n0 + c0 < a.N) {
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[e]);
+          if (prow) {  // this split's partial tile
+            reinterpret_cast<float4*>(prow + c0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+            reinterpret_cast<float4*>(prow + c0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+          } else {
+            store_final(a, row, n0 + c0, v);
           }
-          o[0] = v0;
-          o[1] = v1;
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mb_arrive(&tempty[acc]);
+      mb_arrive(&tempty[acc]);  // the accumulator is free for the MMA warp's next tile
       if (++acc == 2) {
         acc = 0;
         aph ^= 1u;
+      }
+      if (a.splits > 1) {
+        // distributed split-K fixup: every work item is resident (n_work <= grid, one item per CTA),
+        // so the S splits of a tile wait for one another, then split z adds rows
+        // [z*128/S, (z+1)*128/S) of the S partial tiles in split order (deterministic) and writes them
+        int* cnt = a.cnt + 2 * t;
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) {
+          atomicAdd(cnt, 1);
+          while (ld_acquire_gpu(cnt) < a.splits) {
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int r0 = z * kBM / a.splits, r1 = (z + 1) * kBM / a.splits;
+        const int cpr = BN / 8;  // 8-column chunks per row
+        for (int i = et; i < (r1 - r0) * cpr; i += 128) {
+          const int rr = m0 + r0 + i / cpr, c0 = (i % cpr) * 8;
+          if (rr >= a.M || n0 + c0 >= a.N) continue;
+          float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          const float* pr = a.part + (long long)rr * a.N + n0 + c0;
+          for (int zz = 0; zz < a.splits; ++zz) {
+            const float4 p0 = __ldcg(reinterpret_cast<const float4*>(pr + (long long)zz * a.M * a.N));
+            const float4 p1 = __ldcg(reinterpret_cast<const float4*>(pr + (long long)zz * a.M * a.N) + 1);
+            v[0] += p0.x; v[1] += p0.y; v[2] += p0.z; v[3] += p0.w;
+            v[4] += p1.x; v[5] += p1.y; v[6] += p1.z; v[7] += p1.w;
+          }
+          store_final(a, rr, n0 + c0, v);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // the last split to finish resets the tile's counters for the next launch
+        if (et == 0 && atomicAdd(cnt + 1, 1) == a.splits - 1) {
+          cnt[0] = 0;
+          cnt[1] = 0;
+        }
       }
     }
   }
@@ -375,7 +437,8 @@ ddppo_status map_2d(ddppo_ctx* ctx, CUtensorMap* m, const __nv_bfloat16* x, int6
 }
 
 template <int CS, int BN, int NPL, int MODE>
-ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, cudaStream_t st) {
+ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min_iters, int max_splits, int slot,
+                 cudaStream_t st) {
   constexpr uint32_t kStage = TcCfg<CS, BN, NPL, MODE, 1>::kStage;
   constexpr int STAGES = (int)std::min<uint32_t>(8u, (200u * 1024u) / kStage);
   static_assert(STAGES >= 2, "stage too large");
@@ -387,22 +450,24 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, cudaStr
     attr = true;
   }
   const int per_sm = std::max(1, (int)((227u * 1024u) / (Cfg::kSmem + 2048)));
-  const int grid = std::max(1, std::min(a.n_work, ctx->sm_count * std::min(per_sm, 2)));
+  // slot 1 = the side stream (weight gradients beside the critical path): at most ~half the SMs
+  const int cap = slot == 0 ? ctx->sm_count * std::min(per_sm, 2) : ctx->sm_count / 2;
+  // split-K over the k-iterations: ~one work item per resident CTA, each >= min_iters iterations; the
+  // split tiles' fixup needs every work item resident at once (n_work <= grid)
+  const int tiles = a.tiles_m * a.tiles_n;
+  int splits = 1;
+  if (max_splits > 1 && tiles < cap)
+    splits = std::max(1, std::min({cap / tiles, a.n_k / std::max(1, min_iters), max_splits}));
+  a.kper = (a.n_k + splits - 1) / splits;
+  splits = (a.n_k + a.kper - 1) / a.kper;
+  a.splits = splits;
+  a.n_work = tiles * splits;
+  DDPPO_REQUIRE(ctx, splits == 1 || (2 * tiles <= kMaxTileCounters / 2 && a.part), "tconv: split-K needs scratch");
+  const int grid = std::max(1, std::min(a.n_work, cap));
   kern<<<grid, kThreadsTC, Cfg::kSmem, st>>>(maps[0], maps[1], maps[2], maps[3], a);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
-}
-
-// split-K: enough (tile, split) work items for ~2 per SM, each >= min_iters k-iterations
-void plan_splits(ddppo_ctx* ctx, TcArgs& a, int min_iters, int max_splits) {
-  const int tiles = a.tiles_m * a.tiles_n;
-  int splits = 1;
-  if (max_splits > 1)
-    splits = std::max(1, std::min({(2 * ctx->sm_count + tiles - 1) / tiles, a.n_k / std::max(1, min_iters), max_splits}));
-  a.kper = (a.n_k + splits - 1) / splits;
-  splits = (a.n_k + a.kper - 1) / a.kper;
-  a.n_work = tiles * splits;
 }
 
 }  // namespace
@@ -410,11 +475,11 @@ void plan_splits(ddppo_ctx* ctx, TcArgs& a, int min_iters, int max_splits) {
 // FPROP (flip = 0) or stride-1 DGRAD (flip = 1) over x[F][H][W][C]:
 //   out[q][o] (+)= sum_{tap, c} x[q @ tap][c] w[o][tap*C + c],  q over the F x Ho x Wo output grid.
 // w: [N][k*k*C] bf16 (plane stride wplane elements when planes == 2; x likewise xplane).
-// With `partial` (>= splits*M*N floats) and a long k loop the work is split over K; the caller's
-// reduction then sums the partials (returns the split count in *splits_out, 1 = written to out).
+// With `partial` (>= splits*M*N floats) and a long k loop the work is split over K; each tile's last
+// split adds the partial tiles in split order and writes out (*splits_out = 1: nothing left to do).
 ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xplane, int F, int H, int W, int C,
                               int k, int s, int p, int flip, const __nv_bfloat16* w, int64_t wplane, int N, int planes,
-                              float* out, int64_t ldc, int accumulate, float* partial, int max_splits,
+                              float* out, int64_t ldc, int accumulate, float* partial, int max_splits, int slot,
                               int* splits_out, cudaStream_t st) {
   DDPPO_REQUIRE(ctx, C % 32 == 0 && N % 8 == 0 && ldc % 4 == 0, "tconv: C % 32 == 0, N % 8 == 0 required");
   DDPPO_REQUIRE(ctx, !flip || s == 1, "tconv: transposed taps only for stride-1 convolutions");
@@ -437,13 +502,13 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
   a.n_k = k * k * a.nsl;
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (N + bn - 1) / bn;
-  plan_splits(ctx, a, 4, partial ? max_splits : 1);
-  const int splits = a.n_work / (a.tiles_m * a.tiles_n);
-  a.out = splits > 1 ? partial : out;
-  a.ldc = splits > 1 ? N : ldc;
-  a.zs = splits > 1 ? (long long)a.M * N : 0;
+  if (!partial) max_splits = 1;
+  a.out = out;
+  a.ldc = ldc;
+  a.part = partial;
+  a.cnt = ctx->d_tile_cnt + (size_t)slot * (kMaxTileCounters / 2);
   a.accumulate = accumulate;
-  if (splits_out) *splits_out = splits;
+  if (splits_out) *splits_out = 1;  // the split sum happens inside the kernel
   CUtensorMap maps[4];
   memset(maps, 0, sizeof(maps));
   const int K = k * k * C;
@@ -455,7 +520,7 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
   if (r == DDPPO_OK && planes == 2) r = map_2d(ctx, &maps[3], w + wplane, N, K, cs, bn);
   if (r != DDPPO_OK) return r;
 #define TC_CASE(CS_, BN_, NPL_) \
-  if (cs == CS_ && bn == BN_ && planes == NPL_) return run<CS_, BN_, NPL_, TC_FWD>(ctx, maps, a, st);
+  if (cs == CS_ && bn == BN_ && planes == NPL_) return run<CS_, BN_, NPL_, TC_FWD>(ctx, maps, a, 4, max_splits, slot, st);
   TC_CASE(32, 32, 1) TC_CASE(32, 64, 1) TC_CASE(32, 128, 1) TC_CASE(64, 32, 1) TC_CASE(64, 64, 1)
   TC_CASE(64, 128, 1) TC_CASE(32, 32, 2) TC_CASE(32, 64, 2) TC_CASE(32, 128, 2) TC_CASE(64, 32, 2)
   TC_CASE(64, 64, 2) TC_CASE(64, 128, 2)
@@ -464,12 +529,12 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
   return DDPPO_ERR_CONFIG;
 }
 
-// WGRAD: partial[z][(u*k+v)*C + c][o] = sum over the split's output pixels q of
-//   x[q @ (u, v)][c] * dy[q][o]   (x [F][H][W][C] bf16, dy [F*Ho*Wo][N] bf16); splits returned in
-// *splits_out (partials always: the caller's reduction writes the weight gradient).
+// WGRAD: dw[o][c][u][v] (PyTorch order, c < Cr) = sum over the output pixels q of
+//   x[q @ (u, v)][c] * dy[q][o]   (x [F][H][W][C] bf16, dy [F*Ho*Wo][N] bf16); split over pixels
+// with partial tiles in `partial`, summed in split order by each tile's last split.
 ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, int H, int W, int C, int k, int s,
-                                int p, const __nv_bfloat16* dy, int N, float* partial, int max_splits, int* splits_out,
-                                cudaStream_t st) {
+                                int p, const __nv_bfloat16* dy, int N, float* dw, int Cr, float* partial, int max_splits,
+                                int slot, int* splits_out, cudaStream_t st) {
   DDPPO_REQUIRE(ctx, C % 32 == 0 && N % 8 == 0, "tconv wgrad: C % 32 == 0, N % 8 == 0 required");
   DDPPO_REQUIRE(ctx, ((uintptr_t)x & 15) == 0 && ((uintptr_t)dy & 15) == 0 && ((uintptr_t)partial & 15) == 0,
                 "tconv wgrad: 16-byte aligned operands required");
@@ -490,20 +555,19 @@ ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, i
   a.n_k = (pix + kPix - 1) / kPix;
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (N + bn - 1) / bn;
-  plan_splits(ctx, a, 2, max_splits);
-  const int splits = a.n_work / (a.tiles_m * a.tiles_n);
-  a.out = partial;
-  a.ldc = N;
-  a.zs = (long long)a.M * N;
-  a.accumulate = 0;
-  if (splits_out) *splits_out = splits;
+  a.out = dw;
+  a.part = partial;
+  a.cnt = ctx->d_tile_cnt + (size_t)slot * (kMaxTileCounters / 2);
+  a.wg = 1;
+  a.Cr = Cr;
+  if (splits_out) *splits_out = 1;
   CUtensorMap maps[4];
   memset(maps, 0, sizeof(maps));
   ddppo_status r = map_im2col(ctx, &maps[0], x, F, H, W, C, k, s, p, cs);
   if (r == DDPPO_OK) r = map_2d(ctx, &maps[2], dy, pix, N, bn, kPix);
   if (r != DDPPO_OK) return r;
-  if (cs == 32 && bn == 32) return run<32, 32, 1, TC_WGRAD>(ctx, maps, a, st);
-  if (cs == 32 && bn == 64) return run<32, 64, 1, TC_WGRAD>(ctx, maps, a, st);
-  if (cs == 64 && bn == 32) return run<64, 32, 1, TC_WGRAD>(ctx, maps, a, st);
-  return run<64, 64, 1, TC_WGRAD>(ctx, maps, a, st);
+  if (cs == 32 && bn == 32) return run<32, 32, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
+  if (cs == 32 && bn == 64) return run<32, 64, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
+  if (cs == 64 && bn == 32) return run<64, 32, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
+  return run<64, 64, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
 }
