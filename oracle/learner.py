@@ -16,8 +16,10 @@ DEFAULT_CFG = dict(gamma=0.99, tau=0.95, normalize_adv=True, adv_eps=1e-5,
                    adam_eps=1e-8, max_grad_norm=0.5)
 
 
-def minibatch_grad(arch, params, ro, adv, ret, envs, mean_invstd, cfg, hidden=512):
-    """Local gradient and loss stats of one rank on one minibatch of envs."""
+def minibatch_grad(arch, params, ro, adv, ret, envs, mean_invstd, cfg, hidden=512, adopt=None):
+    """Local gradient and loss stats of one rank on one minibatch of envs.  `adopt(batch, cache)`
+    (tests only) may replace the forward's discrete ReLU / max-pool decisions in `cache` before the
+    backward (reading R6: near-ties decided by the kernels)."""
     L = np.asarray(ro["length"])[envs]
     T_run = int(L.max())
     batch = {"goal": ro["goal"][envs, :T_run], "prev_action": ro["prev_action"][envs, :T_run],
@@ -26,6 +28,8 @@ def minibatch_grad(arch, params, ro, adv, ret, envs, mean_invstd, cfg, hidden=51
         batch["obs"] = ro["obs"][envs, :T_run]
         batch["c0"] = ro["c0"][envs]
     logits, values, cache = models.forward(arch, params, batch, hidden=hidden)
+    if adopt is not None:
+        adopt(batch, cache)
     B = len(envs)
     valid = (np.arange(T_run)[None, :] < L[:, None])
     flat = lambda a: np.asarray(a)[..., :T_run].reshape(B * T_run)  # noqa: E731
