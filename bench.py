@@ -282,9 +282,12 @@ def main():
     pinned = []
     for i in range(n_roll):
         hb = lrn.pinned_host_buffers()
+        src = lrn.host_fields(rollouts[i])  # frames as bf16 depth (+ uint8 RGB): the rollout's wire format
         for k in hb:
             if k not in ("__arena__", "perms"):
-                hb[k].copy_(torch.from_numpy(np.ascontiguousarray(rollouts[i][k])).reshape(hb[k].shape))
+                v = src[k]
+                hb[k].copy_((v if isinstance(v, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v)))
+                            .reshape(hb[k].shape))
         pinned.append(hb)
 
     def step(i):

@@ -156,8 +156,11 @@ typedef struct {
   int32_t E, T, ld, B;
   int32_t T_run;              /* steps to run: max len over the minibatch (host value)  */
   int32_t n_valid;            /* sum over the B envs of min(len, T_run) (host value)    */
-  const float* obs;           /* DEPTH: [E][T][1][64][64]; RGBD: [E][T][4][256][256]; else NULL */
+  const uint16_t* obs;        /* depth frames as bf16 bits, values in [0, 1]:     */
+                              /* DEPTH [E][T][1][64][64]; RGBD [E][T][1][256][256]; else NULL */
   const float* c0;            /* LSTM cell state before step 0, like h0 (DEPTH / RGBD)      */
+  const uint8_t* obs_rgb;     /* RGBD: camera bytes [E][T][3][256][256] (normalised channel-   */
+                              /* wise on the device); else NULL                        */
 } ddppo_batch;
 
 /* a5: logits [B][T_run][A], values [B][T_run]; saves activations in ws for the backward. */
@@ -254,8 +257,9 @@ typedef struct {
   const int32_t* host_len;    /* [E] host copy of len */
   const int32_t* host_perms;  /* [epochs][E] host copy of perms */
   int32_t E, T, ld;
-  const float* obs;           /* as ddppo_batch::obs (DEPTH / RGBD, else NULL) */
+  const uint16_t* obs;        /* as ddppo_batch::obs (DEPTH / RGBD, else NULL) */
   const float* c0;            /* as ddppo_batch::c0  (DEPTH / RGBD, else NULL) */
+  const uint8_t* obs_rgb;     /* as ddppo_batch::obs_rgb (RGBD, else NULL) */
 } ddppo_rollout;
 
 typedef struct {

@@ -108,15 +108,30 @@ def ddppo_adv_norm(ctx, stats3, eps, mean_invstd, stream=None):
     _call(ctx, "ddppo_adv_norm", f64(stats3), eps, f32(mean_invstd), _stream(stream))
 
 
-def make_batch(goal, prev_action, mask, h0, length, env_idx, E, T, ld, B, T_run, n_valid, obs=None, c0=None):
+def make_batch(goal, prev_action, mask, h0, length, env_idx, E, T, ld, B, T_run, n_valid, obs=None, c0=None,
+               obs_rgb=None):
+    """obs: depth frames (torch.bfloat16); obs_rgb: RGB camera bytes (torch.uint8, RGB-D only)."""
     b = Batch()
     b.goal, b.prev_action, b.mask, b.h0 = f32(goal), i32(prev_action), f32(mask), f32(h0)
     b.len, b.env_idx = i32(length), i32(env_idx)
     b.E, b.T, b.ld, b.B, b.T_run, b.n_valid = E, T, ld, B, T_run, n_valid
-    b.obs = f32(obs) if obs is not None else None
+    b.obs = dptr(obs, "bfloat16") if obs is not None else None
     b.c0 = f32(c0) if c0 is not None else None
-    b._keep = (goal, prev_action, mask, h0, length, env_idx, obs, c0)  # the struct holds raw device pointers
+    b.obs_rgb = u8(obs_rgb) if obs_rgb is not None else None
+    b._keep = (goal, prev_action, mask, h0, length, env_idx, obs, c0, obs_rgb)  # the struct holds raw pointers
     return b
+
+
+def visual_obs(obs, rgbd):
+    """A synth-style float frame array [E][T][C][H][W] -> the ABI's observation tensors (host, torch):
+    {"obs": depth channel as bf16, "obs_rgb": RGB channels as uint8 (RGB-D only)} -- dtype
+    marshalling only (the generator's depth values are bf16-exact and its RGB values integers)."""
+    import torch
+    a = np.asarray(obs, dtype=np.float32)
+    out = {"obs": torch.from_numpy(np.ascontiguousarray(a[:, :, 3:4] if rgbd else a)).to(torch.bfloat16)}
+    if rgbd:
+        out["obs_rgb"] = torch.from_numpy(np.ascontiguousarray(a[:, :, :3]).astype(np.uint8))
+    return out
 
 
 def ddppo_policy_fwd(ctx, desc, params, batch, logits, values, ws, stream=None):

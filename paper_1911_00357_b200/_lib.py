@@ -43,7 +43,7 @@ class TensorInfo(ctypes.Structure):
 class Batch(ctypes.Structure):
     _fields_ = [("goal", c_vp), ("prev_action", c_vp), ("mask", c_vp), ("h0", c_vp), ("len", c_vp),
                 ("env_idx", c_vp), ("E", c_i32), ("T", c_i32), ("ld", c_i32), ("B", c_i32), ("T_run", c_i32),
-                ("n_valid", c_i32), ("obs", c_vp), ("c0", c_vp)]
+                ("n_valid", c_i32), ("obs", c_vp), ("c0", c_vp), ("obs_rgb", c_vp)]
 
 
 class LossInputs(ctypes.Structure):
@@ -68,7 +68,7 @@ class Rollout(ctypes.Structure):
     _fields_ = [("rew", c_vp), ("val", c_vp), ("done", c_vp), ("len", c_vp), ("goal", c_vp), ("prev_action", c_vp),
                 ("mask", c_vp), ("h0", c_vp), ("action", c_vp), ("logp_old", c_vp), ("perms", c_vp),
                 ("host_len", c_vp), ("host_perms", c_vp), ("E", c_i32), ("T", c_i32), ("ld", c_i32),
-                ("obs", c_vp), ("c0", c_vp)]
+                ("obs", c_vp), ("c0", c_vp), ("obs_rgb", c_vp)]
 
 
 class LearnerCfg(ctypes.Structure):

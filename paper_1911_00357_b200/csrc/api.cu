@@ -490,6 +490,7 @@ ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_mode
       b.T_run = mbs[k].T_run;  // a4: the minibatch runs to its longest env
       b.n_valid = mbs[k].n_valid;
       b.obs = ro->obs;
+      b.obs_rgb = ro->obs_rgb;
       b.c0 = ro->c0;
       float* st_out = w.stats + (size_t)k * 8;
       const float* mis = cfg->normalize_adv ? w.mean_invstd : nullptr;
@@ -608,6 +609,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
                 "learner_step: normalize_adv and loss.normalize_adv must agree");
   const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
   DDPPO_REQUIRE(ctx, !visual || (ro->obs && ro->c0), "learner_step: the visual agents need obs and c0");
+  DDPPO_REQUIRE(ctx, host_desc->arch != DDPPO_ARCH_RGBD_R50_LSTM2 || ro->obs_rgb, "learner_step: RGB-D needs obs_rgb");
   size_t need = 0;
   ddppo_status s =
       ddppo_learner_workspace_size(host_desc, ro->E, ro->T, ro->ld, cfg->minibatches, cfg->epochs, &need);

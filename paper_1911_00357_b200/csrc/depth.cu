@@ -30,37 +30,56 @@ constexpr int kImg = 64;        // Depth input resolution (configs[2])
 constexpr int kImgRgbd = 256;   // RGB-D input resolution (configs[3])
 
 // ------------------------------------------------------------------ kernels
-// obs [E][T][1][64][64] (gathered through env_idx) -> x0 [F][64][64][1]
-__global__ void gather_obs_kernel(const float* __restrict__ obs, const int32_t* __restrict__ env_idx, int T, int T_run,
-                                  int F, float* __restrict__ x0) {
-  const size_t per = (size_t)kImg * kImg;
+// obs [E][T][1][64][64] bf16 (gathered through env_idx) -> x0 [F][64][64][1] fp32 (the SIMT stem's input)
+__global__ void gather_obs_kernel(const __nv_bfloat16* __restrict__ obs, const int32_t* __restrict__ env_idx, int T,
+                                  int T_run, int F, float* __restrict__ x0) {
+  const size_t per = (size_t)kImg * kImg / 8;  // 8 pixels (16 bytes) per item
   const size_t n = (size_t)F * per;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int f = (int)(i / per);
     const int b = f / T_run, t = f - b * T_run;
-    x0[i] = obs[((size_t)env_idx[b] * T + t) * per + (i % per)];
+    const uint4 raw = reinterpret_cast<const uint4*>(obs + ((size_t)env_idx[b] * T + t) * kImg * kImg)[i % per];
+    const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(&raw);
+    float4* o = reinterpret_cast<float4*>(x0) + 2 * i;
+    o[0] = make_float4(__bfloat162float(v[0]), __bfloat162float(v[1]), __bfloat162float(v[2]), __bfloat162float(v[3]));
+    o[1] = make_float4(__bfloat162float(v[4]), __bfloat162float(v[5]), __bfloat162float(v[6]), __bfloat162float(v[7]));
   }
 }
 
-// RGB-D prologue: obs [E][T][4][256][256] -> channel-wise RGB normalisation, 2x2 average
-// pooling -> x0 [F][128][128][8] fp32 NHWC (channels 4..7 zero: the stem's implicit GEMM reads 8
-// channels per 16-byte piece) and its bf16 hi / lo planes
+// RGB-D prologue: camera bytes rgb [E][T][3][256][256] and depth [E][T][1][256][256] (bf16) ->
+// channel-wise RGB normalisation, 2x2 average pooling -> x0 [F][128][128][8] fp32 NHWC
+// (channels 4..7 zero: the stem's implicit GEMM reads 8 channels per 16-byte piece) and its bf16
+// hi / lo planes
 __constant__ float kRgbMean[3] = {0.485f * 255.f, 0.456f * 255.f, 0.406f * 255.f};
 __constant__ float kRgbStd[3] = {0.229f * 255.f, 0.224f * 255.f, 0.225f * 255.f};
-__global__ void rgbd_prologue_kernel(const float* __restrict__ obs, const int32_t* __restrict__ env_idx, int T,
-                                     int T_run, int F, int Hin, float* __restrict__ x0, __nv_bfloat16* __restrict__ x0b) {
-  // thread = (frame, output row, pair of output columns): one float4 per input channel and row
+__global__ void rgbd_prologue_kernel(const uint8_t* __restrict__ rgb, const __nv_bfloat16* __restrict__ depth,
+                                     const int32_t* __restrict__ env_idx, int T, int T_run, int F, int Hin,
+                                     float* __restrict__ x0, __nv_bfloat16* __restrict__ x0b) {
+  // thread = (frame, output row, pair of output columns): 4 input columns of 2 rows per channel
   const int Ho = Hin / 2, Wo = Hin / 2, WP = Wo / 2;
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item >= F * Ho * WP) return;
   const int jp = item % WP, ii = (item / WP) % Ho, f = item / (WP * Ho);
   const int b = f / T_run, t = f - b * T_run;
-  const float* src = obs + ((size_t)env_idx[b] * T + t) * 4 * Hin * Hin + (size_t)(2 * ii) * Hin + 4 * jp;
-  float4 r0[4], r1[4];
+  const size_t fr = (size_t)env_idx[b] * T + t, px = (size_t)(2 * ii) * Hin + 4 * jp;
+  float r0[4][4], r1[4][4];  // [channel][column]
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    r0[c] = *reinterpret_cast<const float4*>(src + (size_t)c * Hin * Hin);
-    r1[c] = *reinterpret_cast<const float4*>(src + (size_t)c * Hin * Hin + Hin);
+  for (int c = 0; c < 3; ++c) {
+    const uint8_t* s = rgb + (fr * 3 + c) * Hin * Hin + px;
+    const uchar4 a = *reinterpret_cast<const uchar4*>(s), bb = *reinterpret_cast<const uchar4*>(s + Hin);
+    r0[c][0] = a.x; r0[c][1] = a.y; r0[c][2] = a.z; r0[c][3] = a.w;
+    r1[c][0] = bb.x; r1[c][1] = bb.y; r1[c][2] = bb.z; r1[c][3] = bb.w;
+  }
+  {
+    const __nv_bfloat16* s = depth + fr * Hin * Hin + px;
+    const uint2 a = *reinterpret_cast<const uint2*>(s), bb = *reinterpret_cast<const uint2*>(s + Hin);
+    const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(&a);
+    const __nv_bfloat16* bv = reinterpret_cast<const __nv_bfloat16*>(&bb);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      r0[3][q] = __bfloat162float(av[q]);
+      r1[3][q] = __bfloat162float(bv[q]);
+    }
   }
   const size_t n = (size_t)F * Ho * Wo * 8;
 #pragma unroll
@@ -69,8 +88,7 @@ __global__ void rgbd_prologue_kernel(const float* __restrict__ obs, const int32_
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const float m = c < 3 ? kRgbMean[c] : 0.f, inv = c < 3 ? 1.f / kRgbStd[c] : 1.f;
-      const float a0 = h ? r0[c].z : r0[c].x, a1 = h ? r0[c].w : r0[c].y;
-      const float b0 = h ? r1[c].z : r1[c].x, b1 = h ? r1[c].w : r1[c].y;
+      const float a0 = r0[c][2 * h], a1 = r0[c][2 * h + 1], b0 = r1[c][2 * h], b1 = r1[c][2 * h + 1];
       v[c] = 0.25f * (((a0 - m) * inv + (a1 - m) * inv) + ((b0 - m) * inv + (b1 - m) * inv));
       v[c + 4] = 0.f;
     }
@@ -117,6 +135,7 @@ struct WeightPrep {
     const float* W;
     __nv_bfloat16 *wr, *wd;  // wd nullable (no input gradient)
     int Co, Ci, Cp, k;
+    int wd_planes;           // 2: Wd also as a lo plane (at wd + Co*Cp*k*k), for hi / lo input gradients
   } it[kMaxConvs];
 };
 __global__ void weights_prep_kernel(const WeightPrep prep) {
@@ -136,7 +155,10 @@ __global__ void weights_prep_kernel(const WeightPrep prep) {
   const __nv_bfloat16 hi = __float2bfloat16_rn(w);
   t.wr[j] = hi;
   t.wr[n + j] = __float2bfloat16_rn(w - __bfloat162float(hi));
-  if (t.wd && c < Ci) t.wd[c * (kk * Co) + uv * Co + o] = hi;
+  if (t.wd && c < Ci) {
+    t.wd[c * (kk * Co) + uv * Co + o] = hi;
+    if (t.wd_planes == 2) t.wd[n + c * (kk * Co) + uv * Co + o] = t.wr[n + j];
+  }
 }
 // fp32 -> bf16 hi / lo planes (plane = n)
 __global__ void to_planes_kernel(const float* __restrict__ x, size_t n, __nv_bfloat16* __restrict__ xb) {
@@ -397,6 +419,14 @@ __device__ __forceinline__ void gn_stage_bwd(float* s_dz, float* s_z, float* s_y
 }
 __host__ __device__ constexpr size_t gn_bwd_smem(int nv, int nt) { return (size_t)3 * nv * nt * sizeof(float); }
 
+// the GN input gradient as bf16 (lo == 0), or as hi / lo planes (x = hi + lo; lo plane at +lo elements)
+// for the deep encoder's input-gradient chain
+__device__ __forceinline__ void put_grad(__nv_bfloat16* dx, size_t lo, size_t i, float v) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  dx[i] = h;
+  if (lo) dx[lo + i] = __float2bfloat16_rn(v - __bfloat162float(h));
+}
+
 // dy_eff = dz * [z > 0] (relu_z nullable): GN backward per group
 //   dx = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),   dxhat = dy_eff * gamma
 // written as bf16 (it only feeds the bf16 gradient GEMMs), plus this frame's per-channel partials
@@ -407,7 +437,8 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_kernel(const float* __res
                                                             const float* __restrict__ y,
                                                             const float* __restrict__ stats,
                                                             const float* __restrict__ gamma, int HW, int C,
-                                                            __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
+                                                            __nv_bfloat16* __restrict__ dx, float* __restrict__ part,
+                                                            size_t lo) {
   __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
   __shared__ float pc[2][gn_bound(NV)];
   extern __shared__ __align__(16) float gsm[];
@@ -452,7 +483,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_kernel(const float* __res
     float d = s_dz[e];
     if (z && s_z[e] <= 0.f) d = 0.f;
     const float xh = (s_y[e] - mu) * rs;
-    dx[base + e] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
+    put_grad(dx, lo, base + e, rs * (d * gm - m1 - xh * m2));
   }
 }
 
@@ -607,7 +638,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_apply_kernel(const float*
                                                                    const float* __restrict__ stats,
                                                                    const float* __restrict__ gamma,
                                                                    const double* __restrict__ gpart, int HW, int C,
-                                                                   __nv_bfloat16* __restrict__ dx) {
+                                                                   __nv_bfloat16* __restrict__ dx, size_t lo) {
   __shared__ float sm1[kGroups], sm2[kGroups];
   extern __shared__ __align__(16) float gsm[];
   const int cap = NV * blockDim.x;
@@ -648,7 +679,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_apply_kernel(const float*
     float d = s_dz[e];
     if (z && s_z[e] <= 0.f) d = 0.f;
     const float xh = (s_y[e] - mu) * rs;
-    dx[base + e0 + e] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
+    put_grad(dx, lo, base + e0 + e, rs * (d * gm - m1 - xh * m2));
   }
 }
 
@@ -664,7 +695,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_cluster_kernel(const floa
                                                                      const float* __restrict__ stats,
                                                                      const float* __restrict__ gamma, int HW, int C,
                                                                      float* __restrict__ part,
-                                                                     __nv_bfloat16* __restrict__ dx) {
+                                                                     __nv_bfloat16* __restrict__ dx, size_t lo) {
   __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
   __shared__ float pc[2][gn_bound(NV)];
   __shared__ float sm1[kGroups], sm2[kGroups];
@@ -733,7 +764,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_cluster_kernel(const floa
     float d = s_dz[e];
     if (z && s_z[e] <= 0.f) d = 0.f;
     const float xh = (s_y[e] - mu) * rs;
-    dx[base + e0 + e] = __float2bfloat16_rn(rs * (d * gm - m1 - xh * m2));
+    put_grad(dx, lo, base + e0 + e, rs * (d * gm - m1 - xh * m2));
   }
 }
 
@@ -1016,6 +1047,7 @@ struct Plan {
   float *part_w = nullptr, *part2 = nullptr;  // side-stream partials (weight gradients)
   size_t part_w_n = 0;
   cudaStream_t side = nullptr;                // backward: weight gradients run here (fork / join)
+  int grad_planes = 1;                        // 2: the input-gradient chain carries bf16 hi / lo planes
   double* gn_gpart;           // GroupNorm per-chunk group partials (large frames)
   size_t bytes = 0;
 };
@@ -1033,6 +1065,10 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   P.rgbd = rgbd;
   P.layers = rgbd ? 2 : 1;
   P.fc_in = rgbd ? 2048 : 512;
+  // ResNet50/2 is ~50 layers deep: its input-gradient GEMMs take hi / lo operand planes so that the
+  // bf16 rounding does not accumulate along the chain (the earliest layers' gradients stay within
+  // north_star's 2e-2); the 20-layer ResNet18/2 chain is within it with single bf16 planes
+  P.grad_planes = rgbd ? 2 : 1;
   P.feat_hw = rgbd ? 16 : 4;
   size_t off = 0;
   auto take_bytes = [&](size_t bytes) {
@@ -1068,8 +1104,8 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
     c.stats = take((size_t)F * kGroups * 2);
     const size_t nw = (size_t)Co * k * k * Ci;
     c.wr_b = Ci > 1 ? take_b(2 * nw) : nullptr;
-    c.wd_b = (Ci > 1 && needs_dx) ? take_b(nw) : nullptr;
-    c.dyb = take_b(act);
+    c.wd_b = (Ci > 1 && needs_dx) ? take_b((size_t)P.grad_planes * nw) : nullptr;
+    c.dyb = take_b((size_t)P.grad_planes * act);
     max_act = std::max(max_act, std::max(act, (size_t)F * H * H * Ci));
     max_w = std::max(max_w, nw);
     const size_t S = ((size_t)c.Ho * c.Wo * Co + gn_chunk(Co) - 1) / gn_chunk(Co);
@@ -1315,8 +1351,11 @@ ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const
 
 // dx (+)= input gradient of the convolution (not for the stem)
 ddppo_status conv_dgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* w, const __nv_bfloat16* wd_b,
-                        const __nv_bfloat16* dy, float* dx, int accumulate_dx, const ConvScratch& sc, cudaStream_t st) {
+                        const __nv_bfloat16* dy, float* dx, int accumulate_dx, const ConvScratch& sc, cudaStream_t st,
+                        int planes = 1) {
   DDPPO_REQUIRE(ctx, !is_stem(g), "stem conv: no input gradient");
+  DDPPO_REQUIRE(ctx, planes == 1 || wd_b, "conv: hi / lo input gradients need prepared weights");
+  const int64_t dy_plane = planes == 2 ? (int64_t)g.M() * g.Co : 0, wd_plane = planes == 2 ? (int64_t)g.Co * g.K() : 0;
   const int K = g.K();
   // dgrad: dx[p][c] (+)= sum_{(u,v,o)} dy[tap^T(p; u, v)][o] W[o][c][u][v]
   if (!wd_b) {
@@ -1331,14 +1370,16 @@ ddppo_status conv_dgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* w, const
     // stride 1: the input gradient is the convolution of dy with the mirrored window
     int splits = 1;
     const int Md = g.F * g.H * g.W;
-    ddppo_status r = launch_tconv_fwd(ctx, dy, 0, g.F, g.Ho, g.Wo, g.Co, g.k, 1, g.k - 1 - g.p, 1, wd_b, 0, g.Ci, 1, dx,
-                                      g.Ci, accumulate_dx, sc.part, split_cap(sc, Md, g.Ci, 16), sc.slot, &splits, st);
+    ddppo_status r = launch_tconv_fwd(ctx, dy, dy_plane, g.F, g.Ho, g.Wo, g.Co, g.k, 1, g.k - 1 - g.p, 1, wd_b,
+                                      wd_plane, g.Ci, planes, dx, g.Ci, accumulate_dx, sc.part,
+                                      split_cap(sc, Md, g.Ci, 16), sc.slot, &splits, st);
     if (r != DDPPO_OK || splits == 1) return r;
     return launch_splitk_reduce(ctx, sc.part, splits, (int64_t)Md * g.Ci, Md, g.Ci, dx, g.Ci, accumulate_dx, st);
   }
   IGemm gm;
-  gm.a = op_pix(dy, g.H, g.W, g.Ho, g.Wo, g.Co, g, 1, 0);
-  gm.b = op_dense(IG_DENSE_K, wd_b, Kd, 0);
+  gm.a = op_pix(dy, g.H, g.W, g.Ho, g.Wo, g.Co, g, 1, dy_plane);
+  gm.b = op_dense(IG_DENSE_K, wd_b, Kd, wd_plane);
+  gm.planes = planes;
   gm.C = dx;
   gm.ldc = g.Ci;
   gm.M = g.F * g.H * g.W;
@@ -1405,7 +1446,8 @@ static ddppo_status gn_smem_attr(ddppo_ctx* ctx, K kernel, size_t bytes) {
 template <typename K>
 static ddppo_status gn_bwd_cluster(ddppo_ctx* ctx, K kern, int S, int F, int nt, size_t smem, const float* dz,
                                    const float* relu_z, const float* y, const float* stats, const float* gamma,
-                                   int HW, int C, float* part, __nv_bfloat16* dy, cudaStream_t st, bool* done) {
+                                   int HW, int C, float* part, __nv_bfloat16* dy, size_t lo, cudaStream_t st,
+                                   bool* done) {
   static std::map<std::pair<const void*, int>, bool> ok_cache;
   *done = false;
   ddppo_status s = gn_smem_attr(ctx, kern, smem);
@@ -1433,7 +1475,7 @@ static ddppo_status gn_bwd_cluster(ddppo_ctx* ctx, K kern, int S, int F, int nt,
     it = ok_cache.emplace(key, ok).first;
   }
   if (!it->second) return DDPPO_OK;
-  DDPPO_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, dz, relu_z, y, stats, gamma, HW, C, part, dy));
+  DDPPO_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, dz, relu_z, y, stats, gamma, HW, C, part, dy, lo));
   ctx->count(1);
   *done = true;
   return DDPPO_OK;
@@ -1441,7 +1483,7 @@ static ddppo_status gn_bwd_cluster(ddppo_ctx* ctx, K kern, int S, int F, int nt,
 
 ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const float* relu_z, const float* y,
                     const float* stats, const float* gamma, __nv_bfloat16* dy, float* dgamma, float* dbeta,
-                    float* part, double* gpart, cudaStream_t st, bool reduce_params = true) {
+                    float* part, double* gpart, cudaStream_t st, bool reduce_params = true, size_t lo = 0) {
   ddppo_status s = DDPPO_OK;
   const int nt = gn_threads(C);
   DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");
@@ -1452,7 +1494,7 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
   do {                                                                                                       \
     s = gn_smem_attr(ctx, gn_bwd_kernel<NV>, gn_bwd_smem(NV, nt));                                           \
     if (s != DDPPO_OK) return s;                                                                             \
-    gn_bwd_kernel<NV><<<F, nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, HW, C, dy, part);     \
+    gn_bwd_kernel<NV><<<F, nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, HW, C, dy, part, lo); \
   } while (0)
     if (nv <= 4) GN_BWD(4);
     else if (nv <= 8) GN_BWD(8);
@@ -1471,12 +1513,12 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
     gn_bwd_part_kernel<NV><<<dim3(S, F), nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, HW, C,  \
                                                                        gpart, part);                        \
     gn_bwd_apply_kernel<NV><<<dim3(S, F), nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, gpart, \
-                                                                        HW, C, dy);                         \
+                                                                        HW, C, dy, lo);                     \
   } while (0)
     bool done = false;
     if (S <= 16) {  // one pass: the frame's chunks as a thread-block cluster
 #define GN_BWDC(NV) s = gn_bwd_cluster(ctx, gn_bwd_cluster_kernel<NV>, S, F, nt, gn_bwd_smem(NV, nt), dz, relu_z, y, \
-                                      stats, gamma, HW, C, part, dy, st, &done)
+                                      stats, gamma, HW, C, part, dy, lo, st, &done)
       if (nt == 1024) GN_BWDC(8);
       else if (nt == 512) GN_BWDC(16);
       else GN_BWDC(32);
@@ -1519,8 +1561,9 @@ ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, c
 // forked after the GN backward (its own dy buffer and partials) and joined once after the backward.
 ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P, ConvGN& c, const float* dz,
                          const float* relu_z, float* dx, int accumulate_dx, cudaStream_t st) {
+  const size_t lo = P.grad_planes == 2 ? (size_t)P.F * c.Ho * c.Wo * c.Co : 0;
   ddppo_status s = gn_bwd(ctx, P.F, c.Ho * c.Wo, c.Co, dz, relu_z, c.y, c.stats, prm + c.gw, c.dyb, grad + c.gw,
-                          grad + c.gb, c.gn_part, P.gn_gpart, st, /*reduce_params=*/false);
+                          grad + c.gb, c.gn_part, P.gn_gpart, st, /*reduce_params=*/false, lo);
   if (s != DDPPO_OK) return s;
   const ConvGeom g = geom_of(P, c);
   if (P.side) {
@@ -1531,7 +1574,7 @@ ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P,
     s = conv_wgrad(ctx, g, c.x, c.xb, c.dyb, grad + c.w, scratch_of(P), st);
   }
   if (s != DDPPO_OK || dx == nullptr) return s;
-  return conv_dgrad(ctx, g, prm + c.w, c.wd_b, c.dyb, dx, accumulate_dx, scratch_of(P), st);
+  return conv_dgrad(ctx, g, prm + c.w, c.wd_b, c.dyb, dx, accumulate_dx, scratch_of(P), st, P.grad_planes);
 }
 
 // gemm_tc with split-K chosen so that small-M / long-K GEMMs still fill the GPU (partials in P.part)
@@ -1606,7 +1649,7 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
       const ConvGN& c = P.convs[i];
       if (c.Ci == 1) continue;  // the Depth stem runs SIMT on fp32 weights
       DDPPO_REQUIRE(ctx, prep.n < kMaxConvs, "too many convolutions for one weight-prep launch");
-      prep.it[prep.n] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k};
+      prep.it[prep.n] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k, P.grad_planes};
       prep.off[prep.n + 1] = prep.off[prep.n] + c.Co * c.Ci * c.k * c.k;
       ++prep.n;
     }
@@ -1614,12 +1657,12 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
     ctx->count(1);
   }
   if (!P.rgbd) {
-    gather_obs_kernel<<<blocks_for(ctx, (size_t)F * kImg * kImg), kThreads, 0, st>>>(b.obs, b.env_idx, b.T, b.T_run,
-                                                                                      F, P.x0);
+    gather_obs_kernel<<<blocks_for(ctx, (size_t)F * kImg * kImg / 8), kThreads, 0, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, P.x0);
   } else {
     DDPPO_REQUIRE(ctx, kImgRgbd % 4 == 0, "rgbd: input width must be a multiple of 4");
     rgbd_prologue_kernel<<<(F * (kImgRgbd / 2) * (kImgRgbd / 4) + kThreads - 1) / kThreads, kThreads, 0, st>>>(
-        b.obs, b.env_idx, b.T, b.T_run, F, kImgRgbd, P.x0, P.x0b);
+        b.obs_rgb, reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, kImgRgbd, P.x0, P.x0b);
   }
   ctx->count(1);
   ddppo_status s = conv_gn_fwd(ctx, prm, P, P.convs[0], nullptr, 1, st);
@@ -1676,6 +1719,9 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
 ddppo_status depth_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, const ddppo_batch& b, float* logits,
                        float* values, void* ws, cudaStream_t st) {
   DDPPO_REQUIRE(ctx, b.obs && b.c0, "visual agent: batch needs obs and c0");
+  DDPPO_REQUIRE(ctx, !is_rgbd(L) || b.obs_rgb, "RGB-D agent: batch needs obs_rgb");
+  DDPPO_REQUIRE(ctx, ((uintptr_t)b.obs & 15) == 0 && ((uintptr_t)b.obs_rgb & 3) == 0,
+                "visual agent: obs must be 16-byte aligned, obs_rgb 4-byte aligned");
   DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= 8 && b.T_run <= 1024, "visual agent: minibatch must hold 1..8 envs, T <= 1024");
   Plan P;
   make_plan(L, is_rgbd(L), b.B, b.T_run, ws, &P);

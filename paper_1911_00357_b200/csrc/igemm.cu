@@ -520,6 +520,10 @@ ddppo_status launch_igemm(ddppo_ctx* ctx, const IGemm& g, cudaStream_t st) {
     if (g.N <= 32) return launch_ig<32, 2, 4, IG_PIX_K, IG_DENSE_K>(ctx, g, st);
     return launch_ig<64, 2, 4, IG_PIX_K, IG_DENSE_K>(ctx, g, st);
   }
+  if (ka == IG_PIX_KT && g.b.kind == IG_DENSE_K && g.planes == 2) {
+    if (g.N <= 32) return launch_ig<32, 2, 4, IG_PIX_KT, IG_DENSE_K>(ctx, g, st);
+    return launch_ig<64, 2, 4, IG_PIX_KT, IG_DENSE_K>(ctx, g, st);
+  }
   if (ka == IG_PIX_KT && g.b.kind == IG_DENSE_K && g.planes == 1) {
     if (g.N <= 32) return launch_ig<32, 1, 4, IG_PIX_KT, IG_DENSE_K>(ctx, g, st);
     if (g.N <= 64) return launch_ig<64, 1, 4, IG_PIX_KT, IG_DENSE_K>(ctx, g, st);

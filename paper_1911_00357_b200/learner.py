@@ -11,14 +11,17 @@ import torch
 
 from . import (Rollout, adam_cfg, ddppo_layout_check, ddppo_learner_register, ddppo_learner_step, ddppo_preempt_poll,
                learner_workspace_size, learner_cfg,
-               loss_cfg, model_desc, param_count, param_layout, preempt_cfg)
+               loss_cfg, model_desc, param_count, param_layout, preempt_cfg, visual_obs)
 
 ROLLOUT_FIELDS = {  # name -> torch dtype
     "rew": torch.float32, "val": torch.float32, "done": torch.uint8, "length": torch.int32,
     "goal": torch.float32, "prev_action": torch.int32, "mask": torch.float32, "h0": torch.float32,
-    "action": torch.int32, "logp_old": torch.float32, "obs": torch.float32, "c0": torch.float32,
+    "action": torch.int32, "logp_old": torch.float32, "obs": torch.bfloat16, "c0": torch.float32,
+    "obs_rgb": torch.uint8,
 }
-OBS_SHAPES = {2: (1, 64, 64), 3: (4, 256, 256)}  # Depth (configs[2]) / RGB-D (configs[3]) frames
+# depth frames (bf16) of the Depth (configs[2]) / RGB-D (configs[3]) agents; RGB-D camera bytes
+OBS_SHAPES = {2: (1, 64, 64), 3: (1, 256, 256)}
+RGB_SHAPE = (3, 256, 256)
 
 
 class Learner:
@@ -58,6 +61,8 @@ class Learner:
                   "logp_old": (E, ld)}
         if self.desc.arch in (2, 3):  # visual agents: + frames and the LSTM cell state
             shapes.update(obs=(E, T) + OBS_SHAPES[self.desc.arch], c0=(E, hs))
+        if self.desc.arch == 3:
+            shapes["obs_rgb"] = (E, T) + RGB_SHAPE
         # all rollout arrays + the epoch permutations in one device arena (256-byte aligned fields), so a
         # packed host arena reaches HBM in a single copy
         shapes["perms"] = (epochs, E)
@@ -91,6 +96,14 @@ class Learner:
         views["__arena__"] = arena
         return views
 
+    def host_fields(self, ro):
+        """A synth rollout dict -> {field: host array in the device arena's dtype} (float frames ->
+        bf16 depth + uint8 RGB; dtype marshalling only)."""
+        out = {k: ro[k] for k in self.dev if k not in ("obs", "obs_rgb")}
+        if "obs" in self.dev:
+            out.update(visual_obs(ro["obs"], self.desc.arch == 3))
+        return out
+
     def load_rollout(self, ro, perms, non_blocking=False):
         """Copy a rollout (synth dict of numpy arrays, or a pinned_host_buffers() arena) + perms to HBM."""
         if "__arena__" in ro:  # packed pinned arena: perms are inside it
@@ -99,6 +112,7 @@ class Learner:
             self.host_perms[:] = ro["perms"].numpy()
             self.host_len[:] = ro["length"].numpy()
             return
+        ro = self.host_fields(ro) if "obs" in self.dev and ro["obs"].dtype != torch.bfloat16 else ro
         for k in self.dev:
             src = ro[k]
             if isinstance(src, np.ndarray):
@@ -124,6 +138,8 @@ class Learner:
         r.E, r.T, r.ld = self.E, self.T, self.ld
         if "obs" in d:
             r.obs, r.c0 = d["obs"].data_ptr(), d["c0"].data_ptr()
+        if "obs_rgb" in d:
+            r.obs_rgb = d["obs_rgb"].data_ptr()
         return r
 
     def step(self, stream=None, stats=None):

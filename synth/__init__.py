@@ -43,6 +43,15 @@ CONFIGS = {
 }
 
 
+def bf16_exact(x):
+    """Round fp32 values to the nearest bf16 (ties to even), returned as fp32: depth frames are
+    delivered to the GPU as bf16, so the generator emits bf16-exact values and every
+    consumer (oracle, kernels) sees the same numbers."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    u = (u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) & np.uint32(0xFFFF0000)
+    return u.view(np.float32)
+
+
 def depth_frames(rng, E, T, C=1, H=64, W=64):
     """Smooth depth-like frames in [0, 1]: 3 seeded low-frequency cosine fields drifting over time
     plus 5 % noise (DESIGN.md input recipe)."""
@@ -55,7 +64,7 @@ def depth_frames(rng, E, T, C=1, H=64, W=64):
         for t in range(T):
             f = sum(np.cos(2 * np.pi * (k[i, 0] * xx + k[i, 1] * yy) + ph[i] + drift[i] * t) for i in range(3))
             f = 0.5 + f / 6.0 + 0.05 * rng.standard_normal((H, W))
-            out[n, t] = np.clip(f, 0.0, 1.0)[None].astype(np.float32).repeat(C, axis=0)
+            out[n, t] = bf16_exact(np.clip(f, 0.0, 1.0))[None].repeat(C, axis=0)
     return out
 
 
@@ -74,7 +83,7 @@ def rgbd_frames(rng, E, T, H=256, W=256):
             for t in range(T):
                 f = sum(cb[i] * np.cos(drift[i] * t) - sb[i] * np.sin(drift[i] * t) for i in range(3))
                 f = np.clip(0.5 + f / 6.0 + 0.05 * rng.standard_normal((H, W)), 0.0, 1.0)
-                out[n, t, ch] = np.rint(255.0 * f) if ch < 3 else f
+                out[n, t, ch] = np.rint(255.0 * f) if ch < 3 else bf16_exact(f)
     return out
 
 

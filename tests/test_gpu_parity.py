@@ -288,9 +288,10 @@ def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
     env_idx = rng.permutation(E)[:B].astype(np.int32)
     L = ro["length"][env_idx]
     T_run = int(L.max())
+    vo_ = {k: t.cuda() for k, t in dd.visual_obs(ro["obs"], arch == "rgbd").items()} if vis else {}
     batch = dd.make_batch(cu(ro["goal"]), cu(ro["prev_action"]), cu(ro["mask"]), cu(ro["h0"]), cu(ro["length"]),
                           cu(env_idx), E, T, ro["ld"], B, T_run, int(L.sum()),
-                          obs=cu(ro["obs"]) if vis else None, c0=cu(ro["c0"]) if vis else None)
+                          obs=vo_.get("obs"), c0=cu(ro["c0"]) if vis else None, obs_rgb=vo_.get("obs_rgb"))
     ws = torch.zeros(dd.workspace_size(desc, B, T_run) // 4 + 64, device="cuda")
     lg = torch.zeros((B, T_run, 4), device="cuda")
     vl = torch.zeros((B, T_run), device="cuda")
@@ -519,7 +520,8 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths):
         g[k] = torch.from_numpy(np.ascontiguousarray(ro[k])).cuda()
     g["done"] = torch.from_numpy(np.ascontiguousarray(ro["done"])).cuda()
     if vis:
-        g["obs"], g["c0"] = cu(ro["obs"]), cu(ro["c0"])
+        g.update({k: t.cuda() for k, t in dd.visual_obs(ro["obs"], c["arch"] == "rgbd").items()})
+        g["c0"] = cu(ro["c0"])
     adv, ret = torch.zeros((E, ld), device="cuda"), torch.zeros((E, ld), device="cuda")
     stats3 = torch.zeros(4, dtype=torch.float64, device="cuda")
     mis = torch.zeros(4, device="cuda")
@@ -549,7 +551,7 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths):
             F = B * T_run
             env_idx = torch.from_numpy(np.ascontiguousarray(envs.astype(np.int32))).cuda()
             batch = dd.make_batch(g["goal"], g["prev_action"], g["mask"], g["h0"], g["length"], env_idx, E, T, ld, B,
-                                  T_run, int(L.sum()), obs=g.get("obs"), c0=g.get("c0"))
+                                  T_run, int(L.sum()), obs=g.get("obs"), c0=g.get("c0"), obs_rgb=g.get("obs_rgb"))
             ws = torch.zeros(dd.workspace_size(desc, B, T_run) // 4 + 64, device="cuda")
             lg, vl = torch.zeros((B, T_run, 4), device="cuda"), torch.zeros((B, T_run), device="cuda")
             dlg, dvl = torch.zeros_like(lg), torch.zeros_like(vl)
