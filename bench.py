@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--conv-engine", default="tma", choices=["tma", "cpasync"],
                     help="visual encoders' convolutions: TMA-fed warp-specialised tcgen05 (default) or the round-1 "
                          "cp.async kernel (A/B)")
-    ap.add_argument("--a8", default="sharded", choices=["sharded", "allread"], help="peer-memory a8 form (N > 1)")
+    ap.add_argument("--a8", default="auto", choices=["auto", "sharded", "allread"], help="peer-memory a8 form (N > 1)")
     return ap.parse_args()
 
 

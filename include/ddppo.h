@@ -293,7 +293,7 @@ ddppo_status ddppo_layout_check(ddppo_ctx* ctx, const ddppo_model_desc* host_des
                                 int minibatches, int epochs);
 
 /* a8 over peer memory (after ddppo_learner_register), Eq. 3:
- *   DDPPO_A8_SHARDED (default): reduce-scatter -> clip + Adam on this rank's 1/N shard -> all-gather
+ *   DDPPO_A8_SHARDED: reduce-scatter -> clip + Adam on this rank's 1/N shard -> all-gather
  *     (NEXT-2; rank r owns float4 units [Q*r/N, Q*(r+1)/N) of the flat vector, Q = P/4, the last
  *     rank also the P%4 tail).  NVLink volume 2(N-1)/N*4P per rank.  Parameters stay bit-identical
  *     on all ranks; Adam's m / v are only maintained on the owned shard (ZeRO-1).
@@ -302,7 +302,11 @@ ddppo_status ddppo_layout_check(ddppo_ctx* ctx, const ddppo_model_desc* host_des
  * bounded (30 s of %globaltimer): on timeout the exchange leaves params / m / v untouched and
  * ddppo_check returns DDPPO_ERR_COMM (fatal).  Host-side setting, read when a learner step
  * is built (graphs are keyed by it). */
-typedef enum { DDPPO_A8_SHARDED = 0, DDPPO_A8_ALLREAD = 1 } ddppo_a8_mode;
+/*   DDPPO_A8_AUTO (default): the form with the lower modelled cost -- all-read moves (N-1)/N*4P more
+ *     bytes per rank but has one cross-rank synchronisation instead of three; sharded is chosen when
+ *     (N-1)(1-2/N)*4P / 770 GB/s + (1-1/N)*28P / 6.5 TB/s exceeds the two extra synchronisations
+ *     (~20 us, measured): Depth at N >= 4, GPS at N = 8, never at N = 2. */
+typedef enum { DDPPO_A8_SHARDED = 0, DDPPO_A8_ALLREAD = 1, DDPPO_A8_AUTO = 2 } ddppo_a8_mode;
 ddppo_status ddppo_set_a8_mode(ddppo_ctx* ctx, int mode);
 
 /* Engine of the visual encoders' implicit-GEMM convolutions (same arithmetic, host-side setting):

@@ -290,8 +290,9 @@ def ddppo_learner_step(ctx, desc, ro, cfg, params, m, v, adv, ret, stats_out, ws
 
 
 def ddppo_set_a8_mode(ctx, mode):
-    """"sharded" (reduce-scatter -> shard Adam -> all-gather, default) or "allread" (v1)."""
-    _call(ctx, "ddppo_set_a8_mode", {"sharded": _lib.A8_SHARDED, "allread": _lib.A8_ALLREAD}.get(mode, mode))
+    """"sharded" (reduce-scatter -> shard Adam -> all-gather), "allread" (v1) or "auto" (default)."""
+    _call(ctx, "ddppo_set_a8_mode", {"sharded": _lib.A8_SHARDED, "allread": _lib.A8_ALLREAD,
+                                     "auto": _lib.A8_AUTO}.get(mode, mode))
 
 
 def _ptr_array(ts):

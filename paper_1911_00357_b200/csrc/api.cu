@@ -575,7 +575,8 @@ extern "C" {
 
 ddppo_status ddppo_set_a8_mode(ddppo_ctx* ctx, int mode) {
   if (!ctx) return DDPPO_ERR_CONFIG;
-  DDPPO_REQUIRE(ctx, mode == DDPPO_A8_SHARDED || mode == DDPPO_A8_ALLREAD, "set_a8_mode: unknown mode");
+  DDPPO_REQUIRE(ctx, mode == DDPPO_A8_SHARDED || mode == DDPPO_A8_ALLREAD || mode == DDPPO_A8_AUTO,
+                "set_a8_mode: unknown mode");
   ctx->a8_mode = mode;
   return DDPPO_OK;
 }
@@ -613,7 +614,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
   size_t need = 0;
   ddppo_status s =
       ddppo_learner_workspace_size(host_desc, ro->E, ro->T, ro->ld, cfg->minibatches, cfg->epochs, &need);
-  if (s != DDPPO_OK) return s;
+  DDPPO_REQUIRE(ctx, s == DDPPO_OK, "learner_step: bad rollout geometry (ld >= T + 1, minibatches | E)");
   DDPPO_REQUIRE(ctx, ws_bytes >= need, "learner_step: workspace too small");
   LearnerWs w;
   carve_learner(host_desc, ro->E, ro->T, cfg->minibatches, cfg->epochs, ws, &w);

@@ -35,7 +35,7 @@ struct ddppo_ctx {
   cudaStream_t cnt_stream = nullptr;     // its own non-blocking stream: not queued behind learner work
   int64_t* h_cnt = nullptr;              // pinned host result
   uint64_t peer_mb = 0;
-  int a8_mode = DDPPO_A8_SHARDED;       // ddppo_set_a8_mode
+  int a8_mode = DDPPO_A8_AUTO;          // ddppo_set_a8_mode
   int conv_engine = DDPPO_CONV_TMA;     // ddppo_set_conv_engine
   int* d_tile_cnt = nullptr;            // split-K tile arrival counters (tconv.cu), zero between kernels
   // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step

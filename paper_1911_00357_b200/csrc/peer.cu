@@ -491,7 +491,14 @@ ddppo_status launch_peer_a8(ddppo_ctx* ctx, float* const* peers, float* const* p
   DDPPO_REQUIRE(ctx, ctx->world <= kMaxPeers && ctx->peer_flags[ctx->rank], "peer: flags not set up");
   PeerArea* areas[kMaxPeers];
   for (int j = 0; j < ctx->world; ++j) areas[j] = reinterpret_cast<PeerArea*>(ctx->peer_flags[j]);
-  return a8_rank(ctx, ctx->a8_mode, ctx->world, ctx->rank, peers, pgs, areas, ctx->d_peer_epoch, true, gsum, params,
+  int mode = ctx->a8_mode;
+  if (mode == DDPPO_A8_AUTO) {  // include/ddppo.h: the cheaper form under the bytes + synchronisation model
+    const double N = ctx->world;
+    const double extra_read_s = (N - 1.0) * (1.0 - 2.0 / N) * 4.0 * (double)P / 770e9;
+    const double adam_saved_s = (1.0 - 1.0 / N) * 28.0 * (double)P / 6.5e12;
+    mode = extra_read_s + adam_saved_s > 20e-6 ? DDPPO_A8_SHARDED : DDPPO_A8_ALLREAD;
+  }
+  return a8_rank(ctx, mode, ctx->world, ctx->rank, peers, pgs, areas, ctx->d_peer_epoch, true, gsum, params,
                  m, v, P, cfg, dstep, step_add, nullptr, st);
 }
 

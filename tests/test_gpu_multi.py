@@ -25,6 +25,15 @@ def _free_port():
 
 
 def _worker(rank, world, port, q):
+    try:
+        _worker_body(rank, world, port, q)
+    except BaseException as e:  # report instead of leaving the parent waiting on the queue
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+        raise
+
+
+def _worker_body(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     torch.cuda.set_device(rank)
@@ -36,6 +45,8 @@ def _worker(rank, world, port, q):
     obj = [dd.get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     ctx = dd.Context(rank, world, obj[0], device=rank)
+    obj2 = [dd.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj2, src=0)
     out = {}
     # a10 before any learner is registered: the NCCL path
     out["counts_nccl"] = dd.ddppo_allreduce_counts(ctx, [rank + 5, 7]).tolist()
@@ -48,14 +59,29 @@ def _worker(rank, world, port, q):
     L = 128 if rank == 0 else 40
     ro = synth.rollout(c["E"], c["T"], 5, rank=rank, length=L)
     pm = synth.perms(5, 0, c["epochs"], c["E"], rank=rank)
-    # a8 over NCCL (unregistered workspace), then over NVLink peer memory (registered workspace)
-    for key, peer in (("params_nccl", False), ("params", True)):
-        lrn = Learner(ctx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, peer=peer, normalize_adv=True)
+    # S:L26 / S:L329: a layout disagreement at rendezvous is a protocol error on every rank
+    try:
+        dd.ddppo_layout_check(ctx, desc, c["E"] + rank, c["T"], 132, c["minibatches"], c["epochs"])
+        out["protocol"] = None
+    except dd.DdppoError as e:
+        out["protocol"] = e.code
+    # a8 over NCCL (unregistered workspace), then over NVLink peer memory (registered workspace; the
+    # sharded reduce-scatter / Adam / all-gather form, then the all-read form on a second context)
+    for key, peer, mode in (("params_nccl", False, "sharded"), ("params_allread", True, "allread"),
+                            ("params", True, "sharded")):
+        cx = ctx
+        if key == "params_allread":  # one registered workspace per context
+            cx = dd.Context(rank, world, obj2[0], device=rank)
+        dd.ddppo_set_a8_mode(cx, mode)
+        lrn = Learner(cx, "gps", c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, peer=peer,
+                      normalize_adv=True)
         lrn.load_rollout(ro, pm)
         lrn.step()
         torch.cuda.synchronize()
-        ctx.check()
+        cx.check()
         out[key] = lrn.params.cpu().numpy()
+        if cx is not ctx:
+            cx.close()
     out["stats"] = lrn.stats.cpu().numpy()
     # a second rollout through the peer path (gradient double buffer continues across calls)
     ro2 = synth.rollout(c["E"], c["T"], 6, rank=rank, length=L)
@@ -64,6 +90,24 @@ def _worker(rank, world, port, q):
     torch.cuda.synchronize()
     ctx.check()
     out["params2"] = lrn.params.cpu().numpy()
+    # ---- the Depth agent (TMA convolutions, side-stream weight gradients) over the sharded a8
+    cd = synth.CONFIGS["depth"]
+    dsc = dd.model_desc("depth")
+    Pd = dd.param_count(dsc)
+    pd0 = synth.init_params([(off, int(np.prod(s_)), fan) for _, off, s_, fan in dd.param_layout(dsc)], Pd, 8)
+    obj3 = [dd.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj3, src=0)
+    cxd = dd.Context(rank, world, obj3[0], device=rank)
+    lrd = Learner(cxd, "depth", cd["E"], 16, cd["epochs"], cd["minibatches"], params=pd0, normalize_adv=True)
+    for it in range(3):
+        lrd.load_rollout(synth.rollout(cd["E"], 16, 8, rank=rank, iteration=it, length=16 if rank == 0 else 9,
+                                       obs_shape=cd["obs"]), synth.perms(8, it, cd["epochs"], cd["E"], rank=rank))
+        lrd.step()
+    torch.cuda.synchronize()
+    cxd.check()
+    out["depth_params"] = lrd.params.cpu().numpy()
+    out["depth_moved"] = float(np.abs(out["depth_params"] - pd0).max())
+    cxd.close()
     # ---- a10 counts
     out["counts"] = dd.ddppo_allreduce_counts(ctx, [c["E"] * L, rank + 1]).tolist()
     # (registered learner: the NVLink exchange; repeated calls cycle its double-buffered slots)
@@ -95,10 +139,17 @@ def test_two_rank_learner_step_and_protocols():
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(world))
+    for r in range(world):
+        assert "error" not in res[r], res[r]["error"]
     for p in procs:
         p.join(timeout=120)
-    for key in ("params", "params_nccl", "params2"):
+    for key in ("params", "params_nccl", "params2", "params_allread", "depth_params"):
         assert np.array_equal(res[0][key], res[1][key]), key  # rank-identical
+    assert res[0]["protocol"] == res[1]["protocol"] == 3  # DDPPO_ERR_PROTOCOL on both ranks
+    assert res[0]["depth_moved"] > 1e-4
+    # the two peer a8 forms differ only in the association order of the clip norm's fp64 partials
+    d = np.abs(res[0]["params"].astype(np.float64) - res[0]["params_allread"]).max()
+    assert d < 1e-6, d
     # oracle: the same two rollouts in one process
     import paper_1911_00357_b200 as dd
     c = synth.CONFIGS["gps"]
@@ -111,7 +162,7 @@ def test_two_rank_learner_step_and_protocols():
     po, _, _, _, info = learner.learner_step("gps", p0, np.zeros(P), np.zeros(P), 0, ros, pms,
                                              dict(epochs=c["epochs"], minibatches=c["minibatches"]))
     dpo = po - p0
-    for key in ("params", "params_nccl"):
+    for key in ("params", "params_nccl", "params_allread"):
         dp = res[0][key].astype(np.float64) - p0
         for name, off, shape, _ in lay:
             n = int(np.prod(shape))
