@@ -161,7 +161,15 @@ typedef struct {
   const float* c0;            /* LSTM cell state before step 0, like h0 (DEPTH / RGBD)      */
   const uint8_t* obs_rgb;     /* RGBD: camera bytes [E][T][3][256][256] (normalised channel-   */
                               /* wise on the device); else NULL                        */
+  /* transfer-learning mechanics (NEXT-4), both optional (0 / NULL):                 */
+  float* dgoal;               /* DEPTH / RGBD backward output [B*T_run][3]: dL/d(goal input), the */
+                              /* gradient a planner receives through a frozen "differentiable    */
+                              /* neural controller"                                  */
+  int32_t flags;              /* DDPPO_BATCH_FREEZE_ENCODER: the visual encoder (enc.* tensors) is */
+                              /* frozen -- no encoder backward runs, its gradient entries are 0    */
+  int32_t reserved_flags;
 } ddppo_batch;
+#define DDPPO_BATCH_FREEZE_ENCODER 1
 
 /* a5: logits [B][T_run][A], values [B][T_run]; saves activations in ws for the backward. */
 ddppo_status ddppo_policy_fwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const float* params,
@@ -268,6 +276,12 @@ typedef struct {
   int32_t epochs, minibatches;
   ddppo_loss_cfg loss;
   ddppo_adam_cfg adam;        /* adam.step = number of updates already taken */
+  /* NEXT-4: freeze_mask (device uint8 [P], nullable, 4-byte aligned): entries != 0 keep
+   * params / m / v bit-identical; freeze_encoder != 0: the visual encoder's backward is
+   * skipped, its gradient entries are 0 (excluded from the clip norm) and its parameters frozen. */
+  const uint8_t* freeze_mask;
+  int32_t freeze_encoder;
+  int32_t reserved;
 } ddppo_learner_cfg;
 
 ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int E, int T, int ld,
@@ -280,6 +294,15 @@ ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int
  * scope, bounded wait -> ddppo_check reports a communication error).  The workspace must stay
  * allocated while the context lives.  World size 1: no-op.  At most one workspace per context. */
 ddppo_status ddppo_learner_register(ddppo_ctx* ctx, void* ws, size_t ws_bytes);
+
+/* Critic re-initialisation ("critic layers are reinitialized"): the value head
+ * (row num_actions of head.weight and head.bias[num_actions]) is resampled from the default
+ * initialiser U(-1/sqrt(fan_in), 1/sqrt(fan_in)) with a counter-based generator (element i of the
+ * head row / bias: u = splitmix64(seed * 0x9E3779B97F4A7C15 + i) >> 40, value = (u * 2^-23 - 1) *
+ * (1 / sqrtf(fan_in)) in fp32; the bias uses i = fan_in); m / v of those entries are zeroed (a fresh
+ * optimiser state); every other entry is untouched.  params / m / v device [P]; stream-ordered. */
+ddppo_status ddppo_reinit_critic(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, float* params, float* m,
+                                 float* v, uint64_t seed, void* stream);
 
 /* Layout agreement at rendezvous ("layout is identical across all workers ... checked at
  * rendezvous by exchanging a layout hash"; S:L329 length mismatch -> fatal protocol error).

@@ -39,7 +39,8 @@ def minibatch_grad(arch, params, ro, adv, ret, envs, mean_invstd, cfg, hidden=51
         flat(ret[envs]), flat(adv[envs]), valid.reshape(-1),
         eps=cfg["clip_eps"], vclip_eps=cfg["vclip_eps"], c_v=cfg["c_v"], c_e=cfg["c_e"],
         use_value_clip=cfg["use_value_clip"], mean_invstd=mean_invstd)
-    g = models.backward(arch, params, cache, dlog.reshape(B, T_run, -1), dval.reshape(B, T_run), hidden=hidden)
+    g = models.backward(arch, params, cache, dlog.reshape(B, T_run, -1), dval.reshape(B, T_run), hidden=hidden,
+                        freeze_encoder=bool(cfg.get("freeze_encoder")))
     return g, stats, (logits, values, dlog, dval)
 
 
@@ -62,6 +63,12 @@ def learner_step(arch, params, m, v, step, rollouts, perms, cfg=None, hidden=512
     gstats = advnorm.combine(stats3)
     mis = advnorm.mean_invstd(gstats, cfg["adv_eps"]) if cfg["normalize_adv"] else None
     params = np.asarray(params, dtype=np.float64)
+    # NEXT-4: cfg["freeze"] (bool [P]) and / or cfg["freeze_encoder"] (the enc.* tensors)
+    freeze = cfg.get("freeze")
+    if cfg.get("freeze_encoder"):
+        from .transfer import encoder_mask
+        enc = encoder_mask(arch, params.size, hidden=hidden)
+        freeze = enc if freeze is None else (np.asarray(freeze, bool) | enc)
     m = np.asarray(m, dtype=np.float64)
     v = np.asarray(v, dtype=np.float64)
     mb_stats, norms = [], []
@@ -80,7 +87,7 @@ def learner_step(arch, params, m, v, step, rollouts, perms, cfg=None, hidden=512
             step += 1
             params, m, v, gn = optim.adam_step(params, gbar, m, v, step, lr=cfg["lr"], beta1=cfg["beta1"],
                                                beta2=cfg["beta2"], eps=cfg["adam_eps"],
-                                               max_grad_norm=cfg["max_grad_norm"])
+                                               max_grad_norm=cfg["max_grad_norm"], freeze=freeze)
             norms.append(gn)
             mb_stats.append({k: float(np.mean([s[k] for s in sts])) for k in ppo.STAT_NAMES})
     steps = int(sum(int(np.sum(ro["length"])) for ro in rollouts))

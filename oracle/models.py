@@ -97,10 +97,12 @@ def unpack(arch, flat, **kw):
 
 
 def pack(arch, tensors, **kw):
+    """Tensors missing from `tensors` (a frozen encoder's, NEXT-4) are packed as zeros."""
     offs, P = offsets(arch, **kw)
     flat = np.zeros(P)
     for k, (o, s) in offs.items():
-        flat[o:o + int(np.prod(s))] = np.asarray(tensors[k], dtype=np.float64).reshape(-1)
+        if k in tensors:
+            flat[o:o + int(np.prod(s))] = np.asarray(tensors[k], dtype=np.float64).reshape(-1)
     return flat
 
 
@@ -172,8 +174,13 @@ def forward(arch, flat, batch, **kw):
     return out[..., :-1], out[..., -1], cache
 
 
-def backward(arch, flat, cache, dlogits, dvalues, **kw):
-    """dlogits [B][T][A], dvalues [B][T] -> flat gradient [P]."""
+def backward(arch, flat, cache, dlogits, dvalues, freeze_encoder=False, extra=None, **kw):
+    """dlogits [B][T][A], dvalues [B][T] -> flat gradient [P].
+
+    Transfer mechanics (NEXT-4), visual agents: freeze_encoder -- the visual encoder
+    (enc.* tensors) is frozen, so the backward stops at the visual FC and the encoder's gradient is 0;
+    extra (a dict) receives "dgoal" [B][T][3] = dL/d(goal input), the gradient a planner gets
+    through a frozen controller."""
     p = unpack(arch, flat, **kw)
     dout = np.concatenate([dlogits, dvalues[..., None]], axis=-1)
     g = {}
@@ -193,12 +200,15 @@ def backward(arch, flat, cache, dlogits, dvalues, **kw):
         dx, g["rnn.weight_ih"], g["rnn.weight_hh"], g["rnn.bias_ih"], g["rnn.bias_hh"] = \
             nets.lstm_seq_bwd(dh, cache["rnn"], p["rnn.weight_ih"], p["rnn.weight_hh"])
         dvis, dge, dae = dx[..., :512], dx[..., 512:544], dx[..., 544:]
-        _, g["goal_fc.weight"], g["goal_fc.bias"] = nets.linear_bwd(cache["goal"], p["goal_fc.weight"], dge)
+        dgoal, g["goal_fc.weight"], g["goal_fc.bias"] = nets.linear_bwd(cache["goal"], p["goal_fc.weight"], dge)
+        if extra is not None:
+            extra["dgoal"] = dgoal
         g["act_embed.weight"] = nets.embedding_bwd(cache["prev_action"], dae, p["act_embed.weight"].shape[0])
         dvpre = dvis * (cache["vis"] > 0)
         dflat, g["visual_fc.weight"], g["visual_fc.bias"] = nets.linear_bwd(cache["flat"], p["visual_fc.weight"],
                                                                             dvpre)
-        convnets.resnet18h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
+        if not freeze_encoder:
+            convnets.resnet18h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
     elif arch == "rgbd":
         dh, g["head.weight"], g["head.bias"] = nets.linear_bwd(cache["h"], p["head.weight"], dout)
         for layer in (1, 0):
@@ -207,12 +217,15 @@ def backward(arch, flat, cache, dlogits, dvalues, **kw):
                                                                p[f"rnn.weight_hh_l{layer}"])
         dx = dh
         dvis, dge, dae = dx[..., :512], dx[..., 512:544], dx[..., 544:]
-        _, g["goal_fc.weight"], g["goal_fc.bias"] = nets.linear_bwd(cache["goal"], p["goal_fc.weight"], dge)
+        dgoal, g["goal_fc.weight"], g["goal_fc.bias"] = nets.linear_bwd(cache["goal"], p["goal_fc.weight"], dge)
+        if extra is not None:
+            extra["dgoal"] = dgoal
         g["act_embed.weight"] = nets.embedding_bwd(cache["prev_action"], dae, p["act_embed.weight"].shape[0])
         dvpre = dvis * (cache["vis"] > 0)
         dflat, g["visual_fc.weight"], g["visual_fc.bias"] = nets.linear_bwd(cache["flat"], p["visual_fc.weight"],
                                                                             dvpre)
-        convnets.resnet50h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
+        if not freeze_encoder:
+            convnets.resnet50h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
     else:
         raise ValueError(arch)
     return pack(arch, g, **kw)

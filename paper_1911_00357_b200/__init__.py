@@ -108,9 +108,14 @@ def ddppo_adv_norm(ctx, stats3, eps, mean_invstd, stream=None):
     _call(ctx, "ddppo_adv_norm", f64(stats3), eps, f32(mean_invstd), _stream(stream))
 
 
+BATCH_FREEZE_ENCODER = 1
+
+
 def make_batch(goal, prev_action, mask, h0, length, env_idx, E, T, ld, B, T_run, n_valid, obs=None, c0=None,
-               obs_rgb=None):
-    """obs: depth frames (torch.bfloat16); obs_rgb: RGB camera bytes (torch.uint8, RGB-D only)."""
+               obs_rgb=None, dgoal=None, freeze_encoder=False):
+    """obs: depth frames (torch.bfloat16); obs_rgb: RGB camera bytes (torch.uint8, RGB-D only);
+    dgoal: optional [B*T_run][3] output of the visual agents' backward (dL/d goal input);
+    freeze_encoder: the visual encoder is frozen (no encoder backward, its gradient 0)."""
     b = Batch()
     b.goal, b.prev_action, b.mask, b.h0 = f32(goal), i32(prev_action), f32(mask), f32(h0)
     b.len, b.env_idx = i32(length), i32(env_idx)
@@ -118,7 +123,9 @@ def make_batch(goal, prev_action, mask, h0, length, env_idx, E, T, ld, B, T_run,
     b.obs = dptr(obs, "bfloat16") if obs is not None else None
     b.c0 = f32(c0) if c0 is not None else None
     b.obs_rgb = u8(obs_rgb) if obs_rgb is not None else None
-    b._keep = (goal, prev_action, mask, h0, length, env_idx, obs, c0, obs_rgb)  # the struct holds raw pointers
+    b.dgoal = f32(dgoal) if dgoal is not None else None
+    b.flags = BATCH_FREEZE_ENCODER if freeze_encoder else 0
+    b._keep = (goal, prev_action, mask, h0, length, env_idx, obs, c0, obs_rgb, dgoal)  # raw pointers held
     return b
 
 
@@ -345,3 +352,8 @@ def ddppo_layout_check(ctx, desc, E, T, ld, minibatches, epochs):
 def ddppo_set_conv_engine(ctx, engine):
     """"tma" (TMA-fed warp-specialised tcgen05 convolutions, default) or "cpasync" (round-1 kernel)."""
     _call(ctx, "ddppo_set_conv_engine", {"cpasync": 0, "tma": 1}.get(engine, engine))
+
+
+def ddppo_reinit_critic(ctx, desc, params, m, v, seed, stream=None):
+    """Resample the value head with the documented counter-based generator."""
+    _call(ctx, "ddppo_reinit_critic", ctypes.byref(desc), f32(params), f32(m), f32(v), int(seed), _stream(stream))

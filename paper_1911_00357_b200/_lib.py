@@ -43,7 +43,8 @@ class TensorInfo(ctypes.Structure):
 class Batch(ctypes.Structure):
     _fields_ = [("goal", c_vp), ("prev_action", c_vp), ("mask", c_vp), ("h0", c_vp), ("len", c_vp),
                 ("env_idx", c_vp), ("E", c_i32), ("T", c_i32), ("ld", c_i32), ("B", c_i32), ("T_run", c_i32),
-                ("n_valid", c_i32), ("obs", c_vp), ("c0", c_vp), ("obs_rgb", c_vp)]
+                ("n_valid", c_i32), ("obs", c_vp), ("c0", c_vp), ("obs_rgb", c_vp), ("dgoal", c_vp),
+                ("flags", c_i32), ("reserved_flags", c_i32)]
 
 
 class LossInputs(ctypes.Structure):
@@ -73,7 +74,8 @@ class Rollout(ctypes.Structure):
 
 class LearnerCfg(ctypes.Structure):
     _fields_ = [("gamma", c_float), ("tau", c_float), ("adv_eps", c_float), ("normalize_adv", c_i32),
-                ("epochs", c_i32), ("minibatches", c_i32), ("loss", LossCfg), ("adam", AdamCfg)]
+                ("epochs", c_i32), ("minibatches", c_i32), ("loss", LossCfg), ("adam", AdamCfg),
+                ("freeze_mask", c_vp), ("freeze_encoder", c_i32), ("reserved", c_i32)]
 
 
 P_ = ctypes.POINTER
@@ -116,6 +118,7 @@ _SIGS = {
     "ddppo_set_graphs": (c_int, [c_vp, c_int]),
     "ddppo_set_a8_mode": (c_int, [c_vp, c_int]),
     "ddppo_set_conv_engine": (c_int, [c_vp, c_int]),
+    "ddppo_reinit_critic": (c_int, [c_vp, P_(ModelDesc), c_vp, c_vp, c_vp, ctypes.c_uint64, c_vp]),
     "ddppo_layout_hash": (c_int, [P_(ModelDesc), c_int, c_int, c_int, c_int, c_int, P_(ctypes.c_uint64)]),
     "ddppo_layout_check": (c_int, [c_vp, P_(ModelDesc), c_int, c_int, c_int, c_int, c_int]),
     "ddppo_debug_peer_a8": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_i64, P_(AdamCfg), c_vp, c_vp,

@@ -6,6 +6,8 @@
 // Two launches: (1) sum of squares of g/N in fp64 per block -> last block -> coef (device
 // scalar, so the update needs no host round trip); (2) the elementwise update, float4.
 // HBM traffic 4P (pass 1) + 28P (pass 2: read g, p, m, v; write p, m, v) bytes.
+#include <string.h>
+
 #include "common.cuh"
 
 namespace {
@@ -50,7 +52,7 @@ grad_norm_kernel(const float* __restrict__ g, int64_t P, float inv_world, float 
 __global__ void __launch_bounds__(kThreads)
 adam_kernel(const float* __restrict__ g, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
             const uint8_t* __restrict__ freeze, int64_t P, const float* __restrict__ scalars, float b1, float b2,
-            float lr, const int* __restrict__ dstep, int step_add, float eps, const int* err) {
+            float lr, const int* __restrict__ dstep, int step_add, float eps, const int* err, int64_t frz_end) {
   __shared__ float sbc[2];
   // a failed peer exchange (ERR_BIT_COMM) or a non-finite gradient norm (ERR_BIT_GRAD) leaves
   // the parameters untouched until ddppo_check reports it
@@ -66,7 +68,8 @@ adam_kernel(const float* __restrict__ g, float* __restrict__ p, float* __restric
   const float scale = scalars[0];
   const int64_t P4 = P / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P4; i += stride) {
+  // entries [0, frz_end) are frozen (the visual encoder of a transfer task: a multiple of 4 in the layout)
+  for (int64_t i = frz_end / 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P4; i += stride) {
     const float4 gg = reinterpret_cast<const float4*>(g)[i];
     float4 pp = reinterpret_cast<float4*>(p)[i];
     float4 mm = reinterpret_cast<float4*>(m)[i];
@@ -102,31 +105,80 @@ adam_kernel(const float* __restrict__ g, float* __restrict__ p, float* __restric
 
 ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, float* m, float* v,
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep,
-                              int step_add, cudaStream_t st) {
+                              int step_add, cudaStream_t st, int64_t frz_end) {
   DDPPO_REQUIRE(ctx, P >= 1 && (dstep || step_add >= 1), "adam: need P >= 1 and step >= 1");
+  DDPPO_REQUIRE(ctx, frz_end % 4 == 0 && frz_end <= P, "adam: frozen prefix must be a multiple of 4");
   const int blocks = grid_for((int)std::min<int64_t>((P + 3) / 4, 1 << 30), kThreads, ctx->sm_count * 4);
   ProfScope ps(ctx, DDPPO_K_ADAM, st, 1);
   adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
-                                           cfg.lr, dstep, step_add, cfg.eps, ctx->d_err);
+                                           cfg.lr, dstep, step_add, cfg.eps, ctx->d_err, frz_end);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
 
 ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float* m, float* v,
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
-                              float* grad_norm, cudaStream_t st, const int* dstep, int step_add) {
+                              float* grad_norm, cudaStream_t st, const int* dstep, int step_add, int64_t frz_end) {
   if (!dstep) step_add = cfg.step;
   DDPPO_REQUIRE(ctx, P >= 1 && (dstep || step_add >= 1), "adam: need P >= 1 and step >= 1");
   DDPPO_REQUIRE(ctx, (uintptr_t)grad % 16 == 0 && (uintptr_t)params % 16 == 0 && (uintptr_t)m % 16 == 0 &&
                          (uintptr_t)v % 16 == 0 && (freeze == nullptr || (uintptr_t)freeze % 4 == 0),
                 "adam: buffers must be 16-byte aligned");
+  DDPPO_REQUIRE(ctx, frz_end % 4 == 0 && frz_end <= P, "adam: frozen prefix must be a multiple of 4");
   const int blocks = grid_for((int)std::min<int64_t>((P + 3) / 4, 1 << 30), kThreads, ctx->sm_count * 4);
   ProfScope ps(ctx, DDPPO_K_ADAM, st, 2);
   grad_norm_kernel<<<blocks, kThreads, 0, st>>>(grad, P, inv_world, cfg.max_grad_norm, ctx->d_partials,
                                                 ctx->d_counters + CNT_NORM, ctx->d_scalars, grad_norm, ctx->d_err);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
-                                           cfg.lr, dstep, step_add, cfg.eps, ctx->d_err);
+                                           cfg.lr, dstep, step_add, cfg.eps, ctx->d_err, frz_end);
+  DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+  return DDPPO_OK;
+}
+
+// ---------------------------------------------------------------- critic re-initialisation (NEXT-4)
+namespace {
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void reinit_critic_kernel(float* __restrict__ w_row, float* __restrict__ b_elem, float* __restrict__ mw,
+                                     float* __restrict__ vw, float* __restrict__ mb, float* __restrict__ vb, int fan_in,
+                                     uint64_t seed) {
+  const float bound = 1.0f / sqrtf((float)fan_in);
+  for (int i = threadIdx.x; i <= fan_in; i += blockDim.x) {
+    const uint64_t u = splitmix64(seed * 0x9E3779B97F4A7C15ull + (uint64_t)i) >> 40;  // 24 random bits
+    const float val = ((float)u * 0x1p-23f - 1.0f) * bound;
+    if (i < fan_in) {
+      w_row[i] = val;
+      mw[i] = 0.f;
+      vw[i] = 0.f;
+    } else {
+      *b_elem = val;
+      *mb = 0.f;
+      *vb = 0.f;
+    }
+  }
+}
+}  // namespace
+
+extern "C" ddppo_status ddppo_reinit_critic(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, float* params, float* m,
+                                            float* v, uint64_t seed, void* stream) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  ModelLayout L;
+  DDPPO_REQUIRE(ctx, build_layout(host_desc, &L) == DDPPO_OK, "reinit_critic: bad model descriptor");
+  DDPPO_REQUIRE(ctx, params && m && v, "reinit_critic: null pointer");
+  const int64_t hw = layout_offset(L, "head.weight"), hb = layout_offset(L, "head.bias");
+  DDPPO_REQUIRE(ctx, hw >= 0 && hb >= 0, "reinit_critic: model has no head");
+  int fan_in = 0, A = host_desc->num_actions;
+  for (int i = 0; i < L.n; ++i)
+    if (strcmp(L.t[i].name, "head.weight") == 0) fan_in = (int)L.t[i].shape[1];
+  const int64_t row = hw + (int64_t)A * fan_in, bi = hb + A;
+  cudaStream_t st = as_stream(stream);
+  reinit_critic_kernel<<<1, 256, 0, st>>>(params + row, params + bi, m + row, v + row, m + bi, v + bi, fan_in, seed);
+  ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }

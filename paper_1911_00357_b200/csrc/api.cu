@@ -227,6 +227,7 @@ ddppo_status ddppo_policy_bwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
     return toy_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
   if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2)
     return depth_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
+  DDPPO_REQUIRE(ctx, host_batch->dgoal == nullptr, "policy_bwd: dgoal is produced by the visual agents only");
   return gps_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
 }
 
@@ -472,6 +473,8 @@ ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_mode
   }
   const int B = ro->E / cfg->minibatches;
   ddppo_loss_inputs li = {ro->action, ro->logp_old, ro->val, ret, adv};
+  // a frozen visual encoder (NEXT-4): its tensors lead the layout; Adam leaves [0, frz_end) untouched
+  const int64_t frz_end = (cfg->freeze_encoder && visual) ? encoder_end(L) : 0;
   const ddppo_adam_cfg acfg = cfg->adam;
   int k = 0;
   for (int e = 0; e < cfg->epochs; ++e) {
@@ -491,6 +494,9 @@ ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_mode
       b.n_valid = mbs[k].n_valid;
       b.obs = ro->obs;
       b.obs_rgb = ro->obs_rgb;
+      b.dgoal = nullptr;
+      b.flags = cfg->freeze_encoder ? DDPPO_BATCH_FREEZE_ENCODER : 0;
+      b.reserved_flags = 0;
       b.c0 = ro->c0;
       float* st_out = w.stats + (size_t)k * 8;
       const float* mis = cfg->normalize_adv ? w.mean_invstd : nullptr;
@@ -521,14 +527,15 @@ ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_mode
           peers[r] = reinterpret_cast<float*>(ctx->peer_ws_base[r] + off);
           pgs[r] = reinterpret_cast<float*>(ctx->peer_ws_base[r] + off_pg);
         }
-        s = launch_peer_a8(ctx, peers, pgs, w.gsum, params, m, v, L.P, acfg, ctx->d_step, k + 1, st);
+        s = launch_peer_a8(ctx, peers, pgs, w.gsum, params, m, v, L.P, acfg, ctx->d_step, k + 1, st, cfg->freeze_mask,
+                           frz_end);
       } else {
         if (ctx->world > 1) {
           ProfScope ps(ctx, DDPPO_K_ALLREDUCE, st, 0);
           DDPPO_NCCL_TRY(ctx, ncclAllReduce(w.grad, w.grad, (size_t)L.P, ncclFloat32, ncclSum, ctx->comm, st));
         }
-        s = launch_clip_adam(ctx, w.grad, params, m, v, nullptr, L.P, acfg, 1.f / (float)ctx->world, nullptr, st,
-                             ctx->d_step, k + 1);
+        s = launch_clip_adam(ctx, w.grad, params, m, v, cfg->freeze_mask, L.P, acfg, 1.f / (float)ctx->world, nullptr,
+                             st, ctx->d_step, k + 1, frz_end);
       }
       if (s != DDPPO_OK) return s;
     }
@@ -606,6 +613,8 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
   DDPPO_REQUIRE(ctx, cfg->minibatches >= 1 && ro->E % cfg->minibatches == 0 && cfg->epochs >= 1,
                 "learner_step: minibatches must divide E (S:L155)");
   DDPPO_REQUIRE(ctx, cfg->adam.step >= 0, "learner_step: adam.step must be >= 0");
+  DDPPO_REQUIRE(ctx, cfg->freeze_mask == nullptr || ((uintptr_t)cfg->freeze_mask & 3) == 0,
+                "learner_step: freeze_mask must be 4-byte aligned");
   DDPPO_REQUIRE(ctx, (cfg->normalize_adv != 0) == (cfg->loss.normalize_adv != 0),
                 "learner_step: normalize_adv and loss.normalize_adv must agree");
   const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;

@@ -248,9 +248,11 @@ ddppo_status launch_loss(ddppo_ctx* ctx, const float* logits, const float* value
                          const ddppo_loss_inputs& in, const float* mean_invstd, const ddppo_loss_cfg& cfg,
                          float* dlogits, float* dvalues, float* stats, cudaStream_t st);
 // Adam's update count: host cfg.step (dstep == null) or device *dstep + step_add (learner runtime)
+// frz_end: entries [0, frz_end) are frozen (a multiple of 4)
 ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float* m, float* v,
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, float inv_world,
-                              float* grad_norm, cudaStream_t st, const int* dstep = nullptr, int step_add = 0);
+                              float* grad_norm, cudaStream_t st, const int* dstep = nullptr, int step_add = 0,
+                              int64_t frz_end = 0);
 
 // bf16-operand implicit-GEMM (igemm.cu): operands read straight into UMMA canonical tiles.
 enum { IG_DENSE_K = 0, IG_DENSE_MN = 1, IG_PIX_K = 2, IG_TAP_MN = 3 };
@@ -313,11 +315,11 @@ ddppo_status peer_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n);
 // staged-shard buffer (both as mapped here); gsum scratch [P]; Adam step = *dstep + step_add
 ddppo_status launch_peer_a8(ddppo_ctx* ctx, float* const* peers, float* const* pgs, float* gsum, float* params,
                             float* m, float* v, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep, int step_add,
-                            cudaStream_t st);
+                            cudaStream_t st, const uint8_t* freeze = nullptr, int64_t frz_end = 0);
 // Adam on an already summed gradient whose clip scale is in ctx->d_scalars[0] (adam.cu)
 ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, float* m, float* v,
                               const uint8_t* freeze, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep,
-                              int step_add, cudaStream_t st);
+                              int step_add, cudaStream_t st, int64_t frz_end = 0);
 
 // tcgen05 GEMM: C[m][n] (+)= sum_k A(m,k) B(n,k) over fp32 operands with generic strides (gemm_tc.cu)
 struct GemmTC {
@@ -343,6 +345,8 @@ struct ModelLayout {
 };
 ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out);
 int64_t layout_offset(const ModelLayout& L, const char* name);
+// one past the last element of the visual encoder's tensors ("enc.*", which lead the layout); 0 if none
+int64_t encoder_end(const ModelLayout& L);
 
 size_t toy_workspace(int max_B, int T);
 ddppo_status toy_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,

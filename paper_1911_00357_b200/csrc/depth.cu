@@ -1001,6 +1001,17 @@ __global__ void __launch_bounds__(kThreads) goal_emb_grads_kernel(const float* _
   }
 }
 
+// dgoal[s][c] = sum_j dx[s][512 + j] * Wg[j][c]: the gradient wrt the goal input of goal_fc
+__global__ void goal_input_grad_kernel(const float* __restrict__ dx, const float* __restrict__ Wg, int S,
+                                       float* __restrict__ dgoal) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S * 3; i += gridDim.x * blockDim.x) {
+    const int s = i / 3, c = i - s * 3;
+    float acc = 0.f;
+    for (int j = 0; j < 32; ++j) acc += dx[(size_t)s * kXin + 512 + j] * Wg[j * 3 + c];
+    dgoal[i] = acc;
+  }
+}
+
 __global__ void relu_mask_kernel(const float* __restrict__ dz, const float* __restrict__ z, size_t n,
                                  float* __restrict__ out) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -1784,6 +1795,11 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
                                                  grad + off_of(L, "goal_fc.weight"), grad + off_of(L, "goal_fc.bias"),
                                                  grad + off_of(L, "act_embed.weight"));
   ctx->count(1);
+  if (b.dgoal) {  // the planner's gradient through the (frozen) controller
+    goal_input_grad_kernel<<<blocks_for(ctx, (size_t)F * 3), kThreads, 0, st>>>(
+        P.dxin, prm + off_of(L, "goal_fc.weight"), F, b.dgoal);
+    ctx->count(1);
+  }
   vis_mask_kernel<<<blocks_for(ctx, (size_t)F * 512), kThreads, 0, st>>>(P.dxin, P.vis, F, P.dvis);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -1794,6 +1810,12 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
                       P, wst, P.part2)) != DDPPO_OK)
     return s;
   if ((s = launch_colsum(ctx, P.dvis, 512, F, 512, grad + off_of(L, "visual_fc.bias"), wst)) != DDPPO_OK) return s;
+  if (b.flags & DDPPO_BATCH_FREEZE_ENCODER) {
+    // frozen encoder (NEXT-4): no encoder backward; its gradient entries are 0 (they lead the layout)
+    DDPPO_CUDA_TRY(ctx, cudaMemsetAsync(grad, 0, (size_t)encoder_end(L) * sizeof(float), st));
+    if (wst != st) DDPPO_CUDA_TRY(ctx, fork_to(ctx, wst, st));
+    return DDPPO_OK;
+  }
   if ((s = gemm_split(ctx, GemmTC{P.dvis, 512, 1, prm + off_of(L, "visual_fc.weight"), 1, P.fc_in, P.dflat, P.fc_in,
                                   F, P.fc_in, 512},
                       P, st)) != DDPPO_OK)

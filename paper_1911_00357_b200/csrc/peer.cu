@@ -222,7 +222,7 @@ peer_adam_shard_kernel(const PeerArgs args, int world, int rank, int64_t P, cons
                        float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, float* __restrict__ pgather,
                        float inv_world, float max_norm, float b1, float b2, float lr, float eps, const int* dstep,
                        int step_add, const unsigned int* d_epoch, unsigned int* counter, float* grad_norm_out,
-                       int* err) {
+                       int* err, const uint8_t* __restrict__ freeze, int64_t frz_end) {
   __shared__ float sc[3];
   __shared__ int ok;
   __shared__ bool am_last;
@@ -255,14 +255,26 @@ peer_adam_shard_kernel(const PeerArgs args, int world, int rank, int64_t P, cons
   const int64_t Q = P / 4, q0 = shard_q(Q, world, rank), q1 = shard_q(Q, world, rank + 1);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = q0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q1; i += stride) {
-    const float4 gg = reinterpret_cast<const float4*>(gsum)[i];
     float4 pp = reinterpret_cast<float4*>(p)[i];
+    if (i < frz_end / 4) {  // frozen prefix: staged unchanged (the peers copy it back)
+      reinterpret_cast<float4*>(pgather)[i] = pp;
+      continue;
+    }
+    const float4 gg = reinterpret_cast<const float4*>(gsum)[i];
     float4 mm = reinterpret_cast<float4*>(m)[i];
     float4 vv = reinterpret_cast<float4*>(v)[i];
+    const float4 po = pp, mo = mm, vo = vv;
     adam_one(pp.x, mm.x, vv.x, gg.x * scale, b1, b2, step_size, inv_sqrt_bc2, eps);
     adam_one(pp.y, mm.y, vv.y, gg.y * scale, b1, b2, step_size, inv_sqrt_bc2, eps);
     adam_one(pp.z, mm.z, vv.z, gg.z * scale, b1, b2, step_size, inv_sqrt_bc2, eps);
     adam_one(pp.w, mm.w, vv.w, gg.w * scale, b1, b2, step_size, inv_sqrt_bc2, eps);
+    if (freeze) {
+      const uint32_t fr = reinterpret_cast<const uint32_t*>(freeze)[i];
+      if (fr & 0xffu) { pp.x = po.x; mm.x = mo.x; vv.x = vo.x; }
+      if (fr & 0xff00u) { pp.y = po.y; mm.y = mo.y; vv.y = vo.y; }
+      if (fr & 0xff0000u) { pp.z = po.z; mm.z = mo.z; vv.z = vo.z; }
+      if (fr & 0xff000000u) { pp.w = po.w; mm.w = mo.w; vv.w = vo.w; }
+    }
     reinterpret_cast<float4*>(p)[i] = pp;
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
@@ -270,6 +282,10 @@ peer_adam_shard_kernel(const PeerArgs args, int world, int rank, int64_t P, cons
   }
   if (rank == world - 1)
     for (int64_t i = Q * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride) {
+      if (freeze && freeze[i]) {
+        pgather[i] = p[i];
+        continue;
+      }
       float pp = p[i], mm = m[i], vv = v[i];
       adam_one(pp, mm, vv, gsum[i] * scale, b1, b2, step_size, inv_sqrt_bc2, eps);
       p[i] = pp;
@@ -445,7 +461,8 @@ ddppo_status peer_setup_flags(ddppo_ctx* ctx) {
 static ddppo_status a8_rank(ddppo_ctx* ctx, int mode, int world, int rank, float* const* grads, float* const* pgs,
                             PeerArea* const* areas, unsigned int* d_epoch, bool barrier, float* gsum, float* params,
                             float* m, float* v, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep, int step_add,
-                            float* grad_norm, cudaStream_t st) {
+                            float* grad_norm, cudaStream_t st, const uint8_t* freeze = nullptr,
+                            int64_t frz_end = 0) {
   PeerArgs a;
   memset(&a, 0, sizeof(a));
   for (int j = 0; j < world; ++j) {
@@ -465,7 +482,7 @@ static ddppo_status a8_rank(ddppo_ctx* ctx, int mode, int world, int rank, float
                                                                     ctx->d_scalars, grad_norm, ctx->d_err);
     ctx->count(1);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
-    return launch_adam_only(ctx, gsum, params, m, v, nullptr, P, cfg, dstep, step_add, st);
+    return launch_adam_only(ctx, gsum, params, m, v, freeze, P, cfg, dstep, step_add, st, frz_end);
   }
   DDPPO_REQUIRE(ctx, pgs != nullptr, "peer: sharded a8 needs staged-shard buffers");
   const int64_t shard = (P + world - 1) / world;
@@ -477,7 +494,7 @@ static ddppo_status a8_rank(ddppo_ctx* ctx, int mode, int world, int rank, float
     peer_adam_shard_kernel<<<blocks, kThreads, 0, st>>>(a, world, rank, P, gsum, params, m, v, pgs[rank], inv_world,
                                                         cfg.max_grad_norm, cfg.beta1, cfg.beta2, cfg.lr, cfg.eps, dstep,
                                                         step_add, d_epoch, ctx->d_counters + CNT_MISC, grad_norm,
-                                                        ctx->d_err);
+                                                        ctx->d_err, freeze, frz_end);
   }
   peer_ag_kernel<<<a8_blocks(ctx, P - shard), kThreads, 0, st>>>(a, world, rank, P, params, d_epoch, ctx->d_err);
   ctx->count(3);
@@ -487,7 +504,7 @@ static ddppo_status a8_rank(ddppo_ctx* ctx, int mode, int world, int rank, float
 
 ddppo_status launch_peer_a8(ddppo_ctx* ctx, float* const* peers, float* const* pgs, float* gsum, float* params,
                             float* m, float* v, int64_t P, const ddppo_adam_cfg& cfg, const int* dstep, int step_add,
-                            cudaStream_t st) {
+                            cudaStream_t st, const uint8_t* freeze, int64_t frz_end) {
   DDPPO_REQUIRE(ctx, ctx->world <= kMaxPeers && ctx->peer_flags[ctx->rank], "peer: flags not set up");
   PeerArea* areas[kMaxPeers];
   for (int j = 0; j < ctx->world; ++j) areas[j] = reinterpret_cast<PeerArea*>(ctx->peer_flags[j]);
@@ -499,7 +516,7 @@ ddppo_status launch_peer_a8(ddppo_ctx* ctx, float* const* peers, float* const* p
     mode = extra_read_s + adam_saved_s > 20e-6 ? DDPPO_A8_SHARDED : DDPPO_A8_ALLREAD;
   }
   return a8_rank(ctx, mode, ctx->world, ctx->rank, peers, pgs, areas, ctx->d_peer_epoch, true, gsum, params,
-                 m, v, P, cfg, dstep, step_add, nullptr, st);
+                 m, v, P, cfg, dstep, step_add, nullptr, st, freeze, frz_end);
 }
 
 ddppo_status peer_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n) {
@@ -581,7 +598,7 @@ extern "C" ddppo_status ddppo_debug_peer_a8(ddppo_ctx* ctx, int N, int mode, flo
       peer_adam_shard_kernel<<<blocks, kThreads, 0, st>>>(pa, N, r, P, host_gsum[r], host_params[r], host_m[r],
                                                           host_v[r], pgs[r], 1.f / N, cfg.max_grad_norm, cfg.beta1,
                                                           cfg.beta2, cfg.lr, cfg.eps, nullptr, cfg.step, epochs + r,
-                                                          ctx->d_counters + CNT_MISC, nullptr, ctx->d_err);
+                                                          ctx->d_counters + CNT_MISC, nullptr, ctx->d_err, nullptr, 0);
     for (int r = 0; r < N; ++r)
       peer_ag_kernel<<<a8_blocks(ctx, P - shard), kThreads, 0, st>>>(pa, N, r, P, host_params[r], epochs + r,
                                                                      ctx->d_err);

@@ -157,6 +157,12 @@ int64_t layout_offset(const ModelLayout& L, const char* name) {
   return -1;
 }
 
+int64_t encoder_end(const ModelLayout& L) {
+  int64_t end = 0;
+  for (int i = 0; i < L.n && strncmp(L.t[i].name, "enc.", 4) == 0; ++i) end = L.t[i].offset + L.t[i].numel;
+  return (end + 3) / 4 * 4;
+}
+
 namespace {
 constexpr int kH = 64, kA1 = 5;
 

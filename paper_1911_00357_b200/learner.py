@@ -29,7 +29,7 @@ class Learner:
     turns it on explicitly."""
     def __init__(self, ctx, arch, E, T, epochs=2, minibatches=2, hidden=None, params=None, device="cuda",
                  normalize_adv=False, use_value_clip=True, lr=2.5e-4, max_grad_norm=0.5, ld=None, adam_eps=1e-8,
-                 peer=True):
+                 peer=True, freeze_encoder=False, freeze_mask=None):
         self.ctx, self.E, self.T = ctx, E, T
         self.ld = ld or ((T + 1 + 3) // 4 * 4)
         self.epochs, self.minibatches = epochs, minibatches
@@ -47,6 +47,12 @@ class Learner:
         self.cfg = learner_cfg(epochs, minibatches, normalize_adv=normalize_adv,
                                loss=loss_cfg(use_value_clip=use_value_clip, normalize_adv=normalize_adv),
                                adam=adam_cfg(0, lr=lr, eps=adam_eps, max_grad_norm=max_grad_norm))
+        # transfer mechanics (NEXT-4): a frozen visual encoder and / or a per-entry freeze mask
+        self.cfg.freeze_encoder = int(freeze_encoder)
+        self.freeze_mask = None
+        if freeze_mask is not None:
+            self.freeze_mask = torch.as_tensor(np.asarray(freeze_mask, dtype=np.uint8)).to(dev).contiguous()
+            self.cfg.freeze_mask = self.freeze_mask.data_ptr()
         wsb = learner_workspace_size(self.desc, E, T, self.ld, minibatches, epochs)
         self.ws = torch.empty(wsb // 4 + 64, **f32)
         if getattr(ctx, "world", 1) > 1:
@@ -194,3 +200,9 @@ def preempt_collect(ctx, step_costs, T, p_percent, exchange=None, world=None, on
             return steps, tick
         if just and active and stop:
             active = False
+
+
+def reinit_critic(lrn, seed):
+    """P:L405 "critic layers are reinitialized" on a Learner's parameters (and their Adam moments)."""
+    from . import ddppo_reinit_critic
+    ddppo_reinit_critic(lrn.ctx, lrn.desc, lrn.params, lrn.m, lrn.v, seed)

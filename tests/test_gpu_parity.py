@@ -487,9 +487,13 @@ def test_learner_step_parity(dd, ctx, cfgname, lengths):
     assert not bad, bad
 
 
-@pytest.mark.parametrize("cfgname,T,lengths", [("gps", 128, [128, 96, 128, 32]), ("depth", 12, [12, 5, 12, 9]),
-                                               ("depth", 128, [128, 128, 70, 128]), ("rgbd", 2, [2, 1, 2, 2])])
-def test_learner_chain_parity(dd, ctx, cfgname, T, lengths):
+@pytest.mark.parametrize("cfgname,T,lengths,frozen", [("gps", 128, [128, 96, 128, 32], False),
+                                                      ("depth", 12, [12, 5, 12, 9], False),
+                                                      ("depth", 128, [128, 128, 70, 128], False),
+                                                      ("rgbd", 2, [2, 1, 2, 2], False),
+                                                      ("depth", 12, [12, 5, 12, 9], True),
+                                                      ("rgbd", 2, [2, 1, 2, 2], True)])
+def test_learner_chain_parity(dd, ctx, cfgname, T, lengths, frozen):
     """The learner step of the config (Adam eps 1e-8, 2 epochs x 2 minibatches) driven one ABI call
     at a time -- ddppo_gae, ddppo_adv_norm, then per minibatch ddppo_policy_fwd,
     ddppo_ppo_loss_grad, ddppo_policy_bwd, ddppo_grad_allreduce_step -- each minibatch checked
@@ -500,7 +504,9 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths):
       gradient 1e-4 (m, v 1e-5).
     Then ddppo_learner_step on the same rollout must reproduce the chained calls' parameters
     (the visual agents: bit for bit -- the same kernels in the same order; GPS: its learner fuses
-    head + loss into the recurrence epilogue, so to 1e-3 of the update)."""
+    head + loss into the recurrence epilogue, so to 1e-3 of the update).
+    frozen: the transfer setting of P:L407 (NEXT-4) -- a frozen visual encoder: no encoder backward
+    (its gradient exactly 0), its parameters bit-identical through the step."""
     from paper_1911_00357_b200.learner import Learner
     c = dict(synth.CONFIGS[cfgname])
     c["T"] = T
@@ -541,7 +547,10 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths):
     params = cu(p0)
     m, v = torch.zeros(P, device="cuda"), torch.zeros(P, device="cuda")
     lcfg = dd.loss_cfg(normalize_adv=True)
-    cfg_o = dict(learner.DEFAULT_CFG, epochs=ep, minibatches=mb)
+    cfg_o = dict(learner.DEFAULT_CFG, epochs=ep, minibatches=mb, freeze_encoder=frozen)
+    from oracle import transfer
+    enc = transfer.encoder_mask(c["arch"], P) if frozen else None
+    fmask = torch.from_numpy(enc.astype(np.uint8)).cuda() if frozen else None
     k = 0
     for e in range(ep):
         for j in range(mb):
@@ -551,7 +560,8 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths):
             F = B * T_run
             env_idx = torch.from_numpy(np.ascontiguousarray(envs.astype(np.int32))).cuda()
             batch = dd.make_batch(g["goal"], g["prev_action"], g["mask"], g["h0"], g["length"], env_idx, E, T, ld, B,
-                                  T_run, int(L.sum()), obs=g.get("obs"), c0=g.get("c0"), obs_rgb=g.get("obs_rgb"))
+                                  T_run, int(L.sum()), obs=g.get("obs"), c0=g.get("c0"), obs_rgb=g.get("obs_rgb"),
+                                  freeze_encoder=frozen)
             ws = torch.zeros(dd.workspace_size(desc, B, T_run) // 4 + 64, device="cuda")
             lg, vl = torch.zeros((B, T_run, 4), device="cuda"), torch.zeros((B, T_run), device="cuda")
             dlg, dvl = torch.zeros_like(lg), torch.zeros_like(vl)
@@ -566,7 +576,9 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths):
             dd.ddppo_policy_bwd(ctx, desc, params, batch, dlg, dvl, grad, ws)
             torch.cuda.synchronize()
             g_k = grad.cpu().numpy().astype(np.float64)
-            dd.ddppo_grad_allreduce_step(ctx, grad, params, m, v, dd.adam_cfg(k + 1))
+            if frozen:
+                assert np.all(g_k[enc] == 0), k
+            dd.ddppo_grad_allreduce_step(ctx, grad, params, m, v, dd.adam_cfg(k + 1), freeze_mask=fmask)
             torch.cuda.synchronize()
             ctx.check()
             # the oracle at the kernels' parameters theta_k, with their decisions
@@ -586,15 +598,17 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths):
                     bad.append((name, e_))
             assert not bad, (k, bad)
             # a8 (N = 1): clip + Adam of the kernels' gradient
-            p_o, mm_o, vv_o, _ = optim.adam_step(theta, g_k, m_k, v_k, k + 1)
+            p_o, mm_o, vv_o, _ = optim.adam_step(theta, g_k, m_k, v_k, k + 1, freeze=enc)
             close_update(params.cpu().numpy(), theta, p_o, 1e-4, f"update {k}")
             close_rel(m.cpu().numpy(), mm_o, 1e-5, f"m {k}")
             close_rel(v.cpu().numpy(), vv_o, 1e-5, f"v {k}")
             k += 1
     chain = params.cpu().numpy()
+    if frozen:
+        assert np.array_equal(chain[enc], p0[enc])
     # the same step through ddppo_learner_step (graph-captured on its second use: run it twice)
     for it in range(2):
-        lrn = Learner(ctx, c["arch"], E, T, ep, mb, params=p0, normalize_adv=True)
+        lrn = Learner(ctx, c["arch"], E, T, ep, mb, params=p0, normalize_adv=True, freeze_encoder=frozen)
         lrn.load_rollout(ro, pm)
         lrn.step()
         torch.cuda.synchronize()
