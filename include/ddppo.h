@@ -295,6 +295,33 @@ ddppo_status ddppo_learner_workspace_size(const ddppo_model_desc* host_desc, int
  * allocated while the context lives.  World size 1: no-op.  At most one workspace per context. */
 ddppo_status ddppo_learner_register(ddppo_ctx* ctx, void* ws, size_t ws_bytes);
 
+/* ------------------------------------------------------------------ collection side (NEXT-1)
+ * Batched single-step policy inference ("collect experience with pi_theta"; P:L461 batching
+ * across a GPU's environments): step t of E envs at once, the recurrent state carried in
+ * h_in/c_in -> h_out/c_out, an action sampled per env.
+ * Inputs use the rollout layout with T = 1 slot (or a rollout's column t through pointer offsets):
+ * goal [E][T][3], prev_action / mask [E][ld] (column t), obs (bf16 depth) [E][T][1][H][W], obs_rgb
+ * (RGBD) [E][T][3][H][W]; the step read is t.  h_in / c_in [E][layers*hidden] (c: visual agents).
+ * Sampling (both the kernels and the oracle implement it): u_e = (splitmix64(seed *
+ * 0x9E3779B97F4A7C15 + counter * 0xD1B54A32D192ED03 + e) >> 40) * 2^-24; with m = max_a z_a,
+ * w_a = expf(z_a - m), S = ((w_0 + w_1) + w_2) + w_3 (fp32, this order), the action is the first a
+ * whose running sum w_0 + .. + w_a exceeds u_e * S (else A-1); logp = (z_a - m) - logf(S).
+ * greedy != 0: the first argmax instead.  Outputs (device, [E]): actions, logp, values; logits
+ * [E][A] nullable.  The workspace (ddppo_act_workspace_size) holds the forward's activations. */
+typedef struct {
+  const float* goal; const int32_t* prev_action; const float* mask;
+  const uint16_t* obs; const uint8_t* obs_rgb;
+  int32_t E, T, ld, t;
+  const float* h_in; const float* c_in;
+  float* h_out; float* c_out;
+  uint64_t seed; int64_t counter;
+  int32_t greedy; int32_t reserved;
+} ddppo_act_batch;
+ddppo_status ddppo_act_workspace_size(const ddppo_model_desc* host_desc, int E, size_t* host_bytes);
+ddppo_status ddppo_policy_act(ddppo_ctx* ctx, const ddppo_model_desc* host_desc, const float* params,
+                              const ddppo_act_batch* host_batch, int32_t* actions, float* logp, float* values,
+                              float* logits, void* ws, size_t ws_bytes, void* stream);
+
 /* Critic re-initialisation ("critic layers are reinitialized"): the value head
  * (row num_actions of head.weight and head.bias[num_actions]) is resampled from the default
  * initialiser U(-1/sqrt(fan_in), 1/sqrt(fan_in)) with a counter-based generator (element i of the

@@ -8,7 +8,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import (ARCH_DEPTH, ARCH_GPS, ARCH_RGBD, ARCH_TOY, AdamCfg, Batch, DdppoError, LearnerCfg, LossCfg, LossInputs, ModelDesc,
+from ._lib import (ActBatch, ARCH_DEPTH, ARCH_GPS, ARCH_RGBD, ARCH_TOY, AdamCfg, Batch, DdppoError, LearnerCfg, LossCfg, LossInputs, ModelDesc,
                    PreemptCfg, Rollout, TensorInfo, check, dptr, f32, f64, i32, lib, u8)
 
 __all__ = ["Context", "model_desc", "param_layout", "ddppo_gae", "ddppo_adv_norm", "ddppo_policy_fwd",
@@ -357,3 +357,30 @@ def ddppo_set_conv_engine(ctx, engine):
 def ddppo_reinit_critic(ctx, desc, params, m, v, seed, stream=None):
     """Resample the value head with the documented counter-based generator."""
     _call(ctx, "ddppo_reinit_critic", ctypes.byref(desc), f32(params), f32(m), f32(v), int(seed), _stream(stream))
+
+
+def act_workspace_size(desc, E):
+    b = ctypes.c_size_t()
+    check("ddppo_act_workspace_size", lib.ddppo_act_workspace_size(ctypes.byref(desc), E, ctypes.byref(b)))
+    return b.value
+
+
+def make_act_batch(goal, prev_action, mask, h_in, h_out, E, T, ld, t, seed, counter, obs=None, obs_rgb=None,
+                   c_in=None, c_out=None, greedy=False):
+    """Step t of E envs (rollout layout, see include/ddppo.h ddppo_act_batch)."""
+    a = ActBatch()
+    a.goal, a.prev_action, a.mask = f32(goal), i32(prev_action), f32(mask)
+    a.obs = dptr(obs, "bfloat16") if obs is not None else None
+    a.obs_rgb = u8(obs_rgb) if obs_rgb is not None else None
+    a.E, a.T, a.ld, a.t = E, T, ld, t
+    a.h_in, a.h_out = f32(h_in), f32(h_out)
+    a.c_in = f32(c_in) if c_in is not None else None
+    a.c_out = f32(c_out) if c_out is not None else None
+    a.seed, a.counter, a.greedy = int(seed), int(counter), int(greedy)
+    a._keep = (goal, prev_action, mask, obs, obs_rgb, h_in, h_out, c_in, c_out)
+    return a
+
+
+def ddppo_policy_act(ctx, desc, params, act_batch, actions, logp, values, ws, logits=None, stream=None):
+    _call(ctx, "ddppo_policy_act", ctypes.byref(desc), f32(params), ctypes.byref(act_batch), i32(actions), f32(logp),
+          f32(values), f32(logits), dptr(ws), ws.numel() * ws.element_size(), _stream(stream))

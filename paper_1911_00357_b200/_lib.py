@@ -78,6 +78,13 @@ class LearnerCfg(ctypes.Structure):
                 ("freeze_mask", c_vp), ("freeze_encoder", c_i32), ("reserved", c_i32)]
 
 
+class ActBatch(ctypes.Structure):
+    _fields_ = [("goal", c_vp), ("prev_action", c_vp), ("mask", c_vp), ("obs", c_vp), ("obs_rgb", c_vp),
+                ("E", c_i32), ("T", c_i32), ("ld", c_i32), ("t", c_i32), ("h_in", c_vp), ("c_in", c_vp),
+                ("h_out", c_vp), ("c_out", c_vp), ("seed", ctypes.c_uint64), ("counter", c_i64),
+                ("greedy", c_i32), ("reserved", c_i32)]
+
+
 P_ = ctypes.POINTER
 _SIGS = {
     "ddppo_abi_version": (c_int, []),
@@ -118,6 +125,8 @@ _SIGS = {
     "ddppo_set_graphs": (c_int, [c_vp, c_int]),
     "ddppo_set_a8_mode": (c_int, [c_vp, c_int]),
     "ddppo_set_conv_engine": (c_int, [c_vp, c_int]),
+    "ddppo_act_workspace_size": (c_int, [P_(ModelDesc), c_int, P_(c_size)]),
+    "ddppo_policy_act": (c_int, [c_vp, P_(ModelDesc), c_vp, P_(ActBatch), c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "ddppo_reinit_critic": (c_int, [c_vp, P_(ModelDesc), c_vp, c_vp, c_vp, ctypes.c_uint64, c_vp]),
     "ddppo_layout_hash": (c_int, [P_(ModelDesc), c_int, c_int, c_int, c_int, c_int, P_(ctypes.c_uint64)]),
     "ddppo_layout_check": (c_int, [c_vp, P_(ModelDesc), c_int, c_int, c_int, c_int, c_int]),

@@ -286,10 +286,29 @@ ddppo_status ddppo_preempt_poll(ddppo_ctx* ctx, int my_steps, int finished, int 
   if (!ctx) return DDPPO_ERR_CONFIG;
   int32_t h[2] = {finished ? 1 : 0, active ? 1 : 0};
   if (ctx->world > 1) {
-    DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_i32, h, sizeof(h), cudaMemcpyHostToDevice, 0));
-    DDPPO_NCCL_TRY(ctx, ncclAllReduce(ctx->d_i32, ctx->d_i32, 2, ncclInt32, ncclSum, ctx->comm, 0));
-    DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(h, ctx->d_i32, sizeof(h), cudaMemcpyDeviceToHost, 0));
-    DDPPO_CUDA_TRY(ctx, cudaStreamSynchronize(0));
+    if (ctx->peer_flags[ctx->rank]) {
+      // a registered learner's NVLink peer areas: one exchange kernel on the context's own stream
+      int64_t v[2] = {h[0], h[1]};
+      ddppo_status s = peer_allreduce_counts(ctx, v, 2);
+      if (s != DDPPO_OK) return s;
+      h[0] = (int32_t)v[0];
+      h[1] = (int32_t)v[1];
+    } else {
+      // NCCL on the context's own non-blocking stream (not queued behind the caller's work)
+      if (!ctx->cnt_stream) {
+        DDPPO_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->cnt_stream, cudaStreamNonBlocking));
+        DDPPO_CUDA_TRY(ctx, cudaMallocHost(&ctx->h_cnt, kMaxCountVals * sizeof(int64_t)));
+      }
+      int32_t* hp = reinterpret_cast<int32_t*>(ctx->h_cnt);
+      hp[0] = h[0];
+      hp[1] = h[1];
+      DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_i32, hp, sizeof(h), cudaMemcpyHostToDevice, ctx->cnt_stream));
+      DDPPO_NCCL_TRY(ctx, ncclAllReduce(ctx->d_i32, ctx->d_i32, 2, ncclInt32, ncclSum, ctx->comm, ctx->cnt_stream));
+      DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(hp, ctx->d_i32, sizeof(h), cudaMemcpyDeviceToHost, ctx->cnt_stream));
+      DDPPO_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->cnt_stream));
+      h[0] = hp[0];
+      h[1] = hp[1];
+    }
   }
   if (host_finished_count) *host_finished_count = h[0];
   if (host_active_count) *host_active_count = h[1];
@@ -310,10 +329,18 @@ ddppo_status ddppo_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n) {
   // with the NVLink peer areas set up (a registered learner): an exchange on the context's own
   // stream, so the host does not wait behind the learner work queued on the caller's stream
   if (ctx->peer_flags[ctx->rank]) return peer_allreduce_counts(ctx, host_vals, n);
-  DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_i64, host_vals, n * sizeof(int64_t), cudaMemcpyHostToDevice, 0));
-  DDPPO_NCCL_TRY(ctx, ncclAllReduce(ctx->d_i64, ctx->d_i64, n, ncclInt64, ncclSum, ctx->comm, 0));
-  DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(host_vals, ctx->d_i64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, 0));
-  DDPPO_CUDA_TRY(ctx, cudaStreamSynchronize(0));
+  if (!ctx->cnt_stream) {
+    DDPPO_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->cnt_stream, cudaStreamNonBlocking));
+    DDPPO_CUDA_TRY(ctx, cudaMallocHost(&ctx->h_cnt, kMaxCountVals * sizeof(int64_t)));
+  }
+  for (int i = 0; i < n; ++i) ctx->h_cnt[i] = host_vals[i];
+  DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_i64, ctx->h_cnt, n * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                      ctx->cnt_stream));
+  DDPPO_NCCL_TRY(ctx, ncclAllReduce(ctx->d_i64, ctx->d_i64, n, ncclInt64, ncclSum, ctx->comm, ctx->cnt_stream));
+  DDPPO_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_cnt, ctx->d_i64, n * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                      ctx->cnt_stream));
+  DDPPO_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->cnt_stream));
+  for (int i = 0; i < n; ++i) host_vals[i] = ctx->h_cnt[i];
   return DDPPO_OK;
 }
 

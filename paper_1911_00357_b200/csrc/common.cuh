@@ -5,6 +5,7 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -390,6 +391,8 @@ ddppo_status launch_lstm_fwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st)
 ddppo_status launch_lstm_bwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
 
 size_t gps_workspace(int max_B, int T);
+const float* gps_hidden_out(void* ws, int B, int T);
+void depth_state_out(const ModelLayout& L, void* ws, int B, int T_run, int l, const float** Hs, const float** Cs);
 ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                      float* logits, float* values, void* ws, cudaStream_t st, bool skip_head = false);
 ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,

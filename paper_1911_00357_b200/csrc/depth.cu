@@ -1635,6 +1635,14 @@ bool is_rgbd(const ModelLayout& L) { return layout_offset(L, "rnn.weight_ih_l0")
 
 }  // namespace
 
+// h_t / c_t of LSTM layer l for every sample [B*T_run][512] in a forward's workspace (act path)
+void depth_state_out(const ModelLayout& L, void* ws, int B, int T_run, int l, const float** Hs, const float** Cs) {
+  Plan P;
+  make_plan(L, is_rgbd(L), B, T_run, ws, &P);
+  *Hs = P.rnn[l].Hs;
+  *Cs = P.rnn[l].Cs;
+}
+
 size_t depth_workspace(int arch, int max_B, int T) {
   ddppo_model_desc d = {};
   d.arch = arch;

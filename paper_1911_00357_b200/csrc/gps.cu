@@ -1045,6 +1045,13 @@ ddppo_status launch_cluster(ddppo_ctx* ctx, K kernel, int threads, size_t smem, 
 
 size_t gps_workspace(int max_B, int T) { return carve(nullptr, max_B, T, nullptr); }
 
+// h_t of every sample [B*T][512] in a forward's workspace (the act path reads the new state there)
+const float* gps_hidden_out(void* ws, int B, int T) {
+  GpsWs w;
+  carve(ws, B, T, &w);
+  return w.Hs;
+}
+
 ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                      float* logits, float* values, void* ws, cudaStream_t st, bool skip_head) {
   DDPPO_REQUIRE(ctx, b.B >= 1 && b.B <= kBMax && b.T_run <= kTMax, "gps: minibatch must hold 1..8 envs, T <= 1024");

@@ -163,7 +163,7 @@ class Learner:
 
 
 def preempt_collect(ctx, step_costs, T, p_percent, exchange=None, world=None, on_step=None,
-                    other_workers=False):
+                    other_workers=False, tick_s=0.0):
     """Collection phase of one rank under the preemption protocol, in virtual ticks.
 
     step_costs: this rank's per-step costs in ticks (>= 1).  Every tick an active rank advances
@@ -172,16 +172,25 @@ def preempt_collect(ctx, step_costs, T, p_percent, exchange=None, world=None, on
     just completed a step applies the threshold decision (computed by the C library).  Ranks
     that stopped keep polling; everybody leaves on the first tick whose exchange shows no
     active rank.  `exchange(finished, active) -> (finished_count, active_count)` replaces the
-    NCCL poll in the gloo CPU tests (then `world` must be given).  Returns (L, ticks).
+    NCCL poll in the gloo CPU tests (then `world` must be given).  tick_s > 0: wall-clock mode (SURVEY
+    8 c-9) -- every tick lasts at least tick_s seconds of real time (the work of a completed step,
+    on_step, runs inside its tick); the decisions stay exact because each tick's exchange is
+    synchronous.  Returns (L, ticks).
     """
+    import time
     from . import ddppo_preempt_decide
     cfg = preempt_cfg(p_percent, T, other_workers=other_workers)
     if world is None:
         world = ctx.world
     steps, elapsed, tick, active, finished = 0, 0, 0, True, False
+    t_next = time.perf_counter()
     while True:
         tick += 1
         just = False
+        if tick_s > 0:
+            t_next += tick_s
+            while time.perf_counter() < t_next:
+                pass
         if active:
             elapsed += 1
             if elapsed == int(step_costs[steps]):

@@ -234,3 +234,81 @@ def random_loss_inputs(M, seed, A=NUM_ACTIONS, scale=1.0):
                 values_old=rng.normal(0, 1, M).astype(f32),
                 returns=rng.normal(0, 1, M).astype(f32),
                 adv=rng.normal(0, 1, M).astype(f32))
+
+
+class PointGoalEnv:
+    """E synthetic PointGoal episodes stepped by the policy's own actions (the collection side of
+    NEXT-1; the same dynamics as rollout(): P:L195-223, P:L207 actions, P:L221 reward, P:L588 goal
+    [d, cos th, sin th]).  Frames: per env and channel three drifting low-frequency cosine fields +
+    5 % noise (depth in [0, 1], bf16-exact; RGB integer bytes), as in depth_frames / rgbd_frames.
+    Episodes start fresh (mask 0, prev action = start token) and end on stop or after 500 steps."""
+
+    def __init__(self, E, seed, rank=0, obs=None, H=64):
+        self.E, self.obs_kind, self.H = E, obs, H
+        self.rng = _rng(seed, 7, rank)
+        rng = self.rng
+        self.d0 = rng.uniform(1.0, 20.0, E)
+        self.d = self.d0.copy()
+        self.theta = rng.uniform(-np.pi, np.pi, E)
+        self.path = np.zeros(E)
+        self.age = np.zeros(E, np.int64)
+        self.prev = np.full(E, START_TOKEN, np.int64)
+        self.m_prev = np.zeros(E)
+        self.C = 0 if obs is None else (4 if obs == "rgbd" else 1)
+        if self.C:
+            yy, xx = np.meshgrid(np.linspace(0, 1, H), np.linspace(0, 1, H), indexing="ij")
+            self._xy = (xx, yy)
+            self.k = rng.uniform(0.5, 3.0, (E, self.C, 3, 2))
+            self.ph = rng.uniform(0, 2 * np.pi, (E, self.C, 3))
+            self.drift = rng.uniform(-0.05, 0.05, (E, self.C, 3))
+
+    def observe(self):
+        """(goal [E][3], prev_action [E], mask [E], frames [E][C][H][W] float32 or None) of the current
+        state (the same arrays until the next step())."""
+        if getattr(self, "_obs", None) is not None:
+            return self._obs
+        goal = np.stack([self.d, np.cos(self.theta), np.sin(self.theta)], 1).astype(np.float32)
+        frames = None
+        if self.C:
+            xx, yy = self._xy
+            frames = np.empty((self.E, self.C, self.H, self.H), np.float32)
+            for n in range(self.E):
+                for ch in range(self.C):
+                    f = sum(np.cos(2 * np.pi * (self.k[n, ch, i, 0] * xx + self.k[n, ch, i, 1] * yy) + self.ph[n, ch, i]
+                                   + self.drift[n, ch, i] * self.age[n]) for i in range(3))
+                    f = np.clip(0.5 + f / 6.0 + 0.05 * self.rng.standard_normal((self.H, self.H)), 0.0, 1.0)
+                    rgb = self.C == 4 and ch < 3
+                    frames[n, ch] = np.rint(255.0 * f) if rgb else bf16_exact(f)
+        self._obs = (goal, self.prev.astype(np.int32), self.m_prev.astype(np.float32), frames)
+        return self._obs
+
+    def step(self, a):
+        """actions [E] in {stop, forward, left, right} -> (reward [E] float32, done [E] uint8)."""
+        a = np.asarray(a, np.int64)
+        rng, E = self.rng, self.E
+        self._obs = None
+        d_old = self.d.copy()
+        collide = rng.random(E) < 0.1
+        fwd = (a == 1) & ~collide
+        gx = self.d * np.cos(self.theta) - 0.25 * fwd
+        gy = self.d * np.sin(self.theta)
+        self.d = np.where(fwd, np.hypot(gx, gy), self.d)
+        th = np.where(fwd, np.arctan2(gy, gx), self.theta)
+        th = th + np.where(a == 2, -np.pi / 18, 0.0) + np.where(a == 3, np.pi / 18, 0.0)
+        self.theta = (th + np.pi) % (2 * np.pi) - np.pi
+        self.path = self.path + 0.25 * fwd
+        r = -(self.d - d_old) - 0.01
+        self.age = self.age + 1
+        ended = (a == 0) | (self.age >= 500)
+        success = (a == 0) & (d_old <= 0.2)
+        r = r + 2.5 * np.where(success, self.d0 / np.maximum(self.d0, np.maximum(self.path, 1e-6)), 0.0)
+        nd0 = rng.uniform(1.0, 20.0, E)
+        nth = rng.uniform(-np.pi, np.pi, E)
+        self.d0 = np.where(ended, nd0, self.d0)
+        self.d = np.where(ended, nd0, self.d)
+        self.theta = np.where(ended, nth, self.theta)
+        self.path = np.where(ended, 0.0, self.path)
+        self.age = np.where(ended, 0, self.age)
+        self.prev = np.where(ended, START_TOKEN, a)
+        self.m_prev = np.where(ended, 0.0, 1.0)
+        return r.astype(np.float32), ended.astype(np.uint8)

@@ -108,6 +108,22 @@ def _worker_body(rank, world, port, q):
     out["depth_params"] = lrd.params.cpu().numpy()
     out["depth_moved"] = float(np.abs(out["depth_params"] - pd0).max())
     cxd.close()
+    # ---- NEXT-1: collection by the policy itself under the preemption protocol in wall-clock ticks
+    # (the poll runs over the registered learner's NVLink peer areas), then the learner step
+    from paper_1911_00357_b200.collect import Collector
+    Tc = 24
+    costs_c = synth.straggler_costs(11, world, Tc, lo=1.0, hi=6.0)
+    costs_c[world - 1] *= 4
+    lrc = Learner(ctx, "gps", c["E"], Tc, c["epochs"], c["minibatches"], params=p0, peer=False, normalize_adv=True)
+    col = Collector(lrc, synth.PointGoalEnv(c["E"], 12, rank=rank), seed=12 + rank)
+    roc = col.collect(Tc, costs=costs_c[rank], p_percent=50, tick_s=1e-4)
+    out["L_collect"] = int(roc["length"][0])
+    out["L_collect_ref"] = int(preempt.closed_form_lengths(costs_c, Tc, 50)[rank])
+    lrc.load_rollout(roc, synth.perms(12, 0, c["epochs"], c["E"], rank=rank))
+    lrc.step()
+    torch.cuda.synchronize()
+    ctx.check()
+    out["collect_params"] = lrc.params.cpu().numpy()
     # ---- a10 counts
     out["counts"] = dd.ddppo_allreduce_counts(ctx, [c["E"] * L, rank + 1]).tolist()
     # (registered learner: the NVLink exchange; repeated calls cycle its double-buffered slots)
@@ -143,7 +159,7 @@ def test_two_rank_learner_step_and_protocols():
         assert "error" not in res[r], res[r]["error"]
     for p in procs:
         p.join(timeout=120)
-    for key in ("params", "params_nccl", "params2", "params_allread", "depth_params"):
+    for key in ("params", "params_nccl", "params2", "params_allread", "depth_params", "collect_params"):
         assert np.array_equal(res[0][key], res[1][key]), key  # rank-identical
     assert res[0]["protocol"] == res[1]["protocol"] == 3  # DDPPO_ERR_PROTOCOL on both ranks
     assert res[0]["depth_moved"] > 1e-4
@@ -173,4 +189,6 @@ def test_two_rank_learner_step_and_protocols():
     assert res[0]["counts_rep"] == res[1]["counts_rep"] == [[20 * i + 1, -2 * i] for i in range(5)]
     for r in range(world):
         assert res[r]["L"] == res[r]["L_ref"]
+        assert res[r]["L_collect"] == res[r]["L_collect_ref"]
+    assert res[0]["L_collect"] == 24 > res[1]["L_collect"]  # the slow rank was preempted
     assert res[0]["ticks"] == res[1]["ticks"]
