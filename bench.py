@@ -390,11 +390,12 @@ def main():
     except Exception:
         pass
     fam_ms = {k: v[0] for k, v in prof.items()}
-    # the dominant compute family (the a8 exchange family's time is mostly the cross-rank barrier
-    # wait at N > 1, not a kernel with a roofline)
-    dom = max((k for k in fam_ms if k != "allreduce"), key=fam_ms.get)
+    # the dominant kernel: the TMA implicit-GEMM convolution for the visual agents, the GRU
+    # recurrence for GPS (sub-families "conv" / "rnn": CUDA events around each launch on its stream)
+    dom = "conv" if c["arch"] in ("depth", "rgbd") else "rnn" if c["arch"] == "gps" else "net_fwd"
     launches = {k: v[1] for k, v in launches_timed.items()}
     roofline = roofline_for(dom, prof, c, lrn, peaks, prof_steps)
+    kernels = kernel_table(prof, c, lrn, peaks, prof_steps)
     gpu_launches = int(sum(v for k, v in launches.items() if k != "allreduce"))
 
     cpu_base = None
@@ -417,7 +418,7 @@ def main():
                        "wall_s_timed_loop": t_wall},
             "clocks": clocks, "e2e": e2e, "gpu_launches": gpu_launches, "preemption": preempt,
             "kernel_ms": {k: round(v, 4) for k, v in fam_ms.items() if v > 0},
-            "kernel_ms_steps": prof_steps,
+            "kernel_ms_steps": prof_steps, "kernels": kernels,
             "roofline": roofline, "cpu_baseline": cpu_base,
         }
         print(json.dumps(out), file=JSON_OUT, flush=True)
@@ -472,49 +473,64 @@ def _traffic(*kernels):
     return sum(vals) if len(vals) == len(kernels) else None
 
 
+def _traffic_r02(kind):
+    """DRAM bytes per launch of a kernel kind from the committed ncu --set full capture summary
+    (profiles/r02_traffic.json, written by tools/make_traffic.py); None if not captured."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    return t.get(kind, {}).get("bytes_per_launch")
+
+
 def roofline_for(fam, prof, c, lrn, peaks, steps):
-    """Algorithmic work of one launch of the dominant family / its mean device time."""
-    ms, n = prof[fam]
-    if c["arch"] in ("depth", "rgbd") and fam in ("net_fwd", "net_bwd"):
-        n = steps * c["epochs"] * c["minibatches"]  # one "launch" = one minibatch pass of the family
+    """The dominant kernel: its algorithmic work (host-side accounting at each launch: useful dense
+    FLOPs, the bf16x3 forward counted once) / its device time (CUDA events around every launch on
+    the launching stream, the eager profiling pass), against the measured sustained bf16 peak."""
+    ms, n, flops = prof[fam]
+    bf16 = peaks.get("bf16_tflops_sustained", 1400.0)
     per_launch_s = (ms / 1e3) / max(n, 1)
+    achieved = flops / max(ms / 1e3, 1e-12) / 1e12
+    kern = {"conv": "tconv_kernel (TMA implicit-GEMM FPROP / DGRAD / WGRAD)",
+            "rnn": "gps_gru_fwd/bwd_kernel" if c["arch"] == "gps" else "lstm_fwd/bwd_kernel"}.get(fam, fam)
+    out = {"bound": "tensor", "kernel": kern, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+           "frac": achieved / bf16, "traffic": _traffic_r02(fam), "launch_us": per_launch_s * 1e6,
+           "launches_per_step": n / max(steps, 1), "flops_per_launch": flops / max(n, 1),
+           "share_of_step": ms / max(sum(v[0] for k, v in prof.items() if k in (
+               "gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other")), 1e-9)}
+    if fam == "rnn":
+        out["note"] = ("latency-bound dependency chain (B = E/2 envs x 128 steps on one 16-CTA cluster); "
+                       "per-step phases in DESIGN.md")
+    else:
+        out["note"] = ("small implicit GEMMs (N = 32..256, <= 512 tiles) latency / launch bound; per-kernel "
+                       "table in 'kernels' and profiles/r02_kernels_depth.md")
+    return out
+
+
+def kernel_table(prof, c, lrn, peaks, steps):
+    """Per kernel (sub-)family: ms and launches per step, achieved rate and fraction of its roofline
+    (tensor: measured sustained bf16; HBM: measured copy bandwidth)."""
     hbm = peaks.get("hbm_gbs", 6650.0)
     bf16 = peaks.get("bf16_tflops_sustained", 1400.0)
-    E, T, H = c["E"], c["T"], lrn.hidden
+    E, T = c["E"], c["T"]
     B = E // c["minibatches"]
-    if fam in ("net_fwd", "net_bwd") and c["arch"] == "gps":
-        # per launch: the tcgen05 matvecs of the 128-step chain (fwd: [W_hh|W_ih][h;x]; bwd: W_hh^T dG_h),
-        # useful (unpadded) FLOPs; peak = measured sustained bf16 (kind::f16 runs fp16/bf16 at one rate)
-        flops = 2.0 * B * T * (3 * H) * (H + (64 if fam == "net_fwd" else 0))
-        achieved = flops / per_launch_s / 1e12
-        kern = "gps_gru_fwd_kernel" if fam == "net_fwd" else "gps_gru_bwd_kernel"
-        return {"bound": "tensor", "kernel": fam, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": _traffic(kern), "traffic_kernel": kern,
-                "launch_us": per_launch_s * 1e6,
-                "note": "latency-bound dependency chain (B=2 envs x 128 steps on 16 SMs); per-step phases in "
-                        "DESIGN.md sec. 7; HBM kernels' fractions in profiles/r01_microbench.jsonl"}
-    if fam in ("net_fwd", "net_bwd") and c["arch"] in ("depth", "rgbd"):
-        # the family = one minibatch pass: encoder implicit GEMMs (+ GroupNorm / pool SIMT), FC,
-        # LSTM input GEMM and recurrence; algorithmic FLOPs = the dense contractions, counted once
-        # (the forward's bf16x3 operand planes cost 3 MMAs per product but count once here)
-        frames = B * T
-        enc = depth_encoder_macs(c["arch"])
-        fc_in, layers = (2048, 2) if c["arch"] == "rgbd" else (512, 1)
-        rnn_in = 576 * 2048 + (layers - 1) * H * 2048  # input GEMMs of the LSTM layers
-        dense_fwd = 2.0 * (enc["all"] + fc_in * 512 + rnn_in + layers * 2048 * H)
-        dense_bwd = 2.0 * (2 * enc["all"] - enc["stem"] + 2 * (fc_in * 512 + rnn_in) + 2 * layers * 2048 * H)
-        flops = frames * (dense_fwd if fam == "net_fwd" else dense_bwd)
-        achieved = flops / per_launch_s / 1e12
-        return {"bound": "tensor", "kernel": fam, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": None, "launch_us": per_launch_s * 1e6,
-                "note": "kernel family of one minibatch pass (ResNet implicit GEMMs + GroupNorm + LSTM-512 "
-                        "recurrences); per-kernel split in profiles/"}
-    byte_per = {"gae": 17.0 * E * T, "loss": 60.0 * B * T, "adam": 28.0 * lrn.P}  # Adam: read g, p, m, v; write p, m, v
-    b = byte_per.get(fam, 0.0)
-    achieved = b / per_launch_s / 1e9 if b else 0.0
-    traffic = {"adam": _traffic("grad_norm_kernel", "adam_kernel")}.get(fam)
-    return {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": traffic, "launch_us": per_launch_s * 1e6}
+    out = {}
+    for fam, (ms, n, flops) in prof.items():
+        if ms <= 0:
+            continue
+        row = {"ms_per_step": ms / max(steps, 1), "launches_per_step": n / max(steps, 1)}
+        if flops > 0:
+            a = flops / (ms / 1e3) / 1e12
+            row.update(achieved_tflops=a, frac=a / bf16)
+        # algorithmic bytes per step: GAE 17 B per element (once per step); loss 60 B per sample and
+        # Adam 28 B per parameter (read g, p, m, v; write p, m, v) once per minibatch update
+        n_mb = c["epochs"] * c["minibatches"]
+        byts = {"gae": 17.0 * E * T, "loss": 60.0 * B * T * n_mb, "adam": 28.0 * lrn.P * n_mb}.get(fam)
+        if byts:
+            a = byts * steps / (ms / 1e3) / 1e9
+            row.update(achieved_gbs=a, frac=a / hbm)
+        out[fam] = row
+    return out
 
 
 if __name__ == "__main__":

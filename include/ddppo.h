@@ -388,12 +388,19 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
  * ddppo_profile_read is blocking (synchronises the recorded events); reset != 0 clears. */
 typedef enum {
   DDPPO_K_GAE = 0, DDPPO_K_ADV_NORM, DDPPO_K_NET_FWD, DDPPO_K_HEAD, DDPPO_K_LOSS, DDPPO_K_NET_BWD,
-  DDPPO_K_WGRAD, DDPPO_K_ALLREDUCE, DDPPO_K_ADAM, DDPPO_K_OTHER, DDPPO_K_COUNT
+  DDPPO_K_WGRAD, DDPPO_K_ALLREDUCE, DDPPO_K_ADAM, DDPPO_K_OTHER,
+  /* sub-families, nested inside the ones above (their time is also counted there): the TMA
+   * implicit-GEMM convolution kernel, the recurrence kernels (GRU / LSTM, fwd + BPTT), GroupNorm */
+  DDPPO_K_CONV, DDPPO_K_RNN, DDPPO_K_GN, DDPPO_K_COUNT
 } ddppo_kernel_family;
 
 ddppo_status ddppo_profile_enable(ddppo_ctx* ctx, int enable);
 ddppo_status ddppo_profile_read(ddppo_ctx* ctx, double* host_ms /* [DDPPO_K_COUNT] */,
                                 int64_t* host_launches /* [DDPPO_K_COUNT] */, int reset);
+/* Algorithmic work issued per family since the last reset (host-side accounting at launch: useful
+ * dense-contraction FLOPs, 2*M*N*K with the bf16x3 forward counted once; counted while profiling
+ * is enabled, i.e. for eager launches).  reset != 0 clears. */
+ddppo_status ddppo_profile_flops(ddppo_ctx* ctx, double* host_flops /* [DDPPO_K_COUNT] */, int reset);
 
 /* Diagnostic entry to the tcgen05 GEMM used inside the backward (stream-ordered):
  * C[m][n] = sum_k A[m*sam + k*sak] * B[n*sbn + k*sbk]; operands rounded to bf16, fp32 accumulate

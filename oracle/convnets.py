@@ -12,7 +12,12 @@ Test infrastructure only.  NumPy float64, NCHW, textbook definitions:
     layers 2-4 with a 1x1/stride conv + GN shortcut), then the 3x3 compression conv to 128
     channels + GN + ReLU (P:L582, Z20);
   * half-width ResNet50 for the RGB-D agent (bottlenecks [3, 4, 6, 3], 2x2 average pooling of the
-    256^2 input first, channel-wise RGB normalisation P:L367) -> 1024x4x4 -> compression to 128x4x4.
+    256^2 input first, channel-wise RGB normalisation P:L367) -> 1024x4x4 -> compression to 128x4x4;
+  * half-width SE-ResNeXt50 (NEXT-3; reading R9 in DESIGN.md): the ResNet50/2
+    topology with each bottleneck's 3x3 convolution grouped (cardinality 16 over an inner width of
+    2 x planes, Xie et al.'s aggregated transformations) and a squeeze-excitation module (Hu et al.:
+    global average pool -> FC C/16 + ReLU -> FC C + sigmoid -> channel scale; reduction 16) on the
+    residual branch before the addition.
 """
 import numpy as np
 
@@ -276,6 +281,149 @@ def resnet50h_bwd(dz, p, caches, g):
         dout = dz * caches[pre + ".out"]
         db = _conv_gn_bwd(dout, p, pre + ".conv3", pre + ".gn3", False, caches, g)
         da = _conv_gn_bwd(db, p, pre + ".conv2", pre + ".gn2", True, caches, g)
+        dx = _conv_gn_bwd(da, p, pre + ".conv1", pre + ".gn1", True, caches, g)
+        if s != 1 or cin != 4 * w:
+            dx = dx + _conv_gn_bwd(dout, p, pre + ".down.conv", pre + ".down.gn", False, caches, g)
+        else:
+            dx = dx + dout
+        dz = dx
+    dz = maxpool_bwd(dz, caches["pool"])
+    dz = _conv_gn_bwd(dz, p, "enc.stem.conv", "enc.stem.gn", True, caches, g)
+    dx = avgpool2_bwd(dz)
+    for c in range(3):
+        dx[:, c] /= RGB_STD[c]
+    return dx
+
+
+# ---------------------------------------------------------------- SE-ResNeXt50/2 (NEXT-3)
+SERX_CARD = 16   # cardinality of the grouped 3x3 convolutions (R9)
+SE_RED = 16      # squeeze-excitation reduction
+
+
+def conv_fwd_grouped(x, W, s, p, groups):
+    """Grouped convolution: input and output channels split into `groups` equal parts, group g's
+    outputs see only group g's inputs; W [O][C/groups][k][k]."""
+    C, O = x.shape[1], W.shape[0]
+    cg, og = C // groups, O // groups
+    ys, cs = [], []
+    for g in range(groups):
+        y, cc = conv_fwd(x[:, g * cg:(g + 1) * cg], W[g * og:(g + 1) * og], s, p)
+        ys.append(y)
+        cs.append(cc)
+    return np.concatenate(ys, axis=1), (cs, groups)
+
+
+def conv_bwd_grouped(dy, W, s, p, cache):
+    cs, groups = cache
+    O = W.shape[0]
+    og = O // groups
+    dxs, dWs = [], []
+    for g in range(groups):
+        dx, dW = conv_bwd(dy[:, g * og:(g + 1) * og], W[g * og:(g + 1) * og], s, p, cs[g])
+        dxs.append(dx)
+        dWs.append(dW)
+    return np.concatenate(dxs, axis=1), np.concatenate(dWs, axis=0)
+
+
+def sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def se_fwd(x, W1, b1, W2, b2):
+    """y = x * s[:, :, None, None], s = sigmoid(W2 relu(W1 mean_hw(x) + b1) + b2)."""
+    pooled = x.mean(axis=(2, 3))
+    a1 = pooled @ W1.T + b1
+    h = np.maximum(a1, 0.0)
+    sc = sigmoid(h @ W2.T + b2)
+    return x * sc[:, :, None, None], (x, pooled, a1, h, sc)
+
+
+def se_bwd(dy, W1, W2, cache):
+    x, pooled, a1, h, sc = cache
+    HW = x.shape[2] * x.shape[3]
+    ds = (dy * x).sum(axis=(2, 3))
+    da2 = ds * sc * (1.0 - sc)
+    dW2, db2 = da2.T @ h, da2.sum(0)
+    da1 = (da2 @ W2) * (a1 > 0)
+    dW1, db1 = da1.T @ pooled, da1.sum(0)
+    dpooled = da1 @ W1
+    dx = dy * sc[:, :, None, None] + dpooled[:, :, None, None] / HW
+    return dx, dW1, db1, dW2, db2
+
+
+def serx50h_spec(in_ch):
+    """Ordered (name, kind, shape, stride, pad) of the SE-ResNeXt50/2 encoder's parameter tensors
+    (kind "gconv": grouped, cardinality SERX_CARD; "fc": SE linear layers with a bias)."""
+    spec = [("enc.stem.conv", "conv", (32, in_ch, 7, 7), 2, 3), ("enc.stem.gn", "gn", (32,), 0, 0)]
+    cin = 32
+    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+        for bi in range(nb):
+            s = 2 if (bi == 0 and li > 0) else 1
+            pre = f"enc.layer{li + 1}.{bi}"
+            wi, co = 2 * w, 4 * w
+            spec += [(pre + ".conv1", "conv", (wi, cin, 1, 1), 1, 0), (pre + ".gn1", "gn", (wi,), 0, 0),
+                     (pre + ".conv2", "gconv", (wi, wi // SERX_CARD, 3, 3), s, 1), (pre + ".gn2", "gn", (wi,), 0, 0),
+                     (pre + ".conv3", "conv", (co, wi, 1, 1), 1, 0), (pre + ".gn3", "gn", (co,), 0, 0),
+                     (pre + ".se.fc1", "fc", (co // SE_RED, co), 0, 0), (pre + ".se.fc2", "fc", (co, co // SE_RED), 0, 0)]
+            if s != 1 or cin != co:
+                spec += [(pre + ".down.conv", "conv", (co, cin, 1, 1), s, 0),
+                         (pre + ".down.gn", "gn", (co,), 0, 0)]
+            cin = co
+    spec += [("enc.compress.conv", "conv", (128, 1024, 3, 3), 1, 1), ("enc.compress.gn", "gn", (128,), 0, 0)]
+    return spec
+
+
+def serx50h_fwd(x, p):
+    """x [N][4][256][256] (raw RGB-D) -> feature [N][128][4][4]."""
+    caches = {}
+    z = avgpool2_fwd(rgbd_normalize(x))
+    z = _conv_gn(z, p, "enc.stem.conv", "enc.stem.gn", 2, 3, True, caches)
+    z, caches["pool"] = maxpool_fwd(z)
+    cin = 32
+    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+        for bi in range(nb):
+            s = 2 if (bi == 0 and li > 0) else 1
+            pre = f"enc.layer{li + 1}.{bi}"
+            a = _conv_gn(z, p, pre + ".conv1", pre + ".gn1", 1, 0, True, caches)
+            y2, cc2 = conv_fwd_grouped(a, p[pre + ".conv2.weight"], s, 1, SERX_CARD)
+            b, gc2 = gn_fwd(y2, p[pre + ".gn2.weight"], p[pre + ".gn2.bias"])
+            caches[pre + ".conv2"] = (cc2, gc2, s, 1)
+            caches[pre + ".conv2.relu"] = b > 0
+            b = np.maximum(b, 0.0)
+            c3 = _conv_gn(b, p, pre + ".conv3", pre + ".gn3", 1, 0, False, caches)
+            e, caches[pre + ".se"] = se_fwd(c3, p[pre + ".se.fc1.weight"], p[pre + ".se.fc1.bias"],
+                                            p[pre + ".se.fc2.weight"], p[pre + ".se.fc2.bias"])
+            sc = z
+            if s != 1 or cin != 4 * w:
+                sc = _conv_gn(z, p, pre + ".down.conv", pre + ".down.gn", s, 0, False, caches)
+            out = e + sc
+            caches[pre + ".out"] = out > 0
+            z = np.maximum(out, 0.0)
+            cin = 4 * w
+    z = _conv_gn(z, p, "enc.compress.conv", "enc.compress.gn", 1, 1, True, caches)
+    return z, caches
+
+
+def serx50h_bwd(dz, p, caches, g):
+    """Parameter gradients into g; returns the gradient wrt the raw input."""
+    dz = _conv_gn_bwd(dz, p, "enc.compress.conv", "enc.compress.gn", True, caches, g)
+    blocks = []
+    cin = 32
+    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+        for bi in range(nb):
+            blocks.append((li, bi, w, cin))
+            cin = 4 * w
+    for li, bi, w, cin in reversed(blocks):
+        s = 2 if (bi == 0 and li > 0) else 1
+        pre = f"enc.layer{li + 1}.{bi}"
+        dout = dz * caches[pre + ".out"]
+        de, g[pre + ".se.fc1.weight"], g[pre + ".se.fc1.bias"], g[pre + ".se.fc2.weight"], g[pre + ".se.fc2.bias"] = \
+            se_bwd(dout, p[pre + ".se.fc1.weight"], p[pre + ".se.fc2.weight"], caches[pre + ".se"])
+        db = _conv_gn_bwd(de, p, pre + ".conv3", pre + ".gn3", False, caches, g)
+        cc2, gc2, s2, pad2 = caches[pre + ".conv2"]
+        db = db * caches[pre + ".conv2.relu"]
+        dy2, g[pre + ".gn2.weight"], g[pre + ".gn2.bias"] = gn_bwd(db, p[pre + ".gn2.weight"], gc2)
+        da, g[pre + ".conv2.weight"] = conv_bwd_grouped(dy2, p[pre + ".conv2.weight"], s2, pad2, cc2)
         dx = _conv_gn_bwd(da, p, pre + ".conv1", pre + ".gn1", True, caches, g)
         if s != 1 or cin != 4 * w:
             dx = dx + _conv_gn_bwd(dout, p, pre + ".down.conv", pre + ".down.gn", False, caches, g)

@@ -19,6 +19,8 @@ Architectures (BASELINE.json configs; readings Z17-Z22):
                      -> 128x2x2 -> flatten (c, h, w order) -> Linear(512, 512) + ReLU
                      (Z17, Z20); x = [visual 512, goal_fc 32, act_emb 32]
                      -> LSTM(576, 512) (PyTorch i, f, g, o) -> Linear(512, A+1).
+  serx50 (NEXT-3, P:L212 / P:L582): the RGB-D agent with the half-width SE-ResNeXt50 encoder
+                     (convnets.serx50h_*; reading R9), same policy.
   rgbd (configs[3]): RGB-D [4][256][256] (RGB in [0, 255] normalised channel-wise) ->
                      2x2 avg-pool -> half-width ResNet50 (convnets.py) -> 128x4x4 -> flatten ->
                      Linear(2048, 512) + ReLU; x = [visual, goal_fc, act_emb] -> 2-layer LSTM-512
@@ -62,12 +64,15 @@ def layout(arch, hidden=512, num_actions=NUM_ACTIONS):
                       ("rnn.weight_ih", (G, 576), H), ("rnn.weight_hh", (G, H), H),
                       ("rnn.bias_ih", (G,), H), ("rnn.bias_hh", (G,), H),
                       ("head.weight", (A1, H), H), ("head.bias", (A1,), H)]
-    if arch == "rgbd":
+    if arch in ("rgbd", "serx50"):
         H, G = hidden, 4 * hidden
         out = []
-        for name, kind, shape, _, _ in convnets.resnet50h_spec(4):
-            if kind == "conv":
+        spec = convnets.resnet50h_spec(4) if arch == "rgbd" else convnets.serx50h_spec(4)
+        for name, kind, shape, _, _ in spec:
+            if kind in ("conv", "gconv"):
                 out.append((name + ".weight", shape, shape[1] * shape[2] * shape[3]))
+            elif kind == "fc":  # SE linear layer: torch's default init U(+-1/sqrt(fan_in)), weight and bias
+                out += [(name + ".weight", shape, shape[1]), (name + ".bias", shape[:1], shape[1])]
             else:
                 out += [(name + ".weight", shape, 0), (name + ".bias", shape, -1)]
         out += [("visual_fc.weight", (512, 2048), 2048), ("visual_fc.bias", (512,), 2048),
@@ -146,10 +151,11 @@ def forward(arch, flat, batch, **kw):
         out = nets.linear_fwd(h, p["head.weight"], p["head.bias"])
         cache = {"goal": goal, "prev_action": np.asarray(batch["prev_action"]), "h": h, "rnn": rc, "enc": ec,
                  "feat_shape": feat.shape, "flat": flat_f, "vis": vis}
-    elif arch == "rgbd":
+    elif arch in ("rgbd", "serx50"):
         obs = np.asarray(batch["obs"], dtype=np.float64)  # [B][T][4][256][256]
         B, T = obs.shape[:2]
-        feat, ec = convnets.resnet50h_fwd(obs.reshape((B * T,) + obs.shape[2:]), p)
+        enc_fwd = convnets.resnet50h_fwd if arch == "rgbd" else convnets.serx50h_fwd
+        feat, ec = enc_fwd(obs.reshape((B * T,) + obs.shape[2:]), p)
         flat_f = feat.reshape(B, T, -1)  # (c, h, w) order, 2048
         vis = np.maximum(nets.linear_fwd(flat_f, p["visual_fc.weight"], p["visual_fc.bias"]), 0.0)
         ge = nets.linear_fwd(goal, p["goal_fc.weight"], p["goal_fc.bias"])
@@ -209,7 +215,7 @@ def backward(arch, flat, cache, dlogits, dvalues, freeze_encoder=False, extra=No
                                                                             dvpre)
         if not freeze_encoder:
             convnets.resnet18h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
-    elif arch == "rgbd":
+    elif arch in ("rgbd", "serx50"):
         dh, g["head.weight"], g["head.bias"] = nets.linear_bwd(cache["h"], p["head.weight"], dout)
         for layer in (1, 0):
             dh, g[f"rnn.weight_ih_l{layer}"], g[f"rnn.weight_hh_l{layer}"], g[f"rnn.bias_ih_l{layer}"], \
@@ -225,7 +231,8 @@ def backward(arch, flat, cache, dlogits, dvalues, freeze_encoder=False, extra=No
         dflat, g["visual_fc.weight"], g["visual_fc.bias"] = nets.linear_bwd(cache["flat"], p["visual_fc.weight"],
                                                                             dvpre)
         if not freeze_encoder:
-            convnets.resnet50h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
+            (convnets.resnet50h_bwd if arch == "rgbd" else convnets.serx50h_bwd)(
+                dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
     else:
         raise ValueError(arch)
     return pack(arch, g, **kw)

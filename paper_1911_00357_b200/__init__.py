@@ -269,12 +269,14 @@ def profile_enable(ctx, on=True):
 
 
 def profile_read(ctx, reset=False):
-    """{family: (ms, launches)} accumulated since the last reset (blocking)."""
+    """{family: (ms, launches, flops)} accumulated since the last reset (blocking)."""
     n = len(_lib.KERNEL_FAMILIES)
     ms = (ctypes.c_double * n)()
     la = (ctypes.c_int64 * n)()
+    fl = (ctypes.c_double * n)()
     _call(ctx, "ddppo_profile_read", ms, la, int(reset))
-    return {k: (ms[i], la[i]) for i, k in enumerate(_lib.KERNEL_FAMILIES)}
+    _call(ctx, "ddppo_profile_flops", fl, int(reset))
+    return {k: (ms[i], la[i], fl[i]) for i, k in enumerate(_lib.KERNEL_FAMILIES)}
 
 
 def ddppo_set_graphs(ctx, enable=True):

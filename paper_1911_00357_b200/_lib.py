@@ -114,6 +114,7 @@ _SIGS = {
                                    c_vp, c_vp, c_size, P_(c_i32), c_vp]),
     "ddppo_profile_enable": (c_int, [c_vp, c_int]),
     "ddppo_profile_read": (c_int, [c_vp, c_vp, c_vp, c_int]),
+    "ddppo_profile_flops": (c_int, [c_vp, c_vp, c_int]),
     "ddppo_debug_gemm_bf16": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_int, c_int,
                                       c_int, c_vp, c_int, c_vp]),
     "ddppo_debug_conv2d": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
@@ -135,7 +136,8 @@ _SIGS = {
     "ddppo_debug_peer_counts": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_size, P_(c_size)]),
     "ddppo_debug_maxpool": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
-KERNEL_FAMILIES = ("gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other")
+KERNEL_FAMILIES = ("gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other",
+                   "conv", "rnn", "gn")
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
     _f.restype = _res

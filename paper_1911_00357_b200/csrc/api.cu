@@ -795,6 +795,15 @@ ddppo_status ddppo_profile_enable(ddppo_ctx* ctx, int enable) {
   return DDPPO_OK;
 }
 
+ddppo_status ddppo_profile_flops(ddppo_ctx* ctx, double* host_flops, int reset) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  for (int i = 0; i < DDPPO_K_COUNT; ++i) {
+    if (host_flops) host_flops[i] = ctx->flops[i];
+    if (reset) ctx->flops[i] = 0.0;
+  }
+  return DDPPO_OK;
+}
+
 ddppo_status ddppo_profile_read(ddppo_ctx* ctx, double* host_ms, int64_t* host_launches, int reset) {
   if (!ctx) return DDPPO_ERR_CONFIG;
   for (auto& r : ctx->pending) {

@@ -1409,6 +1409,7 @@ static int gn_vpt(int n, int nt) { return (n + nt - 1) / nt; }
 ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const float* gamma, const float* beta,
                     const float* residual, int relu, float* stats, float* z, __nv_bfloat16* zb, double* gpart,
                     cudaStream_t st) {
+  ProfScope pg(ctx, DDPPO_K_GN, st, 0);
   const int nt = gn_threads(C);
   DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");
   const int S = (HW * C + gn_chunk(C) - 1) / gn_chunk(C);
@@ -1495,6 +1496,7 @@ static ddppo_status gn_bwd_cluster(ddppo_ctx* ctx, K kern, int S, int F, int nt,
 ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const float* relu_z, const float* y,
                     const float* stats, const float* gamma, __nv_bfloat16* dy, float* dgamma, float* dbeta,
                     float* part, double* gpart, cudaStream_t st, bool reduce_params = true, size_t lo = 0) {
+  ProfScope pg(ctx, DDPPO_K_GN, st, 0);
   ddppo_status s = DDPPO_OK;
   const int nt = gn_threads(C);
   DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");

@@ -1058,7 +1058,9 @@ ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   GpsPtrs p = make_ptrs(L, params, b, ws);
   const int S = b.B * b.T_run;
   {
-    ProfScope ps(ctx, DDPPO_K_NET_FWD, st, 1);
+    ProfScope ps(ctx, DDPPO_K_NET_FWD, st, 0);
+    ProfScope pr(ctx, DDPPO_K_RNN, st, 1);
+    if (ctx->prof) ctx->flops[DDPPO_K_RNN] += 2.0 * S * kG * (kH + kIn);
     ddppo_status s =
         launch_cluster(ctx, gps_gru_fwd_kernel, kFwdThreads, sizeof(FwdSmem) + (size_t)S * sizeof(float), p, st);
     if (s != DDPPO_OK) return s;
@@ -1101,7 +1103,9 @@ ddppo_status gps_fwd_loss(ddppo_ctx* ctx, const ModelLayout& L, const float* par
   l.stats = stats;
   l.err = ctx->d_err;
   const int S = b.B * b.T_run;
-  ProfScope ps(ctx, DDPPO_K_NET_FWD, st, 1);
+  ProfScope ps(ctx, DDPPO_K_NET_FWD, st, 0);
+  ProfScope pr(ctx, DDPPO_K_RNN, st, 1);
+  if (ctx->prof) ctx->flops[DDPPO_K_RNN] += 2.0 * S * kG * (kH + kIn);
   return launch_cluster(ctx, gps_gru_fwd_kernel, kFwdThreads, sizeof(FwdSmem) + (size_t)S * sizeof(float), p, st);
 }
 
@@ -1127,7 +1131,9 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   }
   {
-    ProfScope ps(ctx, DDPPO_K_NET_BWD, st, 1);
+    ProfScope ps(ctx, DDPPO_K_NET_BWD, st, 0);
+    ProfScope pr(ctx, DDPPO_K_RNN, st, 1);
+    if (ctx->prof) ctx->flops[DDPPO_K_RNN] += 2.0 * S * kG * kH;
     s = launch_cluster(ctx, gps_gru_bwd_kernel, kBwdThreads, sizeof(BwdSmem) + (size_t)S * sizeof(float), p, st);
     if (s != DDPPO_OK) return s;
   }

@@ -106,6 +106,7 @@ struct TcArgs {
   int n_k, kper;          // k-iterations (FPROP/DGRAD: taps x channel slices; WGRAD: pixel chunks), per split
   int tiles_m, tiles_n, n_work;
   int Ho, Wo, s, p, k;    // im2col traversal geometry (output pixel grid of the box walk)
+  int F;                  // frames (WGRAD: the reduction runs over F * Ho * Wo pixels)
   int C, nsl;             // channels of the im2col'd tensor, C / CS
   int flip;               // DGRAD: tap (u, v) reads offset (k-1-u, k-1-v)
   float* out;             // result: [M][ldc] rows (FPROP / DGRAD), or the weight gradient (wg)
@@ -464,8 +465,10 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min
   a.n_work = tiles * splits;
   DDPPO_REQUIRE(ctx, splits == 1 || (2 * tiles <= kMaxTileCounters / 2 && a.part), "tconv: split-K needs scratch");
   const int grid = std::max(1, std::min(a.n_work, cap));
+  ProfScope ps(ctx, DDPPO_K_CONV, st, 1);
+  if (ctx->prof) ctx->flops[DDPPO_K_CONV] += 2.0 * a.M * a.N * (MODE == TC_FWD ? (double)a.k * a.k * a.C
+                                                                             : (double)a.Ho * a.Wo * a.F);
   kern<<<grid, kThreadsTC, Cfg::kSmem, st>>>(maps[0], maps[1], maps[2], maps[3], a);
-  ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
@@ -552,6 +555,7 @@ ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, i
   a.C = C;
   a.nsl = C / cs;
   const int pix = F * Ho * Wo;
+  a.F = F;
   a.n_k = (pix + kPix - 1) / kPix;
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (N + bn - 1) / bn;

@@ -272,3 +272,111 @@ def test_rgbd_model_finite_differences():
             fm[o + i] -= 1e-7
             fd = (loss(fp)[0] - loss(fm)[0]) / 2e-7
             assert abs(fd - g[o + i]) < 1e-4 * max(abs(fd), 1e-3), (name, i, fd, g[o + i])
+
+
+# ---------------------------------------------------------------- SE-ResNeXt50/2 (NEXT-3, reading R9)
+@pytest.mark.parametrize("C,O,groups,s", [(8, 8, 4, 1), (16, 32, 16, 2), (6, 9, 3, 1)])
+def test_grouped_conv_matches_torch(C, O, groups, s):
+    rng = np.random.default_rng(C + O)
+    x = rng.normal(size=(2, C, 7, 7))
+    W = rng.normal(size=(O, C // groups, 3, 3))
+    y, cache = convnets.conv_fwd_grouped(x, W, s, 1, groups)
+    xt, Wt = _t(x, True), _t(W, True)
+    yt = F.conv2d(xt, Wt, stride=s, padding=1, groups=groups)
+    assert np.max(np.abs(y - yt.detach().numpy())) < 1e-12
+    dy = rng.normal(size=y.shape)
+    (yt * _t(dy)).sum().backward()
+    dx, dW = convnets.conv_bwd_grouped(dy, W, s, 1, cache)
+    assert np.max(np.abs(dx - xt.grad.numpy())) < 1e-12 and np.max(np.abs(dW - Wt.grad.numpy())) < 1e-12
+    # groups == 1 is the dense convolution
+    yd, _ = convnets.conv_fwd_grouped(x, rng.normal(size=(O, C, 3, 3)), s, 1, 1)
+    assert yd.shape[1] == O
+
+
+def test_squeeze_excite_matches_torch():
+    rng = np.random.default_rng(3)
+    N, C, R = 3, 32, 4
+    x = rng.normal(size=(N, C, 5, 6))
+    W1, b1 = rng.normal(size=(R, C)) * 0.3, rng.normal(size=R) * 0.1
+    W2, b2 = rng.normal(size=(C, R)) * 0.3, rng.normal(size=C) * 0.1
+    y, cache = convnets.se_fwd(x, W1, b1, W2, b2)
+    ts = [_t(a, True) for a in (x, W1, b1, W2, b2)]
+    xt, W1t, b1t, W2t, b2t = ts
+    st = torch.sigmoid(F.linear(F.relu(F.linear(xt.mean(dim=(2, 3)), W1t, b1t)), W2t, b2t))
+    yt = xt * st[:, :, None, None]
+    assert np.max(np.abs(y - yt.detach().numpy())) < 1e-14
+    dy = rng.normal(size=y.shape)
+    (yt * _t(dy)).sum().backward()
+    got = convnets.se_bwd(dy, W1, W2, cache)
+    for mine, ref in zip(got, ts):
+        assert np.max(np.abs(mine - ref.grad.numpy())) < 1e-12
+    # zero FC weights and biases: s = sigmoid(0) = 1/2 exactly (a pure channel halving)
+    y0, _ = convnets.se_fwd(x, 0 * W1, 0 * b1, 0 * W2, 0 * b2)
+    assert np.array_equal(y0, x * 0.5)
+
+
+class _TorchSERX50H(torch.nn.Module):
+    """Independent torch construction of the SE-ResNeXt50/2 RGB-D encoder (R9)."""
+
+    def __init__(self, p):
+        super().__init__()
+        self.p = p
+
+    def forward(self, x):
+        p = self.p
+        mean = torch.tensor([0.485, 0.456, 0.406, 0.0], dtype=torch.float64).view(1, 4, 1, 1) * 255.0
+        std = torch.tensor([0.229, 0.224, 0.225, 1.0 / 255.0], dtype=torch.float64).view(1, 4, 1, 1) * 255.0
+        z = F.avg_pool2d((x - mean) / std, 2)
+
+        def cg(z, c, g, s, pad, relu, groups=1):
+            z = F.conv2d(z, p[c + ".weight"], stride=s, padding=pad, groups=groups)
+            z = F.group_norm(z, 16, p[g + ".weight"], p[g + ".bias"], eps=1e-5)
+            return F.relu(z) if relu else z
+        z = F.max_pool2d(cg(z, "enc.stem.conv", "enc.stem.gn", 2, 3, True), 3, 2, 1)
+        cin = 32
+        for li, (w, nb) in enumerate(zip(convnets.WIDTHS, convnets.R50_BLOCKS)):
+            for bi in range(nb):
+                s = 2 if (bi == 0 and li > 0) else 1
+                pre = f"enc.layer{li + 1}.{bi}"
+                a = cg(z, pre + ".conv1", pre + ".gn1", 1, 0, True)
+                b = cg(a, pre + ".conv2", pre + ".gn2", s, 1, True, groups=16)
+                c3 = cg(b, pre + ".conv3", pre + ".gn3", 1, 0, False)
+                sq = torch.sigmoid(F.linear(F.relu(F.linear(c3.mean(dim=(2, 3)), p[pre + ".se.fc1.weight"],
+                                                            p[pre + ".se.fc1.bias"])),
+                                            p[pre + ".se.fc2.weight"], p[pre + ".se.fc2.bias"]))
+                sc = cg(z, pre + ".down.conv", pre + ".down.gn", s, 0, False) if (s != 1 or cin != 4 * w) else z
+                z = F.relu(c3 * sq[:, :, None, None] + sc)
+                cin = 4 * w
+        return cg(z, "enc.compress.conv", "enc.compress.gn", 1, 1, True)
+
+
+def test_serx50h_matches_torch():
+    lay = models.layout("serx50")
+    offs, P = models.offsets("serx50")
+    ent = [(offs[n][0], int(np.prod(s)), f) for n, s, f in lay]
+    flat = synth.init_params(ent, P, 15).astype(np.float64)
+    rng = np.random.default_rng(16)
+    flat += rng.normal(0, 0.05, P)
+    p = models.unpack("serx50", flat)
+    x = synth.rgbd_frames(rng, 1, 2, H=64, W=64)[0].astype(np.float64)
+    feat, caches = convnets.serx50h_fwd(x, p)
+    pt = {k: _t(v, True) for k, v in p.items() if k.startswith("enc.")}
+    xt = _t(x, True)
+    ft = _TorchSERX50H(pt)(xt)
+    assert feat.shape == tuple(ft.shape) == (2, 128, 1, 1)
+    assert np.max(np.abs(feat - ft.detach().numpy())) < 1e-10
+    dz = rng.normal(size=feat.shape)
+    (ft * _t(dz)).sum().backward()
+    g = {}
+    dx = convnets.serx50h_bwd(dz, p, caches, g)
+    assert np.max(np.abs(dx - xt.grad.numpy())) < 1e-9 * max(1.0, np.abs(xt.grad.numpy()).max())
+    for k, v in pt.items():
+        assert np.max(np.abs(g[k] - v.grad.numpy())) < 1e-9 * max(1.0, np.abs(v.grad.numpy()).max()), k
+
+
+def test_serx50_layout():
+    offs, P = models.offsets("serx50")
+    assert offs["enc.layer1.0.conv2.weight"][1] == (64, 4, 3, 3)      # 16 groups of 4 channels
+    assert offs["enc.layer4.2.conv2.weight"][1] == (512, 32, 3, 3)
+    assert offs["enc.layer4.2.se.fc1.weight"][1] == (64, 1024) and offs["enc.layer1.0.se.fc2.bias"][1] == (128,)
+    assert P == 13321789
