@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="depth", choices=["gps", "toy", "stress_gps", "depth", "rgbd", "stress"])
+    ap.add_argument("--config", default="depth", choices=["gps", "toy", "stress_gps", "depth", "rgbd", "stress", "serx50"])
     ap.add_argument("--seed", type=int, default=1337)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -130,7 +130,7 @@ def blas_threads():
 
 # The oracle's fp64 NumPy ResNet needs ~0.2 s per frame-step of the Depth agent: its bounded sample
 # keeps the configuration but shortens the rollouts (whole learner steps on E x ORACLE_T[cfg]).
-ORACLE_T = {"depth": 32, "stress": 8, "rgbd": 2}
+ORACLE_T = {"depth": 32, "stress": 8, "rgbd": 2, "serx50": 1}
 
 
 def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None, T=None):
@@ -202,10 +202,12 @@ def run_reference(args, rank, world):
 
 
 def workload_name(cfgname, c):
-    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2, "rgbd": 3, "stress": 4}[cfgname]
+    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2, "rgbd": 3, "stress": 4, "serx50": 3}[cfgname]
     net = {"toy": "goal MLP(64, tanh) -> heads",
            "gps": "goal FC + action embedding -> GRU-512 -> heads",
            "depth": "64x64 depth -> ResNet18/2 + GroupNorm -> FC 512; goal FC + action embedding -> LSTM-512 -> heads",
+           "serx50": "256x256 RGB-D -> avg-pool -> SE-ResNeXt50/2 (NEXT-3) + GroupNorm -> FC 2048->512; goal FC + "
+                     "action embedding -> 2-layer LSTM-512 -> heads",
            "rgbd": "256x256 RGB-D -> avg-pool -> ResNet50/2 + GroupNorm -> FC 2048->512; goal FC + action embedding "
                    "-> 2-layer LSTM-512 -> heads"}[c["arch"]]
     return (f"configs[{idx}] {cfgname}: {c['E']} envs/GPU x {c['T']} steps, {net}, "
@@ -392,7 +394,7 @@ def main():
     fam_ms = {k: v[0] for k, v in prof.items()}
     # the dominant kernel: the TMA implicit-GEMM convolution for the visual agents, the GRU
     # recurrence for GPS (sub-families "conv" / "rnn": CUDA events around each launch on its stream)
-    dom = "conv" if c["arch"] in ("depth", "rgbd") else "rnn" if c["arch"] == "gps" else "net_fwd"
+    dom = "conv" if c["arch"] in ("depth", "rgbd", "serx50") else "rnn" if c["arch"] == "gps" else "net_fwd"
     launches = {k: v[1] for k, v in launches_timed.items()}
     roofline = roofline_for(dom, prof, c, lrn, peaks, prof_steps)
     kernels = kernel_table(prof, c, lrn, peaks, prof_steps)

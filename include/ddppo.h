@@ -116,7 +116,11 @@ ddppo_status ddppo_adv_norm(ddppo_ctx* ctx, double* stats3, float eps, float* me
  * head rows 0..A-1 are the action logits, row A the value.  num_actions must be 4;
  * GPS requires hidden == 512. */
 typedef enum {
-  DDPPO_ARCH_TOY_MLP = 0, DDPPO_ARCH_GPS_GRU = 1, DDPPO_ARCH_DEPTH_R18_LSTM = 2, DDPPO_ARCH_RGBD_R50_LSTM2 = 3
+  DDPPO_ARCH_TOY_MLP = 0, DDPPO_ARCH_GPS_GRU = 1, DDPPO_ARCH_DEPTH_R18_LSTM = 2, DDPPO_ARCH_RGBD_R50_LSTM2 = 3,
+  /* NEXT-3: the RGB-D agent with the half-width SE-ResNeXt50 encoder --
+   * ResNet50/2's topology, each bottleneck's 3x3 conv grouped (cardinality 16, inner width 2 x planes)
+   * and a squeeze-excitation module (reduction 16) before the residual addition (reading R9) */
+  DDPPO_ARCH_RGBD_SERX50_LSTM2 = 4
 } ddppo_arch;
 
 typedef struct {

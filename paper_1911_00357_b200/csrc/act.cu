@@ -117,7 +117,7 @@ extern "C" ddppo_status ddppo_policy_act(ddppo_ctx* ctx, const ddppo_model_desc*
   DDPPO_REQUIRE(ctx, a->E >= 1 && a->T >= 1 && a->t >= 0 && a->t < a->T && a->ld >= a->T + 1, "act: bad geometry");
   DDPPO_REQUIRE(ctx, a->goal && a->prev_action && a->mask && a->h_in && a->h_out, "act: null input");
   const int arch = host_desc->arch;
-  const bool visual = arch == DDPPO_ARCH_DEPTH_R18_LSTM || arch == DDPPO_ARCH_RGBD_R50_LSTM2;
+  const bool visual = arch_visual(arch);
   DDPPO_REQUIRE(ctx, arch != DDPPO_ARCH_TOY_MLP, "act: the toy MLP has no recurrent policy (use ddppo_policy_fwd)");
   DDPPO_REQUIRE(ctx, !visual || (a->obs && a->c_in && a->c_out), "act: the visual agents need obs and c_in / c_out");
   const size_t need = carve_act(host_desc, a->E, nullptr, nullptr);
@@ -125,11 +125,11 @@ extern "C" ddppo_status ddppo_policy_act(ddppo_ctx* ctx, const ddppo_model_desc*
   ActWs w;
   carve_act(host_desc, a->E, ws, &w);
   cudaStream_t st = as_stream(stream);
-  const int A = host_desc->num_actions, layers = arch == DDPPO_ARCH_RGBD_R50_LSTM2 ? 2 : 1;
+  const int A = host_desc->num_actions, layers = arch_rgbd(arch) ? 2 : 1;
   const int H = host_desc->hidden, sld = layers * H;
   iota_kernel<<<1, 256, 0, st>>>(w.env_idx, a->E, w.len);
   ctx->count(1);
-  const int64_t HW = arch == DDPPO_ARCH_RGBD_R50_LSTM2 ? 256 * 256 : 64 * 64;
+  const int64_t HW = arch_rgbd(arch) ? 256 * 256 : 64 * 64;
   for (int e0 = 0; e0 < a->E; e0 += kGroup) {
     const int B = std::min(kGroup, a->E - e0);
     ddppo_batch b = {};

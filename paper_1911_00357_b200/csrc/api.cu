@@ -205,7 +205,7 @@ ddppo_status ddppo_policy_fwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
   if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
     return toy_fwd(ctx, L, params, *host_batch, logits, values, ws, as_stream(stream));
   DDPPO_REQUIRE(ctx, host_batch->prev_action && host_batch->mask && host_batch->h0, "gps batch: null pointer");
-  if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2) {
+  if (arch_visual(host_desc->arch)) {
     DDPPO_REQUIRE(ctx, host_batch->obs && host_batch->c0, "visual agent batch: obs and c0 required");
     return depth_fwd(ctx, L, params, *host_batch, logits, values, ws, as_stream(stream));
   }
@@ -225,7 +225,7 @@ ddppo_status ddppo_policy_bwd(ddppo_ctx* ctx, const ddppo_model_desc* host_desc,
   DDPPO_REQUIRE(ctx, ws && ws_bytes >= need, "workspace too small");
   if (host_desc->arch == DDPPO_ARCH_TOY_MLP)
     return toy_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
-  if (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2)
+  if (arch_visual(host_desc->arch))
     return depth_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
   DDPPO_REQUIRE(ctx, host_batch->dgoal == nullptr, "policy_bwd: dgoal is produced by the visual agents only");
   return gps_bwd(ctx, L, params, *host_batch, dlogits, dvalues, grad, ws, as_stream(stream));
@@ -489,7 +489,7 @@ ddppo_status learner_body(ddppo_ctx* ctx, const ModelLayout& L, const ddppo_mode
                           const ddppo_rollout* ro, const ddppo_learner_cfg* cfg, float* params, float* m, float* v,
                           float* adv, float* ret, float* stats_out, void* ws, LearnerWs& w, cudaStream_t st,
                           const std::vector<MbShape>& mbs, bool use_peers, uint64_t peer_mb0) {
-  const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
+  const bool visual = arch_visual(host_desc->arch);
   // a2 GAE (+ local adv stats), a3 global normalisation statistics
   ddppo_status s = launch_gae(ctx, ro->rew, ro->val, ro->done, ro->len, ro->E, ro->T, ro->ld, cfg->gamma, cfg->tau,
                               adv, ret, w.stats3, st);
@@ -644,9 +644,9 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
                 "learner_step: freeze_mask must be 4-byte aligned");
   DDPPO_REQUIRE(ctx, (cfg->normalize_adv != 0) == (cfg->loss.normalize_adv != 0),
                 "learner_step: normalize_adv and loss.normalize_adv must agree");
-  const bool visual = host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
+  const bool visual = arch_visual(host_desc->arch);
   DDPPO_REQUIRE(ctx, !visual || (ro->obs && ro->c0), "learner_step: the visual agents need obs and c0");
-  DDPPO_REQUIRE(ctx, host_desc->arch != DDPPO_ARCH_RGBD_R50_LSTM2 || ro->obs_rgb, "learner_step: RGB-D needs obs_rgb");
+  DDPPO_REQUIRE(ctx, !arch_rgbd(host_desc->arch) || ro->obs_rgb, "learner_step: RGB-D needs obs_rgb");
   size_t need = 0;
   ddppo_status s =
       ddppo_learner_workspace_size(host_desc, ro->E, ro->T, ro->ld, cfg->minibatches, cfg->epochs, &need);

@@ -305,7 +305,7 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
                               int* splits_out, cudaStream_t st);
 ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, int H, int W, int C, int k, int s,
                                 int p, const __nv_bfloat16* dy, int N, float* dw, int Cr, float* partial, int max_splits,
-                                int slot, int* splits_out, cudaStream_t st);
+                                int slot, int* splits_out, cudaStream_t st, int groups = 1);
 
 // NVLink peer memory (peer.cu)
 ddppo_status peer_exchange(ddppo_ctx* ctx, void* local, void** out);
@@ -343,7 +343,7 @@ ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st);
 struct ModelLayout {
   int64_t P = 0;
   int n = 0;
-  ddppo_tensor_info t[192];
+  ddppo_tensor_info t[320];
 };
 ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out);
 int64_t layout_offset(const ModelLayout& L, const char* name);
@@ -405,3 +405,9 @@ ddppo_status gps_fwd_loss(ddppo_ctx* ctx, const ModelLayout& L, const float* par
                           float* dlogits, float* dvalues, float* stats, void* ws, cudaStream_t st);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+// the visual agents (a ResNet encoder over frames + LSTM policy) / those with RGB-D 256^2 input and a
+// 2-layer LSTM
+inline bool arch_visual(int a) {
+  return a == DDPPO_ARCH_DEPTH_R18_LSTM || a == DDPPO_ARCH_RGBD_R50_LSTM2 || a == DDPPO_ARCH_RGBD_SERX50_LSTM2;
+}
+inline bool arch_rgbd(int a) { return a == DDPPO_ARCH_RGBD_R50_LSTM2 || a == DDPPO_ARCH_RGBD_SERX50_LSTM2; }

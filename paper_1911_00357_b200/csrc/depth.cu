@@ -136,6 +136,7 @@ struct WeightPrep {
     __nv_bfloat16 *wr, *wd;  // wd nullable (no input gradient)
     int Co, Ci, Cp, k;
     int wd_planes;           // 2: Wd also as a lo plane (at wd + Co*Cp*k*k), for hi / lo input gradients
+    int groups;              // > 1: W is grouped [Co][Ci/groups][k][k]; the dense operand is block diagonal
   } it[kMaxConvs];
 };
 __global__ void weights_prep_kernel(const WeightPrep prep) {
@@ -151,7 +152,13 @@ __global__ void weights_prep_kernel(const WeightPrep prep) {
   const int Co = t.Co, Ci = t.Ci, Cp = t.Cp, kk = t.k * t.k, n = Co * Cp * kk;
   const int j = g - prep.off[lo];  // Wr index
   const int o = j / (kk * Cp), rem = j - o * (kk * Cp), uv = rem / Cp, c = rem - uv * Cp;
-  const float w = c < Ci ? t.W[(o * Ci + c) * kk + uv] : 0.f;
+  float w = 0.f;
+  if (t.groups > 1) {
+    const int cgi = Ci / t.groups, cgo = Co / t.groups;
+    if (c / cgi == o / cgo) w = t.W[(o * cgi + c % cgi) * kk + uv];
+  } else if (c < Ci) {
+    w = t.W[(o * Ci + c) * kk + uv];
+  }
   const __nv_bfloat16 hi = __float2bfloat16_rn(w);
   t.wr[j] = hi;
   t.wr[n + j] = __float2bfloat16_rn(w - __bfloat162float(hi));
@@ -1019,6 +1026,130 @@ __global__ void relu_mask_kernel(const float* __restrict__ dz, const float* __re
 }
 
 
+// ------------------------------------------------------------------ squeeze-excitation (SE-ResNeXt, R9)
+// One block per frame.  z3 = GN3 output [F][HW][C] (NHWC), sc = shortcut; out = relu(z3 * s + sc) and
+// its bf16 hi / lo planes (plane = F*HW*C); s = sigmoid(W2 relu(W1 pool + b1) + b2), pool = mean_hw z3.
+// Sums in fixed order (thread per channel over pixels; warp per fc1 unit over channels).
+__global__ void __launch_bounds__(256) se_fwd_kernel(const float* __restrict__ z3, const float* __restrict__ sc,
+                                                     const float* __restrict__ W1, const float* __restrict__ b1,
+                                                     const float* __restrict__ W2, const float* __restrict__ b2, int HW,
+                                                     int C, int R, float* __restrict__ out,
+                                                     __nv_bfloat16* __restrict__ outb, size_t plane,
+                                                     float* __restrict__ s_out, float* __restrict__ pool_out,
+                                                     float* __restrict__ a1_out) {
+  extern __shared__ float sm[];  // pool[C], s[C], a1[R]
+  float *pool = sm, *sv = sm + C, *a1 = sm + 2 * C;
+  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t base = (size_t)f * HW * C;
+  for (int c = tid; c < C; c += blockDim.x) {
+    float acc = 0.f;
+    for (int q = 0; q < HW; ++q) acc += z3[base + (size_t)q * C + c];
+    pool[c] = acc / (float)HW;
+    pool_out[(size_t)f * C + c] = pool[c];
+  }
+  __syncthreads();
+  for (int j = warp; j < R; j += blockDim.x / 32) {
+    float acc = 0.f;
+    for (int c = lane; c < C; c += 32) acc += W1[(size_t)j * C + c] * pool[c];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      a1[j] = acc + b1[j];
+      a1_out[(size_t)f * R + j] = a1[j];
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < C; c += blockDim.x) {
+    float t = b2[c];
+    for (int j = 0; j < R; ++j) t += W2[(size_t)c * R + j] * fmaxf(a1[j], 0.f);
+    sv[c] = 1.f / (1.f + expf(-t));
+    s_out[(size_t)f * C + c] = sv[c];
+  }
+  __syncthreads();
+  for (size_t i = tid; i < (size_t)HW * C; i += blockDim.x) {
+    const int c = (int)(i & (size_t)(C - 1));
+    const float v = fmaxf(z3[base + i] * sv[c] + sc[base + i], 0.f);
+    out[base + i] = v;
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    outb[base + i] = h;
+    outb[plane + base + i] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
+// d = dz * [out > 0] (the block output's ReLU); ds = sum_hw d z3; da2 = ds s (1 - s); da1 = (W2^T da2) [a1 > 0];
+// dz3 = d s + (W1^T da1) / HW.  Per-frame da1 / da2 feed se_param_grad_kernel.
+__global__ void __launch_bounds__(256) se_bwd_kernel(const float* __restrict__ dz, const float* __restrict__ out,
+                                                     const float* __restrict__ z3, const float* __restrict__ s_in,
+                                                     const float* __restrict__ a1_in, const float* __restrict__ W1,
+                                                     const float* __restrict__ W2, int HW, int C, int R,
+                                                     float* __restrict__ dz3, float* __restrict__ da1_out,
+                                                     float* __restrict__ da2_out) {
+  extern __shared__ float sm[];  // da2[C], dpool[C], da1[R]
+  float *da2 = sm, *dpool = sm + C, *da1 = sm + 2 * C;
+  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t base = (size_t)f * HW * C;
+  for (int c = tid; c < C; c += blockDim.x) {
+    float acc = 0.f;
+    for (int q = 0; q < HW; ++q) {
+      const size_t i = base + (size_t)q * C + c;
+      if (out[i] > 0.f) acc += dz[i] * z3[i];
+    }
+    const float sv = s_in[(size_t)f * C + c];
+    da2[c] = acc * sv * (1.f - sv);
+    da2_out[(size_t)f * C + c] = da2[c];
+  }
+  __syncthreads();
+  for (int j = warp; j < R; j += blockDim.x / 32) {
+    float acc = 0.f;
+    for (int c = lane; c < C; c += 32) acc += W2[(size_t)c * R + j] * da2[c];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      da1[j] = a1_in[(size_t)f * R + j] > 0.f ? acc : 0.f;
+      da1_out[(size_t)f * R + j] = da1[j];
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < C; c += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < R; ++j) acc += W1[(size_t)j * C + c] * da1[j];
+    dpool[c] = acc / (float)HW;
+  }
+  __syncthreads();
+  for (size_t i = tid; i < (size_t)HW * C; i += blockDim.x) {
+    const int c = (int)(i & (size_t)(C - 1));
+    const float d = out[base + i] > 0.f ? dz[base + i] : 0.f;
+    dz3[base + i] = d * s_in[(size_t)f * C + c] + dpool[c];
+  }
+}
+
+// dW1[j][c] = sum_f da1[f][j] pool[f][c]; db1[j] = sum_f da1[f][j]; dW2[c][j] = sum_f da2[f][c] relu(a1[f][j]);
+// db2[c] = sum_f da2[f][c]  (one thread per output, frames in order)
+__global__ void se_param_grad_kernel(const float* __restrict__ da1, const float* __restrict__ da2,
+                                     const float* __restrict__ pool, const float* __restrict__ a1, int F, int C, int R,
+                                     float* __restrict__ dW1, float* __restrict__ db1, float* __restrict__ dW2,
+                                     float* __restrict__ db2) {
+  const int n1 = R * C, n = 2 * R * C + R + C;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    if (i < n1) {
+      const int j = i / C, c = i - j * C;
+      for (int f = 0; f < F; ++f) acc += da1[(size_t)f * R + j] * pool[(size_t)f * C + c];
+      dW1[i] = acc;
+    } else if (i < 2 * n1) {
+      const int k = i - n1, c = k / R, j = k - c * R;
+      for (int f = 0; f < F; ++f) acc += da2[(size_t)f * C + c] * fmaxf(a1[(size_t)f * R + j], 0.f);
+      dW2[k] = acc;
+    } else if (i < 2 * n1 + R) {
+      const int j = i - 2 * n1;
+      for (int f = 0; f < F; ++f) acc += da1[(size_t)f * R + j];
+      db1[j] = acc;
+    } else {
+      const int c = i - 2 * n1 - R;
+      for (int f = 0; f < F; ++f) acc += da2[(size_t)f * C + c];
+      db2[c] = acc;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ network plan
 struct ConvGN {
   int Ci, Co, k, s, p, H, W, Ho, Wo;  // GEMM geometry: input H x W x Ci (Ci padded to 8 for the RGB-D stem)
@@ -1031,6 +1162,8 @@ struct ConvGN {
   __nv_bfloat16 *wr_b, *wd_b;         // this minibatch's weights as GEMM operands (Wr planes, Wd)
   __nv_bfloat16* dyb;                 // GN-backward output (gradient wrt y, bf16): read by dgrad and, on the
                                       // side stream, by wgrad -- one buffer per layer
+  int groups = 1;                     // grouped convolution (SE-ResNeXt's 3x3): computed as the dense
+                                      // convolution with block-diagonal weights (R9)
 };
 
 struct Plan {
@@ -1041,6 +1174,13 @@ struct Plan {
     std::vector<int> main;   // convs of the residual branch (ReLU after all but the last)
     int down;                // shortcut conv (-1: identity)
     float *in, *out;         // block input, block output (after residual + ReLU)
+    // squeeze-excitation (SE-ResNeXt, R9): out = relu(z3 * s + shortcut), s = sigmoid(W2 relu(W1 pool(z3)
+    // + b1) + b2); per-frame s, pooled z3, fc1 pre-activations and the backward's per-frame fc gradients
+    bool se = false;
+    __nv_bfloat16* outb = nullptr;  // out as bf16 hi / lo planes (the next convolution's operand)
+    float *se_s = nullptr, *se_pool = nullptr, *se_a1 = nullptr, *se_da1 = nullptr, *se_da2 = nullptr;
+    int64_t se_w1 = 0, se_b1 = 0, se_w2 = 0, se_b2 = 0;
+    int C = 0, R = 0, HW = 0;
   };
   std::vector<Block> blocks;
   float *x0, *pool_out;
@@ -1053,7 +1193,7 @@ struct Plan {
   } rnn[2];
   // scratch (reused by every layer)
   __nv_bfloat16* dyb;         // GN-backward output (bf16)
-  float *dwt, *part, *gn_part, *dz_a, *dz_b, *dz_c, *dxin, *dflat, *dvis;
+  float *dwt, *part, *gn_part, *dz_a, *dz_b, *dz_c, *dz_se, *dxin, *dflat, *dvis;
   size_t part_n = 0;
   float *part_w = nullptr, *part2 = nullptr;  // side-stream partials (weight gradients)
   size_t part_w_n = 0;
@@ -1075,6 +1215,7 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   P.F = F;
   P.rgbd = rgbd;
   P.layers = rgbd ? 2 : 1;
+  const bool serx = layout_offset(L, "enc.layer1.0.se.fc1.weight") >= 0;  // SE-ResNeXt50/2 (R9)
   P.fc_in = rgbd ? 2048 : 512;
   // ResNet50/2 is ~50 layers deep: its input-gradient GEMMs take hi / lo operand planes so that the
   // bf16 rounding does not accumulate along the chain (the earliest layers' gradients stay within
@@ -1091,8 +1232,9 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   auto take_b = [&](size_t n) { return reinterpret_cast<__nv_bfloat16*>(take_bytes(n * sizeof(__nv_bfloat16))); };
   size_t max_act = 0, max_w = 0, max_gn_rows = 0, max_gn_part = 0;
   auto add_conv = [&](const std::string& cname, const std::string& gname, int Ci, int Ci_real, int Co, int k, int s,
-                      int p, int H, float* x, __nv_bfloat16* xb, bool planes_out, bool needs_dx) {
+                      int p, int H, float* x, __nv_bfloat16* xb, bool planes_out, bool needs_dx, int groups = 1) {
     ConvGN c;
+    c.groups = groups;
     c.Ci = Ci;
     c.Ci_real = Ci_real;
     c.Co = Co;
@@ -1162,23 +1304,45 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
         const int c2 = add_conv(pre + ".conv2", pre + ".gn2", w, w, w, 3, 1, 1, Ho, P.convs[c1].z, P.convs[c1].zb,
                                 true, true);
         blk.main = {c1, c2};
-      } else {  // Bottleneck: 1x1 -> 3x3 (stride) -> 1x1 (x4)
-        const int c1 = add_conv(pre + ".conv1", pre + ".gn1", cin, cin, w, 1, 1, 0, H, z, zb, true, true);
-        const int c2 = add_conv(pre + ".conv2", pre + ".gn2", w, w, w, 3, s, 1, H, P.convs[c1].z, P.convs[c1].zb,
-                                true, true);
+      } else {  // Bottleneck: 1x1 -> 3x3 (stride) -> 1x1 (x4); SE-ResNeXt: inner width 2w, grouped 3x3, SE
+        const int wi = serx ? 2 * w : w;
+        const int c1 = add_conv(pre + ".conv1", pre + ".gn1", cin, cin, wi, 1, 1, 0, H, z, zb, true, true);
+        const int c2 = add_conv(pre + ".conv2", pre + ".gn2", wi, wi, wi, 3, s, 1, H, P.convs[c1].z, P.convs[c1].zb,
+                                true, true, serx ? 16 : 1);
         Ho = P.convs[c2].Ho;
-        const int c3 = add_conv(pre + ".conv3", pre + ".gn3", w, w, cout, 1, 1, 0, Ho, P.convs[c2].z,
-                                P.convs[c2].zb, true, true);
+        const int c3 = add_conv(pre + ".conv3", pre + ".gn3", wi, wi, cout, 1, 1, 0, Ho, P.convs[c2].z,
+                                P.convs[c2].zb, !serx, true);
         blk.main = {c1, c2, c3};
+        if (serx) {
+          const size_t act = (size_t)F * Ho * Ho * cout;
+          blk.se = true;
+          blk.C = cout;
+          blk.R = cout / 16;
+          blk.HW = Ho * Ho;
+          blk.out = take(act);
+          blk.outb = take_b(2 * act);
+          blk.se_s = take((size_t)F * cout);
+          blk.se_pool = take((size_t)F * cout);
+          blk.se_a1 = take((size_t)F * blk.R);
+          blk.se_da1 = take((size_t)F * blk.R);
+          blk.se_da2 = take((size_t)F * cout);
+          blk.se_w1 = off_of(L, pre + ".se.fc1.weight");
+          blk.se_b1 = off_of(L, pre + ".se.fc1.bias");
+          blk.se_w2 = off_of(L, pre + ".se.fc2.weight");
+          blk.se_b2 = off_of(L, pre + ".se.fc2.bias");
+        }
       }
       blk.down = (s != 1 || cin != cout)
                      ? add_conv(pre + ".down.conv", pre + ".down.gn", cin, cin, cout, 1, s, 0, H, z, zb, false, true)
                      : -1;
       const ConvGN& last = P.convs[blk.main.back()];
-      blk.out = last.z;  // the last main conv's GN output buffer holds relu(gn + shortcut)
+      if (!blk.se) {
+        blk.out = last.z;  // the last main conv's GN output buffer holds relu(gn + shortcut)
+        blk.outb = last.zb;
+      }
       P.blocks.push_back(blk);
       z = blk.out;
-      zb = last.zb;
+      zb = blk.outb;
       H = Ho;
       cin = cout;
     }
@@ -1212,6 +1376,7 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   P.dz_a = take(max_act);
   P.dz_b = take(max_act);
   P.dz_c = take(max_act);
+  P.dz_se = take(max_act);
   P.dxin = take((size_t)F * kXin);
   P.dflat = take((size_t)F * P.fc_in);
   P.dvis = take((size_t)F * 512);
@@ -1230,6 +1395,7 @@ constexpr int kPrecFwd = 3;
 struct ConvGeom {
   int F, H, W, Ci, Co, k, s, p, Ho, Wo;
   int Cr;  // channels of the parameter tensor (Ci may be padded)
+  int groups = 1;
   int K() const { return k * k * Ci; }
   int M() const { return F * Ho * Wo; }
 };
@@ -1334,8 +1500,9 @@ ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const
   if (ctx->conv_engine == DDPPO_CONV_TMA && g.Ci % 32 == 0) {
     int splits = 1;
     return launch_tconv_wgrad(ctx, xb, g.F, g.H, g.W, g.Ci, g.k, g.s, g.p, dy, g.Co, dw, g.Cr, sc.part,
-                              split_cap(sc, K, g.Co, kMaxSplits), sc.slot, &splits, st);
+                              split_cap(sc, K, g.Co, kMaxSplits), sc.slot, &splits, st, g.groups);
   } else {
+    DDPPO_REQUIRE(ctx, g.groups == 1, "conv: grouped convolutions need the TMA engine");
     // split the pixel range so that ~2 CTAs per SM stream (each >= 4 chunks of 64 pixels)
     const int bn = g.Co <= 32 ? 32 : g.Co <= 64 ? 64 : 128;
     const long long tiles = (long long)((g.Co + bn - 1) / bn) * ((K + 127) / 128);
@@ -1555,7 +1722,7 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
 }
 
 ConvGeom geom_of(const Plan& P, const ConvGN& c) {
-  return ConvGeom{P.F, c.H, c.W, c.Ci, c.Co, c.k, c.s, c.p, c.Ho, c.Wo, c.Ci_real};
+  return ConvGeom{P.F, c.H, c.W, c.Ci, c.Co, c.k, c.s, c.p, c.Ho, c.Wo, c.Ci_real, c.groups};
 }
 ConvScratch scratch_of(const Plan& P) { return ConvScratch{nullptr, nullptr, P.dwt, P.part, P.part_n}; }  // weights prepared
 
@@ -1653,7 +1820,7 @@ size_t depth_workspace(int arch, int max_B, int T) {
   ModelLayout L;
   build_layout(&d, &L);
   Plan P;
-  make_plan(L, arch == DDPPO_ARCH_RGBD_R50_LSTM2, max_B, T, nullptr, &P);
+  make_plan(L, arch_rgbd(arch), max_B, T, nullptr, &P);
   return P.bytes;
 }
 
@@ -1670,7 +1837,7 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
       const ConvGN& c = P.convs[i];
       if (c.Ci == 1) continue;  // the Depth stem runs SIMT on fp32 weights
       DDPPO_REQUIRE(ctx, prep.n < kMaxConvs, "too many convolutions for one weight-prep launch");
-      prep.it[prep.n] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k, P.grad_planes};
+      prep.it[prep.n] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k, P.grad_planes, c.groups};
       prep.off[prep.n + 1] = prep.off[prep.n] + c.Co * c.Ci * c.k * c.k;
       ++prep.n;
     }
@@ -1703,7 +1870,20 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
     }
     for (size_t j = 0; j < blk.main.size(); ++j) {
       const bool last = j + 1 == blk.main.size();
-      if ((s = conv_gn_fwd(ctx, prm, P, P.convs[blk.main[j]], last ? sc : nullptr, 1, st)) != DDPPO_OK) return s;
+      // SE blocks: the last GN output (z3) is excited before the residual addition + ReLU
+      const bool fuse_res = last && !blk.se;
+      if ((s = conv_gn_fwd(ctx, prm, P, P.convs[blk.main[j]], fuse_res ? sc : nullptr, last && blk.se ? 0 : 1, st)) !=
+          DDPPO_OK)
+        return s;
+    }
+    if (blk.se) {
+      const ConvGN& c3 = P.convs[blk.main.back()];
+      const size_t smem = (size_t)(2 * blk.C + blk.R) * sizeof(float);
+      se_fwd_kernel<<<F, 256, smem, st>>>(c3.z, sc, prm + blk.se_w1, prm + blk.se_b1, prm + blk.se_w2, prm + blk.se_b2,
+                                          blk.HW, blk.C, blk.R, blk.out, blk.outb, (size_t)F * blk.HW * blk.C,
+                                          blk.se_s, blk.se_pool, blk.se_a1);
+      ctx->count(1);
+      DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     }
   }
   ConvGN& comp = P.convs.back();
@@ -1841,22 +2021,43 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   for (int bi = (int)P.blocks.size() - 1; bi >= 0; --bi) {
     const Plan::Block& blk = P.blocks[bi];
     ConvGN& last = P.convs[blk.main.back()];
-    // out = relu(gn_last(conv_last(...)) + shortcut(in)); the ReLU mask of the sum is `out` (= last.z)
+    // out = relu(gn_last(conv_last(...)) (* SE) + shortcut(in)); the ReLU mask of the sum is `out`
     if (blk.down >= 0) {
-      if ((s = conv_gn_bwd(ctx, prm, grad, P, P.convs[blk.down], dz, last.z, dn, 0, st)) != DDPPO_OK) return s;
+      if ((s = conv_gn_bwd(ctx, prm, grad, P, P.convs[blk.down], dz, blk.out, dn, 0, st)) != DDPPO_OK) return s;
     } else {
       const size_t n = (size_t)F * last.Ho * last.Wo * last.Co;
-      relu_mask_kernel<<<blocks_for(ctx, n), kThreads, 0, st>>>(dz, last.z, n, dn);
+      relu_mask_kernel<<<blocks_for(ctx, n), kThreads, 0, st>>>(dz, blk.out, n, dn);
       ctx->count(1);
     }
-    // main branch, last conv first: its upstream mask is the block output, the others' their own ReLU
+    // main branch, last conv first: its upstream mask is the block output (or, after the SE module, none),
+    // the others' their own ReLU
     float* g_in = dz;    // gradient wrt the current conv's output
     float* g_out = da;   // gradient wrt its input
+    if (blk.se) {
+      const size_t smem = (size_t)(2 * blk.C + blk.R) * sizeof(float);
+      se_bwd_kernel<<<F, 256, smem, st>>>(dz, blk.out, last.z, blk.se_s, blk.se_a1, prm + blk.se_w1, prm + blk.se_w2,
+                                          blk.HW, blk.C, blk.R, P.dz_se, blk.se_da1, blk.se_da2);
+      ctx->count(1);
+      DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+      cudaStream_t pst = st;
+      if (P.side) {  // the SE parameters' gradient only feeds a8: side stream
+        DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, P.side));
+        pst = P.side;
+      }
+      const int n = 2 * blk.R * blk.C + blk.R + blk.C;
+      se_param_grad_kernel<<<blocks_for(ctx, (size_t)n), kThreads, 0, pst>>>(
+          blk.se_da1, blk.se_da2, blk.se_pool, blk.se_a1, F, blk.C, blk.R, grad + blk.se_w1, grad + blk.se_b1,
+          grad + blk.se_w2, grad + blk.se_b2);
+      ctx->count(1);
+      DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+      g_in = P.dz_se;
+    }
     for (int j = (int)blk.main.size() - 1; j >= 0; --j) {
       ConvGN& c = P.convs[blk.main[j]];
       const bool first = j == 0;
       float* target = first ? dn : g_out;
-      if ((s = conv_gn_bwd(ctx, prm, grad, P, c, g_in, c.z, target, first ? 1 : 0, st)) != DDPPO_OK) return s;
+      const float* relu_z = (j + 1 == (int)blk.main.size()) ? (blk.se ? nullptr : blk.out) : c.z;
+      if ((s = conv_gn_bwd(ctx, prm, grad, P, c, g_in, relu_z, target, first ? 1 : 0, st)) != DDPPO_OK) return s;
       if (!first) {
         std::swap(g_in, g_out);  // g_in <- this conv's input gradient; g_out <- a free buffer
         if (g_out == dn) g_out = (g_in == dz) ? da : dz;
@@ -2004,17 +2205,20 @@ extern "C" ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_
   if (!ctx || !host_batch || !host_desc) return DDPPO_ERR_CONFIG;
   ModelLayout L;
   DDPPO_REQUIRE(ctx, build_layout(host_desc, &L) == DDPPO_OK &&
-                         (host_desc->arch == DDPPO_ARCH_DEPTH_R18_LSTM || host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2),
+                         arch_visual(host_desc->arch),
                 "depth decisions: visual agents only");
   Plan P;
-  make_plan(L, host_desc->arch == DDPPO_ARCH_RGBD_R50_LSTM2, host_batch->B, host_batch->T_run, ws, &P);
+  make_plan(L, host_desc->arch != DDPPO_ARCH_DEPTH_R18_LSTM, host_batch->B, host_batch->T_run, ws, &P);
   const int F = P.F;
   std::vector<std::pair<const float*, size_t>> masks;  // (tensor, size); the pool argmax is copied after the first
   auto add = [&](const ConvGN& c) { masks.push_back({c.z, (size_t)F * c.Ho * c.Wo * c.Co}); };
   add(P.convs[0]);
   const size_t pool_n = (size_t)F * P.pool_hw * P.pool_hw * 32;
-  for (const auto& blk : P.blocks)
-    for (int j : blk.main) add(P.convs[j]);  // inner ReLUs, then the block output (last conv's z)
+  for (const auto& blk : P.blocks) {
+    for (size_t j = 0; j + 1 < blk.main.size(); ++j) add(P.convs[blk.main[j]]);  // the branch's inner ReLUs
+    const ConvGN& last = P.convs[blk.main.back()];
+    masks.push_back({blk.out, (size_t)F * last.Ho * last.Wo * last.Co});  // the block output's ReLU
+  }
   add(P.convs.back());
   masks.push_back({P.vis, (size_t)F * 512});
   int64_t total = (int64_t)pool_n;

@@ -116,6 +116,7 @@ struct TcArgs {
   float* part;
   int* cnt;               // per-tile arrival counters (zero; reset by the last arrival)
   int wg, Cr;             // WGRAD: write out[o][c < Cr][tap] (PyTorch order; rows are (tap, c < C))
+  int groups;             // WGRAD of a grouped conv: keep the block-diagonal entries, out[o][c % (C/g)][tap]
 };
 
 // first output pixel q -> im2col box coordinates (W, H, N) of its receptive field's corner
@@ -144,6 +145,13 @@ __device__ __forceinline__ void store_final(const TcArgs& a, int row, int col, c
   } else {
     const int kk = a.k * a.k, tap = row / a.C, c = row - tap * a.C;
     if (c >= a.Cr) return;
+    if (a.groups > 1) {
+      const int cgi = a.C / a.groups, cgo = a.N / a.groups;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (c / cgi == (col + e) / cgo) a.out[((long long)(col + e) * cgi + c % cgi) * kk + tap] = v[e];
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) a.out[((long long)(col + e) * a.Cr + c) * kk + tap] = v[e];
   }
@@ -537,7 +545,7 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
 // with partial tiles in `partial`, summed in split order by each tile's last split.
 ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, int H, int W, int C, int k, int s,
                                 int p, const __nv_bfloat16* dy, int N, float* dw, int Cr, float* partial, int max_splits,
-                                int slot, int* splits_out, cudaStream_t st) {
+                                int slot, int* splits_out, cudaStream_t st, int groups) {
   DDPPO_REQUIRE(ctx, C % 32 == 0 && N % 8 == 0, "tconv wgrad: C % 32 == 0, N % 8 == 0 required");
   DDPPO_REQUIRE(ctx, ((uintptr_t)x & 15) == 0 && ((uintptr_t)dy & 15) == 0 && ((uintptr_t)partial & 15) == 0,
                 "tconv wgrad: 16-byte aligned operands required");
@@ -564,6 +572,8 @@ ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, i
   a.cnt = ctx->d_tile_cnt + (size_t)slot * (kMaxTileCounters / 2);
   a.wg = 1;
   a.Cr = Cr;
+  a.groups = groups;
+  DDPPO_REQUIRE(ctx, groups >= 1 && C % groups == 0 && N % groups == 0, "tconv wgrad: bad group count");
   if (splits_out) *splits_out = 1;
   CUtensorMap maps[4];
   memset(maps, 0, sizeof(maps));

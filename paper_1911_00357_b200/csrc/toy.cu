@@ -48,9 +48,11 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
     add_tensor(&L, "rnn.bias_hh", 1, bg, (int)H);
     add_tensor(&L, "head.weight", 2, hw, (int)H);
     add_tensor(&L, "head.bias", 1, hb, (int)H);
-  } else if (d->arch == DDPPO_ARCH_DEPTH_R18_LSTM || d->arch == DDPPO_ARCH_RGBD_R50_LSTM2) {
+  } else if (d->arch == DDPPO_ARCH_DEPTH_R18_LSTM || d->arch == DDPPO_ARCH_RGBD_R50_LSTM2 ||
+             d->arch == DDPPO_ARCH_RGBD_SERX50_LSTM2) {
     if (d->hidden != 512) return DDPPO_ERR_CONFIG;
-    const bool rgbd = d->arch == DDPPO_ARCH_RGBD_R50_LSTM2;
+    const bool serx = d->arch == DDPPO_ARCH_RGBD_SERX50_LSTM2;
+    const bool rgbd = d->arch == DDPPO_ARCH_RGBD_R50_LSTM2 || serx;
     const int64_t H = d->hidden, G = 4 * H;
     char name[48];
     // conv weight [Co][Ci][k][k] (fan_in Ci*k*k), GroupNorm gamma (ones: fan_in 0) / beta (zeros: -1)
@@ -78,12 +80,26 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
           const int64_t w = widths[li];
           const bool down = (bi == 0 && li > 0) || cin != 4 * w;
           snprintf(pre, sizeof(pre), "enc.layer%d.%d", li + 1, bi);
-          const int64_t cis[3] = {cin, w, w}, cos_[3] = {w, w, 4 * w}, ks[3] = {1, 3, 1};
+          // SE-ResNeXt (R9): inner width 2w, the 3x3 grouped (16 groups: weight [2w][2w/16][3][3])
+          const int64_t wi = serx ? 2 * w : w, gi = serx ? wi / 16 : wi;
+          const int64_t cis[3] = {cin, gi, wi}, cos_[3] = {wi, wi, 4 * w}, ks[3] = {1, 3, 1};
           for (int j = 0; j < 3; ++j) {
             snprintf(sub, sizeof(sub), "%s.conv%d", pre, j + 1);
             conv(sub, cos_[j], cis[j], ks[j]);
             snprintf(sub, sizeof(sub), "%s.gn%d", pre, j + 1);
             gn(sub, cos_[j]);
+          }
+          if (serx) {  // squeeze-excitation: fc1 [4w/16][4w], fc2 [4w][4w/16] with biases (default init)
+            const int64_t co = 4 * w, r = co / 16;
+            int64_t w1[2] = {r, co}, b1[1] = {r}, w2[2] = {co, r}, b2[1] = {co};
+            snprintf(sub, sizeof(sub), "%s.se.fc1.weight", pre);
+            add_tensor(&L, sub, 2, w1, (int)co);
+            snprintf(sub, sizeof(sub), "%s.se.fc1.bias", pre);
+            add_tensor(&L, sub, 1, b1, (int)co);
+            snprintf(sub, sizeof(sub), "%s.se.fc2.weight", pre);
+            add_tensor(&L, sub, 2, w2, (int)r);
+            snprintf(sub, sizeof(sub), "%s.se.fc2.bias", pre);
+            add_tensor(&L, sub, 1, b2, (int)r);
           }
           if (down) {
             snprintf(sub, sizeof(sub), "%s.down.conv", pre);

@@ -38,6 +38,8 @@ CONFIGS = {
     # synthetic stragglers (p = 60 %, minimum T/4); SURVEY 8 pins the depth model for it
     # configs[3]: the paper-shaped RGB-D agent (half-width ResNet50 + 2-layer LSTM-512)
     "rgbd": dict(arch="rgbd", E=4, T=128, epochs=2, minibatches=2, hidden=512, obs=(4, 256, 256), rnn_layers=2),
+    # NEXT-3: the RGB-D agent with the half-width SE-ResNeXt50 encoder (reading R9)
+    "serx50": dict(arch="serx50", E=4, T=128, epochs=2, minibatches=2, hidden=512, obs=(4, 256, 256), rnn_layers=2),
     "stress": dict(arch="depth", E=16, T=128, epochs=2, minibatches=2, hidden=512, obs=(1, 64, 64),
                    preempt_p=60),
 }

@@ -272,7 +272,8 @@ def test_clip_adam(dd, ctx, P, clip, freeze):
 
 
 # ------------------------------------------------------------------ a5 / a7 networks
-VISUAL = {"depth": dict(obs=(1, 64, 64), layers=1), "rgbd": dict(obs=(4, 256, 256), layers=2)}
+VISUAL = {"depth": dict(obs=(1, 64, 64), layers=1), "rgbd": dict(obs=(4, 256, 256), layers=2),
+          "serx50": dict(obs=(4, 256, 256), layers=2)}
 
 
 def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
@@ -288,7 +289,7 @@ def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
     env_idx = rng.permutation(E)[:B].astype(np.int32)
     L = ro["length"][env_idx]
     T_run = int(L.max())
-    vo_ = {k: t.cuda() for k, t in dd.visual_obs(ro["obs"], arch == "rgbd").items()} if vis else {}
+    vo_ = {k: t.cuda() for k, t in dd.visual_obs(ro["obs"], arch in ("rgbd", "serx50")).items()} if vis else {}
     batch = dd.make_batch(cu(ro["goal"]), cu(ro["prev_action"]), cu(ro["mask"]), cu(ro["h0"]), cu(ro["length"]),
                           cu(env_idx), E, T, ro["ld"], B, T_run, int(L.sum()),
                           obs=vo_.get("obs"), c0=cu(ro["c0"]) if vis else None, obs_rgb=vo_.get("obs_rgb"))
@@ -346,7 +347,7 @@ def _adopt_decisions(arch, params, ob, cache, dec, F, tie=2.5e-4):
         y, _ = convnets.conv_fwd(z, p[c + ".weight"], s, pad)
         return convnets.gn_fwd(y, p[g + ".weight"], p[g + ".bias"])[0]
 
-    if arch == "rgbd":
+    if arch in ("rgbd", "serx50"):
         x = convnets.avgpool2_fwd(convnets.rgbd_normalize(x))
     z = adopt("enc.stem.conv.relu", cg(x, "enc.stem.conv", "enc.stem.gn", 2, 3))
     _, pc = convnets.maxpool_fwd(z)
@@ -362,12 +363,20 @@ def _adopt_decisions(arch, params, ob, cache, dec, F, tie=2.5e-4):
     enc["pool"] = pc[:1] + (gpu_arg,) + pc[2:]
     z, _ = convnets.maxpool_fwd(z)  # the pooled values are the same whichever tied element is picked
     cin = 32
-    nblocks = convnets.R50_BLOCKS if arch == "rgbd" else (2, 2, 2, 2)
+    nblocks = convnets.R50_BLOCKS if arch in ("rgbd", "serx50") else (2, 2, 2, 2)
     for li, (w, nb) in enumerate(zip(convnets.WIDTHS, nblocks)):
         for bi in range(nb):
             s = 2 if (bi == 0 and li > 0) else 1
             pre = f"enc.layer{li + 1}.{bi}"
-            if arch == "rgbd":  # bottleneck 1x1 -> 3x3 (stride) -> 1x1
+            if arch == "serx50":  # grouped 3x3 and squeeze-excitation before the addition (R9)
+                cout = 4 * w
+                a = adopt(pre + ".conv1.relu", cg(z, pre + ".conv1", pre + ".gn1", 1, 0))
+                y2, _ = convnets.conv_fwd_grouped(a, p[pre + ".conv2.weight"], s, 1, convnets.SERX_CARD)
+                a = adopt(pre + ".conv2.relu", convnets.gn_fwd(y2, p[pre + ".gn2.weight"], p[pre + ".gn2.bias"])[0])
+                c3 = cg(a, pre + ".conv3", pre + ".gn3", 1, 0)
+                b, _ = convnets.se_fwd(c3, p[pre + ".se.fc1.weight"], p[pre + ".se.fc1.bias"],
+                                       p[pre + ".se.fc2.weight"], p[pre + ".se.fc2.bias"])
+            elif arch == "rgbd":  # bottleneck 1x1 -> 3x3 (stride) -> 1x1
                 cout = 4 * w
                 a = adopt(pre + ".conv1.relu", cg(z, pre + ".conv1", pre + ".gn1", 1, 0))
                 a = adopt(pre + ".conv2.relu", cg(a, pre + ".conv2", pre + ".gn2", s, 1))
@@ -429,10 +438,11 @@ def test_depth_network_parity(dd, ctx, E, T, B, lengths):
     assert not bad, bad
 
 
-# RGB-D agent (configs[3]): the same tolerances; 256x256 frames keep the fp64 oracle to a few frames
-@pytest.mark.parametrize("E,T,B,lengths", [(2, 2, 2, [2, 1])])
-def test_rgbd_network_parity(dd, ctx, E, T, B, lengths):
-    lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, "rgbd", E, T, B, 60 + E + T, lengths)
+# RGB-D agent (configs[3]) and its SE-ResNeXt50/2 variant (NEXT-3): the same tolerances; 256x256
+# frames keep the fp64 oracle to a few frames
+@pytest.mark.parametrize("arch,E,T,B,lengths", [("rgbd", 2, 2, 2, [2, 1]), ("serx50", 2, 2, 2, [2, 1])])
+def test_rgbd_network_parity(dd, ctx, arch, E, T, B, lengths):
+    lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, arch, E, T, B, 60 + E + T, lengths)
     assert rel_l2(lg, lo) < 1e-3 and rel_l2(vl, vo) < 1e-3, (rel_l2(lg, lo), rel_l2(vl, vo))
     bad = []
     for name, off, shape, _ in lay:
@@ -492,7 +502,8 @@ def test_learner_step_parity(dd, ctx, cfgname, lengths):
                                                       ("depth", 128, [128, 128, 70, 128], False),
                                                       ("rgbd", 2, [2, 1, 2, 2], False),
                                                       ("depth", 12, [12, 5, 12, 9], True),
-                                                      ("rgbd", 2, [2, 1, 2, 2], True)])
+                                                      ("rgbd", 2, [2, 1, 2, 2], True),
+                                                      ("serx50", 2, [2, 1, 2, 2], False)])
 def test_learner_chain_parity(dd, ctx, cfgname, T, lengths, frozen):
     """The learner step of the config (Adam eps 1e-8, 2 epochs x 2 minibatches) driven one ABI call
     at a time -- ddppo_gae, ddppo_adv_norm, then per minibatch ddppo_policy_fwd,
@@ -520,13 +531,13 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths, frozen):
     ro = synth.rollout(E, T, 24, length=lengths, hidden=H, obs_shape=c.get("obs"), rnn_layers=c.get("rnn_layers", 1))
     pm = synth.perms(24, 0, ep, E)
     ld = ro["ld"]
-    vis = c["arch"] in ("depth", "rgbd")
+    vis = c["arch"] in ("depth", "rgbd", "serx50")
     g = {k: cu(ro[k]) for k in ("rew", "val", "goal", "mask", "logp_old", "h0")}
     for k in ("prev_action", "action", "length"):
         g[k] = torch.from_numpy(np.ascontiguousarray(ro[k])).cuda()
     g["done"] = torch.from_numpy(np.ascontiguousarray(ro["done"])).cuda()
     if vis:
-        g.update({k: t.cuda() for k, t in dd.visual_obs(ro["obs"], c["arch"] == "rgbd").items()})
+        g.update({k: t.cuda() for k, t in dd.visual_obs(ro["obs"], c["arch"] in ("rgbd", "serx50")).items()})
         g["c0"] = cu(ro["c0"])
     adv, ret = torch.zeros((E, ld), device="cuda"), torch.zeros((E, ld), device="cuda")
     stats3 = torch.zeros(4, dtype=torch.float64, device="cuda")
