@@ -120,7 +120,8 @@ typedef enum {
   /* NEXT-3: the RGB-D agent with the half-width SE-ResNeXt50 encoder --
    * ResNet50/2's topology, each bottleneck's 3x3 conv grouped (cardinality 16, inner width 2 x planes)
    * and a squeeze-excitation module (reduction 16) before the residual addition (reading R9) */
-  DDPPO_ARCH_RGBD_SERX50_LSTM2 = 4
+  DDPPO_ARCH_RGBD_SERX50_LSTM2 = 4,
+  DDPPO_ARCH_RGBD_SERX101_LSTM2 = 5   /* the same with SE-ResNeXt101's block counts [3, 4, 23, 3] */
 } ddppo_arch;
 
 typedef struct {

@@ -297,6 +297,7 @@ def resnet50h_bwd(dz, p, caches, g):
 
 # ---------------------------------------------------------------- SE-ResNeXt50/2 (NEXT-3)
 SERX_CARD = 16   # cardinality of the grouped 3x3 convolutions (R9)
+R101_BLOCKS = (3, 4, 23, 3)  # SE-ResNeXt101 ("SE-ResNeXt101 + 1024-d LSTM")
 SE_RED = 16      # squeeze-excitation reduction
 
 
@@ -351,12 +352,12 @@ def se_bwd(dy, W1, W2, cache):
     return dx, dW1, db1, dW2, db2
 
 
-def serx50h_spec(in_ch):
-    """Ordered (name, kind, shape, stride, pad) of the SE-ResNeXt50/2 encoder's parameter tensors
-    (kind "gconv": grouped, cardinality SERX_CARD; "fc": SE linear layers with a bias)."""
+def serx50h_spec(in_ch, blocks=R50_BLOCKS):
+    """Ordered (name, kind, shape, stride, pad) of the SE-ResNeXt50/2 (blocks R101_BLOCKS: 101/2) encoder's
+    parameter tensors (kind "gconv": grouped, cardinality SERX_CARD; "fc": SE linear layers with a bias)."""
     spec = [("enc.stem.conv", "conv", (32, in_ch, 7, 7), 2, 3), ("enc.stem.gn", "gn", (32,), 0, 0)]
     cin = 32
-    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+    for li, (w, nb) in enumerate(zip(WIDTHS, blocks)):
         for bi in range(nb):
             s = 2 if (bi == 0 and li > 0) else 1
             pre = f"enc.layer{li + 1}.{bi}"
@@ -373,14 +374,14 @@ def serx50h_spec(in_ch):
     return spec
 
 
-def serx50h_fwd(x, p):
+def serx50h_fwd(x, p, blocks=R50_BLOCKS):
     """x [N][4][256][256] (raw RGB-D) -> feature [N][128][4][4]."""
     caches = {}
     z = avgpool2_fwd(rgbd_normalize(x))
     z = _conv_gn(z, p, "enc.stem.conv", "enc.stem.gn", 2, 3, True, caches)
     z, caches["pool"] = maxpool_fwd(z)
     cin = 32
-    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+    for li, (w, nb) in enumerate(zip(WIDTHS, blocks)):
         for bi in range(nb):
             s = 2 if (bi == 0 and li > 0) else 1
             pre = f"enc.layer{li + 1}.{bi}"
@@ -404,12 +405,12 @@ def serx50h_fwd(x, p):
     return z, caches
 
 
-def serx50h_bwd(dz, p, caches, g):
+def serx50h_bwd(dz, p, caches, g, blocks_per_layer=R50_BLOCKS):
     """Parameter gradients into g; returns the gradient wrt the raw input."""
     dz = _conv_gn_bwd(dz, p, "enc.compress.conv", "enc.compress.gn", True, caches, g)
     blocks = []
     cin = 32
-    for li, (w, nb) in enumerate(zip(WIDTHS, R50_BLOCKS)):
+    for li, (w, nb) in enumerate(zip(WIDTHS, blocks_per_layer)):
         for bi in range(nb):
             blocks.append((li, bi, w, cin))
             cin = 4 * w

@@ -19,8 +19,8 @@ Architectures (BASELINE.json configs; readings Z17-Z22):
                      -> 128x2x2 -> flatten (c, h, w order) -> Linear(512, 512) + ReLU
                      (Z17, Z20); x = [visual 512, goal_fc 32, act_emb 32]
                      -> LSTM(576, 512) (PyTorch i, f, g, o) -> Linear(512, A+1).
-  serx50 (NEXT-3, P:L212 / P:L582): the RGB-D agent with the half-width SE-ResNeXt50 encoder
-                     (convnets.serx50h_*; reading R9), same policy.
+  serx50 / serx101 (NEXT-3, P:L212 / P:L313-318 / P:L582): the RGB-D agent with the half-width
+                     SE-ResNeXt50 / 101 encoder (convnets.serx50h_*; reading R9), same policy.
   rgbd (configs[3]): RGB-D [4][256][256] (RGB in [0, 255] normalised channel-wise) ->
                      2x2 avg-pool -> half-width ResNet50 (convnets.py) -> 128x4x4 -> flatten ->
                      Linear(2048, 512) + ReLU; x = [visual, goal_fc, act_emb] -> 2-layer LSTM-512
@@ -64,10 +64,11 @@ def layout(arch, hidden=512, num_actions=NUM_ACTIONS):
                       ("rnn.weight_ih", (G, 576), H), ("rnn.weight_hh", (G, H), H),
                       ("rnn.bias_ih", (G,), H), ("rnn.bias_hh", (G,), H),
                       ("head.weight", (A1, H), H), ("head.bias", (A1,), H)]
-    if arch in ("rgbd", "serx50"):
+    if arch in ("rgbd", "serx50", "serx101"):
         H, G = hidden, 4 * hidden
         out = []
-        spec = convnets.resnet50h_spec(4) if arch == "rgbd" else convnets.serx50h_spec(4)
+        spec = (convnets.resnet50h_spec(4) if arch == "rgbd" else
+                convnets.serx50h_spec(4, convnets.R101_BLOCKS if arch == "serx101" else convnets.R50_BLOCKS))
         for name, kind, shape, _, _ in spec:
             if kind in ("conv", "gconv"):
                 out.append((name + ".weight", shape, shape[1] * shape[2] * shape[3]))
@@ -83,6 +84,10 @@ def layout(arch, hidden=512, num_actions=NUM_ACTIONS):
                     (f"rnn.bias_ih_l{layer}", (G,), H), (f"rnn.bias_hh_l{layer}", (G,), H)]
         return out + [("head.weight", (A1, H), H), ("head.bias", (A1,), H)]
     raise ValueError(arch)
+
+
+def _serx_blocks(arch):
+    return convnets.R101_BLOCKS if arch == "serx101" else convnets.R50_BLOCKS
 
 
 def offsets(arch, **kw):
@@ -151,11 +156,13 @@ def forward(arch, flat, batch, **kw):
         out = nets.linear_fwd(h, p["head.weight"], p["head.bias"])
         cache = {"goal": goal, "prev_action": np.asarray(batch["prev_action"]), "h": h, "rnn": rc, "enc": ec,
                  "feat_shape": feat.shape, "flat": flat_f, "vis": vis}
-    elif arch in ("rgbd", "serx50"):
+    elif arch in ("rgbd", "serx50", "serx101"):
         obs = np.asarray(batch["obs"], dtype=np.float64)  # [B][T][4][256][256]
         B, T = obs.shape[:2]
-        enc_fwd = convnets.resnet50h_fwd if arch == "rgbd" else convnets.serx50h_fwd
-        feat, ec = enc_fwd(obs.reshape((B * T,) + obs.shape[2:]), p)
+        if arch == "rgbd":
+            feat, ec = convnets.resnet50h_fwd(obs.reshape((B * T,) + obs.shape[2:]), p)
+        else:
+            feat, ec = convnets.serx50h_fwd(obs.reshape((B * T,) + obs.shape[2:]), p, _serx_blocks(arch))
         flat_f = feat.reshape(B, T, -1)  # (c, h, w) order, 2048
         vis = np.maximum(nets.linear_fwd(flat_f, p["visual_fc.weight"], p["visual_fc.bias"]), 0.0)
         ge = nets.linear_fwd(goal, p["goal_fc.weight"], p["goal_fc.bias"])
@@ -215,7 +222,7 @@ def backward(arch, flat, cache, dlogits, dvalues, freeze_encoder=False, extra=No
                                                                             dvpre)
         if not freeze_encoder:
             convnets.resnet18h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
-    elif arch in ("rgbd", "serx50"):
+    elif arch in ("rgbd", "serx50", "serx101"):
         dh, g["head.weight"], g["head.bias"] = nets.linear_bwd(cache["h"], p["head.weight"], dout)
         for layer in (1, 0):
             dh, g[f"rnn.weight_ih_l{layer}"], g[f"rnn.weight_hh_l{layer}"], g[f"rnn.bias_ih_l{layer}"], \
@@ -231,8 +238,10 @@ def backward(arch, flat, cache, dlogits, dvalues, freeze_encoder=False, extra=No
         dflat, g["visual_fc.weight"], g["visual_fc.bias"] = nets.linear_bwd(cache["flat"], p["visual_fc.weight"],
                                                                             dvpre)
         if not freeze_encoder:
-            (convnets.resnet50h_bwd if arch == "rgbd" else convnets.serx50h_bwd)(
-                dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
+            if arch == "rgbd":
+                convnets.resnet50h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g)
+            else:
+                convnets.serx50h_bwd(dflat.reshape(cache["feat_shape"]), p, cache["enc"], g, _serx_blocks(arch))
     else:
         raise ValueError(arch)
     return pack(arch, g, **kw)

@@ -26,7 +26,7 @@ def _stream(stream):
 
 def model_desc(arch, hidden=None, num_actions=4):
     arch_id = {"toy": ARCH_TOY, "gps": ARCH_GPS, "depth": ARCH_DEPTH, "rgbd": ARCH_RGBD,
-               "serx50": _lib.ARCH_SERX50}.get(arch, arch)
+               "serx50": _lib.ARCH_SERX50, "serx101": _lib.ARCH_SERX101}.get(arch, arch)
     if hidden is None:
         hidden = 64 if arch_id == ARCH_TOY else 512
     d = ModelDesc()

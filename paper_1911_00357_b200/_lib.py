@@ -21,7 +21,7 @@ c_int, c_float, c_double, c_vp, c_i64 = ctypes.c_int, ctypes.c_float, ctypes.c_d
 c_i32, c_size = ctypes.c_int32, ctypes.c_size_t
 
 STATUS = {0: "ok", 1: "config", 2: "numerical", 3: "protocol", 4: "comm", 5: "cuda", 6: "unsupported"}
-ARCH_TOY, ARCH_GPS, ARCH_DEPTH, ARCH_RGBD, ARCH_SERX50 = 0, 1, 2, 3, 4
+ARCH_TOY, ARCH_GPS, ARCH_DEPTH, ARCH_RGBD, ARCH_SERX50, ARCH_SERX101 = 0, 1, 2, 3, 4, 5
 A8_SHARDED, A8_ALLREAD, A8_AUTO = 0, 1, 2
 
 

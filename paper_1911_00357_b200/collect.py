@@ -24,8 +24,8 @@ class Collector:
         self.ctx, self.desc = lrn.ctx, lrn.desc
         E, dev = lrn.E, lrn.device
         self.E = E
-        self.visual = lrn.desc.arch in (2, 3, 4)
-        self.rgbd = lrn.desc.arch in (3, 4)
+        self.visual = lrn.desc.arch in (2, 3, 4, 5)
+        self.rgbd = lrn.desc.arch in (3, 4, 5)
         hs = lrn.rnn_layers * lrn.hidden
         f32 = dict(dtype=torch.float32, device=dev)
         # one-step staging arena in the rollout layout (T = 1, ld = 2): the act call's inputs

@@ -343,7 +343,7 @@ ddppo_status launch_gemm_tc(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st);
 struct ModelLayout {
   int64_t P = 0;
   int n = 0;
-  ddppo_tensor_info t[320];
+  ddppo_tensor_info t[512];
 };
 ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out);
 int64_t layout_offset(const ModelLayout& L, const char* name);
@@ -407,7 +407,9 @@ ddppo_status gps_fwd_loss(ddppo_ctx* ctx, const ModelLayout& L, const float* par
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // the visual agents (a ResNet encoder over frames + LSTM policy) / those with RGB-D 256^2 input and a
 // 2-layer LSTM
-inline bool arch_visual(int a) {
-  return a == DDPPO_ARCH_DEPTH_R18_LSTM || a == DDPPO_ARCH_RGBD_R50_LSTM2 || a == DDPPO_ARCH_RGBD_SERX50_LSTM2;
+inline bool arch_rgbd(int a) {
+  return a == DDPPO_ARCH_RGBD_R50_LSTM2 || a == DDPPO_ARCH_RGBD_SERX50_LSTM2 || a == DDPPO_ARCH_RGBD_SERX101_LSTM2;
 }
-inline bool arch_rgbd(int a) { return a == DDPPO_ARCH_RGBD_R50_LSTM2 || a == DDPPO_ARCH_RGBD_SERX50_LSTM2; }
+inline bool arch_visual(int a) {
+  return a == DDPPO_ARCH_DEPTH_R18_LSTM || arch_rgbd(a);
+}

@@ -127,7 +127,7 @@ __global__ void weights_bf16_kernel(const float* __restrict__ W, int Co, int Ci,
 // all convolutions' weights of one minibatch in one launch: the convolutions' Wr index ranges are
 // concatenated (off[i] = start of convolution i), one thread per element; Cp >= Ci is the padded
 // channel count of the GEMM operand (extra channels get zero weights)
-constexpr int kMaxConvs = 64;
+constexpr int kMaxConvs = 128;
 struct WeightPrep {
   int n;
   int off[kMaxConvs + 1];
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kThreads) frame_sum_kernel(const float* __rest
 // contiguously (coalesced); with 256 % C == 0 thread t always sees channel t % C, so per-group and
 // per-channel partial sums are per-thread sums combined in a fixed order through shared memory.
 constexpr int kGnMaxThreads = 1024;  // blockDim = max(256, C): a multiple of C
-constexpr int kMaxConvsGn = 64;
+constexpr int kMaxConvsGn = 128;
 __host__ __device__ inline int gn_threads(int C) { return C > 256 ? C : 256; }
 constexpr int kGnChunk = 8192;  // elements per chunk (a multiple of every C): kGnChunk / blockDim per thread
 __host__ __device__ inline int gn_chunk(int) { return kGnChunk; }
@@ -1290,7 +1290,8 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   __nv_bfloat16* zb = P.pool_b;
   int H = hp, cin = 32;
   const int widths[4] = {32, 64, 128, 256};
-  const int nblocks[4] = {3, 4, 6, 3};
+  const bool r101 = layout_offset(L, "enc.layer3.22.conv1.weight") >= 0;  // SE-ResNeXt101/2
+  const int nblocks[4] = {3, 4, r101 ? 23 : 6, 3};
   for (int li = 0; li < 4; ++li) {
     for (int bi = 0; bi < (rgbd ? nblocks[li] : 2); ++bi) {
       const int s = (bi == 0 && li > 0) ? 2 : 1, w = widths[li], cout = rgbd ? 4 * w : w;

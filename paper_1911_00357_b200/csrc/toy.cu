@@ -49,10 +49,12 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
     add_tensor(&L, "head.weight", 2, hw, (int)H);
     add_tensor(&L, "head.bias", 1, hb, (int)H);
   } else if (d->arch == DDPPO_ARCH_DEPTH_R18_LSTM || d->arch == DDPPO_ARCH_RGBD_R50_LSTM2 ||
-             d->arch == DDPPO_ARCH_RGBD_SERX50_LSTM2) {
+             d->arch == DDPPO_ARCH_RGBD_SERX50_LSTM2 || d->arch == DDPPO_ARCH_RGBD_SERX101_LSTM2) {
     if (d->hidden != 512) return DDPPO_ERR_CONFIG;
-    const bool serx = d->arch == DDPPO_ARCH_RGBD_SERX50_LSTM2;
+    const bool serx = d->arch == DDPPO_ARCH_RGBD_SERX50_LSTM2 || d->arch == DDPPO_ARCH_RGBD_SERX101_LSTM2;
+    const bool r101 = d->arch == DDPPO_ARCH_RGBD_SERX101_LSTM2;
     const bool rgbd = d->arch == DDPPO_ARCH_RGBD_R50_LSTM2 || serx;
+    (void)r101;
     const int64_t H = d->hidden, G = 4 * H;
     char name[48];
     // conv weight [Co][Ci][k][k] (fan_in Ci*k*k), GroupNorm gamma (ones: fan_in 0) / beta (zeros: -1)
@@ -74,7 +76,7 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
     int64_t cin = 32;
     char pre[40], sub[48];
     if (rgbd) {  // half-width ResNet50: bottlenecks [3, 4, 6, 3], outputs 4 x width
-      const int nblocks[4] = {3, 4, 6, 3};
+      const int nblocks[4] = {3, 4, r101 ? 23 : 6, 3};
       for (int li = 0; li < 4; ++li)
         for (int bi = 0; bi < nblocks[li]; ++bi) {
           const int64_t w = widths[li];

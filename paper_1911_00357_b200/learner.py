@@ -20,7 +20,7 @@ ROLLOUT_FIELDS = {  # name -> torch dtype
     "obs_rgb": torch.uint8,
 }
 # depth frames (bf16) of the Depth (configs[2]) / RGB-D (configs[3]) agents; RGB-D camera bytes
-OBS_SHAPES = {2: (1, 64, 64), 3: (1, 256, 256), 4: (1, 256, 256)}
+OBS_SHAPES = {2: (1, 64, 64), 3: (1, 256, 256), 4: (1, 256, 256), 5: (1, 256, 256)}
 RGB_SHAPE = (3, 256, 256)
 
 
@@ -60,14 +60,14 @@ class Learner:
             if peer:
                 ddppo_learner_register(ctx, self.ws)  # a8 over NVLink peer memory (collective)
         ld = self.ld
-        self.rnn_layers = 2 if self.desc.arch in (3, 4) else 1  # the RGB-D agents: 2 LSTM layers
+        self.rnn_layers = 2 if self.desc.arch in (3, 4, 5) else 1  # the RGB-D agents: 2 LSTM layers
         hs = self.rnn_layers * self.hidden
         shapes = {"rew": (E, ld), "val": (E, ld), "done": (E, ld), "length": (E,), "goal": (E, T, 3),
                   "prev_action": (E, ld), "mask": (E, ld), "h0": (E, hs), "action": (E, ld),
                   "logp_old": (E, ld)}
-        if self.desc.arch in (2, 3, 4):  # visual agents: + frames and the LSTM cell state
+        if self.desc.arch in (2, 3, 4, 5):  # visual agents: + frames and the LSTM cell state
             shapes.update(obs=(E, T) + OBS_SHAPES[self.desc.arch], c0=(E, hs))
-        if self.desc.arch in (3, 4):
+        if self.desc.arch in (3, 4, 5):
             shapes["obs_rgb"] = (E, T) + RGB_SHAPE
         # all rollout arrays + the epoch permutations in one device arena (256-byte aligned fields), so a
         # packed host arena reaches HBM in a single copy
@@ -107,7 +107,7 @@ class Learner:
         bf16 depth + uint8 RGB; dtype marshalling only)."""
         out = {k: ro[k] for k in self.dev if k not in ("obs", "obs_rgb")}
         if "obs" in self.dev:
-            out.update(visual_obs(ro["obs"], self.desc.arch in (3, 4)))
+            out.update(visual_obs(ro["obs"], self.desc.arch in (3, 4, 5)))
         return out
 
     def load_rollout(self, ro, perms, non_blocking=False):

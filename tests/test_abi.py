@@ -35,7 +35,7 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("arch", ["toy", "gps", "depth", "rgbd", "serx50"])
+@pytest.mark.parametrize("arch", ["toy", "gps", "depth", "rgbd", "serx50", "serx101"])
 def test_layout_matches_oracle(arch):
     lay = dd.param_layout(dd.model_desc(arch))
     offs, P = models.offsets(arch)

@@ -273,7 +273,7 @@ def test_clip_adam(dd, ctx, P, clip, freeze):
 
 # ------------------------------------------------------------------ a5 / a7 networks
 VISUAL = {"depth": dict(obs=(1, 64, 64), layers=1), "rgbd": dict(obs=(4, 256, 256), layers=2),
-          "serx50": dict(obs=(4, 256, 256), layers=2)}
+          "serx50": dict(obs=(4, 256, 256), layers=2), "serx101": dict(obs=(4, 256, 256), layers=2)}
 
 
 def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
@@ -289,7 +289,7 @@ def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
     env_idx = rng.permutation(E)[:B].astype(np.int32)
     L = ro["length"][env_idx]
     T_run = int(L.max())
-    vo_ = {k: t.cuda() for k, t in dd.visual_obs(ro["obs"], arch in ("rgbd", "serx50")).items()} if vis else {}
+    vo_ = {k: t.cuda() for k, t in dd.visual_obs(ro["obs"], arch in ("rgbd", "serx50", "serx101")).items()} if vis else {}
     batch = dd.make_batch(cu(ro["goal"]), cu(ro["prev_action"]), cu(ro["mask"]), cu(ro["h0"]), cu(ro["length"]),
                           cu(env_idx), E, T, ro["ld"], B, T_run, int(L.sum()),
                           obs=vo_.get("obs"), c0=cu(ro["c0"]) if vis else None, obs_rgb=vo_.get("obs_rgb"))
@@ -347,7 +347,7 @@ def _adopt_decisions(arch, params, ob, cache, dec, F, tie=2.5e-4):
         y, _ = convnets.conv_fwd(z, p[c + ".weight"], s, pad)
         return convnets.gn_fwd(y, p[g + ".weight"], p[g + ".bias"])[0]
 
-    if arch in ("rgbd", "serx50"):
+    if arch in ("rgbd", "serx50", "serx101"):
         x = convnets.avgpool2_fwd(convnets.rgbd_normalize(x))
     z = adopt("enc.stem.conv.relu", cg(x, "enc.stem.conv", "enc.stem.gn", 2, 3))
     _, pc = convnets.maxpool_fwd(z)
@@ -363,12 +363,13 @@ def _adopt_decisions(arch, params, ob, cache, dec, F, tie=2.5e-4):
     enc["pool"] = pc[:1] + (gpu_arg,) + pc[2:]
     z, _ = convnets.maxpool_fwd(z)  # the pooled values are the same whichever tied element is picked
     cin = 32
-    nblocks = convnets.R50_BLOCKS if arch in ("rgbd", "serx50") else (2, 2, 2, 2)
+    nblocks = {"rgbd": convnets.R50_BLOCKS, "serx50": convnets.R50_BLOCKS, "serx101": convnets.R101_BLOCKS}.get(
+        arch, (2, 2, 2, 2))
     for li, (w, nb) in enumerate(zip(convnets.WIDTHS, nblocks)):
         for bi in range(nb):
             s = 2 if (bi == 0 and li > 0) else 1
             pre = f"enc.layer{li + 1}.{bi}"
-            if arch == "serx50":  # grouped 3x3 and squeeze-excitation before the addition (R9)
+            if arch in ("serx50", "serx101"):  # grouped 3x3 and squeeze-excitation before the addition (R9)
                 cout = 4 * w
                 a = adopt(pre + ".conv1.relu", cg(z, pre + ".conv1", pre + ".gn1", 1, 0))
                 y2, _ = convnets.conv_fwd_grouped(a, p[pre + ".conv2.weight"], s, 1, convnets.SERX_CARD)
@@ -440,7 +441,8 @@ def test_depth_network_parity(dd, ctx, E, T, B, lengths):
 
 # RGB-D agent (configs[3]) and its SE-ResNeXt50/2 variant (NEXT-3): the same tolerances; 256x256
 # frames keep the fp64 oracle to a few frames
-@pytest.mark.parametrize("arch,E,T,B,lengths", [("rgbd", 2, 2, 2, [2, 1]), ("serx50", 2, 2, 2, [2, 1])])
+@pytest.mark.parametrize("arch,E,T,B,lengths", [("rgbd", 2, 2, 2, [2, 1]), ("serx50", 2, 2, 2, [2, 1]),
+                                                ("serx101", 2, 1, 2, None)])
 def test_rgbd_network_parity(dd, ctx, arch, E, T, B, lengths):
     lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, arch, E, T, B, 60 + E + T, lengths)
     assert rel_l2(lg, lo) < 1e-3 and rel_l2(vl, vo) < 1e-3, (rel_l2(lg, lo), rel_l2(vl, vo))
