@@ -303,6 +303,9 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
                               int k, int s, int p, int flip, const __nv_bfloat16* w, int64_t wplane, int N, int planes,
                               float* out, int64_t ldc, int accumulate, float* partial, int max_splits, int slot,
                               int* splits_out, cudaStream_t st);
+ddppo_status launch_tconv_dgrad_s2(ddppo_ctx* ctx, const __nv_bfloat16* dy, int64_t dy_plane, int F, int Ho, int Wo,
+                                   int Co, int H, int W, int Ci, int k, int p, const __nv_bfloat16* wd,
+                                   int64_t wd_plane, int planes, float* dx, int accumulate, cudaStream_t st);
 ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, int H, int W, int C, int k, int s,
                                 int p, const __nv_bfloat16* dy, int N, float* dw, int Cr, float* partial, int max_splits,
                                 int slot, int* splits_out, cudaStream_t st, int groups = 1);

@@ -1555,6 +1555,12 @@ ddppo_status conv_dgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* w, const
     if (r != DDPPO_OK || splits == 1) return r;
     return launch_splitk_reduce(ctx, sc.part, splits, (int64_t)Md * g.Ci, Md, g.Ci, dx, g.Ci, accumulate_dx, st);
   }
+  if (ctx->conv_engine == DDPPO_CONV_TMA && g.s == 2 && g.Co % 32 == 0 && g.k <= 3 && g.Ci % 8 == 0 &&
+      g.k <= g.p + 2) {
+    // stride 2: the four output phases, each a stride-1 tap subset over dy, in one launch
+    return launch_tconv_dgrad_s2(ctx, dy, dy_plane, g.F, g.Ho, g.Wo, g.Co, g.H, g.W, g.Ci, g.k, g.p, wd_b, wd_plane,
+                                 planes, dx, accumulate_dx, st);
+  }
   IGemm gm;
   gm.a = op_pix(dy, g.H, g.W, g.Ho, g.Wo, g.Co, g, 1, dy_plane);
   gm.b = op_dense(IG_DENSE_K, wd_b, Kd, wd_plane);

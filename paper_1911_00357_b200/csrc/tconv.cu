@@ -108,7 +108,13 @@ struct TcArgs {
   int Ho, Wo, s, p, k;    // im2col traversal geometry (output pixel grid of the box walk)
   int F;                  // frames (WGRAD: the reduction runs over F * Ho * Wo pixels)
   int C, nsl;             // channels of the im2col'd tensor, C / CS
-  int flip;               // DGRAD: tap (u, v) reads offset (k-1-u, k-1-v)
+  // FPROP / DGRAD tap lists: phase q (nphase > 1: the 4 output phases of a stride-2 input gradient)
+  // runs ntap[q] taps; tap i multiplies weight column block uv[q][i] (of k*k) with the im2col box at
+  // offset (oh, ow)[q][i]; phase q's output rows land on pixels (2i + rh[q], 2j + rw[q]) of the
+  // OH x OW output (scatter), else on row q of the grid
+  int nphase, scatter, OH, OW;
+  int8_t ntap[4], rh[4], rw[4];
+  int8_t uv[4][9], oh[4][9], ow[4][9];
   float* out;             // result: [M][ldc] rows (FPROP / DGRAD), or the weight gradient (wg)
   long long ldc;
   int accumulate;         // out (+)= (FPROP / DGRAD)
@@ -201,7 +207,7 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
-  const int tiles = a.tiles_m * a.tiles_n;
+  const int tiles = a.tiles_m * a.tiles_n * max(1, a.nphase);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -210,8 +216,10 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
       uint32_t ph = 0;
       for (int wi = blockIdx.x; wi < a.n_work; wi += gridDim.x) {
         const int z = wi / tiles, t = wi - z * tiles;
-        const int m0 = (t % a.tiles_m) * kBM, n0 = (t / a.tiles_m) * BN;
-        const int k0 = z * a.kper, k1 = min(a.n_k, k0 + a.kper);
+        const int q = t / (a.tiles_m * a.tiles_n), tq = t - q * a.tiles_m * a.tiles_n;
+        const int m0 = (tq % a.tiles_m) * kBM, n0 = (tq / a.tiles_m) * BN;
+        const int nk = MODE == TC_FWD ? a.ntap[q] * a.nsl : a.n_k;
+        const int k0 = z * a.kper, k1 = min(nk, k0 + a.kper);
         int w = 0, h = 0, n = 0;
         if (MODE == TC_FWD) pix_coords(a, m0, w, h, n);
         for (int it = k0; it < k1; ++it) {
@@ -220,13 +228,13 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
           const uint32_t sA = s_u32(smem + stage * Cfg::kStage), sB = sA + NPL * Cfg::kA;
           if constexpr (MODE == TC_FWD) {
             const int tap = it / a.nsl, sl = it - tap * a.nsl;
-            const int u = tap / a.k, v = tap - u * a.k;
-            const uint16_t ow = (uint16_t)(a.flip ? a.k - 1 - v : v), oh = (uint16_t)(a.flip ? a.k - 1 - u : u);
+            const int col = a.uv[q][tap] * a.C + sl * CS;
+            const uint16_t ow = (uint16_t)a.ow[q][tap], oh = (uint16_t)a.oh[q][tap];
             tma_im2col(sA, &mA0, &full[stage], sl * CS, w, h, n, ow, oh);
-            tma_2d(sB, &mB0, &full[stage], tap * a.C + sl * CS, n0);
+            tma_2d(sB, &mB0, &full[stage], col, n0);
             if constexpr (NPL == 2) {
               tma_im2col(sA + Cfg::kA, &mA1, &full[stage], sl * CS, w, h, n, ow, oh);
-              tma_2d(sB + Cfg::kB, &mB1, &full[stage], tap * a.C + sl * CS, n0);
+              tma_2d(sB + Cfg::kB, &mB1, &full[stage], col, n0);
             }
           } else {
             // k-chunk = pixels [it*128, +128); A = 128/CS boxes of (tap, channel slice) rows of this M-block
@@ -258,8 +266,10 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
     int stage = 0, acc = 0;
     uint32_t ph = 0, aph = 0;
     for (int wi = blockIdx.x; wi < a.n_work; wi += gridDim.x) {
-      const int z = wi / tiles;
-      const int k0 = z * a.kper, k1 = min(a.n_k, k0 + a.kper);
+      const int z = wi / tiles, t = wi - z * tiles;
+      const int q = t / (a.tiles_m * a.tiles_n);
+      const int nk = MODE == TC_FWD ? a.ntap[q] * a.nsl : a.n_k;
+      const int k0 = z * a.kper, k1 = min(nk, k0 + a.kper);
       mb_wait(&tempty[acc], aph ^ 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t d = tmem + (uint32_t)(acc * BN);
@@ -311,9 +321,16 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
     uint32_t aph = 0;
     for (int wi = blockIdx.x; wi < a.n_work; wi += gridDim.x) {
       const int z = wi / tiles, t = wi - z * tiles;
-      const int m0 = (t % a.tiles_m) * kBM, n0 = (t / a.tiles_m) * BN;
-      const int row = m0 + q * 32 + lane;
-      const bool rok = row < a.M;
+      const int ph = t / (a.tiles_m * a.tiles_n), tq = t - ph * a.tiles_m * a.tiles_n;
+      const int m0 = (tq % a.tiles_m) * kBM, n0 = (tq / a.tiles_m) * BN;
+      int row = m0 + q * 32 + lane;
+      bool rok = row < a.M;
+      if (a.scatter && rok) {  // phase grid position -> output pixel (2i + rh, 2j + rw)
+        const int hw = a.Ho * a.Wo, f = row / hw, r = row - f * hw, i = r / a.Wo, j = r - i * a.Wo;
+        const int y = 2 * i + a.rh[ph], x = 2 * j + a.rw[ph];
+        rok = y < a.OH && x < a.OW;
+        row = (f * a.OH + y) * a.OW + x;
+      }
       mb_wait(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float* prow = a.splits > 1 ? a.part + ((long long)z * a.M + row) * a.N + n0 : nullptr;
@@ -414,13 +431,15 @@ CUtensorMapSwizzle swz_for(int row_bytes) {
 // im2col view of x[F][H][W][C] (bf16) for a k x k / stride s / pad p window: boxes of 128 output
 // pixels x cs channels
 ddppo_status map_im2col(ddppo_ctx* ctx, CUtensorMap* m, const __nv_bfloat16* x, int F, int H, int W, int C, int k,
-                        int s, int p, int cs) {
+                        int s, int p, int cs, bool corners = false, int lo_c = 0, int up_c = 0) {
   static EncIm2colFn enc = nullptr;
   ddppo_status st = driver_fn(ctx, "cuTensorMapEncodeIm2col", &enc);
   if (st != DDPPO_OK) return st;
   const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)F};
   const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-  const int lower[2] = {-p, -p}, upper[2] = {p - (k - 1), p - (k - 1)};
+  // traversal box: the k x k / pad p window, or explicit corners (the stride-2 input gradient's phases)
+  const int lower[2] = {corners ? lo_c : -p, corners ? lo_c : -p};
+  const int upper[2] = {corners ? up_c : p - (k - 1), corners ? up_c : p - (k - 1)};
   const cuuint32_t estr[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<__nv_bfloat16*>(x), dims, strides, lower, upper,
                    (cuuint32_t)cs, (cuuint32_t)kPix, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_for(cs * 2),
@@ -463,10 +482,11 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min
   const int cap = slot == 0 ? ctx->sm_count * std::min(per_sm, 2) : ctx->sm_count / 2;
   // split-K over the k-iterations: ~one work item per resident CTA, each >= min_iters iterations; the
   // split tiles' fixup needs every work item resident at once (n_work <= grid)
-  const int tiles = a.tiles_m * a.tiles_n;
+  const int tiles = a.tiles_m * a.tiles_n * std::max(1, (int)a.nphase);
   int splits = 1;
-  if (max_splits > 1 && tiles < cap)
+  if (max_splits > 1 && tiles < cap && a.nphase <= 1)
     splits = std::max(1, std::min({cap / tiles, a.n_k / std::max(1, min_iters), max_splits}));
+  DDPPO_REQUIRE(ctx, a.n_k >= 1, "tconv: empty reduction");
   a.kper = (a.n_k + splits - 1) / splits;
   splits = (a.n_k + a.kper - 1) / a.kper;
   a.splits = splits;
@@ -474,8 +494,11 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min
   DDPPO_REQUIRE(ctx, splits == 1 || (2 * tiles <= kMaxTileCounters / 2 && a.part), "tconv: split-K needs scratch");
   const int grid = std::max(1, std::min(a.n_work, cap));
   ProfScope ps(ctx, DDPPO_K_CONV, st, 1);
-  if (ctx->prof) ctx->flops[DDPPO_K_CONV] += 2.0 * a.M * a.N * (MODE == TC_FWD ? (double)a.k * a.k * a.C
-                                                                             : (double)a.Ho * a.Wo * a.F);
+  if (ctx->prof) {
+    double taps = 0;
+    for (int q = 0; q < std::max(1, (int)a.nphase); ++q) taps += a.ntap[q];
+    ctx->flops[DDPPO_K_CONV] += 2.0 * a.M * a.N * (MODE == TC_FWD ? taps * a.C : (double)a.Ho * a.Wo * a.F);
+  }
   kern<<<grid, kThreadsTC, Cfg::kSmem, st>>>(maps[0], maps[1], maps[2], maps[3], a);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
@@ -494,6 +517,7 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
                               int* splits_out, cudaStream_t st) {
   DDPPO_REQUIRE(ctx, C % 32 == 0 && N % 8 == 0 && ldc % 4 == 0, "tconv: C % 32 == 0, N % 8 == 0 required");
   DDPPO_REQUIRE(ctx, !flip || s == 1, "tconv: transposed taps only for stride-1 convolutions");
+  DDPPO_REQUIRE(ctx, k <= 3, "tconv: kernels up to 3x3 (tap lists)");
   DDPPO_REQUIRE(ctx, ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0 && ((uintptr_t)out & 15) == 0,
                 "tconv: 16-byte aligned operands required");
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
@@ -509,7 +533,14 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
   a.k = k;
   a.C = C;
   a.nsl = C / cs;
-  a.flip = flip;
+  a.nphase = 1;
+  a.ntap[0] = (int8_t)(k * k);
+  for (int u = 0; u < k; ++u)
+    for (int v = 0; v < k; ++v) {
+      a.uv[0][u * k + v] = (int8_t)(u * k + v);
+      a.oh[0][u * k + v] = (int8_t)(flip ? k - 1 - u : u);
+      a.ow[0][u * k + v] = (int8_t)(flip ? k - 1 - v : v);
+    }
   a.n_k = k * k * a.nsl;
   a.tiles_m = (a.M + kBM - 1) / kBM;
   a.tiles_n = (N + bn - 1) / bn;
@@ -584,4 +615,98 @@ ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, i
   if (cs == 32 && bn == 64) return run<32, 64, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
   if (cs == 64 && bn == 32) return run<64, 32, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
   return run<64, 64, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
+}
+
+// Input gradient of a stride-2 convolution (k <= 3) as one launch over its 4 output phases: dx pixel
+// (2i + rh, 2j + rw) receives sum over the taps u, v with (rh + p - u), (rw + p - v) even of
+// dy[i + (rh + p - u) / 2][j + (rw + p - v) / 2] Wd[c][(u, v, o)] -- a stride-1 tap subset per phase
+// over dy's grid, the epilogue scattering each phase's rows onto its pixels.  dy [F][Ho][Wo][Co] bf16
+// (hi / lo planes when planes == 2), Wd [Ci][k*k*Co]; dx [F][H][W][Ci] fp32 (+)=.
+ddppo_status launch_tconv_dgrad_s2(ddppo_ctx* ctx, const __nv_bfloat16* dy, int64_t dy_plane, int F, int Ho, int Wo,
+                                   int Co, int H, int W, int Ci, int k, int p, const __nv_bfloat16* wd,
+                                   int64_t wd_plane, int planes, float* dx, int accumulate, cudaStream_t st) {
+  DDPPO_REQUIRE(ctx, Co % 32 == 0 && Ci % 8 == 0 && k <= 3, "tconv dgrad s2: Co % 32 == 0, Ci % 8 == 0, k <= 3");
+  DDPPO_REQUIRE(ctx, ((uintptr_t)dy & 15) == 0 && ((uintptr_t)wd & 15) == 0 && ((uintptr_t)dx & 15) == 0,
+                "tconv dgrad s2: 16-byte aligned operands required");
+  const int cs = Co % 64 == 0 ? 64 : 32;
+  const int bn = Ci <= 32 ? 32 : Ci <= 64 ? 64 : 128;
+  TcArgs a = {};
+  a.M = F * Ho * Wo;
+  a.N = Ci;
+  a.Ho = Ho;
+  a.Wo = Wo;
+  a.s = 1;
+  a.p = 0;
+  a.k = k;
+  a.C = Co;
+  a.nsl = Co / cs;
+  a.nphase = 4;
+  a.scatter = 1;
+  a.OH = H;
+  a.OW = W;
+  bool empty_phase = false;
+  for (int rh = 0; rh < 2; ++rh)
+    for (int rw = 0; rw < 2; ++rw) {
+      const int q = rh * 2 + rw;
+      a.rh[q] = (int8_t)rh;
+      a.rw[q] = (int8_t)rw;
+      int n = 0;
+      for (int u = 0; u < k; ++u)
+        for (int v = 0; v < k; ++v) {
+          if ((rh + p - u) % 2 || (rw + p - v) % 2) continue;
+          const int oh = (rh + p - u) / 2, ow = (rw + p - v) / 2;
+          DDPPO_REQUIRE(ctx, rh + p - u >= 0 && rw + p - v >= 0, "tconv dgrad s2: negative phase offset");
+          a.uv[q][n] = (int8_t)(u * k + v);
+          a.oh[q][n] = (int8_t)oh;
+          a.ow[q][n] = (int8_t)ow;
+          ++n;
+        }
+      a.ntap[q] = (int8_t)n;
+      empty_phase = empty_phase || n == 0;
+    }
+  // phases without taps (a 1x1 stride-2 conv touches only the even pixels) must read 0: zero dx once
+  if (empty_phase && !accumulate) {
+    DDPPO_CUDA_TRY(ctx, cudaMemsetAsync(dx, 0, (size_t)F * H * W * Ci * sizeof(float), st));
+    accumulate = 1;
+  }
+  // skip empty phases: pack the non-empty ones first (the epilogue reads rh / rw per phase)
+  int np = 0;
+  for (int q = 0; q < 4; ++q)
+    if (a.ntap[q] > 0) {
+      if (np != q) {
+        a.ntap[np] = a.ntap[q];
+        a.rh[np] = a.rh[q];
+        a.rw[np] = a.rw[q];
+        for (int i = 0; i < 9; ++i) {
+          a.uv[np][i] = a.uv[q][i];
+          a.oh[np][i] = a.oh[q][i];
+          a.ow[np][i] = a.ow[q][i];
+        }
+      }
+      ++np;
+    }
+  a.nphase = np;
+  for (int q = 0; q < np; ++q) a.n_k = std::max(a.n_k, a.ntap[q] * a.nsl);  // (one split: kper = the longest)
+  a.tiles_m = (a.M + kBM - 1) / kBM;
+  a.tiles_n = (Ci + bn - 1) / bn;
+  a.out = dx;
+  a.ldc = Ci;
+  a.accumulate = accumulate;
+  a.cnt = ctx->d_tile_cnt;
+  CUtensorMap maps[4];
+  memset(maps, 0, sizeof(maps));
+  const int K = k * k * Co;
+  ddppo_status r = map_im2col(ctx, &maps[0], dy, F, Ho, Wo, Co, 1, 1, 0, cs, true, 0, 0);
+  if (r == DDPPO_OK && planes == 2) r = map_im2col(ctx, &maps[1], dy + dy_plane, F, Ho, Wo, Co, 1, 1, 0, cs, true, 0, 0);
+  if (r == DDPPO_OK) r = map_2d(ctx, &maps[2], wd, Ci, K, cs, bn);
+  if (r == DDPPO_OK && planes == 2) r = map_2d(ctx, &maps[3], wd + wd_plane, Ci, K, cs, bn);
+  if (r != DDPPO_OK) return r;
+#define TC_CASE(CS_, BN_, NPL_) \
+  if (cs == CS_ && bn == BN_ && planes == NPL_) return run<CS_, BN_, NPL_, TC_FWD>(ctx, maps, a, 1, 1, 0, st);
+  TC_CASE(32, 32, 1) TC_CASE(32, 64, 1) TC_CASE(32, 128, 1) TC_CASE(64, 32, 1) TC_CASE(64, 64, 1)
+  TC_CASE(64, 128, 1) TC_CASE(32, 32, 2) TC_CASE(32, 64, 2) TC_CASE(32, 128, 2) TC_CASE(64, 32, 2)
+  TC_CASE(64, 64, 2) TC_CASE(64, 128, 2)
+#undef TC_CASE
+  DDPPO_REQUIRE(ctx, false, "tconv dgrad s2: no instantiation for this shape");
+  return DDPPO_ERR_CONFIG;
 }
