@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--conv-engine", default="tma", choices=["tma", "cpasync"],
                     help="visual encoders' convolutions: TMA-fed warp-specialised tcgen05 (default) or the round-1 "
                          "cp.async kernel (A/B)")
+    ap.add_argument("--fwd-planes", type=int, default=2, choices=[1, 2],
+                    help="encoder forward operands: bf16 hi/lo planes (2, default) or plain bf16 (1)")
     ap.add_argument("--a8", default="auto", choices=["auto", "sharded", "allread"], help="peer-memory a8 form (N > 1)")
     return ap.parse_args()
 
@@ -243,6 +245,7 @@ def main():
         uid = obj[0]
     ctx = dd.Context(rank, world, uid, device=local)
     dd.ddppo_set_conv_engine(ctx, args.conv_engine)
+    dd.ddppo_set_fwd_planes(ctx, args.fwd_planes)
     dd.ddppo_set_a8_mode(ctx, args.a8)
     c = synth.CONFIGS[args.config]
     desc = dd.model_desc(c["arch"])

@@ -371,6 +371,10 @@ ddppo_status ddppo_set_a8_mode(ddppo_ctx* ctx, int mode);
  *     stride-2 input gradients and the 8-channel RGB-D stem). */
 typedef enum { DDPPO_CONV_CPASYNC = 0, DDPPO_CONV_TMA = 1 } ddppo_conv_engine;
 ddppo_status ddppo_set_conv_engine(ddppo_ctx* ctx, int engine);
+/* Operand precision of the visual encoders' forward convolutions on the TMA engine: 2 (default) =
+ * bf16 hi / lo planes (x = hi + lo, hi*hi + hi*lo + lo*hi: ~16-bit mantissas -- the ReLU / max-pool
+ * decisions the backward inherits are then within ~2^-16 of the fp32 ones); 1 = plain bf16. */
+ddppo_status ddppo_set_fwd_planes(ddppo_ctx* ctx, int planes);
 
 /* CUDA graphs for ddppo_learner_step (default on): the step is captured once per (configuration,
  * buffer addresses, minibatch shapes) -- after one eager run of a new configuration -- and

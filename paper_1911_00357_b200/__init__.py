@@ -387,3 +387,8 @@ def make_act_batch(goal, prev_action, mask, h_in, h_out, E, T, ld, t, seed, coun
 def ddppo_policy_act(ctx, desc, params, act_batch, actions, logp, values, ws, logits=None, stream=None):
     _call(ctx, "ddppo_policy_act", ctypes.byref(desc), f32(params), ctypes.byref(act_batch), i32(actions), f32(logp),
           f32(values), f32(logits), dptr(ws), ws.numel() * ws.element_size(), _stream(stream))
+
+
+def ddppo_set_fwd_planes(ctx, planes):
+    """Encoder forward operands: 2 = bf16 hi/lo planes (default), 1 = plain bf16."""
+    _call(ctx, "ddppo_set_fwd_planes", int(planes))

@@ -126,6 +126,7 @@ _SIGS = {
     "ddppo_set_graphs": (c_int, [c_vp, c_int]),
     "ddppo_set_a8_mode": (c_int, [c_vp, c_int]),
     "ddppo_set_conv_engine": (c_int, [c_vp, c_int]),
+    "ddppo_set_fwd_planes": (c_int, [c_vp, c_int]),
     "ddppo_act_workspace_size": (c_int, [P_(ModelDesc), c_int, P_(c_size)]),
     "ddppo_policy_act": (c_int, [c_vp, P_(ModelDesc), c_vp, P_(ActBatch), c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "ddppo_reinit_critic": (c_int, [c_vp, P_(ModelDesc), c_vp, c_vp, c_vp, ctypes.c_uint64, c_vp]),

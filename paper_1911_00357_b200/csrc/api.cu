@@ -622,6 +622,13 @@ ddppo_status ddppo_set_conv_engine(ddppo_ctx* ctx, int engine) {
   return DDPPO_OK;
 }
 
+ddppo_status ddppo_set_fwd_planes(ddppo_ctx* ctx, int planes) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  DDPPO_REQUIRE(ctx, planes == 1 || planes == 2, "set_fwd_planes: 1 or 2");
+  ctx->fwd_planes = planes;
+  return DDPPO_OK;
+}
+
 ddppo_status ddppo_set_graphs(ddppo_ctx* ctx, int enable) {
   if (!ctx) return DDPPO_ERR_CONFIG;
   ctx->graphs = enable != 0;
@@ -704,6 +711,7 @@ ddppo_status ddppo_learner_step(ddppo_ctx* ctx, const ddppo_model_desc* host_des
     key_put(key, use_peers);
     key_put(key, ctx->a8_mode);
     key_put(key, ctx->conv_engine);
+    key_put(key, ctx->fwd_planes);
     key_put(key, (int)(mb0 & 1));
     for (const MbShape& sh : mbs) key_put(key, sh);
     if (!ctx->graph) {

@@ -38,6 +38,7 @@ struct ddppo_ctx {
   uint64_t peer_mb = 0;
   int a8_mode = DDPPO_A8_AUTO;          // ddppo_set_a8_mode
   int conv_engine = DDPPO_CONV_TMA;     // ddppo_set_conv_engine
+  int fwd_planes = 2;                   // ddppo_set_fwd_planes: encoder forward operands bf16x3 (2) / bf16 (1)
   int* d_tile_cnt = nullptr;            // split-K tile arrival counters (tconv.cu), zero between kernels
   // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step
   int* d_step = nullptr;

@@ -1455,7 +1455,7 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
   if (ctx->conv_engine == DDPPO_CONV_TMA && g.Ci % 32 == 0) {
     int splits = 1;
     ddppo_status r = launch_tconv_fwd(ctx, xb, (int64_t)g.F * g.H * g.W * g.Ci, g.F, g.H, g.W, g.Ci, g.k, g.s, g.p, 0,
-                                      wr_b, (int64_t)g.Co * K, g.Co, 2, y, g.Co, 0, sc.part,
+                                      wr_b, (int64_t)g.Co * K, g.Co, ctx->fwd_planes, y, g.Co, 0, sc.part,
                                       split_cap(sc, M, g.Co, 16), sc.slot, &splits, st);
     if (r != DDPPO_OK || splits == 1) return r;
     return launch_splitk_reduce(ctx, sc.part, splits, (int64_t)M * g.Co, M, g.Co, y, g.Co, 0, st);
