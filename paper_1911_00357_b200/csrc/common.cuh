@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <string>
@@ -39,6 +40,7 @@ struct ddppo_ctx {
   int a8_mode = DDPPO_A8_AUTO;          // ddppo_set_a8_mode
   int conv_engine = DDPPO_CONV_TMA;     // ddppo_set_conv_engine
   int fwd_planes = 2;                   // ddppo_set_fwd_planes: encoder forward operands bf16x3 (2) / bf16 (1)
+  bool tconv_bn64 = getenv("DDPPO_TCONV_BN128") == nullptr;  // A/B switch for the conv kernel's N tile
   int* d_tile_cnt = nullptr;            // split-K tile arrival counters (tconv.cu), zero between kernels
   // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step
   int* d_step = nullptr;
