@@ -478,12 +478,18 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min
     attr = true;
   }
   const int per_sm = std::max(1, (int)((227u * 1024u) / (Cfg::kSmem + 2048)));
-  // slot 1 = the side stream (weight gradients beside the critical path): at most ~half the SMs
-  const int cap = slot == 0 ? ctx->sm_count * std::min(per_sm, 2) : ctx->sm_count / 2;
+  // slot 1 = the side stream (weight gradients beside the critical path): at most a quarter of the SMs
+  // (measured: 1/2 -1 %, 1/6 -1.4 %, 1/8 -4 %)
+  static const int side_div = getenv("DDPPO_TCONV_SIDEDIV") ? atoi(getenv("DDPPO_TCONV_SIDEDIV")) : 4;  // A/B knob
+  const int cap = slot == 0 ? ctx->sm_count * std::min(per_sm, 2) : std::max(1, ctx->sm_count / side_div);
   // split-K over the k-iterations: ~one work item per resident CTA, each >= min_iters iterations; the
   // split tiles' fixup needs every work item resident at once (n_work <= grid)
   const int tiles = a.tiles_m * a.tiles_n * std::max(1, (int)a.nphase);
   int splits = 1;
+  static const int min_it_f = getenv("DDPPO_TCONV_MINIT_F") ? atoi(getenv("DDPPO_TCONV_MINIT_F")) : 0;
+  static const int min_it_w = getenv("DDPPO_TCONV_MINIT_W") ? atoi(getenv("DDPPO_TCONV_MINIT_W")) : 0;
+  if (MODE == TC_FWD && min_it_f > 0) min_iters = min_it_f;  // A/B knobs
+  if (MODE == TC_WGRAD && min_it_w > 0) min_iters = min_it_w;
   if (max_splits > 1 && tiles < cap && a.nphase <= 1)
     splits = std::max(1, std::min({cap / tiles, a.n_k / std::max(1, min_iters), max_splits}));
   DDPPO_REQUIRE(ctx, a.n_k >= 1, "tconv: empty reduction");
@@ -613,10 +619,10 @@ ddppo_status launch_tconv_wgrad(ddppo_ctx* ctx, const __nv_bfloat16* x, int F, i
   ddppo_status r = map_im2col(ctx, &maps[0], x, F, H, W, C, k, s, p, cs);
   if (r == DDPPO_OK) r = map_2d(ctx, &maps[2], dy, pix, N, bn, kPix);
   if (r != DDPPO_OK) return r;
-  if (cs == 32 && bn == 32) return run<32, 32, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
-  if (cs == 32 && bn == 64) return run<32, 64, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
-  if (cs == 64 && bn == 32) return run<64, 32, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
-  return run<64, 64, 1, TC_WGRAD>(ctx, maps, a, 2, max_splits, slot, st);
+  if (cs == 32 && bn == 32) return run<32, 32, 1, TC_WGRAD>(ctx, maps, a, 32, max_splits, slot, st);
+  if (cs == 32 && bn == 64) return run<32, 64, 1, TC_WGRAD>(ctx, maps, a, 32, max_splits, slot, st);
+  if (cs == 64 && bn == 32) return run<64, 32, 1, TC_WGRAD>(ctx, maps, a, 32, max_splits, slot, st);
+  return run<64, 64, 1, TC_WGRAD>(ctx, maps, a, 32, max_splits, slot, st);
 }
 
 // Input gradient of a stride-2 convolution (k <= 3) as one launch over its 4 output phases: dx pixel
