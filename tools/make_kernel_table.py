@@ -11,6 +11,12 @@ raw = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 col = {h: i for i, h in enumerate(hdr)}
+for i, h in enumerate(hdr):  # section-prefixed raw names ("TPC.TriageCompute.<metric>") by their suffix
+    base = h.split(".", 2)[-1] if h.count(".") >= 2 and h.split(".")[0].isupper() else h
+    col.setdefault(base, i)
+    if "." in h:
+        col.setdefault(h[h.find(".") + 1:], i)
+        col.setdefault(h[h.find(".", h.find(".") + 1) + 1:], i)
 
 
 def g(r, name, default=float("nan")):
@@ -33,28 +39,45 @@ def fam(name):
 
 t_unit = units[col["gpu__time_duration.sum"]]
 scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(t_unit, 1.0)
+ub = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 lines = ["| # | kernel | grid | time (us) | tensor pipe % of peak | DRAM % of peak | DRAM bytes | L2 hit % |",
          "|---|---|---|---|---|---|---|---|"]
 traffic = defaultdict(list)
+agg = defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0.0, 0.0])  # launches, time, tensor%*t, dram%*t, bytes, l2*t
 for n, r in enumerate(data):
     name = r[col["Kernel Name"]]
     t = g(r, "gpu__time_duration.sum") * scale
-    tens = g(r, "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")
+    tens = g(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")
+    if not isinstance(tens, float) or tens != tens:
+        tens = g(r, "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")
+    if not isinstance(tens, float):
+        tens = float("nan")
     dram_pct = g(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")
     rd, wr = g(r, "dram__bytes_read.sum", 0.0), g(r, "dram__bytes_write.sum", 0.0)
-    ub = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd *= ub.get(units[col["dram__bytes_read.sum"]], 1)
     wr *= ub.get(units[col["dram__bytes_write.sum"]], 1)
     l2 = g(r, "lts__t_sector_hit_rate.pct")
     traffic[fam(name)].append(rd + wr)
     short = name.split("(")[0].replace("void ", "").replace("<unnamed>::", "")[:60]
-    lines.append(f"| {n} | `{short}` | {r[col['Grid Size']]} | {t:.2f} | {tens:.1f} | {dram_pct:.1f} | {rd + wr:.3g} | {l2:.1f} |")
+    a = agg[short]
+    a[0] += 1; a[1] += t; a[2] += tens * t; a[3] += dram_pct * t; a[4] += rd + wr; a[5] += l2 * t
+    if n < 80:
+        lines.append(f"| {n} | `{short}` | {r[col['Grid Size']]} | {t:.2f} | {tens:.1f} | {dram_pct:.1f} | {rd + wr:.3g} | {l2:.1f} |")
+tot = sum(a[1] for a in agg.values())
+top = ["| kernel | launches | share of captured time | mean time (us) | tensor pipe % (time-weighted) | DRAM % (time-weighted) | DRAM bytes / launch | L2 hit % |",
+       "|---|---|---|---|---|---|---|---|"]
+for short, a in sorted(agg.items(), key=lambda kv: -kv[1][1])[:12]:
+    top.append(f"| `{short}` | {a[0]} | {100 * a[1] / tot:.1f} % | {a[1] / a[0]:.2f} | {a[2] / a[1]:.1f} | "
+               f"{a[3] / a[1]:.1f} | {a[4] / a[0]:.3g} | {a[5] / a[1]:.1f} |")
 out = {k: {"bytes_per_launch": sum(v) / len(v), "launches": len(v)} for k, v in traffic.items()}
 os.makedirs("profiles", exist_ok=True)
 with open(f"profiles/r02_kernels_{cfg}.md", "w") as f:
-    f.write(f"# ncu --set full, {cfg} learner step (cold caches per replay: compare shares, not absolutes)\n\n")
-    f.write("tensor pipe % = sm__pipe_tensor_cycles_active_realtime (fraction of the tensor roofline);\n")
-    f.write("DRAM % = gpu__dram_throughput (fraction of the HBM roofline).\n\n")
-    f.write("\n".join(lines) + "\n")
+    f.write(f"# ncu --set full, {cfg} learner step ({len(data)} launches captured; ncu replays each launch with\n"
+            "# cold caches and serialised: compare shares, not absolute times)\n\n")
+    f.write("tensor pipe % = sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active (tensor-pipe busy "
+            "cycles over the active SMs' cycles);\n"
+            "DRAM % = gpu__dram_throughput (fraction of the HBM roofline).\n\n")
+    f.write("## Top kernels by captured time\n\n" + "\n".join(top) + "\n\n")
+    f.write("## First 80 launches\n\n" + "\n".join(lines) + "\n")
 json.dump(out, open("profiles/r02_traffic.json", "w"), indent=1)
-print("\n".join(lines[:60]))
+print("\n".join(top))
