@@ -40,7 +40,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="depth", choices=["gps", "toy", "stress_gps", "depth", "rgbd", "stress", "serx50"])
+    ap.add_argument("--config", default="depth", choices=["gps", "toy", "stress_gps", "depth", "rgbd", "stress", "serx50", "serx101",
+                                                         "serx101_1024"])
     ap.add_argument("--seed", type=int, default=1337)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -132,7 +133,7 @@ def blas_threads():
 
 # The oracle's fp64 NumPy ResNet needs ~0.2 s per frame-step of the Depth agent: its bounded sample
 # keeps the configuration but shortens the rollouts (whole learner steps on E x ORACLE_T[cfg]).
-ORACLE_T = {"depth": 32, "stress": 8, "rgbd": 2, "serx50": 1}
+ORACLE_T = {"depth": 32, "stress": 8, "rgbd": 2, "serx50": 1, "serx101": 1, "serx101_1024": 1}
 
 
 def oracle_steps_per_sec(cfgname, seed, budget_s=15.0, max_steps=None, T=None):
@@ -204,12 +205,15 @@ def run_reference(args, rank, world):
 
 
 def workload_name(cfgname, c):
-    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2, "rgbd": 3, "stress": 4, "serx50": 3}[cfgname]
+    idx = {"toy": 0, "gps": 1, "stress_gps": 1, "depth": 2, "rgbd": 3, "stress": 4, "serx50": 3, "serx101": 3,
+           "serx101_1024": 3}[cfgname]
     net = {"toy": "goal MLP(64, tanh) -> heads",
            "gps": "goal FC + action embedding -> GRU-512 -> heads",
            "depth": "64x64 depth -> ResNet18/2 + GroupNorm -> FC 512; goal FC + action embedding -> LSTM-512 -> heads",
            "serx50": "256x256 RGB-D -> avg-pool -> SE-ResNeXt50/2 (NEXT-3) + GroupNorm -> FC 2048->512; goal FC + "
                      "action embedding -> 2-layer LSTM-512 -> heads",
+           "serx101": "256x256 RGB-D -> avg-pool -> SE-ResNeXt101/2 (NEXT-3) + GroupNorm -> FC 2048->512; goal FC + "
+                      f"action embedding -> 2-layer LSTM-{c['hidden']} -> heads",
            "rgbd": "256x256 RGB-D -> avg-pool -> ResNet50/2 + GroupNorm -> FC 2048->512; goal FC + action embedding "
                    "-> 2-layer LSTM-512 -> heads"}[c["arch"]]
     return (f"configs[{idx}] {cfgname}: {c['E']} envs/GPU x {c['T']} steps, {net}, "
@@ -248,11 +252,12 @@ def main():
     dd.ddppo_set_fwd_planes(ctx, args.fwd_planes)
     dd.ddppo_set_a8_mode(ctx, args.a8)
     c = synth.CONFIGS[args.config]
-    desc = dd.model_desc(c["arch"])
+    desc = dd.model_desc(c["arch"], c["hidden"])
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, args.seed)
-    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, normalize_adv=True)
+    lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], hidden=c["hidden"], params=p0,
+                  normalize_adv=True)
     stream = torch.cuda.current_stream()
     n_roll = 4  # distinct rollouts cycled through (different data every step)
     preempt = None
@@ -397,7 +402,7 @@ def main():
     fam_ms = {k: v[0] for k, v in prof.items()}
     # the dominant kernel: the TMA implicit-GEMM convolution for the visual agents, the GRU
     # recurrence for GPS (sub-families "conv" / "rnn": CUDA events around each launch on its stream)
-    dom = "conv" if c["arch"] in ("depth", "rgbd", "serx50") else "rnn" if c["arch"] == "gps" else "net_fwd"
+    dom = "conv" if c["arch"] in ("depth", "rgbd", "serx50", "serx101") else "rnn" if c["arch"] == "gps" else "net_fwd"
     launches = {k: v[1] for k, v in launches_timed.items()}
     roofline = roofline_for(dom, prof, c, lrn, peaks, prof_steps)
     kernels = kernel_table(prof, c, lrn, peaks, prof_steps)
@@ -497,7 +502,8 @@ def roofline_for(fam, prof, c, lrn, peaks, steps):
     per_launch_s = (ms / 1e3) / max(n, 1)
     achieved = flops / max(ms / 1e3, 1e-12) / 1e12
     kern = {"conv": "tconv_kernel (TMA implicit-GEMM FPROP / DGRAD / WGRAD)",
-            "rnn": "gps_gru_fwd/bwd_kernel" if c["arch"] == "gps" else "lstm_fwd/bwd_kernel"}.get(fam, fam)
+            "rnn": "gps_gru_fwd/bwd_kernel" if c["arch"] == "gps" else
+            "lstm1024_fwd/bwd_kernel" if c["hidden"] == 1024 else "lstm_fwd/bwd_kernel"}.get(fam, fam)
     out = {"bound": "tensor", "kernel": kern, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
            "frac": achieved / bf16, "traffic": _traffic_r02(fam), "launch_us": per_launch_s * 1e6,
            "launches_per_step": n / max(steps, 1), "flops_per_launch": flops / max(n, 1),

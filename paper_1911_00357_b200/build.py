@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libddppo.so")
-SOURCES = ["api.cu", "gae.cu", "loss.cu", "adam.cu", "toy.cu", "gps.cu", "gemm_tc.cu", "lstm.cu", "depth.cu", "igemm.cu", "peer.cu", "tconv.cu", "act.cu"]
+SOURCES = ["api.cu", "gae.cu", "loss.cu", "adam.cu", "toy.cu", "gps.cu", "gemm_tc.cu", "lstm.cu", "lstm_wide.cu", "depth.cu", "igemm.cu", "peer.cu", "tconv.cu", "act.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

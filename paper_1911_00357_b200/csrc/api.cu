@@ -178,7 +178,7 @@ ddppo_status ddppo_workspace_size(const ddppo_model_desc* host_desc, int max_B, 
   if (!host_bytes || build_layout(host_desc, &L) != DDPPO_OK || max_B < 1 || T < 1) return DDPPO_ERR_CONFIG;
   *host_bytes = host_desc->arch == DDPPO_ARCH_TOY_MLP   ? toy_workspace(max_B, T)
                 : host_desc->arch == DDPPO_ARCH_GPS_GRU ? gps_workspace(max_B, T)
-                                                        : depth_workspace(host_desc->arch, max_B, T);
+                                                        : depth_workspace(host_desc->arch, host_desc->hidden, max_B, T);
   return DDPPO_OK;
 }
 

@@ -362,13 +362,14 @@ ddppo_status toy_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
 ddppo_status toy_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                      const float* dlogits, const float* dvalues, float* grad, void* ws, cudaStream_t st);
 
-ddppo_status launch_head_fwd(ddppo_ctx* ctx, const float* Wo, const float* bo, const float* Hs, int S, float* logits,
-                             float* values, cudaStream_t st);
+// Linear(H, A+1) head over Hs [S][H] (H = 512 or 1024)
+ddppo_status launch_head_fwd(ddppo_ctx* ctx, const float* Wo, const float* bo, const float* Hs, int S, int H,
+                             float* logits, float* values, cudaStream_t st);
 ddppo_status launch_head_bwd(ddppo_ctx* ctx, const float* Wo, const float* Hs, const float* dlogits,
-                             const float* dvalues, int S, float* dH, float* dWo, float* dbo, cudaStream_t st);
+                             const float* dvalues, int S, int H, float* dH, float* dWo, float* dbo, cudaStream_t st);
 ddppo_status launch_colsum(ddppo_ctx* ctx, const float* A, int lda, int S, int M, float* out, cudaStream_t st);
 
-size_t depth_workspace(int arch, int max_B, int T);
+size_t depth_workspace(int arch, int hidden, int max_B, int T);
 ddppo_status depth_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
                        float* logits, float* values, void* ws, cudaStream_t st);
 ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, const ddppo_batch& b,
@@ -393,7 +394,17 @@ struct LstmPtrs {
   float4* IFGO;        // [S][512] gate activations (i, f, g, o)
   const float* dH;     // [S][512] dL/dh_t from above
   float* dG;           // [S][2048] dL/d(gate pre-activations)
+  int H = 512;         // hidden size: 512 (lstm.cu, one cluster) or 1024 (lstm_wide.cu, 32 CTAs)
+  // LSTM-1024 only: L2 exchange buffers (lstm_wide_exchange_bytes) and the device error word
+  void* hx = nullptr;
+  float* xpart = nullptr;
+  unsigned* xcnt = nullptr;
+  int* err = nullptr;
 };
+constexpr int kLstmWideCounters = 64;  // 4 forward group counters + 32 backward owner counters
+size_t lstm_wide_exchange_bytes();
+ddppo_status launch_lstm1024_fwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
+ddppo_status launch_lstm1024_bwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
 ddppo_status launch_lstm_fwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
 ddppo_status launch_lstm_bwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
 

@@ -25,7 +25,7 @@
 
 namespace {
 
-constexpr int kH = 512, kG4 = 2048, kXin = 576, kA1 = 5, kGroups = 16, kThreads = 256;
+constexpr int kXin = 576, kA1 = 5, kGroups = 16, kThreads = 256;
 constexpr int kImg = 64;        // Depth input resolution (configs[2])
 constexpr int kImgRgbd = 256;   // RGB-D input resolution (configs[3])
 
@@ -1169,6 +1169,8 @@ struct ConvGN {
 struct Plan {
   bool rgbd = false;
   int F = 0, layers = 1, fc_in = 512, feat_hw = 4;
+  int H = 512, G4 = 2048;     // LSTM hidden size (512, or 1024: lstm_wide.cu) and its 4 gates
+  void* lstm_x = nullptr;     // LSTM-1024 L2 exchange buffers (lstm_wide_exchange_bytes)
   std::vector<ConvGN> convs;  // stem, per block: main-branch convs, [down], compress
   struct Block {
     std::vector<int> main;   // convs of the residual branch (ReLU after all but the last)
@@ -1217,6 +1219,15 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   P.layers = rgbd ? 2 : 1;
   const bool serx = layout_offset(L, "enc.layer1.0.se.fc1.weight") >= 0;  // SE-ResNeXt50/2 (R9)
   P.fc_in = rgbd ? 2048 : 512;
+  {
+    const int i = [&] {
+      for (int k = 0; k < L.n; ++k)
+        if (!strcmp(L.t[k].name, "head.weight")) return k;
+      return -1;
+    }();
+    P.H = i >= 0 ? (int)L.t[i].shape[1] : 512;
+    P.G4 = 4 * P.H;
+  }
   // ResNet50/2 is ~50 layers deep: its input-gradient GEMMs take hi / lo operand planes so that the
   // bf16 rounding does not accumulate along the chain (the earliest layers' gradients stay within
   // north_star's 2e-2); the 20-layer ResNet18/2 chain is within it with single bf16 planes
@@ -1354,18 +1365,19 @@ void make_plan(const ModelLayout& L, bool rgbd, int B, int T_run, void* base, Pl
   P.xin = take((size_t)F * kXin);
   for (int l = 0; l < P.layers; ++l) {
     Plan::Rnn& r = P.rnn[l];
-    r.GI = take((size_t)F * kG4);
-    r.Hs = take((size_t)F * kH);
-    r.Hin = take((size_t)F * kH);
-    r.Cin = take((size_t)F * kH);
-    r.Cs = take((size_t)F * kH);
-    r.IFGO = take((size_t)F * kH * 4);
-    r.dH = take((size_t)F * kH);
-    r.dG = take((size_t)F * kG4);
+    r.GI = take((size_t)F * P.G4);
+    r.Hs = take((size_t)F * P.H);
+    r.Hin = take((size_t)F * P.H);
+    r.Cin = take((size_t)F * P.H);
+    r.Cs = take((size_t)F * P.H);
+    r.IFGO = take((size_t)F * P.H * 4);
+    r.dH = take((size_t)F * P.H);
+    r.dG = take((size_t)F * P.G4);
   }
+  if (P.H != 512) P.lstm_x = take_bytes(lstm_wide_exchange_bytes());
   P.dyb = take_b(max_act);
   P.dwt = take(max_w);
-  P.part_n = std::max({(size_t)kMaxSplits * max_w, (size_t)16 * F * kG4, (size_t)16 * kG4 * kXin});
+  P.part_n = std::max({(size_t)kMaxSplits * max_w, (size_t)16 * F * P.G4, (size_t)16 * P.G4 * std::max(kXin, P.H)});
   P.part = take(P.part_n);
   // side-stream scratch: weight-gradient partials (tconv split-K: at most ~2 work items of 128 x 64 per
   // SM; the stem's per-frame partials) and the LSTM / visual-FC weight-gradient GEMMs' partials
@@ -1769,7 +1781,10 @@ ddppo_status gemm_split(ddppo_ctx* ctx, GemmTC g, const Plan& P, cudaStream_t st
   const int bn = g.N <= 32 ? 32 : (g.N <= 64 || g.prec == 3) ? 64 : 128;
   const long long tiles = (long long)((g.N + bn - 1) / bn) * ((g.M + 127) / 128);
   const int chunks = (g.K + 63) / 64;
-  const int splits = (int)std::max(1LL, std::min<long long>({(2LL * ctx->sm_count + tiles - 1) / tiles, chunks / 2, 16}));
+  // split-K toward one wave of CTAs, >= 2 K chunks per split (measured r2: 2x the SM count or
+  // >= 4 chunks per split are 0.4-1.1 % slower per Depth step; no split 6 % slower)
+  const int splits =
+      (int)std::max(1LL, std::min<long long>({((long long)ctx->sm_count + tiles - 1) / tiles, chunks / 2, 16}));
   if (splits > 1) {
     g.splits = splits;
     g.partial = part ? part : P.part;
@@ -1790,9 +1805,15 @@ LstmPtrs lstm_ptrs(const ModelLayout& L, const float* prm, const ddppo_batch& b,
   q.bhh = prm + off_of(L, rnn_name(P, "rnn.bias_hh", l));
   q.GI = r.GI;
   q.mask = b.mask;
-  q.h0 = b.h0 + (size_t)l * kH;
-  q.c0 = b.c0 + (size_t)l * kH;
-  q.sld = P.layers * kH;
+  q.h0 = b.h0 + (size_t)l * P.H;
+  q.c0 = b.c0 + (size_t)l * P.H;
+  q.sld = P.layers * P.H;
+  q.H = P.H;
+  if (P.lstm_x) {
+    q.hx = P.lstm_x;
+    q.xcnt = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(P.lstm_x) + lstm_wide_exchange_bytes() - 256);
+    q.xpart = reinterpret_cast<float*>(reinterpret_cast<char*>(P.lstm_x) + 2 * (size_t)(P.H / 8) * 128);
+  }
   q.env_idx = b.env_idx;
   q.B = b.B;
   q.T_run = b.T_run;
@@ -1811,7 +1832,7 @@ bool is_rgbd(const ModelLayout& L) { return layout_offset(L, "rnn.weight_ih_l0")
 
 }  // namespace
 
-// h_t / c_t of LSTM layer l for every sample [B*T_run][512] in a forward's workspace (act path)
+// h_t / c_t of LSTM layer l for every sample [B*T_run][hidden] in a forward's workspace (act path)
 void depth_state_out(const ModelLayout& L, void* ws, int B, int T_run, int l, const float** Hs, const float** Cs) {
   Plan P;
   make_plan(L, is_rgbd(L), B, T_run, ws, &P);
@@ -1819,10 +1840,10 @@ void depth_state_out(const ModelLayout& L, void* ws, int B, int T_run, int l, co
   *Cs = P.rnn[l].Cs;
 }
 
-size_t depth_workspace(int arch, int max_B, int T) {
+size_t depth_workspace(int arch, int hidden, int max_B, int T) {
   ddppo_model_desc d = {};
   d.arch = arch;
-  d.hidden = 512;
+  d.hidden = hidden;
   d.num_actions = 4;
   ModelLayout L;
   build_layout(&d, &L);
@@ -1913,9 +1934,9 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
   for (int l = 0; l < P.layers; ++l) {
     // GI = x W_ih^T (biases are added inside the recurrence); layer l > 0 reads layer l-1's h
     const float* xl = l == 0 ? P.xin : P.rnn[l - 1].Hs;
-    const int nin = l == 0 ? kXin : kH;
+    const int nin = l == 0 ? kXin : P.H;
     if ((s = gemm_split(ctx, GemmTC{xl, nin, 1, prm + off_of(L, rnn_name(P, "rnn.weight_ih", l)), nin, 1, P.rnn[l].GI,
-                                    kG4, F, kG4, nin, 1, nullptr, kPrecFwd},
+                                    P.G4, F, P.G4, nin, 1, nullptr, kPrecFwd},
                         P, st)) != DDPPO_OK)
       return s;
     if ((s = launch_lstm_fwd(ctx, lstm_ptrs(L, prm, b, P, l), st)) != DDPPO_OK) return s;
@@ -1940,7 +1961,7 @@ ddppo_status depth_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   }
   ProfScope ps(ctx, DDPPO_K_HEAD, st, 0);
   return launch_head_fwd(ctx, prm + off_of(L, "head.weight"), prm + off_of(L, "head.bias"), P.rnn[P.layers - 1].Hs,
-                         P.F, logits, values, st);
+                         P.F, P.H, logits, values, st);
 }
 
 ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, const ddppo_batch& b,
@@ -1951,7 +1972,7 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   ddppo_status s;
   {
     ProfScope ps(ctx, DDPPO_K_HEAD, st, 0);
-    s = launch_head_bwd(ctx, prm + off_of(L, "head.weight"), P.rnn[P.layers - 1].Hs, dlogits, dvalues, F,
+    s = launch_head_bwd(ctx, prm + off_of(L, "head.weight"), P.rnn[P.layers - 1].Hs, dlogits, dvalues, F, P.H,
                         P.rnn[P.layers - 1].dH, grad + off_of(L, "head.weight"), grad + off_of(L, "head.bias"), st);
     if (s != DDPPO_OK) return s;
   }
@@ -1969,7 +1990,8 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     if ((s = launch_lstm_bwd(ctx, lstm_ptrs(L, prm, b, P, l), st)) != DDPPO_OK) return s;
     // weight gradients and db (b_ih and b_hh receive the same gradient)
     const float* xl = l == 0 ? P.xin : P.rnn[l - 1].Hs;
-    const int nin = l == 0 ? kXin : kH;
+    const int nin = l == 0 ? kXin : P.H;
+    const int kG4 = P.G4, kH = P.H;
     const float* Wih = prm + off_of(L, rnn_name(P, "rnn.weight_ih", l));
     if (wst != st) DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, wst));
     if ((s = gemm_split(ctx, GemmTC{r.dG, 1, kG4, xl, 1, nin, grad + off_of(L, rnn_name(P, "rnn.weight_ih", l)), nin,

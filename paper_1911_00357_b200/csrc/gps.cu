@@ -811,15 +811,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1) gps_gru_bwd_kernel(GpsPtrs p) 
 
 // ------------------------------------------------------------------ head (Linear(512, 5)) fwd/bwd
 __global__ void head_fwd_kernel(const float* __restrict__ Wo, const float* __restrict__ bo, const float* __restrict__ Hs,
-                                int S, float* __restrict__ logits, float* __restrict__ values) {
+                                int S, int H, float* __restrict__ logits, float* __restrict__ values) {
   const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
   for (int s = blockIdx.x * warps + (threadIdx.x >> 5); s < S; s += gridDim.x * warps) {
-    const float* h = Hs + (size_t)s * kH;
+    const float* h = Hs + (size_t)s * H;
     float acc[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int k = lane; k < kH; k += 32) {
+    for (int k = lane; k < H; k += 32) {
       const float hv = h[k];
 #pragma unroll
-      for (int o = 0; o < kA1; ++o) acc[o] += Wo[o * kH + k] * hv;
+      for (int o = 0; o < kA1; ++o) acc[o] += Wo[o * H + k] * hv;
     }
 #pragma unroll
     for (int o = 0; o < kA1; ++o) acc[o] = warp_sum(acc[o]);
@@ -833,13 +833,13 @@ __global__ void head_fwd_kernel(const float* __restrict__ Wo, const float* __res
 
 // dH[s][k] = sum_o Wo[o][k] dout[s][o]
 __global__ void head_dgrad_kernel(const float* __restrict__ Wo, const float* __restrict__ dlogits,
-                                  const float* __restrict__ dvalues, int S, float* __restrict__ dH) {
-  const size_t n = (size_t)S * kH;
+                                  const float* __restrict__ dvalues, int S, int H, float* __restrict__ dH) {
+  const size_t n = (size_t)S * H;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int s = (int)(i / kH), k = (int)(i % kH);
+    const int s = (int)(i / H), k = (int)(i % H);
     const float4 dl = *reinterpret_cast<const float4*>(dlogits + (size_t)s * 4);
-    dH[i] = Wo[k] * dl.x + Wo[kH + k] * dl.y + Wo[2 * kH + k] * dl.z + Wo[3 * kH + k] * dl.w +
-            Wo[4 * kH + k] * dvalues[s];
+    dH[i] = Wo[k] * dl.x + Wo[H + k] * dl.y + Wo[2 * H + k] * dl.z + Wo[3 * H + k] * dl.w +
+            Wo[4 * H + k] * dvalues[s];
   }
 }
 
@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ A
 // dWo[o][k] = sum_s dout[s][o] Hs[s][k] (32 k per CTA x 8 sample chunks); CTA 0 also does dbo.
 __global__ void __launch_bounds__(256) head_wgrad_kernel(const float* __restrict__ Hs,
                                                          const float* __restrict__ dlogits,
-                                                         const float* __restrict__ dvalues, int S,
+                                                         const float* __restrict__ dvalues, int S, int H,
                                                          float* __restrict__ dWo, float* __restrict__ dbo) {
   __shared__ float part[kRedChunks][kA1][33];
   const int kk = threadIdx.x & 31, q = threadIdx.x >> 5, k = blockIdx.x * 32 + kk;
@@ -876,7 +876,7 @@ __global__ void __launch_bounds__(256) head_wgrad_kernel(const float* __restrict
   float a[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f}, bsum[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll 8
   for (int s = q * per; s < min(S, (q + 1) * per); ++s) {
-    const float h = Hs[(size_t)s * kH + k];
+    const float h = Hs[(size_t)s * H + k];
     const float4 dl = *reinterpret_cast<const float4*>(dlogits + (size_t)s * 4);
     const float dv = dvalues[s];
     a[0] += dl.x * h;
@@ -899,7 +899,7 @@ __global__ void __launch_bounds__(256) head_wgrad_kernel(const float* __restrict
       float t = 0.f;
 #pragma unroll
       for (int i = 0; i < kRedChunks; ++i) t += part[i][o][kk];
-      dWo[o * kH + k] = t;
+      dWo[o * H + k] = t;
     }
   }
   if (blockIdx.x == 0) {  // biases: chunk partials (identical for every kk) in chunk order
@@ -1067,7 +1067,7 @@ ddppo_status gps_fwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   }
   if (skip_head) return DDPPO_OK;  // the learner runtime fuses head + loss + head input gradient
   ProfScope ps(ctx, DDPPO_K_HEAD, st, 1);
-  head_fwd_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, p.bo, p.Hs, S, logits, values);
+  head_fwd_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, p.bo, p.Hs, S, kH, logits, values);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
@@ -1124,9 +1124,9 @@ ddppo_status gps_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* params, 
   {
     ProfScope ps(ctx, DDPPO_K_HEAD, st, dh_ready ? 1 : 2);
     if (!dh_ready)
-      head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, dlogits, dvalues, S, p.dH);
+      head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(p.Wo, dlogits, dvalues, S, kH, p.dH);
     DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, sa));
-    head_wgrad_kernel<<<kH / 32, 256, 0, sa>>>(p.Hs, dlogits, dvalues, S, grad + layout_offset(L, "head.weight"),
+    head_wgrad_kernel<<<kH / 32, 256, 0, sa>>>(p.Hs, dlogits, dvalues, S, kH, grad + layout_offset(L, "head.weight"),
                                               grad + layout_offset(L, "head.bias"));
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   }
@@ -1173,18 +1173,19 @@ extern "C" int ddppo_debug_trace_bwd(long long* host, int n) {
 #endif
 
 // ------------------------------------------------------------------ shared launchers (used by depth.cu)
-ddppo_status launch_head_fwd(ddppo_ctx* ctx, const float* Wo, const float* bo, const float* Hs, int S, float* logits,
-                             float* values, cudaStream_t st) {
-  head_fwd_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(Wo, bo, Hs, S, logits, values);
+ddppo_status launch_head_fwd(ddppo_ctx* ctx, const float* Wo, const float* bo, const float* Hs, int S, int H,
+                             float* logits, float* values, cudaStream_t st) {
+  head_fwd_kernel<<<grid_for(S, 8, ctx->sm_count * 4), 256, 0, st>>>(Wo, bo, Hs, S, H, logits, values);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
 
 ddppo_status launch_head_bwd(ddppo_ctx* ctx, const float* Wo, const float* Hs, const float* dlogits,
-                             const float* dvalues, int S, float* dH, float* dWo, float* dbo, cudaStream_t st) {
-  head_dgrad_kernel<<<grid_for(S * kH, 256, ctx->sm_count * 4), 256, 0, st>>>(Wo, dlogits, dvalues, S, dH);
-  head_wgrad_kernel<<<kH / 32, 256, 0, st>>>(Hs, dlogits, dvalues, S, dWo, dbo);
+                             const float* dvalues, int S, int H, float* dH, float* dWo, float* dbo,
+                             cudaStream_t st) {
+  head_dgrad_kernel<<<grid_for(S * H, 256, ctx->sm_count * 4), 256, 0, st>>>(Wo, dlogits, dvalues, S, H, dH);
+  head_wgrad_kernel<<<H / 32, 256, 0, st>>>(Hs, dlogits, dvalues, S, H, dWo, dbo);
   ctx->count(2);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;

@@ -417,14 +417,26 @@ ddppo_status launch_cluster16(ddppo_ctx* ctx, K kernel, size_t smem, const LstmP
 // recurrent FLOPs per launch: the W_hh contraction of every step, 2 * B * T * 4H * H
 ddppo_status launch_lstm_fwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st) {
   DDPPO_REQUIRE(ctx, p.B >= 1 && p.B <= kBMax && p.T_run >= 1 && p.T_run <= 1024, "lstm: 1..8 envs, T <= 1024");
+  DDPPO_REQUIRE(ctx, p.H == 512 || p.H == 1024, "lstm: hidden 512 or 1024");
   ProfScope ps(ctx, DDPPO_K_RNN, st, 0);
-  if (ctx->prof) ctx->flops[DDPPO_K_RNN] += 2.0 * p.B * p.T_run * 4.0 * kH * kH;
+  if (ctx->prof) ctx->flops[DDPPO_K_RNN] += 2.0 * p.B * p.T_run * 4.0 * p.H * p.H;
+  if (p.H == 1024) {
+    LstmPtrs q = p;
+    q.err = ctx->d_err;
+    return launch_lstm1024_fwd(ctx, q, st);
+  }
   return launch_cluster16(ctx, lstm_fwd_kernel, sizeof(FwdSmem) + (size_t)p.B * p.T_run * sizeof(float), p, st);
 }
 
 ddppo_status launch_lstm_bwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st) {
   DDPPO_REQUIRE(ctx, p.B >= 1 && p.B <= kBMax && p.T_run >= 1 && p.T_run <= 1024, "lstm: 1..8 envs, T <= 1024");
+  DDPPO_REQUIRE(ctx, p.H == 512 || p.H == 1024, "lstm: hidden 512 or 1024");
   ProfScope ps(ctx, DDPPO_K_RNN, st, 0);
-  if (ctx->prof) ctx->flops[DDPPO_K_RNN] += 2.0 * p.B * p.T_run * 4.0 * kH * kH;
+  if (ctx->prof) ctx->flops[DDPPO_K_RNN] += 2.0 * p.B * p.T_run * 4.0 * p.H * p.H;
+  if (p.H == 1024) {
+    LstmPtrs q = p;
+    q.err = ctx->d_err;
+    return launch_lstm1024_bwd(ctx, q, st);
+  }
   return launch_cluster16(ctx, lstm_bwd_kernel, sizeof(BwdSmem) + (size_t)p.B * p.T_run * sizeof(float), p, st);
 }

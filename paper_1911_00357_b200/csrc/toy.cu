@@ -50,7 +50,9 @@ ddppo_status build_layout(const ddppo_model_desc* d, ModelLayout* out) {
     add_tensor(&L, "head.bias", 1, hb, (int)H);
   } else if (d->arch == DDPPO_ARCH_DEPTH_R18_LSTM || d->arch == DDPPO_ARCH_RGBD_R50_LSTM2 ||
              d->arch == DDPPO_ARCH_RGBD_SERX50_LSTM2 || d->arch == DDPPO_ARCH_RGBD_SERX101_LSTM2) {
-    if (d->hidden != 512) return DDPPO_ERR_CONFIG;
+    // LSTM 512 (one 16-CTA cluster, lstm.cu) or 1024 ("512-dimensional or 1024-dimensional",
+    // 32 CTAs exchanging through L2, lstm_wide.cu)
+    if (d->hidden != 512 && d->hidden != 1024) return DDPPO_ERR_CONFIG;
     const bool serx = d->arch == DDPPO_ARCH_RGBD_SERX50_LSTM2 || d->arch == DDPPO_ARCH_RGBD_SERX101_LSTM2;
     const bool r101 = d->arch == DDPPO_ARCH_RGBD_SERX101_LSTM2;
     const bool rgbd = d->arch == DDPPO_ARCH_RGBD_R50_LSTM2 || serx;

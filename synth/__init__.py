@@ -41,6 +41,9 @@ CONFIGS = {
     # NEXT-3: the RGB-D agent with the half-width SE-ResNeXt50 encoder (reading R9)
     "serx50": dict(arch="serx50", E=4, T=128, epochs=2, minibatches=2, hidden=512, obs=(4, 256, 256), rnn_layers=2),
     "serx101": dict(arch="serx101", E=4, T=128, epochs=2, minibatches=2, hidden=512, obs=(4, 256, 256), rnn_layers=2),
+    # NEXT-3: the paper's best agent, SE-ResNeXt101 + 2-layer 1024-d LSTM
+    "serx101_1024": dict(arch="serx101", E=4, T=128, epochs=2, minibatches=2, hidden=1024, obs=(4, 256, 256),
+                         rnn_layers=2),
     "stress": dict(arch="depth", E=16, T=128, epochs=2, minibatches=2, hidden=512, obs=(1, 64, 64),
                    preempt_p=60),
 }

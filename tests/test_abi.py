@@ -35,12 +35,15 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("arch", ["toy", "gps", "depth", "rgbd", "serx50", "serx101"])
-def test_layout_matches_oracle(arch):
-    lay = dd.param_layout(dd.model_desc(arch))
-    offs, P = models.offsets(arch)
-    assert dd.param_count(dd.model_desc(arch)) == P
-    ref = models.layout(arch)
+@pytest.mark.parametrize("arch,hidden", [("toy", None), ("gps", None), ("depth", None), ("rgbd", None),
+                                         ("serx50", None), ("serx101", None),
+                                         ("depth", 1024), ("serx101", 1024)])  # NEXT-3's 1024-d LSTM
+def test_layout_matches_oracle(arch, hidden):
+    kw = {} if hidden is None else {"hidden": hidden}
+    lay = dd.param_layout(dd.model_desc(arch, hidden))
+    offs, P = models.offsets(arch, **kw)
+    assert dd.param_count(dd.model_desc(arch, hidden)) == P
+    ref = models.layout(arch, **kw)
     assert [n for n, *_ in lay] == [n for n, _, _ in ref]
     for (name, off, shape, fan), (rname, rshape, rfan) in zip(lay, ref):
         assert off == offs[name][0] and tuple(shape) == tuple(rshape) and fan == rfan
@@ -49,6 +52,10 @@ def test_layout_matches_oracle(arch):
 def test_bad_descriptor_rejected():
     with pytest.raises(dd.DdppoError):
         dd.param_count(dd.model_desc("gps", hidden=256))
+    with pytest.raises(dd.DdppoError):  # the GRU agent is built for 512 only
+        dd.param_count(dd.model_desc("gps", hidden=1024))
+    with pytest.raises(dd.DdppoError):
+        dd.param_count(dd.model_desc("depth", hidden=768))
 
 
 def test_preempt_threshold_and_decide_match_oracle():

@@ -276,8 +276,8 @@ VISUAL = {"depth": dict(obs=(1, 64, 64), layers=1), "rgbd": dict(obs=(4, 256, 25
           "serx50": dict(obs=(4, 256, 256), layers=2), "serx101": dict(obs=(4, 256, 256), layers=2)}
 
 
-def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
-    desc = dd.model_desc(arch)
+def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None, hidden=None):
+    desc = dd.model_desc(arch, hidden)
     H = desc.hidden
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
@@ -310,19 +310,19 @@ def _net_case(dd, ctx, arch, E, T, B, seed, lengths=None):
         ob.update(obs=ro["obs"][env_idx, :T_run], c0=ro["c0"][env_idx])
     lo, vo, cache = models.forward(arch, params, ob, hidden=H)
     if vis:
-        _adopt_decisions(arch, params, ob, cache, dec, B * T_run)
+        _adopt_decisions(arch, params, ob, cache, dec, B * T_run, hidden=H)
     go = models.backward(arch, params, cache, dl.astype(np.float64), dv.astype(np.float64), hidden=H)
     return lay, lg.cpu().numpy(), vl.cpu().numpy(), grad.cpu().numpy(), lo, vo, go
 
 
-def _adopt_decisions(arch, params, ob, cache, dec, F, tie=2.5e-4):
+def _adopt_decisions(arch, params, ob, cache, dec, F, tie=2.5e-4, hidden=512):
     """Hand the oracle's backward the kernel forward's ReLU masks / max-pool argmax (reading R6):
     every decision the two sides take differently must be a near-tie in the oracle's fp64
     forward (|pre-activation| <= tie * rms of its layer; pool: within tie of the window max),
     i.e. a case where both choices are correct; everything else must agree exactly.  tie = 2.5e-4
     ~ 16 * 2^-16: the forward GEMMs' bf16x3 products carry ~16-bit mantissas, summed over up to 2304
     terms and divided by the GroupNorm sigma (R6)."""
-    p = models.unpack(arch, params)
+    p = models.unpack(arch, params, hidden=hidden)
     x = np.asarray(ob["obs"], np.float64).reshape((F,) + ob["obs"].shape[2:])
     enc = cache["enc"]
     off = [0]
@@ -429,6 +429,22 @@ def test_gps_network_parity(dd, ctx, E, T, B, lengths):
                                            (16, 4, 8, [4, 1, 3, 4, 2, 4, 4, 1, 3, 4, 4, 2, 1, 4, 3, 4])])
 def test_depth_network_parity(dd, ctx, E, T, B, lengths):
     lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, "depth", E, T, B, 40 + E + T, lengths)
+    assert rel_l2(lg, lo) < 1e-3 and rel_l2(vl, vo) < 1e-3, (rel_l2(lg, lo), rel_l2(vl, vo))
+    bad = []
+    for name, off, shape, _ in lay:
+        n = int(np.prod(shape))
+        e = rel_l2(g[off:off + n], go[off:off + n])
+        if not e < 2e-2:
+            bad.append((name, e))
+    assert not bad, bad
+
+
+# NEXT-3's 1024-d LSTM (lstm_wide.cu: 32 CTAs exchanging h / partials through L2) on the
+# Depth encoder (a cheap oracle), single env to eight envs per minibatch, ragged lengths
+@pytest.mark.parametrize("E,T,B,lengths", [(2, 20, 2, [20, 9]), (4, 6, 4, [6, 2, 5, 6]), (8, 5, 8, None),
+                                           (3, 7, 1, None)])
+def test_depth_lstm1024_network_parity(dd, ctx, E, T, B, lengths):
+    lay, lg, vl, g, lo, vo, go = _net_case(dd, ctx, "depth", E, T, B, 70 + E + T, lengths, hidden=1024)
     assert rel_l2(lg, lo) < 1e-3 and rel_l2(vl, vo) < 1e-3, (rel_l2(lg, lo), rel_l2(vl, vo))
     bad = []
     for name, off, shape, _ in lay:
