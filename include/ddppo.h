@@ -114,7 +114,11 @@ ddppo_status ddppo_adv_norm(ddppo_ctx* ctx, double* stats3, float eps, float* me
  *        visual_fc.bias, goal_fc.*, act_embed.*, rnn.{weight_ih,weight_hh,bias_ih,bias_hh}_l{0,1}
  *        (weight_ih_l0 [4H][576], weight_ih_l1 [4H][H]), head.*
  * head rows 0..A-1 are the action logits, row A the value.  num_actions must be 4;
- * GPS requires hidden == 512. */
+ * GPS requires hidden == 512; the visual agents take hidden 512 or 1024 (NEXT-3: "a 2-layer LSTM
+ * with either a 512-dimensional or 1024-dimensional hidden dimension", P:L593 -- the best agent of
+ * P:L334 is SE-ResNeXt101 + 1024-d LSTM).  hidden 1024 runs 32-CTA recurrences that exchange
+ * through L2 (lstm_wide.cu); it needs 32 SMs free at once while a recurrence runs (a timeout of the
+ * bounded exchange waits sets the device error word: ddppo_check returns DDPPO_ERR_COMM). */
 typedef enum {
   DDPPO_ARCH_TOY_MLP = 0, DDPPO_ARCH_GPS_GRU = 1, DDPPO_ARCH_DEPTH_R18_LSTM = 2, DDPPO_ARCH_RGBD_R50_LSTM2 = 3,
   /* NEXT-3: the RGB-D agent with the half-width SE-ResNeXt50 encoder --
@@ -126,7 +130,7 @@ typedef enum {
 
 typedef struct {
   int32_t arch;        /* ddppo_arch */
-  int32_t hidden;      /* 64 (toy) / 512 (gps, depth) */
+  int32_t hidden;      /* 64 (toy) / 512 (gps) / 512 or 1024 (visual agents) */
   int32_t num_actions; /* 4 */
   int32_t reserved[5];
 } ddppo_model_desc;

@@ -17,6 +17,7 @@ constexpr int kThreads = 256;
 __global__ void __launch_bounds__(kThreads)
 grad_norm_kernel(const float* __restrict__ g, int64_t P, float inv_world, float max_norm, double* partials,
                  unsigned int* counter, float* scalars, float* grad_norm_out, int* err) {
+  pdl_enter();
   __shared__ double red[kThreads / 32];
   __shared__ double fin[1];
   double acc[1] = {0.0};
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(kThreads)
 adam_kernel(const float* __restrict__ g, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
             const uint8_t* __restrict__ freeze, int64_t P, const float* __restrict__ scalars, float b1, float b2,
             float lr, const int* __restrict__ dstep, int step_add, float eps, const int* err, int64_t frz_end) {
+  pdl_enter();
   __shared__ float sbc[2];
   // a failed peer exchange (ERR_BIT_COMM) or a non-finite gradient norm (ERR_BIT_GRAD) leaves
   // the parameters untouched until ddppo_check reports it
@@ -110,7 +112,8 @@ ddppo_status launch_adam_only(ddppo_ctx* ctx, const float* grad, float* params, 
   DDPPO_REQUIRE(ctx, frz_end % 4 == 0 && frz_end <= P, "adam: frozen prefix must be a multiple of 4");
   const int blocks = grid_for((int)std::min<int64_t>((P + 3) / 4, 1 << 30), kThreads, ctx->sm_count * 4);
   ProfScope ps(ctx, DDPPO_K_ADAM, st, 1);
-  adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
+  launch_k(ctx, adam_kernel, blocks, kThreads, 0, st, grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1,
+           cfg.beta2,
                                            cfg.lr, dstep, step_add, cfg.eps, ctx->d_err, frz_end);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
@@ -127,10 +130,11 @@ ddppo_status launch_clip_adam(ddppo_ctx* ctx, float* grad, float* params, float*
   DDPPO_REQUIRE(ctx, frz_end % 4 == 0 && frz_end <= P, "adam: frozen prefix must be a multiple of 4");
   const int blocks = grid_for((int)std::min<int64_t>((P + 3) / 4, 1 << 30), kThreads, ctx->sm_count * 4);
   ProfScope ps(ctx, DDPPO_K_ADAM, st, 2);
-  grad_norm_kernel<<<blocks, kThreads, 0, st>>>(grad, P, inv_world, cfg.max_grad_norm, ctx->d_partials,
+  launch_k(ctx, grad_norm_kernel, blocks, kThreads, 0, st, grad, P, inv_world, cfg.max_grad_norm, ctx->d_partials,
                                                 ctx->d_counters + CNT_NORM, ctx->d_scalars, grad_norm, ctx->d_err);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
-  adam_kernel<<<blocks, kThreads, 0, st>>>(grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1, cfg.beta2,
+  launch_k(ctx, adam_kernel, blocks, kThreads, 0, st, grad, params, m, v, freeze, P, ctx->d_scalars, cfg.beta1,
+           cfg.beta2,
                                            cfg.lr, dstep, step_add, cfg.eps, ctx->d_err, frz_end);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
@@ -147,6 +151,7 @@ __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
 __global__ void reinit_critic_kernel(float* __restrict__ w_row, float* __restrict__ b_elem, float* __restrict__ mw,
                                      float* __restrict__ vw, float* __restrict__ mb, float* __restrict__ vb, int fan_in,
                                      uint64_t seed) {
+  pdl_enter();
   const float bound = 1.0f / sqrtf((float)fan_in);
   for (int i = threadIdx.x; i <= fan_in; i += blockDim.x) {
     const uint64_t u = splitmix64(seed * 0x9E3779B97F4A7C15ull + (uint64_t)i) >> 40;  // 24 random bits
@@ -177,7 +182,8 @@ extern "C" ddppo_status ddppo_reinit_critic(ddppo_ctx* ctx, const ddppo_model_de
     if (strcmp(L.t[i].name, "head.weight") == 0) fan_in = (int)L.t[i].shape[1];
   const int64_t row = hw + (int64_t)A * fan_in, bi = hb + A;
   cudaStream_t st = as_stream(stream);
-  reinit_critic_kernel<<<1, 256, 0, st>>>(params + row, params + bi, m + row, v + row, m + bi, v + bi, fan_in, seed);
+  launch_k(ctx, reinit_critic_kernel, 1, 256, 0, st, params + row, params + bi, m + row, v + row, m + bi, v + bi,
+           fan_in, seed);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;

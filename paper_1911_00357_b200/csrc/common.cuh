@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/ddppo.h"
@@ -41,6 +42,8 @@ struct ddppo_ctx {
   int conv_engine = DDPPO_CONV_TMA;     // ddppo_set_conv_engine
   int fwd_planes = 2;                   // ddppo_set_fwd_planes: encoder forward operands bf16x3 (2) / bf16 (1)
   bool tconv_bn64 = getenv("DDPPO_TCONV_BN128") == nullptr;  // A/B switch for the conv kernel's N tile
+  // programmatic dependent launch of the learner step's kernels (launch_k); DDPPO_PDL=0: plain launches
+  bool pdl = getenv("DDPPO_PDL") == nullptr || atoi(getenv("DDPPO_PDL")) != 0;
   int* d_tile_cnt = nullptr;            // split-K tile arrival counters (tconv.cu), zero between kernels
   // learner runtime: Adam update count on the device; captured CUDA graph of the last learner step
   int* d_step = nullptr;
@@ -106,6 +109,32 @@ constexpr int kMaxCountVals = 64;
 constexpr int kMaxTileCounters = 1 << 16;
 
 enum { ERR_BIT_LOSS = 1, ERR_BIT_GRAD = 2, ERR_BIT_COMM = 4 };
+
+// Programmatic dependent launch (PDL).  Kernels of the learner step are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (launch_k), so a kernel's CTAs are scheduled
+// while its predecessor in the stream is still draining; every such kernel starts with pdl_enter():
+// griddepcontrol.wait (block until the predecessor grid has completed and its memory is visible --
+// nothing of the predecessor's output is touched before it), then griddepcontrol.launch_dependents
+// (let the successor be scheduled now).  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(const ddppo_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = ctx->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 #define DDPPO_CUDA_TRY(ctx, expr)                                                 \
   do {                                                                            \

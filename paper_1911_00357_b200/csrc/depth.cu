@@ -33,6 +33,7 @@ constexpr int kImgRgbd = 256;   // RGB-D input resolution (configs[3])
 // obs [E][T][1][64][64] bf16 (gathered through env_idx) -> x0 [F][64][64][1] fp32 (the SIMT stem's input)
 __global__ void gather_obs_kernel(const __nv_bfloat16* __restrict__ obs, const int32_t* __restrict__ env_idx, int T,
                                   int T_run, int F, float* __restrict__ x0) {
+  pdl_enter();
   const size_t per = (size_t)kImg * kImg / 8;  // 8 pixels (16 bytes) per item
   const size_t n = (size_t)F * per;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -55,6 +56,7 @@ __constant__ float kRgbStd[3] = {0.229f * 255.f, 0.224f * 255.f, 0.225f * 255.f}
 __global__ void rgbd_prologue_kernel(const uint8_t* __restrict__ rgb, const __nv_bfloat16* __restrict__ depth,
                                      const int32_t* __restrict__ env_idx, int T, int T_run, int F, int Hin,
                                      float* __restrict__ x0, __nv_bfloat16* __restrict__ x0b) {
+  pdl_enter();
   // thread = (frame, output row, pair of output columns): 4 input columns of 2 rows per channel
   const int Ho = Hin / 2, Wo = Hin / 2, WP = Wo / 2;
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
@@ -111,6 +113,7 @@ __global__ void rgbd_prologue_kernel(const uint8_t* __restrict__ rgb, const __nv
 //   Wd [Ci][(u, v, o)] bf16                                                (input-gradient B operand)
 __global__ void weights_bf16_kernel(const float* __restrict__ W, int Co, int Ci, int k, __nv_bfloat16* __restrict__ wr,
                                     __nv_bfloat16* __restrict__ wd) {
+  pdl_enter();
   const int n = Co * Ci * k * k;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int o = i / (Ci * k * k), rem = i % (Ci * k * k);
@@ -130,7 +133,8 @@ __global__ void weights_bf16_kernel(const float* __restrict__ W, int Co, int Ci,
 constexpr int kMaxConvs = 128;
 struct WeightPrep {
   int n;
-  int off[kMaxConvs + 1];
+  int off[kMaxConvs + 1];   // prefix sums of the Wr block counts (Co per convolution)
+  int offd[kMaxConvs + 1];  // prefix sums of the Wd block counts (Ci per convolution; 0 without wd)
   struct Item {
     const float* W;
     __nv_bfloat16 *wr, *wd;  // wd nullable (no input gradient)
@@ -139,36 +143,59 @@ struct WeightPrep {
     int groups;              // > 1: W is grouped [Co][Ci/groups][k][k]; the dense operand is block diagonal
   } it[kMaxConvs];
 };
-__global__ void weights_prep_kernel(const WeightPrep prep) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= prep.off[prep.n]) return;
-  int lo = 0, hi_i = prep.n - 1;  // the convolution holding g: off[lo] <= g < off[lo + 1]
+// W[o][c][uv] of convolution t as a dense [Co][Ci] operand entry (0 off the block diagonal of a grouped conv)
+__device__ __forceinline__ float prep_weight(const WeightPrep::Item& t, int o, int c, int uv, int kk) {
+  if (t.groups > 1) {
+    const int cgi = t.Ci / t.groups, cgo = t.Co / t.groups;
+    return c / cgi == o / cgo ? t.W[(o * cgi + c % cgi) * kk + uv] : 0.f;
+  }
+  return c < t.Ci ? t.W[(o * t.Ci + c) * kk + uv] : 0.f;
+}
+__device__ __forceinline__ int prep_item(const int* off, int n, int g) {  // off[lo] <= g < off[lo + 1]
+  int lo = 0, hi_i = n - 1;
   while (lo < hi_i) {
     const int mid = (lo + hi_i + 1) >> 1;
-    if (prep.off[mid] <= g) lo = mid;
+    if (off[mid] <= g) lo = mid;
     else hi_i = mid - 1;
   }
-  const WeightPrep::Item& t = prep.it[lo];
-  const int Co = t.Co, Ci = t.Ci, Cp = t.Cp, kk = t.k * t.k, n = Co * Cp * kk;
-  const int j = g - prep.off[lo];  // Wr index
-  const int o = j / (kk * Cp), rem = j - o * (kk * Cp), uv = rem / Cp, c = rem - uv * Cp;
-  float w = 0.f;
-  if (t.groups > 1) {
-    const int cgi = Ci / t.groups, cgo = Co / t.groups;
-    if (c / cgi == o / cgo) w = t.W[(o * cgi + c % cgi) * kk + uv];
-  } else if (c < Ci) {
-    w = t.W[(o * Ci + c) * kk + uv];
-  }
-  const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-  t.wr[j] = hi;
-  t.wr[n + j] = __float2bfloat16_rn(w - __bfloat162float(hi));
-  if (t.wd && c < Ci) {
-    t.wd[c * (kk * Co) + uv * Co + o] = hi;
-    if (t.wd_planes == 2) t.wd[n + c * (kk * Co) + uv * Co + o] = t.wr[n + j];
+  return lo;
+}
+// One block per output row of Wr [Co][(u,v,c)] (blocks [0, off[n]): conv item, o) and one per input
+// channel row of Wd [Ci][(u,v,o)] (blocks [off[n], off[n] + offd[n]): item, c), so that every store
+// is coalesced; the reads of W [Co][Ci][k][k] stay within one row (Wr) or touch one k*k run per o (Wd).
+__global__ void __launch_bounds__(256) weights_prep_kernel(const WeightPrep prep) {
+  pdl_enter();
+  const int blk = blockIdx.x, nr = prep.off[prep.n];
+  const bool is_wr = blk < nr;
+  const int* off = is_wr ? prep.off : prep.offd;
+  const int bl = is_wr ? blk : blk - nr;
+  if (!is_wr && bl >= prep.offd[prep.n]) return;
+  const int it = prep_item(off, prep.n, bl);
+  const WeightPrep::Item& t = prep.it[it];
+  const int kk = t.k * t.k, n = t.Co * t.Cp * kk, row = bl - off[it];
+  if (is_wr) {
+    const int o = row;
+    for (int e = threadIdx.x; e < kk * t.Cp; e += blockDim.x) {
+      const int uv = e / t.Cp, c = e - uv * t.Cp;
+      const float w = prep_weight(t, o, c, uv, kk);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+      t.wr[(size_t)o * kk * t.Cp + e] = hi;
+      t.wr[n + (size_t)o * kk * t.Cp + e] = __float2bfloat16_rn(w - __bfloat162float(hi));
+    }
+  } else {
+    const int c = row;
+    for (int e = threadIdx.x; e < kk * t.Co; e += blockDim.x) {
+      const int uv = e / t.Co, o = e - uv * t.Co;
+      const float w = prep_weight(t, o, c, uv, kk);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+      t.wd[(size_t)c * kk * t.Co + e] = hi;
+      if (t.wd_planes == 2) t.wd[n + (size_t)c * kk * t.Co + e] = __float2bfloat16_rn(w - __bfloat162float(hi));
+    }
   }
 }
 // fp32 -> bf16 hi / lo planes (plane = n)
 __global__ void to_planes_kernel(const float* __restrict__ x, size_t n, __nv_bfloat16* __restrict__ xb) {
+  pdl_enter();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const __nv_bfloat16 hi = __float2bfloat16_rn(x[i]);
     xb[i] = hi;
@@ -176,6 +203,7 @@ __global__ void to_planes_kernel(const float* __restrict__ x, size_t n, __nv_bfl
   }
 }
 __global__ void to_bf16_kernel(const float* __restrict__ x, size_t n, __nv_bfloat16* __restrict__ xb) {
+  pdl_enter();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     xb[i] = __float2bfloat16_rn(x[i]);
 }
@@ -188,6 +216,7 @@ constexpr int kStemCoMax = 32;
 __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restrict__ x, const float* __restrict__ W,
                                                             int H, int Wd, int Co, int k, int s, int p, int Ho, int Wo,
                                                             float* __restrict__ y) {
+  pdl_enter();
   extern __shared__ __align__(16) float sm[];
   const int kk = k * k;
   float* ws = sm;                   // [k*k][Co]   (Co % 8 == 0)
@@ -238,6 +267,7 @@ __global__ void __launch_bounds__(kThreads) stem_wgrad_kernel(const float* __res
                                                               const __nv_bfloat16* __restrict__ dy, int H, int Wd,
                                                               int Co, int k, int s, int p, int Ho, int Wo,
                                                               float* __restrict__ part) {
+  pdl_enter();
   extern __shared__ __align__(16) float sm[];
   const int HP = H + 2 * p, WP = Wd + 2 * p;
   __nv_bfloat16* dys = reinterpret_cast<__nv_bfloat16*>(sm);           // [Ho*Wo][Co]
@@ -307,6 +337,7 @@ __global__ void __launch_bounds__(kThreads) stem_wgrad_kernel(const float* __res
 // dW[i] = sum over frames (fixed order) of part[f][i]
 __global__ void __launch_bounds__(kThreads) frame_sum_kernel(const float* __restrict__ part, int F, int n,
                                                              float* __restrict__ out) {
+  pdl_enter();
   __shared__ double red[kThreads / 32];
   double acc[1] = {0.0};
   for (int f = threadIdx.x; f < F; f += blockDim.x) acc[0] += part[(size_t)f * n + blockIdx.x];
@@ -355,6 +386,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_fwd_kernel(const float* __res
                                                             const float* __restrict__ residual, int HW, int C,
                                                             int relu, size_t plane, float* __restrict__ stats,
                                                             float* __restrict__ z, __nv_bfloat16* __restrict__ zb) {
+  pdl_enter();
   __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
   __shared__ float smu[kGroups], srs[kGroups];
   const int f = blockIdx.x, n = HW * C, c = threadIdx.x % C, cg = C / kGroups;
@@ -446,6 +478,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_kernel(const float* __res
                                                             const float* __restrict__ gamma, int HW, int C,
                                                             __nv_bfloat16* __restrict__ dx, float* __restrict__ part,
                                                             size_t lo) {
+  pdl_enter();
   __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
   __shared__ float pc[2][gn_bound(NV)];
   extern __shared__ __align__(16) float gsm[];
@@ -501,6 +534,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_kernel(const float* __res
 template <int NV>
 __global__ void __launch_bounds__(gn_bound(NV)) gn_stats_part_kernel(const float* __restrict__ y, int HW, int C,
                                                                       double* __restrict__ gpart) {
+  pdl_enter();
   __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
   const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C);
   const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
@@ -535,6 +569,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_apply_part_kernel(const float
                                                                       int C, int relu, size_t plane,
                                                                       float* __restrict__ stats, float* __restrict__ z,
                                                                       __nv_bfloat16* __restrict__ zb) {
+  pdl_enter();
   __shared__ float smu[kGroups], srs[kGroups];
   const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C), cg = C / kGroups;
   if (threadIdx.x < kGroups) {
@@ -593,6 +628,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_part_kernel(const float* 
                                                                   const float* __restrict__ gamma, int HW, int C,
                                                                   double* __restrict__ gpart,
                                                                   float* __restrict__ part) {
+  pdl_enter();
   __shared__ double sa[gn_bound(NV)], sb[gn_bound(NV)], ga[kGroups], gb[kGroups];
   __shared__ float pc[2][gn_bound(NV)];
   extern __shared__ __align__(16) float gsm[];
@@ -646,6 +682,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_apply_kernel(const float*
                                                                    const float* __restrict__ gamma,
                                                                    const double* __restrict__ gpart, int HW, int C,
                                                                    __nv_bfloat16* __restrict__ dx, size_t lo) {
+  pdl_enter();
   __shared__ float sm1[kGroups], sm2[kGroups];
   extern __shared__ __align__(16) float gsm[];
   const int cap = NV * blockDim.x;
@@ -780,6 +817,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_cluster_kernel(const floa
 __global__ void __launch_bounds__(kThreads) gn_param_reduce_kernel(const float* __restrict__ part, int F, int C,
                                                                    float* __restrict__ dgamma,
                                                                    float* __restrict__ dbeta) {
+  pdl_enter();
   __shared__ double red[2 * (kThreads / 32)];
   const int c = blockIdx.x;
   double acc[2] = {0.0, 0.0};
@@ -806,6 +844,7 @@ struct GnParamAll {
   } it[kMaxConvsGn];
 };
 __global__ void __launch_bounds__(kThreads) gn_param_reduce_all_kernel(const GnParamAll a) {
+  pdl_enter();
   __shared__ double red[2 * (kThreads / 32)];
   int lo = 0, hi = a.n - 1;
   while (lo < hi) {
@@ -831,6 +870,7 @@ __global__ void __launch_bounds__(kThreads) gn_param_reduce_all_kernel(const GnP
 // 4 channels): the 9 window loads (float4) are independent and in flight together; 32-bit indices.
 __global__ void maxpool_fwd_kernel(const float* __restrict__ x, int F, int H, int W, int C, int Ho, int Wo,
                                    float* __restrict__ y, uint8_t* __restrict__ arg, __nv_bfloat16* __restrict__ yb) {
+  pdl_enter();
   const int C4 = C >> 2, n4 = F * Ho * Wo * C4;
   const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
   if (i4 >= n4) return;
@@ -876,6 +916,7 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ x, int F, int H, in
 // before any comparison.
 __global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* __restrict__ arg, int F, int H, int W,
                                    int C, int Ho, int Wo, float* __restrict__ dx) {
+  pdl_enter();
   const int C4 = C >> 2, n4 = F * H * W * C4;
   const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
   if (i4 >= n4) return;
@@ -917,6 +958,7 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* 
 // NHWC [F][HW][C] <-> flat [F][C*HW] in (c, h, w) order (PyTorch flatten of NCHW)
 __global__ void flatten_kernel(const float* __restrict__ in, int F, int HW, int C, float* __restrict__ out,
                                int to_flat) {
+  pdl_enter();
   const int per = HW * C;
   const size_t n = (size_t)F * per;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -930,6 +972,7 @@ __global__ void flatten_kernel(const float* __restrict__ in, int F, int HW, int 
 
 // y[m][n] = act(y[m][n] + bias[n])   (act: 1 = ReLU)
 __global__ void bias_act_kernel(float* __restrict__ y, const float* __restrict__ bias, int M, int N, int relu) {
+  pdl_enter();
   const size_t n = (size_t)M * N;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     float v = y[i] + bias[i % N];
@@ -942,6 +985,7 @@ __global__ void lstm_input_kernel(const float* __restrict__ vis, const float* __
                                   const int32_t* __restrict__ prev_action, const int32_t* __restrict__ env_idx,
                                   const float* __restrict__ Wg, const float* __restrict__ bg,
                                   const float* __restrict__ Emb, int T, int ld, int T_run, int S, float* __restrict__ x) {
+  pdl_enter();
   const size_t n = (size_t)S * kXin;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int s = (int)(i / kXin), k = (int)(i % kXin);
@@ -966,6 +1010,7 @@ __global__ void lstm_input_kernel(const float* __restrict__ vis, const float* __
 // gradients (block per output, fixed-order block reduction over samples)
 __global__ void vis_mask_kernel(const float* __restrict__ dx, const float* __restrict__ vis, int S,
                                 float* __restrict__ dvis) {
+  pdl_enter();
   const size_t n = (size_t)S * 512;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const size_t s = i / 512, k = i % 512;
@@ -978,6 +1023,7 @@ __global__ void __launch_bounds__(kThreads) goal_emb_grads_kernel(const float* _
                                                                   const int32_t* __restrict__ env_idx, int T, int ld,
                                                                   int T_run, int S, float* __restrict__ dWg,
                                                                   float* __restrict__ dbg, float* __restrict__ dEmb) {
+  pdl_enter();
   __shared__ double red[kA1 * (kThreads / 32)];
   const int j = blockIdx.x;  // 0..63: 0..31 goal units, 32..63 embedding dims
   double acc[kA1] = {0, 0, 0, 0, 0};
@@ -1011,6 +1057,7 @@ __global__ void __launch_bounds__(kThreads) goal_emb_grads_kernel(const float* _
 // dgoal[s][c] = sum_j dx[s][512 + j] * Wg[j][c]: the gradient wrt the goal input of goal_fc
 __global__ void goal_input_grad_kernel(const float* __restrict__ dx, const float* __restrict__ Wg, int S,
                                        float* __restrict__ dgoal) {
+  pdl_enter();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S * 3; i += gridDim.x * blockDim.x) {
     const int s = i / 3, c = i - s * 3;
     float acc = 0.f;
@@ -1021,6 +1068,7 @@ __global__ void goal_input_grad_kernel(const float* __restrict__ dx, const float
 
 __global__ void relu_mask_kernel(const float* __restrict__ dz, const float* __restrict__ z, size_t n,
                                  float* __restrict__ out) {
+  pdl_enter();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     out[i] = z[i] > 0.f ? dz[i] : 0.f;
 }
@@ -1037,6 +1085,7 @@ __global__ void __launch_bounds__(256) se_fwd_kernel(const float* __restrict__ z
                                                      __nv_bfloat16* __restrict__ outb, size_t plane,
                                                      float* __restrict__ s_out, float* __restrict__ pool_out,
                                                      float* __restrict__ a1_out) {
+  pdl_enter();
   extern __shared__ float sm[];  // pool[C], s[C], a1[R]
   float *pool = sm, *sv = sm + C, *a1 = sm + 2 * C;
   const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1083,6 +1132,7 @@ __global__ void __launch_bounds__(256) se_bwd_kernel(const float* __restrict__ d
                                                      const float* __restrict__ W2, int HW, int C, int R,
                                                      float* __restrict__ dz3, float* __restrict__ da1_out,
                                                      float* __restrict__ da2_out) {
+  pdl_enter();
   extern __shared__ float sm[];  // da2[C], dpool[C], da1[R]
   float *da2 = sm, *dpool = sm + C, *da1 = sm + 2 * C;
   const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1127,6 +1177,7 @@ __global__ void se_param_grad_kernel(const float* __restrict__ da1, const float*
                                      const float* __restrict__ pool, const float* __restrict__ a1, int F, int C, int R,
                                      float* __restrict__ dW1, float* __restrict__ db1, float* __restrict__ dW2,
                                      float* __restrict__ db2) {
+  pdl_enter();
   const int n1 = R * C, n = 2 * R * C + R + C;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     float acc = 0.f;
@@ -1451,7 +1502,7 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
     DDPPO_REQUIRE(ctx, g.Co <= kStemCoMax && g.Co % 8 == 0 && g.k * g.k <= 64, "stem conv: Co in {8,..,32}, k*k <= 64");
     const size_t smem = (size_t)(g.H * g.W + g.Co * g.k * g.k) * sizeof(float);
     DDPPO_REQUIRE(ctx, smem <= 48 * 1024, "stem conv: frame too large for shared memory");
-    stem_fwd_kernel<<<g.F, kThreads, smem, st>>>(x, w, g.H, g.W, g.Co, g.k, g.s, g.p, g.Ho, g.Wo, y);
+    launch_k(ctx, stem_fwd_kernel, g.F, kThreads, smem, st, x, w, g.H, g.W, g.Co, g.k, g.s, g.p, g.Ho, g.Wo, y);
     ctx->count(1);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     return DDPPO_OK;
@@ -1459,7 +1510,8 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
   const int K = g.K(), M = g.M();
   if (!wr_b) {  // weights not prepared by weights_prep_kernel (diagnostic entry)
     DDPPO_REQUIRE(ctx, sc.wr_b && g.Cr == g.Ci, "conv: unprepared weights need scratch");
-    weights_bf16_kernel<<<blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st>>>(w, g.Co, g.Ci, g.k, sc.wr_b, nullptr);
+    launch_k(ctx, weights_bf16_kernel, blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st, w, g.Co, g.Ci, g.k,
+             sc.wr_b, nullptr);
     ctx->count(1);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     wr_b = sc.wr_b;
@@ -1502,8 +1554,9 @@ ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const
                                                200 * 1024));
       attr_set = true;
     }
-    stem_wgrad_kernel<<<g.F, kThreads, smem, st>>>(x, dy, g.H, g.W, g.Co, g.k, g.s, g.p, g.Ho, g.Wo, sc.part);
-    frame_sum_kernel<<<g.Co * g.k * g.k, kThreads, 0, st>>>(sc.part, g.F, g.Co * g.k * g.k, dw);
+    launch_k(ctx, stem_wgrad_kernel, g.F, kThreads, smem, st, x, dy, g.H, g.W, g.Co, g.k, g.s, g.p, g.Ho, g.Wo,
+             sc.part);
+    launch_k(ctx, frame_sum_kernel, g.Co * g.k * g.k, kThreads, 0, st, sc.part, g.F, g.Co * g.k * g.k, dw);
     ctx->count(2);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     return DDPPO_OK;
@@ -1551,7 +1604,8 @@ ddppo_status conv_dgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* w, const
   // dgrad: dx[p][c] (+)= sum_{(u,v,o)} dy[tap^T(p; u, v)][o] W[o][c][u][v]
   if (!wd_b) {
     DDPPO_REQUIRE(ctx, sc.wd_b && g.Cr == g.Ci, "conv: unprepared weights need scratch");
-    weights_bf16_kernel<<<blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st>>>(w, g.Co, g.Ci, g.k, nullptr, sc.wd_b);
+    launch_k(ctx, weights_bf16_kernel, blocks_for(ctx, (size_t)g.Co * K), kThreads, 0, st, w, g.Co, g.Ci, g.k,
+             nullptr, sc.wd_b);
     ctx->count(1);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     wd_b = sc.wd_b;
@@ -1601,7 +1655,8 @@ ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const 
   const int S = (HW * C + gn_chunk(C) - 1) / gn_chunk(C);
   if (S == 1) {  // one block per frame: statistics and normalisation in one pass over the slab
     const int nv = gn_vpt(HW * C, nt);
-#define GN_FWD(NV) gn_fwd_kernel<NV><<<F, nt, 0, st>>>(y, gamma, beta, residual, HW, C, relu, (size_t)F * HW * C, stats, z, zb)
+#define GN_FWD(NV) \
+  launch_k(ctx, gn_fwd_kernel<NV>, F, nt, 0, st, y, gamma, beta, residual, HW, C, relu, (size_t)F * HW * C, stats, z, zb)
     if (nv <= 4) GN_FWD(4);
     else if (nv <= 8) GN_FWD(8);
     else if (nv <= 16) GN_FWD(16);
@@ -1610,11 +1665,11 @@ ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const 
     ctx->count(1);
   } else {
     DDPPO_REQUIRE(ctx, gpart != nullptr, "groupnorm: large frames need partial-sum scratch");
-#define GN_FWD2(NV)                                                                                          \
-  do {                                                                                                       \
-  gn_stats_part_kernel<NV><<<dim3(S, F), nt, 0, st>>>(y, HW, C, gpart);                                      \
-  gn_apply_part_kernel<NV><<<dim3(S, F), nt, 0, st>>>(y, gpart, gamma, beta, residual, HW, C, relu,          \
-                                                      (size_t)F * HW * C, stats, z, zb); \
+#define GN_FWD2(NV)                                                                                   \
+  do {                                                                                                \
+    launch_k(ctx, gn_stats_part_kernel<NV>, dim3(S, F), nt, 0, st, y, HW, C, gpart);                  \
+    launch_k(ctx, gn_apply_part_kernel<NV>, dim3(S, F), nt, 0, st, y, gpart, gamma, beta, residual, HW, \
+             C, relu, (size_t)F * HW * C, stats, z, zb);                                              \
   } while (0)
     if (nt == 1024) GN_FWD2(8);
     else if (nt == 512) GN_FWD2(16);
@@ -1689,11 +1744,12 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
   const int S = (HW * C + gn_chunk(C) - 1) / gn_chunk(C);
   if (S == 1) {
     const int nv = gn_vpt(HW * C, nt);
-#define GN_BWD(NV)                                                                                           \
-  do {                                                                                                       \
-    s = gn_smem_attr(ctx, gn_bwd_kernel<NV>, gn_bwd_smem(NV, nt));                                           \
-    if (s != DDPPO_OK) return s;                                                                             \
-    gn_bwd_kernel<NV><<<F, nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, HW, C, dy, part, lo); \
+#define GN_BWD(NV)                                                                                    \
+  do {                                                                                                \
+    s = gn_smem_attr(ctx, gn_bwd_kernel<NV>, gn_bwd_smem(NV, nt));                                    \
+    if (s != DDPPO_OK) return s;                                                                      \
+    launch_k(ctx, gn_bwd_kernel<NV>, F, nt, gn_bwd_smem(NV, nt), st, dz, relu_z, y, stats, gamma, HW, \
+             C, dy, part, lo);                                                                        \
   } while (0)
     if (nv <= 4) GN_BWD(4);
     else if (nv <= 8) GN_BWD(8);
@@ -1703,16 +1759,16 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
     ctx->count(1);
   } else {
     DDPPO_REQUIRE(ctx, gpart != nullptr, "groupnorm: large frames need partial-sum scratch");
-#define GN_BWD2(NV)                                                                                          \
-  do {                                                                                                       \
-    s = gn_smem_attr(ctx, gn_bwd_part_kernel<NV>, gn_bwd_smem(NV, nt));                                      \
-    if (s != DDPPO_OK) return s;                                                                             \
-    s = gn_smem_attr(ctx, gn_bwd_apply_kernel<NV>, gn_bwd_smem(NV, nt));                                     \
-    if (s != DDPPO_OK) return s;                                                                             \
-    gn_bwd_part_kernel<NV><<<dim3(S, F), nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, HW, C,  \
-                                                                       gpart, part);                        \
-    gn_bwd_apply_kernel<NV><<<dim3(S, F), nt, gn_bwd_smem(NV, nt), st>>>(dz, relu_z, y, stats, gamma, gpart, \
-                                                                        HW, C, dy, lo);                     \
+#define GN_BWD2(NV)                                                                                   \
+  do {                                                                                                \
+    s = gn_smem_attr(ctx, gn_bwd_part_kernel<NV>, gn_bwd_smem(NV, nt));                               \
+    if (s != DDPPO_OK) return s;                                                                      \
+    s = gn_smem_attr(ctx, gn_bwd_apply_kernel<NV>, gn_bwd_smem(NV, nt));                              \
+    if (s != DDPPO_OK) return s;                                                                      \
+    launch_k(ctx, gn_bwd_part_kernel<NV>, dim3(S, F), nt, gn_bwd_smem(NV, nt), st, dz, relu_z, y,     \
+             stats, gamma, HW, C, gpart, part);                                                       \
+    launch_k(ctx, gn_bwd_apply_kernel<NV>, dim3(S, F), nt, gn_bwd_smem(NV, nt), st, dz, relu_z, y,    \
+             stats, gamma, gpart, HW, C, dy, lo);                                                     \
   } while (0)
     bool done = false;
     if (S <= 16) {  // one pass: the frame's chunks as a thread-block cluster
@@ -1733,7 +1789,7 @@ ddppo_status gn_bwd(ddppo_ctx* ctx, int F, int HW, int C, const float* dz, const
 #undef GN_BWD2
   }
   if (reduce_params) {  // else the caller reduces `part` later (gn_param_reduce_all)
-    gn_param_reduce_kernel<<<C, kThreads, 0, st>>>(part, F * S, C, dgamma, dbeta);
+    launch_k(ctx, gn_param_reduce_kernel, C, kThreads, 0, st, part, F * S, C, dgamma, dbeta);
     ctx->count(1);
   }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -1861,23 +1917,26 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
     WeightPrep prep;
     prep.n = 0;
     prep.off[0] = 0;
+    prep.offd[0] = 0;
     for (size_t i = 0; i < P.convs.size(); ++i) {
       const ConvGN& c = P.convs[i];
       if (c.Ci == 1) continue;  // the Depth stem runs SIMT on fp32 weights
       DDPPO_REQUIRE(ctx, prep.n < kMaxConvs, "too many convolutions for one weight-prep launch");
       prep.it[prep.n] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k, P.grad_planes, c.groups};
-      prep.off[prep.n + 1] = prep.off[prep.n] + c.Co * c.Ci * c.k * c.k;
+      prep.off[prep.n + 1] = prep.off[prep.n] + c.Co;
+      prep.offd[prep.n + 1] = prep.offd[prep.n] + (c.wd_b ? c.Ci_real : 0);
       ++prep.n;
     }
-    weights_prep_kernel<<<(prep.off[prep.n] + 255) / 256, 256, 0, st>>>(prep);
+    launch_k(ctx, weights_prep_kernel, prep.off[prep.n] + prep.offd[prep.n], 256, 0, st, prep);
     ctx->count(1);
   }
   if (!P.rgbd) {
-    gather_obs_kernel<<<blocks_for(ctx, (size_t)F * kImg * kImg / 8), kThreads, 0, st>>>(
+    launch_k(ctx, gather_obs_kernel, blocks_for(ctx, (size_t)F * kImg * kImg / 8), kThreads, 0, st, 
         reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, P.x0);
   } else {
     DDPPO_REQUIRE(ctx, kImgRgbd % 4 == 0, "rgbd: input width must be a multiple of 4");
-    rgbd_prologue_kernel<<<(F * (kImgRgbd / 2) * (kImgRgbd / 4) + kThreads - 1) / kThreads, kThreads, 0, st>>>(
+    launch_k(ctx, rgbd_prologue_kernel, (F * (kImgRgbd / 2) * (kImgRgbd / 4) + kThreads - 1) / kThreads, kThreads, 0,
+             st, 
         b.obs_rgb, reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, kImgRgbd, P.x0, P.x0b);
   }
   ctx->count(1);
@@ -1886,7 +1945,7 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
   {
     ConvGN& c = P.convs[0];
     const int hp = P.pool_hw;
-    maxpool_fwd_kernel<<<(F * hp * hp * 8 + kThreads - 1) / kThreads, kThreads, 0, st>>>(
+    launch_k(ctx, maxpool_fwd_kernel, (F * hp * hp * 8 + kThreads - 1) / kThreads, kThreads, 0, st, 
         c.z, F, c.Ho, c.Wo, 32, hp, hp, P.pool_out, P.pool_arg, P.pool_b);
     ctx->count(1);
   }
@@ -1907,7 +1966,8 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
     if (blk.se) {
       const ConvGN& c3 = P.convs[blk.main.back()];
       const size_t smem = (size_t)(2 * blk.C + blk.R) * sizeof(float);
-      se_fwd_kernel<<<F, 256, smem, st>>>(c3.z, sc, prm + blk.se_w1, prm + blk.se_b1, prm + blk.se_w2, prm + blk.se_b2,
+      launch_k(ctx, se_fwd_kernel, F, 256, smem, st, c3.z, sc, prm + blk.se_w1, prm + blk.se_b1, prm + blk.se_w2,
+               prm + blk.se_b2,
                                           blk.HW, blk.C, blk.R, blk.out, blk.outb, (size_t)F * blk.HW * blk.C,
                                           blk.se_s, blk.se_pool, blk.se_a1);
       ctx->count(1);
@@ -1916,17 +1976,19 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
   }
   ConvGN& comp = P.convs.back();
   if ((s = conv_gn_fwd(ctx, prm, P, comp, nullptr, 1, st)) != DDPPO_OK) return s;
-  flatten_kernel<<<blocks_for(ctx, (size_t)F * P.fc_in), kThreads, 0, st>>>(comp.z, F, P.feat_hw, 128, P.flat, 1);
+  launch_k(ctx, flatten_kernel, blocks_for(ctx, (size_t)F * P.fc_in), kThreads, 0, st, comp.z, F, P.feat_hw, 128,
+           P.flat, 1);
   ctx->count(1);
   // visual FC + ReLU
   if ((s = gemm_split(ctx, GemmTC{P.flat, P.fc_in, 1, prm + off_of(L, "visual_fc.weight"), P.fc_in, 1, P.vis, 512, F,
                                   512, P.fc_in, 1, nullptr, kPrecFwd},
                       P, st)) != DDPPO_OK)
     return s;
-  bias_act_kernel<<<blocks_for(ctx, (size_t)F * 512), kThreads, 0, st>>>(P.vis, prm + off_of(L, "visual_fc.bias"), F,
+  launch_k(ctx, bias_act_kernel, blocks_for(ctx, (size_t)F * 512), kThreads, 0, st, P.vis, prm + off_of(L,
+           "visual_fc.bias"), F,
                                                                          512, 1);
   ctx->count(1);
-  lstm_input_kernel<<<blocks_for(ctx, (size_t)F * kXin), kThreads, 0, st>>>(
+  launch_k(ctx, lstm_input_kernel, blocks_for(ctx, (size_t)F * kXin), kThreads, 0, st, 
       P.vis, b.goal, b.prev_action, b.env_idx, prm + off_of(L, "goal_fc.weight"), prm + off_of(L, "goal_fc.bias"),
       prm + off_of(L, "act_embed.weight"), b.T, b.ld, b.T_run, F, P.xin);
   ctx->count(1);
@@ -2010,16 +2072,17 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     float* dxl = l == 0 ? P.dxin : P.rnn[l - 1].dH;
     if ((s = gemm_split(ctx, GemmTC{r.dG, kG4, 1, Wih, 1, nin, dxl, nin, F, nin, kG4}, P, st)) != DDPPO_OK) return s;
   }
-  goal_emb_grads_kernel<<<64, kThreads, 0, st>>>(P.dxin, b.goal, b.prev_action, b.env_idx, b.T, b.ld, b.T_run, F,
+  launch_k(ctx, goal_emb_grads_kernel, 64, kThreads, 0, st, P.dxin, b.goal, b.prev_action, b.env_idx, b.T, b.ld,
+           b.T_run, F,
                                                  grad + off_of(L, "goal_fc.weight"), grad + off_of(L, "goal_fc.bias"),
                                                  grad + off_of(L, "act_embed.weight"));
   ctx->count(1);
   if (b.dgoal) {  // the planner's gradient through the (frozen) controller
-    goal_input_grad_kernel<<<blocks_for(ctx, (size_t)F * 3), kThreads, 0, st>>>(
+    launch_k(ctx, goal_input_grad_kernel, blocks_for(ctx, (size_t)F * 3), kThreads, 0, st, 
         P.dxin, prm + off_of(L, "goal_fc.weight"), F, b.dgoal);
     ctx->count(1);
   }
-  vis_mask_kernel<<<blocks_for(ctx, (size_t)F * 512), kThreads, 0, st>>>(P.dxin, P.vis, F, P.dvis);
+  launch_k(ctx, vis_mask_kernel, blocks_for(ctx, (size_t)F * 512), kThreads, 0, st, P.dxin, P.vis, F, P.dvis);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   // visual FC: dW = dVpre^T flat, db = colsum(dVpre) (side stream), dflat = dVpre W
@@ -2044,7 +2107,8 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   float* dz = P.dz_a;
   float* da = P.dz_b;
   float* dn = P.dz_c;
-  flatten_kernel<<<blocks_for(ctx, (size_t)F * P.fc_in), kThreads, 0, st>>>(P.dflat, F, P.feat_hw, 128, da, 0);
+  launch_k(ctx, flatten_kernel, blocks_for(ctx, (size_t)F * P.fc_in), kThreads, 0, st, P.dflat, F, P.feat_hw, 128, da,
+           0);
   ctx->count(1);
   if ((s = conv_gn_bwd(ctx, prm, grad, P, comp, da, comp.z, dz, 0, st)) != DDPPO_OK) return s;
   for (int bi = (int)P.blocks.size() - 1; bi >= 0; --bi) {
@@ -2055,7 +2119,7 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
       if ((s = conv_gn_bwd(ctx, prm, grad, P, P.convs[blk.down], dz, blk.out, dn, 0, st)) != DDPPO_OK) return s;
     } else {
       const size_t n = (size_t)F * last.Ho * last.Wo * last.Co;
-      relu_mask_kernel<<<blocks_for(ctx, n), kThreads, 0, st>>>(dz, blk.out, n, dn);
+      launch_k(ctx, relu_mask_kernel, blocks_for(ctx, n), kThreads, 0, st, dz, blk.out, n, dn);
       ctx->count(1);
     }
     // main branch, last conv first: its upstream mask is the block output (or, after the SE module, none),
@@ -2064,7 +2128,8 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     float* g_out = da;   // gradient wrt its input
     if (blk.se) {
       const size_t smem = (size_t)(2 * blk.C + blk.R) * sizeof(float);
-      se_bwd_kernel<<<F, 256, smem, st>>>(dz, blk.out, last.z, blk.se_s, blk.se_a1, prm + blk.se_w1, prm + blk.se_w2,
+      launch_k(ctx, se_bwd_kernel, F, 256, smem, st, dz, blk.out, last.z, blk.se_s, blk.se_a1, prm + blk.se_w1,
+               prm + blk.se_w2,
                                           blk.HW, blk.C, blk.R, P.dz_se, blk.se_da1, blk.se_da2);
       ctx->count(1);
       DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -2074,7 +2139,7 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
         pst = P.side;
       }
       const int n = 2 * blk.R * blk.C + blk.R + blk.C;
-      se_param_grad_kernel<<<blocks_for(ctx, (size_t)n), kThreads, 0, pst>>>(
+      launch_k(ctx, se_param_grad_kernel, blocks_for(ctx, (size_t)n), kThreads, 0, pst, 
           blk.se_da1, blk.se_da2, blk.se_pool, blk.se_a1, F, blk.C, blk.R, grad + blk.se_w1, grad + blk.se_b1,
           grad + blk.se_w2, grad + blk.se_b2);
       ctx->count(1);
@@ -2096,7 +2161,7 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   }
   // max-pool, then the stem (no input gradient)
   ConvGN& stem = P.convs[0];
-  maxpool_bwd_kernel<<<(F * stem.Ho * stem.Wo * 8 + kThreads - 1) / kThreads, kThreads, 0, st>>>(
+  launch_k(ctx, maxpool_bwd_kernel, (F * stem.Ho * stem.Wo * 8 + kThreads - 1) / kThreads, kThreads, 0, st, 
       dz, P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -2111,7 +2176,7 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     a.ch_off[a.n + 1] = a.ch_off[a.n] + c.Co;
     ++a.n;
   }
-  gn_param_reduce_all_kernel<<<a.ch_off[a.n], kThreads, 0, st>>>(a);
+  launch_k(ctx, gn_param_reduce_all_kernel, a.ch_off[a.n], kThreads, 0, st, a);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   if (wst != st) DDPPO_CUDA_TRY(ctx, fork_to(ctx, wst, st));  // join: every weight gradient is final
@@ -2153,14 +2218,14 @@ extern "C" ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const
   sc.part_n = nf - ok;
   cudaStream_t st = as_stream(stream);
   ProfScope ps(ctx, DDPPO_K_OTHER, st, 0);
-  to_planes_kernel<<<blocks_for(ctx, nx), kThreads, 0, st>>>(x, nx, xb);
+  launch_k(ctx, to_planes_kernel, blocks_for(ctx, nx), kThreads, 0, st, x, nx, xb);
   ctx->count(1);
   if (y) {
     ddppo_status r = conv_fwd(ctx, g, x, xb, w, nullptr, y, sc, st);
     if (r != DDPPO_OK) return r;
   }
   if (dy) {
-    to_bf16_kernel<<<blocks_for(ctx, ny), kThreads, 0, st>>>(dy, ny, dyb);
+    launch_k(ctx, to_bf16_kernel, blocks_for(ctx, ny), kThreads, 0, st, dy, ny, dyb);
     ctx->count(1);
     ddppo_status r = conv_wgrad(ctx, g, x, xb, dyb, dw, sc, st);
     if (r != DDPPO_OK || Ci == 1 || dx == nullptr) return r;
@@ -2172,6 +2237,7 @@ extern "C" ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const
 
 namespace {
 __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ x, size_t n, float* __restrict__ y) {
+  pdl_enter();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     y[i] = __bfloat162float(x[i]);
 }
@@ -2193,7 +2259,7 @@ extern "C" ddppo_status ddppo_debug_groupnorm(ddppo_ctx* ctx, const float* y, co
   if (r != DDPPO_OK || !dz) return r;
   r = gn_bwd(ctx, F, HW, C, dz, relu ? z : nullptr, y, stats, gamma, dyb, dgamma, dbeta, part, gpart, st);
   if (r != DDPPO_OK) return r;
-  bf16_to_f32_kernel<<<blocks_for(ctx, (size_t)F * HW * C), kThreads, 0, st>>>(dyb, (size_t)F * HW * C, dy);
+  launch_k(ctx, bf16_to_f32_kernel, blocks_for(ctx, (size_t)F * HW * C), kThreads, 0, st, dyb, (size_t)F * HW * C, dy);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
@@ -2207,11 +2273,13 @@ extern "C" ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int 
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
   cudaStream_t st = as_stream(stream);
   ProfScope ps(ctx, DDPPO_K_OTHER, st, 0);
-  maxpool_fwd_kernel<<<(F * Ho * Wo * (C / 4) + kThreads - 1) / kThreads, kThreads, 0, st>>>(x, F, H, W, C, Ho, Wo, y, arg,
+  launch_k(ctx, maxpool_fwd_kernel, (F * Ho * Wo * (C / 4) + kThreads - 1) / kThreads, kThreads, 0, st, x, F, H, W, C,
+           Ho, Wo, y, arg,
                                                                                      nullptr);
   ctx->count(1);
   if (dy) {
-    maxpool_bwd_kernel<<<(F * H * W * (C / 4) + kThreads - 1) / kThreads, kThreads, 0, st>>>(dy, arg, F, H, W, C, Ho,
+    launch_k(ctx, maxpool_bwd_kernel, (F * H * W * (C / 4) + kThreads - 1) / kThreads, kThreads, 0, st, dy, arg, F, H,
+             W, C, Ho,
                                                                                           Wo, dx);
     ctx->count(1);
   }
@@ -2221,6 +2289,7 @@ extern "C" ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int 
 
 namespace {
 __global__ void positive_mask_kernel(const float* __restrict__ z, size_t n, uint8_t* __restrict__ out) {
+  pdl_enter();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     out[i] = z[i] > 0.f ? 1 : 0;
 }
@@ -2258,7 +2327,8 @@ extern "C" ddppo_status ddppo_debug_depth_decisions(ddppo_ctx* ctx, const ddppo_
   cudaStream_t st = as_stream(stream);
   size_t off = 0;
   for (size_t i = 0; i < masks.size(); ++i) {
-    positive_mask_kernel<<<blocks_for(ctx, masks[i].second), kThreads, 0, st>>>(masks[i].first, masks[i].second,
+    launch_k(ctx, positive_mask_kernel, blocks_for(ctx, masks[i].second), kThreads, 0, st, masks[i].first,
+             masks[i].second,
                                                                                out + off);
     off += masks[i].second;
     if (i == 0) {

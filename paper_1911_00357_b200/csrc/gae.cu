@@ -21,6 +21,7 @@ gae_kernel(const float* __restrict__ rew, const float* __restrict__ val, const u
            const int32_t* __restrict__ len, int E, int T, int ld, float gamma, float tau,
            float* __restrict__ adv, float* __restrict__ ret, double* partials, unsigned int* counter,
            double* stats3) {
+  pdl_enter();
   __shared__ double red[3 * kWarps];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 gae1_kernel(const float* __restrict__ rew, const float* __restrict__ val, const uint8_t* __restrict__ done,
             const int32_t* __restrict__ len, int E, int T, int ld, float gamma, float tau, float* __restrict__ adv,
             float* __restrict__ ret, double* partials, unsigned int* counter, double* stats3) {
+  pdl_enter();
   __shared__ double red[3 * kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float gt = gamma * tau;
@@ -228,6 +230,7 @@ gae1_kernel(const float* __restrict__ rew, const float* __restrict__ val, const 
 }
 
 __global__ void adv_finalize_kernel(const double* stats3, float eps, float* mean_invstd) {
+  pdl_enter();
   if (threadIdx.x != 0) return;
   const double S = stats3[0], Q = stats3[1], n = stats3[2];
   const double mu = n > 0 ? S / n : 0.0;
@@ -252,13 +255,14 @@ ddppo_status launch_gae(ddppo_ctx* ctx, const float* rew, const float* val, cons
   const int blocks = grid_for(E, kWarps, ctx->sm_count * 8);
   ProfScope ps(ctx, DDPPO_K_GAE, st, 1);
   if (vec && T <= 128)
-    gae1_kernel<<<blocks, kWarps * 32, 0, st>>>(rew, val, done, len, E, T, ld, gamma, tau, adv, ret, ctx->d_partials,
+    launch_k(ctx, gae1_kernel, blocks, kWarps * 32, 0, st, rew, val, done, len, E, T, ld, gamma, tau, adv, ret,
+             ctx->d_partials,
                                                 ctx->d_counters + CNT_GAE, stats3);
   else if (vec)
-    gae_kernel<true><<<blocks, kWarps * 32, 0, st>>>(rew, val, done, len, E, T, ld, gamma, tau, adv, ret,
+    launch_k(ctx, gae_kernel<true>, blocks, kWarps * 32, 0, st, rew, val, done, len, E, T, ld, gamma, tau, adv, ret,
                                                      ctx->d_partials, ctx->d_counters + CNT_GAE, stats3);
   else
-    gae_kernel<false><<<blocks, kWarps * 32, 0, st>>>(rew, val, done, len, E, T, ld, gamma, tau, adv, ret,
+    launch_k(ctx, gae_kernel<false>, blocks, kWarps * 32, 0, st, rew, val, done, len, E, T, ld, gamma, tau, adv, ret,
                                                       ctx->d_partials, ctx->d_counters + CNT_GAE, stats3);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
@@ -267,7 +271,7 @@ ddppo_status launch_gae(ddppo_ctx* ctx, const float* rew, const float* val, cons
 ddppo_status launch_adv_finalize(ddppo_ctx* ctx, const double* stats3, float eps, float* mean_invstd,
                                  cudaStream_t st) {
   ProfScope ps(ctx, DDPPO_K_ADV_NORM, st, 1);
-  adv_finalize_kernel<<<1, 32, 0, st>>>(stats3, eps, mean_invstd);
+  launch_k(ctx, adv_finalize_kernel, 1, 32, 0, st, stats3, eps, mean_invstd);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }

@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, const float* __restrict__ B,
                     long long sbn, long long sbk, float* __restrict__ C, long long ldc, int M, int N, int K, int kper,
                     long long cz_stride, int amode, int bmode, int accumulate) {
+  pdl_enter();
   constexpr int kTmemCols = BN < 32 ? 32 : BN;
   constexpr uint32_t kABytes = kBM * kBK * 2, kBBytes = BN * kBK * 2;
   constexpr uint32_t kRawA = raw_bytes<kBM>(), kRawB = raw_bytes<BN>();
@@ -346,6 +347,7 @@ gemm_bf16_tc_kernel(const float* __restrict__ A, long long sam, long long sak, c
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, long long zs, int M, int N,
                                      float* __restrict__ C, long long ldc, int accumulate) {
+  pdl_enter();
   const long long n = (long long)M * N;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long m = i / N, c = i % N;
@@ -380,15 +382,17 @@ ddppo_status launch_bn(ddppo_ctx* ctx, const GemmTC& g, cudaStream_t st) {
   dim3 grid((g.N + BN - 1) / BN, (g.M + kBM - 1) / kBM, nz);
   ctx->count(nz == 1 ? 1 : 2);
   if (nz == 1) {
-    kern<<<grid, kThreads, smem, st>>>(g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.C, g.ldc, g.M, g.N, g.K, kper, 0, am, bm,
+    launch_k(ctx, kern, grid, kThreads, smem, st, g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.C, g.ldc, g.M, g.N, g.K,
+             kper, 0, am, bm,
                                        g.accumulate);
   } else {
     const long long zs = (long long)g.M * g.N;
-    kern<<<grid, kThreads, smem, st>>>(g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.partial, g.N, g.M, g.N, g.K, kper, zs, am,
+    launch_k(ctx, kern, grid, kThreads, smem, st, g.A, g.sam, g.sak, g.B, g.sbn, g.sbk, g.partial, g.N, g.M, g.N, g.K,
+             kper, zs, am,
                                        bm, 0);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
-    splitk_reduce_kernel<<<grid_for((int)std::min<long long>(zs, 1 << 30), 256, ctx->sm_count * 8), 256, 0, st>>>(
-        g.partial, nz, zs, g.M, g.N, g.C, g.ldc, g.accumulate);
+    launch_k(ctx, splitk_reduce_kernel, grid_for((int)std::min<long long>(zs, 1 << 30), 256, ctx->sm_count * 8), 256, 0,
+             st, g.partial, nz, zs, g.M, g.N, g.C, g.ldc, g.accumulate);
   }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;

@@ -25,6 +25,7 @@ ppo_loss_kernel(const float* __restrict__ logits, const float* __restrict__ valu
                 const float* __restrict__ mean_invstd, float inv_n, float eps, float vclip_eps, float c_v, float c_e,
                 int use_vclip, float* __restrict__ dlogits, float* __restrict__ dvalues, double* partials,
                 unsigned int* counter, float* stats_out, int* err, float n_valid) {
+  pdl_enter();
   __shared__ double red[6 * (kThreads / 32)];
   __shared__ double fin[6];
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -71,7 +72,7 @@ ddppo_status launch_loss(ddppo_ctx* ctx, const float* logits, const float* value
   const int M = b.B * b.T_run;
   const int blocks = grid_for(M, kThreads, ctx->sm_count * 8);
   ProfScope ps(ctx, DDPPO_K_LOSS, st, 1);
-  ppo_loss_kernel<<<blocks, kThreads, 0, st>>>(
+  launch_k(ctx, ppo_loss_kernel, blocks, kThreads, 0, st, 
       logits, values, b.env_idx, b.len, b.B, b.T_run, b.ld, in.action, in.logp_old, in.value_old, in.ret, in.adv,
       cfg.normalize_adv ? mean_invstd : nullptr, 1.f / (float)b.n_valid, cfg.clip_eps, cfg.vclip_eps, cfg.c_v,
       cfg.c_e, cfg.use_value_clip, dlogits, dvalues, ctx->d_partials, ctx->d_counters + CNT_LOSS, stats,

@@ -61,17 +61,22 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// every lane of the warp polls (each lane's own acquire orders its later loads); false on timeout
+// lane 0 polls with acquire loads, the warp barrier then orders the other lanes' reads after it;
+// false on timeout (warp-uniform)
 __device__ __forceinline__ bool wait_count(const unsigned* cnt, unsigned target, int* err) {
-  if (ld_acquire_gpu(cnt) >= target) return true;
-  const uint64_t t0 = globaltimer();
-  for (int i = 0;; ++i) {
-    if (ld_acquire_gpu(cnt) >= target) return true;
-    if ((i & 255) == 255 && globaltimer() - t0 > kTimeoutNs) {
-      atomicOr(err, ERR_BIT_COMM);
-      return false;
+  int ok = 1;
+  if ((threadIdx.x & 31) == 0 && ld_acquire_gpu(cnt) < target) {
+    const uint64_t t0 = globaltimer();
+    for (int i = 0;; ++i) {
+      if (ld_acquire_gpu(cnt) >= target) break;
+      if ((i & 255) == 255 && globaltimer() - t0 > kTimeoutNs) {
+        atomicOr(err, ERR_BIT_COMM);
+        ok = 0;
+        break;
+      }
     }
   }
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 
 // ------------------------------------------------------------------ forward

@@ -208,6 +208,9 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
   const int tiles = a.tiles_m * a.tiles_n * max(1, a.nphase);
+  // PDL: barriers, TMEM and the tensor-map prefetch above overlap the predecessor's tail; nothing it
+  // writes is read before this point
+  pdl_enter();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -505,7 +508,7 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min
     for (int q = 0; q < std::max(1, (int)a.nphase); ++q) taps += a.ntap[q];
     ctx->flops[DDPPO_K_CONV] += 2.0 * a.M * a.N * (MODE == TC_FWD ? taps * a.C : (double)a.Ho * a.Wo * a.F);
   }
-  kern<<<grid, kThreadsTC, Cfg::kSmem, st>>>(maps[0], maps[1], maps[2], maps[3], a);
+  launch_k(ctx, kern, grid, kThreadsTC, Cfg::kSmem, st, maps[0], maps[1], maps[2], maps[3], a);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }

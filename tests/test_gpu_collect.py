@@ -31,16 +31,17 @@ def rel_l2(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def _params(arch, seed):
-    desc = dd.model_desc(arch)
+def _params(arch, seed, hidden=None):
+    desc = dd.model_desc(arch, hidden)
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     return desc, synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, seed)
 
 
-@pytest.mark.parametrize("arch,E", [("gps", 4), ("gps", 13), ("depth", 4), ("depth", 12), ("rgbd", 3)])
-def test_policy_act_matches_oracle_step(ctx, arch, E):
-    desc, p0 = _params(arch, 2)
+@pytest.mark.parametrize("arch,E,hidden", [("gps", 4, None), ("gps", 13, None), ("depth", 4, None), ("depth", 12, None),
+                                           ("rgbd", 3, None), ("depth", 5, 1024)])  # NEXT-3's 1024-d LSTM
+def test_policy_act_matches_oracle_step(ctx, arch, E, hidden):
+    desc, p0 = _params(arch, 2, hidden)
     H = desc.hidden
     layers = 2 if arch == "rgbd" else 1
     vis = arch != "gps"
@@ -72,7 +73,7 @@ def test_policy_act_matches_oracle_step(ctx, arch, E):
              "mask": m.reshape(E, 1).astype(np.float64), "h0": h0.astype(np.float64)}
     if vis:
         batch.update(obs=frames[:, None].astype(np.float64), c0=c0.astype(np.float64))
-    lo, vo, cache = models.forward(arch, p0, batch)
+    lo, vo, cache = models.forward(arch, p0, batch, hidden=H)
     lim = 1e-3 if vis else 2e-2
     assert rel_l2(lg.cpu().numpy(), lo[:, 0]) < lim and rel_l2(vals.cpu().numpy(), vo[:, 0]) < lim
     ho, co = h_out.cpu().numpy(), c_out.cpu().numpy()

@@ -11,11 +11,13 @@ from paper_1911_00357_b200.learner import Learner
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "depth"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+hidden = int(sys.argv[3]) if len(sys.argv) > 3 else None  # e.g. 1024: the NEXT-3 LSTM on this config
 ctx = dd.Context(0, 1)
 c = synth.CONFIGS[cfg]
-desc = dd.model_desc(c["arch"]); lay = dd.param_layout(desc); P = dd.param_count(desc)
+desc = dd.model_desc(c["arch"], hidden or c["hidden"]); lay = dd.param_layout(desc); P = dd.param_count(desc)
 p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 0)
-lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, normalize_adv=True)
+lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], hidden=desc.hidden, params=p0,
+              normalize_adv=True)
 ro = synth.rollout(c["E"], c["T"], 0, hidden=desc.hidden, obs_shape=c.get("obs"), rnn_layers=c.get("rnn_layers", 1))
 pm = synth.perms(0, 0, c["epochs"], c["E"])
 lrn.load_rollout(ro, pm)

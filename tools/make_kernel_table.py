@@ -72,7 +72,7 @@ for short, a in sorted(agg.items(), key=lambda kv: -kv[1][1])[:12]:
 out = {k: {"bytes_per_launch": sum(v) / len(v), "launches": len(v)} for k, v in traffic.items()}
 os.makedirs("profiles", exist_ok=True)
 with open(f"profiles/r02_kernels_{cfg}.md", "w") as f:
-    f.write(f"# ncu --set full, {cfg} learner step ({len(data)} launches captured; ncu replays each launch with\n"
+    f.write(f"# ncu (sections SpeedOfLight, ComputeWorkloadAnalysis, MemoryWorkloadAnalysis + DRAM bytes + tensor pipe), {cfg} learner step ({len(data)} launches captured; ncu replays each launch with\n"
             "# cold caches and serialised: compare shares, not absolute times)\n\n")
     f.write("tensor pipe % = sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active (tensor-pipe busy "
             "cycles over the active SMs' cycles);\n"

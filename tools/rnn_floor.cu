@@ -7,7 +7,10 @@
 //           4 accumulators, commit, wait, tcgen05.ld of the accumulators, __syncthreads
 //   mode 2  mode 0 + mode 1 in sequence (the r1 step skeleton)
 //   mode 3  mode 2 with the MMAs of each group of 4 source CTAs issued as soon as that group's
-//           slices arrived (per-group mbarriers) -- the overlap the r2 recurrences use
+//           slices arrived (per-group mbarriers)
+//   mode 4  MMA chain only, ONE warp issuing all 32 MMAs into one accumulator (one commit)
+//   mode 5  MMA chain only, 2 warps x 16 MMAs
+//   mode 6  MMA chain only, 8 warps x 4 MMAs into 8 accumulators (each reader sums 8)
 //
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1911_00357_b200/csrc \
 //          tools/rnn_floor.cu -o tools/rnn_floor
@@ -52,7 +55,7 @@ __global__ void __launch_bounds__(kThreads, 1) floor_kernel(int T, int B, int N,
   if (tid == 0) {
     for (int p = 0; p < 2; ++p)
       for (int g = 0; g < groups; ++g) mbar_init(&sm.bar[p][g], 1);
-    mbar_init(&sm.mma_bar, 4);
+    mbar_init(&sm.mma_bar, MODE == 4 ? 1 : MODE == 5 ? 2 : MODE == 6 ? 8 : 4);
     fence_mbar_init_cluster();
   }
   if (warp == 0) tmem_alloc<512>(&sm.tmem_slot);
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1) floor_kernel(int T, int B, int N,
   const uint64_t g0 = gtimer();
   for (int t = 0; t < T; ++t) {
     const int cur = t & 1;
-    if (MODE != 1 && t > 0 && warp < 4) {
+    if (MODE != 1 && MODE < 4 && t > 0 && warp < 4) {
       if (MODE == 3) {
         if (lane == 0) mbar_arrive_expect_tx(&sm.bar[cur][warp], tx_grp);
         mbar_wait_parity(&sm.bar[cur][warp], (uint32_t)(((t - 1) >> 1) & 1));
@@ -102,7 +105,48 @@ __global__ void __launch_bounds__(kThreads, 1) floor_kernel(int T, int B, int N,
       }
     }
     if (MODE == 0) __syncthreads();  // gate warps >= 4 (B = 8) wait for the slices too
-    if (MODE != 0) {
+    if (MODE == 6) {
+      tc_fence_after();
+      const uint64_t bd0 = umma_desc(h_base0 + (uint32_t)cur * parity_bytes, 128, kSBO);
+      const uint32_t d_acc = tmem + 256u + 16u * (uint32_t)warp;
+      for (int j = 0; j < nmma / 8; ++j) {
+        const int kk = warp + 8 * j;
+        mma_ts(d_acc, tmem + 8u * (uint32_t)kk, bd0 + (uint64_t)(16 * kk), idesc, (uint32_t)j);
+      }
+      mma_commit(&sm.mma_bar);
+      if (warp < 4) {
+        mbar_wait_parity(&sm.mma_bar, (uint32_t)(t & 1));
+        tc_fence_after();
+        uint32_t v[8][8];
+        for (int a = 0; a < 8; ++a) tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + 256u + 16u * (uint32_t)a, v[a]);
+        tmem_wait_ld();
+        if (v[0][0] == 12345u && v[7][7] == 54321u) out[1] = 1;
+        tc_fence_before();
+      }
+      __syncthreads();
+    } else if (MODE >= 4) {
+      const int nw = MODE == 4 ? 1 : 2;
+      if (warp < nw) {
+        tc_fence_after();
+        const uint64_t bd0 = umma_desc(h_base0 + (uint32_t)cur * parity_bytes, 128, kSBO);
+        const uint32_t d_acc = tmem + 256u + 16u * (uint32_t)warp;
+        for (int j = 0; j < nmma / nw; ++j) {
+          const int kk = warp * (nmma / nw) + j;
+          mma_ts(d_acc, tmem + 8u * (uint32_t)kk, bd0 + (uint64_t)(16 * kk), idesc, (uint32_t)j);
+        }
+        mma_commit(&sm.mma_bar);
+      }
+      if (warp < 4) {
+        mbar_wait_parity(&sm.mma_bar, (uint32_t)(t & 1));
+        tc_fence_after();
+        uint32_t v[2][8];
+        for (int a = 0; a < nw; ++a) tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + 256u + 16u * (uint32_t)a, v[a]);
+        tmem_wait_ld();
+        if (v[0][0] == 12345u && v[nw - 1][7] == 54321u) out[1] = 1;
+        tc_fence_before();
+      }
+      __syncthreads();
+    } else if (MODE != 0) {
       if (warp < 4) {
         fence_proxy_async();
         tc_fence_after();
@@ -123,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) floor_kernel(int T, int B, int N,
       }
       __syncthreads();
     }
-    if (MODE != 1 && gate_warp && t + 1 < T) {
+    if (MODE != 1 && MODE < 4 && gate_warp && t + 1 < T) {
       __half* st = reinterpret_cast<__half*>(sm.stage[cur]) + warp * kUPC;
       st[lane] = __float2half((float)t);
       __syncwarp();
@@ -174,8 +218,9 @@ void run(int T, int B, int N, unsigned long long* d_out) {
     if ((double)h[0] / T < best_c) best_c = (double)h[0] / T;
     if ((double)h[2] / T < best_ns) best_ns = (double)h[2] / T;
   }
-  static const char* names[4] = {"exchange only", "MMA chain only", "exchange + MMA (serial)",
-                                 "exchange + MMA (per-group overlap)"};
+  static const char* names[7] = {"exchange only", "MMA chain only", "exchange + MMA (serial)",
+                                 "exchange + MMA (per-group overlap)", "MMA chain, 1 issuing warp",
+                                 "MMA chain, 2 issuing warps", "MMA chain, 8 issuing warps"};
   printf("mode %d %-36s N=%2d B=%d : %7.1f cycles/step  %7.1f ns/step\n", MODE, names[MODE], N, B, best_c, best_ns);
 }
 }  // namespace
@@ -184,6 +229,12 @@ int main() {
   unsigned long long* d_out;
   cudaMalloc(&d_out, 64);
   const int T = 4096;
+  for (int N : {16, 8}) {
+    run<4>(T, 2, N, d_out);
+    run<5>(T, 2, N, d_out);
+    run<1>(T, 2, N, d_out);
+    run<6>(T, 2, N, d_out);
+  }
   for (int B : {2, 8}) {
     run<0>(T, B, 16, d_out);
     for (int N : {16, 8}) {
