@@ -210,8 +210,8 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, size_t n, __nv_bfloa
 
 // Single-channel stem convolution in fp32 SIMT (K = k*k taps over 1 channel is too narrow for the
 // 16-byte implicit-GEMM pieces): block per frame, the frame and the weights staged in shared
-// memory; a thread computes 4 horizontally adjacent pixels x 8 output channels per work item, so
-// every weight load (float4 x 2, broadcast) feeds 32 FMAs.
+// memory; a thread computes 8 horizontally adjacent pixels x 8 output channels per work item, so
+// every weight load (float4 x 2, broadcast) feeds 64 FMAs.
 constexpr int kStemCoMax = 32;
 __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restrict__ x, const float* __restrict__ W,
                                                             int H, int Wd, int Co, int k, int s, int p, int Ho, int Wo,
@@ -225,12 +225,13 @@ __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restr
   for (int i = threadIdx.x; i < H * Wd; i += blockDim.x) xs[i] = x[(size_t)f * H * Wd + i];
   for (int i = threadIdx.x; i < Co * kk; i += blockDim.x) ws[(i % kk) * Co + i / kk] = W[i];
   __syncthreads();
-  const int og = Co / 8, jg = (Wo + 3) / 4;
+  constexpr int kPx = 8;  // horizontally adjacent output pixels per work item (x 8 channels: 64 FMAs per tap)
+  const int og = Co / 8, jg = (Wo + kPx - 1) / kPx;
   for (int item = threadIdx.x; item < Ho * jg * og; item += blockDim.x) {
-    const int o0 = (item % og) * 8, rest = item / og, j0 = (rest % jg) * 4, i = rest / jg;
-    float acc[4][8];
+    const int o0 = (item % og) * 8, rest = item / og, j0 = (rest % jg) * kPx, i = rest / jg;
+    float acc[kPx][8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < kPx; ++a)
 #pragma unroll
       for (int o = 0; o < 8; ++o) acc[a][o] = 0.f;
     for (int u = 0; u < k; ++u) {
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restr
         const float4 w1 = *reinterpret_cast<const float4*>(ws + (u * k + v) * Co + o0 + 4);
         const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < kPx; ++a) {
           const int xx = (j0 + a) * s - p + v;
           const float xv = (xx >= 0 && xx < Wd) ? xs[yy * Wd + xx] : 0.f;
 #pragma unroll
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restr
       }
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
+    for (int a = 0; a < kPx; ++a) {
       if (j0 + a >= Wo) break;
       float* yo = y + (((size_t)f * Ho + i) * Wo + j0 + a) * Co + o0;
       *reinterpret_cast<float4*>(yo) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
