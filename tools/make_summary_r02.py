@@ -30,10 +30,10 @@ for name, p in [("depth (configs[2], the metric's config)", "profiles/r02_bench_
         rows.append(line(name, p))
 scale = []
 for cfg in ("depth", "gps", "stress"):
-    for n in (1, 2, 4):
+    for n, tag in ((1, "2-GPU box"), (2, "2-GPU box"), ("1_box4", "4-GPU box"), (4, "4-GPU box")):
         p = f"profiles/r02_scale_{cfg}_n{n}.json"
         if os.path.exists(p):
-            scale.append(line(f"{cfg}", p))
+            scale.append(line(f"{cfg} ({tag})", p))
 ref = ld("profiles/r02_reference_depth.json") if os.path.exists("profiles/r02_reference_depth.json") else None
 kt = open("profiles/r02_kernels_depth.md").read().split("## First 80 launches")[0].split("## Top kernels by captured time")[1]
 floor = open("profiles/r02_rnn_floor.txt").read()
