@@ -913,47 +913,36 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ x, int F, int H, in
   }
 }
 // dx[f][y][x][c] = sum over windows whose argmax is (y, x) of dy (gather, fixed window order).
-// Thread = (input pixel, 4 channels); the <= 4 candidate windows' arg / dy loads are all issued
-// before any comparison.
+// Thread = (input pixel, 4 channels) of one frame (grid.y).
 __global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* __restrict__ arg, int F, int H, int W,
                                    int C, int Ho, int Wo, float* __restrict__ dx) {
   pdl_enter();
-  const int C4 = C >> 2, n4 = F * H * W * C4;
+  // grid (pixels x channel quads of one frame, F): no division by runtime frame sizes for the frame
+  const int C4 = C >> 2, f = blockIdx.y;
   const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i4 >= n4) return;
+  if (i4 >= H * W * C4) return;
   const int c4 = i4 % C4, pix = i4 / C4;
-  const int xx = pix % W, yq = (pix / W) % H, f = pix / (W * H);
-  // windows (ii, jj) with 2*ii - 1 + u = y, u in [0, 3)
-  uchar4 a[4];
-  float4 d[4];
-  int uv[4];
+  const int xx = pix % W, yq = pix / W;
+  // windows (ii, jj) with 2*ii - 1 + u = y, u in [0, 3): even y one window (u = 1), odd y two
+  // (u = 0, 2); the same for x / v.  q = 0..3 enumerates them with (u, v) ascending, so summing in
+  // q order is the reference order (windows by (u, v) ascending).
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    // even y: one window (u = 1); odd y: two (u = 0, 2); the same for x / v
     const int u = (yq & 1) ? 2 * (q >> 1) : 1, v = (xx & 1) ? 2 * (q & 1) : 1;
     const int yy = yq + 1 - u, xv = xx + 1 - v;
     const int ii = yy >> 1, jj = xv >> 1;
     const bool dup = (!(yq & 1) && (q >> 1)) || (!(xx & 1) && (q & 1));
-    const bool ok = !dup && yy >= 0 && xv >= 0 && ii < Ho && jj < Wo;
-    uv[q] = ok ? u * 3 + v : -1;
-    const int o = ((f * Ho + (ok ? ii : 0)) * Wo + (ok ? jj : 0)) * C + 4 * c4;
-    a[q] = ok ? *reinterpret_cast<const uchar4*>(arg + o) : make_uchar4(255, 255, 255, 255);
-    d[q] = ok ? *reinterpret_cast<const float4*>(dy + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (dup || yy < 0 || xv < 0 || ii >= Ho || jj >= Wo) continue;
+    const int o = ((f * Ho + ii) * Wo + jj) * C + 4 * c4, uv = u * 3 + v;
+    const uchar4 a = *reinterpret_cast<const uchar4*>(arg + o);
+    const float4 d = *reinterpret_cast<const float4*>(dy + o);
+    if (a.x == uv) acc[0] += d.x;
+    if (a.y == uv) acc[1] += d.y;
+    if (a.z == uv) acc[2] += d.z;
+    if (a.w == uv) acc[3] += d.w;
   }
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-  for (int u = 0; u < 3; ++u)  // the reference order: windows by (u, v) ascending
-#pragma unroll
-    for (int v = 0; v < 3; ++v)
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (uv[q] == u * 3 + v) {
-          if (a[q].x == u * 3 + v) acc[0] += d[q].x;
-          if (a[q].y == u * 3 + v) acc[1] += d[q].y;
-          if (a[q].z == u * 3 + v) acc[2] += d[q].z;
-          if (a[q].w == u * 3 + v) acc[3] += d[q].w;
-        }
-  *reinterpret_cast<float4*>(dx + pix * C + 4 * c4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  *reinterpret_cast<float4*>(dx + ((size_t)f * H * W + pix) * C + 4 * c4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
 }
 
 // NHWC [F][HW][C] <-> flat [F][C*HW] in (c, h, w) order (PyTorch flatten of NCHW)
@@ -2162,8 +2151,8 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   }
   // max-pool, then the stem (no input gradient)
   ConvGN& stem = P.convs[0];
-  launch_k(ctx, maxpool_bwd_kernel, (F * stem.Ho * stem.Wo * 8 + kThreads - 1) / kThreads, kThreads, 0, st, 
-      dz, P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
+  launch_k(ctx, maxpool_bwd_kernel, dim3((stem.Ho * stem.Wo * 8 + kThreads - 1) / kThreads, F), kThreads, 0, st, dz,
+           P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   if ((s = conv_gn_bwd(ctx, prm, grad, P, stem, da, stem.z, nullptr, 0, st)) != DDPPO_OK) return s;
@@ -2279,9 +2268,8 @@ extern "C" ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int 
                                                                                      nullptr);
   ctx->count(1);
   if (dy) {
-    launch_k(ctx, maxpool_bwd_kernel, (F * H * W * (C / 4) + kThreads - 1) / kThreads, kThreads, 0, st, dy, arg, F, H,
-             W, C, Ho,
-                                                                                          Wo, dx);
+    launch_k(ctx, maxpool_bwd_kernel, dim3((H * W * (C / 4) + kThreads - 1) / kThreads, F), kThreads, 0, st, dy, arg,
+             F, H, W, C, Ho, Wo, dx);
     ctx->count(1);
   }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());

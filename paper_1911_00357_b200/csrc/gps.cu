@@ -816,10 +816,14 @@ __global__ void head_fwd_kernel(const float* __restrict__ Wo, const float* __res
   for (int s = blockIdx.x * warps + (threadIdx.x >> 5); s < S; s += gridDim.x * warps) {
     const float* h = Hs + (size_t)s * H;
     float acc[kA1] = {0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int k = lane; k < H; k += 32) {
-      const float hv = h[k];
+#pragma unroll 4
+    for (int k = 4 * lane; k < H; k += 128) {  // H % 128 == 0: float4 per lane, all loads independent
+      const float4 hv = *reinterpret_cast<const float4*>(h + k);
 #pragma unroll
-      for (int o = 0; o < kA1; ++o) acc[o] += Wo[o * H + k] * hv;
+      for (int o = 0; o < kA1; ++o) {
+        const float4 w = *reinterpret_cast<const float4*>(Wo + o * H + k);
+        acc[o] += w.x * hv.x + w.y * hv.y + w.z * hv.z + w.w * hv.w;
+      }
     }
 #pragma unroll
     for (int o = 0; o < kA1; ++o) acc[o] = warp_sum(acc[o]);
