@@ -1903,6 +1903,7 @@ namespace {
 ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, const ddppo_batch& b, Plan& P,
                            cudaStream_t st) {
   const int F = P.F;
+  cudaStream_t prep_st = st;
   {
     WeightPrep prep;
     prep.n = 0;
@@ -1917,9 +1918,24 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
       prep.offd[prep.n + 1] = prep.offd[prep.n] + (c.wd_b ? c.Ci_real : 0);
       ++prep.n;
     }
-    launch_k(ctx, weights_prep_kernel, prep.off[prep.n] + prep.offd[prep.n], 256, 0, st, prep);
+    // the operand prep (the conv kernels' bf16 weight planes: the role of a bf16 parameter shadow)
+    // runs on the side stream beside the input prologue and (Depth) the SIMT stem + max-pool; joined
+    // before the first TMA convolution
+    if (ctx->conv_engine == DDPPO_CONV_TMA) {
+      cudaStream_t sb = nullptr;
+      ddppo_status r = ctx_side_streams(ctx, &P.side, &sb);
+      if (r != DDPPO_OK) return r;
+      DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, P.side));
+      prep_st = P.side;
+    }
+    launch_k(ctx, weights_prep_kernel, prep.off[prep.n] + prep.offd[prep.n], 256, 0, prep_st, prep);
     ctx->count(1);
   }
+  auto join_prep = [&]() -> cudaError_t {
+    if (prep_st == st) return cudaSuccess;
+    prep_st = st;
+    return fork_to(ctx, P.side, st);
+  };
   if (!P.rgbd) {
     launch_k(ctx, gather_obs_kernel, blocks_for(ctx, (size_t)F * kImg * kImg / 8), kThreads, 0, st, 
         reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, P.x0);
@@ -1930,6 +1946,7 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
         b.obs_rgb, reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, kImgRgbd, P.x0, P.x0b);
   }
   ctx->count(1);
+  if (P.convs[0].Ci != 1) DDPPO_CUDA_TRY(ctx, join_prep());  // RGB-D: the stem is a TMA convolution
   ddppo_status s = conv_gn_fwd(ctx, prm, P, P.convs[0], nullptr, 1, st);
   if (s != DDPPO_OK) return s;
   {
@@ -1939,6 +1956,7 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
         c.z, F, c.Ho, c.Wo, 32, hp, hp, P.pool_out, P.pool_arg, P.pool_b);
     ctx->count(1);
   }
+  DDPPO_CUDA_TRY(ctx, join_prep());
   for (auto& blk : P.blocks) {
     const float* sc = blk.in;
     if (blk.down >= 0) {

@@ -123,7 +123,26 @@ struct TcArgs {
   int* cnt;               // per-tile arrival counters (zero; reset by the last arrival)
   int wg, Cr;             // WGRAD: write out[o][c < Cr][tap] (PyTorch order; rows are (tap, c < C))
   int groups;             // WGRAD of a grouped conv: keep the block-diagonal entries, out[o][c % (C/g)][tap]
+  int trace;              // debug build (DDPPO_TCONV_TRACE): this launch's slot in the phase trace
 };
+
+// Debug-build phase trace (compiled out of the product library): %globaltimer stamps per CTA --
+// 0 entry, 1 prologue done, 2 past griddepcontrol.wait, 3 producer issued its last TMA, 4 first
+// accumulator ready (epilogue warp 2), 5 epilogue done, 6 exit.
+#ifdef DDPPO_TCONV_TRACE
+constexpr int kTcTraceLaunches = 1024, kTcTraceCtas = 160;
+__device__ unsigned long long g_tc_trace[kTcTraceLaunches][kTcTraceCtas][8];
+long long g_tc_meta[kTcTraceLaunches][16];
+int g_tc_next = 0;
+#define TC_STAMP(cond, k)                                                                          \
+  if ((cond) && a.trace < kTcTraceLaunches && blockIdx.x < kTcTraceCtas) {                         \
+    unsigned long long t_;                                                                         \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                         \
+    g_tc_trace[a.trace][blockIdx.x][k] = t_;                                                       \
+  }
+#else
+#define TC_STAMP(cond, k)
+#endif
 
 // first output pixel q -> im2col box coordinates (W, H, N) of its receptive field's corner
 __device__ __forceinline__ void pix_coords(const TcArgs& a, int q, int& w, int& h, int& n) {
@@ -179,6 +198,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
              const __grid_constant__ CUtensorMap mB0, const __grid_constant__ CUtensorMap mB1, const TcArgs a) {
   using Cfg = TcCfg<CS, BN, NPL, MODE, STAGES>;
+  TC_STAMP(threadIdx.x == 0, 0);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024 - (s_u32(smem_raw) & 1023)) & 1023);
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
@@ -208,9 +228,11 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
   const int tiles = a.tiles_m * a.tiles_n * max(1, a.nphase);
+  TC_STAMP(threadIdx.x == 0, 1);
   // PDL: barriers, TMEM and the tensor-map prefetch above overlap the predecessor's tail; nothing it
   // writes is read before this point
   pdl_enter();
+  TC_STAMP(threadIdx.x == 0, 2);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -260,6 +282,7 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
           }
         }
       }
+      TC_STAMP(true, 3);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -335,6 +358,7 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
         row = (f * a.OH + y) * a.OW + x;
       }
       mb_wait(&tfull[acc], aph);
+      TC_STAMP(et == 0 && wi == (int)blockIdx.x, 4);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float* prow = a.splits > 1 ? a.part + ((long long)z * a.M + row) * a.N + n0 : nullptr;
 #pragma unroll 1
@@ -400,10 +424,12 @@ tconv_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CU
       }
     }
   }
+  TC_STAMP(threadIdx.x == 64, 5);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::kTmemCols) : "memory");
+  TC_STAMP(threadIdx.x == 0, 6);
 }
 
 // ---------------------------------------------------------------- host: tensor maps
@@ -484,6 +510,9 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min
   // slot 1 = the side stream (weight gradients beside the critical path): at most a quarter of the SMs
   // (measured: 1/2 -1 %, 1/6 -1.4 %, 1/8 -4 %)
   static const int side_div = getenv("DDPPO_TCONV_SIDEDIV") ? atoi(getenv("DDPPO_TCONV_SIDEDIV")) : 4;  // A/B knob
+  // (measured: leaving the side stream's SMs free for critical-path grids while it runs -- the
+  // phase trace shows their last CTAs starting up to 15 us late -- is 0.3 % / 1.3 % slower on Depth /
+  // RGB-D: the fuller grids win)
   const int cap = slot == 0 ? ctx->sm_count * std::min(per_sm, 2) : std::max(1, ctx->sm_count / side_div);
   // split-K over the k-iterations: ~one work item per resident CTA, each >= min_iters iterations; the
   // split tiles' fixup needs every work item resident at once (n_work <= grid)
@@ -508,12 +537,43 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min
     for (int q = 0; q < std::max(1, (int)a.nphase); ++q) taps += a.ntap[q];
     ctx->flops[DDPPO_K_CONV] += 2.0 * a.M * a.N * (MODE == TC_FWD ? taps * a.C : (double)a.Ho * a.Wo * a.F);
   }
+#ifdef DDPPO_TCONV_TRACE
+  {
+    const int next = g_tc_next++;
+    a.trace = next;
+    if (next < kTcTraceLaunches) {
+      long long* m = g_tc_meta[next];
+      m[0] = MODE; m[1] = CS; m[2] = BN; m[3] = NPL; m[4] = a.M; m[5] = a.N; m[6] = a.n_k; m[7] = a.kper;
+      m[8] = a.n_work; m[9] = grid; m[10] = slot; m[11] = splits;
+    }
+  }
+#else
+  a.trace = 0;
+#endif
   launch_k(ctx, kern, grid, kThreadsTC, Cfg::kSmem, st, maps[0], maps[1], maps[2], maps[3], a);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
 }
 
 }  // namespace
+
+#ifdef DDPPO_TCONV_TRACE
+extern "C" int ddppo_debug_tconv_trace(unsigned long long* host, long long* meta, int n) {
+  memcpy(meta, g_tc_meta, sizeof(long long) * 16 * (size_t)std::min(n, kTcTraceLaunches));
+  return (int)cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(unsigned long long) * kTcTraceCtas * 8 *
+                                                         (size_t)std::min(n, kTcTraceLaunches));
+}
+#endif
+
+// N tile of FPROP / DGRAD (tiles_m = 128-row M tiles)
+// (measured: RGB-D +0.9 %, Depth unchanged -- none of its layers has 148 128-wide tiles; 128 for
+// every N >= 128: Depth -3 %, RGB-D +1.7 %)
+static int bn_for(const ddppo_ctx* ctx, int N, int tiles_m) {
+  if (N <= 32) return 32;
+  if (N <= 64) return 64;
+  if (!ctx->tconv_bn64) return 128;
+  return (long long)tiles_m * ((N + 127) / 128) >= ctx->sm_count ? 128 : 64;
+}
 
 // FPROP (flip = 0) or stride-1 DGRAD (flip = 1) over x[F][H][W][C]:
 //   out[q][o] (+)= sum_{tap, c} x[q @ tap][c] w[o][tap*C + c],  q over the F x Ho x Wo output grid.
@@ -531,9 +591,10 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
                 "tconv: 16-byte aligned operands required");
   const int Ho = (H + 2 * p - k) / s + 1, Wo = (W + 2 * p - k) / s + 1;
   const int cs = C % 64 == 0 ? 64 : 32;
-  // N tiles of at most 64 columns: twice the tiles of 128-wide ones for the small-M deep layers (less
-  // split-K) and deeper rings (a 64-column stage is 3/4 the bytes) -- measured faster
-  const int bn = N <= 32 ? 32 : (N <= 64 || ctx->tconv_bn64) ? 64 : 128;
+  // N tile: 64 columns for the small-M deep layers (twice the tiles: less split-K, deeper rings);
+  // 128 once 128-wide tiles alone fill a wave of the SMs (each A box then feeds twice the columns:
+  // half the im2col re-reads) -- measured, DESIGN.md §7
+  const int bn = bn_for(ctx, N, (F * Ho * Wo + kBM - 1) / kBM);
   TcArgs a = {};
   a.M = F * Ho * Wo;
   a.N = N;
@@ -640,7 +701,7 @@ ddppo_status launch_tconv_dgrad_s2(ddppo_ctx* ctx, const __nv_bfloat16* dy, int6
   DDPPO_REQUIRE(ctx, ((uintptr_t)dy & 15) == 0 && ((uintptr_t)wd & 15) == 0 && ((uintptr_t)dx & 15) == 0,
                 "tconv dgrad s2: 16-byte aligned operands required");
   const int cs = Co % 64 == 0 ? 64 : 32;
-  const int bn = Ci <= 32 ? 32 : (Ci <= 64 || ctx->tconv_bn64) ? 64 : 128;
+  const int bn = bn_for(ctx, Ci, (F * Ho * Wo + kBM - 1) / kBM);
   TcArgs a = {};
   a.M = F * Ho * Wo;
   a.N = Ci;
