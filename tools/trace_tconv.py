@@ -57,7 +57,7 @@ for i in range(n - per, n):
     dur = (t[:, 6].max() - t0.min()) / 1e3
     tot += dur
     rel = lambda k: np.median(t[:, k] - t0) / 1e3  # noqa: E731
-    names = {0: "FPROP", 1: "WGRAD"}
+    names = {0: "FPROP", 1: "WGRAD", 2: "HALO"}
     print(f"{names.get(int(m[0]), m[0]):>5} {m[1]:3d} {m[2]:3d} {m[3]:2d} {m[4]:7d} {m[5]:4d} {m[6]:4d} {m[7]:4d} {m[8]:5d} "
           f"{m[9]:4d} {m[10]:4d} {m[11]:3d} | {dur:6.1f} {(t0.max() - t0.min()) / 1e3:5.1f} {rel(1):5.1f} {rel(2):5.1f} "
           f"{rel(4):6.1f} {rel(5):6.1f} {rel(6):6.1f}")
