@@ -334,7 +334,8 @@ ddppo_status launch_splitk_reduce_wgrad(ddppo_ctx* ctx, const float* part, int s
 ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xplane, int F, int H, int W, int C,
                               int k, int s, int p, int flip, const __nv_bfloat16* w, int64_t wplane, int N, int planes,
                               float* out, int64_t ldc, int accumulate, float* partial, int max_splits, int slot,
-                              int* splits_out, cudaStream_t st);
+                              int* splits_out, cudaStream_t st, const float* res = nullptr,
+                              const float* res_mask = nullptr);
 ddppo_status launch_tconv_dgrad_s2(ddppo_ctx* ctx, const __nv_bfloat16* dy, int64_t dy_plane, int F, int Ho, int Wo,
                                    int Co, int H, int W, int Ci, int k, int p, const __nv_bfloat16* wd,
                                    int64_t wd_plane, int planes, float* dx, int accumulate, cudaStream_t st);

@@ -1584,9 +1584,11 @@ ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const
 }
 
 // dx (+)= input gradient of the convolution (not for the stem)
+// res != nullptr: dx = dgrad + (res_mask > 0 ? res : 0) (accumulate_dx must be 0): the TMA engine adds
+// it in the conv epilogue, the other paths write the masked residual first and accumulate onto it
 ddppo_status conv_dgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* w, const __nv_bfloat16* wd_b,
                         const __nv_bfloat16* dy, float* dx, int accumulate_dx, const ConvScratch& sc, cudaStream_t st,
-                        int planes = 1) {
+                        int planes = 1, const float* res = nullptr, const float* res_mask = nullptr) {
   DDPPO_REQUIRE(ctx, !is_stem(g), "stem conv: no input gradient");
   DDPPO_REQUIRE(ctx, planes == 1 || wd_b, "conv: hi / lo input gradients need prepared weights");
   const int64_t dy_plane = planes == 2 ? (int64_t)g.M() * g.Co : 0, wd_plane = planes == 2 ? (int64_t)g.Co * g.K() : 0;
@@ -1607,9 +1609,16 @@ ddppo_status conv_dgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* w, const
     const int Md = g.F * g.H * g.W;
     ddppo_status r = launch_tconv_fwd(ctx, dy, dy_plane, g.F, g.Ho, g.Wo, g.Co, g.k, 1, g.k - 1 - g.p, 1, wd_b,
                                       wd_plane, g.Ci, planes, dx, g.Ci, accumulate_dx, sc.part,
-                                      split_cap(sc, Md, g.Ci, 16), sc.slot, &splits, st);
+                                      split_cap(sc, Md, g.Ci, 16), sc.slot, &splits, st, res, res_mask);
     if (r != DDPPO_OK || splits == 1) return r;
     return launch_splitk_reduce(ctx, sc.part, splits, (int64_t)Md * g.Ci, Md, g.Ci, dx, g.Ci, accumulate_dx, st);
+  }
+  if (res) {  // the other engines: the masked residual first, then accumulate onto it
+    const size_t n = (size_t)g.F * g.H * g.W * g.Ci;
+    launch_k(ctx, relu_mask_kernel, blocks_for(ctx, n), kThreads, 0, st, res, res_mask, n, dx);
+    ctx->count(1);
+    DDPPO_CUDA_TRY(ctx, cudaGetLastError());
+    accumulate_dx = 1;
   }
   if (ctx->conv_engine == DDPPO_CONV_TMA && g.s == 2 && g.Co % 32 == 0 && g.k <= 3 && g.Ci % 8 == 0 &&
       g.k <= g.p + 2) {
@@ -1805,7 +1814,8 @@ ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, c
 // The weight gradient only feeds a8, so with a side stream it leaves the critical path: it is
 // forked after the GN backward (its own dy buffer and partials) and joined once after the backward.
 ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P, ConvGN& c, const float* dz,
-                         const float* relu_z, float* dx, int accumulate_dx, cudaStream_t st) {
+                         const float* relu_z, float* dx, int accumulate_dx, cudaStream_t st, const float* res = nullptr,
+                         const float* res_mask = nullptr) {
   const size_t lo = P.grad_planes == 2 ? (size_t)P.F * c.Ho * c.Wo * c.Co : 0;
   ddppo_status s = gn_bwd(ctx, P.F, c.Ho * c.Wo, c.Co, dz, relu_z, c.y, c.stats, prm + c.gw, c.dyb, grad + c.gw,
                           grad + c.gb, c.gn_part, P.gn_gpart, st, /*reduce_params=*/false, lo);
@@ -1819,7 +1829,8 @@ ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P,
     s = conv_wgrad(ctx, g, c.x, c.xb, c.dyb, grad + c.w, scratch_of(P), st);
   }
   if (s != DDPPO_OK || dx == nullptr) return s;
-  return conv_dgrad(ctx, g, prm + c.w, c.wd_b, c.dyb, dx, accumulate_dx, scratch_of(P), st, P.grad_planes);
+  return conv_dgrad(ctx, g, prm + c.w, c.wd_b, c.dyb, dx, accumulate_dx, scratch_of(P), st, P.grad_planes, res,
+                    res_mask);
 }
 
 // gemm_tc with split-K chosen so that small-M / long-K GEMMs still fill the GPU (partials in P.part)
@@ -2123,9 +2134,12 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     const Plan::Block& blk = P.blocks[bi];
     ConvGN& last = P.convs[blk.main.back()];
     // out = relu(gn_last(conv_last(...)) (* SE) + shortcut(in)); the ReLU mask of the sum is `out`
+    // identity shortcut of a two-conv block: the first conv's input-gradient epilogue adds the masked
+    // shortcut gradient (dz stays intact until then); otherwise it is written first and accumulated onto
+    const bool fuse_res = blk.down < 0 && blk.main.size() == 2 && !blk.se;
     if (blk.down >= 0) {
       if ((s = conv_gn_bwd(ctx, prm, grad, P, P.convs[blk.down], dz, blk.out, dn, 0, st)) != DDPPO_OK) return s;
-    } else {
+    } else if (!fuse_res) {
       const size_t n = (size_t)F * last.Ho * last.Wo * last.Co;
       launch_k(ctx, relu_mask_kernel, blocks_for(ctx, n), kThreads, 0, st, dz, blk.out, n, dn);
       ctx->count(1);
@@ -2159,7 +2173,11 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
       const bool first = j == 0;
       float* target = first ? dn : g_out;
       const float* relu_z = (j + 1 == (int)blk.main.size()) ? (blk.se ? nullptr : blk.out) : c.z;
-      if ((s = conv_gn_bwd(ctx, prm, grad, P, c, g_in, relu_z, target, first ? 1 : 0, st)) != DDPPO_OK) return s;
+      if (first && fuse_res)
+        s = conv_gn_bwd(ctx, prm, grad, P, c, g_in, relu_z, target, 0, st, dz, blk.out);
+      else
+        s = conv_gn_bwd(ctx, prm, grad, P, c, g_in, relu_z, target, first ? 1 : 0, st);
+      if (s != DDPPO_OK) return s;
       if (!first) {
         std::swap(g_in, g_out);  // g_in <- this conv's input gradient; g_out <- a free buffer
         if (g_out == dn) g_out = (g_in == dz) ? da : dz;

@@ -124,6 +124,9 @@ struct TcArgs {
   int wg, Cr;             // WGRAD: write out[o][c < Cr][tap] (PyTorch order; rows are (tap, c < C))
   int groups;             // WGRAD of a grouped conv: keep the block-diagonal entries, out[o][c % (C/g)][tap]
   int trace;              // debug build (DDPPO_TCONV_TRACE): this launch's slot in the phase trace
+  // FPROP / DGRAD: out = result + (res_mask > 0 ? res : 0) (a residual block's ReLU-masked shortcut
+  // gradient added in the epilogue; res == nullptr: off)
+  const float *res, *res_mask;
 };
 
 // Debug-build phase trace (compiled out of the product library): %globaltimer stamps per CTA --
@@ -160,7 +163,16 @@ __device__ __forceinline__ void store_final(const TcArgs& a, int row, int col, c
   if (!a.wg) {
     float4* o = reinterpret_cast<float4*>(a.out + (long long)row * a.ldc + col);
     float4 v0 = make_float4(v[0], v[1], v[2], v[3]), v1 = make_float4(v[4], v[5], v[6], v[7]);
-    if (a.accumulate) {
+    if (a.res) {
+      const long long o8 = (long long)row * a.ldc + col;
+      const float4 r0 = *reinterpret_cast<const float4*>(a.res + o8), r1 = *reinterpret_cast<const float4*>(a.res + o8 + 4);
+      const float4 m0 = *reinterpret_cast<const float4*>(a.res_mask + o8),
+                   m1 = *reinterpret_cast<const float4*>(a.res_mask + o8 + 4);
+      v0.x += m0.x > 0.f ? r0.x : 0.f; v0.y += m0.y > 0.f ? r0.y : 0.f;
+      v0.z += m0.z > 0.f ? r0.z : 0.f; v0.w += m0.w > 0.f ? r0.w : 0.f;
+      v1.x += m1.x > 0.f ? r1.x : 0.f; v1.y += m1.y > 0.f ? r1.y : 0.f;
+      v1.z += m1.z > 0.f ? r1.z : 0.f; v1.w += m1.w > 0.f ? r1.w : 0.f;
+    } else if (a.accumulate) {
       const float4 p0 = o[0], p1 = o[1];
       v0.x += p0.x; v0.y += p0.y; v0.z += p0.z; v0.w += p0.w;
       v1.x += p1.x; v1.y += p1.y; v1.z += p1.z; v1.w += p1.w;
@@ -583,8 +595,10 @@ static int bn_for(const ddppo_ctx* ctx, int N, int tiles_m) {
 ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xplane, int F, int H, int W, int C,
                               int k, int s, int p, int flip, const __nv_bfloat16* w, int64_t wplane, int N, int planes,
                               float* out, int64_t ldc, int accumulate, float* partial, int max_splits, int slot,
-                              int* splits_out, cudaStream_t st) {
+                              int* splits_out, cudaStream_t st, const float* res, const float* res_mask) {
   DDPPO_REQUIRE(ctx, C % 32 == 0 && N % 8 == 0 && ldc % 4 == 0, "tconv: C % 32 == 0, N % 8 == 0 required");
+  DDPPO_REQUIRE(ctx, !res || (res_mask && !accumulate && ((uintptr_t)res & 15) == 0 && ((uintptr_t)res_mask & 15) == 0),
+                "tconv: the masked residual needs 16-byte aligned res / res_mask and no accumulation");
   DDPPO_REQUIRE(ctx, !flip || s == 1, "tconv: transposed taps only for stride-1 convolutions");
   DDPPO_REQUIRE(ctx, k <= 3, "tconv: kernels up to 3x3 (tap lists)");
   DDPPO_REQUIRE(ctx, ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0 && ((uintptr_t)out & 15) == 0,
@@ -622,6 +636,8 @@ ddppo_status launch_tconv_fwd(ddppo_ctx* ctx, const __nv_bfloat16* x, int64_t xp
   a.part = partial;
   a.cnt = ctx->d_tile_cnt + (size_t)slot * (kMaxTileCounters / 2);
   a.accumulate = accumulate;
+  a.res = res;
+  a.res_mask = res_mask;
   if (splits_out) *splits_out = 1;  // the split sum happens inside the kernel
   CUtensorMap maps[4];
   memset(maps, 0, sizeof(maps));
