@@ -650,22 +650,28 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths, frozen):
 
 
 # ------------------------------------------------------------------ CUDA-graph replay of the learner step
-@pytest.mark.parametrize("cfgname", ["gps", "toy"])
-def test_learner_graph_replay_matches_eager(dd, ctx, cfgname):
+@pytest.mark.parametrize("cfgname,hidden", [("gps", None), ("toy", None), ("depth", None), ("depth", 1024)])
+def test_learner_graph_replay_matches_eager(dd, ctx, cfgname, hidden):
     """Three learner steps: eager (graphs off) vs captured-and-replayed (the second step is captured,
-    the third replays) -- the parameters, Adam moments and loss statistics agree bit for bit."""
+    the third replays) -- the parameters, Adam moments and loss statistics agree bit for bit.  Depth
+    with the 1024-d LSTM: the 32-CTA recurrences' L2 exchange (counters reset in the graph) replays
+    deterministically too."""
     from paper_1911_00357_b200.learner import Learner
-    c = synth.CONFIGS[cfgname]
-    desc = dd.model_desc(c["arch"])
+    c = dict(synth.CONFIGS[cfgname])
+    if cfgname == "depth":
+        c.update(T=16)  # a short rollout keeps the test fast; the path is the config's
+    desc = dd.model_desc(c["arch"], hidden)
     lay = dd.param_layout(desc)
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 31)
     out = {}
     for graphs in (False, True):
         dd.ddppo_set_graphs(ctx, graphs)
-        lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], params=p0, normalize_adv=True)
+        lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], hidden=desc.hidden, params=p0,
+                      normalize_adv=True)
         for it in range(3):
-            ro = synth.rollout(c["E"], c["T"], 32, iteration=it, hidden=desc.hidden)
+            ro = synth.rollout(c["E"], c["T"], 32, iteration=it, hidden=desc.hidden, obs_shape=c.get("obs"),
+                               rnn_layers=c.get("rnn_layers", 1))
             lrn.load_rollout(ro, synth.perms(32, it, c["epochs"], c["E"]))
             lrn.step()
         torch.cuda.synchronize()
