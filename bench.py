@@ -257,7 +257,7 @@ def main():
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, args.seed)
     lrn = Learner(ctx, c["arch"], c["E"], c["T"], c["epochs"], c["minibatches"], hidden=c["hidden"], params=p0,
-                  normalize_adv=True)
+                  normalize_adv=True, rollout_buffers=2)
     stream = torch.cuda.current_stream()
     n_roll = 4  # distinct rollouts cycled through (different data every step)
     preempt = None
@@ -360,13 +360,16 @@ def main():
         h2d = pinned[0]["__arena__"].numel()
         d2h = lrn.stats.numel() * 4
         # a training loop's shape: step i+1 is enqueued before step i's statistics are read back (two
-        # statistics buffers, D2H on a copy stream after step i's completion event)
+        # statistics buffers, D2H on a copy stream after step i's completion event); the rollout H2D
+        # copies run on their own stream into the arena the previous step is not reading (two device
+        # arenas), so step i+1's input transfer overlaps step i
         stats_dev = [torch.zeros_like(lrn.stats) for _ in range(2)]
         stats_host = [torch.zeros(lrn.stats.shape, dtype=lrn.stats.dtype).pin_memory() for _ in range(2)]
         copy_stream = torch.cuda.Stream()
+        h2d_stream = torch.cuda.Stream()
         done = [torch.cuda.Event() for _ in range(2)]
-        for i in range(2):  # warm the loop's own buffers (not timed)
-            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True)
+        for i in range(4):  # warm the loop's own buffers and graph keys (2 arenas x 2 uses; not timed)
+            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d_stream)
             lrn.step(stream, stats=stats_dev[i % 2])
             dd.ddppo_allreduce_counts(ctx, [lrn.steps_per_rollout()])
         barrier()
@@ -374,7 +377,7 @@ def main():
         e_exp = 0
         e0.record(stream)
         for i in range(args.steps):
-            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True)
+            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d_stream)
             lrn.step(stream, stats=stats_dev[i % 2])
             copy_stream.wait_stream(stream)
             with torch.cuda.stream(copy_stream):

@@ -29,7 +29,7 @@ class Learner:
     turns it on explicitly."""
     def __init__(self, ctx, arch, E, T, epochs=2, minibatches=2, hidden=None, params=None, device="cuda",
                  normalize_adv=False, use_value_clip=True, lr=2.5e-4, max_grad_norm=0.5, ld=None, adam_eps=1e-8,
-                 peer=True, freeze_encoder=False, freeze_mask=None):
+                 peer=True, freeze_encoder=False, freeze_mask=None, rollout_buffers=1):
         self.ctx, self.E, self.T = ctx, E, T
         self.ld = ld or ((T + 1 + 3) // 4 * 4)
         self.epochs, self.minibatches = epochs, minibatches
@@ -79,9 +79,14 @@ class Learner:
             self._layout[k] = (off, shp, dt, nbytes)
             off = (off + nbytes + 255) // 256 * 256
         self._arena_bytes = off
-        self.arena = torch.zeros(off, dtype=torch.uint8, device=dev)
-        self.dev = {k: self._view(self.arena, k) for k in shapes if k != "perms"}
-        self.perms = self._view(self.arena, "perms")
+        # rollout_buffers = 2: two device arenas, so the next rollout's H2D copy (load_rollout with a
+        # copy stream) overlaps the current learner step; each arena is its own CUDA-graph key
+        self.shapes_nop = [k for k in shapes if k != "perms"]
+        self._arenas = [torch.zeros(off, dtype=torch.uint8, device=dev) for _ in range(max(1, rollout_buffers))]
+        self._ready = [None] * len(self._arenas)   # copy-stream event: the arena holds its rollout
+        self._free = [None] * len(self._arenas)    # step-stream event: the last step reading it is done
+        self._next = 0                              # the arena load_rollout fills next
+        self._use(0)
         self.adv = torch.zeros((E, ld), **f32)
         self.ret = torch.zeros((E, ld), **f32)
         self.stats = torch.zeros((epochs * minibatches, 8), **f32)
@@ -90,6 +95,12 @@ class Learner:
         self.shapes = shapes
 
     # --------------------------------------------------------------- inputs
+    def _use(self, i):
+        self._cur = i
+        self.arena = self._arenas[i]
+        self.dev = {k: self._view(self.arena, k) for k in self.shapes_nop}
+        self.perms = self._view(self.arena, "perms")
+
     def _view(self, arena, k):
         off, shp, dt, nbytes = self._layout[k]
         return arena[off:off + nbytes].view(dt).view(shp)
@@ -110,11 +121,27 @@ class Learner:
             out.update(visual_obs(ro["obs"], self.desc.arch in (3, 4, 5)))
         return out
 
-    def load_rollout(self, ro, perms, non_blocking=False):
-        """Copy a rollout (synth dict of numpy arrays, or a pinned_host_buffers() arena) + perms to HBM."""
+    def load_rollout(self, ro, perms, non_blocking=False, copy_stream=None):
+        """Copy a rollout (synth dict of numpy arrays, or a pinned_host_buffers() arena) + perms to HBM.
+        With rollout_buffers = 2 and a packed arena, `copy_stream` carries the H2D copy into the arena
+        the next step() will read, after the step that last read that arena."""
         if "__arena__" in ro:  # packed pinned arena: perms are inside it
             ro["perms"].copy_(torch.as_tensor(np.asarray(perms, dtype=np.int32)))
-            self.arena.copy_(ro["__arena__"], non_blocking=non_blocking)
+            i = 0
+            if copy_stream is not None:  # alternate the arenas only for stream-overlapped loads
+                i = self._next
+                self._next = (i + 1) % len(self._arenas)
+            self._use(i)
+            if copy_stream is not None:
+                if self._free[i] is not None:
+                    copy_stream.wait_event(self._free[i])
+                with torch.cuda.stream(copy_stream):
+                    self.arena.copy_(ro["__arena__"], non_blocking=non_blocking)
+                    self._ready[i] = torch.cuda.Event()
+                    self._ready[i].record(copy_stream)
+            else:
+                self.arena.copy_(ro["__arena__"], non_blocking=non_blocking)
+                self._ready[i] = None
             self.host_perms[:] = ro["perms"].numpy()
             self.host_len[:] = ro["length"].numpy()
             return
@@ -152,10 +179,18 @@ class Learner:
         """One learner step (stream-ordered).  `stats` (optional [epochs*minibatches][8] CUDA tensor)
         receives the loss statistics instead of self.stats (double-buffering for pipelined reads)."""
         self.cfg.adam.step = self.adam_step
+        i = self._cur
+        st = stream if stream is not None else torch.cuda.current_stream()
+        if self._ready[i] is not None:  # the arena's H2D copy ran on a copy stream
+            st.wait_event(self._ready[i])
+            self._ready[i] = None
         self._ro = self._rollout_struct()
         out = self.stats if stats is None else stats
         self.adam_step = ddppo_learner_step(self.ctx, self.desc, self._ro, self.cfg, self.params, self.m, self.v,
                                             self.adv, self.ret, out, self.ws, stream)
+        if len(self._arenas) > 1:
+            self._free[i] = torch.cuda.Event()
+            self._free[i].record(st)
         return out
 
     def steps_per_rollout(self):
