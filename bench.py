@@ -346,6 +346,7 @@ def main():
     barrier()
     dd.profile_enable(ctx, False)
     prof = dd.profile_read(ctx, reset=True)
+    smem_bytes = dd.profile_smem_bytes(ctx, reset=True)
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -407,7 +408,7 @@ def main():
     # recurrence for GPS (sub-families "conv" / "rnn": CUDA events around each launch on its stream)
     dom = "conv" if c["arch"] in ("depth", "rgbd", "serx50", "serx101") else "rnn" if c["arch"] == "gps" else "net_fwd"
     launches = {k: v[1] for k, v in launches_timed.items()}
-    roofline = roofline_for(dom, prof, c, lrn, peaks, prof_steps)
+    roofline = roofline_for(dom, prof, c, lrn, peaks, prof_steps, smem_bytes)
     kernels = kernel_table(prof, c, lrn, peaks, prof_steps)
     gpu_launches = int(sum(v for k, v in launches.items() if k != "allreduce"))
 
@@ -496,7 +497,7 @@ def _traffic_r02(kind):
     return t.get(kind, {}).get("bytes_per_launch")
 
 
-def roofline_for(fam, prof, c, lrn, peaks, steps):
+def roofline_for(fam, prof, c, lrn, peaks, steps, smem_bytes=None):
     """The dominant kernel: its algorithmic work (host-side accounting at each launch: useful dense
     FLOPs, the bf16x3 forward counted once) / its device time (CUDA events around every launch on
     the launching stream, the eager profiling pass), against the measured sustained bf16 peak."""
@@ -512,12 +513,20 @@ def roofline_for(fam, prof, c, lrn, peaks, steps):
            "launches_per_step": n / max(steps, 1), "flops_per_launch": flops / max(n, 1),
            "share_of_step": ms / max(sum(v[0] for k, v in prof.items() if k in (
                "gae", "adv_norm", "net_fwd", "head", "loss", "net_bwd", "wgrad", "allreduce", "adam", "other")), 1e-9)}
+    if smem_bytes and smem_bytes.get(fam, 0) > 0:
+        # the binding resource of the conv kernels for N <= 64: shared-memory traffic
+        # (TMA operand writes + the bf16x3 MMAs' operand reads) against 128 B / cycle / SM at the max
+        # SM clock over the whole chip (side-stream launches use a quarter of the SMs: a lower bound)
+        sm_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        sm_ach = smem_bytes[fam] / max(ms / 1e3, 1e-12) / 1e12
+        out["smem"] = {"achieved": sm_ach, "peak": sm_peak, "unit": "TB/s", "frac": sm_ach / sm_peak,
+                       "bytes_per_launch": smem_bytes[fam] / max(n, 1)}
     if fam == "rnn":
         out["note"] = ("latency-bound dependency chain (B = E/2 envs x 128 steps on one 16-CTA cluster); "
                        "per-step phases in DESIGN.md")
     else:
-        out["note"] = ("small implicit GEMMs (N = 32..256, <= 512 tiles) latency / launch bound; per-kernel "
-                       "table in 'kernels' and profiles/r02_kernels_depth.md")
+        out["note"] = ("small implicit GEMMs (N = 32..256, <= 512 tiles): shared-memory-bandwidth bound for "
+                       "N <= 64 ('smem'), per-kernel table in 'kernels' and profiles/r02_kernels_depth.md")
     return out
 
 

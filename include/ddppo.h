@@ -414,6 +414,11 @@ ddppo_status ddppo_profile_read(ddppo_ctx* ctx, double* host_ms /* [DDPPO_K_COUN
  * dense-contraction FLOPs, 2*M*N*K with the bf16x3 forward counted once; counted while profiling
  * is enabled, i.e. for eager launches).  reset != 0 clears. */
 ddppo_status ddppo_profile_flops(ddppo_ctx* ctx, double* host_flops /* [DDPPO_K_COUNT] */, int reset);
+/* Shared-memory traffic of the TMA conv kernels per family since the last reset (same accounting
+ * mode): per k-iteration the TMA's operand writes (A and B, every plane) plus the tcgen05.mma operand
+ * reads (bf16x3: three products; SM100 MMA reads A and B from shared memory) -- the conv kernels'
+ * binding resource for N <= 64.  reset != 0 clears. */
+ddppo_status ddppo_profile_smem_bytes(ddppo_ctx* ctx, double* host_bytes /* [DDPPO_K_COUNT] */, int reset);
 
 /* Diagnostic entry to the tcgen05 GEMM used inside the backward (stream-ordered):
  * C[m][n] = sum_k A[m*sam + k*sak] * B[n*sbn + k*sbk]; operands rounded to bf16, fp32 accumulate

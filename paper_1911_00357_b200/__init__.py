@@ -280,6 +280,14 @@ def profile_read(ctx, reset=False):
     return {k: (ms[i], la[i], fl[i]) for i, k in enumerate(_lib.KERNEL_FAMILIES)}
 
 
+def profile_smem_bytes(ctx, reset=False):
+    """{family: shared-memory bytes moved by the tensor-core conv kernels} since the last reset."""
+    n = len(_lib.KERNEL_FAMILIES)
+    b = (ctypes.c_double * n)()
+    _call(ctx, "ddppo_profile_smem_bytes", b, int(reset))
+    return {k: b[i] for i, k in enumerate(_lib.KERNEL_FAMILIES)}
+
+
 def ddppo_set_graphs(ctx, enable=True):
     """CUDA-graph replay of ddppo_learner_step (default on; eager while profiling)."""
     _call(ctx, "ddppo_set_graphs", int(enable))

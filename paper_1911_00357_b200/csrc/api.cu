@@ -812,6 +812,15 @@ ddppo_status ddppo_profile_flops(ddppo_ctx* ctx, double* host_flops, int reset) 
   return DDPPO_OK;
 }
 
+ddppo_status ddppo_profile_smem_bytes(ddppo_ctx* ctx, double* host_bytes, int reset) {
+  if (!ctx) return DDPPO_ERR_CONFIG;
+  for (int i = 0; i < DDPPO_K_COUNT; ++i) {
+    if (host_bytes) host_bytes[i] = ctx->smem_bytes[i];
+    if (reset) ctx->smem_bytes[i] = 0.0;
+  }
+  return DDPPO_OK;
+}
+
 ddppo_status ddppo_profile_read(ddppo_ctx* ctx, double* host_ms, int64_t* host_launches, int reset) {
   if (!ctx) return DDPPO_ERR_CONFIG;
   for (auto& r : ctx->pending) {

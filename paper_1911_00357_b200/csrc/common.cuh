@@ -60,6 +60,7 @@ struct ddppo_ctx {
   int64_t launches[DDPPO_K_COUNT] = {};
   double ms[DDPPO_K_COUNT] = {};
   double flops[DDPPO_K_COUNT] = {};            // algorithmic FLOPs issued (profiling mode)
+  double smem_bytes[DDPPO_K_COUNT] = {};       // shared-memory bytes moved by the tensor-core kernels (idem)
   int cur_fam = DDPPO_K_OTHER;                 // family of the innermost open ProfScope
   void count(int n) { launches[cur_fam] += n; }  // launches made by shared launchers
   struct Rec { int fam; cudaEvent_t a, b; };

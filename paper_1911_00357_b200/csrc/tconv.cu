@@ -548,6 +548,12 @@ ddppo_status run(ddppo_ctx* ctx, const CUtensorMap (&maps)[4], TcArgs a, int min
     double taps = 0;
     for (int q = 0; q < std::max(1, (int)a.nphase); ++q) taps += a.ntap[q];
     ctx->flops[DDPPO_K_CONV] += 2.0 * a.M * a.N * (MODE == TC_FWD ? taps * a.C : (double)a.Ho * a.Wo * a.F);
+    // shared-memory traffic: every k-iteration of every tile (splits partition the iterations) has
+    // the TMA write its stage and the MMAs read A (128 x 16) and B (BN x 16) bf16 per K = 16 step, once
+    // per product (bf16x3: 3)
+    const double iters = (double)a.tiles_m * a.tiles_n * (MODE == TC_FWD ? taps * a.nsl : (double)a.n_k);
+    const double k16 = MODE == TC_FWD ? CS / 16 : kPix / 16, prods = NPL == 2 ? 3 : 1;
+    ctx->smem_bytes[DDPPO_K_CONV] += iters * (Cfg::kStage + k16 * prods * (kBM * 16 * 2 + BN * 16 * 2));
   }
 #ifdef DDPPO_TCONV_TRACE
   {
