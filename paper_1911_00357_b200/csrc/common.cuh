@@ -434,6 +434,7 @@ struct LstmPtrs {
 };
 constexpr int kLstmWideCounters = 64;  // 4 forward group counters + 32 backward owner counters
 size_t lstm_wide_exchange_bytes();
+size_t lstm_wide_part_offset();  // byte offset of the backward's partials in the exchange buffer
 ddppo_status launch_lstm1024_fwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
 ddppo_status launch_lstm1024_bwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);
 ddppo_status launch_lstm_fwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st);

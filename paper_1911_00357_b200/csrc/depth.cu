@@ -1869,7 +1869,7 @@ LstmPtrs lstm_ptrs(const ModelLayout& L, const float* prm, const ddppo_batch& b,
   if (P.lstm_x) {
     q.hx = P.lstm_x;
     q.xcnt = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(P.lstm_x) + lstm_wide_exchange_bytes() - 256);
-    q.xpart = reinterpret_cast<float*>(reinterpret_cast<char*>(P.lstm_x) + 2 * (size_t)(P.H / 8) * 128);
+    q.xpart = reinterpret_cast<float*>(reinterpret_cast<char*>(P.lstm_x) + lstm_wide_part_offset());
   }
   q.env_idx = b.env_idx;
   q.B = b.B;

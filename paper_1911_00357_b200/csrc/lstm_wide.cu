@@ -61,6 +61,54 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// LL ("low latency") exchange words: 8 bytes = 4 bytes of payload + a 4-byte flag (the step + 1), one
+// naturally aligned 8-byte store, so a reader that sees the flag sees the payload: no release fence,
+// no counter, one L2 round trip per step.  Buffers are zeroed before every launch (flags start at 1).
+__device__ __forceinline__ void st_ll2(void* p, uint32_t d0, uint32_t d1, uint32_t flag) {  // two words
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(d0), "r"(flag), "r"(d1), "r"(flag)
+               : "memory");
+}
+__device__ __forceinline__ void st_ll1(void* p, uint32_t d0, uint32_t flag) {
+  asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(d0), "r"(flag) : "memory");
+}
+// poll a 16-byte pair of words until both carry `flag`; false after the timeout (sets ERR_BIT_COMM)
+__device__ __forceinline__ bool ld_ll2(const void* p, uint32_t flag, uint32_t& d0, uint32_t& d1, int* err) {
+  uint32_t a, f0, b, f1;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(f0), "=r"(b), "=r"(f1) : "l"(p) : "memory");
+  if (f0 != flag || f1 != flag) {
+    const uint64_t t0 = globaltimer();
+    for (int i = 0;; ++i) {
+      asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(f0), "=r"(b), "=r"(f1) : "l"(p) : "memory");
+      if (f0 == flag && f1 == flag) break;
+      if ((i & 255) == 255 && globaltimer() - t0 > kTimeoutNs) {
+        atomicOr(err, ERR_BIT_COMM);
+        return false;
+      }
+    }
+  }
+  d0 = a;
+  d1 = b;
+  return true;
+}
+__device__ __forceinline__ bool ld_ll1(const void* p, uint32_t flag, uint32_t& d0, int* err) {
+  uint32_t a, f0;
+  asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(f0) : "l"(p) : "memory");
+  if (f0 != flag) {
+    const uint64_t t0 = globaltimer();
+    for (int i = 0;; ++i) {
+      asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(f0) : "l"(p) : "memory");
+      if (f0 == flag) break;
+      if ((i & 255) == 255 && globaltimer() - t0 > kTimeoutNs) {
+        atomicOr(err, ERR_BIT_COMM);
+        return false;
+      }
+    }
+  }
+  d0 = a;
+  return true;
+}
+constexpr size_t kHxWords = 2 * kBMax * (kH / 2);  // fwd: [parity][env row][unit pair]
+
 // lane 0 polls with acquire loads, the warp barrier then orders the other lanes' reads after it;
 // false on timeout (warp-uniform)
 __device__ __forceinline__ bool wait_count(const unsigned* cnt, unsigned target, int* err) {
@@ -176,24 +224,49 @@ __global__ void __launch_bounds__(kThreads, 1) lstm1024_fwd_kernel(LstmPtrs p) {
         for (int g = 0; g < 4; ++g) gi[j][g] = g0[g * kH];
       }
     }
-    unsigned* cnt_mine = p.xcnt + (c / kGroupCtas);
-    const unsigned* cnt_wait = p.xcnt + w;
     const uint32_t a_s_base = smem_u32(sm.a_s), h_base0 = smem_u32(sm.h_tile[0]);
     const uint32_t d_acc = tmem + kKTmem / 2 + 8u * (uint32_t)w;
     bool ok = true;
     for (int t = 0; t < T_run; ++t) {
       const int cur = t & 1;
       if (t > 0) {
-        // h_{t-1} of group w: published by its 8 CTAs x 4 warps at step t-1 (the t-th publication)
-        ok = ok && wait_count(cnt_wait, (unsigned)(kGroupCtas * kMmaWarps * t), p.err);
-        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(p.hx) +
-                                                          (size_t)((t - 1) & 1) * kHTile + (size_t)w * kQuarter);
-        uint4* dst = reinterpret_cast<uint4*>(sm.h_tile[cur] + w * kQuarter);
-        uint4 v[kQuarter / 16 / 32];
+        // h_{t-1} of group w (units [256w, +256)), LL words of step t-1 (flag t): 4 units per 16 bytes;
+        // every load of the lane in flight at once, re-read until all flags match
+        const uint2* hx = reinterpret_cast<const uint2*>(p.hx) + (size_t)((t - 1) & 1) * kBMax * (kH / 2);
+        constexpr int kPer = 2 * kBMax;  // 16-byte loads per lane (B = 8)
+        uint4 v[kPer];
+        const uint64_t t0 = globaltimer();
+        for (int spin = 0;; ++spin) {
+          bool all = true;
 #pragma unroll
-        for (int i = 0; i < (int)(kQuarter / 16 / 32); ++i) v[i] = __ldcg(src + lane + 32 * i);
+          for (int q = 0; q < kPer; ++q) {
+            const int i = lane + 32 * q;
+            if (i < 64 * B) {
+              const int b = i >> 6, u0 = 256 * w + 4 * (i & 63);
+              asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v[q].x), "=r"(v[q].y), "=r"(v[q].z), "=r"(v[q].w)
+                           : "l"(hx + (size_t)b * (kH / 2) + u0 / 2)
+                           : "memory");
+            }
+          }
 #pragma unroll
-        for (int i = 0; i < (int)(kQuarter / 16 / 32); ++i) dst[lane + 32 * i] = v[i];
+          for (int q = 0; q < kPer; ++q)
+            if (lane + 32 * q < 64 * B) all = all && v[q].y == (uint32_t)t && v[q].w == (uint32_t)t;
+          if (__all_sync(0xffffffffu, all)) break;
+          if ((spin & 63) == 63 && globaltimer() - t0 > kTimeoutNs) {
+            if (lane == 0) atomicOr(p.err, ERR_BIT_COMM);
+            ok = false;
+            break;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          const int i = lane + 32 * q;
+          if (i < 64 * B) {
+            const int b = i >> 6, u0 = 256 * w + 4 * (i & 63);
+            *reinterpret_cast<uint2*>(sm.h_tile[cur] + tile_off(b, u0, kHTile)) = make_uint2(v[q].x, v[q].z);
+          }
+        }
         fence_proxy_async();
         __syncwarp();
       }
@@ -256,15 +329,15 @@ __global__ void __launch_bounds__(kThreads, 1) lstm1024_fwd_kernel(LstmPtrs p) {
           reinterpret_cast<__half*>(sm.stage[w])[b * 8 + u8] = __float2half(m * hv[j]);
         }
       }
-      if (t + 1 < T_run) {  // publish: row b, units [32c + 8w, +8) of hx[t%2]; then count
+      if (t + 1 < T_run) {  // publish units [32c + 8w, +8) of env row b as 4 LL words (flag t + 1)
         __syncwarp();
-        if (lane < B) {
-          const uint4 pkt = *reinterpret_cast<const uint4*>(sm.stage[w] + 16 * lane);
-          *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(p.hx) + (size_t)cur * kHTile +
-                                    tile_off(lane, gunit - u8, kHTile)) = pkt;
+        if (lane < 2 * B) {
+          const int b = lane >> 1, half = lane & 1;
+          const uint2 pk = *reinterpret_cast<const uint2*>(sm.stage[w] + 16 * b + 8 * half);
+          uint2* hx = reinterpret_cast<uint2*>(p.hx) + (size_t)cur * kBMax * (kH / 2) + (size_t)b * (kH / 2) +
+                      (gunit - u8) / 2 + 2 * half;
+          st_ll2(hx, pk.x, pk.y, (uint32_t)(t + 1));
         }
-        __syncwarp();
-        if (lane == 0) red_release_gpu(cnt_mine, 1u);
       }
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
@@ -365,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm1024_bwd_kernel(LstmPtrs p) {
     }
     tmem_wait_st();
   }
-  const int ustride = B <= 2 ? 2 : (B <= 4 ? 4 : 8);
+  const int ustride = B == 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : 8));  // LL words per (source, unit)
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
@@ -449,40 +522,56 @@ __global__ void __launch_bounds__(kThreads, 1) lstm1024_bwd_kernel(LstmPtrs p) {
       }
       mbar_wait_parity(&sm.mma_bar, (uint32_t)(it & 1));
       tc_fence_after();
-      // partials of units 128q + 32w + lane (owner CTA 4q + w) into the owners' slots
-      float* part = p.xpart + (size_t)par * parity_stride;
+      // partials of units 128q + 32w + lane (owner CTA 4q + w) into the owners' slots as LL words
+      // {partial, it + 1}: word ((owner * 32 + src) * 32 + unit) * ustride + b
+      uint2* part = reinterpret_cast<uint2*>(p.xpart) + (size_t)par * parity_stride;
+      const uint32_t flag = (uint32_t)(it + 1);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         uint32_t a[8];
         tmem_ld8(tmem + ((uint32_t)(w * 32) << 16) + kBwdAcc0 + 8u * (uint32_t)q, a);
         tmem_wait_ld();
-        float* dst = part + (size_t)(4 * q + w) * owner_stride + ((size_t)c * kUPC + lane) * ustride;
-        if (ustride == 2) {
-          __stcg(reinterpret_cast<float2*>(dst), make_float2(__uint_as_float(a[0]), __uint_as_float(a[1])));
+        uint2* dst = part + (size_t)(4 * q + w) * owner_stride + ((size_t)c * kUPC + lane) * ustride;
+        if (B == 1) {
+          st_ll1(dst, a[0], flag);
         } else {
-          __stcg(reinterpret_cast<float4*>(dst), make_float4(__uint_as_float(a[0]), __uint_as_float(a[1]),
-                                                              __uint_as_float(a[2]), __uint_as_float(a[3])));
-          if (ustride == 8)
-            __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(__uint_as_float(a[4]), __uint_as_float(a[5]),
-                                                                    __uint_as_float(a[6]), __uint_as_float(a[7])));
+#pragma unroll
+          for (int e = 0; e < kBMax; e += 2)
+            if (e < B) st_ll2(dst + e, a[e], a[e + 1], flag);
         }
       }
       tc_fence_before();
-      __syncwarp();
-      if (lane < 8) red_release_gpu(p.xcnt + 4 + (4 * lane + w), 1u);  // owner counters follow the fwd's 4
       // own units: all 32 sources' partials, summed in CTA order
-      ok = ok && wait_count(p.xcnt + 4 + c, (unsigned)(kNCta * (it + 1)), p.err);
-      const float* mine = part + (size_t)c * owner_stride;
+      const uint2* mine = part + (size_t)c * owner_stride;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int b = (lane >> 3) + 4 * j;
-        if (b < B) {
-          float v[kNCta];
+        if (j == 1 && B <= 4) break;  // warp-uniform: slot 1 only exists for B > 4
+        uint2 v[kNCta];
+        const uint64_t t0 = globaltimer();
+        for (int spin = 0;; ++spin) {  // all 32 sources' words in flight, re-read until every flag matches
+          bool all = true;
+          if (b < B) {
 #pragma unroll
-          for (int s = 0; s < kNCta; ++s) v[s] = __ldcg(mine + ((size_t)s * kUPC + u) * ustride + b);
+            for (int s2 = 0; s2 < kNCta; ++s2)
+              asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];"
+                           : "=r"(v[s2].x), "=r"(v[s2].y)
+                           : "l"(mine + ((size_t)s2 * kUPC + u) * ustride + b)
+                           : "memory");
+#pragma unroll
+            for (int s2 = 0; s2 < kNCta; ++s2) all = all && v[s2].y == flag;
+          }
+          if (__all_sync(0xffffffffu, all)) break;
+          if ((spin & 63) == 63 && globaltimer() - t0 > kTimeoutNs) {
+            if (lane == 0) atomicOr(p.err, ERR_BIT_COMM);
+            ok = false;
+            break;
+          }
+        }
+        if (b < B) {
           float s = 0.f;
 #pragma unroll
-          for (int q = 0; q < kNCta; ++q) s += v[q];
+          for (int q = 0; q < kNCta; ++q) s += __uint_as_float(v[q].x);
           carry_h[j] = smask[b * T_run + t] * s;
         }
       }
@@ -494,9 +583,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm1024_bwd_kernel(LstmPtrs p) {
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-ddppo_status launch_wide(ddppo_ctx* ctx, void (*kernel)(LstmPtrs), size_t smem, const LstmPtrs& p, cudaStream_t st) {
+ddppo_status launch_wide(ddppo_ctx* ctx, void (*kernel)(LstmPtrs), size_t smem, const LstmPtrs& p, cudaStream_t st,
+                         void* ll, size_t ll_bytes) {
   DDPPO_CUDA_TRY(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  DDPPO_CUDA_TRY(ctx, cudaMemsetAsync(p.xcnt, 0, kLstmWideCounters * sizeof(unsigned), st));
+  DDPPO_CUDA_TRY(ctx, cudaMemsetAsync(ll, 0, ll_bytes, st));  // LL flags start below every step's
   kernel<<<kNCta, kThreads, smem, st>>>(p);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -505,19 +595,24 @@ ddppo_status launch_wide(ddppo_ctx* ctx, void (*kernel)(LstmPtrs), size_t smem, 
 
 }  // namespace
 
+size_t lstm_wide_part_offset() { return kHxWords * 8; }
+
 size_t lstm_wide_exchange_bytes() {
-  // hx: 2 x 16 KB fp16 tiles; partials: 2 x 32 owners x 32 sources x 32 units x 8 floats; counters
-  return 2 * (size_t)kHTile + 2 * (size_t)kNCta * kNCta * kUPC * kBMax * sizeof(float) + 256;
+  // LL words (8 bytes): hx [2][8 rows][512 unit pairs]; partials [2][32 owners][32 sources][32 units][<= 8]
+  return kHxWords * 8 + 2 * (size_t)kNCta * kNCta * kUPC * kBMax * 8 + 256;
 }
 
 ddppo_status launch_lstm1024_fwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, p.hx && p.xcnt && p.err, "lstm-1024: exchange buffers missing");
+  DDPPO_REQUIRE(ctx, p.hx && p.err, "lstm-1024: exchange buffers missing");
   DDPPO_REQUIRE(ctx, ctx->sm_count >= kNCta, "lstm-1024: needs 32 SMs");
-  return launch_wide(ctx, lstm1024_fwd_kernel, sizeof(FwdSmem) + (size_t)p.B * p.T_run * sizeof(float), p, st);
+  return launch_wide(ctx, lstm1024_fwd_kernel, sizeof(FwdSmem) + (size_t)p.B * p.T_run * sizeof(float), p, st, p.hx,
+                     kHxWords * 8);
 }
 
 ddppo_status launch_lstm1024_bwd(ddppo_ctx* ctx, const LstmPtrs& p, cudaStream_t st) {
-  DDPPO_REQUIRE(ctx, p.xpart && p.xcnt && p.err, "lstm-1024: exchange buffers missing");
+  DDPPO_REQUIRE(ctx, p.xpart && p.err, "lstm-1024: exchange buffers missing");
   DDPPO_REQUIRE(ctx, ctx->sm_count >= kNCta, "lstm-1024: needs 32 SMs");
-  return launch_wide(ctx, lstm1024_bwd_kernel, sizeof(BwdSmem) + (size_t)p.B * p.T_run * sizeof(float), p, st);
+  const int ustride = p.B == 1 ? 1 : (p.B <= 2 ? 2 : (p.B <= 4 ? 4 : 8));
+  return launch_wide(ctx, lstm1024_bwd_kernel, sizeof(BwdSmem) + (size_t)p.B * p.T_run * sizeof(float), p, st,
+                     p.xpart, 2 * (size_t)kNCta * kNCta * kUPC * ustride * 8);
 }
