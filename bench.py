@@ -44,6 +44,8 @@ def parse():
                                                          "serx101_1024"])
     ap.add_argument("--seed", type=int, default=1337)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-arenas", type=int, default=2, choices=[1, 2],
+                    help="device rollout arenas of the e2e loop (2: the H2D copy overlaps the previous step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--conv-engine", default="tma", choices=["tma", "cpasync"],
                     help="visual encoders' convolutions: TMA-fed warp-specialised tcgen05 (default) or the round-1 "
@@ -369,8 +371,9 @@ def main():
         copy_stream = torch.cuda.Stream()
         h2d_stream = torch.cuda.Stream()
         done = [torch.cuda.Event() for _ in range(2)]
+        h2d = h2d_stream if args.e2e_arenas == 2 else None
         for i in range(4):  # warm the loop's own buffers and graph keys (2 arenas x 2 uses; not timed)
-            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d_stream)
+            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d)
             lrn.step(stream, stats=stats_dev[i % 2])
             dd.ddppo_allreduce_counts(ctx, [lrn.steps_per_rollout()])
         barrier()
@@ -378,7 +381,7 @@ def main():
         e_exp = 0
         e0.record(stream)
         for i in range(args.steps):
-            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d_stream)
+            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d)
             lrn.step(stream, stats=stats_dev[i % 2])
             copy_stream.wait_stream(stream)
             with torch.cuda.stream(copy_stream):
