@@ -371,9 +371,9 @@ def main():
         copy_stream = torch.cuda.Stream()
         h2d_stream = torch.cuda.Stream()
         done = [torch.cuda.Event() for _ in range(2)]
-        h2d = h2d_stream if args.e2e_arenas == 2 else None
+        h2d_st = h2d_stream if args.e2e_arenas == 2 else None
         for i in range(4):  # warm the loop's own buffers and graph keys (2 arenas x 2 uses; not timed)
-            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d)
+            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d_st)
             lrn.step(stream, stats=stats_dev[i % 2])
             dd.ddppo_allreduce_counts(ctx, [lrn.steps_per_rollout()])
         barrier()
@@ -381,7 +381,7 @@ def main():
         e_exp = 0
         e0.record(stream)
         for i in range(args.steps):
-            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d)
+            lrn.load_rollout(pinned[i % n_roll], perms[i % n_roll], non_blocking=True, copy_stream=h2d_st)
             lrn.step(stream, stats=stats_dev[i % 2])
             copy_stream.wait_stream(stream)
             with torch.cuda.stream(copy_stream):
