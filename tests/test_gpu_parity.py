@@ -515,14 +515,18 @@ def test_learner_step_parity(dd, ctx, cfgname, lengths):
     assert not bad, bad
 
 
-@pytest.mark.parametrize("cfgname,T,lengths,frozen", [("gps", 128, [128, 96, 128, 32], False),
-                                                      ("depth", 12, [12, 5, 12, 9], False),
-                                                      ("depth", 128, [128, 128, 70, 128], False),
-                                                      ("rgbd", 2, [2, 1, 2, 2], False),
-                                                      ("depth", 12, [12, 5, 12, 9], True),
-                                                      ("rgbd", 2, [2, 1, 2, 2], True),
-                                                      ("serx50", 2, [2, 1, 2, 2], False)])
-def test_learner_chain_parity(dd, ctx, cfgname, T, lengths, frozen):
+@pytest.mark.parametrize("cfgname,T,lengths,frozen,replay", [("gps", 128, [128, 96, 128, 32], False, False),
+                                                             ("depth", 12, [12, 5, 12, 9], False, False),
+                                                             ("depth", 128, [128, 128, 70, 128], False, False),
+                                                             ("rgbd", 2, [2, 1, 2, 2], False, False),
+                                                             ("depth", 12, [12, 5, 12, 9], True, False),
+                                                             ("rgbd", 2, [2, 1, 2, 2], True, False),
+                                                             ("serx50", 2, [2, 1, 2, 2], False, False),
+                                                             # logp_old / V_old from a replay
+                                                             # forward of theta -> rho = 1 at minibatch 1
+                                                             ("gps", 128, [128, 96, 128, 32], False, True),
+                                                             ("depth", 12, [12, 5, 12, 9], False, True)])
+def test_learner_chain_parity(dd, ctx, cfgname, T, lengths, frozen, replay):
     """The learner step of the config (Adam eps 1e-8, 2 epochs x 2 minibatches) driven one ABI call
     at a time -- ddppo_gae, ddppo_adv_norm, then per minibatch ddppo_policy_fwd,
     ddppo_ppo_loss_grad, ddppo_policy_bwd, ddppo_grad_allreduce_step -- each minibatch checked
@@ -547,6 +551,17 @@ def test_learner_chain_parity(dd, ctx, cfgname, T, lengths, frozen):
     P = dd.param_count(desc)
     p0 = synth.init_params([(off, int(np.prod(s)), fan) for _, off, s, fan in lay], P, 23)
     ro = synth.rollout(E, T, 24, length=lengths, hidden=H, obs_shape=c.get("obs"), rnn_layers=c.get("rnn_layers", 1))
+    if replay:  # the behaviour policy is theta itself: log pi_theta(a|s) and V_theta(s) from the oracle
+        ob = {k: ro[k] for k in ("goal", "prev_action", "mask", "h0")}
+        if "obs" in ro:
+            ob.update(obs=ro["obs"], c0=ro["c0"])
+        ob["prev_action"] = ro["prev_action"][:, :T]
+        ob["mask"] = ro["mask"][:, :T]
+        lo, vo, _ = models.forward(c["arch"], p0, ob, hidden=H)
+        logp = lo - np.log(np.exp(lo - lo.max(-1, keepdims=True)).sum(-1, keepdims=True)) - lo.max(-1, keepdims=True)
+        a = ro["action"][:, :T]
+        ro["logp_old"][:, :T] = np.take_along_axis(logp, a[..., None].astype(np.int64), -1)[..., 0]
+        ro["val"][:, :T] = vo
     pm = synth.perms(24, 0, ep, E)
     ld = ro["ld"]
     vis = c["arch"] in ("depth", "rgbd", "serx50")
