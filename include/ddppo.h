@@ -262,6 +262,10 @@ ddppo_status ddppo_preempt_poll(ddppo_ctx* ctx, int my_steps, int finished, int 
 
 /* a10: collective, blocking int64 sum of n host values (step accounting). */
 ddppo_status ddppo_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n);
+/* a10 input of one rank: the experience steps its rollout holds, sum_e min(len[e], T) (the steps a
+ * learner step trains on; a preempted env contributes its L_w).  host_len: [E] int32 host
+ * array; ERR_CONFIG on E < 1, T < 1 or a negative length. */
+ddppo_status ddppo_rollout_steps(const int32_t* host_len, int E, int T, int64_t* host_steps);
 
 /* ------------------------------------------------------------------ the whole learner step
  * a2..a8 for one rollout on this rank: GAE -> (adv norm) -> epochs x minibatches of

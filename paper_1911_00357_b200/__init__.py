@@ -280,6 +280,16 @@ def profile_read(ctx, reset=False):
     return {k: (ms[i], la[i], fl[i]) for i, k in enumerate(_lib.KERNEL_FAMILIES)}
 
 
+def ddppo_rollout_steps(host_len, T):
+    """a10 input: sum_e min(len_e, T) of an int32 host array (computed in the C library)."""
+    ln = np.ascontiguousarray(np.asarray(host_len, dtype=np.int32))
+    out = ctypes.c_int64()
+    r = _lib.lib.ddppo_rollout_steps(ln.ctypes.data, int(ln.size), int(T), ctypes.byref(out))
+    if r != 0:
+        raise DdppoError("ddppo_rollout_steps", r, "lengths must be >= 0, E >= 1, T >= 1")
+    return int(out.value)
+
+
 def profile_smem_bytes(ctx, reset=False):
     """{family: shared-memory bytes moved by the tensor-core conv kernels} since the last reset."""
     n = len(_lib.KERNEL_FAMILIES)

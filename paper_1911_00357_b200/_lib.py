@@ -116,6 +116,7 @@ _SIGS = {
     "ddppo_profile_read": (c_int, [c_vp, c_vp, c_vp, c_int]),
     "ddppo_profile_flops": (c_int, [c_vp, c_vp, c_int]),
     "ddppo_profile_smem_bytes": (c_int, [c_vp, c_vp, c_int]),
+    "ddppo_rollout_steps": (c_int, [c_vp, c_int, c_int, c_vp]),
     "ddppo_debug_gemm_bf16": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_int, c_int,
                                       c_int, c_vp, c_int, c_vp]),
     "ddppo_debug_conv2d": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,

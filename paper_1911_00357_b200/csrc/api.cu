@@ -322,6 +322,17 @@ ddppo_status ddppo_preempt_poll(ddppo_ctx* ctx, int my_steps, int finished, int 
   return DDPPO_OK;
 }
 
+ddppo_status ddppo_rollout_steps(const int32_t* host_len, int E, int T, int64_t* host_steps) {
+  if (!host_len || !host_steps || E < 1 || T < 1) return DDPPO_ERR_CONFIG;
+  int64_t n = 0;
+  for (int e = 0; e < E; ++e) {
+    if (host_len[e] < 0) return DDPPO_ERR_CONFIG;
+    n += host_len[e] < T ? host_len[e] : T;
+  }
+  *host_steps = n;
+  return DDPPO_OK;
+}
+
 ddppo_status ddppo_allreduce_counts(ddppo_ctx* ctx, int64_t* host_vals, int n) {
   if (!ctx) return DDPPO_ERR_CONFIG;
   DDPPO_REQUIRE(ctx, host_vals && n >= 0 && n <= kMaxCountVals, "allreduce_counts: 0 <= n <= 64");

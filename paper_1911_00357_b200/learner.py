@@ -194,7 +194,9 @@ class Learner:
         return out
 
     def steps_per_rollout(self):
-        return int(np.minimum(self.host_len, self.T).sum())
+        """The a10 input of this rank (ddppo_rollout_steps: sum_e min(len_e, T))."""
+        from . import ddppo_rollout_steps
+        return ddppo_rollout_steps(self.host_len, self.T)
 
 
 def preempt_collect(ctx, step_costs, T, p_percent, exchange=None, world=None, on_step=None,

@@ -84,3 +84,17 @@ def test_layout_hash_distinguishes_configs():
     assert dd.ddppo_layout_hash(dd.model_desc("gps"), **base) == h["gps"]  # deterministic
     for k, v in (("E", 8), ("T", 64), ("ld", 136), ("minibatches", 4), ("epochs", 1)):
         assert dd.ddppo_layout_hash(dd.model_desc("depth"), **dict(base, **{k: v})) != h["depth"], k
+
+
+def test_rollout_steps_is_the_a10_input():
+    """ddppo_rollout_steps = sum_e min(L_e, T) (P:L635 step accounting; a preempted env counts its
+    L_w) -- brute force over random lengths, including L = 0 and L > T; bad input rejected."""
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        E, T = int(rng.integers(1, 40)), int(rng.integers(1, 300))
+        L = rng.integers(0, 2 * T, E).astype(np.int32)
+        assert dd.ddppo_rollout_steps(L, T) == sum(min(int(x), T) for x in L)
+    with pytest.raises(dd.DdppoError):
+        dd.ddppo_rollout_steps(np.array([3, -1], np.int32), 8)
+    with pytest.raises(dd.DdppoError):
+        dd.ddppo_rollout_steps(np.array([3], np.int32), 0)
