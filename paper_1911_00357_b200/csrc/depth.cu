@@ -209,20 +209,26 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, size_t n, __nv_bfloa
 }
 
 // Single-channel stem convolution in fp32 SIMT (K = k*k taps over 1 channel is too narrow for the
-// 16-byte implicit-GEMM pieces): block per frame, the frame and the weights staged in shared
-// memory; a thread computes 8 horizontally adjacent pixels x 8 output channels per work item, so
-// every weight load (float4 x 2, broadcast) feeds 64 FMAs.
+// 16-byte implicit-GEMM pieces): block per frame, the zero-padded frame and the weights staged in
+// shared memory (no bounds tests in the tap loops, which unroll: K, S compile-time); a thread computes
+// 8 horizontally adjacent pixels x 8 output channels per work item, so every weight load (float4 x
+// 2, broadcast) feeds 64 FMAs.
 constexpr int kStemCoMax = 32;
+template <int K, int S>
 __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restrict__ x, const float* __restrict__ W,
-                                                            int H, int Wd, int Co, int k, int s, int p, int Ho, int Wo,
+                                                            int H, int Wd, int Co, int p, int Ho, int Wo,
                                                             float* __restrict__ y) {
   pdl_enter();
   extern __shared__ __align__(16) float sm[];
-  const int kk = k * k;
-  float* ws = sm;                   // [k*k][Co]   (Co % 8 == 0)
-  float* xs = sm + kk * Co;         // [H][Wd]
+  constexpr int kk = K * K;
+  const int Hp = H + 2 * p, Wp = Wd + 2 * p + 8 * S;  // + a right margin: the last item's unused columns
+  float* ws = sm;                                     // [k*k][Co]   (Co % 8 == 0)
+  float* xs = sm + kk * Co;                           // [Hp][Wp], zero borders
   const int f = blockIdx.x;
-  for (int i = threadIdx.x; i < H * Wd; i += blockDim.x) xs[i] = x[(size_t)f * H * Wd + i];
+  for (int i = threadIdx.x; i < Hp * Wp; i += blockDim.x) {
+    const int r = i / Wp - p, q = i % Wp - p;
+    xs[i] = (r >= 0 && r < H && q >= 0 && q < Wd) ? x[((size_t)f * H + r) * Wd + q] : 0.f;
+  }
   for (int i = threadIdx.x; i < Co * kk; i += blockDim.x) ws[(i % kk) * Co + i / kk] = W[i];
   __syncthreads();
   constexpr int kPx = 8;  // horizontally adjacent output pixels per work item (x 8 channels: 64 FMAs per tap)
@@ -234,17 +240,17 @@ __global__ void __launch_bounds__(kThreads) stem_fwd_kernel(const float* __restr
     for (int a = 0; a < kPx; ++a)
 #pragma unroll
       for (int o = 0; o < 8; ++o) acc[a][o] = 0.f;
-    for (int u = 0; u < k; ++u) {
-      const int yy = i * s - p + u;
-      if (yy < 0 || yy >= H) continue;
-      for (int v = 0; v < k; ++v) {
-        const float4 w0 = *reinterpret_cast<const float4*>(ws + (u * k + v) * Co + o0);
-        const float4 w1 = *reinterpret_cast<const float4*>(ws + (u * k + v) * Co + o0 + 4);
+#pragma unroll 1
+    for (int u = 0; u < K; ++u) {
+      const float* xr = xs + (i * S + u) * Wp + j0 * S;  // padded coordinates: (i*S - p + u) + p
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        const float4 w0 = *reinterpret_cast<const float4*>(ws + (u * K + v) * Co + o0);
+        const float4 w1 = *reinterpret_cast<const float4*>(ws + (u * K + v) * Co + o0 + 4);
         const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
         for (int a = 0; a < kPx; ++a) {
-          const int xx = (j0 + a) * s - p + v;
-          const float xv = (xx >= 0 && xx < Wd) ? xs[yy * Wd + xx] : 0.f;
+          const float xv = xr[a * S + v];
 #pragma unroll
           for (int o = 0; o < 8; ++o) acc[a][o] = fmaf(xv, wv[o], acc[a][o]);
         }
@@ -1489,10 +1495,15 @@ IgOperand op_dense(int kind, const __nv_bfloat16* x, int64_t ld, int64_t plane) 
 ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const __nv_bfloat16* xb, const float* w,
                       const __nv_bfloat16* wr_b, float* y, const ConvScratch& sc, cudaStream_t st) {
   if (is_stem(g)) {
-    DDPPO_REQUIRE(ctx, g.Co <= kStemCoMax && g.Co % 8 == 0 && g.k * g.k <= 64, "stem conv: Co in {8,..,32}, k*k <= 64");
-    const size_t smem = (size_t)(g.H * g.W + g.Co * g.k * g.k) * sizeof(float);
+    DDPPO_REQUIRE(ctx, g.Co <= kStemCoMax && g.Co % 8 == 0 && (g.k == 3 || g.k == 5 || g.k == 7) && g.s <= 2,
+                  "stem conv: Co in {8,..,32}, k in {3, 5, 7}, stride 1 or 2");
+    const size_t smem = (size_t)((g.H + 2 * g.p) * (g.W + 2 * g.p + 16) + g.Co * g.k * g.k) * sizeof(float);
     DDPPO_REQUIRE(ctx, smem <= 48 * 1024, "stem conv: frame too large for shared memory");
-    launch_k(ctx, stem_fwd_kernel, g.F, kThreads, smem, st, x, w, g.H, g.W, g.Co, g.k, g.s, g.p, g.Ho, g.Wo, y);
+#define STEM_FWD(K_, S_)                                                                                   \
+  if (g.k == K_ && g.s == S_)                                                                             \
+    launch_k(ctx, stem_fwd_kernel<K_, S_>, g.F, kThreads, smem, st, x, w, g.H, g.W, g.Co, g.p, g.Ho, g.Wo, y);
+    STEM_FWD(7, 2) STEM_FWD(7, 1) STEM_FWD(5, 2) STEM_FWD(5, 1) STEM_FWD(3, 2) STEM_FWD(3, 1)
+#undef STEM_FWD
     ctx->count(1);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     return DDPPO_OK;
@@ -1539,8 +1550,6 @@ ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const
     static bool attr_set = false;
     if (!attr_set) {
       DDPPO_CUDA_TRY(ctx, cudaFuncSetAttribute(stem_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               200 * 1024));
-      DDPPO_CUDA_TRY(ctx, cudaFuncSetAttribute(stem_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                200 * 1024));
       attr_set = true;
     }
