@@ -30,7 +30,7 @@ constexpr int kImg = 64;        // Depth input resolution (configs[2])
 constexpr int kImgRgbd = 256;   // RGB-D input resolution (configs[3])
 
 // ------------------------------------------------------------------ kernels
-// obs [E][T][1][64][64] bf16 (gathered through env_idx) -> x0 [F][64][64][1] fp32 (the SIMT stem's input)
+// obs [E][T][1][64][64] bf16 (gathered through env_idx) -> x0 [F][64][64][1] fp32 (the stem's input)
 __global__ void gather_obs_kernel(const __nv_bfloat16* __restrict__ obs, const int32_t* __restrict__ env_idx, int T,
                                   int T_run, int F, float* __restrict__ x0) {
   pdl_enter();
@@ -339,6 +339,220 @@ __global__ void __launch_bounds__(kThreads) stem_wgrad_kernel(const float* __res
         const int tap = t0 + b2;
         if (tap < kk) part[(size_t)f * Co * kk + (o0 + a) * kk + tap] = acc[a][b2] + red[r * 16 + a * 4 + b2];
       }
+  }
+}
+
+// ---- stem on the warp-level tensor path (mma.sync m16n8k16 bf16 -> fp32) ----
+// The single-channel stem has K = k*k <= 49 taps: too narrow for the 16-byte TMA / tcgen05 pieces
+// (its one-channel im2col cannot be a TMA box) but dense enough for warp MMAs whose fragments are
+// gathered straight from the zero-padded frame in shared memory.  The frame is staged as packed
+// bf16 (hi | lo << 16) pairs, x = hi + lo to 2^-17, so one 32-bit shared load yields both planes.
+__device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};\n"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_hilo(float v) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+  return (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
+}
+// zero-padded frame f -> xp[HP][WP] packed hi/lo
+__device__ __forceinline__ void stage_frame_hilo(const float* __restrict__ x, int f, int H, int Wd, int p, int HP,
+                                                 int WP, uint32_t* xp) {
+  constexpr int kB = 8;  // loads in flight per thread (the loop is latency-bound otherwise)
+  const float* xf = x + (size_t)f * H * Wd;
+  for (int i0 = 0; i0 < HP * WP; i0 += kB * (int)blockDim.x) {
+    float v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int i = i0 + u * blockDim.x + threadIdx.x, r = i / WP - p, q = i % WP - p;
+      v[u] = (i < HP * WP && r >= 0 && r < H && q >= 0 && q < Wd) ? xf[r * Wd + q] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int i = i0 + u * blockDim.x + threadIdx.x;
+      if (i < HP * WP) xp[i] = pack_hilo(v[u]);
+    }
+  }
+}
+
+// y[f][q][o] = sum_tap col[q][tap] W[o][tap] as an M = pixels x N = Co x K = taps (padded to 16)
+// GEMM per frame, bf16x3 (xh Wh + xh Wl + xl Wh, the forward convention of the other convs).  Block
+// per frame; warp w takes the 16-pixel m-tiles w, w + 8, ...; the W fragments stay in registers.
+template <int K, int S, int CO>
+__global__ void __launch_bounds__(kThreads, 2) stem_fwd_mma_kernel(const float* __restrict__ x,
+                                                                   const float* __restrict__ W, int H, int Wd,
+                                                                   int p, int Ho, int Wo, float* __restrict__ y) {
+  constexpr int kk = K * K, KS = (kk + 15) / 16, NT = CO / 8;
+  extern __shared__ __align__(16) uint32_t smu[];
+  const int HP = H + 2 * p, WP = Wd + 2 * p;
+  const int f = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  pdl_enter();  // W is the parameter vector the previous step's update writes
+  // B fragments (k = tap, n = o): b0 = taps 16ks + 2t, +1; b1 = taps 16ks + 2t + 8, +9; column o = 8nt + g
+  uint32_t bh[KS][NT][2], bl[KS][NT][2];
+  int toff[KS][4];  // frame offsets of taps 16ks + 2t + {0, 1, 8, 9} (0 past k*k: W is zero there)
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int tap = 16 * ks + 2 * t + (e & 1) + (e >> 1) * 8;
+      toff[ks][e] = tap < kk ? (tap / K) * WP + tap % K : 0;
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int tap = 16 * ks + 2 * t + 8 * h, o = 8 * nt + g;
+        const uint32_t p0 = tap < kk ? pack_hilo(W[o * kk + tap]) : 0u;
+        const uint32_t p1 = tap + 1 < kk ? pack_hilo(W[o * kk + tap + 1]) : 0u;
+        bh[ks][nt][h] = __byte_perm(p0, p1, 0x5410);
+        bl[ks][nt][h] = __byte_perm(p0, p1, 0x7632);
+      }
+  }
+  stage_frame_hilo(x, f, H, Wd, p, HP, WP, smu);
+  __syncthreads();
+  const int M = Ho * Wo;
+  for (int m0 = warp * 16; m0 < M; m0 += 16 * (kThreads / 32)) {
+    int base[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = m0 + g + 8 * h, i = q / Wo, j = q % Wo;
+      base[h] = i * S * WP + j * S;
+    }
+    float acc[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      // A (row = pixel, k = tap): a0 (g, 2t..), a1 (g + 8, 2t..), a2 (g, 2t + 8..), a3 (g + 8, 2t + 8..)
+      uint32_t ah[4], al[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int b = base[r & 1], e0 = (r >> 1) * 2;
+        const uint32_t p0 = smu[b + toff[ks][e0]], p1 = smu[b + toff[ks][e0 + 1]];
+        ah[r] = __byte_perm(p0, p1, 0x5410);
+        al[r] = __byte_perm(p0, p1, 0x7632);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        mma_bf16_16816(acc[nt], ah, bh[ks][nt][0], bh[ks][nt][1]);
+        mma_bf16_16816(acc[nt], ah, bl[ks][nt][0], bl[ks][nt][1]);
+        mma_bf16_16816(acc[nt], al, bh[ks][nt][0], bh[ks][nt][1]);
+      }
+    }
+    float* yf = y + (size_t)f * M * CO;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      *reinterpret_cast<float2*>(yf + (size_t)(m0 + g) * CO + 8 * nt + 2 * t) = make_float2(acc[nt][0], acc[nt][1]);
+      *reinterpret_cast<float2*>(yf + (size_t)(m0 + g + 8) * CO + 8 * nt + 2 * t) =
+          make_float2(acc[nt][2], acc[nt][3]);
+    }
+  }
+}
+
+// part[f][o*k*k + tap] = sum_q dy[f][q][o] col[q][tap] as an M = Co x N = taps (padded to 8) x
+// K = pixels GEMM per frame: A = dy^T by ldmatrix.trans from the frame's dy rows (16-byte chunks
+// XOR-swizzled: conflict-free), B = im2col gathered from the packed frame, two MMAs (x hi, x lo) per
+// fragment.  Warp w takes the 16-pixel k-steps w, w + 8, ...; the 8 warps' tiles are added in a
+// fixed order.
+template <int K, int CO>
+__global__ void __launch_bounds__(kThreads, 2) stem_wgrad_mma_kernel(const float* __restrict__ x,
+                                                                     const __nv_bfloat16* __restrict__ dy, int H,
+                                                                     int Wd, int s, int p, int Ho, int Wo,
+                                                                     float* __restrict__ part) {
+  constexpr int kk = K * K, NT = (kk + 7) / 8, MT = CO / 16, CPR = CO / 8;  // CPR: 16-byte chunks per dy row
+  constexpr int kWarps = kThreads / 32;
+  pdl_enter();
+  extern __shared__ __align__(16) uint32_t smu[];
+  const int HP = H + 2 * p, WP = Wd + 2 * p, M = Ho * Wo;
+  const int f = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const size_t dy_words = (size_t)M * CO / 2 > (size_t)kWarps * CO * NT * 8 ? (size_t)M * CO / 2
+                                                                             : (size_t)kWarps * CO * NT * 8;
+  uint4* dys = reinterpret_cast<uint4*>(smu);  // [M][CPR] chunks, chunk c of row q at c ^ swz(q)
+  uint32_t* xp = smu + dy_words;               // [HP][WP] packed hi/lo
+  auto swz = [](int q) { return CPR == 4 ? (q >> 1) & 3 : (q >> 2) & 1; };
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(dy + (size_t)f * M * CO);
+    for (int i = threadIdx.x; i < M * CPR; i += blockDim.x) {  // all of the frame's dy rows in flight
+      const int q = i / CPR, c = i % CPR;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(dys + q * CPR + (c ^ swz(q)));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  stage_frame_hilo(x, f, H, Wd, p, HP, WP, xp);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  int toff[NT];  // frame offset of tap 8nt + g (0 past k*k: those columns are computed, never stored)
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int tap = 8 * nt + g;
+    toff[nt] = tap < kk ? (tap / K) * WP + tap % K : 0;
+  }
+  float acc[MT][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+  const uint32_t dys_addr = (uint32_t)__cvta_generic_to_shared(dys);
+  for (int q0 = warp * 16; q0 < M; q0 += 16 * kWarps) {
+    uint32_t a[MT][4];
+    {
+      const int q = q0 + (lane & 7) + ((lane >> 4) & 1) * 8;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int c = 2 * mt + ((lane >> 3) & 1);
+        const uint32_t addr = dys_addr + (uint32_t)(q * CPR + (c ^ swz(q))) * 16u;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                     : "=r"(a[mt][0]), "=r"(a[mt][1]), "=r"(a[mt][2]), "=r"(a[mt][3])
+                     : "r"(addr));
+      }
+    }
+    // B (k = pixel, n = tap): b0 = pixels q0 + 2t, +1; b1 = pixels q0 + 2t + 8, +9; column tap 8nt + g
+    int base[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int q = q0 + 2 * t + (e & 1) + (e >> 1) * 8, i = q / Wo, j = q % Wo;
+      base[e] = i * s * WP + j * s;
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const uint32_t p0 = xp[base[0] + toff[nt]], p1 = xp[base[1] + toff[nt]];
+      const uint32_t p2 = xp[base[2] + toff[nt]], p3 = xp[base[3] + toff[nt]];
+      const uint32_t h0 = __byte_perm(p0, p1, 0x5410), h1 = __byte_perm(p2, p3, 0x5410);
+      const uint32_t l0 = __byte_perm(p0, p1, 0x7632), l1 = __byte_perm(p2, p3, 0x7632);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        mma_bf16_16816(acc[mt][nt], a[mt], h0, h1);
+        mma_bf16_16816(acc[mt][nt], a[mt], l0, l1);
+      }
+    }
+  }
+  __syncthreads();  // dy no longer needed: its space holds the per-warp tiles
+  float* red = reinterpret_cast<float*>(smu);  // [warp][CO][NT*8]
+  constexpr int NC = NT * 8;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int o = 16 * mt + g + 8 * (e >> 1), c = 8 * nt + 2 * t + (e & 1);
+        red[(warp * CO + o) * NC + c] = acc[mt][nt][e];
+      }
+  __syncthreads();
+  for (int i = threadIdx.x; i < CO * kk; i += blockDim.x) {
+    const int o = i / kk, tap = i % kk;
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) v += red[(w * CO + o) * NC + tap];
+    part[(size_t)f * CO * kk + i] = v;
   }
 }
 // dW[i] = sum over frames (fixed order) of part[f][i]
@@ -1499,11 +1713,22 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
                   "stem conv: Co in {8,..,32}, k in {3, 5, 7}, stride 1 or 2");
     const size_t smem = (size_t)((g.H + 2 * g.p) * (g.W + 2 * g.p + 16) + g.Co * g.k * g.k) * sizeof(float);
     DDPPO_REQUIRE(ctx, smem <= 48 * 1024, "stem conv: frame too large for shared memory");
+    if ((g.Co == 16 || g.Co == 32) && (g.Ho * g.Wo) % 16 == 0) {  // warp-MMA stem
+      const size_t sm2 = (size_t)(g.H + 2 * g.p) * (g.W + 2 * g.p) * sizeof(uint32_t);
+#define STEM_FWD(K_, S_, C_)                                                                                  \
+  if (g.k == K_ && g.s == S_ && g.Co == C_)                                                                  \
+    launch_k(ctx, stem_fwd_mma_kernel<K_, S_, C_>, g.F, kThreads, sm2, st, x, w, g.H, g.W, g.p, g.Ho, g.Wo, y);
+      STEM_FWD(7, 2, 32) STEM_FWD(7, 1, 32) STEM_FWD(5, 2, 32) STEM_FWD(5, 1, 32) STEM_FWD(3, 2, 32)
+      STEM_FWD(3, 1, 32) STEM_FWD(7, 2, 16) STEM_FWD(7, 1, 16) STEM_FWD(5, 2, 16) STEM_FWD(5, 1, 16)
+      STEM_FWD(3, 2, 16) STEM_FWD(3, 1, 16)
+#undef STEM_FWD
+    } else {
 #define STEM_FWD(K_, S_)                                                                                   \
   if (g.k == K_ && g.s == S_)                                                                             \
     launch_k(ctx, stem_fwd_kernel<K_, S_>, g.F, kThreads, smem, st, x, w, g.H, g.W, g.Co, g.p, g.Ho, g.Wo, y);
-    STEM_FWD(7, 2) STEM_FWD(7, 1) STEM_FWD(5, 2) STEM_FWD(5, 1) STEM_FWD(3, 2) STEM_FWD(3, 1)
+      STEM_FWD(7, 2) STEM_FWD(7, 1) STEM_FWD(5, 2) STEM_FWD(5, 1) STEM_FWD(3, 2) STEM_FWD(3, 1)
 #undef STEM_FWD
+    }
     ctx->count(1);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
     return DDPPO_OK;
@@ -1553,8 +1778,29 @@ ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const
                                                200 * 1024));
       attr_set = true;
     }
-    launch_k(ctx, stem_wgrad_kernel, g.F, kThreads, smem, st, x, dy, g.H, g.W, g.Co, g.k, g.s, g.p, g.Ho, g.Wo,
+    if ((g.Co == 16 || g.Co == 32) && (g.Ho * g.Wo) % 16 == 0) {  // warp-MMA stem
+      const int NC = (g.k * g.k + 7) / 8 * 8;
+      const size_t dyw = std::max<size_t>((size_t)g.Ho * g.Wo * g.Co / 2, (size_t)(kThreads / 32) * g.Co * NC);
+      const size_t sm2 = (dyw + hp) * sizeof(uint32_t);
+      DDPPO_REQUIRE(ctx, sm2 <= 200 * 1024, "stem conv: frame too large for shared memory");
+      static bool attr2 = false;
+      if (!attr2) {
+        for (const void* fn : {(const void*)stem_wgrad_mma_kernel<7, 32>, (const void*)stem_wgrad_mma_kernel<5, 32>,
+                               (const void*)stem_wgrad_mma_kernel<3, 32>, (const void*)stem_wgrad_mma_kernel<7, 16>,
+                               (const void*)stem_wgrad_mma_kernel<5, 16>, (const void*)stem_wgrad_mma_kernel<3, 16>})
+          DDPPO_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr2 = true;
+      }
+#define STEM_WG(K_, C_)                                                                                  \
+  if (g.k == K_ && g.Co == C_)                                                                          \
+    launch_k(ctx, stem_wgrad_mma_kernel<K_, C_>, g.F, kThreads, sm2, st, x, dy, g.H, g.W, g.s, g.p, g.Ho, g.Wo, \
              sc.part);
+      STEM_WG(7, 32) STEM_WG(5, 32) STEM_WG(3, 32) STEM_WG(7, 16) STEM_WG(5, 16) STEM_WG(3, 16)
+#undef STEM_WG
+    } else {
+      launch_k(ctx, stem_wgrad_kernel, g.F, kThreads, smem, st, x, dy, g.H, g.W, g.Co, g.k, g.s, g.p, g.Ho, g.Wo,
+               sc.part);
+    }
     launch_k(ctx, frame_sum_kernel, g.Co * g.k * g.k, kThreads, 0, st, sc.part, g.F, g.Co * g.k * g.k, dw);
     ctx->count(2);
     DDPPO_CUDA_TRY(ctx, cudaGetLastError());
@@ -1931,7 +2177,7 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
     prep.offd[0] = 0;
     for (size_t i = 0; i < P.convs.size(); ++i) {
       const ConvGN& c = P.convs[i];
-      if (c.Ci == 1) continue;  // the Depth stem runs SIMT on fp32 weights
+      if (c.Ci == 1) continue;  // the Depth stem splits its fp32 weights into bf16 planes itself
       DDPPO_REQUIRE(ctx, prep.n < kMaxConvs, "too many convolutions for one weight-prep launch");
       prep.it[prep.n] = WeightPrep::Item{prm + c.w, c.wr_b, c.wd_b, c.Co, c.Ci_real, c.Ci, c.k, P.grad_planes, c.groups};
       prep.off[prep.n + 1] = prep.off[prep.n] + c.Co;
@@ -1939,7 +2185,7 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
       ++prep.n;
     }
     // the operand prep (the conv kernels' bf16 weight planes: the role of a bf16 parameter shadow)
-    // runs on the side stream beside the input prologue and (Depth) the SIMT stem + max-pool; joined
+    // runs on the side stream beside the input prologue and (Depth) the stem + max-pool; joined
     // before the first TMA convolution
     if (ctx->conv_engine == DDPPO_CONV_TMA) {
       cudaStream_t sb = nullptr;
@@ -2194,7 +2440,9 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     }
     std::swap(dz, dn);  // dn (the block input's gradient) becomes the next dz
   }
-  // max-pool, then the stem (no input gradient)
+  // max-pool, then the stem (no input gradient).  (Gathering the pool's gradient inside the stem's
+  // GroupNorm backward instead -- no dense gradient in HBM -- measured 3 us slower per minibatch:
+  // the cluster kernel's 2 CTAs / SM cannot hide the gather's L2 latency.)
   ConvGN& stem = P.convs[0];
   launch_k(ctx, maxpool_bwd_kernel, dim3((stem.Ho * stem.Wo * 8 + kThreads - 1) / kThreads, F), kThreads, 0, st, dz,
            P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);

@@ -2,7 +2,7 @@
 oracle.convnets (fp64, NCHW; transposed to the kernels' NHWC here).
 
 Tolerances (DESIGN.md "Depth precision"):
-  conv forward (bf16 hi/lo operand planes; the 1-channel stem in fp32): |err| <= 2e-5 * (|x| conv |W|);
+  conv forward (bf16 hi/lo operand planes, the stem's warp MMAs too; the SIMT stem in fp32): |err| <= 2e-5 * (|x| conv |W|);
   conv dgrad / wgrad (bf16 operands, fp32 accumulation): |err| <= 1e-2 * the same op on |.|;
   GroupNorm (fp32 SIMT): 1e-4 relative to the tensor's scale (its input gradient is delivered in
   bf16: + 2^-8 relative); max-pool: exact forward."""
@@ -50,7 +50,9 @@ def nchw(a):
     (5, 2, 256, 128, 3, 1, 1),  # compress (2x2 maps)
     (3, 7, 24, 40, 3, 2, 1),    # ragged
     (4, 5, 8, 16, 1, 1, 0),     # 1x1 / stride 1
-    (2, 9, 1, 16, 3, 1, 1),     # single-channel (stem kernels) at another geometry
+    (2, 9, 1, 16, 3, 1, 1),     # single-channel (SIMT stem kernels: 81 pixels, not a multiple of 16)
+    (2, 16, 1, 16, 5, 1, 2),    # single-channel, warp-MMA stem at another geometry (Co 16, 5x5 s1)
+    (3, 24, 1, 32, 3, 2, 1),    # single-channel, warp-MMA stem (3x3 s2, 144 pixels)
     (2, 32, 8, 32, 7, 2, 3),    # RGB-D stem (4 channels padded to 8)
     (2, 8, 64, 256, 1, 1, 0),   # bottleneck 1x1 expansion
     (2, 4, 1024, 128, 3, 1, 1),   # RGB-D compression (1024 -> 128 at 4x4)
