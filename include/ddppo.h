@@ -438,7 +438,8 @@ ddppo_status ddppo_debug_gemm_bf16(ddppo_ctx* ctx, const float* A, int64_t sam, 
  * activations NHWC fp32; conv weights PyTorch [Co][Ci][k][k].
  * conv2d: y[F][Ho][Wo][Co] = conv(x[F][H][W][Ci], w) (stride s, zero padding p; bf16 hi/lo
  *   operand planes) if y != NULL; if dy != NULL: dw = weight gradient, dx = input gradient (dx
- *   nullable), bf16 operands.  Ci == 1 (the stem: fp32 SIMT, no dx) or Ci, Co multiples of 8.
+ *   nullable), bf16 operands.  Ci == 1 (the stem: warp MMAs on bf16 hi/lo planes, fp32 SIMT off
+ *   that grid; no dx) or Ci, Co multiples of 8.
  *   scratch == NULL: only *host_need (bytes) is written. */
 ddppo_status ddppo_debug_conv2d(ddppo_ctx* ctx, const float* x, const float* w, int F, int H, int W,
                                 int Ci, int Co, int k, int s, int p, float* y, const float* dy,
