@@ -358,9 +358,12 @@ __device__ __forceinline__ uint32_t pack_hilo(float v) {
   const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
   return (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
 }
-// zero-padded frame f -> xp[HP][WP] packed hi/lo
-__device__ __forceinline__ void stage_frame_hilo(const float* __restrict__ x, int f, int H, int Wd, int p, int HP,
+// zero-padded frame f -> xp[HP][WP] packed hi/lo; returns (block-uniformly, after the barrier)
+// whether any lo half is nonzero -- a frame of bf16 values (the Depth observations are stored as
+// bf16) has an all-zero lo plane, whose MMAs then add exact zeros and are skipped
+__device__ __forceinline__ bool stage_frame_hilo(const float* __restrict__ x, int f, int H, int Wd, int p, int HP,
                                                  int WP, uint32_t* xp) {
+  int any_lo = 0;
   constexpr int kB = 8;  // loads in flight per thread (the loop is latency-bound otherwise)
   const float* xf = x + (size_t)f * H * Wd;
   for (int i0 = 0; i0 < HP * WP; i0 += kB * (int)blockDim.x) {
@@ -373,20 +376,30 @@ __device__ __forceinline__ void stage_frame_hilo(const float* __restrict__ x, in
 #pragma unroll
     for (int u = 0; u < kB; ++u) {
       const int i = i0 + u * blockDim.x + threadIdx.x;
-      if (i < HP * WP) xp[i] = pack_hilo(v[u]);
+      const uint32_t pk = pack_hilo(v[u]);
+      any_lo |= (pk >> 16) & 0x7fff;  // (a -0 lo half would add -0 products: exact no-ops too)
+      if (i < HP * WP) xp[i] = pk;
     }
   }
+  return __syncthreads_or(any_lo) != 0;
 }
 
 // y[f][q][o] = sum_tap col[q][tap] W[o][tap] as an M = pixels x N = Co x K = taps (padded to 16)
 // GEMM per frame, bf16x3 (xh Wh + xh Wl + xl Wh, the forward convention of the other convs).  Block
 // per frame; warp w takes the 16-pixel m-tiles w, w + 8, ...; the W fragments stay in registers.
+// gsum (nullable): the frame's GroupNorm sums [F][16][2] = (sum y, sum y^2) per group (double; the
+// per-thread sums in pixel order, then a fixed butterfly over the 8 row lanes and the warps in
+// order), so the stem's GroupNorm needs no statistics pass over y.
 template <int K, int S, int CO>
 __global__ void __launch_bounds__(kThreads, 2) stem_fwd_mma_kernel(const float* __restrict__ x,
                                                                    const float* __restrict__ W, int H, int Wd,
-                                                                   int p, int Ho, int Wo, float* __restrict__ y) {
+                                                                   int p, int Ho, int Wo, float* __restrict__ y,
+                                                                   double* __restrict__ gsum) {
   constexpr int kk = K * K, KS = (kk + 15) / 16, NT = CO / 8;
+  constexpr int CG = CO / kGroups, GE = CG == 2 ? 1 : 2;  // channels per group; groups per (thread, n-tile)
+  static_assert(CO % kGroups == 0 && CG <= 2, "stem: 16 or 32 channels");
   extern __shared__ __align__(16) uint32_t smu[];
+  __shared__ double gred[kThreads / 32][CO][2];
   const int HP = H + 2 * p, WP = Wd + 2 * p;
   const int f = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   pdl_enter();  // W is the parameter vector the previous step's update writes
@@ -411,9 +424,13 @@ __global__ void __launch_bounds__(kThreads, 2) stem_fwd_mma_kernel(const float* 
         bl[ks][nt][h] = __byte_perm(p0, p1, 0x7632);
       }
   }
-  stage_frame_hilo(x, f, H, Wd, p, HP, WP, smu);
-  __syncthreads();
+  const bool x_lo = stage_frame_hilo(x, f, H, Wd, p, HP, WP, smu);
   const int M = Ho * Wo;
+  double s1[NT][GE], s2[NT][GE];  // group sums of this thread's columns 8nt + 2t (+ 1)
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < GE; ++e) s1[nt][e] = s2[nt][e] = 0.0;
   for (int m0 = warp * 16; m0 < M; m0 += 16 * (kThreads / 32)) {
     int base[2];
 #pragma unroll
@@ -441,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 2) stem_fwd_mma_kernel(const float* 
       for (int nt = 0; nt < NT; ++nt) {
         mma_bf16_16816(acc[nt], ah, bh[ks][nt][0], bh[ks][nt][1]);
         mma_bf16_16816(acc[nt], ah, bl[ks][nt][0], bl[ks][nt][1]);
-        mma_bf16_16816(acc[nt], al, bh[ks][nt][0], bh[ks][nt][1]);
+        if (x_lo) mma_bf16_16816(acc[nt], al, bh[ks][nt][0], bh[ks][nt][1]);
       }
     }
     float* yf = y + (size_t)f * M * CO;
@@ -450,6 +467,48 @@ __global__ void __launch_bounds__(kThreads, 2) stem_fwd_mma_kernel(const float* 
       *reinterpret_cast<float2*>(yf + (size_t)(m0 + g) * CO + 8 * nt + 2 * t) = make_float2(acc[nt][0], acc[nt][1]);
       *reinterpret_cast<float2*>(yf + (size_t)(m0 + g + 8) * CO + 8 * nt + 2 * t) =
           make_float2(acc[nt][2], acc[nt][3]);
+    }
+    if (gsum) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double v = acc[nt][e];
+          s1[nt][GE == 1 ? 0 : (e & 1)] += v;
+          s2[nt][GE == 1 ? 0 : (e & 1)] += v * v;
+        }
+    }
+  }
+  if (gsum) {  // (block-uniform)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < GE; ++e)
+#pragma unroll
+        for (int sh = 4; sh < 32; sh <<= 1) {  // over g (lane bits 2-4)
+          s1[nt][e] += __shfl_xor_sync(0xffffffffu, s1[nt][e], sh);
+          s2[nt][e] += __shfl_xor_sync(0xffffffffu, s2[nt][e], sh);
+        }
+    if (g == 0) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < GE; ++e) {
+          const int col = 8 * nt + 2 * t + e;  // GE == 1: the group's first channel holds its sums
+          gred[warp][col][0] = s1[nt][e];
+          gred[warp][col][1] = s2[nt][e];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < kGroups) {
+      double a = 0.0, b = 0.0;
+      const int col = threadIdx.x * CG;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        a += gred[w][col][0];
+        b += gred[w][col][1];
+      }
+      gsum[((size_t)f * kGroups + threadIdx.x) * 2] = a;
+      gsum[((size_t)f * kGroups + threadIdx.x) * 2 + 1] = b;
     }
   }
 }
@@ -484,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 2) stem_wgrad_mma_kernel(const float
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
-  stage_frame_hilo(x, f, H, Wd, p, HP, WP, xp);
+  const bool x_lo = stage_frame_hilo(x, f, H, Wd, p, HP, WP, xp);
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   int toff[NT];  // frame offset of tap 8nt + g (0 past k*k: those columns are computed, never stored)
@@ -530,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 2) stem_wgrad_mma_kernel(const float
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         mma_bf16_16816(acc[mt][nt], a[mt], h0, h1);
-        mma_bf16_16816(acc[mt][nt], a[mt], l0, l1);
+        if (x_lo) mma_bf16_16816(acc[mt][nt], a[mt], l0, l1);
       }
     }
   }
@@ -789,10 +848,11 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_apply_part_kernel(const float
                                                                       const float* __restrict__ residual, int HW,
                                                                       int C, int relu, size_t plane,
                                                                       float* __restrict__ stats, float* __restrict__ z,
-                                                                      __nv_bfloat16* __restrict__ zb) {
+                                                                      __nv_bfloat16* __restrict__ zb, int nparts) {
   pdl_enter();
   __shared__ float smu[kGroups], srs[kGroups];
-  const int f = blockIdx.y, S = gridDim.x, n = HW * C, chunk = gn_chunk(C), cg = C / kGroups;
+  // gpart holds nparts partial sums per frame (gn_stats_part: one per chunk; the stem kernel: 1)
+  const int f = blockIdx.y, S = nparts, n = HW * C, chunk = gn_chunk(C), cg = C / kGroups;
   if (threadIdx.x < kGroups) {
     double a = 0.0, b = 0.0;
     for (int s = 0; s < S; ++s) {
@@ -1706,8 +1766,12 @@ IgOperand op_dense(int kind, const __nv_bfloat16* x, int64_t ld, int64_t plane) 
 }
 
 // y[F][Ho][Wo][Co] = conv(x, W[Co][Ci][k][k]); xb = x as bf16 hi/lo planes (unused by the stem)
+// gsum (nullable): scratch for the stem's GroupNorm sums [F][16][2]; *gsum_done = whether the
+// launched kernel wrote them (the warp-MMA stem does, every other path does not)
 ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const __nv_bfloat16* xb, const float* w,
-                      const __nv_bfloat16* wr_b, float* y, const ConvScratch& sc, cudaStream_t st) {
+                      const __nv_bfloat16* wr_b, float* y, const ConvScratch& sc, cudaStream_t st,
+                      double* gsum = nullptr, bool* gsum_done = nullptr) {
+  if (gsum_done) *gsum_done = false;
   if (is_stem(g)) {
     DDPPO_REQUIRE(ctx, g.Co <= kStemCoMax && g.Co % 8 == 0 && (g.k == 3 || g.k == 5 || g.k == 7) && g.s <= 2,
                   "stem conv: Co in {8,..,32}, k in {3, 5, 7}, stride 1 or 2");
@@ -1717,11 +1781,12 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
       const size_t sm2 = (size_t)(g.H + 2 * g.p) * (g.W + 2 * g.p) * sizeof(uint32_t);
 #define STEM_FWD(K_, S_, C_)                                                                                  \
   if (g.k == K_ && g.s == S_ && g.Co == C_)                                                                  \
-    launch_k(ctx, stem_fwd_mma_kernel<K_, S_, C_>, g.F, kThreads, sm2, st, x, w, g.H, g.W, g.p, g.Ho, g.Wo, y);
+    launch_k(ctx, stem_fwd_mma_kernel<K_, S_, C_>, g.F, kThreads, sm2, st, x, w, g.H, g.W, g.p, g.Ho, g.Wo, y, gsum);
       STEM_FWD(7, 2, 32) STEM_FWD(7, 1, 32) STEM_FWD(5, 2, 32) STEM_FWD(5, 1, 32) STEM_FWD(3, 2, 32)
       STEM_FWD(3, 1, 32) STEM_FWD(7, 2, 16) STEM_FWD(7, 1, 16) STEM_FWD(5, 2, 16) STEM_FWD(5, 1, 16)
       STEM_FWD(3, 2, 16) STEM_FWD(3, 1, 16)
 #undef STEM_FWD
+      if (gsum_done) *gsum_done = gsum != nullptr;
     } else {
 #define STEM_FWD(K_, S_)                                                                                   \
   if (g.k == K_ && g.s == S_)                                                                             \
@@ -1902,7 +1967,7 @@ static int gn_vpt(int n, int nt) { return (n + nt - 1) / nt; }
 // z = (relu)(GN(y) (+ residual)); stats [F][16][2] = (mean, rstd); zb (nullable) = z as bf16 planes
 ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const float* gamma, const float* beta,
                     const float* residual, int relu, float* stats, float* z, __nv_bfloat16* zb, double* gpart,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool pre_stats = false) {
   ProfScope pg(ctx, DDPPO_K_GN, st, 0);
   const int nt = gn_threads(C);
   DDPPO_REQUIRE(ctx, C >= kGroups && C <= kGnMaxThreads && nt % C == 0, "groupnorm: C a power of two in [16, 1024]");
@@ -1919,17 +1984,18 @@ ddppo_status gn_fwd(ddppo_ctx* ctx, int F, int HW, int C, const float* y, const 
     ctx->count(1);
   } else {
     DDPPO_REQUIRE(ctx, gpart != nullptr, "groupnorm: large frames need partial-sum scratch");
+    // pre_stats: gpart already holds each frame's total sums (one part per frame: the stem kernel)
 #define GN_FWD2(NV)                                                                                   \
   do {                                                                                                \
-    launch_k(ctx, gn_stats_part_kernel<NV>, dim3(S, F), nt, 0, st, y, HW, C, gpart);                  \
+    if (!pre_stats) launch_k(ctx, gn_stats_part_kernel<NV>, dim3(S, F), nt, 0, st, y, HW, C, gpart);  \
     launch_k(ctx, gn_apply_part_kernel<NV>, dim3(S, F), nt, 0, st, y, gpart, gamma, beta, residual, HW, \
-             C, relu, (size_t)F * HW * C, stats, z, zb);                                              \
+             C, relu, (size_t)F * HW * C, stats, z, zb, pre_stats ? 1 : S);                           \
   } while (0)
     if (nt == 1024) GN_FWD2(8);
     else if (nt == 512) GN_FWD2(16);
     else GN_FWD2(32);
 #undef GN_FWD2
-    ctx->count(2);
+    ctx->count(pre_stats ? 1 : 2);
   }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   return DDPPO_OK;
@@ -2058,10 +2124,11 @@ ConvScratch scratch_of(const Plan& P) { return ConvScratch{nullptr, nullptr, P.d
 // conv (+GN (+residual) (+ReLU)) forward
 ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, const float* residual, int relu,
                          cudaStream_t st) {
-  ddppo_status s = conv_fwd(ctx, geom_of(P, c), c.x, c.xb, prm + c.w, c.wr_b, c.y, scratch_of(P), st);
+  bool pre = false;  // (the stem writes its GroupNorm sums itself)
+  ddppo_status s = conv_fwd(ctx, geom_of(P, c), c.x, c.xb, prm + c.w, c.wr_b, c.y, scratch_of(P), st, P.gn_gpart, &pre);
   if (s != DDPPO_OK) return s;
   return gn_fwd(ctx, P.F, c.Ho * c.Wo, c.Co, c.y, prm + c.gw, prm + c.gb, residual, relu, c.stats, c.z, c.zb,
-                P.gn_gpart, st);
+                P.gn_gpart, st, pre);
 }
 
 // backward of conv+GN: dz = gradient wrt the GN(+residual)(+ReLU) output; relu_z = that output if a
