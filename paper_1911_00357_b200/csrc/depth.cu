@@ -1225,6 +1225,55 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* 
   *reinterpret_cast<float4*>(dx + ((size_t)f * H * W + pix) * C + 4 * c4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
 }
 
+// The same for even H = 2 Hp, W = 2 Wp, thread = (2x2 pixel block (2a.., 2b..), 4 channels): the
+// block's candidate windows are (a | a+1) x (b | b+1), each (argmax, gradient) pair loaded once for
+// the 4 pixels (the per-pixel kernel loads 2.25 pairs per pixel); every pixel adds its windows in
+// the same (u, v) order as maxpool_bwd_kernel, so the result is bit-identical.
+__global__ void maxpool_bwd2_kernel(const float* __restrict__ dy, const uint8_t* __restrict__ arg, int Hp, int Wp,
+                                    int C, float* __restrict__ dx) {
+  pdl_enter();
+  const int C4 = C >> 2, f = blockIdx.y;
+  const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i4 >= Hp * Wp * C4) return;
+  const int c4 = i4 % C4, blk = i4 / C4, b = blk % Wp, a = blk / Wp;
+  uchar4 wa[2][2];
+  float4 wd[2][2];
+#pragma unroll
+  for (int da = 0; da < 2; ++da)
+#pragma unroll
+    for (int db = 0; db < 2; ++db) {
+      const bool ok = a + da < Hp && b + db < Wp;
+      const size_t o = ok ? (((size_t)f * Hp + a + da) * Wp + b + db) * C + 4 * c4 : 0;
+      wa[da][db] = ok ? *reinterpret_cast<const uchar4*>(arg + o) : make_uchar4(255, 255, 255, 255);
+      wd[da][db] = ok ? *reinterpret_cast<const float4*>(dy + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  auto add = [](float (&acc)[4], const uchar4 a4, const float4 d4, int uv) {
+    if (a4.x == uv) acc[0] += d4.x;
+    if (a4.y == uv) acc[1] += d4.y;
+    if (a4.z == uv) acc[2] += d4.z;
+    if (a4.w == uv) acc[3] += d4.w;
+  };
+  // pixel (2a + r, 2b + s): windows in (u, v) ascending order; uv = u * 3 + v
+  float p00[4] = {0.f, 0.f, 0.f, 0.f}, p01[4] = {0.f, 0.f, 0.f, 0.f}, p10[4] = {0.f, 0.f, 0.f, 0.f},
+        p11[4] = {0.f, 0.f, 0.f, 0.f};
+  add(p00, wa[0][0], wd[0][0], 4);  // (u 1, v 1)
+  add(p01, wa[0][1], wd[0][1], 3);  // (1, 0) window b + 1
+  add(p01, wa[0][0], wd[0][0], 5);  // (1, 2) window b
+  add(p10, wa[1][0], wd[1][0], 1);  // (0, 1) window a + 1
+  add(p10, wa[0][0], wd[0][0], 7);  // (2, 1) window a
+  add(p11, wa[1][1], wd[1][1], 0);  // (0, 0)
+  add(p11, wa[1][0], wd[1][0], 2);  // (0, 2)
+  add(p11, wa[0][1], wd[0][1], 6);  // (2, 0)
+  add(p11, wa[0][0], wd[0][0], 8);  // (2, 2)
+  const int W = 2 * Wp;
+  float* o0 = dx + (((size_t)f * 2 * Hp + 2 * a) * W + 2 * b) * C + 4 * c4;
+  float* o1 = o0 + (size_t)W * C;
+  *reinterpret_cast<float4*>(o0) = make_float4(p00[0], p00[1], p00[2], p00[3]);
+  *reinterpret_cast<float4*>(o0 + C) = make_float4(p01[0], p01[1], p01[2], p01[3]);
+  *reinterpret_cast<float4*>(o1) = make_float4(p10[0], p10[1], p10[2], p10[3]);
+  *reinterpret_cast<float4*>(o1 + C) = make_float4(p11[0], p11[1], p11[2], p11[3]);
+}
+
 // NHWC [F][HW][C] <-> flat [F][C*HW] in (c, h, w) order (PyTorch flatten of NCHW)
 __global__ void flatten_kernel(const float* __restrict__ in, int F, int HW, int C, float* __restrict__ out,
                                int to_flat) {
@@ -2511,8 +2560,12 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
   // GroupNorm backward instead -- no dense gradient in HBM -- measured 3 us slower per minibatch:
   // the cluster kernel's 2 CTAs / SM cannot hide the gather's L2 latency.)
   ConvGN& stem = P.convs[0];
-  launch_k(ctx, maxpool_bwd_kernel, dim3((stem.Ho * stem.Wo * 8 + kThreads - 1) / kThreads, F), kThreads, 0, st, dz,
-           P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
+  if (stem.Ho == 2 * P.pool_hw && stem.Wo == 2 * P.pool_hw)
+    launch_k(ctx, maxpool_bwd2_kernel, dim3((P.pool_hw * P.pool_hw * 8 + kThreads - 1) / kThreads, F), kThreads, 0, st,
+             dz, P.pool_arg, P.pool_hw, P.pool_hw, 32, da);
+  else
+    launch_k(ctx, maxpool_bwd_kernel, dim3((stem.Ho * stem.Wo * 8 + kThreads - 1) / kThreads, F), kThreads, 0, st, dz,
+             P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
   if ((s = conv_gn_bwd(ctx, prm, grad, P, stem, da, stem.z, nullptr, 0, st)) != DDPPO_OK) return s;
@@ -2627,9 +2680,13 @@ extern "C" ddppo_status ddppo_debug_maxpool(ddppo_ctx* ctx, const float* x, int 
            Ho, Wo, y, arg,
                                                                                      nullptr);
   ctx->count(1);
-  if (dy) {
-    launch_k(ctx, maxpool_bwd_kernel, dim3((H * W * (C / 4) + kThreads - 1) / kThreads, F), kThreads, 0, st, dy, arg,
-             F, H, W, C, Ho, Wo, dx);
+  if (dy) {  // the Depth step's dispatch: the 2x2-block kernel for even maps
+    if (H == 2 * Ho && W == 2 * Wo)
+      launch_k(ctx, maxpool_bwd2_kernel, dim3((Ho * Wo * (C / 4) + kThreads - 1) / kThreads, F), kThreads, 0, st, dy,
+               arg, Ho, Wo, C, dx);
+    else
+      launch_k(ctx, maxpool_bwd_kernel, dim3((H * W * (C / 4) + kThreads - 1) / kThreads, F), kThreads, 0, st, dy, arg,
+               F, H, W, C, Ho, Wo, dx);
     ctx->count(1);
   }
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());

@@ -126,7 +126,7 @@ def test_groupnorm(dd, ctx, F, HW, C, relu, res):
     assert np.max(np.abs(db.cpu().numpy() - db_o)) <= 1e-4 * np.abs(db_o).max()
 
 
-@pytest.mark.parametrize("F,H,C", [(3, 32, 32), (2, 7, 12), (1, 2, 16), (2, 9, 4)])
+@pytest.mark.parametrize("F,H,C", [(3, 32, 32), (2, 7, 12), (1, 2, 16), (2, 9, 4), (2, 10, 8)])  # even H: 2x2-block backward
 def test_maxpool(dd, ctx, F, H, C):
     rng = np.random.default_rng(F * H * C)
     x = np.maximum(rng.normal(size=(F, C, H, H)), 0).astype(np.float32)  # ReLU zeros: ties
