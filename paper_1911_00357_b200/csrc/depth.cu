@@ -361,17 +361,34 @@ __device__ __forceinline__ uint32_t pack_hilo(float v) {
 // zero-padded frame f -> xp[HP][WP] packed hi/lo; returns (block-uniformly, after the barrier)
 // whether any lo half is nonzero -- a frame of bf16 values (the Depth observations are stored as
 // bf16) has an all-zero lo plane, whose MMAs then add exact zeros and are skipped
-__device__ __forceinline__ bool stage_frame_hilo(const float* __restrict__ x, int f, int H, int Wd, int p, int HP,
-                                                 int WP, uint32_t* xp) {
+// The stem's input frames: x [F][H][W] fp32, or (obs != null) straight from the rollout's bf16
+// observations obs [E][T][H][W], frame f = (env b = f / T_run, step t = f % T_run) of env_idx[b]
+// (the Depth step then needs no gather pass: the frames are read where they lie)
+struct FrameSrc {
+  const float* x;
+  const __nv_bfloat16* obs;
+  const int32_t* env_idx;
+  int T, T_run;
+};
+__device__ __forceinline__ bool stage_frame_hilo(const FrameSrc& fs, int f, int H, int Wd, int p, int HP, int WP,
+                                                 uint32_t* xp) {
   int any_lo = 0;
   constexpr int kB = 8;  // loads in flight per thread (the loop is latency-bound otherwise)
-  const float* xf = x + (size_t)f * H * Wd;
+  const float* xf = nullptr;
+  const __nv_bfloat16* of = nullptr;
+  if (fs.obs) {
+    const int b = f / fs.T_run, t = f - b * fs.T_run;
+    of = fs.obs + ((size_t)fs.env_idx[b] * fs.T + t) * H * Wd;
+  } else {
+    xf = fs.x + (size_t)f * H * Wd;
+  }
   for (int i0 = 0; i0 < HP * WP; i0 += kB * (int)blockDim.x) {
     float v[kB];
 #pragma unroll
     for (int u = 0; u < kB; ++u) {
       const int i = i0 + u * blockDim.x + threadIdx.x, r = i / WP - p, q = i % WP - p;
-      v[u] = (i < HP * WP && r >= 0 && r < H && q >= 0 && q < Wd) ? xf[r * Wd + q] : 0.f;
+      v[u] = (i < HP * WP && r >= 0 && r < H && q >= 0 && q < Wd) ? (of ? __bfloat162float(of[r * Wd + q]) : xf[r * Wd + q])
+                                                                  : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < kB; ++u) {
@@ -391,7 +408,7 @@ __device__ __forceinline__ bool stage_frame_hilo(const float* __restrict__ x, in
 // per-thread sums in pixel order, then a fixed butterfly over the 8 row lanes and the warps in
 // order), so the stem's GroupNorm needs no statistics pass over y.
 template <int K, int S, int CO>
-__global__ void __launch_bounds__(kThreads, 2) stem_fwd_mma_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, 2) stem_fwd_mma_kernel(const FrameSrc x,
                                                                    const float* __restrict__ W, int H, int Wd,
                                                                    int p, int Ho, int Wo, float* __restrict__ y,
                                                                    double* __restrict__ gsum) {
@@ -519,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 2) stem_fwd_mma_kernel(const float* 
 // fragment.  Warp w takes the 16-pixel k-steps w, w + 8, ...; the 8 warps' tiles are added in a
 // fixed order.
 template <int K, int CO>
-__global__ void __launch_bounds__(kThreads, 2) stem_wgrad_mma_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, 2) stem_wgrad_mma_kernel(const FrameSrc x,
                                                                      const __nv_bfloat16* __restrict__ dy, int H,
                                                                      int Wd, int s, int p, int Ho, int Wo,
                                                                      float* __restrict__ part) {
@@ -1819,6 +1836,11 @@ inline int split_cap(const ConvScratch& sc, long long M, long long N, int cap) {
 }
 
 bool is_stem(const ConvGeom& g) { return g.Ci == 1; }
+// the stem shapes the warp-MMA kernels take (the fp32 SIMT kernels take the rest)
+bool stem_mma_ok(const ConvGeom& g) {
+  return is_stem(g) && (g.Co == 16 || g.Co == 32) && (g.Ho * g.Wo) % 16 == 0 && (g.k == 3 || g.k == 5 || g.k == 7) &&
+         g.s <= 2;
+}
 
 // Implicit-GEMM operands over NHWC bf16 tensors
 IgOperand op_pix(const __nv_bfloat16* x, int PH, int PW, int SH, int SW, int SC, const ConvGeom& g, int transposed,
@@ -1844,24 +1866,26 @@ IgOperand op_dense(int kind, const __nv_bfloat16* x, int64_t ld, int64_t plane) 
 // launched kernel wrote them (the warp-MMA stem does, every other path does not)
 ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const __nv_bfloat16* xb, const float* w,
                       const __nv_bfloat16* wr_b, float* y, const ConvScratch& sc, cudaStream_t st,
-                      double* gsum = nullptr, bool* gsum_done = nullptr) {
+                      double* gsum = nullptr, bool* gsum_done = nullptr, const FrameSrc* fs = nullptr) {
   if (gsum_done) *gsum_done = false;
   if (is_stem(g)) {
     DDPPO_REQUIRE(ctx, g.Co <= kStemCoMax && g.Co % 8 == 0 && (g.k == 3 || g.k == 5 || g.k == 7) && g.s <= 2,
                   "stem conv: Co in {8,..,32}, k in {3, 5, 7}, stride 1 or 2");
     const size_t smem = (size_t)((g.H + 2 * g.p) * (g.W + 2 * g.p + 16) + g.Co * g.k * g.k) * sizeof(float);
     DDPPO_REQUIRE(ctx, smem <= 48 * 1024, "stem conv: frame too large for shared memory");
-    if ((g.Co == 16 || g.Co == 32) && (g.Ho * g.Wo) % 16 == 0) {  // warp-MMA stem
+    if (stem_mma_ok(g)) {  // warp-MMA stem
+      const FrameSrc src = fs ? *fs : FrameSrc{x, nullptr, nullptr, 0, 1};
       const size_t sm2 = (size_t)(g.H + 2 * g.p) * (g.W + 2 * g.p) * sizeof(uint32_t);
 #define STEM_FWD(K_, S_, C_)                                                                                  \
   if (g.k == K_ && g.s == S_ && g.Co == C_)                                                                  \
-    launch_k(ctx, stem_fwd_mma_kernel<K_, S_, C_>, g.F, kThreads, sm2, st, x, w, g.H, g.W, g.p, g.Ho, g.Wo, y, gsum);
+    launch_k(ctx, stem_fwd_mma_kernel<K_, S_, C_>, g.F, kThreads, sm2, st, src, w, g.H, g.W, g.p, g.Ho, g.Wo, y, gsum);
       STEM_FWD(7, 2, 32) STEM_FWD(7, 1, 32) STEM_FWD(5, 2, 32) STEM_FWD(5, 1, 32) STEM_FWD(3, 2, 32)
       STEM_FWD(3, 1, 32) STEM_FWD(7, 2, 16) STEM_FWD(7, 1, 16) STEM_FWD(5, 2, 16) STEM_FWD(5, 1, 16)
       STEM_FWD(3, 2, 16) STEM_FWD(3, 1, 16)
 #undef STEM_FWD
       if (gsum_done) *gsum_done = gsum != nullptr;
     } else {
+      DDPPO_REQUIRE(ctx, !fs || !fs->obs, "stem conv: observation frames need the warp-MMA stem");
 #define STEM_FWD(K_, S_)                                                                                   \
   if (g.k == K_ && g.s == S_)                                                                             \
     launch_k(ctx, stem_fwd_kernel<K_, S_>, g.F, kThreads, smem, st, x, w, g.H, g.W, g.Co, g.p, g.Ho, g.Wo, y);
@@ -1905,7 +1929,8 @@ ddppo_status conv_fwd(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const _
 
 // dy (bf16, gradient wrt the conv output) -> dw (PyTorch order)
 ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const __nv_bfloat16* xb,
-                        const __nv_bfloat16* dy, float* dw, const ConvScratch& sc, cudaStream_t st) {
+                        const __nv_bfloat16* dy, float* dw, const ConvScratch& sc, cudaStream_t st,
+                        const FrameSrc* fs = nullptr) {
   if (is_stem(g)) {
     DDPPO_REQUIRE(ctx, (g.Ho * g.Wo * g.Co) % 8 == 0, "stem conv: Ho*Wo*Co must be a multiple of 8");
     const size_t hp = (size_t)(g.H + 2 * g.p) * (g.W + 2 * g.p);
@@ -1917,7 +1942,8 @@ ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const
                                                200 * 1024));
       attr_set = true;
     }
-    if ((g.Co == 16 || g.Co == 32) && (g.Ho * g.Wo) % 16 == 0) {  // warp-MMA stem
+    if (stem_mma_ok(g)) {  // warp-MMA stem
+      const FrameSrc src = fs ? *fs : FrameSrc{x, nullptr, nullptr, 0, 1};
       const int NC = (g.k * g.k + 7) / 8 * 8;
       const size_t dyw = std::max<size_t>((size_t)g.Ho * g.Wo * g.Co / 2, (size_t)(kThreads / 32) * g.Co * NC);
       const size_t sm2 = (dyw + hp) * sizeof(uint32_t);
@@ -1932,11 +1958,12 @@ ddppo_status conv_wgrad(ddppo_ctx* ctx, const ConvGeom& g, const float* x, const
       }
 #define STEM_WG(K_, C_)                                                                                  \
   if (g.k == K_ && g.Co == C_)                                                                          \
-    launch_k(ctx, stem_wgrad_mma_kernel<K_, C_>, g.F, kThreads, sm2, st, x, dy, g.H, g.W, g.s, g.p, g.Ho, g.Wo, \
+    launch_k(ctx, stem_wgrad_mma_kernel<K_, C_>, g.F, kThreads, sm2, st, src, dy, g.H, g.W, g.s, g.p, g.Ho, g.Wo, \
              sc.part);
       STEM_WG(7, 32) STEM_WG(5, 32) STEM_WG(3, 32) STEM_WG(7, 16) STEM_WG(5, 16) STEM_WG(3, 16)
 #undef STEM_WG
     } else {
+      DDPPO_REQUIRE(ctx, !fs || !fs->obs, "stem conv: observation frames need the warp-MMA stem");
       launch_k(ctx, stem_wgrad_kernel, g.F, kThreads, smem, st, x, dy, g.H, g.W, g.Co, g.k, g.s, g.p, g.Ho, g.Wo,
                sc.part);
     }
@@ -2197,9 +2224,10 @@ ConvScratch scratch_of(const Plan& P) { return ConvScratch{nullptr, nullptr, P.d
 
 // conv (+GN (+residual) (+ReLU)) forward
 ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, const float* residual, int relu,
-                         cudaStream_t st) {
+                         cudaStream_t st, const FrameSrc* fs = nullptr) {
   bool pre = false;  // (the stem writes its GroupNorm sums itself)
-  ddppo_status s = conv_fwd(ctx, geom_of(P, c), c.x, c.xb, prm + c.w, c.wr_b, c.y, scratch_of(P), st, P.gn_gpart, &pre);
+  ddppo_status s =
+      conv_fwd(ctx, geom_of(P, c), c.x, c.xb, prm + c.w, c.wr_b, c.y, scratch_of(P), st, P.gn_gpart, &pre, fs);
   if (s != DDPPO_OK) return s;
   return gn_fwd(ctx, P.F, c.Ho * c.Wo, c.Co, c.y, prm + c.gw, prm + c.gb, residual, relu, c.stats, c.z, c.zb,
                 P.gn_gpart, st, pre);
@@ -2211,7 +2239,7 @@ ddppo_status conv_gn_fwd(ddppo_ctx* ctx, const float* prm, Plan& P, ConvGN& c, c
 // forked after the GN backward (its own dy buffer and partials) and joined once after the backward.
 ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P, ConvGN& c, const float* dz,
                          const float* relu_z, float* dx, int accumulate_dx, cudaStream_t st, const float* res = nullptr,
-                         const float* res_mask = nullptr) {
+                         const float* res_mask = nullptr, const FrameSrc* fs = nullptr) {
   const size_t lo = P.grad_planes == 2 ? (size_t)P.F * c.Ho * c.Wo * c.Co : 0;
   ddppo_status s = gn_bwd(ctx, P.F, c.Ho * c.Wo, c.Co, dz, relu_z, c.y, c.stats, prm + c.gw, c.dyb, grad + c.gw,
                           grad + c.gb, c.gn_part, P.gn_gpart, st, /*reduce_params=*/false, lo);
@@ -2220,9 +2248,9 @@ ddppo_status conv_gn_bwd(ddppo_ctx* ctx, const float* prm, float* grad, Plan& P,
   if (P.side) {
     DDPPO_CUDA_TRY(ctx, fork_to(ctx, st, P.side));
     ConvScratch ws = {nullptr, nullptr, P.dwt, P.part_w, P.part_w_n, 1};
-    s = conv_wgrad(ctx, g, c.x, c.xb, c.dyb, grad + c.w, ws, P.side);
+    s = conv_wgrad(ctx, g, c.x, c.xb, c.dyb, grad + c.w, ws, P.side, fs);
   } else {
-    s = conv_wgrad(ctx, g, c.x, c.xb, c.dyb, grad + c.w, scratch_of(P), st);
+    s = conv_wgrad(ctx, g, c.x, c.xb, c.dyb, grad + c.w, scratch_of(P), st, fs);
   }
   if (s != DDPPO_OK || dx == nullptr) return s;
   return conv_dgrad(ctx, g, prm + c.w, c.wd_b, c.dyb, dx, accumulate_dx, scratch_of(P), st, P.grad_planes, res,
@@ -2343,18 +2371,21 @@ ddppo_status depth_fwd_net(ddppo_ctx* ctx, const ModelLayout& L, const float* pr
     prep_st = st;
     return fork_to(ctx, P.side, st);
   };
-  if (!P.rgbd) {
-    launch_k(ctx, gather_obs_kernel, blocks_for(ctx, (size_t)F * kImg * kImg / 8), kThreads, 0, st, 
-        reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, P.x0);
-  } else {
+  const FrameSrc fs{P.x0, reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run};
+  const bool direct = !P.rgbd && stem_mma_ok(geom_of(P, P.convs[0]));  // the stem reads the observations
+  if (!P.rgbd && !direct) {
+    launch_k(ctx, gather_obs_kernel, blocks_for(ctx, (size_t)F * kImg * kImg / 8), kThreads, 0, st,
+             reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, P.x0);
+    ctx->count(1);
+  } else if (P.rgbd) {
     DDPPO_REQUIRE(ctx, kImgRgbd % 4 == 0, "rgbd: input width must be a multiple of 4");
     launch_k(ctx, rgbd_prologue_kernel, (F * (kImgRgbd / 2) * (kImgRgbd / 4) + kThreads - 1) / kThreads, kThreads, 0,
-             st, 
-        b.obs_rgb, reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, kImgRgbd, P.x0, P.x0b);
+             st, b.obs_rgb, reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run, F, kImgRgbd,
+             P.x0, P.x0b);
+    ctx->count(1);
   }
-  ctx->count(1);
   if (P.convs[0].Ci != 1) DDPPO_CUDA_TRY(ctx, join_prep());  // RGB-D: the stem is a TMA convolution
-  ddppo_status s = conv_gn_fwd(ctx, prm, P, P.convs[0], nullptr, 1, st);
+  ddppo_status s = conv_gn_fwd(ctx, prm, P, P.convs[0], nullptr, 1, st, direct ? &fs : nullptr);
   if (s != DDPPO_OK) return s;
   {
     ConvGN& c = P.convs[0];
@@ -2593,7 +2624,11 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
              P.pool_arg, F, stem.Ho, stem.Wo, 32, P.pool_hw, P.pool_hw, da);
   ctx->count(1);
   DDPPO_CUDA_TRY(ctx, cudaGetLastError());
-  if ((s = conv_gn_bwd(ctx, prm, grad, P, stem, da, stem.z, nullptr, 0, st)) != DDPPO_OK) return s;
+  const FrameSrc fs{P.x0, reinterpret_cast<const __nv_bfloat16*>(b.obs), b.env_idx, b.T, b.T_run};
+  const bool direct = !P.rgbd && stem_mma_ok(geom_of(P, stem));  // (as in the forward)
+  if ((s = conv_gn_bwd(ctx, prm, grad, P, stem, da, stem.z, nullptr, 0, st, nullptr, nullptr, direct ? &fs : nullptr)) !=
+      DDPPO_OK)
+    return s;
   // all layers' dgamma / dbeta from their row partials, one launch
   GnParamAll a;
   a.n = 0;
