@@ -2563,7 +2563,8 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     // out = relu(gn_last(conv_last(...)) (* SE) + shortcut(in)); the ReLU mask of the sum is `out`
     // identity shortcut of a two-conv block: the first conv's input-gradient epilogue adds the masked
     // shortcut gradient (dz stays intact until then); otherwise it is written first and accumulated onto
-    const bool fuse_res = blk.down < 0 && blk.main.size() == 2 && !blk.se;
+    // (bottlenecks: the middle conv's gradient goes to dz_se, free outside SE blocks, so dz survives)
+    const bool fuse_res = blk.down < 0 && !blk.se;
     if (blk.down >= 0) {
       if ((s = conv_gn_bwd(ctx, prm, grad, P, P.convs[blk.down], dz, blk.out, dn, 0, st)) != DDPPO_OK) return s;
     } else if (!fuse_res) {
@@ -2608,6 +2609,7 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
       if (!first) {
         std::swap(g_in, g_out);  // g_in <- this conv's input gradient; g_out <- a free buffer
         if (g_out == dn) g_out = (g_in == dz) ? da : dz;
+        if (fuse_res && g_out == dz) g_out = (g_in == P.dz_se) ? da : P.dz_se;  // dz: the first conv's residual
       }
     }
     std::swap(dz, dn);  // dn (the block input's gradient) becomes the next dz
