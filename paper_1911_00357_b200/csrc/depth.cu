@@ -2563,8 +2563,9 @@ ddppo_status depth_bwd(ddppo_ctx* ctx, const ModelLayout& L, const float* prm, c
     // out = relu(gn_last(conv_last(...)) (* SE) + shortcut(in)); the ReLU mask of the sum is `out`
     // identity shortcut of a two-conv block: the first conv's input-gradient epilogue adds the masked
     // shortcut gradient (dz stays intact until then); otherwise it is written first and accumulated onto
-    // (bottlenecks: the middle conv's gradient goes to dz_se, free outside SE blocks, so dz survives)
-    const bool fuse_res = blk.down < 0 && !blk.se;
+    // (bottlenecks: the middle conv's gradient goes to dz_se, free outside SE blocks, so dz survives;
+    // in SE blocks the chain starts from dz_se and never touches dz)
+    const bool fuse_res = blk.down < 0;
     if (blk.down >= 0) {
       if ((s = conv_gn_bwd(ctx, prm, grad, P, P.convs[blk.down], dz, blk.out, dn, 0, st)) != DDPPO_OK) return s;
     } else if (!fuse_res) {
