@@ -870,6 +870,15 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_apply_part_kernel(const float
   __shared__ float smu[kGroups], srs[kGroups];
   // gpart holds nparts partial sums per frame (gn_stats_part: one per chunk; the stem kernel: 1)
   const int f = blockIdx.y, S = nparts, n = HW * C, chunk = gn_chunk(C), cg = C / kGroups;
+  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
+  const size_t base = (size_t)f * n;
+  float v[NV], rv[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {  // the chunk's loads first: in flight while the statistics are formed
+    const int e = e0 + threadIdx.x + i * blockDim.x;
+    v[i] = e < e1 ? y[base + e] : 0.f;
+    rv[i] = (residual && e < e1) ? residual[base + e] : 0.f;
+  }
   if (threadIdx.x < kGroups) {
     double a = 0.0, b = 0.0;
     for (int s = 0; s < S; ++s) {
@@ -890,16 +899,6 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_apply_part_kernel(const float
   __syncthreads();
   const int c = threadIdx.x % C;
   const float mu = smu[c / cg], rs = srs[c / cg], gm = gamma[c], bt = beta[c];
-  const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
-  const size_t base = (size_t)f * n;
-  float v[NV], rv[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int e = e0 + threadIdx.x + i * blockDim.x;
-    v[i] = e < e1 ? y[base + e] : 0.f;
-    rv[i] = (residual && e < e1) ? residual[base + e] : 0.f;
-  }
-  asm volatile("" ::: "memory");  // every load above is issued before any result is consumed
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int e = e0 + threadIdx.x + i * blockDim.x;
