@@ -688,6 +688,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_fwd_kernel(const float* __res
   __shared__ float smu[kGroups], srs[kGroups];
   const int f = blockIdx.x, n = HW * C, c = threadIdx.x % C, cg = C / kGroups;
   const size_t base = (size_t)f * n;
+  const float gm = gamma[c], bt = beta[c];  // (issued with the slab's loads, not after the reduction)
   float v[NV], rv[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_fwd_kernel(const float* __res
     stats[(f * kGroups + threadIdx.x) * 2 + 1] = srs[threadIdx.x];
   }
   __syncthreads();
-  const float mu = smu[c / cg], rs = srs[c / cg], gm = gamma[c], bt = beta[c];
+  const float mu = smu[c / cg], rs = srs[c / cg];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int e = threadIdx.x + i * blockDim.x;
@@ -783,8 +784,9 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_kernel(const float* __res
   float *s_dz = gsm, *s_z = gsm + cap, *s_y = gsm + 2 * cap;
   const int f = blockIdx.x, n = HW * C, c = threadIdx.x % C, cg = C / kGroups, g = c / cg;
   const size_t base = (size_t)f * n;
-  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, 0, n, cap);
+  // (the statistics / gamma loads are issued before the staging wait, not after it)
   const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
+  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, 0, n, cap);
   double a1 = 0.0, a2 = 0.0;
   float pg = 0.f, pb = 0.f;
 #pragma unroll
@@ -872,6 +874,8 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_apply_part_kernel(const float
   const int f = blockIdx.y, S = nparts, n = HW * C, chunk = gn_chunk(C), cg = C / kGroups;
   const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const size_t base = (size_t)f * n;
+  const int c = threadIdx.x % C;
+  const float gm = gamma[c], bt = beta[c];
   float v[NV], rv[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {  // the chunk's loads first: in flight while the statistics are formed
@@ -897,8 +901,7 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_apply_part_kernel(const float
     }
   }
   __syncthreads();
-  const int c = threadIdx.x % C;
-  const float mu = smu[c / cg], rs = srs[c / cg], gm = gamma[c], bt = beta[c];
+  const float mu = smu[c / cg], rs = srs[c / cg];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int e = e0 + threadIdx.x + i * blockDim.x;
@@ -935,8 +938,9 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_part_kernel(const float* 
             g = c / cg;
   const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const size_t base = (size_t)f * n;
-  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, e0, e1, cap);
+  // (the statistics / gamma loads are issued before the staging wait, not after it)
   const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
+  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, e0, e1, cap);
   double a1 = 0.0, a2 = 0.0;
   float pg = 0.f, pb = 0.f;
 #pragma unroll
@@ -1047,8 +1051,9 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_cluster_kernel(const floa
             g = c / cg;
   const int e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const size_t base = (size_t)f * n;
-  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, e0, e1, cap);
+  // (the statistics / gamma loads are issued before the staging wait, not after it)
   const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
+  gn_stage_bwd(s_dz, s_z, s_y, dz, z, y, base, e0, e1, cap);
   double a1 = 0.0, a2 = 0.0;
   float pg = 0.f, pb = 0.f;
 #pragma unroll
