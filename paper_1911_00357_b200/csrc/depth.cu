@@ -1012,10 +1012,10 @@ __global__ void __launch_bounds__(gn_bound(NV)) gn_bwd_apply_kernel(const float*
     sm1[threadIdx.x] = (float)(a / cnt);
     sm2[threadIdx.x] = (float)(b / cnt);
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
   const int c = threadIdx.x % C, g = c / cg;
   const float mu = stats[(f * kGroups + g) * 2], rs = stats[(f * kGroups + g) * 2 + 1], gm = gamma[c];
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
   const float m1 = sm1[g], m2 = sm2[g];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
